@@ -1,0 +1,291 @@
+"""Pins of the CPU oracle against things other than itself (task rule ③).
+
+Each test names the paper passage / DESIGN.md reading it pins and the independent source
+of truth: a closed form, an invariant, brute force on tiny inputs, or a library routine
+(torch nn.Linear, scipy.ndimage.convolve, torch conv2d, scipy.signal.fftconvolve,
+torch grid_sample). None of them re-types the oracle's own loops. A plausible mistake in
+the oracle — dropped term, wrong sign/index, transposed operand, correlation instead of
+convolution, scatter instead of gather order, wrong boundary — fails at least one.
+"""
+import numpy as np
+import pytest
+import scipy.ndimage
+import scipy.signal
+import torch
+
+import oracle
+from paper_2107_11627_b200 import synth
+
+
+def _mlp_const(n_in, h, K, b3):
+    """W1..W3 = 0 => beta == b3 everywhere (spatially constant beta)."""
+    return {"W1": np.zeros((h, n_in), np.float32), "b1": np.zeros(h, np.float32),
+            "W2": np.zeros((h, h), np.float32), "b2": np.zeros(h, np.float32),
+            "W3": np.zeros((K, h), np.float32), "b3": np.asarray(b3, np.float32)}
+
+
+def _small(seed=0, B=1, C=1, H=24, W=20, K=6, S=5, n_in=7, h=9, tstd=1.3):
+    spec = synth.custom("pin", 100 + seed, B=B, C=C, H=H, W=W, K=K, S=S, n_in=n_in, h1=h,
+                        h2=h + 2, z_sigma=2.0, z_std=0.8, t_sigma=3.0, t_std=tstd)
+    return synth.make_inputs(spec)
+
+
+def _render(inp, tilt="same", **kw):
+    t = inp.tilt if tilt == "same" else tilt
+    return oracle.render(inp.image, inp.zernike, t, inp.basis, inp.mlp, want_blur=True, **kw)
+
+
+# ---------------------------------------------------------------- step a1: P2S MLP
+def test_mlp_matches_torch_linear_stack():
+    """P6 — PAPER.md:283 'three fully connected layers' (ReLU hidden, linear out, A11)
+    vs torch.nn.Linear/ReLU in float64 (library routine)."""
+    inp = _small(1)
+    b = oracle.beta(inp.image, inp.zernike, inp.basis, inp.mlp)
+    m = inp.mlp
+    net = torch.nn.Sequential(torch.nn.Linear(*m["W1"].shape[::-1]), torch.nn.ReLU(),
+                              torch.nn.Linear(*m["W2"].shape[::-1]), torch.nn.ReLU(),
+                              torch.nn.Linear(*m["W3"].shape[::-1])).double()
+    with torch.no_grad():
+        for li, layer in zip((1, 2, 3), (net[0], net[2], net[4])):
+            layer.weight.copy_(torch.from_numpy(m[f"W{li}"].astype(np.float64)))
+            layer.bias.copy_(torch.from_numpy(m[f"b{li}"].astype(np.float64)))
+        z = torch.from_numpy(inp.zernike[0].astype(np.float64)).permute(1, 2, 0)  # H W n_in
+        ref = net(z).permute(2, 0, 1).numpy()
+    np.testing.assert_allclose(b[0], ref, rtol=0, atol=1e-12)
+    # the stack must be non-trivial: some hidden units clipped, output not affine in z
+    assert np.std(ref) > 0.05
+
+
+def test_mlp_zero_weights_gives_bias():
+    """S:272 idea — zero weights => output equals b3 (no output activation, A11)."""
+    inp = _small(2)
+    K = inp.basis.shape[0]
+    b3 = np.linspace(-1, 1, K).astype(np.float32)
+    mlp = _mlp_const(inp.zernike.shape[1], 9, K, b3)
+    mlp["W2"] = np.zeros((9, 9), np.float32)
+    b = oracle.beta(inp.image, inp.zernike, inp.basis, mlp)
+    np.testing.assert_array_equal(b[0], np.broadcast_to(b3[:, None, None], b[0].shape))
+
+
+# ---------------------------------------------------------------- step a2: Eq. (5)
+def test_identity_delta_basis():
+    """North-star (a): K=1, phi = centred Dirac, beta = 1 => J = I and out = I (zero tilt)."""
+    for S in (1, 15):
+        inp = _small(3, S=S, K=1, tstd=0.0)
+        basis = np.zeros((1, S, S), np.float32)
+        basis[0, S // 2, S // 2] = 1.0
+        inp.basis = basis
+        inp.mlp = _mlp_const(inp.zernike.shape[1], 4, 1, [1.0])
+        out, J = _render(inp)
+        np.testing.assert_array_equal(J, inp.image.astype(np.float64))
+        np.testing.assert_array_equal(out, inp.image.astype(np.float64))
+
+
+def test_delta_basis_shift_sign():
+    """P8 — true convolution (A2, A3): phi[r+dy][r+dx] = 1 moves content by +(dy, dx),
+    replicate boundary (A4): J(y,x) = I[clamp(y-dy)][clamp(x-dx)]."""
+    S, r = 7, 3
+    for dy, dx in ((2, -1), (-3, 3), (0, 1)):
+        inp = _small(4, S=S, K=1, tstd=0.0)
+        basis = np.zeros((1, S, S), np.float32)
+        basis[0, r + dy, r + dx] = 1.0
+        inp.basis = basis
+        inp.mlp = _mlp_const(inp.zernike.shape[1], 4, 1, [1.0])
+        _, J = _render(inp)
+        H, W = inp.image.shape[2:]
+        yy = np.clip(np.arange(H) - dy, 0, H - 1)
+        xx = np.clip(np.arange(W) - dx, 0, W - 1)
+        np.testing.assert_array_equal(J[0, 0], inp.image[0, 0][yy][:, xx].astype(np.float64))
+
+
+def test_constant_beta_equals_scipy_and_torch_conv():
+    """P2 — spatially constant beta: J = I * (sum_k beta0_k phi_k) equals
+    scipy.ndimage.convolve(mode='nearest') and torch conv2d(replicate pad, flipped taps)."""
+    inp = _small(5, C=3, S=9, K=5, H=30, W=17, tstd=0.0)
+    beta0 = np.array([0.7, -0.4, 1.3, 0.2, -0.9], np.float32)
+    inp.mlp = _mlp_const(inp.zernike.shape[1], 6, 5, beta0)
+    _, J = _render(inp)
+    h = np.tensordot(beta0.astype(np.float64), inp.basis.astype(np.float64), axes=1)
+    for c in range(3):
+        ref = scipy.ndimage.convolve(inp.image[0, c].astype(np.float64), h, mode="nearest")
+        np.testing.assert_allclose(J[0, c], ref, rtol=0, atol=1e-12)
+    x = torch.from_numpy(inp.image.astype(np.float64))
+    xp = torch.nn.functional.pad(x, (4, 4, 4, 4), mode="replicate")
+    w = torch.from_numpy(np.flip(h, (0, 1)).copy())[None, None].repeat(3, 1, 1, 1)
+    ref_t = torch.nn.functional.conv2d(xp, w, groups=3).numpy()
+    np.testing.assert_allclose(J, ref_t, rtol=0, atol=1e-12)
+
+
+def test_one_hot_beta_each_basis():
+    """P5 — beta = e_k => J = I * phi_k (per-k indexing), FFT convolution on an
+    edge-padded image (scipy.signal.fftconvolve, 'valid')."""
+    inp = _small(6, S=7, K=4, H=21, W=26, tstd=0.0)
+    I = inp.image[0, 0].astype(np.float64)
+    Ip = np.pad(I, 3, mode="edge")
+    for k in range(4):
+        e = np.zeros(4, np.float32)
+        e[k] = 1
+        inp.mlp = _mlp_const(inp.zernike.shape[1], 5, 4, e)
+        _, J = _render(inp)
+        ref = scipy.signal.fftconvolve(Ip, inp.basis[k].astype(np.float64), mode="valid")
+        np.testing.assert_allclose(J[0, 0], ref, rtol=0, atol=1e-12)
+
+
+def test_brute_force_spatially_varying_conv():
+    """North-star (c) — Eq. (3)/(4): per-pixel PSF
+    h_{y,x} = sum_k beta_k(y,x) phi_k applied directly equals the Eq. (5) basis-sum form."""
+    inp = _small(7, C=2, S=5, K=6, H=13, W=11)
+    _, J = _render(inp, tilt=None)
+    beta = oracle.beta(inp.image, inp.zernike, inp.basis, inp.mlp)[0]  # K H W (pinned by P6)
+    H, W, S, r = 13, 11, 5, 2
+    phi = inp.basis.astype(np.float64)
+    for c in range(2):
+        I = inp.image[0, c].astype(np.float64)
+        ref = np.zeros((H, W))
+        for y in range(H):
+            for x in range(W):
+                h = np.tensordot(beta[:, y, x], phi, axes=1)       # the row h_n of H (Eq. 3)
+                for i in range(S):
+                    for j in range(S):
+                        ref[y, x] += h[i, j] * I[min(max(y - (i - r), 0), H - 1),
+                                                 min(max(x - (j - r), 0), W - 1)]
+        np.testing.assert_allclose(J[0, c], ref, rtol=0, atol=1e-12)
+
+
+def test_gather_order_delta_image():
+    """P1 / reading A1 — Eq. (5) weights at the OUTPUT pixel: for a delta image at p0,
+    J(p) = sum_k beta_k(p) phi_k(p - p0) (gather). The scatter order
+    sum_k (beta_k I) * phi_k would give beta_k(p0) instead and must differ."""
+    inp = _small(8, S=7, K=5, H=20, W=20, tstd=0.0)
+    I = np.zeros((20, 20), np.float32)
+    I[10, 9] = 1.0
+    inp.image = I[None, None]
+    _, J = _render(inp)
+    beta = oracle.beta(inp.image, inp.zernike, inp.basis, inp.mlp)[0]
+    ref = np.zeros((20, 20))
+    scat = np.zeros((20, 20))
+    for y in range(20):
+        for x in range(20):
+            i, j = y - 10 + 3, x - 9 + 3
+            if 0 <= i < 7 and 0 <= j < 7:
+                ref[y, x] = np.dot(beta[:, y, x], inp.basis[:, i, j].astype(np.float64))
+                scat[y, x] = np.dot(beta[:, 10, 9], inp.basis[:, i, j].astype(np.float64))
+    np.testing.assert_allclose(J[0, 0], ref, rtol=0, atol=1e-13)
+    assert np.abs(ref - scat).max() > 1e-2
+
+
+def test_mean_preservation_constant_image():
+    """North-star (d): W = 0, b3 = s/|s|^2 with s_k = sum of taps of phi_k => sum_k beta_k s_k = 1;
+    a constant image stays constant through the blur (replicate) and any warp."""
+    inp = _small(9, C=3, S=9, K=7, tstd=2.5)
+    s = inp.basis.astype(np.float64).sum(axis=(1, 2))
+    inp.mlp = _mlp_const(inp.zernike.shape[1], 5, 7, (s / np.dot(s, s)).astype(np.float32))
+    inp.image = np.full_like(inp.image, 0.625)
+    out, J = _render(inp)
+    b3 = inp.mlp["b3"].astype(np.float64)
+    expect = 0.625 * np.dot(b3, s)  # = 0.625 up to the fp32 rounding of b3
+    assert abs(np.dot(b3, s) - 1) < 1e-6
+    np.testing.assert_allclose(J, expect, rtol=0, atol=1e-13)
+    np.testing.assert_allclose(out, expect, rtol=0, atol=1e-13)
+
+
+def test_linearity_in_image():
+    """North-star (b): out(2*I1 - I2) = 2*out(I1) - out(I2) with fixed Z and tilt (A12: no clamp).
+    Images on a 2^-10 grid so the fp32 combination is exact."""
+    inp = _small(10, C=2, S=5, K=4)
+    rng = np.random.default_rng(0)
+    I1 = (rng.integers(0, 1024, inp.image.shape) / 1024).astype(np.float32)
+    I2 = (rng.integers(0, 1024, inp.image.shape) / 1024).astype(np.float32)
+    outs = []
+    for I in (I1, I2, 2 * I1 - I2):
+        inp.image = I
+        outs.append(_render(inp)[0])
+    lhs, rhs = outs[2], 2 * outs[0] - outs[1]
+    assert np.abs(lhs - rhs).max() <= 1e-12 * max(1.0, np.abs(lhs).max())
+
+
+def test_colour_channels_share_beta():
+    """P7 / A13: a gray image replicated to 3 channels gives 3 identical outputs."""
+    inp = _small(11, C=3, S=5, K=4)
+    inp.image = np.repeat(inp.image[:, :1], 3, axis=1)
+    out, J = _render(inp)
+    assert np.array_equal(out[0, 0], out[0, 1]) and np.array_equal(out[0, 0], out[0, 2])
+
+
+# ---------------------------------------------------------------- step a3: tilt warp
+def test_zero_tilt_is_identity_warp():
+    """North-star (e): t = 0 => out = J exactly."""
+    inp = _small(12, C=2, tstd=0.0)
+    out, J = _render(inp)
+    np.testing.assert_array_equal(out, J)
+
+
+def test_warp_matches_grid_sample():
+    """P3 — backward bilinear warp, clamp-to-edge (A6-A8) equals torch grid_sample
+    (bilinear, padding 'border', align_corners=True) with grid = p - t normalised."""
+    rng = np.random.default_rng(1)
+    B, C, H, W = 2, 3, 19, 23
+    J = rng.standard_normal((B, C, H, W))
+    t = (rng.standard_normal((B, 2, H, W)) * 3).astype(np.float32)
+    out = oracle.warp(J, t)
+    yy, xx = np.meshgrid(np.arange(H), np.arange(W), indexing="ij")
+    gx = 2 * (xx[None] - t[:, 0].astype(np.float64)) / (W - 1) - 1
+    gy = 2 * (yy[None] - t[:, 1].astype(np.float64)) / (H - 1) - 1
+    grid = torch.from_numpy(np.stack([gx, gy], -1))
+    ref = torch.nn.functional.grid_sample(torch.from_numpy(J), grid, mode="bilinear",
+                                          padding_mode="border", align_corners=True).numpy()
+    np.testing.assert_allclose(out, ref, rtol=0, atol=1e-12)
+
+
+def test_warp_integer_and_half_shift():
+    """P4: t = (1, 0) moves content right one pixel, column 0 replicated;
+    t = (0.5, 0) averages with the left neighbour. t = (0, -2): content moves up 2 rows."""
+    rng = np.random.default_rng(2)
+    J = rng.standard_normal((1, 1, 8, 9))
+    t = np.zeros((1, 2, 8, 9), np.float32)
+    t[:, 0] = 1.0
+    left = J[..., np.maximum(np.arange(9) - 1, 0)]
+    np.testing.assert_array_equal(oracle.warp(J, t), left)
+    t[:, 0] = 0.5
+    np.testing.assert_allclose(oracle.warp(J, t), 0.5 * (left + J), rtol=0, atol=1e-15)
+    t[:, 0] = 0.0
+    t[:, 1] = -2.0
+    np.testing.assert_array_equal(oracle.warp(J, t), J[..., np.minimum(np.arange(8) + 2, 7), :])
+
+
+def test_warp_reproduces_affine_field():
+    """Bilinear interpolation is exact on affine functions: for J = a + b*y + c*x and samples
+    that stay inside the image, out(y,x) = a + b*(y - t1) + c*(x - t0)."""
+    H, W = 16, 18
+    yy, xx = np.meshgrid(np.arange(H), np.arange(W), indexing="ij")
+    J = (0.3 + 0.7 * yy - 1.1 * xx)[None, None].astype(np.float64)
+    rng = np.random.default_rng(3)
+    t = rng.uniform(-0.9, 0.9, (1, 2, H, W)).astype(np.float32)
+    out = oracle.warp(J, t)
+    ref = 0.3 + 0.7 * (yy - t[0, 1].astype(np.float64)) - 1.1 * (xx - t[0, 0].astype(np.float64))
+    inner = (slice(1, H - 1), slice(1, W - 1))
+    np.testing.assert_allclose(out[0, 0][inner], ref[inner], rtol=0, atol=1e-12)
+
+
+# ---------------------------------------------------------------- sampled / banded paths
+def test_pixels_and_rows_agree_with_full_render():
+    """The sampled path (used for full-size GPU parity) and the row-band path (used for the
+    bounded cpu_baseline sample) compute exactly what the full render computes."""
+    inp = _small(13, B=2, C=3, S=7, K=5, H=22, W=19, tstd=2.0)
+    out, J = _render(inp)
+    rng = np.random.default_rng(4)
+    bxy = np.stack([rng.integers(0, 2, 40), rng.integers(0, 22, 40), rng.integers(0, 19, 40)], 1)
+    bxy[:4] = [[0, 0, 0], [1, 21, 18], [0, 0, 18], [1, 21, 0]]
+    Jp, op = oracle.pixels(inp.image, inp.zernike, inp.tilt, inp.basis, inp.mlp, bxy)
+    np.testing.assert_array_equal(Jp, J[bxy[:, 0], :, bxy[:, 1], bxy[:, 2]])
+    np.testing.assert_array_equal(op, out[bxy[:, 0], :, bxy[:, 1], bxy[:, 2]])
+    out_band, _ = oracle.render(inp.image, inp.zernike, inp.tilt, inp.basis, inp.mlp, rows=(5, 12))
+    np.testing.assert_array_equal(out_band[:, :, 5:12], out[:, :, 5:12])
+
+
+def test_thread_count_does_not_change_results():
+    """Determinism regardless of worker count."""
+    inp = _small(14, C=2, S=5, K=4)
+    a, _ = oracle.render(inp.image, inp.zernike, inp.tilt, inp.basis, inp.mlp, threads=1)
+    b, _ = oracle.render(inp.image, inp.zernike, inp.tilt, inp.basis, inp.mlp, threads=5)
+    np.testing.assert_array_equal(a, b)
