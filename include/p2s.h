@@ -1,0 +1,140 @@
+/* p2s.h — C ABI of the B200-native Phase-to-Space (P2S) turbulence renderer.
+ *
+ * One frame = three steps of Mao, Chimitt & Chan, "Accelerating Atmospheric Turbulence
+ * Simulation via Learned Phase-to-Space Transform" (ICCV 2021; /root/reference/PAPER.md):
+ *   a1  P2S network: per pixel, "three fully connected layers" map the high-order Zernike
+ *       coefficients to the PSF-basis coefficients beta (Sec. 3.3);
+ *   a2  Eq. (5): y_n = sum_m beta_{m,n} phi_m^T x — M spatially invariant convolutions
+ *       weighted at the output pixel (Sec. 3.1);
+ *   a3  tilt: "locally shifting the image according to its tilt" after the blur
+ *       (PAPER.md:172), the first two Zernike coefficients "displace the pixels".
+ * Readings of the points the paper leaves open (true convolution, replicate borders,
+ * backward bilinear warp, ReLU hidden layers, no output clamp, ...) are DESIGN.md §3.
+ *
+ * Conventions for every entry point:
+ *  - Return a p2s_status; no C++ exception crosses the ABI. Argument/shape errors are
+ *    reported synchronously before any work is queued.
+ *  - "DEVICE" pointers are CUDA device pointers on the current device; "HOST" pointers are
+ *    ordinary host memory. All tensors are dense, row-major, fp32, 16-byte aligned (DEVICE).
+ *  - Work is queued on `stream` (NULL = legacy default stream) and is asynchronous: DEVICE
+ *    inputs must stay valid and unmodified, and outputs must not be read, until the
+ *    stream has reached the work. Asynchronous faults surface at the caller's next sync.
+ *  - A handle owns device copies of the basis/weights plus a workspace; it serves one
+ *    stream at a time (use one handle per concurrently rendering stream).
+ *  - Envelope (else P2S_ERR_UNSUPPORTED): S odd, 1 <= S <= 65; 1 <= K <= 128;
+ *    1 <= n_in <= 64; 1 <= h1, h2 <= 256; C in {1,2,3}; B, H, W >= 1; S*S >= 1;
+ *    device = sm_100 (B200).
+ */
+#ifndef P2S_H
+#define P2S_H
+
+#if defined(__GNUC__)
+#define P2S_API __attribute__((visibility("default")))
+#else
+#define P2S_API
+#endif
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+typedef enum {
+  P2S_OK = 0,
+  P2S_ERR_INVALID_ARG = 1, /* null pointer, inconsistent dims, aliasing output */
+  P2S_ERR_UNSUPPORTED = 2, /* outside the envelope above, or not an sm_100 device */
+  P2S_ERR_CUDA = 3,        /* a CUDA runtime/launch error (see p2s_last_cuda_error) */
+  P2S_ERR_OOM = 4          /* device allocation failed */
+} p2s_status;
+
+typedef struct CUstream_st* p2s_stream_t; /* == cudaStream_t */
+typedef struct CUevent_st* p2s_event_t;   /* == cudaEvent_t  */
+typedef struct p2s_handle p2s_handle;     /* opaque */
+
+/* PSF basis phi_k, k = 0..K-1 (the paper's M basis functions).
+ * HOST pointer to [K][S][S] fp32 row-major; taps[k][i][j] is the tap at offset
+ * (dy, dx) = (i - r, j - r), r = (S-1)/2, applied as a TRUE convolution (A2/A3). */
+typedef struct {
+  int K, S;
+  const float* taps;
+} p2s_basis;
+
+/* P2S network: beta = W3 relu(W2 relu(W1 z + b1) + b2) + b3.
+ * HOST pointers, torch.nn.Linear layout: W1 [h1][n_in], W2 [h2][h1], W3 [n_out][h2] row-major,
+ * b* [out]. n_out must equal the basis K. */
+typedef struct {
+  int n_in, h1, h2, n_out;
+  const float *W1, *b1, *W2, *b2, *W3, *b3;
+} p2s_mlp;
+
+/* Source image x of Eq. (3): DEVICE [B][C][H][W] fp32 (values in [0,1]
+ * for the stated tolerance; any finite values are accepted). Channels share beta and tilt
+ * (PAPER.md:320). */
+typedef struct {
+  const float* data;
+  int B, C, H, W;
+} p2s_image;
+
+/* Deep-copies and repacks `basis` and `mlp_weights` (the caller may free them on return):
+ * taps are flipped/regrouped into the tensor-core operand layout and converted to fp16,
+ * weights to fp16, biases and tap sums kept in fp32. Allocates device memory on the
+ * current device. On success *out_handle owns everything; release with p2s_destroy. */
+P2S_API p2s_status p2s_init(const p2s_basis* basis, const p2s_mlp* mlp_weights, p2s_handle** out_handle);
+
+/* Renders B frames: out = warp_t( J ), J_c = sum_k beta_k (I_c * phi_k), beta = P2S(z).
+ *   zernike_field DEVICE [B][n_in][H][W] fp32: per-pixel high-order Zernike coefficients
+ *                 (Noll Z4..Z36 for n_in = 33; "last K-2 coefficients").
+ *   tilt_field    DEVICE [B][2][H][W] fp32, in pixels; channel 0 = x (columns, alpha_2),
+ *                 channel 1 = y (rows, alpha_3). May be NULL (= zero tilt).
+ *                 out(y,x) = bilinear J at (y - t1, x - t0), clamp-to-edge.
+ *   out           DEVICE [B][C][H][W] fp32; must not overlap any input.
+ * No host synchronisation and no allocation, except the first use or growth of the
+ * handle's workspace (B*C*H*W fp32), which synchronises the device; p2s_reserve avoids it. */
+P2S_API p2s_status p2s_render(p2s_handle* h, p2s_image image, const float* zernike_field,
+                      const float* tilt_field, float* out, p2s_stream_t stream);
+
+/* Same computation with HOST buffers (same shapes as p2s_render): copies the inputs to the
+ * handle's device staging buffers, renders, copies `out` back, and synchronises `stream`
+ * before returning. Host buffers should be pinned for full copy bandwidth. */
+P2S_API p2s_status p2s_render_host(p2s_handle* h, const float* image_host, int B, int C, int H, int W,
+                           const float* zernike_host, const float* tilt_host, float* out_host,
+                           p2s_stream_t stream);
+
+/* Pre-sizes the workspace (and host-path staging) for frames up to B x C x H x W. */
+P2S_API p2s_status p2s_reserve(p2s_handle* h, int B, int C, int H, int W);
+
+/* When both events are non-NULL, every later p2s_render records ev_begin right before the
+ * fused MLP+convolution kernel and ev_end right after it on the render stream (so its
+ * duration can be timed alone); pass NULLs to stop. Events stay owned by the caller. */
+P2S_API p2s_status p2s_set_profile_events(p2s_handle* h, p2s_event_t ev_begin, p2s_event_t ev_end);
+
+/* Static facts about the handle's execution plan (for reports/tests). */
+typedef struct {
+  int K, S, n_in, h1, h2;
+  int n_pad, h1_pad, h2_pad, in_pad; /* tensor-core padded dims */
+  int conv_steps;                    /* 16-tap K-slices per channel (sum of taps padded) */
+  int smem_bytes;                    /* dynamic shared memory of the fused kernel */
+  int kernels_per_render;            /* launches queued by one p2s_render */
+} p2s_info;
+P2S_API p2s_status p2s_get_info(const p2s_handle* h, p2s_info* info);
+
+/* Releases every resource of the handle (synchronises the device). NULL is a no-op. */
+P2S_API void p2s_destroy(p2s_handle* h);
+
+/* Static string for a status code. */
+P2S_API const char* p2s_status_string(p2s_status s);
+
+/* Message of the last CUDA error seen by this library on this thread ("" if none). */
+P2S_API const char* p2s_last_cuda_error(void);
+
+/* ---- test/debug taps (same stream semantics as p2s_render) ----
+ * p2s_debug_beta: step a1 only; beta_out DEVICE [B][K][H][W] fp32.
+ * p2s_debug_blur: steps a1+a2 only (no warp); J_out DEVICE [B][C][H][W] fp32. */
+P2S_API p2s_status p2s_debug_beta(p2s_handle* h, const float* zernike_field, int B, int H, int W,
+                          float* beta_out, p2s_stream_t stream);
+P2S_API p2s_status p2s_debug_blur(p2s_handle* h, p2s_image image, const float* zernike_field,
+                          float* J_out, p2s_stream_t stream);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* P2S_H */

@@ -1,0 +1,211 @@
+"""Python binding of the C ABI in include/p2s.h (argument marshalling only).
+
+Every step of the hot path runs in libp2s.so (sm_100a kernels); this module only turns
+numpy arrays / torch CUDA tensors into the plain pointers, sizes and stream handles the
+C ABI takes. There is no CPU fallback: if the library is missing or the device is not a
+B200 the calls raise.
+
+Names follow the ABI: ``p2s_init`` -> :class:`Renderer`, ``p2s_render`` ->
+:meth:`Renderer.render`, ``p2s_render_host`` -> :meth:`Renderer.render_host`,
+``p2s_debug_beta`` / ``p2s_debug_blur`` -> :meth:`Renderer.debug_beta` / :meth:`Renderer.debug_blur`.
+"""
+from __future__ import annotations
+
+import ctypes
+import os
+from typing import Optional
+
+import numpy as np
+
+_PKG = os.path.dirname(os.path.abspath(__file__))
+LIB_PATH = os.path.join(_PKG, "libp2s.so")
+
+P2S_OK, P2S_ERR_INVALID_ARG, P2S_ERR_UNSUPPORTED, P2S_ERR_CUDA, P2S_ERR_OOM = range(5)
+
+EXPORTED = ("p2s_init", "p2s_render", "p2s_render_host", "p2s_reserve", "p2s_set_profile_events",
+            "p2s_get_info", "p2s_destroy", "p2s_status_string", "p2s_last_cuda_error",
+            "p2s_debug_beta", "p2s_debug_blur")
+
+
+class P2SError(RuntimeError):
+    def __init__(self, status: int, what: str):
+        lib = _lib
+        name = lib.p2s_status_string(status).decode() if lib else str(status)
+        cuda = lib.p2s_last_cuda_error().decode() if lib else ""
+        super().__init__(f"{what}: {name}" + (f" ({cuda})" if cuda and status == P2S_ERR_CUDA else ""))
+        self.status = status
+
+
+class _Basis(ctypes.Structure):
+    _fields_ = [("K", ctypes.c_int), ("S", ctypes.c_int), ("taps", ctypes.c_void_p)]
+
+
+class _Mlp(ctypes.Structure):
+    _fields_ = [("n_in", ctypes.c_int), ("h1", ctypes.c_int), ("h2", ctypes.c_int), ("n_out", ctypes.c_int),
+                ("W1", ctypes.c_void_p), ("b1", ctypes.c_void_p), ("W2", ctypes.c_void_p),
+                ("b2", ctypes.c_void_p), ("W3", ctypes.c_void_p), ("b3", ctypes.c_void_p)]
+
+
+class _Image(ctypes.Structure):
+    _fields_ = [("data", ctypes.c_void_p), ("B", ctypes.c_int), ("C", ctypes.c_int), ("H", ctypes.c_int),
+                ("W", ctypes.c_int)]
+
+
+class Info(ctypes.Structure):
+    _fields_ = [(n, ctypes.c_int) for n in ("K", "S", "n_in", "h1", "h2", "n_pad", "h1_pad", "h2_pad",
+                                            "in_pad", "conv_steps", "smem_bytes", "kernels_per_render")]
+
+    def as_dict(self):
+        return {n: getattr(self, n) for n, _ in self._fields_}
+
+
+_lib = None
+
+
+def load_library(path: str = LIB_PATH) -> ctypes.CDLL:
+    """Loads libp2s.so (built by ``paper_2107_11627_b200.build``); raises if absent."""
+    global _lib
+    if _lib is not None:
+        return _lib
+    if not os.path.exists(path):
+        raise ImportError(f"{path} is missing: run `python -m paper_2107_11627_b200.build` "
+                          "(the CUDA path has no fallback)")
+    lib = ctypes.CDLL(path)
+    v, i, st = ctypes.c_void_p, ctypes.c_int, ctypes.c_int
+    lib.p2s_init.argtypes = [ctypes.POINTER(_Basis), ctypes.POINTER(_Mlp), ctypes.POINTER(v)]
+    lib.p2s_render.argtypes = [v, _Image, v, v, v, v]
+    lib.p2s_render_host.argtypes = [v, v, i, i, i, i, v, v, v, v]
+    lib.p2s_reserve.argtypes = [v, i, i, i, i]
+    lib.p2s_set_profile_events.argtypes = [v, v, v]
+    lib.p2s_get_info.argtypes = [v, ctypes.POINTER(Info)]
+    lib.p2s_destroy.argtypes = [v]
+    lib.p2s_destroy.restype = None
+    lib.p2s_status_string.argtypes = [st]
+    lib.p2s_status_string.restype = ctypes.c_char_p
+    lib.p2s_last_cuda_error.argtypes = []
+    lib.p2s_last_cuda_error.restype = ctypes.c_char_p
+    lib.p2s_debug_beta.argtypes = [v, v, i, i, i, v, v]
+    lib.p2s_debug_blur.argtypes = [v, _Image, v, v, v]
+    for name in ("p2s_init", "p2s_render", "p2s_render_host", "p2s_reserve", "p2s_set_profile_events",
+                 "p2s_get_info", "p2s_debug_beta", "p2s_debug_blur"):
+        getattr(lib, name).restype = st
+    _lib = lib
+    return lib
+
+
+def _check(status: int, what: str):
+    if status != P2S_OK:
+        raise P2SError(status, what)
+
+
+def _f32(a) -> np.ndarray:
+    return np.ascontiguousarray(a, dtype=np.float32)
+
+
+def _dev_ptr(t, name, shape=None):
+    import torch
+    if not isinstance(t, torch.Tensor) or not t.is_cuda or t.dtype != torch.float32 or not t.is_contiguous():
+        raise ValueError(f"{name} must be a contiguous float32 CUDA tensor")
+    if shape is not None and tuple(t.shape) != tuple(shape):
+        raise ValueError(f"{name} has shape {tuple(t.shape)}, expected {tuple(shape)}")
+    return ctypes.c_void_p(t.data_ptr())
+
+
+def _stream_handle(stream):
+    import torch
+    s = stream if stream is not None else torch.cuda.current_stream()
+    return ctypes.c_void_p(s.cuda_stream)
+
+
+class Renderer:
+    """One p2s handle: device copies of the PSF basis phi_k and the P2S MLP weights."""
+
+    def __init__(self, basis: np.ndarray, mlp: dict):
+        lib = load_library()
+        basis = _f32(basis)
+        K, S, S2 = basis.shape
+        assert S == S2
+        self._keep = {k: _f32(v) for k, v in mlp.items()}
+        m = self._keep
+        h1, n_in = m["W1"].shape
+        h2 = m["W2"].shape[0]
+        n_out = m["W3"].shape[0]
+        b = _Basis(K, S, basis.ctypes.data)
+        ml = _Mlp(n_in, h1, h2, n_out, *(m[k].ctypes.data for k in ("W1", "b1", "W2", "b2", "W3", "b3")))
+        h = ctypes.c_void_p()
+        _check(lib.p2s_init(ctypes.byref(b), ctypes.byref(ml), ctypes.byref(h)), "p2s_init")
+        self._h = h
+        self.K, self.S, self.n_in = K, S, n_in
+        self._lib = lib
+
+    # -------------------------------------------------------------- device API
+    def render(self, image, zernike, tilt=None, out=None, stream=None):
+        """p2s_render on CUDA tensors: image [B,C,H,W], zernike [B,n_in,H,W], tilt [B,2,H,W]|None."""
+        import torch
+        B, C, H, W = image.shape
+        im = _Image(_dev_ptr(image, "image").value, B, C, H, W)
+        zp = _dev_ptr(zernike, "zernike_field", (B, self.n_in, H, W))
+        tp = _dev_ptr(tilt, "tilt_field", (B, 2, H, W)) if tilt is not None else ctypes.c_void_p()
+        if out is None:
+            out = torch.empty_like(image)
+        op = _dev_ptr(out, "out", (B, C, H, W))
+        _check(self._lib.p2s_render(self._h, im, zp, tp, op, _stream_handle(stream)), "p2s_render")
+        return out
+
+    def debug_beta(self, zernike, out=None, stream=None):
+        import torch
+        B, n_in, H, W = zernike.shape
+        if out is None:
+            out = torch.empty((B, self.K, H, W), device=zernike.device, dtype=torch.float32)
+        _check(self._lib.p2s_debug_beta(self._h, _dev_ptr(zernike, "zernike_field", (B, self.n_in, H, W)),
+                                        B, H, W, _dev_ptr(out, "beta_out", (B, self.K, H, W)),
+                                        _stream_handle(stream)), "p2s_debug_beta")
+        return out
+
+    def debug_blur(self, image, zernike, out=None, stream=None):
+        import torch
+        B, C, H, W = image.shape
+        if out is None:
+            out = torch.empty_like(image)
+        im = _Image(_dev_ptr(image, "image").value, B, C, H, W)
+        _check(self._lib.p2s_debug_blur(self._h, im, _dev_ptr(zernike, "zernike_field", (B, self.n_in, H, W)),
+                                        _dev_ptr(out, "J_out", (B, C, H, W)), _stream_handle(stream)),
+               "p2s_debug_blur")
+        return out
+
+    # -------------------------------------------------------------- host API (e2e)
+    def render_host(self, image: np.ndarray, zernike: np.ndarray, tilt: Optional[np.ndarray],
+                    out: np.ndarray, stream=None) -> np.ndarray:
+        """p2s_render_host: host buffers in and out (copies inside), synchronous."""
+        B, C, H, W = image.shape
+        for a, n in ((image, "image"), (zernike, "zernike"), (out, "out")):
+            if a.dtype != np.float32 or not a.flags.c_contiguous:
+                raise ValueError(f"{n} must be C-contiguous float32")
+        tp = tilt.ctypes.data if tilt is not None else None
+        _check(self._lib.p2s_render_host(self._h, image.ctypes.data, B, C, H, W, zernike.ctypes.data, tp,
+                                         out.ctypes.data, _stream_handle(stream)), "p2s_render_host")
+        return out
+
+    def reserve(self, B, C, H, W):
+        _check(self._lib.p2s_reserve(self._h, B, C, H, W), "p2s_reserve")
+
+    def set_profile_events(self, ev_begin=None, ev_end=None):
+        a = ctypes.c_void_p(ev_begin.cuda_event) if ev_begin is not None else ctypes.c_void_p()
+        b = ctypes.c_void_p(ev_end.cuda_event) if ev_end is not None else ctypes.c_void_p()
+        _check(self._lib.p2s_set_profile_events(self._h, a, b), "p2s_set_profile_events")
+
+    def info(self) -> dict:
+        inf = Info()
+        _check(self._lib.p2s_get_info(self._h, ctypes.byref(inf)), "p2s_get_info")
+        return inf.as_dict()
+
+    def close(self):
+        if getattr(self, "_h", None):
+            self._lib.p2s_destroy(self._h)
+            self._h = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
