@@ -190,6 +190,10 @@ class Renderer:
         _check(self._lib.p2s_reserve(self._h, B, C, H, W), "p2s_reserve")
 
     def set_profile_events(self, ev_begin=None, ev_end=None):
+        """p2s_set_profile_events with torch.cuda.Event objects (created on first use)."""
+        for ev in (ev_begin, ev_end):
+            if ev is not None and not ev.cuda_event:
+                ev.record()  # torch creates the CUDA event lazily on its first record
         a = ctypes.c_void_p(ev_begin.cuda_event) if ev_begin is not None else ctypes.c_void_p()
         b = ctypes.c_void_p(ev_end.cuda_event) if ev_end is not None else ctypes.c_void_p()
         _check(self._lib.p2s_set_profile_events(self._h, a, b), "p2s_set_profile_events")
