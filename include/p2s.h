@@ -133,6 +133,10 @@ P2S_API p2s_status p2s_debug_beta(p2s_handle* h, const float* zernike_field, int
                           float* beta_out, p2s_stream_t stream);
 P2S_API p2s_status p2s_debug_blur(p2s_handle* h, p2s_image image, const float* zernike_field,
                           float* J_out, p2s_stream_t stream);
+/* p2s_debug_profile_buffer: in a library built with -DP2S_PROFILE, later launches write per-CTA
+ * role timers (clock64 cycles; layout documented in tools/role_profile.py) to
+ * device_counters [grid][4][20] u64; NULL disables. Other builds return P2S_ERR_UNSUPPORTED. */
+P2S_API p2s_status p2s_debug_profile_buffer(p2s_handle* h, void* device_counters);
 
 #ifdef __cplusplus
 }

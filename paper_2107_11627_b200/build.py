@@ -9,31 +9,33 @@ PKG = os.path.dirname(os.path.abspath(__file__))
 ROOT = os.path.dirname(PKG)
 CSRC = os.path.join(PKG, "csrc")
 LIB = os.path.join(PKG, "libp2s.so")
+LIB_PROF = os.path.join(PKG, "libp2s_prof.so")  # -DP2S_PROFILE variant (tools only)
 SOURCES = [os.path.join(CSRC, "p2s_host.cu")]
 DEPS = SOURCES + [os.path.join(CSRC, f) for f in ("p2s_kernels.cuh", "sm100.cuh")] + \
     [os.path.join(ROOT, "include", "p2s.h")]
 NVCC = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")
 FLAGS = ["-gencode", "arch=compute_100a,code=sm_100a", "-O3", "-lineinfo", "-std=c++17",
          "-shared", "-Xcompiler", "-fPIC", "-Xcompiler", "-fvisibility=hidden",
-         "-Xptxas", "-v", f"-I{os.path.join(ROOT, 'include')}", f"-I{CSRC}"]
+         "-Xptxas", "-v", "-maxrregcount=144", f"-I{os.path.join(ROOT, 'include')}", f"-I{CSRC}"]
 
 
-def build(force: bool = False, verbose: bool = False) -> str:
-    stale = force or not os.path.exists(LIB) or \
-        any(os.path.getmtime(d) > os.path.getmtime(LIB) for d in DEPS)
+def build(force: bool = False, verbose: bool = False, profile: bool = False) -> str:
+    lib = LIB_PROF if profile else LIB
+    stale = force or not os.path.exists(lib) or \
+        any(os.path.getmtime(d) > os.path.getmtime(lib) for d in DEPS)
     if not stale:
-        return LIB
-    tmp = LIB + f".tmp{os.getpid()}"
-    cmd = [NVCC, *FLAGS, *SOURCES, "-o", tmp]
+        return lib
+    tmp = lib + f".tmp{os.getpid()}"
+    cmd = [NVCC, *FLAGS, *(["-DP2S_PROFILE"] if profile else []), *SOURCES, "-o", tmp]
     r = subprocess.run(cmd, capture_output=True, text=True)
     if r.returncode != 0:
         sys.stderr.write(r.stdout + r.stderr)
         raise RuntimeError("nvcc failed building libp2s.so")
     if verbose:
         sys.stderr.write(r.stderr)
-    os.replace(tmp, LIB)
-    return LIB
+    os.replace(tmp, lib)
+    return lib
 
 
 if __name__ == "__main__":
-    print(build(force="--force" in sys.argv, verbose=True))
+    print(build(force="--force" in sys.argv, verbose=True, profile="--profile" in sys.argv))

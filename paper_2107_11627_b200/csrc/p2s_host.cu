@@ -45,11 +45,12 @@ struct ConvStep { uint32_t off, lbo; Tap tap[16]; };
 struct ConvPlan {
   std::vector<ConvStep> steps;
   std::vector<int> ey_a0, ex_a;
-  int npos_y = 0, npos_x = 0, chan_bytes = 0;
+  int npos_y = 0, npos_x = 0, chan_bytes = 0, rr = 0;
 };
 
 ConvPlan plan_conv(int S) {
   ConvPlan P;
+  const int r = (S - 1) / 2, rr = (r + 3) / 4 * 4, sh = rr - r;  // E entry 0 <-> column x0 - rr
   const int nv16 = S / 16, L = S - 16 * nv16;
   int left = 0;  // 0 none, 1 H rows, 2 V8 block, 3 extra V16 group
   if (L == 0) left = 0;
@@ -63,13 +64,13 @@ ConvPlan plan_conv(int S) {
     for (int a = 16 * nv16; a < S; ++a) P.ex_a.push_back(a);
   const int nblk = (int)P.ey_a0.size(), nex = (int)P.ex_a.size();
   const int Pairs = ((S + 7) / 8 + 1) / 2;
-  P.npos_y = nblk ? 128 + S + 1 : 0;
-  P.npos_x = nex ? 128 + 16 * Pairs : 0;
+  P.npos_y = nblk ? (sh + 128 + S + 1 + 3) / 4 * 4 : 0;
+  P.npos_x = nex ? (sh + 128 + 16 * Pairs + 3) / 4 * 4 : 0;
   const uint32_t ystride = (uint32_t)P.npos_y * 16, xbase = (uint32_t)nblk * ystride;
   P.chan_bytes = (int)(xbase + (uint32_t)nex * P.npos_x * 16);
   for (int g = 0; g < ngroups; ++g)
     for (int b = 0; b < S; ++b) {
-      ConvStep st{(uint32_t)(2 * g) * ystride + (uint32_t)b * 16, ystride, {}};
+      ConvStep st{(uint32_t)(2 * g) * ystride + (uint32_t)(b + sh) * 16, ystride, {}};
       for (int kk = 0; kk < 16; ++kk) {
         const int a = 16 * g + 8 * (kk / 8) + (kk % 8);
         st.tap[kk] = a < S ? Tap{a, b} : Tap{-1, -1};
@@ -79,7 +80,7 @@ ConvPlan plan_conv(int S) {
   if (left == 2) {
     const int a0 = 16 * nv16;
     for (int b = 0; b < S; b += 2) {
-      ConvStep st{(uint32_t)(nblk - 1) * ystride + (uint32_t)b * 16, 16, {}};
+      ConvStep st{(uint32_t)(nblk - 1) * ystride + (uint32_t)(b + sh) * 16, 16, {}};
       for (int kk = 0; kk < 16; ++kk) {
         const int a = a0 + kk % 8, bb = b + kk / 8;
         st.tap[kk] = (a < S && bb < S) ? Tap{a, bb} : Tap{-1, -1};
@@ -90,11 +91,12 @@ ConvPlan plan_conv(int S) {
   for (int e = 0; e < nex; ++e)
     for (int pr = 0; pr < Pairs; ++pr) {
       const int b0 = 16 * pr;
-      ConvStep st{xbase + (uint32_t)e * P.npos_x * 16 + (uint32_t)b0 * 16, 128, {}};
+      ConvStep st{xbase + (uint32_t)e * P.npos_x * 16 + (uint32_t)(b0 + sh) * 16, 128, {}};
       for (int kk = 0; kk < 16; ++kk)
         st.tap[kk] = (b0 + kk < S) ? Tap{P.ex_a[e], b0 + kk} : Tap{-1, -1};
       P.steps.push_back(st);
     }
+  P.rr = rr;
   return P;
 }
 
@@ -108,20 +110,23 @@ constexpr int kSmemLimit = 232448;  // 227 KB opt-in per block on sm_100
 struct p2s_handle {
   int K, S, r, n_in, h1, h2, Nk, K1, N1, N2;
   ConvPlan plan;
-  std::vector<StageDesc> stages;
-  int nst_l[4];
-  int stage_bytes, nring, smem_bytes;
-  int off_ring, off_a1, off_a2, off_e, off_tab, off_bar, a1_sbo, a2_sbo;
+  std::vector<Item> items;  // [items_full | items_beta]
+  int n_items_full = 0, n_items_beta = 0;
+  MlpOp ops[kMaxOps];
+  int n_ops = 0;
+  int stage_bytes, nring, smem_bytes, n_ebuf, scr_col;
+  int off_ring, off_a1, off_a2, off_e, off_tab, off_const, off_red, off_bar, a1_sbo, a2_sbo;
   int sm_count;
   uint8_t* d_stream = nullptr;
-  StageDesc* d_stages = nullptr;
-  uint2* d_steps = nullptr;
-  float *d_b1 = nullptr, *d_b2 = nullptr, *d_b3 = nullptr, *d_s = nullptr;
+  Item* d_items = nullptr;
+  uint32_t* d_steps = nullptr;
+  float* d_consts = nullptr;
   float* d_J = nullptr;
   size_t J_cap = 0;
   float *h_img = nullptr, *h_z = nullptr, *h_t = nullptr, *h_out = nullptr;  // device staging (host path)
   size_t stage_px_cap = 0, stage_chw_cap = 0;
   cudaEvent_t ev_begin = nullptr, ev_end = nullptr;
+  unsigned long long* prof = nullptr;
 };
 
 namespace {
@@ -150,22 +155,28 @@ FusedParams make_params(const p2s_handle* h, int B, int C, int H, int W, int mod
   p.ntiles = B * p.nstrips * H;
   p.mode = mode;
   p.stream = h->d_stream;
-  p.stages = h->d_stages;
-  for (int i = 0; i < 4; ++i) p.nst_l[i] = h->nst_l[i];
-  p.nstages = h->nst_l[0] + h->nst_l[1] + h->nst_l[2] + h->nst_l[3];
+  p.items = h->d_items;
+  p.n_items_full = h->n_items_full;
+  p.n_items_beta = h->n_items_beta;
+  for (int i = 0; i < h->n_ops; ++i) p.ops[i] = h->ops[i];
+  p.n_ops = h->n_ops;
   p.conv_steps = h->d_steps;
   p.nconv = (int)h->plan.steps.size();
-  p.b1 = h->d_b1; p.b2 = h->d_b2; p.b3 = h->d_b3; p.svec = h->d_s;
-  p.K = h->K; p.Nk = h->Nk; p.K1 = h->K1; p.N1 = h->N1; p.N2 = h->N2; p.r = h->r;
+  p.consts = h->d_consts;
+  p.K = h->K; p.Nk = h->Nk; p.K1 = h->K1; p.N1 = h->N1; p.N2 = h->N2; p.r = h->r; p.rr = h->plan.rr;
   p.n_ey = (int)h->plan.ey_a0.size(); p.n_ex = (int)h->plan.ex_a.size();
   p.npos_y = h->plan.npos_y; p.npos_x = h->plan.npos_x;
   for (int i = 0; i < p.n_ey; ++i) p.ey_a0[i] = h->plan.ey_a0[i];
   for (int i = 0; i < p.n_ex; ++i) p.ex_a[i] = h->plan.ex_a[i];
   p.chan_bytes = h->plan.chan_bytes;
+  p.n_ebuf = h->n_ebuf;
+  p.scr_col = h->scr_col;
   p.stage_bytes = h->stage_bytes; p.nring = h->nring;
   p.off_ring = h->off_ring; p.off_a1 = h->off_a1; p.off_a2 = h->off_a2; p.off_e = h->off_e;
-  p.off_tab = h->off_tab; p.off_bar = h->off_bar; p.smem_bytes = h->smem_bytes;
+  p.off_tab = h->off_tab; p.off_const = h->off_const; p.off_red = h->off_red; p.off_bar = h->off_bar;
+  p.smem_bytes = h->smem_bytes;
   p.a1_sbo = h->a1_sbo; p.a2_sbo = h->a2_sbo;
+  p.prof = h->prof;
   return p;
 }
 
@@ -229,112 +240,163 @@ p2s_status p2s_init(const p2s_basis* basis, const p2s_mlp* mlp, p2s_handle** out
   h->plan = plan_conv(S);
   h->sm_count = prop.multiProcessorCount;
   const ConvPlan& P = h->plan;
-
-  // ---- shared-memory layout (E sized for C = 3)
   const int nconv = (int)P.steps.size();
+  if (nconv > kMaxConvSteps) { delete h; return P2S_ERR_UNSUPPORTED; }
+
+  // ---- TMEM: conv accumulators [0, 3*Nk), MLP scratch / beta [3*Nk, 3*Nk + CH)
+  h->scr_col = 3 * h->Nk;
+  const int CH = std::min(256, (512 - h->scr_col) / 16 * 16);  // widest MLP chunk
+  // ---- MLP ops: each layer split into <= 2 column chunks of <= CH (L3 = one chunk = beta)
+  const int layer_N[3] = {h->N1, h->N2, h->Nk};
+  const int layer_K[3] = {h->K1, h->N1, h->N2};
+  h->n_ops = 0;
+  for (int l = 0; l < 3; ++l) {
+    const int N = layer_N[l];
+    const int nch = (N + CH - 1) / CH;
+    if (nch > 2 || (l == 2 && nch > 1)) { delete h; return P2S_ERR_UNSUPPORTED; }
+    const int w0 = nch == 1 ? N : std::min(CH, (N / 2 + 15) / 16 * 16 > CH ? CH : 128);
+    int n0 = 0;
+    for (int c = 0; c < nch; ++c) {
+      const int w = nch == 1 ? N : (c == 0 ? w0 : N - w0);
+      h->ops[h->n_ops++] = MlpOp{l, n0, w, layer_K[l] / 16, c == 0, c == nch - 1};
+      n0 += w;
+    }
+  }
+
+  // ---- shared-memory layout
   const int a1_bytes = kTileM * h->K1 * 2;
   const int kh = std::max(h->N1, h->N2);
   const int a2_bytes = kTileM * kh * 2;
-  const int e_bytes = 3 * P.chan_bytes;
-  const int tab_bytes = kMaxStages * (int)sizeof(StageDesc) + nconv * 8;
-  const int bar_bytes = (8 + 2 * 4) * 8 + 16;
-  const int fixed = a1_bytes + a2_bytes + e_bytes + tab_bytes + bar_bytes + 4 * 128;
-  const int ring_avail = kSmemLimit - fixed;
+  const int e1_bytes = 3 * P.chan_bytes;
+  const int tab_bytes = kMaxItems * (int)sizeof(Item) + nconv * 4;
+  const int const_bytes = (2 * kMaxN + 256) * 4;
+  const int red_bytes = 2 * 128 * 16;
+  const int bar_bytes = (BAR_RING + 2 * 4) * 8 + 16;
+  auto al = [](int v) { return (v + 127) / 128 * 128; };
+  const int fixed = al(a1_bytes) + al(a2_bytes) + al(tab_bytes) + al(const_bytes) + al(red_bytes) + al(bar_bytes);
+  const int max_slab = std::max(std::max(CH, h->N1 > CH ? CH : h->N1), h->Nk) * 32;
+  int ring_avail = 0;
+  h->n_ebuf = 2;
+  for (; h->n_ebuf >= 1; --h->n_ebuf) {
+    ring_avail = kSmemLimit - fixed - al(h->n_ebuf * e1_bytes) - 1024;
+    if (ring_avail >= 3 * 16384) break;
+  }
+  if (h->n_ebuf < 1) h->n_ebuf = 1;
+  ring_avail = kSmemLimit - fixed - al(h->n_ebuf * e1_bytes) - 1024;
   int nring = 4, sb = 0;
   for (nring = 4; nring >= 2; --nring) {
     sb = std::min(32768, (ring_avail / nring) / 1024 * 1024);
-    if (sb >= 16384 || nring == 2) break;
+    if (sb >= 20480 || nring == 2) break;
   }
-  const int max_slab = std::max(std::max(h->N1, h->N2), h->Nk) * 32;
-  if (sb < max_slab || nconv > kMaxConvSteps) { delete h; return P2S_ERR_UNSUPPORTED; }
+  if (sb < max_slab) { delete h; return P2S_ERR_UNSUPPORTED; }
   h->nring = nring;
   h->stage_bytes = sb;
   int off = 0;
   h->off_ring = off; off += nring * sb;
-  h->off_a1 = off; off += (a1_bytes + 127) / 128 * 128;
-  h->off_a2 = off; off += (a2_bytes + 127) / 128 * 128;
-  h->off_e = off; off += (e_bytes + 127) / 128 * 128;
-  h->off_tab = off; off += (tab_bytes + 127) / 128 * 128;
-  h->off_bar = off; off += (8 + 2 * nring) * 8 + 16;
+  h->off_a1 = off; off += al(a1_bytes);
+  h->off_a2 = off; off += al(a2_bytes);
+  h->off_e = off; off += al(h->n_ebuf * e1_bytes);
+  h->off_tab = off; off += al(tab_bytes);
+  h->off_const = off; off += al(const_bytes);
+  h->off_red = off; off += al(red_bytes);
+  h->off_bar = off; off += (BAR_RING + 2 * nring) * 8 + 16;
   h->smem_bytes = off;
   h->a1_sbo = (h->K1 / 8) * 128;
   h->a2_sbo = (kh / 8) * 128;
   if (h->smem_bytes > kSmemLimit) { delete h; return P2S_ERR_UNSUPPORTED; }
 
-  // ---- pack the streamed B operands: [W1 slabs][W2 slabs][W3 slabs][conv slabs]
-  const int n_slabs[4] = {h->K1 / 16, h->N1 / 16, h->N2 / 16, nconv};
-  const int rows[4] = {h->N1, h->N2, h->Nk, h->Nk};
-  size_t layer_off[4], total = 0;
-  for (int l = 0; l < 4; ++l) { layer_off[l] = total; total += (size_t)n_slabs[l] * rows[l] * 32; }
+  // ---- pack the streamed B operands: [op 0 slabs]...[op n-1 slabs][conv slabs]
+  //      op slab (ks) = rows [n0, n0+N) of the layer weight, K columns [16ks, 16ks+16)
+  std::vector<size_t> op_off(h->n_ops);
+  size_t total = 0;
+  for (int o = 0; o < h->n_ops; ++o) { op_off[o] = total; total += (size_t)h->ops[o].nks * h->ops[o].N * 32; }
+  const size_t conv_off = total;
+  total += (size_t)nconv * h->Nk * 32;
   std::vector<__half> stream(total / 2, __float2half(0.f));
-  auto put = [&](int l, int ks, int n, int kk, float v) {
-    stream[layer_off[l] / 2 + (size_t)ks * rows[l] * 16 + slab_idx(n, kk)] = __float2half_rn(v);
-  };
-  for (int ks = 0; ks < n_slabs[0]; ++ks)
-    for (int n = 0; n < h->h1; ++n)
-      for (int kk = 0; kk < 16; ++kk) {
-        const int k = ks * 16 + kk;
-        if (k < h->n_in) put(0, ks, n, kk, mlp->W1[(size_t)n * h->n_in + k]);
-      }
-  for (int ks = 0; ks < n_slabs[1]; ++ks)
-    for (int n = 0; n < h->h2; ++n)
-      for (int kk = 0; kk < 16; ++kk) {
-        const int k = ks * 16 + kk;
-        if (k < h->h1) put(1, ks, n, kk, mlp->W2[(size_t)n * h->h1 + k]);
-      }
-  for (int ks = 0; ks < n_slabs[2]; ++ks)
-    for (int n = 0; n < K; ++n)
-      for (int kk = 0; kk < 16; ++kk) {
-        const int k = ks * 16 + kk;
-        if (k < h->h2) put(2, ks, n, kk, mlp->W3[(size_t)n * h->h2 + k]);
-      }
+  const float* Wl[3] = {mlp->W1, mlp->W2, mlp->W3};
+  const int outl[3] = {h->h1, h->h2, K}, inl[3] = {h->n_in, h->h1, h->h2};
+  for (int o = 0; o < h->n_ops; ++o) {
+    const MlpOp& op = h->ops[o];
+    for (int ks = 0; ks < op.nks; ++ks)
+      for (int n = 0; n < op.N; ++n)
+        for (int kk = 0; kk < 16; ++kk) {
+          const int row = op.n0 + n, k = ks * 16 + kk;
+          if (row < outl[op.layer] && k < inl[op.layer])
+            stream[op_off[o] / 2 + (size_t)ks * op.N * 16 + slab_idx(n, kk)] =
+                __float2half_rn(Wl[op.layer][(size_t)row * inl[op.layer] + k]);
+        }
+  }
   for (int g = 0; g < nconv; ++g)
     for (int n = 0; n < K; ++n)
       for (int kk = 0; kk < 16; ++kk) {
         const Tap t = P.steps[g].tap[kk];
         if (t.a < 0) continue;
         // psi[a][b] = phi[S-1-a][S-1-b]  (true convolution, A2)
-        put(3, g, n, kk, basis->taps[((size_t)n * S + (S - 1 - t.a)) * S + (S - 1 - t.b)]);
+        stream[conv_off / 2 + (size_t)g * h->Nk * 16 + slab_idx(n, kk)] =
+            __float2half_rn(basis->taps[((size_t)n * S + (S - 1 - t.a)) * S + (S - 1 - t.b)]);
       }
-  // ---- stage list
-  for (int l = 0; l < 4; ++l) {
-    const int slab = rows[l] * 32;
-    const int per = std::max(1, sb / slab);
-    h->nst_l[l] = 0;
-    for (int s0 = 0; s0 < n_slabs[l]; s0 += per) {
-      const int ns = std::min(per, n_slabs[l] - s0);
-      h->stages.push_back(StageDesc{(uint32_t)(layer_off[l] + (size_t)s0 * slab), (uint32_t)(ns * slab),
-                                    (uint32_t)l, (uint32_t)s0});
-      h->nst_l[l]++;
+
+  // ---- per-tile item lists (ring stages in issue order)
+  auto op_items = [&](int o, std::vector<Item>& out) {
+    const MlpOp& op = h->ops[o];
+    const int slab = op.N * 32, per = std::max(1, sb / slab);
+    for (int s0 = 0; s0 < op.nks; s0 += per) {
+      const int ns = std::min(per, op.nks - s0);
+      uint8_t fl = (s0 == 0 ? IT_BEGIN : 0) | (s0 + ns >= op.nks ? IT_END : 0);
+      out.push_back(Item{(uint32_t)(op_off[o] + (size_t)s0 * slab), (uint32_t)(ns * slab), (uint16_t)s0,
+                         (uint16_t)ns, 0, (uint8_t)o, fl, 0});
+    }
+  };
+  std::vector<Item> conv_items;
+  {
+    const int slab = h->Nk * 32, per = std::max(1, sb / slab);
+    for (int s0 = 0; s0 < nconv; s0 += per) {
+      const int ns = std::min(per, nconv - s0);
+      uint8_t fl = (s0 == 0 ? IT_BEGIN : 0) | (s0 + ns >= nconv ? IT_END : 0);
+      conv_items.push_back(Item{(uint32_t)(conv_off + (size_t)s0 * slab), (uint32_t)(ns * slab), (uint16_t)s0,
+                                (uint16_t)ns, 1, 0, fl, 0});
     }
   }
-  if ((int)h->stages.size() > kMaxStages) { delete h; return P2S_ERR_UNSUPPORTED; }
-  // ---- biases (zero-padded), tap sums s_k = sum phi_k (for the centred-image identity)
-  std::vector<float> b1(h->N1, 0.f), b2(h->N2, 0.f), b3(h->Nk, 0.f), sv(h->Nk, 0.f);
-  for (int i = 0; i < h->h1; ++i) b1[i] = mlp->b1[i];
-  for (int i = 0; i < h->h2; ++i) b2[i] = mlp->b2[i];
-  for (int i = 0; i < K; ++i) {
-    b3[i] = mlp->b3[i];
-    double s = 0.0;
-    for (int t = 0; t < S * S; ++t) s += basis->taps[(size_t)i * S * S + t];
-    sv[i] = (float)s;
+  std::vector<Item> full, beta;
+  size_t ci = 0;
+  for (int o = 0; o < h->n_ops; ++o) {
+    op_items(o, full);
+    op_items(o, beta);
+    // one conv stage after every MLP op but the last (L3) covers the epilogue's drain;
+    // L3 is always issued before the last conv stage so ACC_FULL covers it
+    if (o + 1 < h->n_ops && ci + 1 < conv_items.size()) full.push_back(conv_items[ci++]);
   }
-  std::vector<uint2> steps(nconv);
-  for (int g = 0; g < nconv; ++g) steps[g] = make_uint2(P.steps[g].off, P.steps[g].lbo);
+  while (ci < conv_items.size()) full.push_back(conv_items[ci++]);
+  h->n_items_full = (int)full.size();
+  h->n_items_beta = (int)beta.size();
+  if (h->n_items_full > kMaxItems || h->n_items_beta > kMaxItems) { delete h; return P2S_ERR_UNSUPPORTED; }
+  h->items = full;
+  h->items.insert(h->items.end(), beta.begin(), beta.end());
 
-  auto fail = [&](p2s_status s) { p2s_destroy(h); return s; };
+  // ---- constants: b1, b2 (kMaxN each), b3, svec (128 each), zero padded;
+  //      svec[k] = sum of the taps of phi_k (centred-image identity)
+  std::vector<float> consts(2 * kMaxN + 256, 0.f);
+  for (int i = 0; i < h->h1; ++i) consts[i] = mlp->b1[i];
+  for (int i = 0; i < h->h2; ++i) consts[kMaxN + i] = mlp->b2[i];
+  for (int i = 0; i < K; ++i) {
+    consts[2 * kMaxN + i] = mlp->b3[i];
+    double sum = 0.0;
+    for (int t = 0; t < S * S; ++t) sum += basis->taps[(size_t)i * S * S + t];
+    consts[2 * kMaxN + 128 + i] = (float)sum;
+  }
+  std::vector<uint32_t> steps(nconv);
+  for (int g = 0; g < nconv; ++g) steps[g] = (P.steps[g].off >> 4) | ((P.steps[g].lbo >> 4) << 16);
+
+  auto fail = [&](p2s_status st) { p2s_destroy(h); return st; };
   cudaError_t e;
-#define UP(dst, src, bytes)                                                        \
-  if ((e = cudaMalloc(&(dst), (bytes))) != cudaSuccess) return fail(cuda_fail(e, "cudaMalloc")); \
-  if ((e = cudaMemcpy((dst), (src), (bytes), cudaMemcpyHostToDevice)) != cudaSuccess) \
+#define UP(dst, src, bytes)                                                                         \
+  if ((e = cudaMalloc(&(dst), (bytes))) != cudaSuccess) return fail(cuda_fail(e, "cudaMalloc"));   \
+  if ((e = cudaMemcpy((dst), (src), (bytes), cudaMemcpyHostToDevice)) != cudaSuccess)               \
     return fail(cuda_fail(e, "cudaMemcpy"));
   UP(h->d_stream, stream.data(), total);
-  UP(h->d_stages, h->stages.data(), h->stages.size() * sizeof(StageDesc));
-  UP(h->d_steps, steps.data(), steps.size() * sizeof(uint2));
-  UP(h->d_b1, b1.data(), b1.size() * 4);
-  UP(h->d_b2, b2.data(), b2.size() * 4);
-  UP(h->d_b3, b3.data(), b3.size() * 4);
-  UP(h->d_s, sv.data(), sv.size() * 4);
+  UP(h->d_items, h->items.data(), h->items.size() * sizeof(Item));
+  UP(h->d_steps, steps.data(), steps.size() * sizeof(uint32_t));
+  UP(h->d_consts, consts.data(), consts.size() * 4);
 #undef UP
   if ((e = cudaFuncSetAttribute(k_fused_p2s, cudaFuncAttributeMaxDynamicSharedMemorySize, kSmemLimit)) !=
       cudaSuccess)
@@ -447,6 +509,17 @@ p2s_status p2s_render_host(p2s_handle* h, const float* image_host, int B, int C,
   return P2S_OK;
 }
 
+p2s_status p2s_debug_profile_buffer(p2s_handle* h, void* device_counters) {
+  if (!h) return P2S_ERR_INVALID_ARG;
+#ifdef P2S_PROFILE
+  h->prof = (unsigned long long*)device_counters;
+  return P2S_OK;
+#else
+  (void)device_counters;
+  return P2S_ERR_UNSUPPORTED;
+#endif
+}
+
 p2s_status p2s_get_info(const p2s_handle* h, p2s_info* info) {
   if (!h || !info) return P2S_ERR_INVALID_ARG;
   info->K = h->K; info->S = h->S; info->n_in = h->n_in; info->h1 = h->h1; info->h2 = h->h2;
@@ -460,8 +533,7 @@ p2s_status p2s_get_info(const p2s_handle* h, p2s_info* info) {
 void p2s_destroy(p2s_handle* h) {
   if (!h) return;
   cudaDeviceSynchronize();
-  cudaFree(h->d_stream); cudaFree(h->d_stages); cudaFree(h->d_steps);
-  cudaFree(h->d_b1); cudaFree(h->d_b2); cudaFree(h->d_b3); cudaFree(h->d_s);
+  cudaFree(h->d_stream); cudaFree(h->d_items); cudaFree(h->d_steps); cudaFree(h->d_consts);
   cudaFree(h->d_J);
   cudaFree(h->h_img); cudaFree(h->h_z); cudaFree(h->h_t); cudaFree(h->h_out);
   delete h;

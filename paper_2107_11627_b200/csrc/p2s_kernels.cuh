@@ -10,39 +10,60 @@
 // Layouts:
 //  * UMMA operands use the SWIZZLE_NONE K-major canonical layout: element (row, k) at
 //    (row%8)*16 + (row/8)*SBO + (k%8)*2 + (k/8)*LBO.
-//  * B operands (weights, basis) are pre-packed on the host into 16-K "slabs"
-//    (LBO = 128, SBO = 256 -> rows*32 bytes) and streamed by the bulk-copy engine into a
-//    ring of multi-slab stages.
-//  * The convolution A operand (im2col, one input channel) is never materialised per
+//  * B operands (weight chunks, basis) are pre-packed on the host into 16-K "slabs"
+//    (LBO = 128, SBO = 256 -> rows*32 bytes), in exactly the order the MMA issuer consumes
+//    them, and streamed by the bulk-copy (TMA) engine into a ring of multi-slab stages.
+//  * The convolution A operand (im2col of one input channel) is never materialised per
 //    K-step: an 8x-expanded view of the image ("EY" blocks: 8 consecutive rows of one
 //    column per 16-byte entry; "EX" rows: 8 consecutive columns of one row) is built once
-//    per tile, and each K-step addresses it with an overlapping descriptor (SBO = 16 B per
-//    pixel row, LBO = block stride / 128 B / 16 B). See plan_conv() in p2s_host.cu.
+//    per tile (double-buffered), and each K-step addresses it with an overlapping
+//    descriptor (SBO = 16 B per pixel row). See plan_conv() in p2s_host.cu.
+//
+// Schedule per tile (one thread issues every UMMA; items come from a host-built list):
+//   L1 chunk 0 | conv stage | L1 chunk 1 | conv stage | L2 chunk 0 | conv stage | ... | L3 |
+//   remaining conv stages. MLP chunks accumulate in a TMEM "scratch" region next to the
+//   C conv accumulators; the epilogue warps drain each chunk (bias, ReLU, fp16) into the
+//   shared-memory A operand of the next layer while the tensor core runs conv stages.
 #pragma once
 #include "sm100.cuh"
 
 namespace p2s {
 
 constexpr int kTileM = 128;          // pixels per tile (UMMA M)
-constexpr int kThreads = 320;        // 10 warps
 constexpr int kWarpProducer = 0;     // bulk-copy producer (lane 0)
 constexpr int kWarpMma = 1;          // UMMA issuer (lane 0) + TMEM owner
 constexpr int kWarpBuild0 = 2;       // warps 2..5: A1 (Zernike tile) and E (im2col views)
-constexpr int kWarpEpi0 = 6;         // warps 6..9: TMEM drains, MLP activations, J epilogue
-constexpr int kBuildThreads = 128;
-constexpr int kEpiThreads = 128;
+constexpr int kNumBuildWarps = 4;
+constexpr int kWarpEpi0 = kWarpBuild0 + kNumBuildWarps;  // warps 6..13: two epilogue warpgroups
+constexpr int kNumEpiWarps = 8;
+constexpr int kThreads = 32 * (kWarpEpi0 + kNumEpiWarps);  // 448
+constexpr int kBuildThreads = 32 * kNumBuildWarps;
 constexpr uint32_t kTmemCols = 512;
-constexpr uint32_t kBetaCol = 384;   // beta (L3 accumulator) lives in columns [384, 384+Nk)
-constexpr int kMaxStages = 128;      // per-tile stage list capacity
+constexpr int kMaxItems = 96;        // per-tile item list capacity (both modes together)
 constexpr int kMaxConvSteps = 512;
+constexpr int kMaxOps = 6;
 constexpr int kMaxEy = 16, kMaxEx = 4;
+constexpr int kMaxN = 256;           // padded bias vectors
 
-// One ring stage = nslabs consecutive 16-K slabs of one layer, contiguous in the stream.
-struct StageDesc {
+// One ring stage ("item") = nslabs consecutive 16-K slabs of one MLP op or of the conv.
+enum ItemFlags : uint8_t { IT_BEGIN = 1, IT_END = 2 };
+struct Item {
   uint32_t src_off;   // byte offset in the packed stream
   uint32_t bytes;     // nslabs * slab_bytes
-  uint32_t layer;     // 0,1,2 = MLP layers, 3 = convolution
-  uint32_t first;     // index of the first slab (K-step) within its layer
+  uint16_t first;     // first K-step (slab) index within the op / conv
+  uint16_t nslabs;
+  uint8_t kind;       // 0 = MLP op, 1 = conv
+  uint8_t op;         // MLP op index
+  uint8_t flags;      // IT_BEGIN / IT_END (first / last item of the op or of the conv)
+  uint8_t pad;
+};
+
+// One MLP "op" = one output-column chunk of one layer: D[scratch] = A * W[n0:n0+N, :]^T.
+struct MlpOp {
+  int layer;          // 0, 1, 2
+  int n0, N;          // output columns [n0, n0+N) of the layer
+  int nks;            // K-steps (input width / 16)
+  int first_of_layer, last_of_layer;
 };
 
 struct FusedParams {
@@ -53,28 +74,39 @@ struct FusedParams {
   int B, C, H, W, n_in;
   int nstrips, ntiles, mode;  // mode 0: MLP + conv -> J ; mode 1: MLP only -> beta
   const uint8_t* stream;
-  const StageDesc* stages;
-  int nst_l[4];               // number of stages of each layer per tile
-  int nstages;                // nst_l[0]+...+nst_l[3]
-  const uint2* conv_steps;    // per conv K-step: (A byte offset in a channel's E region, LBO)
+  const Item* items;          // [items_full | items_beta]
+  int n_items_full, n_items_beta;
+  MlpOp ops[kMaxOps];
+  int n_ops;
+  const uint32_t* conv_steps; // per conv K-step: descriptor low word (E-relative start>>4 | (LBO>>4)<<16)
   int nconv;
-  const float *b1, *b2, *b3, *svec;  // padded biases; svec[k] = sum of taps of phi_k
+  const float* consts;        // b1[kMaxN] b2[kMaxN] b3[128] svec[128] (zero padded)
   int K, Nk, K1, N1, N2;
-  int r;
+  int r, rr;                  // rr = r rounded up to a multiple of 4 (E column origin)
   int n_ey, n_ex, npos_y, npos_x;
   int ey_a0[kMaxEy], ex_a[kMaxEx];
   int chan_bytes;             // E region bytes per channel
+  int n_ebuf;                 // 1 or 2 E buffers
+  int scr_col;                // TMEM column of the MLP scratch (= C_max * Nk)
   int stage_bytes, nring;
-  int off_ring, off_a1, off_a2, off_e, off_tab, off_bar, smem_bytes;
+  int off_ring, off_a1, off_a2, off_e, off_tab, off_const, off_red, off_bar, smem_bytes;
   int a1_sbo, a2_sbo;
+  unsigned long long* prof;   // P2S_PROFILE builds only: [grid][32] cycle counters
 };
+
+#ifdef P2S_PROFILE
+#define PROF_T0() const long long _pt0 = clock64()
+#define PROF_ADD(slot) prof_acc[slot] += (unsigned long long)(clock64() - _pt0)
+#else
+#define PROF_T0() do {} while (0)
+#define PROF_ADD(slot) do {} while (0)
+#endif
 
 __device__ __forceinline__ int clampi(int v, int lo, int hi) { return v < lo ? lo : (v > hi ? hi : v); }
 
-// barrier slots in shared memory
 enum Bar {
-  BAR_A1_FULL = 0, BAR_A1_EMPTY, BAR_E_FULL, BAR_E_EMPTY, BAR_MLP_DONE, BAR_A2_FULL,
-  BAR_ACC_FULL, BAR_TMEM_FREE, BAR_RING = 8  // then ring_full[n], ring_empty[n]
+  BAR_A1_FULL = 0, BAR_A1_EMPTY, BAR_E_FULL0, BAR_E_FULL1, BAR_E_EMPTY0, BAR_E_EMPTY1,
+  BAR_MLP_DONE, BAR_SCR_FREE, BAR_ACC_FULL, BAR_TMEM_FREE, BAR_RING = 10
 };
 
 __device__ __forceinline__ void tile_coords(const FusedParams& p, int t, int& b, int& y, int& x0) {
@@ -86,7 +118,82 @@ __device__ __forceinline__ void tile_coords(const FusedParams& p, int t, int& b,
   x0 = s * kTileM;
 }
 
-__global__ void __launch_bounds__(kThreads, 1) k_fused_p2s(const __grid_constant__ FusedParams p) {
+__device__ __forceinline__ uint4 pack8(const float* v) {
+  return make_uint4(pack_half2(v[0], v[1]), pack_half2(v[2], v[3]), pack_half2(v[4], v[5]),
+                    pack_half2(v[6], v[7]));
+}
+
+__device__ __forceinline__ void named_bar_sync(int id, int nthreads) {
+  asm volatile("bar.sync %0, %1;" ::"r"(id), "r"(nthreads) : "memory");
+}
+
+// ---------------------------------------------------------------- im2col view builders
+// EY block `blk`: entry i = 8 rows (y - r + a0 + j) at column cx0 + i, centred, fp16.
+// EX row `e`:     entry i = 8 columns cx0 + i + j of row (y - r + a), centred, fp16.
+__device__ __forceinline__ void build_E(const FusedParams& p, uint8_t* Ec, const float* img, int y,
+                                        int x0, int tid) {
+  const int cx0 = x0 - p.rr;
+  const bool vec = (p.W & 3) == 0;
+  const int ngy = p.npos_y >> 2;
+  const int n_items_y = p.n_ey * ngy;
+  for (int w = tid; w < n_items_y; w += kBuildThreads) {
+    const int blk = w / ngy, g = w - blk * ngy;
+    const int col0 = cx0 + 4 * g;
+    float v[8][4];
+    const int ybase = y - p.r + p.ey_a0[blk];
+    if (vec && col0 >= 0 && col0 + 3 < p.W) {
+#pragma unroll
+      for (int j = 0; j < 8; ++j) {
+        const float4 q = __ldg(reinterpret_cast<const float4*>(img + (size_t)clampi(ybase + j, 0, p.H - 1) * p.W + col0));
+        v[j][0] = q.x; v[j][1] = q.y; v[j][2] = q.z; v[j][3] = q.w;
+      }
+    } else {
+#pragma unroll
+      for (int j = 0; j < 8; ++j) {
+        const float* row = img + (size_t)clampi(ybase + j, 0, p.H - 1) * p.W;
+#pragma unroll
+        for (int e = 0; e < 4; ++e) v[j][e] = __ldg(row + clampi(col0 + e, 0, p.W - 1));
+      }
+    }
+    uint8_t* dst = Ec + (size_t)blk * p.npos_y * 16 + (size_t)(4 * g) * 16;
+#pragma unroll
+    for (int e = 0; e < 4; ++e) {
+      float t[8];
+#pragma unroll
+      for (int j = 0; j < 8; ++j) t[j] = v[j][e] - 0.5f;
+      *reinterpret_cast<uint4*>(dst + e * 16) = pack8(t);
+    }
+  }
+  const int ngx = p.npos_x >> 2;
+  const int n_items_x = p.n_ex * ngx;
+  uint8_t* xb = Ec + (size_t)p.n_ey * p.npos_y * 16;
+  for (int w = tid; w < n_items_x; w += kBuildThreads) {
+    const int e = w / ngx, g = w - e * ngx;
+    const int col0 = cx0 + 4 * g;
+    const float* row = img + (size_t)clampi(y - p.r + p.ex_a[e], 0, p.H - 1) * p.W;
+    float v[12];
+    if (vec && col0 >= 0 && col0 + 11 < p.W) {
+#pragma unroll
+      for (int q = 0; q < 3; ++q) {
+        const float4 f = __ldg(reinterpret_cast<const float4*>(row + col0 + 4 * q));
+        v[4 * q] = f.x; v[4 * q + 1] = f.y; v[4 * q + 2] = f.z; v[4 * q + 3] = f.w;
+      }
+    } else {
+#pragma unroll
+      for (int q = 0; q < 12; ++q) v[q] = __ldg(row + clampi(col0 + q, 0, p.W - 1));
+    }
+    uint8_t* dst = xb + (size_t)e * p.npos_x * 16 + (size_t)(4 * g) * 16;
+#pragma unroll
+    for (int s = 0; s < 4; ++s) {
+      float t[8];
+#pragma unroll
+      for (int j = 0; j < 8; ++j) t[j] = v[s + j] - 0.5f;
+      *reinterpret_cast<uint4*>(dst + s * 16) = pack8(t);
+    }
+  }
+}
+
+__global__ void __launch_bounds__(kThreads) k_fused_p2s(const __grid_constant__ FusedParams p) {
   extern __shared__ __align__(1024) uint8_t smem[];
   uint64_t* bars = reinterpret_cast<uint64_t*>(smem + p.off_bar);
   uint64_t* ring_full = bars + BAR_RING;
@@ -96,28 +203,43 @@ __global__ void __launch_bounds__(kThreads, 1) k_fused_p2s(const __grid_constant
   uint8_t* sA1 = smem + p.off_a1;
   uint8_t* sA2 = smem + p.off_a2;
   uint8_t* sE = smem + p.off_e;
-  StageDesc* sStages = reinterpret_cast<StageDesc*>(smem + p.off_tab);
-  uint2* sSteps = reinterpret_cast<uint2*>(smem + p.off_tab + kMaxStages * sizeof(StageDesc));
+  Item* sItems = reinterpret_cast<Item*>(smem + p.off_tab);
+  uint32_t* sSteps = reinterpret_cast<uint32_t*>(smem + p.off_tab + kMaxItems * sizeof(Item));
+  float* sConst = reinterpret_cast<float*>(smem + p.off_const);
+  float* sB1 = sConst;
+  float* sB2 = sConst + kMaxN;
+  float* sB3 = sConst + 2 * kMaxN;
+  float* sSv = sConst + 2 * kMaxN + 128;
+  float4* sRed = reinterpret_cast<float4*>(smem + p.off_red);  // [2][128] partial J (WG1 -> WG0)
 
   const int warp = warp_id();
   const int lane = lane_id();
-
-  // per-CTA contiguous range of tiles
   const int t_begin = (int)(((long long)blockIdx.x * p.ntiles) / gridDim.x);
   const int t_end = (int)(((long long)(blockIdx.x + 1) * p.ntiles) / gridDim.x);
+  const int n_items = p.mode == 0 ? p.n_items_full : p.n_items_beta;
+#ifdef P2S_PROFILE
+  unsigned long long prof_acc[20];
+#pragma unroll
+  for (int i = 0; i < 20; ++i) prof_acc[i] = 0;
+  const long long prof_start = clock64();
+#endif
+  const Item* gItems = p.items + (p.mode == 0 ? 0 : p.n_items_full);
 
   // ---- setup
-  for (int i = threadIdx.x; i < p.nstages; i += kThreads) sStages[i] = p.stages[i];
+  for (int i = threadIdx.x; i < n_items; i += kThreads) sItems[i] = gItems[i];
   for (int i = threadIdx.x; i < p.nconv; i += kThreads) sSteps[i] = p.conv_steps[i];
+  for (int i = threadIdx.x; i < 2 * kMaxN + 256; i += kThreads) sConst[i] = p.consts[i];
   if (threadIdx.x == 0) {
-    mbar_init(&bars[BAR_A1_FULL], kBuildThreads / 32);
+    mbar_init(&bars[BAR_A1_FULL], kNumBuildWarps);
     mbar_init(&bars[BAR_A1_EMPTY], 1);
-    mbar_init(&bars[BAR_E_FULL], kBuildThreads / 32);
-    mbar_init(&bars[BAR_E_EMPTY], 1);
+    mbar_init(&bars[BAR_E_FULL0], kNumBuildWarps);
+    mbar_init(&bars[BAR_E_FULL1], kNumBuildWarps);
+    mbar_init(&bars[BAR_E_EMPTY0], 1);
+    mbar_init(&bars[BAR_E_EMPTY1], 1);
     mbar_init(&bars[BAR_MLP_DONE], 1);
-    mbar_init(&bars[BAR_A2_FULL], kEpiThreads / 32);
+    mbar_init(&bars[BAR_SCR_FREE], kNumEpiWarps);
     mbar_init(&bars[BAR_ACC_FULL], 1);
-    mbar_init(&bars[BAR_TMEM_FREE], kEpiThreads / 32);
+    mbar_init(&bars[BAR_TMEM_FREE], kNumEpiWarps);
     for (int i = 0; i < p.nring; ++i) { mbar_init(&ring_full[i], 1); mbar_init(&ring_empty[i], 1); }
     fence_mbar_init();
   }
@@ -126,7 +248,6 @@ __global__ void __launch_bounds__(kThreads, 1) k_fused_p2s(const __grid_constant
   __syncthreads();
   tc_fence_after();
   const uint32_t tmem = *tmem_slot;
-  const int nst_tile = p.mode == 0 ? p.nstages : p.nst_l[0] + p.nst_l[1] + p.nst_l[2];
 
   if (warp == kWarpProducer) {
     // ================= producer: stream weight/basis slabs into the ring =================
@@ -134,218 +255,295 @@ __global__ void __launch_bounds__(kThreads, 1) k_fused_p2s(const __grid_constant
       int s = 0;
       uint32_t ph = 0;
       for (int t = t_begin; t < t_end; ++t) {
-        for (int g = 0; g < nst_tile; ++g) {
-          const StageDesc sd = sStages[g];
-          mbar_wait(&ring_empty[s], ph ^ 1);
-          mbar_arrive_expect_tx(&ring_full[s], sd.bytes);
-          bulk_g2s(ring + (size_t)s * p.stage_bytes, p.stream + sd.src_off, sd.bytes, &ring_full[s]);
+        for (int g = 0; g < n_items; ++g) {
+          const Item it = sItems[g];
+          {
+            PROF_T0();
+            mbar_wait(&ring_empty[s], ph ^ 1);
+            PROF_ADD(7);
+          }
+          mbar_arrive_expect_tx(&ring_full[s], it.bytes);
+          bulk_g2s(ring + (size_t)s * p.stage_bytes, p.stream + it.src_off, it.bytes, &ring_full[s]);
           if (++s == p.nring) { s = 0; ph ^= 1; }
         }
       }
     }
   } else if (warp == kWarpMma) {
-    // ================= UMMA issuer (single thread) =================
-    if (lane == 0) {
-      const uint32_t ring_s = smem_u32(ring), a1_s = smem_u32(sA1), a2_s = smem_u32(sA2),
-                     e_s = smem_u32(sE);
-      const uint32_t id_l[4] = {idesc_f16(128, p.N1), idesc_f16(128, p.N2), idesc_f16(128, p.Nk),
-                                idesc_f16(128, p.Nk)};
-      const uint32_t slab_l[4] = {(uint32_t)p.N1 * 32u, (uint32_t)p.N2 * 32u, (uint32_t)p.Nk * 32u,
-                                  (uint32_t)p.Nk * 32u};
+    // ================= UMMA issuer (whole warp, uniform values; one elected lane issues) ====
+    // Descriptors are assembled from precomputed 32-bit halves so the per-UMMA work is one
+    // or two uniform adds: lo = start>>4 | (LBO>>4)<<16, hi = SBO>>4 | version(bit 46).
+    {
+      const uint32_t ring_lo = (smem_u32(ring) >> 4) | ((128u >> 4) << 16);
+      const uint32_t a1_lo = (smem_u32(sA1) >> 4) | ((128u >> 4) << 16);
+      const uint32_t a2_lo = (smem_u32(sA2) >> 4) | ((128u >> 4) << 16);
+      const uint32_t e_lo = smem_u32(sE) >> 4;
+      const uint32_t hi_b = (256u >> 4) | (1u << 14);
+      const uint32_t hi_conv = (128u >> 4) | (1u << 14);
+      const uint32_t hi_a1 = ((uint32_t)p.a1_sbo >> 4) | (1u << 14);
+      const uint32_t hi_a2 = ((uint32_t)p.a2_sbo >> 4) | (1u << 14);
+      const uint32_t id_conv = idesc_f16(128, p.Nk);
+      const uint32_t conv_slab16 = (uint32_t)p.Nk * 2u;  // slab bytes >> 4
+      const uint32_t stage16 = (uint32_t)p.stage_bytes >> 4;
+      const uint32_t ch16 = (uint32_t)p.chan_bytes >> 4;
+      const uint32_t ebuf16 = 3u * ch16;
+      const int C = p.C, nring = p.nring, ebufs = p.n_ebuf, mode = p.mode;
+      const uint32_t scr = tmem + (uint32_t)p.scr_col;
+      const uint32_t acc1 = tmem + (uint32_t)p.Nk, acc2 = tmem + 2u * (uint32_t)p.Nk;
       int s = 0;
       uint32_t ph = 0;
+      uint32_t scr_waits = 0;
+      uint32_t e_use0 = 0, e_use1 = 0;
       int it = 0;
       for (int t = t_begin; t < t_end; ++t, ++it) {
-        int g = 0;
-        for (int layer = 0; layer < (p.mode == 0 ? 4 : 3); ++layer) {
-          // layer entry dependencies
-          if (layer == 0) {
-            mbar_wait(&bars[BAR_A1_FULL], it & 1);
-            mbar_wait(&bars[BAR_TMEM_FREE], (it & 1) ^ 1);
-          } else if (layer == 1) {
-            mbar_wait(&bars[BAR_A2_FULL], 0);
-          } else if (layer == 2) {
-            mbar_wait(&bars[BAR_A2_FULL], 1);
-          } else {
-            mbar_wait(&bars[BAR_E_FULL], it & 1);
-          }
-          tc_fence_after();
-          const uint32_t dcol = layer == 2 ? kBetaCol : 0u;
-          for (int gl = 0; gl < p.nst_l[layer]; ++gl, ++g) {
-            const StageDesc sd = sStages[g];
-            mbar_wait(&ring_full[s], ph);
-            tc_fence_after();
-            const uint32_t nsl = sd.bytes / slab_l[layer];
-            const uint32_t bbase = ring_s + (uint32_t)s * p.stage_bytes;
-            for (uint32_t j = 0; j < nsl; ++j) {
-              const uint32_t ks = sd.first + j;
-              const uint64_t bd = sdesc(bbase + j * slab_l[layer], 128, 256);
-              if (layer < 3) {
-                const uint64_t ad = layer == 0 ? sdesc(a1_s + ks * 256, 128, p.a1_sbo)
-                                               : sdesc(a2_s + ks * 256, 128, p.a2_sbo);
-                umma_f16(tmem + dcol, ad, bd, id_l[layer], ks > 0);
+        const int eb = ebufs == 2 ? (it & 1) : 0;
+        for (int g = 0; g < n_items; ++g) {
+          const Item itm = sItems[g];
+          const uint32_t b_lo0 = ring_lo + (uint32_t)s * stage16;
+          if (itm.kind == 0) {
+            const MlpOp op = p.ops[itm.op];
+            if (itm.flags & IT_BEGIN) {
+              if (op.layer == 0 && op.first_of_layer) {
+                { PROF_T0(); mbar_wait(&bars[BAR_A1_FULL], it & 1); PROF_ADD(0); }
+                { PROF_T0(); mbar_wait(&bars[BAR_TMEM_FREE], (it & 1) ^ 1); PROF_ADD(1); }
               } else {
-                const uint2 st = sSteps[ks];
-                for (int c = 0; c < p.C; ++c) {
-                  const uint64_t ad = sdesc(e_s + c * p.chan_bytes + st.x, st.y, 128);
-                  umma_f16(tmem + c * p.Nk, ad, bd, id_l[3], ks > 0);
-                }
+                { PROF_T0(); mbar_wait(&bars[BAR_SCR_FREE], scr_waits & 1); PROF_ADD(2); }
+                ++scr_waits;
               }
+              tc_fence_after();
             }
-            umma_commit(&ring_empty[s]);
-            if (++s == p.nring) { s = 0; ph ^= 1; }
-          }
-          if (layer == 0) umma_commit(&bars[BAR_A1_EMPTY]);
-          if (layer == 0 || layer == 1) umma_commit(&bars[BAR_MLP_DONE]);
-          if (layer == 2 && p.mode == 1) umma_commit(&bars[BAR_ACC_FULL]);
-          if (layer == 3) {
-            umma_commit(&bars[BAR_E_EMPTY]);
-            umma_commit(&bars[BAR_ACC_FULL]);
+            { PROF_T0(); mbar_wait(&ring_full[s], ph); PROF_ADD(4); }
+            tc_fence_after();
+            const uint32_t idesc = idesc_f16(128, op.N);
+            const uint32_t slab16 = (uint32_t)op.N * 2u;
+            const uint32_t a_lo0 = (op.layer == 0 ? a1_lo : a2_lo) + (uint32_t)itm.first * 16u;
+            const uint32_t a_hi = op.layer == 0 ? hi_a1 : hi_a2;
+            const uint32_t n = itm.nslabs;
+#pragma unroll 2
+            for (uint32_t j = 0; j < n; ++j) {
+              const uint64_t ad = ((uint64_t)a_hi << 32) | (a_lo0 + j * 16u);
+              const uint64_t bd = ((uint64_t)hi_b << 32) | (b_lo0 + j * slab16);
+              umma_f16_elect(scr, ad, bd, idesc, (itm.first + j) > 0);
+            }
+            umma_commit_elect(&ring_empty[s]);
+            if (++s == nring) { s = 0; ph ^= 1; }
+            if (itm.flags & IT_END) {
+              if (op.layer == 0 && op.last_of_layer) umma_commit_elect(&bars[BAR_A1_EMPTY]);
+              if (op.layer < 2) umma_commit_elect(&bars[BAR_MLP_DONE]);
+              else if (mode == 1) umma_commit_elect(&bars[BAR_ACC_FULL]);
+            }
+          } else {
+            if (itm.flags & IT_BEGIN) {
+              { PROF_T0(); mbar_wait(&bars[BAR_E_FULL0 + eb], (eb ? e_use1 : e_use0) & 1); PROF_ADD(3); }
+              tc_fence_after();
+            }
+            { PROF_T0(); mbar_wait(&ring_full[s], ph); PROF_ADD(5); }
+            tc_fence_after();
+            const uint32_t e0 = e_lo + (uint32_t)eb * ebuf16;
+            const uint32_t* steps = sSteps + itm.first;
+            const uint32_t n = itm.nslabs;
+            const uint32_t acc_first = itm.first;
+#pragma unroll 2
+            for (uint32_t j = 0; j < n; ++j) {
+              const uint32_t a_lo = e0 + steps[j];
+              const uint64_t bd = ((uint64_t)hi_b << 32) | (b_lo0 + j * conv_slab16);
+              const uint32_t accum = (acc_first + j) > 0;
+              umma_f16_elect(tmem, ((uint64_t)hi_conv << 32) | a_lo, bd, id_conv, accum);
+              if (C > 1) umma_f16_elect(acc1, ((uint64_t)hi_conv << 32) | (a_lo + ch16), bd, id_conv, accum);
+              if (C > 2) umma_f16_elect(acc2, ((uint64_t)hi_conv << 32) | (a_lo + 2u * ch16), bd, id_conv, accum);
+            }
+            umma_commit_elect(&ring_empty[s]);
+            if (++s == nring) { s = 0; ph ^= 1; }
+            if (itm.flags & IT_END) {
+              umma_commit_elect(&bars[BAR_E_EMPTY0 + eb]);
+              umma_commit_elect(&bars[BAR_ACC_FULL]);
+              if (eb) ++e_use1; else ++e_use0;
+            }
           }
         }
       }
     }
-  } else if (warp >= kWarpBuild0 && warp < kWarpBuild0 + kBuildThreads / 32) {
+  } else if (warp < kWarpEpi0) {
     // ================= builders: A1 (Zernike tile, fp16) and E views (fp16, centred) =====
     const int tid = threadIdx.x - kWarpBuild0 * 32;
     const size_t HW = (size_t)p.H * p.W;
+    uint32_t e_use0 = 0, e_use1 = 0;
     int it = 0;
     for (int t = t_begin; t < t_end; ++t, ++it) {
       int b, y, x0;
       tile_coords(p, t, b, y, x0);
       // --- A1: row m = pixel x0+m, k = Zernike index (zero-padded to K1)
-      mbar_wait(&bars[BAR_A1_EMPTY], (it & 1) ^ 1);
+      {
+        PROF_T0();
+        mbar_wait(&bars[BAR_A1_EMPTY], (it & 1) ^ 1);
+        PROF_ADD(9);
+      }
       {
         const int m = tid;
         const int x = min(x0 + m, p.W - 1);
         const float* zp = p.zernike + (size_t)b * p.n_in * HW + (size_t)y * p.W + x;
         uint8_t* dst = sA1 + (m & 7) * 16 + (m >> 3) * p.a1_sbo;
-        for (int k0 = 0; k0 < p.K1; k0 += 8) {
-          float v[8];
+        for (int k0 = 0; k0 < p.K1; k0 += 16) {
+          float v[16];
 #pragma unroll
-          for (int i = 0; i < 8; ++i) v[i] = (k0 + i < p.n_in) ? __ldg(zp + (size_t)(k0 + i) * HW) : 0.f;
-          uint4 q = make_uint4(pack_half2(v[0], v[1]), pack_half2(v[2], v[3]), pack_half2(v[4], v[5]),
-                               pack_half2(v[6], v[7]));
-          *reinterpret_cast<uint4*>(dst + (k0 >> 3) * 128) = q;
+          for (int i = 0; i < 16; ++i) v[i] = (k0 + i < p.n_in) ? __ldg(zp + (size_t)(k0 + i) * HW) : 0.f;
+          *reinterpret_cast<uint4*>(dst + (k0 >> 3) * 128) = pack8(v);
+          *reinterpret_cast<uint4*>(dst + ((k0 >> 3) + 1) * 128) = pack8(v + 8);
         }
       }
       fence_proxy_async_smem();
       __syncwarp();
       if (lane == 0) mbar_arrive(&bars[BAR_A1_FULL]);
       if (p.mode != 0) continue;
-      // --- E views for every channel
-      mbar_wait(&bars[BAR_E_EMPTY], (it & 1) ^ 1);
-      for (int c = 0; c < p.C; ++c) {
-        const float* img = p.image + ((size_t)b * p.C + c) * HW;
-        uint8_t* Ec = sE + (size_t)c * p.chan_bytes;
-        for (int blk = 0; blk < p.n_ey; ++blk) {
-          const float* rows[8];
-#pragma unroll
-          for (int j = 0; j < 8; ++j)
-            rows[j] = img + (size_t)clampi(y - p.r + p.ey_a0[blk] + j, 0, p.H - 1) * p.W;
-          uint8_t* dst = Ec + (size_t)blk * p.npos_y * 16;
-          for (int i = tid; i < p.npos_y; i += kBuildThreads) {
-            const int col = clampi(x0 - p.r + i, 0, p.W - 1);
-            float v[8];
-#pragma unroll
-            for (int j = 0; j < 8; ++j) v[j] = __ldg(rows[j] + col) - 0.5f;
-            *reinterpret_cast<uint4*>(dst + i * 16) =
-                make_uint4(pack_half2(v[0], v[1]), pack_half2(v[2], v[3]), pack_half2(v[4], v[5]),
-                           pack_half2(v[6], v[7]));
-          }
-        }
-        for (int e = 0; e < p.n_ex; ++e) {
-          const float* row = img + (size_t)clampi(y - p.r + p.ex_a[e], 0, p.H - 1) * p.W;
-          uint8_t* dst = Ec + (size_t)p.n_ey * p.npos_y * 16 + (size_t)e * p.npos_x * 16;
-          for (int i = tid; i < p.npos_x; i += kBuildThreads) {
-            float v[8];
-#pragma unroll
-            for (int j = 0; j < 8; ++j) v[j] = __ldg(row + clampi(x0 - p.r + i + j, 0, p.W - 1)) - 0.5f;
-            *reinterpret_cast<uint4*>(dst + i * 16) =
-                make_uint4(pack_half2(v[0], v[1]), pack_half2(v[2], v[3]), pack_half2(v[4], v[5]),
-                           pack_half2(v[6], v[7]));
-          }
-        }
+      // --- E views of every channel
+      const int eb = p.n_ebuf == 2 ? (it & 1) : 0;
+      {
+        PROF_T0();
+        mbar_wait(&bars[BAR_E_EMPTY0 + eb], ((eb ? e_use1 : e_use0) & 1) ^ 1);
+        PROF_ADD(11);
+      }
+      if (eb) ++e_use1; else ++e_use0;
+      uint8_t* Eb = sE + (size_t)eb * 3 * p.chan_bytes;  // buffers are sized for C = 3
+      {
+        PROF_T0();
+        for (int c = 0; c < p.C; ++c)
+          build_E(p, Eb + (size_t)c * p.chan_bytes, p.image + ((size_t)b * p.C + c) * HW, y, x0, tid);
+        PROF_ADD(12);
       }
       fence_proxy_async_smem();
       __syncwarp();
-      if (lane == 0) mbar_arrive(&bars[BAR_E_FULL]);
+      if (lane == 0) mbar_arrive(&bars[BAR_E_FULL0 + eb]);
     }
-  } else if (warp >= kWarpEpi0) {
-    // ================= epilogue: MLP activations, beta, J =================
+  } else {
+    // ================= epilogue: two warpgroups split every TMEM drain by 16-col groups =====
+    const int ew = warp - kWarpEpi0;        // 0..7
+    const int wg = ew >> 2;                 // warpgroup 0 / 1
     const int q = warp & 3;                 // TMEM lane quadrant this warp may access
     const int m = q * 32 + lane;            // pixel (row of every accumulator)
     const uint32_t tl = tmem + ((uint32_t)(q * 32) << 16);
     const size_t HW = (size_t)p.H * p.W;
+    uint32_t mlp_waits = 0;
+    uint8_t* a2row = sA2 + (m & 7) * 16 + (m >> 3) * p.a2_sbo;
     int it = 0;
     for (int t = t_begin; t < t_end; ++t, ++it) {
       int b, y, x0;
       tile_coords(p, t, b, y, x0);
-      // hidden layers: D (cols [0,N)) -> +bias, ReLU -> fp16 -> A2 (K-major, k = column)
-      for (int layer = 0; layer < 2; ++layer) {
-        const int N = layer == 0 ? p.N1 : p.N2;
-        const float* bias = layer == 0 ? p.b1 : p.b2;
-        mbar_wait(&bars[BAR_MLP_DONE], layer);
+      uint4 held[8];                        // L2 chunk 0 (<= 128 cols): this WG's <= 4 groups
+      int held_n0 = -1, held_G = 0;
+      for (int o = 0; o < p.n_ops; ++o) {
+        const MlpOp op = p.ops[o];
+        if (op.layer == 2) continue;        // beta stays in TMEM for the conv epilogue
+        {
+          PROF_T0();
+          mbar_wait(&bars[BAR_MLP_DONE], mlp_waits & 1);
+          PROF_ADD(13);
+        }
+        ++mlp_waits;
         tc_fence_after();
-        uint8_t* dst = sA2 + (m & 7) * 16 + (m >> 3) * p.a2_sbo;
-        for (int c0 = 0; c0 < N; c0 += 16) {
+        const float* bias = (op.layer == 0 ? sB1 : sB2) + op.n0;
+        const int G = op.N >> 4;
+        const bool hold = op.layer == 1 && !op.last_of_layer;
+#pragma unroll
+        for (int hg = 0; hg < 8; ++hg) {       // this WG's 16-column groups gi = wg + 2*hg
+          const int gi = wg + 2 * hg;
+          if (gi >= G) break;
           float v[16];
-          tmem_ld16(tl + c0, v);
+          tmem_ld16(tl + p.scr_col + gi * 16, v);
           tmem_ld_wait();
 #pragma unroll
-          for (int i = 0; i < 16; ++i) v[i] = fmaxf(v[i] + __ldg(bias + c0 + i), 0.f);
-          *reinterpret_cast<uint4*>(dst + (c0 >> 3) * 128) =
-              make_uint4(pack_half2(v[0], v[1]), pack_half2(v[2], v[3]), pack_half2(v[4], v[5]),
-                         pack_half2(v[6], v[7]));
-          *reinterpret_cast<uint4*>(dst + ((c0 >> 3) + 1) * 128) =
-              make_uint4(pack_half2(v[8], v[9]), pack_half2(v[10], v[11]), pack_half2(v[12], v[13]),
-                         pack_half2(v[14], v[15]));
+          for (int i = 0; i < 16; ++i) v[i] = fmaxf(v[i] + bias[gi * 16 + i], 0.f);
+          const uint4 lo = pack8(v), hi = pack8(v + 8);
+          if (hold && hg < 4) {
+            held[2 * hg] = lo;
+            held[2 * hg + 1] = hi;
+          } else {
+            const int kc = (op.n0 >> 3) + gi * 2;
+            *reinterpret_cast<uint4*>(a2row + kc * 128) = lo;
+            *reinterpret_cast<uint4*>(a2row + (kc + 1) * 128) = hi;
+          }
+        }
+        if (hold) { held_n0 = op.n0; held_G = G; }
+        if (op.layer == 1 && op.last_of_layer && held_n0 >= 0) {
+#pragma unroll
+          for (int hg = 0; hg < 4; ++hg) {
+            const int gi = wg + 2 * hg;
+            if (gi >= held_G) break;
+            const int kc = (held_n0 >> 3) + gi * 2;
+            *reinterpret_cast<uint4*>(a2row + kc * 128) = held[2 * hg];
+            *reinterpret_cast<uint4*>(a2row + (kc + 1) * 128) = held[2 * hg + 1];
+          }
+          held_n0 = -1;
         }
         fence_proxy_async_smem();
         tc_fence_before();
         __syncwarp();
-        if (lane == 0) mbar_arrive(&bars[BAR_A2_FULL]);
+        if (lane == 0) mbar_arrive(&bars[BAR_SCR_FREE]);
       }
-      mbar_wait(&bars[BAR_ACC_FULL], it & 1);
+      {
+        PROF_T0();
+        mbar_wait(&bars[BAR_ACC_FULL], it & 1);
+        PROF_ADD(15);
+      }
       tc_fence_after();
       const int x = x0 + m;
+      const int GK = p.Nk >> 4;
       if (p.mode == 1) {
-        for (int k0 = 0; k0 < p.Nk; k0 += 16) {
+        for (int gi = wg; gi < GK; gi += 2) {
           float bv[16];
-          tmem_ld16(tl + kBetaCol + k0, bv);
+          tmem_ld16(tl + p.scr_col + gi * 16, bv);
           tmem_ld_wait();
           if (x < p.W)
-            for (int i = 0; i < 16 && k0 + i < p.K; ++i)
-              p.beta_out[((size_t)b * p.K + k0 + i) * HW + (size_t)y * p.W + x] = bv[i] + __ldg(p.b3 + k0 + i);
+            for (int i = 0; i < 16 && gi * 16 + i < p.K; ++i)
+              p.beta_out[((size_t)b * p.K + gi * 16 + i) * HW + (size_t)y * p.W + x] = bv[i] + sB3[gi * 16 + i];
         }
       } else {
         float jc[3] = {0.f, 0.f, 0.f};
         float bs = 0.f;
-        for (int k0 = 0; k0 < p.Nk; k0 += 16) {
+        for (int gi = wg; gi < GK; gi += 2) {
           float bv[16], av[3][16];
-          tmem_ld16(tl + kBetaCol + k0, bv);
+          tmem_ld16(tl + p.scr_col + gi * 16, bv);
 #pragma unroll
           for (int c = 0; c < 3; ++c)
-            if (c < p.C) tmem_ld16(tl + c * p.Nk + k0, av[c]);
+            if (c < p.C) tmem_ld16(tl + c * p.Nk + gi * 16, av[c]);
           tmem_ld_wait();
 #pragma unroll
           for (int i = 0; i < 16; ++i) {
-            const float be = bv[i] + __ldg(p.b3 + k0 + i);
-            bs = fmaf(be, __ldg(p.svec + k0 + i), bs);
+            const float be = bv[i] + sB3[gi * 16 + i];
+            bs = fmaf(be, sSv[gi * 16 + i], bs);
 #pragma unroll
             for (int c = 0; c < 3; ++c)
               if (c < p.C) jc[c] = fmaf(be, av[c][i], jc[c]);
           }
         }
-        if (x < p.W)
-          for (int c = 0; c < p.C; ++c)
-            p.J[((size_t)b * p.C + c) * HW + (size_t)y * p.W + x] = fmaf(0.5f, bs, jc[c]);
+        float4* red = sRed + (it & 1) * 128;
+        if (wg == 1) red[m] = make_float4(jc[0], jc[1], jc[2], bs);
+        named_bar_sync(1, 32 * kNumEpiWarps);
+        if (wg == 0) {
+          const float4 o = red[m];
+          bs += o.w;
+          jc[0] += o.x; jc[1] += o.y; jc[2] += o.z;
+          if (x < p.W)
+            for (int c = 0; c < p.C; ++c)
+              p.J[((size_t)b * p.C + c) * HW + (size_t)y * p.W + x] = fmaf(0.5f, bs, jc[c]);
+        }
       }
       tc_fence_before();
       __syncwarp();
       if (lane == 0) mbar_arrive(&bars[BAR_TMEM_FREE]);
     }
   }
+#ifdef P2S_PROFILE
+  {
+    prof_acc[19] = (unsigned long long)(clock64() - prof_start);
+    int base = -1;
+    if (warp == kWarpMma && lane == 0) base = 0;
+    else if (warp == kWarpProducer && lane == 0) base = 1;
+    else if (warp == kWarpBuild0 && lane == 0) base = 2;
+    else if (warp == kWarpEpi0 && lane == 0) base = 3;
+    if (p.prof && base >= 0)
+      for (int i = 0; i < 20; ++i)
+        if (prof_acc[i]) p.prof[((size_t)blockIdx.x * 4 + base) * 20 + i] = prof_acc[i];
+  }
+#endif
   // ---- teardown
   tc_fence_before();
   __syncthreads();

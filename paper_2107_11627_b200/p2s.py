@@ -18,13 +18,13 @@ from typing import Optional
 import numpy as np
 
 _PKG = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(_PKG, "libp2s.so")
+LIB_PATH = os.environ.get("P2S_LIB", os.path.join(_PKG, "libp2s.so"))
 
 P2S_OK, P2S_ERR_INVALID_ARG, P2S_ERR_UNSUPPORTED, P2S_ERR_CUDA, P2S_ERR_OOM = range(5)
 
 EXPORTED = ("p2s_init", "p2s_render", "p2s_render_host", "p2s_reserve", "p2s_set_profile_events",
             "p2s_get_info", "p2s_destroy", "p2s_status_string", "p2s_last_cuda_error",
-            "p2s_debug_beta", "p2s_debug_blur")
+            "p2s_debug_beta", "p2s_debug_blur", "p2s_debug_profile_buffer")
 
 
 class P2SError(RuntimeError):
@@ -86,8 +86,9 @@ def load_library(path: str = LIB_PATH) -> ctypes.CDLL:
     lib.p2s_last_cuda_error.restype = ctypes.c_char_p
     lib.p2s_debug_beta.argtypes = [v, v, i, i, i, v, v]
     lib.p2s_debug_blur.argtypes = [v, _Image, v, v, v]
+    lib.p2s_debug_profile_buffer.argtypes = [v, v]
     for name in ("p2s_init", "p2s_render", "p2s_render_host", "p2s_reserve", "p2s_set_profile_events",
-                 "p2s_get_info", "p2s_debug_beta", "p2s_debug_blur"):
+                 "p2s_get_info", "p2s_debug_beta", "p2s_debug_blur", "p2s_debug_profile_buffer"):
         getattr(lib, name).restype = st
     _lib = lib
     return lib
@@ -197,6 +198,11 @@ class Renderer:
         a = ctypes.c_void_p(ev_begin.cuda_event) if ev_begin is not None else ctypes.c_void_p()
         b = ctypes.c_void_p(ev_end.cuda_event) if ev_end is not None else ctypes.c_void_p()
         _check(self._lib.p2s_set_profile_events(self._h, a, b), "p2s_set_profile_events")
+
+    def debug_profile_buffer(self, counters=None):
+        """Profiling builds only (P2S_LIB=libp2s_prof.so): per-CTA role timers into `counters`."""
+        ptr = ctypes.c_void_p(counters.data_ptr()) if counters is not None else ctypes.c_void_p()
+        _check(self._lib.p2s_debug_profile_buffer(self._h, ptr), "p2s_debug_profile_buffer")
 
     def info(self) -> dict:
         inf = Info()

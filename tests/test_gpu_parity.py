@@ -62,6 +62,11 @@ SMALL = {
     "S31": synth.custom("s31", 207, B=1, C=3, H=12, W=100, K=40, S=31, h1=64, h2=64, t_std=1.0),
     "S25": synth.custom("s25", 208, B=1, C=1, H=12, W=129, K=60, S=25, h1=100, h2=150, t_std=1.0),
     "W1_H1": synth.custom("w1h1", 209, B=3, C=3, H=1, W=1, K=8, S=5, h1=16, h2=16, t_std=0.7),
+    # many tiles per CTA (both E buffers, ring wrap-around) with C = 2 and C = 1
+    "many_tiles_C2": synth.custom("mt2", 211, B=2, C=2, H=300, W=130, K=32, S=17, h1=64, h2=96,
+                                  t_std=1.2),
+    "many_tiles_C1_S9": synth.custom("mt1", 212, B=3, C=1, H=200, W=257, K=24, S=9, h1=40, h2=40,
+                                     t_std=2.2),
 }
 # Degenerate 1x1 frames: every tap reads the same pixel, so J = I * sum_k beta_k s_k is tiny
 # (rms 0.04) and its relative L2 error is the fp16 rounding of (I - 0.5) divided by I --

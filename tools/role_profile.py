@@ -1,0 +1,45 @@
+"""Per-role cycle breakdown of k_fused_p2s (needs libp2s_prof.so, built with -DP2S_PROFILE).
+
+Usage: P2S_LIB=paper_2107_11627_b200/libp2s_prof.so python tools/role_profile.py [cfg]
+Counters (clock64 cycles, averaged over CTAs), per role:
+  MMA issuer : 0 wait A1_FULL, 1 wait TMEM_FREE, 2 wait SCR_FREE, 3 wait E_FULL,
+               4 wait ring (MLP), 5 wait ring (conv), 19 total
+  producer   : 7 wait ring_empty, 19 total
+  builder t0 : 9 wait A1_EMPTY, 11 wait E_EMPTY, 12 build E, 19 total
+  epilogue t0: 13 wait MLP_DONE, 15 wait ACC_FULL, 19 total
+"""
+import os
+import sys
+
+sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+import numpy as np  # noqa: E402
+import torch  # noqa: E402
+
+from paper_2107_11627_b200 import p2s, synth  # noqa: E402
+
+cfg = int(sys.argv[1]) if len(sys.argv) > 1 else 3
+spec = synth.CONFIGS[cfg]
+inp = synth.make_inputs(spec, frames=range(1))
+r = p2s.Renderer(inp.basis, inp.mlp)
+img, z, t = (torch.from_numpy(a).cuda() for a in (inp.image, inp.zernike, inp.tilt))
+out = torch.empty_like(img)
+for _ in range(3):
+    r.render(img, z, t, out=out)
+buf = torch.zeros(148 * 4 * 20, dtype=torch.int64, device="cuda")
+r.debug_profile_buffer(buf)
+r.render(img, z, t, out=out)
+torch.cuda.synchronize()
+r.debug_profile_buffer(None)
+c = buf.view(148, 4, 20).cpu().numpy().astype(np.float64)
+names = {0: {0: "wait A1_FULL", 1: "wait TMEM_FREE", 2: "wait SCR_FREE", 3: "wait E_FULL", 4: "wait ring(MLP)",
+             5: "wait ring(conv)", 19: "total"},
+         1: {7: "wait ring_empty", 19: "total"},
+         2: {9: "wait A1_EMPTY", 11: "wait E_EMPTY", 12: "build E", 19: "total"},
+         3: {13: "wait MLP_DONE", 15: "wait ACC_FULL", 19: "total"}}
+roles = ["MMA", "producer", "builder", "epilogue"]
+ntiles = spec.H * ((spec.W + 127) // 128)
+print(f"cfg{cfg}: {ntiles} tiles over 148 CTAs (~{ntiles / 148:.1f} tiles/CTA); cycles per CTA (mean / max)")
+for ri, role in enumerate(roles):
+    for k, n in names[ri].items():
+        v = c[:, ri, k]
+        print(f"  {role:9s} {n:18s} {v.mean():12.0f} {v.max():12.0f}")
