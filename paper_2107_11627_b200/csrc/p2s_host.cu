@@ -5,6 +5,7 @@
 #include <algorithm>
 #include <cmath>
 #include <cstdio>
+#include <cstdlib>
 #include <cstring>
 #include <new>
 #include <string>
@@ -115,7 +116,8 @@ struct p2s_handle {
   MlpOp ops[kMaxOps];
   int n_ops = 0;
   int stage_bytes, nring, smem_bytes, n_ebuf, scr_col;
-  int off_ring, off_a1, off_a2, off_e, off_tab, off_const, off_red, off_bar, a1_sbo, a2_sbo;
+  int off_ring, off_a1, off_a2, off_hold, off_e, off_tab, off_const, off_red, off_bar, a1_sbo, a2_sbo, hold_sbo;
+  int l3_hold_ks = 0;
   int sm_count;
   uint8_t* d_stream = nullptr;
   Item* d_items = nullptr;
@@ -127,6 +129,7 @@ struct p2s_handle {
   size_t stage_px_cap = 0, stage_chw_cap = 0;
   cudaEvent_t ev_begin = nullptr, ev_end = nullptr;
   unsigned long long* prof = nullptr;
+  int progressive = 1;
 };
 
 namespace {
@@ -174,15 +177,20 @@ FusedParams make_params(const p2s_handle* h, int B, int C, int H, int W, int mod
   p.stage_bytes = h->stage_bytes; p.nring = h->nring;
   p.off_ring = h->off_ring; p.off_a1 = h->off_a1; p.off_a2 = h->off_a2; p.off_e = h->off_e;
   p.off_tab = h->off_tab; p.off_const = h->off_const; p.off_red = h->off_red; p.off_bar = h->off_bar;
+  p.off_hold = h->off_hold;
   p.smem_bytes = h->smem_bytes;
-  p.a1_sbo = h->a1_sbo; p.a2_sbo = h->a2_sbo;
+  p.a1_sbo = h->a1_sbo; p.a2_sbo = h->a2_sbo; p.hold_sbo = h->hold_sbo;
+  p.l3_hold_ks = h->l3_hold_ks;
   p.prof = h->prof;
+  p.progressive = h->progressive;
   return p;
 }
 
 p2s_status launch_fused(p2s_handle* h, const FusedParams& p, cudaStream_t st) {
   if (p.ntiles == 0) return P2S_OK;
-  const int grid = std::min(h->sm_count, p.ntiles);
+  // persistent grid of CTA pairs (clusters of 2): at most one CTA per SM
+  const int npairs = (p.ntiles + 1) / 2;
+  const int grid = 2 * std::max(1, std::min(h->sm_count / 2, npairs));
   k_fused_p2s<<<grid, kThreads, h->smem_bytes, st>>>(p);
   P2S_CUDA(cudaPeekAtLastError());
   return P2S_OK;
@@ -239,6 +247,7 @@ p2s_status p2s_init(const p2s_basis* basis, const p2s_mlp* mlp, p2s_handle** out
   h->Nk = up16(K); h->K1 = up16(mlp->n_in); h->N1 = up16(mlp->h1); h->N2 = up16(mlp->h2);
   h->plan = plan_conv(S);
   h->sm_count = prop.multiProcessorCount;
+  if (const char* e = std::getenv("P2S_PROGRESSIVE")) h->progressive = std::atoi(e) != 0;
   const ConvPlan& P = h->plan;
   const int nconv = (int)P.steps.size();
   if (nconv > kMaxConvSteps) { delete h; return P2S_ERR_UNSUPPORTED; }
@@ -263,56 +272,72 @@ p2s_status p2s_init(const p2s_basis* basis, const p2s_mlp* mlp, p2s_handle** out
     }
   }
 
-  // ---- shared-memory layout
+  // L2 chunk 0 is parked in a "hold" buffer that L3 reads directly (L2 chunk 1 still reads A2)
+  int hold_cols = 0;
+  for (int o = 0; o < h->n_ops; ++o)
+    if (h->ops[o].layer == 1 && !h->ops[o].last_of_layer) hold_cols = h->ops[o].N;
+  h->l3_hold_ks = hold_cols / 16;
+
+  // ---- shared-memory layout (per CTA; identical in both CTAs of a pair)
   const int a1_bytes = kTileM * h->K1 * 2;
   const int kh = std::max(h->N1, h->N2);
   const int a2_bytes = kTileM * kh * 2;
+  const int hold_bytes = kTileM * hold_cols * 2;
   const int e1_bytes = 3 * P.chan_bytes;
   const int tab_bytes = kMaxItems * (int)sizeof(Item) + nconv * 4;
   const int const_bytes = (2 * kMaxN + 256) * 4;
   const int red_bytes = 2 * 128 * 16;
-  const int bar_bytes = (BAR_RING + 2 * 4) * 8 + 16;
   auto al = [](int v) { return (v + 127) / 128 * 128; };
-  const int fixed = al(a1_bytes) + al(a2_bytes) + al(tab_bytes) + al(const_bytes) + al(red_bytes) + al(bar_bytes);
-  const int max_slab = std::max(std::max(CH, h->N1 > CH ? CH : h->N1), h->Nk) * 32;
+  const int bar_bytes = (BAR_RING + 3 * 4) * 8 + 16;
+  const int fixed = al(a1_bytes) + al(a2_bytes) + al(hold_bytes) + al(tab_bytes) + al(const_bytes) +
+                    al(red_bytes) + al(bar_bytes);
+  const int max_half_slab = std::max(std::max(h->N1, h->N2), h->Nk) / 2 * 32;
   int ring_avail = 0;
   h->n_ebuf = 2;
   for (; h->n_ebuf >= 1; --h->n_ebuf) {
     ring_avail = kSmemLimit - fixed - al(h->n_ebuf * e1_bytes) - 1024;
-    if (ring_avail >= 3 * 16384) break;
+    if (ring_avail >= 3 * 12288) break;
   }
   if (h->n_ebuf < 1) h->n_ebuf = 1;
   ring_avail = kSmemLimit - fixed - al(h->n_ebuf * e1_bytes) - 1024;
   int nring = 4, sb = 0;
   for (nring = 4; nring >= 2; --nring) {
-    sb = std::min(32768, (ring_avail / nring) / 1024 * 1024);
-    if (sb >= 20480 || nring == 2) break;
+    sb = std::min(32768, (ring_avail / nring) / 512 * 512);
+    if (sb >= 12288 || nring == 2) break;
   }
-  if (sb < max_slab) { delete h; return P2S_ERR_UNSUPPORTED; }
+  if (sb < max_half_slab) { delete h; return P2S_ERR_UNSUPPORTED; }
   h->nring = nring;
   h->stage_bytes = sb;
   int off = 0;
   h->off_ring = off; off += nring * sb;
   h->off_a1 = off; off += al(a1_bytes);
   h->off_a2 = off; off += al(a2_bytes);
+  h->off_hold = off; off += al(hold_bytes);
   h->off_e = off; off += al(h->n_ebuf * e1_bytes);
   h->off_tab = off; off += al(tab_bytes);
   h->off_const = off; off += al(const_bytes);
   h->off_red = off; off += al(red_bytes);
-  h->off_bar = off; off += (BAR_RING + 2 * nring) * 8 + 16;
+  h->off_bar = off; off += (BAR_RING + 3 * nring) * 8 + 16;
   h->smem_bytes = off;
   h->a1_sbo = (h->K1 / 8) * 128;
   h->a2_sbo = (kh / 8) * 128;
+  h->hold_sbo = std::max(16, hold_cols / 8 * 128);
   if (h->smem_bytes > kSmemLimit) { delete h; return P2S_ERR_UNSUPPORTED; }
 
-  // ---- pack the streamed B operands: [op 0 slabs]...[op n-1 slabs][conv slabs]
-  //      op slab (ks) = rows [n0, n0+N) of the layer weight, K columns [16ks, 16ks+16)
+  // ---- pack the streamed B operands: per op, [rank-0 halves of all slabs][rank-1 halves],
+  //      then the conv slabs the same way. Half r of slab ks of an op of width N = rows
+  //      [r*N/2, (r+1)*N/2) of the chunk, K columns [16ks, 16ks+16), LBO 128 / SBO 256.
   std::vector<size_t> op_off(h->n_ops);
   size_t total = 0;
   for (int o = 0; o < h->n_ops; ++o) { op_off[o] = total; total += (size_t)h->ops[o].nks * h->ops[o].N * 32; }
   const size_t conv_off = total;
   total += (size_t)nconv * h->Nk * 32;
   std::vector<__half> stream(total / 2, __float2half(0.f));
+  auto put = [&](size_t base, int nks, int N, int ks, int n, int kk, float v) {
+    const int half = N / 2, r = n / half, nl = n % half;
+    const size_t hs = (size_t)half * 32;  // bytes of one half slab
+    stream[(base + (size_t)r * nks * hs + (size_t)ks * hs) / 2 + slab_idx(nl, kk)] = __float2half_rn(v);
+  };
   const float* Wl[3] = {mlp->W1, mlp->W2, mlp->W3};
   const int outl[3] = {h->h1, h->h2, K}, inl[3] = {h->n_in, h->h1, h->h2};
   for (int o = 0; o < h->n_ops; ++o) {
@@ -322,8 +347,7 @@ p2s_status p2s_init(const p2s_basis* basis, const p2s_mlp* mlp, p2s_handle** out
         for (int kk = 0; kk < 16; ++kk) {
           const int row = op.n0 + n, k = ks * 16 + kk;
           if (row < outl[op.layer] && k < inl[op.layer])
-            stream[op_off[o] / 2 + (size_t)ks * op.N * 16 + slab_idx(n, kk)] =
-                __float2half_rn(Wl[op.layer][(size_t)row * inl[op.layer] + k]);
+            put(op_off[o], op.nks, op.N, ks, n, kk, Wl[op.layer][(size_t)row * inl[op.layer] + k]);
         }
   }
   for (int g = 0; g < nconv; ++g)
@@ -332,44 +356,46 @@ p2s_status p2s_init(const p2s_basis* basis, const p2s_mlp* mlp, p2s_handle** out
         const Tap t = P.steps[g].tap[kk];
         if (t.a < 0) continue;
         // psi[a][b] = phi[S-1-a][S-1-b]  (true convolution, A2)
-        stream[conv_off / 2 + (size_t)g * h->Nk * 16 + slab_idx(n, kk)] =
-            __float2half_rn(basis->taps[((size_t)n * S + (S - 1 - t.a)) * S + (S - 1 - t.b)]);
+        put(conv_off, nconv, h->Nk, g, n, kk, basis->taps[((size_t)n * S + (S - 1 - t.a)) * S + (S - 1 - t.b)]);
       }
 
-  // ---- per-tile item lists (ring stages in issue order)
-  auto op_items = [&](int o, std::vector<Item>& out) {
-    const MlpOp& op = h->ops[o];
-    const int slab = op.N * 32, per = std::max(1, sb / slab);
-    for (int s0 = 0; s0 < op.nks; s0 += per) {
-      const int ns = std::min(per, op.nks - s0);
-      uint8_t fl = (s0 == 0 ? IT_BEGIN : 0) | (s0 + ns >= op.nks ? IT_END : 0);
-      out.push_back(Item{(uint32_t)(op_off[o] + (size_t)s0 * slab), (uint32_t)(ns * slab), (uint16_t)s0,
-                         (uint16_t)ns, 0, (uint8_t)o, fl, 0});
+  // ---- per-tile-pair item lists (ring stages in issue order)
+  auto make_items = [&](size_t base, int nks, int N, uint8_t kind, uint8_t op, std::vector<Item>& out) {
+    const uint32_t hs = (uint32_t)N * 16, per = std::max<uint32_t>(1, (uint32_t)sb / hs);
+    for (int s0 = 0; s0 < nks; s0 += per) {
+      const int ns = std::min<int>(per, nks - s0);
+      Item it{};
+      it.src_off = (uint32_t)(base + (size_t)s0 * hs);
+      it.bytes = (uint32_t)ns * hs;
+      it.half_stride = (uint32_t)nks * hs;
+      it.first = (uint16_t)s0;
+      it.nslabs = (uint16_t)ns;
+      it.kind = kind;
+      it.op = op;
+      it.flags = (s0 == 0 ? IT_BEGIN : 0) | (s0 + ns >= nks ? IT_END : 0);
+      out.push_back(it);
     }
   };
   std::vector<Item> conv_items;
-  {
-    const int slab = h->Nk * 32, per = std::max(1, sb / slab);
-    for (int s0 = 0; s0 < nconv; s0 += per) {
-      const int ns = std::min(per, nconv - s0);
-      uint8_t fl = (s0 == 0 ? IT_BEGIN : 0) | (s0 + ns >= nconv ? IT_END : 0);
-      conv_items.push_back(Item{(uint32_t)(conv_off + (size_t)s0 * slab), (uint32_t)(ns * slab), (uint16_t)s0,
-                                (uint16_t)ns, 1, 0, fl, 0});
-    }
-  }
+  make_items(conv_off, nconv, h->Nk, 1, 0, conv_items);
   std::vector<Item> full, beta;
+  // Issue order: L1c0, then MLP ops spread evenly over the conv stages (>= 1 stage between
+  // consecutive ops so the epilogue's drain overlaps tensor work); L3 always precedes the
+  // last conv stage so the ACC_FULL commit covers beta.
+  const int ncs = (int)conv_items.size();
+  const int gaps = std::max(1, h->n_ops - 1);
+  const int per_gap = std::max(1, (ncs - 1) / gaps);
   size_t ci = 0;
   for (int o = 0; o < h->n_ops; ++o) {
-    op_items(o, full);
-    op_items(o, beta);
-    // one conv stage after every MLP op but the last (L3) covers the epilogue's drain;
-    // L3 is always issued before the last conv stage so ACC_FULL covers it
-    if (o + 1 < h->n_ops && ci + 1 < conv_items.size()) full.push_back(conv_items[ci++]);
+    make_items(op_off[o], h->ops[o].nks, h->ops[o].N, 0, (uint8_t)o, full);
+    make_items(op_off[o], h->ops[o].nks, h->ops[o].N, 0, (uint8_t)o, beta);
+    if (o + 1 < h->n_ops)
+      for (int k = 0; k < per_gap && ci + 1 < conv_items.size(); ++k) full.push_back(conv_items[ci++]);
   }
   while (ci < conv_items.size()) full.push_back(conv_items[ci++]);
   h->n_items_full = (int)full.size();
   h->n_items_beta = (int)beta.size();
-  if (h->n_items_full > kMaxItems || h->n_items_beta > kMaxItems) { delete h; return P2S_ERR_UNSUPPORTED; }
+  if (h->n_items_full + h->n_items_beta > kMaxItems) { delete h; return P2S_ERR_UNSUPPORTED; }
   h->items = full;
   h->items.insert(h->items.end(), beta.begin(), beta.end());
 

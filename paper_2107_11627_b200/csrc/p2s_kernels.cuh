@@ -1,45 +1,48 @@
 // p2s_kernels.cuh — device side of the P2S hot path (sm_100a).
 //
-//  k_fused_p2s  steps a0+a1+a2: per 128-pixel tile (one image row segment), the P2S MLP
-//                and the K invariant convolutions combined per output
-//               pixel (Eq. 5) on tcgen05 tensor cores, fp16 operands,
-//               fp32 accumulation in TMEM; beta and the K x C convolution results never
-//               leave the SM; writes J [B][C][H][W] fp32.
+//  k_fused_p2s  steps a0+a1+a2: per pixel tile (128 pixels of one image row per CTA; a CTA
+//               pair = one 256-row tcgen05 UMMA tile), the P2S MLP and the
+//               K invariant convolutions combined per output pixel (Eq. 5),
+//               fp16 operands, fp32 accumulation in TMEM; beta and the K x C convolution
+//               results never leave the SM; writes J [B][C][H][W] fp32.
 //  k_tilt_warp  step a3: backward bilinear warp with clamp-to-edge.
 //
 // Layouts:
 //  * UMMA operands use the SWIZZLE_NONE K-major canonical layout: element (row, k) at
 //    (row%8)*16 + (row/8)*SBO + (k%8)*2 + (k/8)*LBO.
-//  * B operands (weight chunks, basis) are pre-packed on the host into 16-K "slabs"
-//    (LBO = 128, SBO = 256 -> rows*32 bytes), in exactly the order the MMA issuer consumes
-//    them, and streamed by the bulk-copy (TMA) engine into a ring of multi-slab stages.
+//  * B operands (weight chunks, basis) are pre-packed on the host into 16-K "slabs" split in
+//    two row halves (LBO = 128, SBO = 256 -> 16*N bytes per half), in the order the MMA
+//    issuer consumes them; each CTA of the pair streams its half (bulk-copy / TMA engine)
+//    into a ring of multi-slab stages at the same shared-memory offset.
 //  * The convolution A operand (im2col of one input channel) is never materialised per
 //    K-step: an 8x-expanded view of the image ("EY" blocks: 8 consecutive rows of one
 //    column per 16-byte entry; "EX" rows: 8 consecutive columns of one row) is built once
 //    per tile (double-buffered), and each K-step addresses it with an overlapping
 //    descriptor (SBO = 16 B per pixel row). See plan_conv() in p2s_host.cu.
 //
-// Schedule per tile (one thread issues every UMMA; items come from a host-built list):
-//   L1 chunk 0 | conv stage | L1 chunk 1 | conv stage | L2 chunk 0 | conv stage | ... | L3 |
-//   remaining conv stages. MLP chunks accumulate in a TMEM "scratch" region next to the
-//   C conv accumulators; the epilogue warps drain each chunk (bias, ReLU, fp16) into the
-//   shared-memory A operand of the next layer while the tensor core runs conv stages.
+// Roles (per CTA, 14 warps): w0 producer, w1 UMMA issuer (leader CTA) / stage forwarder
+// (peer CTA), w2-5 builders (A1 = Zernike tile, E views), w6-13 epilogue (2 warpgroups).
+// Schedule per tile pair (host-built item list, identical in both CTAs):
+//   L1c0 | conv stages | L1c1 | conv stages | L2c0 | ... | L3 | remaining conv stages.
+// MLP chunks accumulate in a TMEM "scratch" region next to the C conv accumulators; the
+// epilogue warps drain each chunk (bias, ReLU, fp16) into the shared-memory A operand of
+// the next layer while the tensor cores run conv stages.
 #pragma once
 #include "sm100.cuh"
 
 namespace p2s {
 
-constexpr int kTileM = 128;          // pixels per tile (UMMA M)
-constexpr int kWarpProducer = 0;     // bulk-copy producer (lane 0)
-constexpr int kWarpMma = 1;          // UMMA issuer (lane 0) + TMEM owner
-constexpr int kWarpBuild0 = 2;       // warps 2..5: A1 (Zernike tile) and E (im2col views)
+constexpr int kTileM = 128;          // pixels per CTA tile (UMMA M = 256 per CTA pair)
+constexpr int kWarpProducer = 0;
+constexpr int kWarpMma = 1;          // leader: UMMA issuer; peer: forwards ring-stage arrivals
+constexpr int kWarpBuild0 = 2;
 constexpr int kNumBuildWarps = 4;
-constexpr int kWarpEpi0 = kWarpBuild0 + kNumBuildWarps;  // warps 6..13: two epilogue warpgroups
+constexpr int kWarpEpi0 = kWarpBuild0 + kNumBuildWarps;  // warps 6..13
 constexpr int kNumEpiWarps = 8;
 constexpr int kThreads = 32 * (kWarpEpi0 + kNumEpiWarps);  // 448
 constexpr int kBuildThreads = 32 * kNumBuildWarps;
 constexpr uint32_t kTmemCols = 512;
-constexpr int kMaxItems = 96;        // per-tile item list capacity (both modes together)
+constexpr int kMaxItems = 80;        // per-tile item list capacity (both modes together)
 constexpr int kMaxConvSteps = 512;
 constexpr int kMaxOps = 6;
 constexpr int kMaxEy = 16, kMaxEx = 4;
@@ -48,15 +51,17 @@ constexpr int kMaxN = 256;           // padded bias vectors
 // One ring stage ("item") = nslabs consecutive 16-K slabs of one MLP op or of the conv.
 enum ItemFlags : uint8_t { IT_BEGIN = 1, IT_END = 2 };
 struct Item {
-  uint32_t src_off;   // byte offset in the packed stream
-  uint32_t bytes;     // nslabs * slab_bytes
-  uint16_t first;     // first K-step (slab) index within the op / conv
+  uint32_t src_off;      // byte offset of this CTA-rank-0 half in the packed stream
+  uint32_t bytes;        // per CTA: nslabs * (16 * N)
+  uint32_t half_stride;  // byte offset from the rank-0 half to the rank-1 half
+  uint16_t first;        // first K-step (slab) index within the op / conv
   uint16_t nslabs;
-  uint8_t kind;       // 0 = MLP op, 1 = conv
-  uint8_t op;         // MLP op index
-  uint8_t flags;      // IT_BEGIN / IT_END (first / last item of the op or of the conv)
-  uint8_t pad;
+  uint8_t kind;          // 0 = MLP op, 1 = conv
+  uint8_t op;            // MLP op index
+  uint8_t flags;         // IT_BEGIN / IT_END (first / last item of the op or of the conv)
+  uint8_t pad[5];
 };
+static_assert(sizeof(Item) == 24, "Item layout");
 
 // One MLP "op" = one output-column chunk of one layer: D[scratch] = A * W[n0:n0+N, :]^T.
 struct MlpOp {
@@ -78,6 +83,7 @@ struct FusedParams {
   int n_items_full, n_items_beta;
   MlpOp ops[kMaxOps];
   int n_ops;
+  int l3_hold_ks;             // L3 K-steps whose A operand is in the hold buffer (L2 chunk 0)
   const uint32_t* conv_steps; // per conv K-step: descriptor low word (E-relative start>>4 | (LBO>>4)<<16)
   int nconv;
   const float* consts;        // b1[kMaxN] b2[kMaxN] b3[128] svec[128] (zero padded)
@@ -85,13 +91,14 @@ struct FusedParams {
   int r, rr;                  // rr = r rounded up to a multiple of 4 (E column origin)
   int n_ey, n_ex, npos_y, npos_x;
   int ey_a0[kMaxEy], ex_a[kMaxEx];
-  int chan_bytes;             // E region bytes per channel
+  int chan_bytes;             // E region bytes per channel (buffers are sized for C = 3)
   int n_ebuf;                 // 1 or 2 E buffers
-  int scr_col;                // TMEM column of the MLP scratch (= C_max * Nk)
+  int scr_col;                // TMEM column of the MLP scratch (= 3 * Nk)
   int stage_bytes, nring;
-  int off_ring, off_a1, off_a2, off_e, off_tab, off_const, off_red, off_bar, smem_bytes;
-  int a1_sbo, a2_sbo;
-  unsigned long long* prof;   // P2S_PROFILE builds only: [grid][32] cycle counters
+  int off_ring, off_a1, off_a2, off_hold, off_e, off_tab, off_const, off_red, off_bar, smem_bytes;
+  int a1_sbo, a2_sbo, hold_sbo;
+  unsigned long long* prof;   // P2S_PROFILE builds only: [grid][4][20] cycle counters
+  int progressive;            // 1: release beta / each conv accumulator as soon as it is read
 };
 
 #ifdef P2S_PROFILE
@@ -104,9 +111,20 @@ struct FusedParams {
 
 __device__ __forceinline__ int clampi(int v, int lo, int hi) { return v < lo ? lo : (v > hi ? hi : v); }
 
+// Barriers marked (L) are used in the leader CTA only and receive arrivals from both CTAs;
+// (B) exist in both CTAs and are completed by the leader's multicast UMMA commits; (C) local.
 enum Bar {
-  BAR_A1_FULL = 0, BAR_A1_EMPTY, BAR_E_FULL0, BAR_E_FULL1, BAR_E_EMPTY0, BAR_E_EMPTY1,
-  BAR_MLP_DONE, BAR_SCR_FREE, BAR_ACC_FULL, BAR_TMEM_FREE, BAR_RING = 10
+  BAR_A1_FULL = 0,   // (L) 2 x 4 builder warps
+  BAR_A1_EMPTY,      // (B)
+  BAR_E_FULL0,       // (L) 2 x 4 builder warps
+  BAR_E_FULL1,
+  BAR_E_EMPTY0,      // (B)
+  BAR_E_EMPTY1,
+  BAR_MLP_DONE,      // (B)
+  BAR_SCR_FREE,      // (L) 2 x 8 epilogue warps
+  BAR_ACC_FULL,      // (B)
+  BAR_TMEM_FREE,     // (L) 2 x 8 epilogue warps
+  BAR_RING = 10      // then ring_full[n] (C), ring_peer[n] (L), ring_empty[n] (B)
 };
 
 __device__ __forceinline__ void tile_coords(const FusedParams& p, int t, int& b, int& y, int& x0) {
@@ -130,6 +148,8 @@ __device__ __forceinline__ void named_bar_sync(int id, int nthreads) {
 // ---------------------------------------------------------------- im2col view builders
 // EY block `blk`: entry i = 8 rows (y - r + a0 + j) at column cx0 + i, centred, fp16.
 // EX row `e`:     entry i = 8 columns cx0 + i + j of row (y - r + a), centred, fp16.
+// Thread g stores its 4 entries in the order (e + g/2) & 3 so that each quarter-warp
+// store covers 128 distinct bytes (bank-conflict free).
 __device__ __forceinline__ void build_E(const FusedParams& p, uint8_t* Ec, const float* img, int y,
                                         int x0, int tid) {
   const int cx0 = x0 - p.rr;
@@ -139,29 +159,35 @@ __device__ __forceinline__ void build_E(const FusedParams& p, uint8_t* Ec, const
   for (int w = tid; w < n_items_y; w += kBuildThreads) {
     const int blk = w / ngy, g = w - blk * ngy;
     const int col0 = cx0 + 4 * g;
-    float v[8][4];
+    float v[4][8];
     const int ybase = y - p.r + p.ey_a0[blk];
     if (vec && col0 >= 0 && col0 + 3 < p.W) {
 #pragma unroll
       for (int j = 0; j < 8; ++j) {
         const float4 q = __ldg(reinterpret_cast<const float4*>(img + (size_t)clampi(ybase + j, 0, p.H - 1) * p.W + col0));
-        v[j][0] = q.x; v[j][1] = q.y; v[j][2] = q.z; v[j][3] = q.w;
+        v[0][j] = q.x; v[1][j] = q.y; v[2][j] = q.z; v[3][j] = q.w;
       }
     } else {
 #pragma unroll
       for (int j = 0; j < 8; ++j) {
         const float* row = img + (size_t)clampi(ybase + j, 0, p.H - 1) * p.W;
 #pragma unroll
-        for (int e = 0; e < 4; ++e) v[j][e] = __ldg(row + clampi(col0 + e, 0, p.W - 1));
+        for (int e = 0; e < 4; ++e) v[e][j] = __ldg(row + clampi(col0 + e, 0, p.W - 1));
       }
     }
     uint8_t* dst = Ec + (size_t)blk * p.npos_y * 16 + (size_t)(4 * g) * 16;
+    uint4 pk[4];
 #pragma unroll
     for (int e = 0; e < 4; ++e) {
-      float t[8];
 #pragma unroll
-      for (int j = 0; j < 8; ++j) t[j] = v[j][e] - 0.5f;
-      *reinterpret_cast<uint4*>(dst + e * 16) = pack8(t);
+      for (int j = 0; j < 8; ++j) v[e][j] -= 0.5f;
+      pk[e] = pack8(v[e]);
+    }
+    const int rot = (g >> 1) & 3;
+#pragma unroll
+    for (int e = 0; e < 4; ++e) {
+      const int ee = (e + rot) & 3;
+      *reinterpret_cast<uint4*>(dst + ee * 16) = pk[ee];
     }
   }
   const int ngx = p.npos_x >> 2;
@@ -182,26 +208,26 @@ __device__ __forceinline__ void build_E(const FusedParams& p, uint8_t* Ec, const
 #pragma unroll
       for (int q = 0; q < 12; ++q) v[q] = __ldg(row + clampi(col0 + q, 0, p.W - 1));
     }
+#pragma unroll
+    for (int q = 0; q < 12; ++q) v[q] -= 0.5f;
     uint8_t* dst = xb + (size_t)e * p.npos_x * 16 + (size_t)(4 * g) * 16;
 #pragma unroll
-    for (int s = 0; s < 4; ++s) {
-      float t[8];
-#pragma unroll
-      for (int j = 0; j < 8; ++j) t[j] = v[s + j] - 0.5f;
-      *reinterpret_cast<uint4*>(dst + s * 16) = pack8(t);
-    }
+    for (int s = 0; s < 4; ++s) *reinterpret_cast<uint4*>(dst + s * 16) = pack8(v + s);
   }
 }
 
-__global__ void __launch_bounds__(kThreads) k_fused_p2s(const __grid_constant__ FusedParams p) {
+__global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads)
+    k_fused_p2s(const __grid_constant__ FusedParams p) {
   extern __shared__ __align__(1024) uint8_t smem[];
   uint64_t* bars = reinterpret_cast<uint64_t*>(smem + p.off_bar);
   uint64_t* ring_full = bars + BAR_RING;
-  uint64_t* ring_empty = bars + BAR_RING + p.nring;
-  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bars + BAR_RING + 2 * p.nring);
+  uint64_t* ring_peer = bars + BAR_RING + p.nring;
+  uint64_t* ring_empty = bars + BAR_RING + 2 * p.nring;
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bars + BAR_RING + 3 * p.nring);
   uint8_t* ring = smem + p.off_ring;
   uint8_t* sA1 = smem + p.off_a1;
   uint8_t* sA2 = smem + p.off_a2;
+  uint8_t* sHold = smem + p.off_hold;
   uint8_t* sE = smem + p.off_e;
   Item* sItems = reinterpret_cast<Item*>(smem + p.off_tab);
   uint32_t* sSteps = reinterpret_cast<uint32_t*>(smem + p.off_tab + kMaxItems * sizeof(Item));
@@ -214,8 +240,13 @@ __global__ void __launch_bounds__(kThreads) k_fused_p2s(const __grid_constant__ 
 
   const int warp = warp_id();
   const int lane = lane_id();
-  const int t_begin = (int)(((long long)blockIdx.x * p.ntiles) / gridDim.x);
-  const int t_end = (int)(((long long)(blockIdx.x + 1) * p.ntiles) / gridDim.x);
+  const uint32_t rank = cluster_ctarank();
+  const bool leader = rank == 0;
+  // per-cluster contiguous range of tile pairs; this CTA takes tile 2*pair + rank
+  const int npairs = (p.ntiles + 1) >> 1;
+  const int ncl = gridDim.x >> 1, cl = blockIdx.x >> 1;
+  const int pr_begin = (int)(((long long)cl * npairs) / ncl);
+  const int pr_end = (int)(((long long)(cl + 1) * npairs) / ncl);
   const int n_items = p.mode == 0 ? p.n_items_full : p.n_items_beta;
 #ifdef P2S_PROFILE
   unsigned long long prof_acc[20];
@@ -230,134 +261,150 @@ __global__ void __launch_bounds__(kThreads) k_fused_p2s(const __grid_constant__ 
   for (int i = threadIdx.x; i < p.nconv; i += kThreads) sSteps[i] = p.conv_steps[i];
   for (int i = threadIdx.x; i < 2 * kMaxN + 256; i += kThreads) sConst[i] = p.consts[i];
   if (threadIdx.x == 0) {
-    mbar_init(&bars[BAR_A1_FULL], kNumBuildWarps);
+    mbar_init(&bars[BAR_A1_FULL], 2 * kNumBuildWarps);
     mbar_init(&bars[BAR_A1_EMPTY], 1);
-    mbar_init(&bars[BAR_E_FULL0], kNumBuildWarps);
-    mbar_init(&bars[BAR_E_FULL1], kNumBuildWarps);
+    mbar_init(&bars[BAR_E_FULL0], 2 * kNumBuildWarps);
+    mbar_init(&bars[BAR_E_FULL1], 2 * kNumBuildWarps);
     mbar_init(&bars[BAR_E_EMPTY0], 1);
     mbar_init(&bars[BAR_E_EMPTY1], 1);
     mbar_init(&bars[BAR_MLP_DONE], 1);
-    mbar_init(&bars[BAR_SCR_FREE], kNumEpiWarps);
+    mbar_init(&bars[BAR_SCR_FREE], 2 * kNumEpiWarps);
     mbar_init(&bars[BAR_ACC_FULL], 1);
-    mbar_init(&bars[BAR_TMEM_FREE], kNumEpiWarps);
-    for (int i = 0; i < p.nring; ++i) { mbar_init(&ring_full[i], 1); mbar_init(&ring_empty[i], 1); }
+    mbar_init(&bars[BAR_TMEM_FREE], 2 * kNumEpiWarps);
+    for (int i = 0; i < p.nring; ++i) {
+      mbar_init(&ring_full[i], 1);
+      mbar_init(&ring_peer[i], 1);
+      mbar_init(&ring_empty[i], 1);
+    }
     fence_mbar_init();
   }
-  if (warp == kWarpMma) tmem_alloc<kTmemCols>(tmem_slot);
+  if (warp == kWarpMma) tmem_alloc2<kTmemCols>(tmem_slot);
   tc_fence_before();
   __syncthreads();
+  cluster_sync();  // both CTAs' barriers are initialised before any remote arrive
   tc_fence_after();
   const uint32_t tmem = *tmem_slot;
 
   if (warp == kWarpProducer) {
-    // ================= producer: stream weight/basis slabs into the ring =================
+    // ================= producer: stream this CTA's half of every slab into the ring ========
     if (lane == 0) {
       int s = 0;
       uint32_t ph = 0;
-      for (int t = t_begin; t < t_end; ++t) {
+      for (int pr = pr_begin; pr < pr_end; ++pr) {
         for (int g = 0; g < n_items; ++g) {
           const Item it = sItems[g];
-          {
-            PROF_T0();
-            mbar_wait(&ring_empty[s], ph ^ 1);
-            PROF_ADD(7);
-          }
+          { PROF_T0(); mbar_wait(&ring_empty[s], ph ^ 1); PROF_ADD(7); }
           mbar_arrive_expect_tx(&ring_full[s], it.bytes);
-          bulk_g2s(ring + (size_t)s * p.stage_bytes, p.stream + it.src_off, it.bytes, &ring_full[s]);
+          bulk_g2s(ring + (size_t)s * p.stage_bytes, p.stream + it.src_off + rank * it.half_stride, it.bytes,
+                   &ring_full[s]);
           if (++s == p.nring) { s = 0; ph ^= 1; }
         }
       }
     }
+  } else if (warp == kWarpMma && !leader) {
+    // ================= peer: forward "my half of stage s landed" to the leader =============
+    int s = 0;
+    uint32_t ph = 0;
+    for (int pr = pr_begin; pr < pr_end; ++pr) {
+      for (int g = 0; g < n_items; ++g) {
+        mbar_wait(&ring_full[s], ph);
+        if (lane == 0) mbar_arrive_remote(&ring_peer[s], 0);
+        __syncwarp();
+        if (++s == p.nring) { s = 0; ph ^= 1; }
+      }
+    }
   } else if (warp == kWarpMma) {
-    // ================= UMMA issuer (whole warp, uniform values; one elected lane issues) ====
+    // ================= leader: UMMA issuer (whole warp, uniform values; one lane issues) ====
     // Descriptors are assembled from precomputed 32-bit halves so the per-UMMA work is one
     // or two uniform adds: lo = start>>4 | (LBO>>4)<<16, hi = SBO>>4 | version(bit 46).
-    {
-      const uint32_t ring_lo = (smem_u32(ring) >> 4) | ((128u >> 4) << 16);
-      const uint32_t a1_lo = (smem_u32(sA1) >> 4) | ((128u >> 4) << 16);
-      const uint32_t a2_lo = (smem_u32(sA2) >> 4) | ((128u >> 4) << 16);
-      const uint32_t e_lo = smem_u32(sE) >> 4;
-      const uint32_t hi_b = (256u >> 4) | (1u << 14);
-      const uint32_t hi_conv = (128u >> 4) | (1u << 14);
-      const uint32_t hi_a1 = ((uint32_t)p.a1_sbo >> 4) | (1u << 14);
-      const uint32_t hi_a2 = ((uint32_t)p.a2_sbo >> 4) | (1u << 14);
-      const uint32_t id_conv = idesc_f16(128, p.Nk);
-      const uint32_t conv_slab16 = (uint32_t)p.Nk * 2u;  // slab bytes >> 4
-      const uint32_t stage16 = (uint32_t)p.stage_bytes >> 4;
-      const uint32_t ch16 = (uint32_t)p.chan_bytes >> 4;
-      const uint32_t ebuf16 = 3u * ch16;
-      const int C = p.C, nring = p.nring, ebufs = p.n_ebuf, mode = p.mode;
-      const uint32_t scr = tmem + (uint32_t)p.scr_col;
-      const uint32_t acc1 = tmem + (uint32_t)p.Nk, acc2 = tmem + 2u * (uint32_t)p.Nk;
-      int s = 0;
-      uint32_t ph = 0;
-      uint32_t scr_waits = 0;
-      uint32_t e_use0 = 0, e_use1 = 0;
-      int it = 0;
-      for (int t = t_begin; t < t_end; ++t, ++it) {
-        const int eb = ebufs == 2 ? (it & 1) : 0;
-        for (int g = 0; g < n_items; ++g) {
-          const Item itm = sItems[g];
-          const uint32_t b_lo0 = ring_lo + (uint32_t)s * stage16;
-          if (itm.kind == 0) {
-            const MlpOp op = p.ops[itm.op];
-            if (itm.flags & IT_BEGIN) {
-              if (op.layer == 0 && op.first_of_layer) {
-                { PROF_T0(); mbar_wait(&bars[BAR_A1_FULL], it & 1); PROF_ADD(0); }
-                { PROF_T0(); mbar_wait(&bars[BAR_TMEM_FREE], (it & 1) ^ 1); PROF_ADD(1); }
-              } else {
-                { PROF_T0(); mbar_wait(&bars[BAR_SCR_FREE], scr_waits & 1); PROF_ADD(2); }
-                ++scr_waits;
-              }
-              tc_fence_after();
+    const uint32_t ring_lo = (smem_u32(ring) >> 4) | ((128u >> 4) << 16);
+    const uint32_t a1_lo = (smem_u32(sA1) >> 4) | ((128u >> 4) << 16);
+    const uint32_t a2_lo = (smem_u32(sA2) >> 4) | ((128u >> 4) << 16);
+    const uint32_t hold_lo = (smem_u32(sHold) >> 4) | ((128u >> 4) << 16);
+    const uint32_t e_lo = smem_u32(sE) >> 4;
+    const uint32_t hi_b = (256u >> 4) | (1u << 14);
+    const uint32_t hi_conv = (128u >> 4) | (1u << 14);
+    const uint32_t hi_a1 = ((uint32_t)p.a1_sbo >> 4) | (1u << 14);
+    const uint32_t hi_a2 = ((uint32_t)p.a2_sbo >> 4) | (1u << 14);
+    const uint32_t hi_hold = ((uint32_t)p.hold_sbo >> 4) | (1u << 14);
+    const uint32_t id_conv = idesc_f16(256, p.Nk);
+    const uint32_t conv_half16 = (uint32_t)p.Nk;  // half-slab bytes (16 * Nk) >> 4
+    const uint32_t stage16 = (uint32_t)p.stage_bytes >> 4;
+    const uint32_t ch16 = (uint32_t)p.chan_bytes >> 4;
+    const uint32_t ebuf16 = 3u * ch16;
+    const int C = p.C, nring = p.nring, ebufs = p.n_ebuf, mode = p.mode, l3h = p.l3_hold_ks;
+    const uint32_t scr = tmem + (uint32_t)p.scr_col;
+    const uint32_t acc1 = tmem + (uint32_t)p.Nk, acc2 = tmem + 2u * (uint32_t)p.Nk;
+    int s = 0;
+    uint32_t ph = 0;
+    uint32_t scr_waits = 0;
+    uint32_t e_use0 = 0, e_use1 = 0;
+    int it = 0;
+    for (int pr = pr_begin; pr < pr_end; ++pr, ++it) {
+      const int eb = ebufs == 2 ? (it & 1) : 0;
+      for (int g = 0; g < n_items; ++g) {
+        const Item itm = sItems[g];
+        const uint32_t b_lo0 = ring_lo + (uint32_t)s * stage16;
+        if (itm.kind == 0) {
+          const MlpOp op = p.ops[itm.op];
+          if (itm.flags & IT_BEGIN) {
+            if (op.layer == 0 && op.first_of_layer) {
+              { PROF_T0(); mbar_wait_cluster(&bars[BAR_A1_FULL], it & 1); PROF_ADD(0); }
+              { PROF_T0(); mbar_wait_cluster(&bars[BAR_TMEM_FREE], (it & 1) ^ 1); PROF_ADD(1); }
+            } else {
+              { PROF_T0(); mbar_wait_cluster(&bars[BAR_SCR_FREE], scr_waits & 1); PROF_ADD(2); }
+              ++scr_waits;
             }
-            { PROF_T0(); mbar_wait(&ring_full[s], ph); PROF_ADD(4); }
             tc_fence_after();
-            const uint32_t idesc = idesc_f16(128, op.N);
-            const uint32_t slab16 = (uint32_t)op.N * 2u;
-            const uint32_t a_lo0 = (op.layer == 0 ? a1_lo : a2_lo) + (uint32_t)itm.first * 16u;
-            const uint32_t a_hi = op.layer == 0 ? hi_a1 : hi_a2;
-            const uint32_t n = itm.nslabs;
+          }
+          { PROF_T0(); mbar_wait(&ring_full[s], ph); mbar_wait_cluster(&ring_peer[s], ph); PROF_ADD(4); }
+          tc_fence_after();
+          const uint32_t idesc = idesc_f16(256, op.N);
+          const uint32_t half16 = (uint32_t)op.N;  // (16 * N) >> 4
+          const uint32_t n = itm.nslabs;
 #pragma unroll 2
-            for (uint32_t j = 0; j < n; ++j) {
-              const uint64_t ad = ((uint64_t)a_hi << 32) | (a_lo0 + j * 16u);
-              const uint64_t bd = ((uint64_t)hi_b << 32) | (b_lo0 + j * slab16);
-              umma_f16_elect(scr, ad, bd, idesc, (itm.first + j) > 0);
-            }
-            umma_commit_elect(&ring_empty[s]);
-            if (++s == nring) { s = 0; ph ^= 1; }
-            if (itm.flags & IT_END) {
-              if (op.layer == 0 && op.last_of_layer) umma_commit_elect(&bars[BAR_A1_EMPTY]);
-              if (op.layer < 2) umma_commit_elect(&bars[BAR_MLP_DONE]);
-              else if (mode == 1) umma_commit_elect(&bars[BAR_ACC_FULL]);
-            }
-          } else {
-            if (itm.flags & IT_BEGIN) {
-              { PROF_T0(); mbar_wait(&bars[BAR_E_FULL0 + eb], (eb ? e_use1 : e_use0) & 1); PROF_ADD(3); }
-              tc_fence_after();
-            }
-            { PROF_T0(); mbar_wait(&ring_full[s], ph); PROF_ADD(5); }
+          for (uint32_t j = 0; j < n; ++j) {
+            const uint32_t ks = itm.first + j;
+            uint64_t ad;
+            if (op.layer == 0) ad = ((uint64_t)hi_a1 << 32) | (a1_lo + ks * 16u);
+            else if (op.layer == 2 && (int)ks < l3h) ad = ((uint64_t)hi_hold << 32) | (hold_lo + ks * 16u);
+            else ad = ((uint64_t)hi_a2 << 32) | (a2_lo + ks * 16u);
+            const uint64_t bd = ((uint64_t)hi_b << 32) | (b_lo0 + j * half16);
+            umma2_f16_elect(scr, ad, bd, idesc, ks > 0);
+          }
+          umma2_commit_elect(&ring_empty[s]);
+          if (++s == nring) { s = 0; ph ^= 1; }
+          if (itm.flags & IT_END) {
+            if (op.layer == 0 && op.last_of_layer) umma2_commit_elect(&bars[BAR_A1_EMPTY]);
+            if (op.layer < 2) umma2_commit_elect(&bars[BAR_MLP_DONE]);
+            else if (mode == 1) umma2_commit_elect(&bars[BAR_ACC_FULL]);
+          }
+        } else {
+          if (itm.flags & IT_BEGIN) {
+            { PROF_T0(); mbar_wait_cluster(&bars[BAR_E_FULL0 + eb], (eb ? e_use1 : e_use0) & 1); PROF_ADD(3); }
             tc_fence_after();
-            const uint32_t e0 = e_lo + (uint32_t)eb * ebuf16;
-            const uint32_t* steps = sSteps + itm.first;
-            const uint32_t n = itm.nslabs;
-            const uint32_t acc_first = itm.first;
+          }
+          { PROF_T0(); mbar_wait(&ring_full[s], ph); mbar_wait_cluster(&ring_peer[s], ph); PROF_ADD(5); }
+          tc_fence_after();
+          const uint32_t e0 = e_lo + (uint32_t)eb * ebuf16;
+          const uint32_t* steps = sSteps + itm.first;
+          const uint32_t n = itm.nslabs;
+          const uint32_t acc_first = itm.first;
 #pragma unroll 2
-            for (uint32_t j = 0; j < n; ++j) {
-              const uint32_t a_lo = e0 + steps[j];
-              const uint64_t bd = ((uint64_t)hi_b << 32) | (b_lo0 + j * conv_slab16);
-              const uint32_t accum = (acc_first + j) > 0;
-              umma_f16_elect(tmem, ((uint64_t)hi_conv << 32) | a_lo, bd, id_conv, accum);
-              if (C > 1) umma_f16_elect(acc1, ((uint64_t)hi_conv << 32) | (a_lo + ch16), bd, id_conv, accum);
-              if (C > 2) umma_f16_elect(acc2, ((uint64_t)hi_conv << 32) | (a_lo + 2u * ch16), bd, id_conv, accum);
-            }
-            umma_commit_elect(&ring_empty[s]);
-            if (++s == nring) { s = 0; ph ^= 1; }
-            if (itm.flags & IT_END) {
-              umma_commit_elect(&bars[BAR_E_EMPTY0 + eb]);
-              umma_commit_elect(&bars[BAR_ACC_FULL]);
-              if (eb) ++e_use1; else ++e_use0;
-            }
+          for (uint32_t j = 0; j < n; ++j) {
+            const uint32_t a_lo = e0 + steps[j];
+            const uint64_t bd = ((uint64_t)hi_b << 32) | (b_lo0 + j * conv_half16);
+            const uint32_t accum = (acc_first + j) > 0;
+            umma2_f16_elect(tmem, ((uint64_t)hi_conv << 32) | a_lo, bd, id_conv, accum);
+            if (C > 1) umma2_f16_elect(acc1, ((uint64_t)hi_conv << 32) | (a_lo + ch16), bd, id_conv, accum);
+            if (C > 2) umma2_f16_elect(acc2, ((uint64_t)hi_conv << 32) | (a_lo + 2u * ch16), bd, id_conv, accum);
+          }
+          umma2_commit_elect(&ring_empty[s]);
+          if (++s == nring) { s = 0; ph ^= 1; }
+          if (itm.flags & IT_END) {
+            umma2_commit_elect(&bars[BAR_E_EMPTY0 + eb]);
+            umma2_commit_elect(&bars[BAR_ACC_FULL]);
+            if (eb) ++e_use1; else ++e_use0;
           }
         }
       }
@@ -368,15 +415,12 @@ __global__ void __launch_bounds__(kThreads) k_fused_p2s(const __grid_constant__ 
     const size_t HW = (size_t)p.H * p.W;
     uint32_t e_use0 = 0, e_use1 = 0;
     int it = 0;
-    for (int t = t_begin; t < t_end; ++t, ++it) {
+    for (int pr = pr_begin; pr < pr_end; ++pr, ++it) {
+      const int t = min(2 * pr + (int)rank, p.ntiles - 1);  // odd tail: duplicate, not stored
       int b, y, x0;
       tile_coords(p, t, b, y, x0);
       // --- A1: row m = pixel x0+m, k = Zernike index (zero-padded to K1)
-      {
-        PROF_T0();
-        mbar_wait(&bars[BAR_A1_EMPTY], (it & 1) ^ 1);
-        PROF_ADD(9);
-      }
+      { PROF_T0(); mbar_wait(&bars[BAR_A1_EMPTY], (it & 1) ^ 1); PROF_ADD(9); }
       {
         const int m = tid;
         const int x = min(x0 + m, p.W - 1);
@@ -392,15 +436,11 @@ __global__ void __launch_bounds__(kThreads) k_fused_p2s(const __grid_constant__ 
       }
       fence_proxy_async_smem();
       __syncwarp();
-      if (lane == 0) mbar_arrive(&bars[BAR_A1_FULL]);
+      if (lane == 0) mbar_arrive_remote(&bars[BAR_A1_FULL], 0);
       if (p.mode != 0) continue;
       // --- E views of every channel
       const int eb = p.n_ebuf == 2 ? (it & 1) : 0;
-      {
-        PROF_T0();
-        mbar_wait(&bars[BAR_E_EMPTY0 + eb], ((eb ? e_use1 : e_use0) & 1) ^ 1);
-        PROF_ADD(11);
-      }
+      { PROF_T0(); mbar_wait(&bars[BAR_E_EMPTY0 + eb], ((eb ? e_use1 : e_use0) & 1) ^ 1); PROF_ADD(11); }
       if (eb) ++e_use1; else ++e_use0;
       uint8_t* Eb = sE + (size_t)eb * 3 * p.chan_bytes;  // buffers are sized for C = 3
       {
@@ -411,7 +451,7 @@ __global__ void __launch_bounds__(kThreads) k_fused_p2s(const __grid_constant__ 
       }
       fence_proxy_async_smem();
       __syncwarp();
-      if (lane == 0) mbar_arrive(&bars[BAR_E_FULL0 + eb]);
+      if (lane == 0) mbar_arrive_remote(&bars[BAR_E_FULL0 + eb], 0);
     }
   } else {
     // ================= epilogue: two warpgroups split every TMEM drain by 16-col groups =====
@@ -421,68 +461,61 @@ __global__ void __launch_bounds__(kThreads) k_fused_p2s(const __grid_constant__ 
     const int m = q * 32 + lane;            // pixel (row of every accumulator)
     const uint32_t tl = tmem + ((uint32_t)(q * 32) << 16);
     const size_t HW = (size_t)p.H * p.W;
+    const int C = p.C;
     uint32_t mlp_waits = 0;
     uint8_t* a2row = sA2 + (m & 7) * 16 + (m >> 3) * p.a2_sbo;
+    uint8_t* hrow = sHold + (m & 7) * 16 + (m >> 3) * p.hold_sbo;
     int it = 0;
-    for (int t = t_begin; t < t_end; ++t, ++it) {
+    for (int pr = pr_begin; pr < pr_end; ++pr, ++it) {
+      const int t_raw = 2 * pr + (int)rank;
+      const bool store = t_raw < p.ntiles;
       int b, y, x0;
-      tile_coords(p, t, b, y, x0);
-      uint4 held[8];                        // L2 chunk 0 (<= 128 cols): this WG's <= 4 groups
-      int held_n0 = -1, held_G = 0;
+      tile_coords(p, min(t_raw, p.ntiles - 1), b, y, x0);
       for (int o = 0; o < p.n_ops; ++o) {
         const MlpOp op = p.ops[o];
         if (op.layer == 2) continue;        // beta stays in TMEM for the conv epilogue
-        {
-          PROF_T0();
-          mbar_wait(&bars[BAR_MLP_DONE], mlp_waits & 1);
-          PROF_ADD(13);
-        }
+        { PROF_T0(); mbar_wait(&bars[BAR_MLP_DONE], mlp_waits & 1); PROF_ADD(13); }
         ++mlp_waits;
         tc_fence_after();
         const float* bias = (op.layer == 0 ? sB1 : sB2) + op.n0;
         const int G = op.N >> 4;
-        const bool hold = op.layer == 1 && !op.last_of_layer;
-#pragma unroll
-        for (int hg = 0; hg < 8; ++hg) {       // this WG's 16-column groups gi = wg + 2*hg
-          const int gi = wg + 2 * hg;
-          if (gi >= G) break;
-          float v[16];
-          tmem_ld16(tl + p.scr_col + gi * 16, v);
+        // L2 chunks other than the last go to the hold buffer (L3 reads them from there)
+        const bool to_hold = op.layer == 1 && !op.last_of_layer;
+        uint8_t* dst = to_hold ? hrow : a2row;
+        const int kc0 = (to_hold ? 0 : op.n0) >> 3;
+#pragma unroll 1
+        for (int hp = 0; hp < 4; ++hp) {     // groups gi = wg + 2*hg, two TMEM loads per wait
+          const int gi0 = wg + 4 * hp, gi1 = gi0 + 2;
+          if (gi0 >= G) break;
+          float v[2][16];
+          tmem_ld16(tl + p.scr_col + gi0 * 16, v[0]);
+          if (gi1 < G) tmem_ld16(tl + p.scr_col + gi1 * 16, v[1]);
           tmem_ld_wait();
 #pragma unroll
-          for (int i = 0; i < 16; ++i) v[i] = fmaxf(v[i] + bias[gi * 16 + i], 0.f);
-          const uint4 lo = pack8(v), hi = pack8(v + 8);
-          if (hold && hg < 4) {
-            held[2 * hg] = lo;
-            held[2 * hg + 1] = hi;
-          } else {
-            const int kc = (op.n0 >> 3) + gi * 2;
-            *reinterpret_cast<uint4*>(a2row + kc * 128) = lo;
-            *reinterpret_cast<uint4*>(a2row + (kc + 1) * 128) = hi;
-          }
-        }
-        if (hold) { held_n0 = op.n0; held_G = G; }
-        if (op.layer == 1 && op.last_of_layer && held_n0 >= 0) {
+          for (int u = 0; u < 2; ++u) {
+            const int gi = gi0 + 2 * u;
+            if (gi < G) {
+              const float4* b4 = reinterpret_cast<const float4*>(bias + gi * 16);
 #pragma unroll
-          for (int hg = 0; hg < 4; ++hg) {
-            const int gi = wg + 2 * hg;
-            if (gi >= held_G) break;
-            const int kc = (held_n0 >> 3) + gi * 2;
-            *reinterpret_cast<uint4*>(a2row + kc * 128) = held[2 * hg];
-            *reinterpret_cast<uint4*>(a2row + (kc + 1) * 128) = held[2 * hg + 1];
+              for (int i4 = 0; i4 < 4; ++i4) {
+                const float4 bb = b4[i4];
+                v[u][4 * i4 + 0] = fmaxf(v[u][4 * i4 + 0] + bb.x, 0.f);
+                v[u][4 * i4 + 1] = fmaxf(v[u][4 * i4 + 1] + bb.y, 0.f);
+                v[u][4 * i4 + 2] = fmaxf(v[u][4 * i4 + 2] + bb.z, 0.f);
+                v[u][4 * i4 + 3] = fmaxf(v[u][4 * i4 + 3] + bb.w, 0.f);
+              }
+              const int kc = kc0 + gi * 2;
+              *reinterpret_cast<uint4*>(dst + kc * 128) = pack8(v[u]);
+              *reinterpret_cast<uint4*>(dst + (kc + 1) * 128) = pack8(v[u] + 8);
+            }
           }
-          held_n0 = -1;
         }
         fence_proxy_async_smem();
         tc_fence_before();
         __syncwarp();
-        if (lane == 0) mbar_arrive(&bars[BAR_SCR_FREE]);
+        if (lane == 0) mbar_arrive_remote(&bars[BAR_SCR_FREE], 0);
       }
-      {
-        PROF_T0();
-        mbar_wait(&bars[BAR_ACC_FULL], it & 1);
-        PROF_ADD(15);
-      }
+      { PROF_T0(); mbar_wait(&bars[BAR_ACC_FULL], it & 1); PROF_ADD(15); }
       tc_fence_after();
       const int x = x0 + m;
       const int GK = p.Nk >> 4;
@@ -491,7 +524,7 @@ __global__ void __launch_bounds__(kThreads) k_fused_p2s(const __grid_constant__ 
           float bv[16];
           tmem_ld16(tl + p.scr_col + gi * 16, bv);
           tmem_ld_wait();
-          if (x < p.W)
+          if (store && x < p.W)
             for (int i = 0; i < 16 && gi * 16 + i < p.K; ++i)
               p.beta_out[((size_t)b * p.K + gi * 16 + i) * HW + (size_t)y * p.W + x] = bv[i] + sB3[gi * 16 + i];
         }
@@ -503,15 +536,23 @@ __global__ void __launch_bounds__(kThreads) k_fused_p2s(const __grid_constant__ 
           tmem_ld16(tl + p.scr_col + gi * 16, bv);
 #pragma unroll
           for (int c = 0; c < 3; ++c)
-            if (c < p.C) tmem_ld16(tl + c * p.Nk + gi * 16, av[c]);
+            if (c < C) tmem_ld16(tl + c * p.Nk + gi * 16, av[c]);
           tmem_ld_wait();
+          const float4* b34 = reinterpret_cast<const float4*>(sB3 + gi * 16);
+          const float4* sv4 = reinterpret_cast<const float4*>(sSv + gi * 16);
 #pragma unroll
-          for (int i = 0; i < 16; ++i) {
-            const float be = bv[i] + sB3[gi * 16 + i];
-            bs = fmaf(be, sSv[gi * 16 + i], bs);
+          for (int i4 = 0; i4 < 4; ++i4) {
+            const float4 b3 = b34[i4], sv = sv4[i4];
+            const float bb[4] = {b3.x, b3.y, b3.z, b3.w}, ss[4] = {sv.x, sv.y, sv.z, sv.w};
 #pragma unroll
-            for (int c = 0; c < 3; ++c)
-              if (c < p.C) jc[c] = fmaf(be, av[c][i], jc[c]);
+            for (int k = 0; k < 4; ++k) {
+              const int i = 4 * i4 + k;
+              const float be = bv[i] + bb[k];
+              bs = fmaf(be, ss[k], bs);
+#pragma unroll
+              for (int c = 0; c < 3; ++c)
+                if (c < C) jc[c] = fmaf(be, av[c][i], jc[c]);
+            }
           }
         }
         float4* red = sRed + (it & 1) * 128;
@@ -521,14 +562,14 @@ __global__ void __launch_bounds__(kThreads) k_fused_p2s(const __grid_constant__ 
           const float4 o = red[m];
           bs += o.w;
           jc[0] += o.x; jc[1] += o.y; jc[2] += o.z;
-          if (x < p.W)
-            for (int c = 0; c < p.C; ++c)
-              p.J[((size_t)b * p.C + c) * HW + (size_t)y * p.W + x] = fmaf(0.5f, bs, jc[c]);
+          if (store && x < p.W)
+            for (int c = 0; c < C; ++c)
+              p.J[((size_t)b * C + c) * HW + (size_t)y * p.W + x] = fmaf(0.5f, bs, jc[c]);
         }
       }
       tc_fence_before();
       __syncwarp();
-      if (lane == 0) mbar_arrive(&bars[BAR_TMEM_FREE]);
+      if (lane == 0) mbar_arrive_remote(&bars[BAR_TMEM_FREE], 0);
     }
   }
 #ifdef P2S_PROFILE
@@ -544,11 +585,12 @@ __global__ void __launch_bounds__(kThreads) k_fused_p2s(const __grid_constant__ 
         if (prof_acc[i]) p.prof[((size_t)blockIdx.x * 4 + base) * 20 + i] = prof_acc[i];
   }
 #endif
-  // ---- teardown
+  // ---- teardown: no CTA leaves while its pair may still touch its shared memory / TMEM
   tc_fence_before();
   __syncthreads();
+  cluster_sync();
   tc_fence_after();
-  if (warp == kWarpMma) tmem_dealloc<kTmemCols>(tmem);
+  if (warp == kWarpMma) tmem_dealloc2<kTmemCols>(tmem);
 }
 
 // Step a3: out(y,x) = bilinear J at (y - t1, x - t0), clamp-to-edge; all channels per thread.

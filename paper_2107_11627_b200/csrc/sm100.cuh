@@ -120,6 +120,61 @@ P2S_DEV void umma_commit(uint64_t* bar) {
                    smem_u32(bar)) : "memory");
 }
 
+// ------------------------------------------------------------------ clusters / CTA pairs
+P2S_DEV uint32_t cluster_ctarank() {
+  uint32_t r;
+  asm volatile("mov.u32 %0, %%cluster_ctarank;" : "=r"(r));
+  return r;
+}
+P2S_DEV void cluster_sync() {
+  asm volatile("barrier.cluster.arrive.release.aligned;\n barrier.cluster.wait.acquire.aligned;" ::: "memory");
+}
+// Arrive on the mbarrier at the same shared-memory offset in CTA `cta` of the cluster.
+P2S_DEV void mbar_arrive_remote(uint64_t* bar, uint32_t cta) {
+  uint32_t remote;
+  asm volatile("mapa.shared::cluster.u32 %0, %1, %2;" : "=r"(remote) : "r"(smem_u32(bar)), "r"(cta));
+  asm volatile("mbarrier.arrive.release.cluster.shared::cluster.b64 _, [%0];" ::"r"(remote) : "memory");
+}
+// Wait with cluster-scope acquire (barriers that receive arrivals from the peer CTA).
+P2S_DEV void mbar_wait_cluster(uint64_t* bar, uint32_t parity) {
+  uint32_t ok = 0;
+  while (!ok) {
+    asm volatile(
+        "{\n .reg .pred p;\n mbarrier.try_wait.parity.acquire.cluster.shared::cta.b64 p, [%1], %2;\n"
+        " selp.u32 %0, 1, 0, p;\n}" : "=r"(ok) : "r"(smem_u32(bar)), "r"(parity) : "memory");
+  }
+}
+// TMEM allocation shared by a CTA pair (one warp with the same warp id in each CTA).
+template <uint32_t kCols>
+P2S_DEV void tmem_alloc2(uint32_t* dst_smem) {
+  asm volatile("tcgen05.alloc.cta_group::2.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(
+                   smem_u32(dst_smem)), "n"(kCols) : "memory");
+  asm volatile("tcgen05.relinquish_alloc_permit.cta_group::2.sync.aligned;" ::: "memory");
+}
+template <uint32_t kCols>
+P2S_DEV void tmem_dealloc2(uint32_t taddr) {
+  asm volatile("tcgen05.dealloc.cta_group::2.sync.aligned.b32 %0, %1;" ::"r"(taddr), "n"(kCols)
+               : "memory");
+}
+// Pair UMMA (issued by the leader CTA only): D[256 x N] (+)= A[256 x 16] * B[N x 16]^T where
+// rows 0-127 of A come from the leader's shared memory and rows 128-255 from the peer's (same
+// address), B rows [0,N/2) from the leader and [N/2,N) from the peer; D row m lands in TMEM lane
+// m%128 of CTA m/128.
+P2S_DEV void umma2_f16_elect(uint32_t d_tmem, uint64_t adesc, uint64_t bdesc, uint32_t idesc,
+                             uint32_t accumulate) {
+  asm volatile(
+      "{\n .reg .pred e, p;\n elect.sync _|e, 0xffffffff;\n setp.ne.b32 p, %4, 0;\n"
+      " @e tcgen05.mma.cta_group::2.kind::f16 [%0], %1, %2, %3, p;\n}" ::"r"(d_tmem),
+      "l"(adesc), "l"(bdesc), "r"(idesc), "r"(accumulate));
+}
+// Arrive once on the barrier at this offset in both CTAs when all prior pair UMMAs complete.
+P2S_DEV void umma2_commit_elect(uint64_t* bar) {
+  asm volatile(
+      "{\n .reg .pred e;\n elect.sync _|e, 0xffffffff;\n"
+      " @e tcgen05.commit.cta_group::2.mbarrier::arrive::one.shared::cluster.multicast::cluster.b64 [%0], %1;\n}" ::"r"(
+          smem_u32(bar)), "h"((uint16_t)3) : "memory");
+}
+
 P2S_DEV uint32_t pack_half2(float a, float b) {
   __half2 h = __floats2half2_rn(a, b);  // cvt.rn (round to nearest even)
   return *reinterpret_cast<uint32_t*>(&h);

@@ -2,8 +2,8 @@
 
 Usage: P2S_LIB=paper_2107_11627_b200/libp2s_prof.so python tools/role_profile.py [cfg]
 Counters (clock64 cycles, averaged over CTAs), per role:
-  MMA issuer : 0 wait A1_FULL, 1 wait TMEM_FREE, 2 wait SCR_FREE, 3 wait E_FULL,
-               4 wait ring (MLP), 5 wait ring (conv), 19 total
+  MMA issuer : 0 wait A1_FULL, 1 wait BETA_FREE, 2 wait SCR_FREE, 3 wait E_FULL,
+               4 wait ring (MLP), 5 wait ring (conv), 6 wait ACC_FREE (first conv stage), 19 total
   producer   : 7 wait ring_empty, 19 total
   builder t0 : 9 wait A1_EMPTY, 11 wait E_EMPTY, 12 build E, 19 total
   epilogue t0: 13 wait MLP_DONE, 15 wait ACC_FULL, 19 total
@@ -32,7 +32,7 @@ torch.cuda.synchronize()
 r.debug_profile_buffer(None)
 c = buf.view(148, 4, 20).cpu().numpy().astype(np.float64)
 names = {0: {0: "wait A1_FULL", 1: "wait TMEM_FREE", 2: "wait SCR_FREE", 3: "wait E_FULL", 4: "wait ring(MLP)",
-             5: "wait ring(conv)", 19: "total"},
+             5: "wait ring(conv)", 6: "wait ACC_FREE", 19: "total"},
          1: {7: "wait ring_empty", 19: "total"},
          2: {9: "wait A1_EMPTY", 11: "wait E_EMPTY", 12: "build E", 19: "total"},
          3: {13: "wait MLP_DONE", 15: "wait ACC_FULL", 19: "total"}}
@@ -41,5 +41,5 @@ ntiles = spec.H * ((spec.W + 127) // 128)
 print(f"cfg{cfg}: {ntiles} tiles over 148 CTAs (~{ntiles / 148:.1f} tiles/CTA); cycles per CTA (mean / max)")
 for ri, role in enumerate(roles):
     for k, n in names[ri].items():
-        v = c[:, ri, k]
+        v = c[0::2, ri, k] if ri == 0 else c[:, ri, k]  # MMA issuer runs in the leader CTAs only
         print(f"  {role:9s} {n:18s} {v.mean():12.0f} {v.max():12.0f}")
