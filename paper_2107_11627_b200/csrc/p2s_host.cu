@@ -1,5 +1,7 @@
 // p2s_host.cu — the C ABI of include/p2s.h: validation, asset packing, execution plan and
 // launches of the sm_100a kernels in p2s_kernels.cuh. No torch types, no oracle code.
+#include <cuda.h>
+#include <cudaTypedefs.h>
 #include <cuda_runtime.h>
 
 #include <algorithm>
@@ -129,6 +131,8 @@ struct p2s_handle {
   size_t stage_px_cap = 0, stage_chw_cap = 0;
   cudaEvent_t ev_begin = nullptr, ev_end = nullptr;
   unsigned long long* prof = nullptr;
+  CUtensorMap maps[kMaxMaps];
+  int n_maps = 0;
   int progressive = 1;
 };
 
@@ -182,6 +186,7 @@ FusedParams make_params(const p2s_handle* h, int B, int C, int H, int W, int mod
   p.a1_sbo = h->a1_sbo; p.a2_sbo = h->a2_sbo; p.hold_sbo = h->hold_sbo;
   p.l3_hold_ks = h->l3_hold_ks;
   p.prof = h->prof;
+  for (int i = 0; i < kMaxMaps; ++i) p.maps[i] = h->maps[i];
   p.progressive = h->progressive;
   return p;
 }
@@ -288,7 +293,7 @@ p2s_status p2s_init(const p2s_basis* basis, const p2s_mlp* mlp, p2s_handle** out
   const int const_bytes = (2 * kMaxN + 256) * 4;
   const int red_bytes = 2 * 128 * 16;
   auto al = [](int v) { return (v + 127) / 128 * 128; };
-  const int bar_bytes = (BAR_RING + 3 * 4) * 8 + 16;
+  const int bar_bytes = (BAR_RING + 2 * 4) * 8 + 16;
   const int fixed = al(a1_bytes) + al(a2_bytes) + al(hold_bytes) + al(tab_bytes) + al(const_bytes) +
                     al(red_bytes) + al(bar_bytes);
   const int max_half_slab = std::max(std::max(h->N1, h->N2), h->Nk) / 2 * 32;
@@ -317,7 +322,7 @@ p2s_status p2s_init(const p2s_basis* basis, const p2s_mlp* mlp, p2s_handle** out
   h->off_tab = off; off += al(tab_bytes);
   h->off_const = off; off += al(const_bytes);
   h->off_red = off; off += al(red_bytes);
-  h->off_bar = off; off += (BAR_RING + 3 * nring) * 8 + 16;
+  h->off_bar = off; off += (BAR_RING + 2 * nring) * 8 + 16;
   h->smem_bytes = off;
   h->a1_sbo = (h->K1 / 8) * 128;
   h->a2_sbo = (kh / 8) * 128;
@@ -360,8 +365,18 @@ p2s_status p2s_init(const p2s_basis* basis, const p2s_mlp* mlp, p2s_handle** out
       }
 
   // ---- per-tile-pair item lists (ring stages in issue order)
+  // one tensor map per distinct half-slab height (N/16 rows of 256 B)
+  std::vector<int> map_rows;
+  auto map_of = [&](int N) {
+    const int rows = N / 16;
+    for (size_t i = 0; i < map_rows.size(); ++i)
+      if (map_rows[i] == rows) return (int)i;
+    map_rows.push_back(rows);
+    return (int)map_rows.size() - 1;
+  };
   auto make_items = [&](size_t base, int nks, int N, uint8_t kind, uint8_t op, std::vector<Item>& out) {
     const uint32_t hs = (uint32_t)N * 16, per = std::max<uint32_t>(1, (uint32_t)sb / hs);
+    const int mi = map_of(N);
     for (int s0 = 0; s0 < nks; s0 += per) {
       const int ns = std::min<int>(per, nks - s0);
       Item it{};
@@ -373,6 +388,8 @@ p2s_status p2s_init(const p2s_basis* basis, const p2s_mlp* mlp, p2s_handle** out
       it.kind = kind;
       it.op = op;
       it.flags = (s0 == 0 ? IT_BEGIN : 0) | (s0 + ns >= nks ? IT_END : 0);
+      it.map = (uint8_t)mi;
+      it.rows = (uint8_t)(N / 16);
       out.push_back(it);
     }
   };
@@ -420,6 +437,31 @@ p2s_status p2s_init(const p2s_basis* basis, const p2s_mlp* mlp, p2s_handle** out
   if ((e = cudaMemcpy((dst), (src), (bytes), cudaMemcpyHostToDevice)) != cudaSuccess)               \
     return fail(cuda_fail(e, "cudaMemcpy"));
   UP(h->d_stream, stream.data(), total);
+  if ((int)map_rows.size() > kMaxMaps) return fail(P2S_ERR_UNSUPPORTED);
+  {
+    void* fn = nullptr;
+    cudaDriverEntryPointQueryResult q;
+    if ((e = cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &fn, cudaEnableDefault, &q)) != cudaSuccess ||
+        q != cudaDriverEntryPointSuccess || !fn)
+      return fail(cuda_fail(e != cudaSuccess ? e : cudaErrorUnknown, "cuTensorMapEncodeTiled entry point"));
+    auto encode = reinterpret_cast<PFN_cuTensorMapEncodeTiled>(fn);
+    std::memset(h->maps, 0, sizeof(h->maps));
+    for (size_t i = 0; i < map_rows.size(); ++i) {
+      // the stream viewed as uint8 [total/256][256]; one box = one half slab
+      cuuint64_t gdim[2] = {256, (cuuint64_t)(total / 256)};
+      cuuint64_t gstride[1] = {256};
+      cuuint32_t box[2] = {256, (cuuint32_t)map_rows[i]};
+      cuuint32_t estr[2] = {1, 1};
+      CUresult cr = encode(&h->maps[i], CU_TENSOR_MAP_DATA_TYPE_UINT8, 2, h->d_stream, gdim, gstride, box, estr,
+                           CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE,
+                           CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+      if (cr != CUDA_SUCCESS) {
+        g_last_cuda_error = "cuTensorMapEncodeTiled failed (" + std::to_string((int)cr) + ")";
+        return fail(P2S_ERR_CUDA);
+      }
+    }
+    h->n_maps = (int)map_rows.size();
+  }
   UP(h->d_items, h->items.data(), h->items.size() * sizeof(Item));
   UP(h->d_steps, steps.data(), steps.size() * sizeof(uint32_t));
   UP(h->d_consts, consts.data(), consts.size() * 4);

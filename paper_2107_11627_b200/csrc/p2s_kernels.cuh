@@ -20,21 +20,22 @@
 //    per tile (double-buffered), and each K-step addresses it with an overlapping
 //    descriptor (SBO = 16 B per pixel row). See plan_conv() in p2s_host.cu.
 //
-// Roles (per CTA, 14 warps): w0 producer, w1 UMMA issuer (leader CTA) / stage forwarder
-// (peer CTA), w2-5 builders (A1 = Zernike tile, E views), w6-13 epilogue (2 warpgroups).
+// Roles (per CTA, 14 warps): w0 TMA producer, w1 UMMA issuer (leader CTA only), w2-5
+// builders (A1 = Zernike tile, E views), w6-13 epilogue (2 warpgroups).
 // Schedule per tile pair (host-built item list, identical in both CTAs):
 //   L1c0 | conv stages | L1c1 | conv stages | L2c0 | ... | L3 | remaining conv stages.
 // MLP chunks accumulate in a TMEM "scratch" region next to the C conv accumulators; the
 // epilogue warps drain each chunk (bias, ReLU, fp16) into the shared-memory A operand of
 // the next layer while the tensor cores run conv stages.
 #pragma once
+#include <cuda.h>
 #include "sm100.cuh"
 
 namespace p2s {
 
 constexpr int kTileM = 128;          // pixels per CTA tile (UMMA M = 256 per CTA pair)
 constexpr int kWarpProducer = 0;
-constexpr int kWarpMma = 1;          // leader: UMMA issuer; peer: forwards ring-stage arrivals
+constexpr int kWarpMma = 1;          // leader CTA: UMMA issuer (idle in the peer)
 constexpr int kWarpBuild0 = 2;
 constexpr int kNumBuildWarps = 4;
 constexpr int kWarpEpi0 = kWarpBuild0 + kNumBuildWarps;  // warps 6..13
@@ -59,7 +60,9 @@ struct Item {
   uint8_t kind;          // 0 = MLP op, 1 = conv
   uint8_t op;            // MLP op index
   uint8_t flags;         // IT_BEGIN / IT_END (first / last item of the op or of the conv)
-  uint8_t pad[5];
+  uint8_t map;           // tensor map (box = one half slab: N/16 rows of 256 B)
+  uint8_t rows;          // 256-B rows per half slab (N / 16)
+  uint8_t pad[3];
 };
 static_assert(sizeof(Item) == 24, "Item layout");
 
@@ -71,7 +74,9 @@ struct MlpOp {
   int first_of_layer, last_of_layer;
 };
 
+constexpr int kMaxMaps = 6;
 struct FusedParams {
+  CUtensorMap maps[kMaxMaps];  // the packed B stream as uint8 [rows][256], box {256, N/16}
   const float* image;    // [B][C][H][W]
   const float* zernike;  // [B][n_in][H][W]
   float* J;              // [B][C][H][W] (mode 0)
@@ -124,7 +129,7 @@ enum Bar {
   BAR_SCR_FREE,      // (L) 2 x 8 epilogue warps
   BAR_ACC_FULL,      // (B)
   BAR_TMEM_FREE,     // (L) 2 x 8 epilogue warps
-  BAR_RING = 10      // then ring_full[n] (C), ring_peer[n] (L), ring_empty[n] (B)
+  BAR_RING = 10      // then ring_full[n] (L: both CTAs' TMA bytes), ring_empty[n] (B)
 };
 
 __device__ __forceinline__ void tile_coords(const FusedParams& p, int t, int& b, int& y, int& x0) {
@@ -221,9 +226,8 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads)
   extern __shared__ __align__(1024) uint8_t smem[];
   uint64_t* bars = reinterpret_cast<uint64_t*>(smem + p.off_bar);
   uint64_t* ring_full = bars + BAR_RING;
-  uint64_t* ring_peer = bars + BAR_RING + p.nring;
-  uint64_t* ring_empty = bars + BAR_RING + 2 * p.nring;
-  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bars + BAR_RING + 3 * p.nring);
+  uint64_t* ring_empty = bars + BAR_RING + p.nring;
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bars + BAR_RING + 2 * p.nring);
   uint8_t* ring = smem + p.off_ring;
   uint8_t* sA1 = smem + p.off_a1;
   uint8_t* sA2 = smem + p.off_a2;
@@ -253,6 +257,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads)
 #pragma unroll
   for (int i = 0; i < 20; ++i) prof_acc[i] = 0;
   const long long prof_start = clock64();
+  prof_acc[10] = globaltimer_ns();
 #endif
   const Item* gItems = p.items + (p.mode == 0 ? 0 : p.n_items_full);
 
@@ -273,7 +278,6 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads)
     mbar_init(&bars[BAR_TMEM_FREE], 2 * kNumEpiWarps);
     for (int i = 0; i < p.nring; ++i) {
       mbar_init(&ring_full[i], 1);
-      mbar_init(&ring_peer[i], 1);
       mbar_init(&ring_empty[i], 1);
     }
     fence_mbar_init();
@@ -286,34 +290,27 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads)
   const uint32_t tmem = *tmem_slot;
 
   if (warp == kWarpProducer) {
-    // ================= producer: stream this CTA's half of every slab into the ring ========
+    // ================= producer: TMA this CTA's half of every slab into the ring; both CTAs'
+    // copies complete on the leader's ring_full (the leader arms it with both halves' bytes)
     if (lane == 0) {
+      for (int i = 0; i < kMaxMaps; ++i) prefetch_tmap(&p.maps[i]);
       int s = 0;
       uint32_t ph = 0;
       for (int pr = pr_begin; pr < pr_end; ++pr) {
         for (int g = 0; g < n_items; ++g) {
           const Item it = sItems[g];
           { PROF_T0(); mbar_wait(&ring_empty[s], ph ^ 1); PROF_ADD(7); }
-          mbar_arrive_expect_tx(&ring_full[s], it.bytes);
-          bulk_g2s(ring + (size_t)s * p.stage_bytes, p.stream + it.src_off + rank * it.half_stride, it.bytes,
-                   &ring_full[s]);
+          if (leader) mbar_arrive_expect_tx(&ring_full[s], 2u * it.bytes);
+          const uint32_t mb = cluster_addr(&ring_full[s], 0);
+          const int y0 = (int)((it.src_off + rank * it.half_stride) >> 8);
+          uint8_t* dst = ring + (size_t)s * p.stage_bytes;
+          for (int j = 0; j < it.nslabs; ++j)
+            tma2_load_2d(dst + (size_t)j * it.rows * 256, &p.maps[it.map], 0, y0 + j * it.rows, mb);
           if (++s == p.nring) { s = 0; ph ^= 1; }
         }
       }
     }
-  } else if (warp == kWarpMma && !leader) {
-    // ================= peer: forward "my half of stage s landed" to the leader =============
-    int s = 0;
-    uint32_t ph = 0;
-    for (int pr = pr_begin; pr < pr_end; ++pr) {
-      for (int g = 0; g < n_items; ++g) {
-        mbar_wait(&ring_full[s], ph);
-        if (lane == 0) mbar_arrive_remote(&ring_peer[s], 0);
-        __syncwarp();
-        if (++s == p.nring) { s = 0; ph ^= 1; }
-      }
-    }
-  } else if (warp == kWarpMma) {
+  } else if (warp == kWarpMma && leader) {
     // ================= leader: UMMA issuer (whole warp, uniform values; one lane issues) ====
     // Descriptors are assembled from precomputed 32-bit halves so the per-UMMA work is one
     // or two uniform adds: lo = start>>4 | (LBO>>4)<<16, hi = SBO>>4 | version(bit 46).
@@ -340,6 +337,9 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads)
     uint32_t scr_waits = 0;
     uint32_t e_use0 = 0, e_use1 = 0;
     int it = 0;
+#ifdef P2S_PROFILE
+    prof_acc[11] = globaltimer_ns();
+#endif
     for (int pr = pr_begin; pr < pr_end; ++pr, ++it) {
       const int eb = ebufs == 2 ? (it & 1) : 0;
       for (int g = 0; g < n_items; ++g) {
@@ -357,7 +357,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads)
             }
             tc_fence_after();
           }
-          { PROF_T0(); mbar_wait(&ring_full[s], ph); mbar_wait_cluster(&ring_peer[s], ph); PROF_ADD(4); }
+          { PROF_T0(); mbar_wait(&ring_full[s], ph); PROF_ADD(4); }
           tc_fence_after();
           const uint32_t idesc = idesc_f16(256, op.N);
           const uint32_t half16 = (uint32_t)op.N;  // (16 * N) >> 4
@@ -384,7 +384,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads)
             { PROF_T0(); mbar_wait_cluster(&bars[BAR_E_FULL0 + eb], (eb ? e_use1 : e_use0) & 1); PROF_ADD(3); }
             tc_fence_after();
           }
-          { PROF_T0(); mbar_wait(&ring_full[s], ph); mbar_wait_cluster(&ring_peer[s], ph); PROF_ADD(5); }
+          { PROF_T0(); mbar_wait(&ring_full[s], ph); PROF_ADD(5); }
           tc_fence_after();
           const uint32_t e0 = e_lo + (uint32_t)eb * ebuf16;
           const uint32_t* steps = sSteps + itm.first;
@@ -409,7 +409,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads)
         }
       }
     }
-  } else if (warp < kWarpEpi0) {
+  } else if (warp >= kWarpBuild0 && warp < kWarpEpi0) {
     // ================= builders: A1 (Zernike tile, fp16) and E views (fp16, centred) =====
     const int tid = threadIdx.x - kWarpBuild0 * 32;
     const size_t HW = (size_t)p.H * p.W;
@@ -453,7 +453,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads)
       __syncwarp();
       if (lane == 0) mbar_arrive_remote(&bars[BAR_E_FULL0 + eb], 0);
     }
-  } else {
+  } else if (warp >= kWarpEpi0) {
     // ================= epilogue: two warpgroups split every TMEM drain by 16-col groups =====
     const int ew = warp - kWarpEpi0;        // 0..7
     const int wg = ew >> 2;                 // warpgroup 0 / 1
@@ -555,6 +555,10 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads)
             }
           }
         }
+        // every TMEM read of this tile is done: release TMEM before combining / storing J
+        tc_fence_before();
+        __syncwarp();
+        if (lane == 0) mbar_arrive_remote(&bars[BAR_TMEM_FREE], 0);
         float4* red = sRed + (it & 1) * 128;
         if (wg == 1) red[m] = make_float4(jc[0], jc[1], jc[2], bs);
         named_bar_sync(1, 32 * kNumEpiWarps);
@@ -567,13 +571,16 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads)
               p.J[((size_t)b * C + c) * HW + (size_t)y * p.W + x] = fmaf(0.5f, bs, jc[c]);
         }
       }
-      tc_fence_before();
-      __syncwarp();
-      if (lane == 0) mbar_arrive_remote(&bars[BAR_TMEM_FREE], 0);
+      if (p.mode == 1) {
+        tc_fence_before();
+        __syncwarp();
+        if (lane == 0) mbar_arrive_remote(&bars[BAR_TMEM_FREE], 0);
+      }
     }
   }
 #ifdef P2S_PROFILE
   {
+    prof_acc[12] = globaltimer_ns();
     prof_acc[19] = (unsigned long long)(clock64() - prof_start);
     int base = -1;
     if (warp == kWarpMma && lane == 0) base = 0;

@@ -32,6 +32,14 @@ P2S_DEV bool mbar_try_wait(uint64_t* bar, uint32_t parity) {
       " selp.u32 %0, 1, 0, p;\n}" : "=r"(ok) : "r"(smem_u32(bar)), "r"(parity) : "memory");
   return ok != 0;
 }
+// Non-blocking probe: true if the phase with this parity has completed.
+P2S_DEV bool mbar_test(uint64_t* bar, uint32_t parity) {
+  uint32_t ok;
+  asm volatile(
+      "{\n .reg .pred p;\n mbarrier.test_wait.parity.shared::cta.b64 p, [%1], %2;\n"
+      " selp.u32 %0, 1, 0, p;\n}" : "=r"(ok) : "r"(smem_u32(bar)), "r"(parity) : "memory");
+  return ok != 0;
+}
 P2S_DEV void mbar_wait(uint64_t* bar, uint32_t parity) {
   while (!mbar_try_wait(bar, parity)) {
   }
@@ -45,6 +53,23 @@ P2S_DEV void bulk_g2s(void* dst_smem, const void* src_gmem, uint32_t bytes, uint
           smem_u32(dst_smem)),
       "l"(src_gmem), "r"(bytes), "r"(smem_u32(bar))
       : "memory");
+}
+// TMA 2-D tile load for a CTA pair: writes this CTA's shared memory and completes the
+// transaction bytes on `mbar_cluster` (a shared::cluster address, typically the leader's).
+P2S_DEV void tma2_load_2d(void* dst_smem, const void* tmap, int x, int y, uint32_t mbar_cluster) {
+  asm volatile(
+      "cp.async.bulk.tensor.2d.cta_group::2.shared::cluster.global.mbarrier::complete_tx::bytes"
+      " [%0], [%1, {%2, %3}], [%4];" ::"r"(smem_u32(dst_smem)),
+      "l"(tmap), "r"(x), "r"(y), "r"(mbar_cluster)
+      : "memory");
+}
+P2S_DEV void prefetch_tmap(const void* tmap) {
+  asm volatile("prefetch.tensormap [%0];" ::"l"(tmap) : "memory");
+}
+P2S_DEV uint32_t cluster_addr(const void* smem_ptr, uint32_t cta) {
+  uint32_t a;
+  asm volatile("mapa.shared::cluster.u32 %0, %1, %2;" : "=r"(a) : "r"(smem_u32(smem_ptr)), "r"(cta));
+  return a;
 }
 P2S_DEV void fence_proxy_async_smem() { asm volatile("fence.proxy.async.shared::cta;" ::: "memory"); }
 
@@ -135,15 +160,10 @@ P2S_DEV void mbar_arrive_remote(uint64_t* bar, uint32_t cta) {
   asm volatile("mapa.shared::cluster.u32 %0, %1, %2;" : "=r"(remote) : "r"(smem_u32(bar)), "r"(cta));
   asm volatile("mbarrier.arrive.release.cluster.shared::cluster.b64 _, [%0];" ::"r"(remote) : "memory");
 }
-// Wait with cluster-scope acquire (barriers that receive arrivals from the peer CTA).
-P2S_DEV void mbar_wait_cluster(uint64_t* bar, uint32_t parity) {
-  uint32_t ok = 0;
-  while (!ok) {
-    asm volatile(
-        "{\n .reg .pred p;\n mbarrier.try_wait.parity.acquire.cluster.shared::cta.b64 p, [%1], %2;\n"
-        " selp.u32 %0, 1, 0, p;\n}" : "=r"(ok) : "r"(smem_u32(bar)), "r"(parity) : "memory");
-  }
-}
+// Wait on a barrier that also receives arrivals from the peer CTA (release.cluster on the
+// arriving side). A CTA-scope acquire suffices for the UMMA consumer (as in CUTLASS's 2-SM
+// kernels) and avoids the L1 invalidation a cluster-scope acquire implies.
+P2S_DEV void mbar_wait_cluster(uint64_t* bar, uint32_t parity) { mbar_wait(bar, parity); }
 // TMEM allocation shared by a CTA pair (one warp with the same warp id in each CTA).
 template <uint32_t kCols>
 P2S_DEV void tmem_alloc2(uint32_t* dst_smem) {
@@ -180,6 +200,11 @@ P2S_DEV uint32_t pack_half2(float a, float b) {
   return *reinterpret_cast<uint32_t*>(&h);
 }
 
+P2S_DEV unsigned long long globaltimer_ns() {
+  unsigned long long t;
+  asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+  return t;
+}
 P2S_DEV uint32_t lane_id() { return threadIdx.x & 31u; }
 P2S_DEV uint32_t warp_id() { return __shfl_sync(0xffffffffu, threadIdx.x >> 5, 0); }
 

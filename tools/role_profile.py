@@ -43,3 +43,13 @@ for ri, role in enumerate(roles):
     for k, n in names[ri].items():
         v = c[0::2, ri, k] if ri == 0 else c[:, ri, k]  # MMA issuer runs in the leader CTAs only
         print(f"  {role:9s} {n:18s} {v.mean():12.0f} {v.max():12.0f}")
+
+# wall-clock phases (globaltimer ns): kernel entry (slot 10), MMA loop start (11), role end (12)
+t0 = c[:, :, 10][c[:, :, 10] > 0].min()
+ent = c[0::2, 0, 10] - t0
+lst = c[0::2, 0, 11] - t0
+lend = c[0::2, 0, 12] - t0
+eend = c[:, 3, 12] - t0
+print(f"wall (us, rel. first CTA entry): entry max {ent.max()/1e3:.1f}; MMA loop start mean {lst.mean()/1e3:.1f} "
+      f"max {lst.max()/1e3:.1f}; MMA loop end min {lend.min()/1e3:.1f} mean {lend.mean()/1e3:.1f} max {lend.max()/1e3:.1f}; "
+      f"epilogue end max {eend.max()/1e3:.1f}")

@@ -203,6 +203,76 @@ __global__ void __launch_bounds__(256, 1) k_tmem_ld(int nwarps, int iters, unsig
   if (warp_id() == 0) tmem_dealloc<512>(tmem);
 }
 
+
+// ---- 6. interference: UMMA (N=112, M=128, overlapped A) while other warps either stream
+// tcgen05.ld from other TMEM columns (mode 1) or spin in mbarrier try_wait (mode 2).
+__global__ void __launch_bounds__(384, 1) k_interf(int mode, int iters, unsigned long long* cyc, float* sink) {
+  extern __shared__ __align__(1024) uint8_t smem[];
+  __shared__ uint64_t bar, bar_never;
+  __shared__ uint32_t tslot;
+  __shared__ volatile int done;
+  for (int i = threadIdx.x * 16; i < 96 * 1024; i += 384 * 16) *reinterpret_cast<int4*>(smem + i) = make_int4(0, 0, 0, 0);
+  fence_proxy_async_smem();
+  if (threadIdx.x == 0) { mbar_init(&bar, 1); mbar_init(&bar_never, 1); done = 0; fence_mbar_init(); }
+  if (warp_id() == 0) tmem_alloc<512>(&tslot);
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
+  uint32_t tmem = tslot;
+  const int w = warp_id();
+  if (w == 0) {
+    constexpr uint32_t id = idesc_f16(128, 112);
+    const uint32_t sa = smem_u32(smem), sb = smem_u32(smem + 64 * 1024);
+    uint64_t ad[4], bd[4];
+#pragma unroll
+    for (int i = 0; i < 4; ++i) { ad[i] = sdesc(sa + i * 16 * 5, 128, 128); bd[i] = sdesc(sb + i * 8192, 128, 256); }
+    long long t0 = clock64();
+    for (int it = 0; it < iters; it += 3) {
+#pragma unroll
+      for (int j = 0; j < 3; ++j) umma_f16_elect(tmem + j * 112, ad[j], bd[(it / 3) & 3], id, 1);
+    }
+    umma_commit_elect(&bar);
+    mbar_wait(&bar, 0);
+    long long t1 = clock64();
+    if (lane_id() == 0) { cyc[blockIdx.x] = (unsigned long long)(t1 - t0); done = 1; }
+  } else if (mode == 1 && w >= 4) {
+    // TMEM readers: 8 warps (2 per lane quadrant) reading columns [384, 512)
+    int q = w & 3;
+    float acc = 0;
+    while (!done) {
+      for (int c = 384; c < 512; c += 16) {
+        float v[16];
+        tmem_ld16(tmem + ((uint32_t)(q * 32) << 16) + c, v);
+        tmem_ld_wait();
+        for (int i = 0; i < 16; ++i) acc += v[i];
+      }
+    }
+    sink[threadIdx.x] = acc;
+  } else if (mode == 2 && w >= 4) {
+    while (!done) { mbar_try_wait(&bar_never, 0); }
+  }
+  tc_fence_before();
+  __syncthreads();
+  if (warp_id() == 0) tmem_dealloc<512>(tmem);
+}
+
+static void run_interf(int nsm) {
+  unsigned long long* dc; float* sink; CK(cudaMalloc(&dc, 1024 * 8)); CK(cudaMalloc(&sink, 4096 * 4));
+  CK(cudaFuncSetAttribute(k_interf, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024));
+  const int iters = 6144;
+  for (int mode = 0; mode < 3; ++mode) {
+    k_interf<<<nsm, 384, 200 * 1024>>>(mode, iters, dc, sink);
+    CK(cudaGetLastError()); CK(cudaDeviceSynchronize());
+    k_interf<<<nsm, 384, 200 * 1024>>>(mode, iters, dc, sink);
+    CK(cudaGetLastError()); CK(cudaDeviceSynchronize());
+    std::vector<unsigned long long> c(nsm);
+    CK(cudaMemcpy(c.data(), dc, nsm * 8, cudaMemcpyDeviceToHost));
+    double mx = 0; for (auto v : c) mx = fmax(mx, (double)v);
+    printf("interference mode=%d (%s): %.1f cyc/mma (floor 56)\\n", mode,
+           mode == 0 ? "alone" : mode == 1 ? "8 warps tcgen05.ld" : "8 warps spin try_wait", mx / iters);
+  }
+}
+
 int main() {
   int fails = 0;
   unsigned s = 12345;
@@ -271,6 +341,7 @@ int main() {
     run_tput<112, 1, 1, 6>(nsm); run_tput<112, 1, 2, 6>(nsm);
     run_tput<208, 0, 0, 2>(nsm); run_tput<64, 0, 0, 4>(nsm);
   }
+  { int nsm = 0; CK(cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, 0)); run_interf(nsm); }
   // ---- 5. TMEM load throughput
   {
     unsigned long long* dc; float* sink; CK(cudaMalloc(&dc, 8)); CK(cudaMalloc(&sink, 1024 * 4));
