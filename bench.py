@@ -26,6 +26,7 @@ import numpy as np
 ROOT = os.path.dirname(os.path.abspath(__file__))
 sys.path.insert(0, ROOT)
 
+from paper_2107_11627_b200 import dist as pdist  # noqa: E402
 from paper_2107_11627_b200 import synth  # noqa: E402
 
 CFG_ID = 3
@@ -44,9 +45,12 @@ def _peaks():
 
 
 class ClockSampler:
-    """nvidia-smi clocks/throttle reasons sampled during the timed region (B200_PROFILING.md)."""
+    """nvidia-smi clocks/throttle reasons sampled during the timed region (B200_PROFILING.md).
 
-    Q = ("index,clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
+    Sampling starts before the region (waiting for the first sample) and only samples whose
+    timestamps fall inside [mark_start, mark_end] are summarised."""
+
+    Q = ("timestamp,index,clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
          "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
          "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
 
@@ -54,25 +58,35 @@ class ClockSampler:
         self.idx = gpu_index
         self.proc = None
         self.lines = []
+        self.t0 = self.t1 = None
 
     def __enter__(self):
         try:
             self.proc = subprocess.Popen(["nvidia-smi", "-i", str(self.idx), f"--query-gpu={self.Q}",
-                                          "--format=csv,noheader,nounits", "-lms", "100"],
+                                          "--format=csv,noheader,nounits", "-lms", "50"],
                                          stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
             self.t = threading.Thread(target=self._read, daemon=True)
             self.t.start()
+            deadline = time.time() + 5
+            while not self.lines and time.time() < deadline:
+                time.sleep(0.02)
         except Exception:
             self.proc = None
         return self
 
     def _read(self):
         for line in self.proc.stdout:
-            self.lines.append(line.strip())
+            self.lines.append((time.time(), line.strip()))
+
+    def mark_start(self):
+        self.t0 = time.time()
+
+    def mark_end(self):
+        self.t1 = time.time()
 
     def __exit__(self, *a):
         if self.proc:
-            time.sleep(0.25)
+            time.sleep(0.15)
             self.proc.terminate()
             try:
                 self.proc.wait(timeout=2)
@@ -80,24 +94,27 @@ class ClockSampler:
                 self.proc.kill()
 
     def summary(self):
-        sm, mx, reasons = [], None, set()
+        sm, pw, mx, reasons = [], [], None, set()
         names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
-        for ln in self.lines:
+        for ts, ln in self.lines:
+            if self.t0 is not None and not (self.t0 <= ts <= (self.t1 or ts) + 0.06):
+                continue
             f = [x.strip() for x in ln.split(",")]
-            if len(f) < 9:
+            if len(f) < 10:
                 continue
             try:
-                sm.append(float(f[1]))
-                mx = float(f[2])
+                sm.append(float(f[2]))
+                mx = float(f[3])
+                pw.append(float(f[4]))
             except ValueError:
                 continue
-            for n, v in zip(names, f[5:9]):
+            for n, v in zip(names, f[6:10]):
                 if v.lower().startswith("active"):
                     reasons.add(n)
         if not sm:
             return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["unavailable"], "samples": 0}
         return {"sm_mhz": float(np.median(sm)), "sm_max_mhz": mx, "reasons": sorted(reasons),
-                "samples": len(sm)}
+                "samples": len(sm), "power_w_max": max(pw) if pw else None}
 
 
 def cpu_reference(spec, inp, budget_s: float, threads: int):
@@ -137,7 +154,7 @@ def lscpu_model():
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
-    ap.add_argument("--steps", type=int, default=20)
+    ap.add_argument("--steps", type=int, default=400)
     ap.add_argument("--warmup", type=int, default=5)
     ap.add_argument("--impl", default="b200", choices=["b200", "reference"])
     ap.add_argument("--no-cpu-baseline", action="store_true")
@@ -145,9 +162,7 @@ def main():
     ap.add_argument("--e2e-steps", type=int, default=None)
     args = ap.parse_args()
 
-    rank = int(os.environ.get("RANK", "0"))
-    world = int(os.environ.get("WORLD_SIZE", "1"))
-    local_rank = int(os.environ.get("LOCAL_RANK", "0"))
+    rank, world, local_rank = pdist.env_rank_world()
     spec = synth.CONFIGS[CFG_ID]
     peak, peak_sust, hbm, peak_src = _peaks()
     flops_frame = spec.flops_per_frame()
@@ -179,14 +194,13 @@ def main():
     import torch
     dist = None
     if world > 1:
-        import torch.distributed as dist
-        dist.init_process_group("nccl", device_id=torch.device("cuda", local_rank))
+        dist = pdist.init("nccl", device_id=torch.device("cuda", local_rank))
     torch.cuda.set_device(local_rank)
     dev = torch.device("cuda", local_rank)
     from paper_2107_11627_b200 import p2s
 
     # each rank renders its own frame (per-frame seeds = rank): weak scaling, no data-path collective
-    inp = synth.make_inputs(spec, frames=range(rank, rank + 1))
+    inp = synth.make_inputs(spec, frames=pdist.rank_frames(rank, 1))
     r = p2s.Renderer(inp.basis, inp.mlp)
     B, C, H, W = inp.image.shape
     r.reserve(B, C, H, W)
@@ -210,6 +224,7 @@ def main():
         if dist:
             dist.barrier()
         torch.cuda.synchronize()
+        clk.mark_start()
         t_wall0 = time.perf_counter()
         for i in range(args.steps):
             flush.fill_(float(i))  # L2 flush outside the timed step
@@ -222,15 +237,11 @@ def main():
         if dist:
             dist.barrier()
         t_wall = time.perf_counter() - t_wall0
+        clk.mark_end()
     step_ms = np.array([ev_s0[i].elapsed_time(ev_s1[i]) for i in range(args.steps)])
     fused_ms = np.array([ev_f0[i].elapsed_time(ev_f1[i]) for i in range(args.steps)])
-    tot_ms = float(step_ms.sum())
-    if dist:
-        tt = torch.tensor([tot_ms], device=dev)
-        dist.all_reduce(tt, op=dist.ReduceOp.MAX)
-        tot_ms = float(tt.item())
-    frames = world * B * args.steps
-    value = frames / (tot_ms / 1e3)
+    tot_ms = pdist.max_over_ranks(float(step_ms.sum()), dist, dev)
+    value = pdist.throughput(B, world, args.steps, tot_ms)
 
     # ---- e2e: same metric through p2s_render_host (pinned host buffers, copies inside the step)
     e2e_steps = args.e2e_steps or max(3, min(args.steps, 10))
@@ -251,19 +262,15 @@ def main():
         r.render_host(h_img, h_z, h_t, h_out)
         e1[i].record(stream)
     torch.cuda.synchronize()
-    e2e_ms = float(sum(e0[i].elapsed_time(e1[i]) for i in range(e2e_steps)))
-    if dist:
-        tt = torch.tensor([e2e_ms], device=dev)
-        dist.all_reduce(tt, op=dist.ReduceOp.MAX)
-        e2e_ms = float(tt.item())
-    e2e_value = world * B * e2e_steps / (e2e_ms / 1e3)
+    e2e_ms = pdist.max_over_ranks(float(sum(e0[i].elapsed_time(e1[i]) for i in range(e2e_steps))), dist, dev)
+    e2e_value = pdist.throughput(B, world, e2e_steps, e2e_ms)
     h2d = inp.image.nbytes + inp.zernike.nbytes + inp.tilt.nbytes
     d2h = h_out.nbytes
 
     if dist:
         dist.barrier()
     if rank != 0:
-        dist.destroy_process_group()
+        pdist.shutdown(dist)
         return
 
     fused_mean = float(fused_ms.mean())
@@ -309,8 +316,7 @@ def main():
         line["cpu_baseline"] = {"value": fps, "unit": "frames/s", "cores": threads, "kind": "oracle",
                                 "sample": sample + f"; host: {lscpu_model()}"}
     print(json.dumps(line))
-    if dist:
-        dist.destroy_process_group()
+    pdist.shutdown(dist)
 
 
 if __name__ == "__main__":
