@@ -293,7 +293,7 @@ p2s_status p2s_init(const p2s_basis* basis, const p2s_mlp* mlp, p2s_handle** out
   const int const_bytes = (2 * kMaxN + 256) * 4;
   const int red_bytes = 2 * 128 * 16;
   auto al = [](int v) { return (v + 127) / 128 * 128; };
-  const int bar_bytes = (BAR_RING + 2 * 4) * 8 + 16;
+  const int bar_bytes = (BAR_RING + 2 * 4) * 8 + 16;  // BAR_RING fixed barriers + ring
   const int fixed = al(a1_bytes) + al(a2_bytes) + al(hold_bytes) + al(tab_bytes) + al(const_bytes) +
                     al(red_bytes) + al(bar_bytes);
   const int max_half_slab = std::max(std::max(h->N1, h->N2), h->Nk) / 2 * 32;

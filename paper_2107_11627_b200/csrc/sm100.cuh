@@ -158,7 +158,10 @@ P2S_DEV void cluster_sync() {
 P2S_DEV void mbar_arrive_remote(uint64_t* bar, uint32_t cta) {
   uint32_t remote;
   asm volatile("mapa.shared::cluster.u32 %0, %1, %2;" : "=r"(remote) : "r"(smem_u32(bar)), "r"(cta));
-  asm volatile("mbarrier.arrive.release.cluster.shared::cluster.b64 _, [%0];" ::"r"(remote) : "memory");
+  // default .release.cta semantics (as CUTLASS's ClusterBarrier::arrive): the data the arrival
+  // publishes is consumed by the async proxy of the CTA that wrote it (fence.proxy.async on
+  // the writer side), so no cluster-scope memory barrier is needed
+  asm volatile("mbarrier.arrive.shared::cluster.b64 _, [%0];" ::"r"(remote) : "memory");
 }
 // Wait on a barrier that also receives arrivals from the peer CTA (release.cluster on the
 // arriving side). A CTA-scope acquire suffices for the UMMA consumer (as in CUTLASS's 2-SM

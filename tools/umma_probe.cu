@@ -220,7 +220,7 @@ __global__ void __launch_bounds__(384, 1) k_interf(int mode, int iters, unsigned
   tc_fence_after();
   uint32_t tmem = tslot;
   const int w = warp_id();
-  if (w == 0) {
+  if (w == 0 && mode != 3) {
     constexpr uint32_t id = idesc_f16(128, 112);
     const uint32_t sa = smem_u32(smem), sb = smem_u32(smem + 64 * 1024);
     uint64_t ad[4], bd[4];
@@ -235,19 +235,29 @@ __global__ void __launch_bounds__(384, 1) k_interf(int mode, int iters, unsigned
     mbar_wait(&bar, 0);
     long long t1 = clock64();
     if (lane_id() == 0) { cyc[blockIdx.x] = (unsigned long long)(t1 - t0); done = 1; }
-  } else if (mode == 1 && w >= 4) {
+  } else if ((mode == 1 || mode == 3) && w >= 4) {
     // TMEM readers: 8 warps (2 per lane quadrant) reading columns [384, 512)
     int q = w & 3;
     float acc = 0;
+    long long t0 = clock64();
+    unsigned long long nld = 0;
     while (!done) {
       for (int c = 384; c < 512; c += 16) {
         float v[16];
         tmem_ld16(tmem + ((uint32_t)(q * 32) << 16) + c, v);
         tmem_ld_wait();
+        ++nld;
         for (int i = 0; i < 16; ++i) acc += v[i];
       }
     }
+    long long t1 = clock64();
     sink[threadIdx.x] = acc;
+    if (lane_id() == 0 && blockIdx.x == 0) cyc[1000 + w] = (unsigned long long)((t1 - t0) / (nld ? nld : 1));
+  } else if (w == 0 && mode == 3) {
+    // no MMA: let the readers run alone for a while
+    long long t0 = clock64();
+    while (clock64() - t0 < 400000) {}
+    if (lane_id() == 0) { cyc[blockIdx.x] = 400000ull * 3 / 6144; done = 1; }
   } else if (mode == 2 && w >= 4) {
     while (!done) { mbar_try_wait(&bar_never, 0); }
   }
@@ -257,10 +267,10 @@ __global__ void __launch_bounds__(384, 1) k_interf(int mode, int iters, unsigned
 }
 
 static void run_interf(int nsm) {
-  unsigned long long* dc; float* sink; CK(cudaMalloc(&dc, 1024 * 8)); CK(cudaMalloc(&sink, 4096 * 4));
+  unsigned long long* dc; float* sink; CK(cudaMalloc(&dc, 2048 * 8)); CK(cudaMalloc(&sink, 4096 * 4));
   CK(cudaFuncSetAttribute(k_interf, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024));
   const int iters = 6144;
-  for (int mode = 0; mode < 3; ++mode) {
+  for (int mode = 0; mode < 4; ++mode) {
     k_interf<<<nsm, 384, 200 * 1024>>>(mode, iters, dc, sink);
     CK(cudaGetLastError()); CK(cudaDeviceSynchronize());
     k_interf<<<nsm, 384, 200 * 1024>>>(mode, iters, dc, sink);
@@ -268,8 +278,11 @@ static void run_interf(int nsm) {
     std::vector<unsigned long long> c(nsm);
     CK(cudaMemcpy(c.data(), dc, nsm * 8, cudaMemcpyDeviceToHost));
     double mx = 0; for (auto v : c) mx = fmax(mx, (double)v);
-    printf("interference mode=%d (%s): %.1f cyc/mma (floor 56)\\n", mode,
-           mode == 0 ? "alone" : mode == 1 ? "8 warps tcgen05.ld" : "8 warps spin try_wait", mx / iters);
+    unsigned long long ldc[16];
+    CK(cudaMemcpy(ldc, dc + 1000, 16 * 8, cudaMemcpyDeviceToHost));
+    printf("interference mode=%d (%s): %.1f cyc/mma (floor 56); reader cycles per ld16+wait (warp 4): %llu\\n", mode,
+           mode == 0 ? "alone" : mode == 1 ? "8 warps tcgen05.ld" : mode == 2 ? "8 warps spin try_wait" : "readers alone",
+           mx / iters, (mode == 1 || mode == 3) ? ldc[4] : 0ull);
   }
 }
 
