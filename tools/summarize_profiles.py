@@ -1,0 +1,79 @@
+"""Summarise gpurun_out/ ncu captures into profiles/ (committed evidence).
+
+  python tools/summarize_profiles.py <round-tag>
+Writes profiles/<tag>_launches.csv (per-launch device times of one bench invocation),
+profiles/<tag>_launch_shares.txt, profiles/<tag>_ncu_fused.txt (key metrics of one
+--set full capture of k_fused_p2s) and profiles/ncu_fused_summary.json (read by bench.py:
+DRAM bytes per launch for roofline.traffic).
+"""
+import csv
+import json
+import os
+import shutil
+import subprocess
+import sys
+from collections import defaultdict
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+OUT = os.path.join(ROOT, "gpurun_out")
+PROF = os.path.join(ROOT, "profiles")
+tag = sys.argv[1] if len(sys.argv) > 1 else "r01"
+
+# ---- launch list
+rows = list(csv.reader(open(os.path.join(OUT, "launches.csv"))))
+start = next(i for i, r in enumerate(rows) if r and r[0] == "ID")
+hdr = rows[start]
+ki, vi = hdr.index("Kernel Name"), hdr.index("Metric Value")
+tot, cnt = defaultdict(float), defaultdict(int)
+for r in rows[start + 1:]:
+    name = r[ki].split("(")[0]
+    tot[name] += float(r[vi].replace(",", ""))
+    cnt[name] += 1
+shutil.copy(os.path.join(OUT, "launches.csv"), os.path.join(PROF, f"{tag}_launches.csv"))
+ours = {k: v for k, v in tot.items() if k.startswith("p2s::")}
+step_ns = sum(ours.values()) / max(cnt.get("p2s::k_fused_p2s", 1), 1)
+with open(os.path.join(PROF, f"{tag}_launch_shares.txt"), "w") as f:
+    f.write("ncu --metrics gpu__time_duration.sum --clock-control none (cold-cache, serialised launches)\n")
+    f.write("of: python bench.py --steps 5 --warmup 3 --no-cpu-baseline\n\n")
+    for k in sorted(tot, key=lambda k: -tot[k]):
+        f.write(f"{tot[k] / cnt[k] / 1e3:10.1f} us/launch x{cnt[k]:3d}  {k}\n")
+    f.write("\nshare of one p2s_render (our kernels only):\n")
+    for k, v in ours.items():
+        f.write(f"  {k:28s} {v / cnt[k] / step_ns * 100:5.1f} %\n")
+
+# ---- full capture of the fused kernel
+rep = os.path.join(OUT, "prof_fused.ncu-rep")
+raw = subprocess.run(["ncu", "-i", rep, "--page", "raw", "--csv"], capture_output=True, text=True).stdout
+rr = list(csv.reader(raw.splitlines()))
+h, u, v = rr[0], rr[1], rr[2]
+m = {a: (c, b) for a, b, c in zip(h, u, v)}
+want = ["gpu__time_duration.sum", "sm__cycles_elapsed.avg.per_second", "dram__bytes_read.sum",
+        "dram__bytes_write.sum", "sm__pipe_tensor_cycles_active.avg.pct_of_peak_sustained_elapsed",
+        "sm__pipe_tensor_subpipe_hmma_cycles_active.avg.pct_of_peak_sustained_active",
+        "l1tex__data_pipe_tc_wavefronts_mem_shared.sum.pct_of_peak_sustained_elapsed",
+        "l1tex__data_pipe_lsu_wavefronts_mem_shared.sum.pct_of_peak_sustained_elapsed",
+        "lts__t_bytes.sum", "launch__registers_per_thread", "launch__grid_size", "launch__block_size",
+        "launch__cluster_dim_x", "smsp__mem_tensor_reads_op_utcmma_matrix_c.sum",
+        "smsp__mem_tensor_writes_op_utcmma.sum", "launch__shared_mem_per_block_dynamic"]
+lines = []
+for k in want:
+    if k in m:
+        lines.append(f"{k:80s} {m[k][0]:>16s} {m[k][1]}")
+
+
+def to_bytes(val, unit):
+    val = float(val.replace(",", ""))
+    return val * {"byte": 1, "Kbyte": 1e3, "Mbyte": 1e6, "Gbyte": 1e9}.get(unit, 1)
+
+
+dram = to_bytes(*m["dram__bytes_read.sum"]) + to_bytes(*m["dram__bytes_write.sum"])
+with open(os.path.join(PROF, f"{tag}_ncu_fused.txt"), "w") as f:
+    f.write("ncu --set full --clock-control none -k regex:k_fused -s 1 -c 1 (cfg3, one frame)\n\n")
+    f.write("\n".join(lines) + "\n")
+    f.write(f"\nDRAM bytes per launch (read+write): {dram:.0f}\n")
+json.dump({"dram_bytes_per_launch": dram, "source": f"profiles/{tag}_ncu_fused.txt",
+           "kernel": "k_fused_p2s", "workload": "cfg3_512_rgb_K100_S33"},
+          open(os.path.join(PROF, "ncu_fused_summary.json"), "w"), indent=1)
+print(open(os.path.join(PROF, f"{tag}_launch_shares.txt")).read())
+print("\n".join(lines))
+print("dram bytes/launch", dram)
