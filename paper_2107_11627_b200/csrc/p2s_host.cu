@@ -119,10 +119,12 @@ struct p2s_handle {
   int n_ops = 0;
   int stage_bytes, nring, smem_bytes, n_ebuf, scr_col;
   int off_ring, off_a1, off_a2, off_hold, off_e, off_tab, off_const, off_red, off_bar, a1_sbo, a2_sbo, hold_sbo;
-  int l3_hold_ks = 0;
+  int l3_hold_ks = 0, hold_k0 = 0;
+  std::vector<MmaItem> mma_items;
   int sm_count;
   uint8_t* d_stream = nullptr;
   Item* d_items = nullptr;
+  MmaItem* d_mma = nullptr;
   uint32_t* d_steps = nullptr;
   float* d_consts = nullptr;
   float* d_J = nullptr;
@@ -185,6 +187,8 @@ FusedParams make_params(const p2s_handle* h, int B, int C, int H, int W, int mod
   p.smem_bytes = h->smem_bytes;
   p.a1_sbo = h->a1_sbo; p.a2_sbo = h->a2_sbo; p.hold_sbo = h->hold_sbo;
   p.l3_hold_ks = h->l3_hold_ks;
+  p.hold_k0 = h->hold_k0;
+  p.mma_items = h->d_mma;
   p.prof = h->prof;
   for (int i = 0; i < kMaxMaps; ++i) p.maps[i] = h->maps[i];
   p.progressive = h->progressive;
@@ -268,20 +272,24 @@ p2s_status p2s_init(const p2s_basis* basis, const p2s_mlp* mlp, p2s_handle** out
     const int N = layer_N[l];
     const int nch = (N + CH - 1) / CH;
     if (nch > 2 || (l == 2 && nch > 1)) { delete h; return P2S_ERR_UNSUPPORTED; }
-    const int w0 = nch == 1 ? N : std::min(CH, (N / 2 + 15) / 16 * 16 > CH ? CH : 128);
-    int n0 = 0;
-    for (int c = 0; c < nch; ++c) {
-      const int w = nch == 1 ? N : (c == 0 ? w0 : N - w0);
-      h->ops[h->n_ops++] = MlpOp{l, n0, w, layer_K[l] / 16, c == 0, c == nch - 1};
-      n0 += w;
+    const int w0 = nch == 1 ? N : std::min(CH, 128);  // columns [0, w0) and [w0, N)
+    if (nch == 1) {
+      h->ops[h->n_ops++] = MlpOp{l, 0, N, layer_K[l] / 16, 1, 1};
+    } else {
+      // the upper (narrower) chunk goes first: for L2 it is the one parked in the hold buffer
+      // while the lower chunk still reads A2, so the hold buffer is as small as possible
+      h->ops[h->n_ops++] = MlpOp{l, w0, N - w0, layer_K[l] / 16, 1, 0};
+      h->ops[h->n_ops++] = MlpOp{l, 0, w0, layer_K[l] / 16, 0, 1};
     }
   }
 
-  // L2 chunk 0 is parked in a "hold" buffer that L3 reads directly (L2 chunk 1 still reads A2)
-  int hold_cols = 0;
+  // The first-issued L2 chunk is parked in a "hold" buffer that L3 reads directly (the other
+  // L2 chunk still reads A2); L3 K-steps [hold_k0, hold_k0 + hold_cols/16) come from it.
+  int hold_cols = 0, hold_n0 = 0;
   for (int o = 0; o < h->n_ops; ++o)
-    if (h->ops[o].layer == 1 && !h->ops[o].last_of_layer) hold_cols = h->ops[o].N;
+    if (h->ops[o].layer == 1 && !h->ops[o].last_of_layer) { hold_cols = h->ops[o].N; hold_n0 = h->ops[o].n0; }
   h->l3_hold_ks = hold_cols / 16;
+  h->hold_k0 = hold_n0 / 16;
 
   // ---- shared-memory layout (per CTA; identical in both CTAs of a pair)
   const int a1_bytes = kTileM * h->K1 * 2;
@@ -294,8 +302,10 @@ p2s_status p2s_init(const p2s_basis* basis, const p2s_mlp* mlp, p2s_handle** out
   const int red_bytes = 2 * 128 * 16;
   auto al = [](int v) { return (v + 127) / 128 * 128; };
   const int bar_bytes = (BAR_RING + 2 * 4) * 8 + 16;  // BAR_RING fixed barriers + ring
-  const int fixed = al(a1_bytes) + al(a2_bytes) + al(hold_bytes) + al(tab_bytes) + al(const_bytes) +
-                    al(red_bytes) + al(bar_bytes);
+  const bool red_in_hold = hold_bytes >= red_bytes;  // the J reduction buffer reuses the hold buffer
+  const int tab_all = tab_bytes + kMaxItems * (int)sizeof(MmaItem);
+  const int fixed = al(a1_bytes) + al(a2_bytes) + al(std::max(hold_bytes, red_in_hold ? 0 : 0)) + al(tab_all) +
+                    al(const_bytes) + (red_in_hold ? 0 : al(red_bytes)) + al(bar_bytes);
   const int max_half_slab = std::max(std::max(h->N1, h->N2), h->Nk) / 2 * 32;
   int ring_avail = 0;
   h->n_ebuf = 2;
@@ -305,10 +315,12 @@ p2s_status p2s_init(const p2s_basis* basis, const p2s_mlp* mlp, p2s_handle** out
   }
   if (h->n_ebuf < 1) h->n_ebuf = 1;
   ring_avail = kSmemLimit - fixed - al(h->n_ebuf * e1_bytes) - 1024;
-  int nring = 4, sb = 0;
-  for (nring = 4; nring >= 2; --nring) {
-    sb = std::min(32768, (ring_avail / nring) / 512 * 512);
-    if (sb >= 12288 || nring == 2) break;
+  // prefer 3 large stages (fewer ring transitions for the UMMA issuer), else 4, else 2
+  int nring = 3, sb = std::min(32768, (ring_avail / 3) / 512 * 512);
+  if (sb < 16384) {
+    nring = 4;
+    sb = std::min(32768, (ring_avail / 4) / 512 * 512);
+    if (sb < 12288) { nring = 2; sb = std::min(32768, (ring_avail / 2) / 512 * 512); }
   }
   if (sb < max_half_slab) { delete h; return P2S_ERR_UNSUPPORTED; }
   h->nring = nring;
@@ -319,9 +331,13 @@ p2s_status p2s_init(const p2s_basis* basis, const p2s_mlp* mlp, p2s_handle** out
   h->off_a2 = off; off += al(a2_bytes);
   h->off_hold = off; off += al(hold_bytes);
   h->off_e = off; off += al(h->n_ebuf * e1_bytes);
-  h->off_tab = off; off += al(tab_bytes);
+  h->off_tab = off; off += al(tab_all);
   h->off_const = off; off += al(const_bytes);
-  h->off_red = off; off += al(red_bytes);
+  if (red_in_hold) {
+    h->off_red = h->off_hold;
+  } else {
+    h->off_red = off; off += al(red_bytes);
+  }
   h->off_bar = off; off += (BAR_RING + 2 * nring) * 8 + 16;
   h->smem_bytes = off;
   h->a1_sbo = (h->K1 / 8) * 128;
@@ -377,8 +393,15 @@ p2s_status p2s_init(const p2s_basis* basis, const p2s_mlp* mlp, p2s_handle** out
   auto make_items = [&](size_t base, int nks, int N, uint8_t kind, uint8_t op, std::vector<Item>& out) {
     const uint32_t hs = (uint32_t)N * 16, per = std::max<uint32_t>(1, (uint32_t)sb / hs);
     const int mi = map_of(N);
-    for (int s0 = 0; s0 < nks; s0 += per) {
-      const int ns = std::min<int>(per, nks - s0);
+    // L3 items never straddle the hold-buffer / A2 boundary of their A operand
+    const bool is_l3 = kind == 0 && h->ops[op].layer == 2 && h->l3_hold_ks > 0;
+    const int cut0 = h->hold_k0, cut1 = h->hold_k0 + h->l3_hold_ks;
+    for (int s0 = 0; s0 < nks;) {
+      int ns = std::min<int>(per, nks - s0);
+      if (is_l3) {
+        if (s0 < cut0) ns = std::min(ns, cut0 - s0);
+        else if (s0 < cut1) ns = std::min(ns, cut1 - s0);
+      }
       Item it{};
       it.src_off = (uint32_t)(base + (size_t)s0 * hs);
       it.bytes = (uint32_t)ns * hs;
@@ -391,6 +414,7 @@ p2s_status p2s_init(const p2s_basis* basis, const p2s_mlp* mlp, p2s_handle** out
       it.map = (uint8_t)mi;
       it.rows = (uint8_t)(N / 16);
       out.push_back(it);
+      s0 += ns;
     }
   };
   std::vector<Item> conv_items;
@@ -415,6 +439,37 @@ p2s_status p2s_init(const p2s_basis* basis, const p2s_mlp* mlp, p2s_handle** out
   if (h->n_items_full + h->n_items_beta > kMaxItems) { delete h; return P2S_ERR_UNSUPPORTED; }
   h->items = full;
   h->items.insert(h->items.end(), beta.begin(), beta.end());
+  // UMMA-side view of every item (precomputed so the issue loop does one LDS.128 per item)
+  auto mma_of = [&](const Item& it, int mode) {
+    MmaItem mi{};
+    mi.first = it.first;
+    mi.nslabs = (uint8_t)it.nslabs;
+    if (it.kind == 1) {
+      mi.n16 = (uint8_t)(h->Nk / 16);
+      mi.flags = MI_CONV | ((it.flags & IT_BEGIN) ? MI_WAIT_E : 0) | ((it.flags & IT_END) ? MI_COMMIT_ACC : 0);
+      return mi;
+    }
+    const MlpOp& op = h->ops[it.op];
+    mi.n16 = (uint8_t)(op.N / 16);
+    uint32_t off, sbo;
+    if (op.layer == 0) { off = h->off_a1 + it.first * 256; sbo = h->a1_sbo; }
+    else if (op.layer == 2 && h->l3_hold_ks > 0 && it.first >= h->hold_k0 && it.first < h->hold_k0 + h->l3_hold_ks) {
+      off = h->off_hold + (it.first - h->hold_k0) * 256; sbo = h->hold_sbo;
+    } else { off = h->off_a2 + it.first * 256; sbo = h->a2_sbo; }
+    mi.a_lo_rel = (off >> 4) | ((128u >> 4) << 16);
+    mi.a_hi = (sbo >> 4) | (1u << 14);
+    uint16_t f = 0;
+    if (it.flags & IT_BEGIN) f |= (op.layer == 0 && op.first_of_layer) ? MI_WAIT_A1 : MI_WAIT_SCR;
+    if (it.flags & IT_END) {
+      if (op.layer == 0 && op.last_of_layer) f |= MI_COMMIT_A1;
+      if (op.layer < 2) f |= MI_COMMIT_MLP;
+      else if (mode == 1) f |= MI_COMMIT_ACC;
+    }
+    mi.flags = f;
+    return mi;
+  };
+  for (const Item& it : full) h->mma_items.push_back(mma_of(it, 0));
+  for (const Item& it : beta) h->mma_items.push_back(mma_of(it, 1));
 
   // ---- constants: b1, b2 (kMaxN each), b3, svec (128 each), zero padded;
   //      svec[k] = sum of the taps of phi_k (centred-image identity)
@@ -463,6 +518,7 @@ p2s_status p2s_init(const p2s_basis* basis, const p2s_mlp* mlp, p2s_handle** out
     h->n_maps = (int)map_rows.size();
   }
   UP(h->d_items, h->items.data(), h->items.size() * sizeof(Item));
+  UP(h->d_mma, h->mma_items.data(), h->mma_items.size() * sizeof(MmaItem));
   UP(h->d_steps, steps.data(), steps.size() * sizeof(uint32_t));
   UP(h->d_consts, consts.data(), consts.size() * 4);
 #undef UP
@@ -601,7 +657,7 @@ p2s_status p2s_get_info(const p2s_handle* h, p2s_info* info) {
 void p2s_destroy(p2s_handle* h) {
   if (!h) return;
   cudaDeviceSynchronize();
-  cudaFree(h->d_stream); cudaFree(h->d_items); cudaFree(h->d_steps); cudaFree(h->d_consts);
+  cudaFree(h->d_stream); cudaFree(h->d_items); cudaFree(h->d_mma); cudaFree(h->d_steps); cudaFree(h->d_consts);
   cudaFree(h->d_J);
   cudaFree(h->h_img); cudaFree(h->h_z); cudaFree(h->h_t); cudaFree(h->h_out);
   delete h;

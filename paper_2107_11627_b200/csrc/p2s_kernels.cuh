@@ -66,6 +66,23 @@ struct Item {
 };
 static_assert(sizeof(Item) == 24, "Item layout");
 
+// UMMA-issuer view of an item (one LDS.128): A-operand descriptor halves for MLP items (the
+// shared-memory base is added on the device), width, dependency waits and commits.
+enum MmaItemFlags : uint16_t {
+  MI_CONV = 1, MI_WAIT_A1 = 2, MI_WAIT_SCR = 4, MI_WAIT_E = 8,
+  MI_COMMIT_A1 = 16, MI_COMMIT_MLP = 32, MI_COMMIT_ACC = 64
+};
+struct MmaItem {
+  uint32_t a_lo_rel;   // (smem offset >> 4) | (LBO >> 4) << 16, without the smem base
+  uint32_t a_hi;       // SBO >> 4 | version bit
+  uint16_t first;      // first K-step (accumulate = first + j > 0; conv step index)
+  uint8_t nslabs;
+  uint8_t n16;         // N / 16 (UMMA N; B half-slab = N rows/2 * 32 B = 16 N bytes)
+  uint16_t flags;
+  uint16_t pad;
+};
+static_assert(sizeof(MmaItem) == 16, "MmaItem layout");
+
 // One MLP "op" = one output-column chunk of one layer: D[scratch] = A * W[n0:n0+N, :]^T.
 struct MlpOp {
   int layer;          // 0, 1, 2
@@ -88,7 +105,8 @@ struct FusedParams {
   int n_items_full, n_items_beta;
   MlpOp ops[kMaxOps];
   int n_ops;
-  int l3_hold_ks;             // L3 K-steps whose A operand is in the hold buffer (L2 chunk 0)
+  int l3_hold_ks, hold_k0;    // L3 K-steps [hold_k0, hold_k0 + l3_hold_ks) read the hold buffer
+  const MmaItem* mma_items;   // UMMA view of items (same order / modes as `items`)
   const uint32_t* conv_steps; // per conv K-step: descriptor low word (E-relative start>>4 | (LBO>>4)<<16)
   int nconv;
   const float* consts;        // b1[kMaxN] b2[kMaxN] b3[128] svec[128] (zero padded)
@@ -234,7 +252,8 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads)
   uint8_t* sHold = smem + p.off_hold;
   uint8_t* sE = smem + p.off_e;
   Item* sItems = reinterpret_cast<Item*>(smem + p.off_tab);
-  uint32_t* sSteps = reinterpret_cast<uint32_t*>(smem + p.off_tab + kMaxItems * sizeof(Item));
+  MmaItem* sMma = reinterpret_cast<MmaItem*>(smem + p.off_tab + kMaxItems * sizeof(Item));
+  uint32_t* sSteps = reinterpret_cast<uint32_t*>(smem + p.off_tab + kMaxItems * (sizeof(Item) + sizeof(MmaItem)));
   float* sConst = reinterpret_cast<float*>(smem + p.off_const);
   float* sB1 = sConst;
   float* sB2 = sConst + kMaxN;
@@ -262,7 +281,10 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads)
   const Item* gItems = p.items + (p.mode == 0 ? 0 : p.n_items_full);
 
   // ---- setup
-  for (int i = threadIdx.x; i < n_items; i += kThreads) sItems[i] = gItems[i];
+  for (int i = threadIdx.x; i < n_items; i += kThreads) {
+    sItems[i] = gItems[i];
+    sMma[i] = p.mma_items[i + (p.mode == 0 ? 0 : p.n_items_full)];
+  }
   for (int i = threadIdx.x; i < p.nconv; i += kThreads) sSteps[i] = p.conv_steps[i];
   for (int i = threadIdx.x; i < 2 * kMaxN + 256; i += kThreads) sConst[i] = p.consts[i];
   if (threadIdx.x == 0) {
@@ -315,100 +337,91 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads)
     // Descriptors are assembled from precomputed 32-bit halves so the per-UMMA work is one
     // or two uniform adds: lo = start>>4 | (LBO>>4)<<16, hi = SBO>>4 | version(bit 46).
     const uint32_t ring_lo = (smem_u32(ring) >> 4) | ((128u >> 4) << 16);
-    const uint32_t a1_lo = (smem_u32(sA1) >> 4) | ((128u >> 4) << 16);
-    const uint32_t a2_lo = (smem_u32(sA2) >> 4) | ((128u >> 4) << 16);
-    const uint32_t hold_lo = (smem_u32(sHold) >> 4) | ((128u >> 4) << 16);
     const uint32_t e_lo = smem_u32(sE) >> 4;
     const uint32_t hi_b = (256u >> 4) | (1u << 14);
     const uint32_t hi_conv = (128u >> 4) | (1u << 14);
-    const uint32_t hi_a1 = ((uint32_t)p.a1_sbo >> 4) | (1u << 14);
-    const uint32_t hi_a2 = ((uint32_t)p.a2_sbo >> 4) | (1u << 14);
-    const uint32_t hi_hold = ((uint32_t)p.hold_sbo >> 4) | (1u << 14);
     const uint32_t id_conv = idesc_f16(256, p.Nk);
-    const uint32_t conv_half16 = (uint32_t)p.Nk;  // half-slab bytes (16 * Nk) >> 4
     const uint32_t stage16 = (uint32_t)p.stage_bytes >> 4;
     const uint32_t ch16 = (uint32_t)p.chan_bytes >> 4;
     const uint32_t ebuf16 = 3u * ch16;
-    const int C = p.C, nring = p.nring, ebufs = p.n_ebuf, mode = p.mode, l3h = p.l3_hold_ks;
+    const int C = p.C, nring = p.nring, ebufs = p.n_ebuf, mode = p.mode;
     const uint32_t scr = tmem + (uint32_t)p.scr_col;
     const uint32_t acc1 = tmem + (uint32_t)p.Nk, acc2 = tmem + 2u * (uint32_t)p.Nk;
+    const uint32_t smem_lo = smem_u32(smem) >> 4;
+    const uint32_t id_base = idesc_f16(256, 0);
     int s = 0;
     uint32_t ph = 0;
     uint32_t scr_waits = 0;
     uint32_t e_use0 = 0, e_use1 = 0;
-    int it = 0;
+    int pending = -1;  // ring slot whose release commit is deferred behind the next UMMAs
 #ifdef P2S_PROFILE
     prof_acc[11] = globaltimer_ns();
 #endif
-    for (int pr = pr_begin; pr < pr_end; ++pr, ++it) {
+    const int total = (pr_end - pr_begin) * n_items;
+    MmaItem cur = sMma[0];
+    for (int step = 0, it = 0, g = 0; step < total; ++step) {
+      const MmaItem nxt = sMma[g + 1 < n_items ? g + 1 : 0];  // prefetched one item ahead
       const int eb = ebufs == 2 ? (it & 1) : 0;
-      for (int g = 0; g < n_items; ++g) {
-        const Item itm = sItems[g];
-        const uint32_t b_lo0 = ring_lo + (uint32_t)s * stage16;
-        if (itm.kind == 0) {
-          const MlpOp op = p.ops[itm.op];
-          if (itm.flags & IT_BEGIN) {
-            if (op.layer == 0 && op.first_of_layer) {
-              { PROF_T0(); mbar_wait_cluster(&bars[BAR_A1_FULL], it & 1); PROF_ADD(0); }
-              { PROF_T0(); mbar_wait_cluster(&bars[BAR_TMEM_FREE], (it & 1) ^ 1); PROF_ADD(1); }
-            } else {
-              { PROF_T0(); mbar_wait_cluster(&bars[BAR_SCR_FREE], scr_waits & 1); PROF_ADD(2); }
-              ++scr_waits;
-            }
-            tc_fence_after();
-          }
-          { PROF_T0(); mbar_wait(&ring_full[s], ph); PROF_ADD(4); }
-          tc_fence_after();
-          const uint32_t idesc = idesc_f16(256, op.N);
-          const uint32_t half16 = (uint32_t)op.N;  // (16 * N) >> 4
-          const uint32_t n = itm.nslabs;
+      const uint32_t f = cur.flags;
+      if (f & MI_WAIT_A1) {
+        { PROF_T0(); mbar_wait(&bars[BAR_A1_FULL], it & 1); PROF_ADD(0); }
+        { PROF_T0(); mbar_wait(&bars[BAR_TMEM_FREE], (it & 1) ^ 1); PROF_ADD(1); }
+      }
+      if (f & MI_WAIT_SCR) {
+        { PROF_T0(); mbar_wait(&bars[BAR_SCR_FREE], scr_waits & 1); PROF_ADD(2); }
+        ++scr_waits;
+      }
+      if (f & MI_WAIT_E) { PROF_T0(); mbar_wait(&bars[BAR_E_FULL0 + eb], (eb ? e_use1 : e_use0) & 1); PROF_ADD(3); }
+      { PROF_T0(); mbar_wait(&ring_full[s], ph); PROF_ADD(5); }
+      tc_fence_after();
+      const uint32_t b_lo0 = ring_lo + (uint32_t)s * stage16;
+      const uint32_t n = cur.nslabs;
+      const uint32_t half16 = (uint32_t)cur.n16 * 16u;  // (16 * N) >> 4
+      const uint32_t first = cur.first;
+      if (f & MI_CONV) {
+        const uint32_t e0 = e_lo + (uint32_t)eb * ebuf16;
+        const uint32_t* steps = sSteps + first;
 #pragma unroll 2
-          for (uint32_t j = 0; j < n; ++j) {
-            const uint32_t ks = itm.first + j;
-            uint64_t ad;
-            if (op.layer == 0) ad = ((uint64_t)hi_a1 << 32) | (a1_lo + ks * 16u);
-            else if (op.layer == 2 && (int)ks < l3h) ad = ((uint64_t)hi_hold << 32) | (hold_lo + ks * 16u);
-            else ad = ((uint64_t)hi_a2 << 32) | (a2_lo + ks * 16u);
-            const uint64_t bd = ((uint64_t)hi_b << 32) | (b_lo0 + j * half16);
-            umma2_f16_elect(scr, ad, bd, idesc, ks > 0);
-          }
-          umma2_commit_elect(&ring_empty[s]);
-          if (++s == nring) { s = 0; ph ^= 1; }
-          if (itm.flags & IT_END) {
-            if (op.layer == 0 && op.last_of_layer) umma2_commit_elect(&bars[BAR_A1_EMPTY]);
-            if (op.layer < 2) umma2_commit_elect(&bars[BAR_MLP_DONE]);
-            else if (mode == 1) umma2_commit_elect(&bars[BAR_ACC_FULL]);
-          }
-        } else {
-          if (itm.flags & IT_BEGIN) {
-            { PROF_T0(); mbar_wait_cluster(&bars[BAR_E_FULL0 + eb], (eb ? e_use1 : e_use0) & 1); PROF_ADD(3); }
-            tc_fence_after();
-          }
-          { PROF_T0(); mbar_wait(&ring_full[s], ph); PROF_ADD(5); }
-          tc_fence_after();
-          const uint32_t e0 = e_lo + (uint32_t)eb * ebuf16;
-          const uint32_t* steps = sSteps + itm.first;
-          const uint32_t n = itm.nslabs;
-          const uint32_t acc_first = itm.first;
+        for (uint32_t j = 0; j < n; ++j) {
+          const uint32_t a_lo = e0 + steps[j];
+          const uint64_t bd = ((uint64_t)hi_b << 32) | (b_lo0 + j * half16);
+          const uint32_t accum = (first + j) > 0;
+          umma2_f16_elect(tmem, ((uint64_t)hi_conv << 32) | a_lo, bd, id_conv, accum);
+          if (C > 1) umma2_f16_elect(acc1, ((uint64_t)hi_conv << 32) | (a_lo + ch16), bd, id_conv, accum);
+          if (C > 2) umma2_f16_elect(acc2, ((uint64_t)hi_conv << 32) | (a_lo + 2u * ch16), bd, id_conv, accum);
+          if (j == 0 && pending >= 0) { umma2_commit_elect(&ring_empty[pending]); pending = -1; }
+        }
+      } else {
+        const uint32_t idesc = id_base | ((uint32_t)cur.n16 << 18);  // N>>3 at bit 17
+        const uint32_t a_lo0 = smem_lo + cur.a_lo_rel;
 #pragma unroll 2
-          for (uint32_t j = 0; j < n; ++j) {
-            const uint32_t a_lo = e0 + steps[j];
-            const uint64_t bd = ((uint64_t)hi_b << 32) | (b_lo0 + j * conv_half16);
-            const uint32_t accum = (acc_first + j) > 0;
-            umma2_f16_elect(tmem, ((uint64_t)hi_conv << 32) | a_lo, bd, id_conv, accum);
-            if (C > 1) umma2_f16_elect(acc1, ((uint64_t)hi_conv << 32) | (a_lo + ch16), bd, id_conv, accum);
-            if (C > 2) umma2_f16_elect(acc2, ((uint64_t)hi_conv << 32) | (a_lo + 2u * ch16), bd, id_conv, accum);
-          }
-          umma2_commit_elect(&ring_empty[s]);
-          if (++s == nring) { s = 0; ph ^= 1; }
-          if (itm.flags & IT_END) {
-            umma2_commit_elect(&bars[BAR_E_EMPTY0 + eb]);
-            umma2_commit_elect(&bars[BAR_ACC_FULL]);
-            if (eb) ++e_use1; else ++e_use0;
-          }
+        for (uint32_t j = 0; j < n; ++j) {
+          const uint64_t ad = ((uint64_t)cur.a_hi << 32) | (a_lo0 + j * 16u);
+          const uint64_t bd = ((uint64_t)hi_b << 32) | (b_lo0 + j * half16);
+          umma2_f16_elect(scr, ad, bd, idesc, (first + j) > 0);
+          if (j == 0 && pending >= 0) { umma2_commit_elect(&ring_empty[pending]); pending = -1; }
         }
       }
+      // completion signals for the epilogue / builders are not deferred
+      if (f & (MI_COMMIT_A1 | MI_COMMIT_MLP | MI_COMMIT_ACC)) {
+        umma2_commit_elect(&ring_empty[s]);  // keep ring releases in order before a hand-off
+        if (f & MI_COMMIT_A1) umma2_commit_elect(&bars[BAR_A1_EMPTY]);
+        if (f & MI_COMMIT_MLP) umma2_commit_elect(&bars[BAR_MLP_DONE]);
+        if (f & MI_COMMIT_ACC) {
+          if ((f & MI_CONV) && mode == 0) {
+            umma2_commit_elect(&bars[BAR_E_EMPTY0 + eb]);
+            if (eb) ++e_use1; else ++e_use0;
+          }
+          umma2_commit_elect(&bars[BAR_ACC_FULL]);
+        }
+      } else {
+        pending = s;
+      }
+      if (++s == nring) { s = 0; ph ^= 1; }
+      cur = nxt;
+      if (++g == n_items) { g = 0; ++it; }
     }
+    if (pending >= 0) umma2_commit_elect(&ring_empty[pending]);
   } else if (warp >= kWarpBuild0 && warp < kWarpEpi0) {
     // ================= builders: A1 (Zernike tile, fp16) and E views (fp16, centred) =====
     const int tid = threadIdx.x - kWarpBuild0 * 32;

@@ -286,6 +286,67 @@ static void run_interf(int nsm) {
   }
 }
 
+
+// ---- 7. 2-CTA (cluster pair) UMMA throughput: M=256, N=112, A = overlapped E view, B = half per CTA.
+// MODE 0: back-to-back; MODE 1: + multicast commit + try_wait (already complete) every MPS UMMAs.
+template <int MODE, int MPS>
+__global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(128, 1) k_tput2(int iters, unsigned long long* cyc) {
+  extern __shared__ __align__(1024) uint8_t smem[];
+  __shared__ uint64_t bar, bar2;
+  __shared__ uint32_t tslot;
+  for (int i = threadIdx.x * 16; i < 96 * 1024; i += 128 * 16) *reinterpret_cast<int4*>(smem + i) = make_int4(0, 0, 0, 0);
+  fence_proxy_async_smem();
+  if (threadIdx.x == 0) { mbar_init(&bar, 1); mbar_init(&bar2, 1); fence_mbar_init(); }
+  if (warp_id() == 0) tmem_alloc2<512>(&tslot);
+  tc_fence_before();
+  __syncthreads();
+  cluster_sync();
+  tc_fence_after();
+  uint32_t tmem = tslot;
+  const bool leader = cluster_ctarank() == 0;
+  if (warp_id() == 0 && leader) {
+    if (lane_id() == 0) mbar_arrive(&bar2);
+    __syncwarp();
+    constexpr uint32_t id = idesc_f16(256, 112);
+    const uint32_t sa = smem_u32(smem), sb = smem_u32(smem + 64 * 1024);
+    uint64_t ad[4], bd[4];
+#pragma unroll
+    for (int i = 0; i < 4; ++i) { ad[i] = sdesc(sa + i * 16 * 5, 2624, 128); bd[i] = sdesc(sb + i * 2048, 128, 256); }
+    long long t0 = clock64();
+    for (int it = 0; it < iters; it += MPS) {
+      if (MODE == 1) mbar_wait(&bar2, 0);
+#pragma unroll
+      for (int j = 0; j < MPS; ++j) umma2_f16_elect(tmem + (j % 3) * 112, ad[j & 3], bd[(it / MPS) & 3], id, 1);
+      if (MODE == 1) umma2_commit_elect(&bar);
+    }
+    umma2_commit_elect(&bar2);
+    mbar_wait(&bar2, 1);
+    long long t1 = clock64();
+    if (lane_id() == 0) cyc[blockIdx.x] = (unsigned long long)(t1 - t0);
+  }
+  tc_fence_before();
+  __syncthreads();
+  cluster_sync();
+  if (warp_id() == 0) tmem_dealloc2<512>(tmem);
+}
+
+template <int MODE, int MPS>
+static void run_tput2(int nsm) {
+  unsigned long long* dc; CK(cudaMalloc(&dc, 1024 * 8)); CK(cudaMemset(dc, 0, 1024 * 8));
+  auto k = k_tput2<MODE, MPS>;
+  CK(cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024));
+  const int iters = 6144 / MPS * MPS;
+  k<<<nsm, 128, 200 * 1024>>>(iters, dc);
+  CK(cudaGetLastError()); CK(cudaDeviceSynchronize());
+  k<<<nsm, 128, 200 * 1024>>>(iters, dc);
+  CK(cudaGetLastError()); CK(cudaDeviceSynchronize());
+  std::vector<unsigned long long> c(nsm);
+  CK(cudaMemcpy(c.data(), dc, nsm * 8, cudaMemcpyDeviceToHost));
+  double mx = 0; for (auto v : c) mx = fmax(mx, (double)v);
+  printf("2CTA tput M=256 N=112 mode=%d mps=%d: %.1f cyc/mma (floor 56)\n", MODE, MPS, mx / iters);
+  cudaFree(dc);
+}
+
 int main() {
   int fails = 0;
   unsigned s = 12345;
@@ -354,7 +415,8 @@ int main() {
     run_tput<112, 1, 1, 6>(nsm); run_tput<112, 1, 2, 6>(nsm);
     run_tput<208, 0, 0, 2>(nsm); run_tput<64, 0, 0, 4>(nsm);
   }
-  { int nsm = 0; CK(cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, 0)); run_interf(nsm); }
+  { int nsm = 0; CK(cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, 0)); run_interf(nsm);
+    run_tput2<0, 24>(nsm); run_tput2<1, 24>(nsm); run_tput2<1, 12>(nsm); run_tput2<1, 48>(nsm); }
   // ---- 5. TMEM load throughput
   {
     unsigned long long* dc; float* sink; CK(cudaMalloc(&dc, 8)); CK(cudaMalloc(&sink, 1024 * 4));
