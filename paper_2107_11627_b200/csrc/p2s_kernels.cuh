@@ -209,8 +209,9 @@ __device__ __forceinline__ void build_E(const FusedParams& p, uint8_t* Ec, const
     const int rot = (g >> 1) & 3;
 #pragma unroll
     for (int e = 0; e < 4; ++e) {
-      const int ee = (e + rot) & 3;
-      *reinterpret_cast<uint4*>(dst + ee * 16) = pk[ee];
+      const int ee = (e + rot) & 3;  // register select, not a dynamically indexed local array
+      const uint4 v01 = (ee & 1) ? pk[1] : pk[0], v23 = (ee & 1) ? pk[3] : pk[2];
+      *reinterpret_cast<uint4*>(dst + ee * 16) = (ee & 2) ? v23 : v01;
     }
   }
   const int ngx = p.npos_x >> 2;
@@ -579,9 +580,11 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads)
           const float4 o = red[m];
           bs += o.w;
           jc[0] += o.x; jc[1] += o.y; jc[2] += o.z;
-          if (store && x < p.W)
-            for (int c = 0; c < C; ++c)
-              p.J[((size_t)b * C + c) * HW + (size_t)y * p.W + x] = fmaf(0.5f, bs, jc[c]);
+          if (store && x < p.W) {
+#pragma unroll
+            for (int c = 0; c < 3; ++c)
+              if (c < C) p.J[((size_t)b * C + c) * HW + (size_t)y * p.W + x] = fmaf(0.5f, bs, jc[c]);
+          }
         }
       }
       if (p.mode == 1) {
