@@ -114,7 +114,7 @@ struct p2s_handle {
   int K, S, r, n_in, h1, h2, Nk, K1, N1, N2;
   ConvPlan plan;
   std::vector<Item> items;  // [items_full | items_beta]
-  int n_items_full = 0, n_items_beta = 0;
+  int n_items_full = 0, n_items_beta = 0, n_items_first = 0, tab_cap = 0;
   MlpOp ops[kMaxOps];
   int n_ops = 0;
   int stage_bytes, nring, smem_bytes, n_ebuf, scr_col;
@@ -167,6 +167,10 @@ FusedParams make_params(const p2s_handle* h, int B, int C, int H, int W, int mod
   p.items = h->d_items;
   p.n_items_full = h->n_items_full;
   p.n_items_beta = h->n_items_beta;
+  p.n_items_first = h->n_items_first;
+  p.tab_cap = h->tab_cap;
+  p.off_mma = h->off_tab + h->tab_cap * (int)sizeof(Item);
+  p.off_steps = p.off_mma + h->tab_cap * (int)sizeof(MmaItem);
   for (int i = 0; i < h->n_ops; ++i) p.ops[i] = h->ops[i];
   p.n_ops = h->n_ops;
   p.conv_steps = h->d_steps;
@@ -291,38 +295,69 @@ p2s_status p2s_init(const p2s_basis* basis, const p2s_mlp* mlp, p2s_handle** out
   h->l3_hold_ks = hold_cols / 16;
   h->hold_k0 = hold_n0 / 16;
 
-  // ---- shared-memory layout (per CTA; identical in both CTAs of a pair)
+  // ---- shared-memory layout (per CTA; identical in both CTAs of a pair). The item tables are
+  //      sized from the number of ring stages, which depends on the stage size: iterate.
   const int a1_bytes = kTileM * h->K1 * 2;
   const int kh = std::max(h->N1, h->N2);
   const int a2_bytes = kTileM * kh * 2;
   const int hold_bytes = kTileM * hold_cols * 2;
   const int e1_bytes = 3 * P.chan_bytes;
-  const int tab_bytes = kMaxItems * (int)sizeof(Item) + nconv * 4;
   const int const_bytes = (2 * kMaxN + 256) * 4;
   const int red_bytes = 2 * 128 * 16;
   auto al = [](int v) { return (v + 127) / 128 * 128; };
   const int bar_bytes = (BAR_RING + 2 * 4) * 8 + 16;  // BAR_RING fixed barriers + ring
   const bool red_in_hold = hold_bytes >= red_bytes;  // the J reduction buffer reuses the hold buffer
-  const int tab_all = tab_bytes + kMaxItems * (int)sizeof(MmaItem);
-  const int fixed = al(a1_bytes) + al(a2_bytes) + al(std::max(hold_bytes, red_in_hold ? 0 : 0)) + al(tab_all) +
-                    al(const_bytes) + (red_in_hold ? 0 : al(red_bytes)) + al(bar_bytes);
   const int max_half_slab = std::max(std::max(h->N1, h->N2), h->Nk) / 2 * 32;
-  int ring_avail = 0;
-  h->n_ebuf = 2;
-  for (; h->n_ebuf >= 1; --h->n_ebuf) {
+  // number of ring stages of one op / of the conv for stage size sb (mirrors make_items below)
+  auto count_stages = [&](int sb, int nks, int N, bool l3) {
+    const int per = std::max(1, sb / (N * 16));
+    int n = 0;
+    for (int s0 = 0; s0 < nks;) {
+      int ns = std::min(per, nks - s0);
+      if (l3) {
+        const int c0 = h->hold_k0, c1 = h->hold_k0 + h->l3_hold_ks;
+        if (s0 < c0) ns = std::min(ns, c0 - s0);
+        else if (s0 < c1) ns = std::min(ns, c1 - s0);
+      }
+      s0 += ns;
+      ++n;
+    }
+    return n;
+  };
+  auto table_need = [&](int sb) {
+    int mlp = 0;
+    for (int o = 0; o < h->n_ops; ++o)
+      mlp += count_stages(sb, h->ops[o].nks, h->ops[o].N, h->ops[o].layer == 2 && h->l3_hold_ks > 0);
+    const int full = mlp + count_stages(sb, nconv, h->Nk, false);
+    return std::max(2 * full, 2 * mlp);  // [first | steady] or [beta | beta]
+  };
+  int tab_cap = 48, sb = 0, nring = 3;
+  for (int iter = 0; iter < 6; ++iter) {
+    const int tab_all = tab_cap * (int)(sizeof(Item) + sizeof(MmaItem)) + nconv * 4;
+    const int fixed = al(a1_bytes) + al(a2_bytes) + al(hold_bytes) + al(tab_all) + al(const_bytes) +
+                      (red_in_hold ? 0 : al(red_bytes)) + al(bar_bytes);
+    int ring_avail = 0;
+    for (h->n_ebuf = 2; h->n_ebuf >= 1; --h->n_ebuf) {
+      ring_avail = kSmemLimit - fixed - al(h->n_ebuf * e1_bytes) - 1024;
+      if (ring_avail >= 3 * 12288) break;
+    }
+    if (h->n_ebuf < 1) h->n_ebuf = 1;
     ring_avail = kSmemLimit - fixed - al(h->n_ebuf * e1_bytes) - 1024;
-    if (ring_avail >= 3 * 12288) break;
+    // prefer 3 large stages (fewer ring transitions for the UMMA issuer), else 4, else 2
+    nring = 3;
+    sb = std::min(32768, (ring_avail / 3) / 512 * 512);
+    if (sb < 16384) {
+      nring = 4;
+      sb = std::min(32768, (ring_avail / 4) / 512 * 512);
+      if (sb < 12288) { nring = 2; sb = std::min(32768, (ring_avail / 2) / 512 * 512); }
+    }
+    if (sb < max_half_slab) { delete h; return P2S_ERR_UNSUPPORTED; }
+    const int need = table_need(sb);
+    if (need <= tab_cap) break;
+    tab_cap = (need + 7) / 8 * 8;
   }
-  if (h->n_ebuf < 1) h->n_ebuf = 1;
-  ring_avail = kSmemLimit - fixed - al(h->n_ebuf * e1_bytes) - 1024;
-  // prefer 3 large stages (fewer ring transitions for the UMMA issuer), else 4, else 2
-  int nring = 3, sb = std::min(32768, (ring_avail / 3) / 512 * 512);
-  if (sb < 16384) {
-    nring = 4;
-    sb = std::min(32768, (ring_avail / 4) / 512 * 512);
-    if (sb < 12288) { nring = 2; sb = std::min(32768, (ring_avail / 2) / 512 * 512); }
-  }
-  if (sb < max_half_slab) { delete h; return P2S_ERR_UNSUPPORTED; }
+  if (table_need(sb) > tab_cap) { delete h; return P2S_ERR_UNSUPPORTED; }
+  h->tab_cap = tab_cap;
   h->nring = nring;
   h->stage_bytes = sb;
   int off = 0;
@@ -331,7 +366,7 @@ p2s_status p2s_init(const p2s_basis* basis, const p2s_mlp* mlp, p2s_handle** out
   h->off_a2 = off; off += al(a2_bytes);
   h->off_hold = off; off += al(hold_bytes);
   h->off_e = off; off += al(h->n_ebuf * e1_bytes);
-  h->off_tab = off; off += al(tab_all);
+  h->off_tab = off; off += al(tab_cap * (int)(sizeof(Item) + sizeof(MmaItem)) + nconv * 4);
   h->off_const = off; off += al(const_bytes);
   if (red_in_hold) {
     h->off_red = h->off_hold;
@@ -434,11 +469,21 @@ p2s_status p2s_init(const p2s_basis* basis, const p2s_mlp* mlp, p2s_handle** out
       for (int k = 0; k < per_gap && ci + 1 < conv_items.size(); ++k) full.push_back(conv_items[ci++]);
   }
   while (ci < conv_items.size()) full.push_back(conv_items[ci++]);
+  // First tile of every CTA: all MLP ops before the conv stages (the epilogue is idle then and
+  // the MLP phase overlaps the builders' first im2col views); later tiles interleave.
+  std::vector<Item> first;
+  for (const Item& it : full) if (it.kind == 0) first.push_back(it);
+  for (const Item& it : full) if (it.kind == 1) first.push_back(it);
   h->n_items_full = (int)full.size();
   h->n_items_beta = (int)beta.size();
-  if (h->n_items_full + h->n_items_beta > kMaxItems) { delete h; return P2S_ERR_UNSUPPORTED; }
+  h->n_items_first = (int)first.size();
+  if (h->n_items_full + h->n_items_first > h->tab_cap || 2 * h->n_items_beta > h->tab_cap) {
+    delete h;
+    return P2S_ERR_UNSUPPORTED;
+  }
   h->items = full;
   h->items.insert(h->items.end(), beta.begin(), beta.end());
+  h->items.insert(h->items.end(), first.begin(), first.end());
   // UMMA-side view of every item (precomputed so the issue loop does one LDS.128 per item)
   auto mma_of = [&](const Item& it, int mode) {
     MmaItem mi{};
@@ -470,6 +515,7 @@ p2s_status p2s_init(const p2s_basis* basis, const p2s_mlp* mlp, p2s_handle** out
   };
   for (const Item& it : full) h->mma_items.push_back(mma_of(it, 0));
   for (const Item& it : beta) h->mma_items.push_back(mma_of(it, 1));
+  for (const Item& it : first) h->mma_items.push_back(mma_of(it, 0));
 
   // ---- constants: b1, b2 (kMaxN each), b3, svec (128 each), zero padded;
   //      svec[k] = sum of the taps of phi_k (centred-image identity)

@@ -43,7 +43,6 @@ constexpr int kNumEpiWarps = 8;
 constexpr int kThreads = 32 * (kWarpEpi0 + kNumEpiWarps);  // 448
 constexpr int kBuildThreads = 32 * kNumBuildWarps;
 constexpr uint32_t kTmemCols = 512;
-constexpr int kMaxItems = 80;        // per-tile item list capacity (both modes together)
 constexpr int kMaxConvSteps = 512;
 constexpr int kMaxOps = 6;
 constexpr int kMaxEy = 16, kMaxEx = 4;
@@ -101,8 +100,10 @@ struct FusedParams {
   int B, C, H, W, n_in;
   int nstrips, ntiles, mode;  // mode 0: MLP + conv -> J ; mode 1: MLP only -> beta
   const uint8_t* stream;
-  const Item* items;          // [items_full | items_beta]
-  int n_items_full, n_items_beta;
+  const Item* items;          // [items_full | items_beta | items_first]
+  int n_items_full, n_items_beta, n_items_first;
+  int tab_cap;                // entries of the shared-memory item tables
+  int off_mma, off_steps;     // byte offsets of the MmaItem and conv-step tables
   MlpOp ops[kMaxOps];
   int n_ops;
   int l3_hold_ks, hold_k0;    // L3 K-steps [hold_k0, hold_k0 + l3_hold_ks) read the hold buffer
@@ -253,8 +254,8 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads)
   uint8_t* sHold = smem + p.off_hold;
   uint8_t* sE = smem + p.off_e;
   Item* sItems = reinterpret_cast<Item*>(smem + p.off_tab);
-  MmaItem* sMma = reinterpret_cast<MmaItem*>(smem + p.off_tab + kMaxItems * sizeof(Item));
-  uint32_t* sSteps = reinterpret_cast<uint32_t*>(smem + p.off_tab + kMaxItems * (sizeof(Item) + sizeof(MmaItem)));
+  MmaItem* sMma = reinterpret_cast<MmaItem*>(smem + p.off_mma);
+  uint32_t* sSteps = reinterpret_cast<uint32_t*>(smem + p.off_steps);
   float* sConst = reinterpret_cast<float*>(smem + p.off_const);
   float* sB1 = sConst;
   float* sB2 = sConst + kMaxN;
@@ -271,7 +272,11 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads)
   const int ncl = gridDim.x >> 1, cl = blockIdx.x >> 1;
   const int pr_begin = (int)(((long long)cl * npairs) / ncl);
   const int pr_end = (int)(((long long)(cl + 1) * npairs) / ncl);
-  const int n_items = p.mode == 0 ? p.n_items_full : p.n_items_beta;
+  // per-tile item lists: tile 0 of this CTA uses list A (MLP first), later tiles list B
+  const int nA = p.mode == 0 ? p.n_items_first : p.n_items_beta;
+  const int nB = p.mode == 0 ? p.n_items_full : p.n_items_beta;
+  const int offA = p.mode == 0 ? p.n_items_full + p.n_items_beta : p.n_items_full;
+  const int offB = p.mode == 0 ? 0 : p.n_items_full;
 #ifdef P2S_PROFILE
   unsigned long long prof_acc[20];
 #pragma unroll
@@ -279,12 +284,12 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads)
   const long long prof_start = clock64();
   prof_acc[10] = globaltimer_ns();
 #endif
-  const Item* gItems = p.items + (p.mode == 0 ? 0 : p.n_items_full);
 
   // ---- setup
-  for (int i = threadIdx.x; i < n_items; i += kThreads) {
-    sItems[i] = gItems[i];
-    sMma[i] = p.mma_items[i + (p.mode == 0 ? 0 : p.n_items_full)];
+  for (int i = threadIdx.x; i < nA + nB; i += kThreads) {
+    const int src = i < nA ? offA + i : offB + (i - nA);
+    sItems[i] = p.items[src];
+    sMma[i] = p.mma_items[src];
   }
   for (int i = threadIdx.x; i < p.nconv; i += kThreads) sSteps[i] = p.conv_steps[i];
   for (int i = threadIdx.x; i < 2 * kMaxN + 256; i += kThreads) sConst[i] = p.consts[i];
@@ -320,8 +325,9 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads)
       int s = 0;
       uint32_t ph = 0;
       for (int pr = pr_begin; pr < pr_end; ++pr) {
+        const int n_items = pr == pr_begin ? nA : nB, base = pr == pr_begin ? 0 : nA;
         for (int g = 0; g < n_items; ++g) {
-          const Item it = sItems[g];
+          const Item it = sItems[base + g];
           { PROF_T0(); mbar_wait(&ring_empty[s], ph ^ 1); PROF_ADD(7); }
           if (leader) mbar_arrive_expect_tx(&ring_full[s], 2u * it.bytes);
           const uint32_t mb = cluster_addr(&ring_full[s], 0);
@@ -358,10 +364,12 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads)
 #ifdef P2S_PROFILE
     prof_acc[11] = globaltimer_ns();
 #endif
-    const int total = (pr_end - pr_begin) * n_items;
+    const int total = pr_end > pr_begin ? nA + (pr_end - pr_begin - 1) * nB : 0;
     MmaItem cur = sMma[0];
     for (int step = 0, it = 0, g = 0; step < total; ++step) {
-      const MmaItem nxt = sMma[g + 1 < n_items ? g + 1 : 0];  // prefetched one item ahead
+      const int n_items = it == 0 ? nA : nB;
+      // prefetch the next item (sMma holds list A then list B)
+      const MmaItem nxt = sMma[g + 1 < n_items ? (it == 0 ? g + 1 : nA + g + 1) : nA];
       const int eb = ebufs == 2 ? (it & 1) : 0;
       const uint32_t f = cur.flags;
       if (f & MI_WAIT_A1) {

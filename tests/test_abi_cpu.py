@@ -86,3 +86,8 @@ def test_sass_has_tcgen05_and_tma(lib):
     for mnem in ("UTCHMMA.2CTA", "LDTM", "UTMALDG"):
         assert mnem in sass, mnem
     assert "HMMA" not in sass.replace("UTCHMMA", "")
+    # the UMMA issue loop must stay on the uniform datapath: descriptors in uniform registers,
+    # no per-UMMA divergence/elect loops (a silent 1.5x slowdown when uniformity is lost)
+    fused = sass[sass.index("k_fused_p2s"):]
+    fused = fused[:fused.index("Function :")] if "Function :" in fused else fused
+    assert "R2UR.BROADCAST" not in fused
