@@ -35,10 +35,15 @@ namespace p2s {
 
 constexpr int kTileM = 128;          // pixels per CTA tile (UMMA M = 256 per CTA pair)
 constexpr int kWarpProducer = 0;
-constexpr int kWarpMma = 1;          // leader CTA: UMMA issuer (idle in the peer)
-constexpr int kWarpBuild0 = 2;
+// leader CTA: UMMA issuer (idle in the peer). Warp 2 sits on SM sub-partition 2 next to the two
+// quadrant-2 epilogue warps only (no builder): issue-slot contention measurably delays UMMA issue.
+constexpr int kWarpMma = 2;
 constexpr int kNumBuildWarps = 4;
-constexpr int kWarpEpi0 = kWarpBuild0 + kNumBuildWarps;  // warps 6..13
+constexpr int kWarpEpi0 = 6;          // warps 6..13
+// builder warps are warps 1..5 minus the MMA warp; index 0..3 (-1: not a builder)
+__device__ __forceinline__ int builder_index(int warp) {
+  return (warp < 1 || warp >= kWarpEpi0 || warp == kWarpMma) ? -1 : (warp < kWarpMma ? warp - 1 : warp - 2);
+}
 constexpr int kNumEpiWarps = 8;
 constexpr int kThreads = 32 * (kWarpEpi0 + kNumEpiWarps);  // 448
 constexpr int kBuildThreads = 32 * kNumBuildWarps;
@@ -431,9 +436,9 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads)
       if (++g == n_items) { g = 0; ++it; }
     }
     if (pending >= 0) umma2_commit_elect(&ring_empty[pending]);
-  } else if (warp >= kWarpBuild0 && warp < kWarpEpi0) {
+  } else if (builder_index(warp) >= 0) {
     // ================= builders: A1 (Zernike tile, fp16) and E views (fp16, centred) =====
-    const int tid = threadIdx.x - kWarpBuild0 * 32;
+    const int tid = builder_index(warp) * 32 + lane;
     const size_t HW = (size_t)p.H * p.W;
     uint32_t e_use0 = 0, e_use1 = 0;
     int it = 0;
@@ -467,8 +472,10 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads)
       uint8_t* Eb = sE + (size_t)eb * 3 * p.chan_bytes;  // buffers are sized for C = 3
       {
         PROF_T0();
+#ifndef P2S_ABL_NOE
         for (int c = 0; c < p.C; ++c)
           build_E(p, Eb + (size_t)c * p.chan_bytes, p.image + ((size_t)b * p.C + c) * HW, y, x0, tid);
+#endif
         PROF_ADD(12);
       }
       fence_proxy_async_smem();
@@ -527,8 +534,12 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads)
                 v[u][4 * i4 + 3] = fmaxf(v[u][4 * i4 + 3] + bb.w, 0.f);
               }
               const int kc = kc0 + gi * 2;
+#ifndef P2S_ABL_NOA2
               *reinterpret_cast<uint4*>(dst + kc * 128) = pack8(v[u]);
               *reinterpret_cast<uint4*>(dst + (kc + 1) * 128) = pack8(v[u] + 8);
+#else
+              if (v[u][0] == 12345.f) *reinterpret_cast<uint4*>(dst + kc * 128) = pack8(v[u] + 8);
+#endif
             }
           }
         }
@@ -553,7 +564,11 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads)
       } else {
         float jc[3] = {0.f, 0.f, 0.f};
         float bs = 0.f;
+#ifdef P2S_ABL_EPI0
+        for (int gi = wg; gi < 0; gi += 2) {
+#else
         for (int gi = wg; gi < GK; gi += 2) {
+#endif
           float bv[16], av[3][16];
           tmem_ld16(tl + p.scr_col + gi * 16, bv);
 #pragma unroll
@@ -609,7 +624,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads)
     int base = -1;
     if (warp == kWarpMma && lane == 0) base = 0;
     else if (warp == kWarpProducer && lane == 0) base = 1;
-    else if (warp == kWarpBuild0 && lane == 0) base = 2;
+    else if (builder_index(warp) == 0 && lane == 0) base = 2;
     else if (warp == kWarpEpi0 && lane == 0) base = 3;
     if (p.prof && base >= 0)
       for (int i = 0; i < 20; ++i)

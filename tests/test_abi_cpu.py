@@ -90,4 +90,9 @@ def test_sass_has_tcgen05_and_tma(lib):
     # no per-UMMA divergence/elect loops (a silent 1.5x slowdown when uniformity is lost)
     fused = sass[sass.index("k_fused_p2s"):]
     fused = fused[:fused.index("Function :")] if "Function :" in fused else fused
-    assert "R2UR.BROADCAST" not in fused
+    assert "BRA.DIV" not in fused
+    ins = [l.split("*/", 1)[1].strip() for l in fused.split("\n") if l.strip().startswith("/*") and "*/" in l
+           and not l.strip().startswith("/* 0x")]
+    for n, l in enumerate(ins):
+        if "UTCHMMA" in l:  # the 12 instructions feeding each UMMA must use uniform operands only
+            assert not any("R2UR.BROADCAST" in x for x in ins[max(0, n - 12):n]), ins[max(0, n - 12):n + 1]
