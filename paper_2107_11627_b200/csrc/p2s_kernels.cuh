@@ -130,6 +130,21 @@ struct FusedParams {
   int progressive;            // 1: release beta / each conv accumulator as soon as it is read
 };
 
+#ifdef P2S_SLEEP_BUILD
+#define WAIT_BUILD(bar, par) mbar_wait_sleep(bar, par, P2S_SLEEP_BUILD)
+#else
+#define WAIT_BUILD(bar, par) mbar_wait(bar, par)
+#endif
+#ifdef P2S_SLEEP_EPI
+#define WAIT_EPI(bar, par) mbar_wait_sleep(bar, par, P2S_SLEEP_EPI)
+#else
+#define WAIT_EPI(bar, par) mbar_wait(bar, par)
+#endif
+#ifdef P2S_SLEEP_PROD
+#define WAIT_PROD(bar, par) mbar_wait_sleep(bar, par, P2S_SLEEP_PROD)
+#else
+#define WAIT_PROD(bar, par) mbar_wait(bar, par)
+#endif
 #ifdef P2S_PROFILE
 #define PROF_T0() const long long _pt0 = clock64()
 #define PROF_ADD(slot) prof_acc[slot] += (unsigned long long)(clock64() - _pt0)
@@ -163,6 +178,22 @@ __device__ __forceinline__ void tile_coords(const FusedParams& p, int t, int& b,
   const int s = rem / p.H;
   y = rem - s * p.H;
   x0 = s * kTileM;
+}
+
+// fp32x2 -> fp16x2 (cvt.rn), then max(., 0) in fp16x2
+__device__ __forceinline__ uint32_t relu_half2(float2 a) {
+  __half2 h = __hmax2(__float22half2_rn(a), __float2half2_rn(0.f));
+  return *reinterpret_cast<uint32_t*>(&h);
+}
+
+// 8 fp32 image samples -> centred fp16 (x - 0.5 in fp32x2, then cvt.rn to fp16x2)
+__device__ __forceinline__ uint32_t centred_half2(float a, float b) {
+  __half2 h = __float22half2_rn(__fadd2_rn(make_float2(a, b), make_float2(-0.5f, -0.5f)));
+  return *reinterpret_cast<uint32_t*>(&h);
+}
+__device__ __forceinline__ uint4 pack8_centred(const float* v) {
+  return make_uint4(centred_half2(v[0], v[1]), centred_half2(v[2], v[3]), centred_half2(v[4], v[5]),
+                    centred_half2(v[6], v[7]));
 }
 
 __device__ __forceinline__ uint4 pack8(const float* v) {
@@ -207,11 +238,7 @@ __device__ __forceinline__ void build_E(const FusedParams& p, uint8_t* Ec, const
     uint8_t* dst = Ec + (size_t)blk * p.npos_y * 16 + (size_t)(4 * g) * 16;
     uint4 pk[4];
 #pragma unroll
-    for (int e = 0; e < 4; ++e) {
-#pragma unroll
-      for (int j = 0; j < 8; ++j) v[e][j] -= 0.5f;
-      pk[e] = pack8(v[e]);
-    }
+    for (int e = 0; e < 4; ++e) pk[e] = pack8_centred(v[e]);
     const int rot = (g >> 1) & 3;
 #pragma unroll
     for (int e = 0; e < 4; ++e) {
@@ -238,11 +265,41 @@ __device__ __forceinline__ void build_E(const FusedParams& p, uint8_t* Ec, const
 #pragma unroll
       for (int q = 0; q < 12; ++q) v[q] = __ldg(row + clampi(col0 + q, 0, p.W - 1));
     }
-#pragma unroll
-    for (int q = 0; q < 12; ++q) v[q] -= 0.5f;
     uint8_t* dst = xb + (size_t)e * p.npos_x * 16 + (size_t)(4 * g) * 16;
 #pragma unroll
-    for (int s = 0; s < 4; ++s) *reinterpret_cast<uint4*>(dst + s * 16) = pack8(v + s);
+    for (int s = 0; s < 4; ++s) *reinterpret_cast<uint4*>(dst + s * 16) = pack8_centred(v + s);
+  }
+}
+
+// One 16-column group of the conv epilogue (Eq. 5 reduction): NC real columns of beta (scratch)
+// and of each channel's accumulator, fp32x2 FMAs into jc2 (sum_k beta_k C_k) and bs2
+// (sum_k beta_k s_k for the centring term).
+template <int NC>
+__device__ __forceinline__ void conv_epi_group(uint32_t tl, int scr_col, int Nk, int gi, int C,
+                                               const float* sB3, const float* sSv, float2 (&jc2)[3],
+                                               float2& bs2) {
+  float bv[NC], av[3][NC];
+  tmem_ld_n<NC>(tl + scr_col + gi * 16, bv);
+#pragma unroll
+  for (int c = 0; c < 3; ++c)
+    if (c < C) tmem_ld_n<NC>(tl + c * Nk + gi * 16, av[c]);
+  tmem_ld_wait();
+  const float4* b34 = reinterpret_cast<const float4*>(sB3 + gi * 16);
+  const float4* sv4 = reinterpret_cast<const float4*>(sSv + gi * 16);
+#pragma unroll
+  for (int i4 = 0; i4 < NC / 4; ++i4) {
+    const float4 b3 = b34[i4], sv = sv4[i4];
+    const int i = 4 * i4;
+    const float2 be0 = __fadd2_rn(make_float2(bv[i], bv[i + 1]), make_float2(b3.x, b3.y));
+    const float2 be1 = __fadd2_rn(make_float2(bv[i + 2], bv[i + 3]), make_float2(b3.z, b3.w));
+    bs2 = __ffma2_rn(be0, make_float2(sv.x, sv.y), bs2);
+    bs2 = __ffma2_rn(be1, make_float2(sv.z, sv.w), bs2);
+#pragma unroll
+    for (int c = 0; c < 3; ++c)
+      if (c < C) {
+        jc2[c] = __ffma2_rn(be0, make_float2(av[c][i], av[c][i + 1]), jc2[c]);
+        jc2[c] = __ffma2_rn(be1, make_float2(av[c][i + 2], av[c][i + 3]), jc2[c]);
+      }
   }
 }
 
@@ -323,6 +380,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads)
   const uint32_t tmem = *tmem_slot;
 
   if (warp == kWarpProducer) {
+#ifndef P2S_ABL_NOTMA
     // ================= producer: TMA this CTA's half of every slab into the ring; both CTAs'
     // copies complete on the leader's ring_full (the leader arms it with both halves' bytes)
     if (lane == 0) {
@@ -333,7 +391,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads)
         const int n_items = pr == pr_begin ? nA : nB, base = pr == pr_begin ? 0 : nA;
         for (int g = 0; g < n_items; ++g) {
           const Item it = sItems[base + g];
-          { PROF_T0(); mbar_wait(&ring_empty[s], ph ^ 1); PROF_ADD(7); }
+          { PROF_T0(); WAIT_PROD(&ring_empty[s], ph ^ 1); PROF_ADD(7); }
           if (leader) mbar_arrive_expect_tx(&ring_full[s], 2u * it.bytes);
           const uint32_t mb = cluster_addr(&ring_full[s], 0);
           const int y0 = (int)((it.src_off + rank * it.half_stride) >> 8);
@@ -344,6 +402,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads)
         }
       }
     }
+#endif
   } else if (warp == kWarpMma && leader) {
     // ================= leader: UMMA issuer (whole warp, uniform values; one lane issues) ====
     // Descriptors are assembled from precomputed 32-bit halves so the per-UMMA work is one
@@ -377,6 +436,9 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads)
       const MmaItem nxt = sMma[g + 1 < n_items ? (it == 0 ? g + 1 : nA + g + 1) : nA];
       const int eb = ebufs == 2 ? (it & 1) : 0;
       const uint32_t f = cur.flags;
+#ifdef P2S_PROFILE
+      const long long tr_a = clock64();
+#endif
       if (f & MI_WAIT_A1) {
         { PROF_T0(); mbar_wait(&bars[BAR_A1_FULL], it & 1); PROF_ADD(0); }
         { PROF_T0(); mbar_wait(&bars[BAR_TMEM_FREE], (it & 1) ^ 1); PROF_ADD(1); }
@@ -386,13 +448,23 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads)
         ++scr_waits;
       }
       if (f & MI_WAIT_E) { PROF_T0(); mbar_wait(&bars[BAR_E_FULL0 + eb], (eb ? e_use1 : e_use0) & 1); PROF_ADD(3); }
+#ifndef P2S_ABL_NOTMA
       { PROF_T0(); mbar_wait(&ring_full[s], ph); PROF_ADD(5); }
+#endif
       tc_fence_after();
+#ifdef P2S_PROFILE
+      const long long tr_b = clock64();
+#endif
       const uint32_t b_lo0 = ring_lo + (uint32_t)s * stage16;
       const uint32_t n = cur.nslabs;
       const uint32_t half16 = (uint32_t)cur.n16 * 16u;  // (16 * N) >> 4
       const uint32_t first = cur.first;
+#if defined(P2S_ABL_NOCONVMMA)
+      if ((f & MI_CONV) && n == 0) {
+#else
       if (f & MI_CONV) {
+#endif
+        PROF_T0();
         const uint32_t e0 = e_lo + (uint32_t)eb * ebuf16;
         const uint32_t* steps = sSteps + first;
 #pragma unroll 2
@@ -405,7 +477,17 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads)
           if (C > 2) umma2_f16_elect(acc2, ((uint64_t)hi_conv << 32) | (a_lo + 2u * ch16), bd, id_conv, accum);
           if (j == 0 && pending >= 0) { umma2_commit_elect(&ring_empty[pending]); pending = -1; }
         }
+        PROF_ADD(4);
+#if defined(P2S_ABL_NOCONVMMA)
+      } else if (!(f & MI_CONV)) {
+#else
       } else {
+#endif
+#ifdef P2S_ABL_NOMLPMMA
+        if (n == 0)
+#endif
+        {
+        PROF_T0();
         const uint32_t idesc = id_base | ((uint32_t)cur.n16 << 18);  // N>>3 at bit 17
         const uint32_t a_lo0 = smem_lo + cur.a_lo_rel;
 #pragma unroll 2
@@ -415,7 +497,12 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads)
           umma2_f16_elect(scr, ad, bd, idesc, (first + j) > 0);
           if (j == 0 && pending >= 0) { umma2_commit_elect(&ring_empty[pending]); pending = -1; }
         }
+        PROF_ADD(6);
+        }
       }
+#if defined(P2S_ABL_NOCONVMMA) || defined(P2S_ABL_NOMLPMMA)
+      if (pending >= 0) { umma2_commit_elect(&ring_empty[pending]); pending = -1; }
+#endif
       // completion signals for the epilogue / builders are not deferred
       if (f & (MI_COMMIT_A1 | MI_COMMIT_MLP | MI_COMMIT_ACC)) {
         umma2_commit_elect(&ring_empty[s]);  // keep ring releases in order before a hand-off
@@ -431,6 +518,15 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads)
       } else {
         pending = s;
       }
+#ifdef P2S_PROFILE
+      if (p.prof && blockIdx.x == 0 && step < 256 && lane == 0) {  // per-item issue timeline
+        unsigned long long* tr = p.prof + 148 * 4 * 20 + 4 * step;
+        tr[0] = (unsigned long long)(tr_a - prof_start);
+        tr[1] = (unsigned long long)(tr_b - prof_start);
+        tr[2] = (unsigned long long)(clock64() - prof_start);
+        tr[3] = f | ((unsigned long long)cur.nslabs << 16) | ((unsigned long long)cur.n16 << 24);
+      }
+#endif
       if (++s == nring) { s = 0; ph ^= 1; }
       cur = nxt;
       if (++g == n_items) { g = 0; ++it; }
@@ -447,7 +543,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads)
       int b, y, x0;
       tile_coords(p, t, b, y, x0);
       // --- A1: row m = pixel x0+m, k = Zernike index (zero-padded to K1)
-      { PROF_T0(); mbar_wait(&bars[BAR_A1_EMPTY], (it & 1) ^ 1); PROF_ADD(9); }
+      { PROF_T0(); WAIT_BUILD(&bars[BAR_A1_EMPTY], (it & 1) ^ 1); PROF_ADD(9); }
       {
         const int m = tid;
         const int x = min(x0 + m, p.W - 1);
@@ -467,7 +563,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads)
       if (p.mode != 0) continue;
       // --- E views of every channel
       const int eb = p.n_ebuf == 2 ? (it & 1) : 0;
-      { PROF_T0(); mbar_wait(&bars[BAR_E_EMPTY0 + eb], ((eb ? e_use1 : e_use0) & 1) ^ 1); PROF_ADD(11); }
+      { PROF_T0(); WAIT_BUILD(&bars[BAR_E_EMPTY0 + eb], ((eb ? e_use1 : e_use0) & 1) ^ 1); PROF_ADD(11); }
       if (eb) ++e_use1; else ++e_use0;
       uint8_t* Eb = sE + (size_t)eb * 3 * p.chan_bytes;  // buffers are sized for C = 3
       {
@@ -503,7 +599,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads)
       for (int o = 0; o < p.n_ops; ++o) {
         const MlpOp op = p.ops[o];
         if (op.layer == 2) continue;        // beta stays in TMEM for the conv epilogue
-        { PROF_T0(); mbar_wait(&bars[BAR_MLP_DONE], mlp_waits & 1); PROF_ADD(13); }
+        { PROF_T0(); WAIT_EPI(&bars[BAR_MLP_DONE], mlp_waits & 1); PROF_ADD(13); }
         ++mlp_waits;
         tc_fence_after();
         const float* bias = (op.layer == 0 ? sB1 : sB2) + op.n0;
@@ -513,7 +609,11 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads)
         uint8_t* dst = to_hold ? hrow : a2row;
         const int kc0 = (to_hold ? 0 : op.n0) >> 3;
 #pragma unroll 1
+#ifdef P2S_ABL_NODRAIN
+        for (int hp = 0; hp < 0; ++hp) {
+#else
         for (int hp = 0; hp < 4; ++hp) {     // groups gi = wg + 2*hg, two TMEM loads per wait
+#endif
           const int gi0 = wg + 4 * hp, gi1 = gi0 + 2;
           if (gi0 >= G) break;
           float v[2][16];
@@ -524,21 +624,24 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads)
           for (int u = 0; u < 2; ++u) {
             const int gi = gi0 + 2 * u;
             if (gi < G) {
+              // bias add in packed fp32x2, round to fp16x2 (RN), then ReLU in fp16x2: rounding is
+              // monotone and sign-preserving, so relu(rn(x)) == rn(relu(x))
               const float4* b4 = reinterpret_cast<const float4*>(bias + gi * 16);
+              uint32_t hv[8];
 #pragma unroll
               for (int i4 = 0; i4 < 4; ++i4) {
                 const float4 bb = b4[i4];
-                v[u][4 * i4 + 0] = fmaxf(v[u][4 * i4 + 0] + bb.x, 0.f);
-                v[u][4 * i4 + 1] = fmaxf(v[u][4 * i4 + 1] + bb.y, 0.f);
-                v[u][4 * i4 + 2] = fmaxf(v[u][4 * i4 + 2] + bb.z, 0.f);
-                v[u][4 * i4 + 3] = fmaxf(v[u][4 * i4 + 3] + bb.w, 0.f);
+                const float2 s0 = __fadd2_rn(make_float2(v[u][4 * i4 + 0], v[u][4 * i4 + 1]), make_float2(bb.x, bb.y));
+                const float2 s1 = __fadd2_rn(make_float2(v[u][4 * i4 + 2], v[u][4 * i4 + 3]), make_float2(bb.z, bb.w));
+                hv[2 * i4 + 0] = relu_half2(s0);
+                hv[2 * i4 + 1] = relu_half2(s1);
               }
               const int kc = kc0 + gi * 2;
 #ifndef P2S_ABL_NOA2
-              *reinterpret_cast<uint4*>(dst + kc * 128) = pack8(v[u]);
-              *reinterpret_cast<uint4*>(dst + (kc + 1) * 128) = pack8(v[u] + 8);
+              *reinterpret_cast<uint4*>(dst + kc * 128) = make_uint4(hv[0], hv[1], hv[2], hv[3]);
+              *reinterpret_cast<uint4*>(dst + (kc + 1) * 128) = make_uint4(hv[4], hv[5], hv[6], hv[7]);
 #else
-              if (v[u][0] == 12345.f) *reinterpret_cast<uint4*>(dst + kc * 128) = pack8(v[u] + 8);
+              if (hv[0] == 12345u) *reinterpret_cast<uint4*>(dst + kc * 128) = make_uint4(hv[4], hv[5], hv[6], hv[7]);
 #endif
             }
           }
@@ -548,10 +651,14 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads)
         __syncwarp();
         if (lane == 0) mbar_arrive_remote(&bars[BAR_SCR_FREE], 0);
       }
-      { PROF_T0(); mbar_wait(&bars[BAR_ACC_FULL], it & 1); PROF_ADD(15); }
+      { PROF_T0(); WAIT_EPI(&bars[BAR_ACC_FULL], it & 1); PROF_ADD(15); }
       tc_fence_after();
+#ifdef P2S_PROFILE
+      const long long te0 = clock64();
+#endif
       const int x = x0 + m;
       const int GK = p.Nk >> 4;
+      const int GF = p.K >> 4, tail = p.K & 15;  // full 16-column groups, real columns after them
       if (p.mode == 1) {
         for (int gi = wg; gi < GK; gi += 2) {
           float bv[16];
@@ -562,40 +669,28 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads)
               p.beta_out[((size_t)b * p.K + gi * 16 + i) * HW + (size_t)y * p.W + x] = bv[i] + sB3[gi * 16 + i];
         }
       } else {
-        float jc[3] = {0.f, 0.f, 0.f};
-        float bs = 0.f;
+        // packed fp32x2 accumulation: lane .x sums even k, .y odd k (combined after the loop)
+        float2 jc2[3] = {make_float2(0.f, 0.f), make_float2(0.f, 0.f), make_float2(0.f, 0.f)};
+        float2 bs2 = make_float2(0.f, 0.f);
 #ifdef P2S_ABL_EPI0
         for (int gi = wg; gi < 0; gi += 2) {
 #else
         for (int gi = wg; gi < GK; gi += 2) {
 #endif
-          float bv[16], av[3][16];
-          tmem_ld16(tl + p.scr_col + gi * 16, bv);
-#pragma unroll
-          for (int c = 0; c < 3; ++c)
-            if (c < C) tmem_ld16(tl + c * p.Nk + gi * 16, av[c]);
-          tmem_ld_wait();
-          const float4* b34 = reinterpret_cast<const float4*>(sB3 + gi * 16);
-          const float4* sv4 = reinterpret_cast<const float4*>(sSv + gi * 16);
-#pragma unroll
-          for (int i4 = 0; i4 < 4; ++i4) {
-            const float4 b3 = b34[i4], sv = sv4[i4];
-            const float bb[4] = {b3.x, b3.y, b3.z, b3.w}, ss[4] = {sv.x, sv.y, sv.z, sv.w};
-#pragma unroll
-            for (int k = 0; k < 4; ++k) {
-              const int i = 4 * i4 + k;
-              const float be = bv[i] + bb[k];
-              bs = fmaf(be, ss[k], bs);
-#pragma unroll
-              for (int c = 0; c < 3; ++c)
-                if (c < C) jc[c] = fmaf(be, av[c][i], jc[c]);
-            }
-          }
+          // a tail group with <= 4 real columns (K % 16 in 1..4, e.g. K = 100) reads only those:
+          // the columns past K are zero padding (N % 16 == 0)
+          if (gi == GF && tail <= 4) conv_epi_group<4>(tl, p.scr_col, p.Nk, gi, C, sB3, sSv, jc2, bs2);
+          else conv_epi_group<16>(tl, p.scr_col, p.Nk, gi, C, sB3, sSv, jc2, bs2);
         }
+        float jc[3] = {jc2[0].x + jc2[0].y, jc2[1].x + jc2[1].y, jc2[2].x + jc2[2].y};
+        float bs = bs2.x + bs2.y;
         // every TMEM read of this tile is done: release TMEM before combining / storing J
         tc_fence_before();
         __syncwarp();
         if (lane == 0) mbar_arrive_remote(&bars[BAR_TMEM_FREE], 0);
+#ifdef P2S_PROFILE
+        prof_acc[16] += (unsigned long long)(clock64() - te0);
+#endif
         float4* red = sRed + (it & 1) * 128;
         if (wg == 1) red[m] = make_float4(jc[0], jc[1], jc[2], bs);
         named_bar_sync(1, 32 * kNumEpiWarps);

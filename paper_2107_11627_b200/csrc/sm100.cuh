@@ -44,6 +44,12 @@ P2S_DEV void mbar_wait(uint64_t* bar, uint32_t parity) {
   while (!mbar_try_wait(bar, parity)) {
   }
 }
+// Wait for latency-tolerant roles: a non-blocking probe with nanosleep backoff. Spinning
+// try_wait warps steal shared-memory issue slots from the tensor core's operand reads
+// (tools/umma_probe.cu interference modes 2/5: ~5% vs ~1% UMMA slowdown for 8 waiting warps).
+P2S_DEV void mbar_wait_sleep(uint64_t* bar, uint32_t parity, uint32_t ns) {
+  while (!mbar_test(bar, parity)) __nanosleep(ns);
+}
 
 // ------------------------------------------------------------------ bulk async copy (TMA engine)
 // global -> shared, completes `bytes` of transaction on `bar`. 16-B aligned, bytes % 16 == 0.
@@ -99,6 +105,35 @@ P2S_DEV void tmem_ld16(uint32_t taddr, float (&v)[16]) {
       : "r"(taddr));
 #pragma unroll
   for (int i = 0; i < 16; ++i) v[i] = __uint_as_float(r[i]);
+}
+// 32 lanes x 8 / x 4 consecutive fp32 columns (padding-free tails of a 16-column group).
+P2S_DEV void tmem_ld8(uint32_t taddr, float* v) {
+  uint32_t r[8];
+  asm volatile("tcgen05.ld.sync.aligned.32x32b.x8.b32 {%0,%1,%2,%3,%4,%5,%6,%7}, [%8];"
+               : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3]), "=r"(r[4]), "=r"(r[5]), "=r"(r[6]),
+                 "=r"(r[7])
+               : "r"(taddr));
+#pragma unroll
+  for (int i = 0; i < 8; ++i) v[i] = __uint_as_float(r[i]);
+}
+P2S_DEV void tmem_ld4(uint32_t taddr, float* v) {
+  uint32_t r[4];
+  asm volatile("tcgen05.ld.sync.aligned.32x32b.x4.b32 {%0,%1,%2,%3}, [%4];"
+               : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3])
+               : "r"(taddr));
+#pragma unroll
+  for (int i = 0; i < 4; ++i) v[i] = __uint_as_float(r[i]);
+}
+template <int NC>
+P2S_DEV void tmem_ld_n(uint32_t taddr, float* v) {
+  if constexpr (NC == 16) {
+    tmem_ld16(taddr, *reinterpret_cast<float(*)[16]>(v));
+  } else if constexpr (NC == 8) {
+    tmem_ld8(taddr, v);
+  } else {
+    static_assert(NC == 4, "x4 / x8 / x16 only");
+    tmem_ld4(taddr, v);
+  }
 }
 P2S_DEV void tmem_ld_wait() { asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory"); }
 

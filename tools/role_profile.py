@@ -25,17 +25,17 @@ img, z, t = (torch.from_numpy(a).cuda() for a in (inp.image, inp.zernike, inp.ti
 out = torch.empty_like(img)
 for _ in range(3):
     r.render(img, z, t, out=out)
-buf = torch.zeros(148 * 4 * 20, dtype=torch.int64, device="cuda")
+buf = torch.zeros(148 * 4 * 20 + 4 * 256, dtype=torch.int64, device="cuda")
 r.debug_profile_buffer(buf)
 r.render(img, z, t, out=out)
 torch.cuda.synchronize()
 r.debug_profile_buffer(None)
-c = buf.view(148, 4, 20).cpu().numpy().astype(np.float64)
-names = {0: {0: "wait A1_FULL", 1: "wait TMEM_FREE", 2: "wait SCR_FREE", 3: "wait E_FULL", 4: "wait ring(MLP)",
-             5: "wait ring(conv)", 6: "wait ACC_FREE", 19: "total"},
+c = buf[:148 * 4 * 20].view(148, 4, 20).cpu().numpy().astype(np.float64)
+names = {0: {0: "wait A1_FULL", 1: "wait TMEM_FREE", 2: "wait SCR_FREE", 3: "wait E_FULL", 5: "wait ring",
+             4: "conv UMMA loops", 6: "MLP UMMA loops", 19: "total"},
          1: {7: "wait ring_empty", 19: "total"},
          2: {9: "wait A1_EMPTY", 11: "wait E_EMPTY", 12: "build E", 19: "total"},
-         3: {13: "wait MLP_DONE", 15: "wait ACC_FULL", 19: "total"}}
+         3: {13: "wait MLP_DONE", 15: "wait ACC_FULL", 16: "conv epi to release", 19: "total"}}
 roles = ["MMA", "producer", "builder", "epilogue"]
 ntiles = spec.H * ((spec.W + 127) // 128)
 print(f"cfg{cfg}: {ntiles} tiles over 148 CTAs (~{ntiles / 148:.1f} tiles/CTA); cycles per CTA (mean / max)")

@@ -260,6 +260,22 @@ __global__ void __launch_bounds__(384, 1) k_interf(int mode, int iters, unsigned
     if (lane_id() == 0) { cyc[blockIdx.x] = 400000ull * 3 / 6144; done = 1; }
   } else if (mode == 2 && w >= 4) {
     while (!done) { mbar_try_wait(&bar_never, 0); }
+  } else if (mode == 4 && w >= 4) {
+    // try_wait with an explicit suspend-time hint (ns)
+    while (!done) {
+      uint32_t ok;
+      asm volatile(
+          "{\n .reg .pred p;\n mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2, %3;\n"
+          " selp.u32 %0, 1, 0, p;\n}" : "=r"(ok) : "r"(smem_u32(&bar_never)), "r"(0u), "r"(1000000u) : "memory");
+    }
+  } else if (mode == 5 && w >= 4) {
+    // non-blocking test_wait + nanosleep backoff
+    while (!done) { if (!mbar_test(&bar_never, 0)) __nanosleep(256); }
+  } else if (mode == 6 && w >= 4) {
+    // 8 warps streaming 16-B shared stores (what the builders / drains do)
+    uint8_t* buf = smem + 160 * 1024 + (w - 4) * 4096;
+    int i = 0;
+    while (!done) { *reinterpret_cast<int4*>(buf + ((i++ * 512 + lane_id() * 16) & 4095)) = make_int4(i, i, i, i); }
   }
   tc_fence_before();
   __syncthreads();
@@ -270,7 +286,7 @@ static void run_interf(int nsm) {
   unsigned long long* dc; float* sink; CK(cudaMalloc(&dc, 2048 * 8)); CK(cudaMalloc(&sink, 4096 * 4));
   CK(cudaFuncSetAttribute(k_interf, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024));
   const int iters = 6144;
-  for (int mode = 0; mode < 4; ++mode) {
+  for (int mode = 0; mode < 7; ++mode) {
     k_interf<<<nsm, 384, 200 * 1024>>>(mode, iters, dc, sink);
     CK(cudaGetLastError()); CK(cudaDeviceSynchronize());
     k_interf<<<nsm, 384, 200 * 1024>>>(mode, iters, dc, sink);
@@ -281,7 +297,8 @@ static void run_interf(int nsm) {
     unsigned long long ldc[16];
     CK(cudaMemcpy(ldc, dc + 1000, 16 * 8, cudaMemcpyDeviceToHost));
     printf("interference mode=%d (%s): %.1f cyc/mma (floor 56); reader cycles per ld16+wait (warp 4): %llu\\n", mode,
-           mode == 0 ? "alone" : mode == 1 ? "8 warps tcgen05.ld" : mode == 2 ? "8 warps spin try_wait" : "readers alone",
+           mode == 0 ? "alone" : mode == 1 ? "8 warps tcgen05.ld" : mode == 2 ? "8 warps spin try_wait" : mode == 3 ? "readers alone" :
+           mode == 4 ? "8 warps try_wait+suspend hint" : mode == 5 ? "8 warps test_wait+nanosleep" : "8 warps st.shared.v4 stream",
            mx / iters, (mode == 1 || mode == 3) ? ldc[4] : 0ull);
   }
 }
