@@ -132,6 +132,9 @@ struct p2s_handle {
   float *h_img = nullptr, *h_z = nullptr, *h_t = nullptr, *h_out = nullptr;  // device staging (host path)
   size_t stage_px_cap = 0, stage_chw_cap = 0;
   cudaEvent_t ev_begin = nullptr, ev_end = nullptr;
+  // host path (p2s_render_host): input-copy stream and its events
+  cudaStream_t s_in = nullptr;
+  cudaEvent_t ev_entry = nullptr, ev_band = nullptr;
   unsigned long long* prof = nullptr;
   CUtensorMap maps[kMaxMaps];
   int n_maps = 0;
@@ -161,6 +164,8 @@ FusedParams make_params(const p2s_handle* h, int B, int C, int H, int W, int mod
   FusedParams p{};
   p.B = B; p.C = C; p.H = H; p.W = W; p.n_in = h->n_in;
   p.nstrips = (W + kTileM - 1) / kTileM;
+  p.y0 = 0;
+  p.ny = H;
   p.ntiles = B * p.nstrips * H;
   p.mode = mode;
   p.stream = h->d_stream;
@@ -469,8 +474,8 @@ p2s_status p2s_init(const p2s_basis* basis, const p2s_mlp* mlp, p2s_handle** out
       for (int k = 0; k < per_gap && ci + 1 < conv_items.size(); ++k) full.push_back(conv_items[ci++]);
   }
   while (ci < conv_items.size()) full.push_back(conv_items[ci++]);
-  // First tile of every CTA: all MLP ops before the conv stages (the epilogue is idle then and
-  // the MLP phase overlaps the builders' first im2col views); later tiles interleave.
+  // First tile of every CTA: all MLP ops before the conv stages (its first im2col views take
+  // ~10 us of cold loads to build, longer than the MLP chain; interleaving measured slower).
   std::vector<Item> first;
   for (const Item& it : full) if (it.kind == 0) first.push_back(it);
   for (const Item& it : full) if (it.kind == 1) first.push_back(it);
@@ -655,7 +660,7 @@ p2s_status p2s_render_host(p2s_handle* h, const float* image_host, int B, int C,
   p2s_status s = check_image(h, im);
   if (s != P2S_OK) return s;
   cudaStream_t st = (cudaStream_t)stream;
-  const size_t px = (size_t)B * H * W, chw = px * C;
+  const size_t HW = (size_t)H * W, px = (size_t)B * HW, chw = px * C;
   if (px > h->stage_px_cap || chw > h->stage_chw_cap) {
     P2S_CUDA(cudaDeviceSynchronize());
     cudaFree(h->h_img); cudaFree(h->h_z); cudaFree(h->h_t); cudaFree(h->h_out);
@@ -668,14 +673,88 @@ p2s_status p2s_render_host(p2s_handle* h, const float* image_host, int B, int C,
     h->stage_px_cap = px;
     h->stage_chw_cap = chw;
   }
-  P2S_CUDA(cudaMemcpyAsync(h->h_img, image_host, chw * 4, cudaMemcpyHostToDevice, st));
-  P2S_CUDA(cudaMemcpyAsync(h->h_z, zernike_host, px * h->n_in * 4, cudaMemcpyHostToDevice, st));
-  if (tilt_host) P2S_CUDA(cudaMemcpyAsync(h->h_t, tilt_host, px * 2 * 4, cudaMemcpyHostToDevice, st));
-  im.data = h->h_img;
-  s = render_impl(h, im, h->h_z, tilt_host ? h->h_t : nullptr, h->h_out, nullptr, st);
+  if (!h->s_in) {
+    P2S_CUDA(cudaStreamCreateWithFlags(&h->s_in, cudaStreamNonBlocking));
+    P2S_CUDA(cudaEventCreateWithFlags(&h->ev_entry, cudaEventDisableTiming));
+    P2S_CUDA(cudaEventCreateWithFlags(&h->ev_band, cudaEventDisableTiming));
+  }
+  s = ensure_J(h, chw);
   if (s != P2S_OK) return s;
-  P2S_CUDA(cudaMemcpyAsync(out_host, h->h_out, chw * 4, cudaMemcpyDeviceToHost, st));
+  // Pipelined over row bands (inputs are PCIe-bound): the input stream copies
+  // each frame's image and tilt, then its Zernike field band by band (one 2D copy over the
+  // n_in planes per band); the caller's stream renders each band as soon as it has landed,
+  // then warps the frame and copies it back. The last band is small, so little work is left
+  // once the last input byte has arrived. Stream order on `st` is preserved (the input stream
+  // starts behind it).
+  // P2S_HOST_TRACE=1: print a per-call timeline of the pipeline (development aid)
+  static const bool trace = std::getenv("P2S_HOST_TRACE") != nullptr;
+  std::vector<std::pair<const char*, cudaEvent_t>> tev;
+  auto mark = [&](const char* what, cudaStream_t on) {
+    if (!trace) return;
+    cudaEvent_t e;
+    cudaEventCreate(&e);
+    cudaEventRecord(e, on);
+    tev.emplace_back(what, e);
+  };
+  mark("entry", st);
+  P2S_CUDA(cudaEventRecord(h->ev_entry, st));
+  P2S_CUDA(cudaStreamWaitEvent(h->s_in, h->ev_entry, 0));
+  // Band heights: the tail shrinks geometrically (16, 32, 64, 128 rows from the bottom) so each
+  // band renders faster than the next one copies (a row of n_in fp32 Zernike planes takes ~3.6x
+  // longer over PCIe than to render); the head is split into bands of <= 160 rows.
+  std::vector<int> bands;
+  {
+    std::vector<int> tailb;
+    int left = H;
+    for (int t = 16; t <= 128 && left > 0; t *= 2) { const int n = std::min(t, left); tailb.push_back(n); left -= n; }
+    const int nhead = (left + 159) / 160;
+    for (int k = 0; k < nhead; ++k) bands.push_back(left * (k + 1) / nhead - left * k / nhead);
+    bands.insert(bands.end(), tailb.rbegin(), tailb.rend());
+  }
+  for (int f = 0; f < B; ++f) {
+    const size_t fo_img = (size_t)f * C * HW, fo_z = (size_t)f * h->n_in * HW, fo_t = (size_t)f * 2 * HW;
+    P2S_CUDA(cudaMemcpyAsync(h->h_img + fo_img, image_host + fo_img, (size_t)C * HW * 4, cudaMemcpyHostToDevice, h->s_in));
+    if (tilt_host)
+      P2S_CUDA(cudaMemcpyAsync(h->h_t + fo_t, tilt_host + fo_t, 2 * HW * 4, cudaMemcpyHostToDevice, h->s_in));
+    mark("image+tilt in", h->s_in);
+    for (size_t k = 0, y0 = 0; k < bands.size(); ++k) {
+      const int ny = bands[k];
+      if (ny == 0) continue;
+      P2S_CUDA(cudaMemcpy2DAsync(h->h_z + fo_z + (size_t)y0 * W, HW * 4, zernike_host + fo_z + (size_t)y0 * W,
+                                 HW * 4, (size_t)ny * W * 4, h->n_in, cudaMemcpyHostToDevice, h->s_in));
+      mark("zernike band in", h->s_in);
+      P2S_CUDA(cudaEventRecord(h->ev_band, h->s_in));
+      P2S_CUDA(cudaStreamWaitEvent(st, h->ev_band, 0));
+      FusedParams p = make_params(h, 1, C, H, W, 0);
+      p.y0 = y0;
+      p.ny = ny;
+      p.ntiles = p.nstrips * ny;
+      p.image = h->h_img + fo_img;
+      p.zernike = h->h_z + fo_z;
+      p.J = h->d_J;
+      s = launch_fused(h, p, st);
+      if (s != P2S_OK) return s;
+      mark("band rendered", st);
+      y0 += ny;
+    }
+    const int grid = (int)std::min<size_t>((HW + 255) / 256, (size_t)h->sm_count * 16);
+    k_tilt_warp<<<grid, 256, 0, st>>>(h->d_J, tilt_host ? h->h_t + fo_t : nullptr, h->h_out + fo_img, 1, C, H, W);
+    P2S_CUDA(cudaPeekAtLastError());
+    mark("warped", st);
+    P2S_CUDA(cudaMemcpyAsync(out_host + fo_img, h->h_out + fo_img, (size_t)C * HW * 4, cudaMemcpyDeviceToHost, st));
+    mark("out copied", st);
+  }
   P2S_CUDA(cudaStreamSynchronize(st));
+  if (trace) {
+    cudaDeviceSynchronize();
+    for (auto& te : tev) {
+      float ms = 0.f;
+      cudaEventElapsedTime(&ms, tev[0].second, te.second);
+      std::fprintf(stderr, "[p2s host] %8.1f us  %s\n", ms * 1e3f, te.first);
+    }
+    for (auto& te : tev) cudaEventDestroy(te.second);
+    (void)cudaGetLastError();
+  }
   return P2S_OK;
 }
 
@@ -706,6 +785,9 @@ void p2s_destroy(p2s_handle* h) {
   cudaFree(h->d_stream); cudaFree(h->d_items); cudaFree(h->d_mma); cudaFree(h->d_steps); cudaFree(h->d_consts);
   cudaFree(h->d_J);
   cudaFree(h->h_img); cudaFree(h->h_z); cudaFree(h->h_t); cudaFree(h->h_out);
+  if (h->s_in) cudaStreamDestroy(h->s_in);
+  if (h->ev_entry) cudaEventDestroy(h->ev_entry);
+  if (h->ev_band) cudaEventDestroy(h->ev_band);
   delete h;
 }
 

@@ -69,6 +69,8 @@ P2S_DEV void tma2_load_2d(void* dst_smem, const void* tmap, int x, int y, uint32
       "l"(tmap), "r"(x), "r"(y), "r"(mbar_cluster)
       : "memory");
 }
+// Fire-and-forget L2 prefetch of the 128-B line holding `ptr`.
+P2S_DEV void prefetch_l2(const void* ptr) { asm volatile("prefetch.global.L2 [%0];" ::"l"(ptr)); }
 P2S_DEV void prefetch_tmap(const void* tmap) {
   asm volatile("prefetch.tensormap [%0];" ::"l"(tmap) : "memory");
 }

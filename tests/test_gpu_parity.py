@@ -153,13 +153,24 @@ def test_cfg5_sampled(p2s):
     _sampled(p2s, 5, n=192, seed=2)
 
 
-def test_render_host_matches_device(p2s):
-    """p2s_render_host (host buffers, copies inside) gives the device path's result."""
-    inp = synth.make_inputs(SMALL["ragged_rgb_S7"])
+HOST_CASES = {
+    "one_band": SMALL["ragged_rgb_S7"],
+    # H = 300: two 118-row bands + a 64-row last band, two frames, ragged W
+    "bands_B2": synth.custom("bands", 211, B=2, C=3, H=300, W=130, K=20, S=9, h1=32, h2=32, t_std=2.0),
+}
+
+
+@pytest.mark.parametrize("name", list(HOST_CASES))
+@pytest.mark.parametrize("with_tilt", [True, False])
+def test_render_host_matches_device(p2s, name, with_tilt):
+    """p2s_render_host (host buffers; copies pipelined with the per-band renders inside) gives
+    the device path's result bit for bit (banding changes no per-tile arithmetic)."""
+    inp = synth.make_inputs(HOST_CASES[name])
     r = p2s.Renderer(inp.basis, inp.mlp)
-    dev = r.render(_dev(inp.image), _dev(inp.zernike), _dev(inp.tilt)).cpu().numpy()
+    tilt = inp.tilt if with_tilt else None
+    dev = r.render(_dev(inp.image), _dev(inp.zernike), _dev(tilt) if with_tilt else None).cpu().numpy()
     host = np.empty_like(inp.image)
-    r.render_host(inp.image, inp.zernike, inp.tilt, host)
+    r.render_host(inp.image, inp.zernike, tilt, host)
     np.testing.assert_array_equal(host, dev)
 
 

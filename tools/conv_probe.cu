@@ -132,6 +132,65 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(128, 1) k_qdepth(uns
   if (warp_id() == 0) tmem_dealloc2<512>(tmem);
 }
 
+// TMEM -> register bandwidth: NW warps (quadrant = warp % 4), each loading NL x (32 lanes x
+// X columns) per tcgen05.wait::ld, for `iters` rounds over 448 columns.
+template <int X>
+__device__ __forceinline__ void tld(uint32_t a, float* v) {
+  if constexpr (X == 16) tmem_ld16(a, *reinterpret_cast<float(*)[16]>(v));
+  else if constexpr (X == 8) tmem_ld8(a, v);
+  else tmem_ld4(a, v);
+}
+template <int X, int NL>
+__global__ void __launch_bounds__(512, 1) k_tmem_bw(int nw, int iters, unsigned long long* cyc, float* sink) {
+  __shared__ uint32_t tslot;
+  if (warp_id() == 0) tmem_alloc<512>(&tslot);
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
+  const uint32_t tmem = tslot;
+  const int w = warp_id();
+  float acc8[X];
+#pragma unroll
+  for (int i = 0; i < X; ++i) acc8[i] = 0.f;
+  long long t0 = clock64();
+  if (w < nw) {
+    const uint32_t tl = tmem + ((uint32_t)((w & 3) * 32) << 16);
+    for (int it = 0; it < iters; ++it) {
+      for (int c = 0; c + NL * X <= 448; c += NL * X) {
+        float v[NL][X];
+#pragma unroll
+        for (int l = 0; l < NL; ++l) tld<X>(tl + c + l * X, v[l]);
+        tmem_ld_wait();
+#pragma unroll
+        for (int l = 0; l < NL; ++l)
+#pragma unroll
+          for (int i = 0; i < X; ++i) acc8[i] += v[l][i];  // independent chains
+      }
+    }
+  }
+  long long t1 = clock64();
+  __syncthreads();
+  if (threadIdx.x == 0) cyc[0] = (unsigned long long)(clock64() - t0);
+  float acc = 0.f;
+#pragma unroll
+  for (int i = 0; i < X; ++i) acc += acc8[i];
+  sink[threadIdx.x] = acc + (float)(t1 - t0) * 0.f;
+  tc_fence_before();
+  __syncthreads();
+  if (warp_id() == 0) tmem_dealloc<512>(tmem);
+}
+template <int X, int NL>
+static void run_tmem_bw(int nw) {
+  unsigned long long* dc; float* sink; CK(cudaMalloc(&dc, 8)); CK(cudaMalloc(&sink, 512 * 4));
+  const int iters = 200;
+  for (int w = 0; w < 2; ++w) { k_tmem_bw<X, NL><<<1, 512>>>(nw, iters, dc, sink); CK(cudaGetLastError()); CK(cudaDeviceSynchronize()); }
+  unsigned long long c; CK(cudaMemcpy(&c, dc, 8, cudaMemcpyDeviceToHost));
+  const int per = 448 / (NL * X) * (NL * X);
+  const double bytes = (double)iters * per * 32 * 4 * nw;
+  printf("tmem ld x%-2d x %d per wait, %2d warps: %.1f B/cyc\n", X, NL, nw, bytes / c);
+  cudaFree(dc); cudaFree(sink);
+}
+
 template <int A, int B, int CH, int COMMIT>
 static void run(int nsm, const Step* d_steps, int fill = 0) {
   unsigned long long* dc; CK(cudaMalloc(&dc, 1024 * 8)); CK(cudaMemset(dc, 0, 1024 * 8));
@@ -178,6 +237,8 @@ int main() {
     for (int j = 0; j < 64; ++j) printf("%s%llu", j % 16 ? " " : "\n  ", h[j]);
     printf("\n  all 64 complete at %llu\n", h[64]);
   }
+  for (int nw : {4, 8, 12, 16}) { run_tmem_bw<16, 1>(nw); run_tmem_bw<16, 2>(nw); run_tmem_bw<16, 4>(nw); }
+  run_tmem_bw<8, 4>(8); run_tmem_bw<4, 4>(8); run_tmem_bw<16, 6>(8);
   printf("PROBE DONE\n");
   return 0;
 }

@@ -18,6 +18,9 @@ cfg = int(sys.argv[1]) if len(sys.argv) > 1 else 3
 first = int(sys.argv[2]) if len(sys.argv) > 2 else 0
 count = int(sys.argv[3]) if len(sys.argv) > 3 else 80
 spec = synth.CONFIGS[cfg]
+if os.environ.get("TRACE_H"):  # e.g. TRACE_H=16: one tile per CTA (launch-latency view)
+    spec = synth.custom("h", cfg, B=1, C=spec.C, H=int(os.environ["TRACE_H"]), W=spec.W, K=spec.K, S=spec.S,
+                        h1=spec.h1, h2=spec.h2)
 inp = synth.make_inputs(spec, frames=range(1))
 r = p2s.Renderer(inp.basis, inp.mlp)
 img, z, t = (torch.from_numpy(a).cuda() for a in (inp.image, inp.zernike, inp.tilt))
