@@ -115,8 +115,9 @@ struct p2s_handle {
   ConvPlan plan;
   std::vector<Item> items;  // [items_full | items_beta]
   int n_items_full = 0, n_items_beta = 0, n_items_first = 0, tab_cap = 0;
-  MlpOp ops[kMaxOps];
-  int n_ops = 0;
+  MlpOp ops[kMaxOps];  // [0, n_ops) per-tile ops, then n_fops first-tile whole-layer ops
+  int n_ops = 0, n_fops = 0;
+  bool bias_folded = false;
   int stage_bytes, nring, smem_bytes, n_ebuf, scr_col;
   int off_ring, off_a1, off_a2, off_hold, off_e, off_tab, off_const, off_red, off_bar, a1_sbo, a2_sbo, hold_sbo;
   int l3_hold_ks = 0, hold_k0 = 0;
@@ -176,8 +177,10 @@ FusedParams make_params(const p2s_handle* h, int B, int C, int H, int W, int mod
   p.tab_cap = h->tab_cap;
   p.off_mma = h->off_tab + h->tab_cap * (int)sizeof(Item);
   p.off_steps = p.off_mma + h->tab_cap * (int)sizeof(MmaItem);
-  for (int i = 0; i < h->n_ops; ++i) p.ops[i] = h->ops[i];
+  for (int i = 0; i < h->n_ops + h->n_fops; ++i) p.ops[i] = h->ops[i];
   p.n_ops = h->n_ops;
+  p.n_fops = h->n_fops;
+  p.bias_folded = h->bias_folded ? 1 : 0;
   p.conv_steps = h->d_steps;
   p.nconv = (int)h->plan.steps.size();
   p.consts = h->d_consts;
@@ -270,6 +273,11 @@ p2s_status p2s_init(const p2s_basis* basis, const p2s_mlp* mlp, p2s_handle** out
   const int nconv = (int)P.steps.size();
   if (nconv > kMaxConvSteps) { delete h; return P2S_ERR_UNSUPPORTED; }
 
+  // Biases folded into the GEMMs when every layer's input has a padding column to carry a
+  // constant 1: the drains are then a single relu-convert per two values.
+  h->bias_folded = h->n_in + 2 <= h->K1 && h->h1 + 2 <= h->N1 && h->h2 + 2 <= h->N2;
+  if (const char* e = std::getenv("P2S_NO_BIAS_FOLD")) h->bias_folded = std::atoi(e) == 0 && h->bias_folded;
+
   // ---- TMEM: conv accumulators [0, 3*Nk), MLP scratch / beta [3*Nk, 3*Nk + CH)
   h->scr_col = 3 * h->Nk;
   const int CH = std::min(256, (512 - h->scr_col) / 16 * 16);  // widest MLP chunk
@@ -283,13 +291,21 @@ p2s_status p2s_init(const p2s_basis* basis, const p2s_mlp* mlp, p2s_handle** out
     if (nch > 2 || (l == 2 && nch > 1)) { delete h; return P2S_ERR_UNSUPPORTED; }
     const int w0 = nch == 1 ? N : std::min(CH, 128);  // columns [0, w0) and [w0, N)
     if (nch == 1) {
-      h->ops[h->n_ops++] = MlpOp{l, 0, N, layer_K[l] / 16, 1, 1};
+      h->ops[h->n_ops++] = MlpOp{l, 0, N, layer_K[l] / 16, 1, 1, h->scr_col};
     } else {
       // the upper (narrower) chunk goes first: for L2 it is the one parked in the hold buffer
       // while the lower chunk still reads A2, so the hold buffer is as small as possible
-      h->ops[h->n_ops++] = MlpOp{l, w0, N - w0, layer_K[l] / 16, 1, 0};
-      h->ops[h->n_ops++] = MlpOp{l, 0, w0, layer_K[l] / 16, 0, 1};
+      h->ops[h->n_ops++] = MlpOp{l, w0, N - w0, layer_K[l] / 16, 1, 0, h->scr_col};
+      h->ops[h->n_ops++] = MlpOp{l, 0, w0, layer_K[l] / 16, 0, 1, h->scr_col};
     }
+  }
+  // A CTA's first tile has no conv accumulator to protect yet: its L1 and L2 run as single
+  // whole-layer ops into TMEM columns [0, N1) and [N1, N1 + N2) (two drain round trips instead
+  // of four; L2's output goes straight to A2, L3 then reads all of it from A2).
+  h->n_fops = 0;
+  if (h->N1 + h->N2 <= 512) {
+    h->ops[h->n_ops + h->n_fops++] = MlpOp{0, 0, h->N1, h->K1 / 16, 1, 1, 0};
+    h->ops[h->n_ops + h->n_fops++] = MlpOp{1, 0, h->N2, h->N1 / 16, 1, 1, h->N1};
   }
 
   // The first-issued L2 chunk is parked in a "hold" buffer that L3 reads directly (the other
@@ -333,8 +349,13 @@ p2s_status p2s_init(const p2s_basis* basis, const p2s_mlp* mlp, p2s_handle** out
     int mlp = 0;
     for (int o = 0; o < h->n_ops; ++o)
       mlp += count_stages(sb, h->ops[o].nks, h->ops[o].N, h->ops[o].layer == 2 && h->l3_hold_ks > 0);
-    const int full = mlp + count_stages(sb, nconv, h->Nk, false);
-    return std::max(2 * full, 2 * mlp);  // [first | steady] or [beta | beta]
+    const int conv = count_stages(sb, nconv, h->Nk, false);
+    int fst = 0;  // first-tile list: whole-layer L1 / L2 (or the per-tile L1 / L2), L3, conv
+    for (int o = 0; o < h->n_ops + h->n_fops; ++o) {
+      const bool in_first = h->n_fops > 0 ? (o >= h->n_ops || h->ops[o].layer == 2) : true;
+      if (in_first) fst += count_stages(sb, h->ops[o].nks, h->ops[o].N, h->ops[o].layer == 2 && h->l3_hold_ks > 0);
+    }
+    return std::max(mlp + conv + fst + conv, 2 * mlp);  // [first | steady] or [beta | beta]
   };
   int tab_cap = 48, sb = 0, nring = 3;
   for (int iter = 0; iter < 6; ++iter) {
@@ -388,9 +409,10 @@ p2s_status p2s_init(const p2s_basis* basis, const p2s_mlp* mlp, p2s_handle** out
   // ---- pack the streamed B operands: per op, [rank-0 halves of all slabs][rank-1 halves],
   //      then the conv slabs the same way. Half r of slab ks of an op of width N = rows
   //      [r*N/2, (r+1)*N/2) of the chunk, K columns [16ks, 16ks+16), LBO 128 / SBO 256.
-  std::vector<size_t> op_off(h->n_ops);
+  const int n_all_ops = h->n_ops + h->n_fops;
+  std::vector<size_t> op_off(n_all_ops);
   size_t total = 0;
-  for (int o = 0; o < h->n_ops; ++o) { op_off[o] = total; total += (size_t)h->ops[o].nks * h->ops[o].N * 32; }
+  for (int o = 0; o < n_all_ops; ++o) { op_off[o] = total; total += (size_t)h->ops[o].nks * h->ops[o].N * 32; }
   const size_t conv_off = total;
   total += (size_t)nconv * h->Nk * 32;
   std::vector<__half> stream(total / 2, __float2half(0.f));
@@ -400,15 +422,29 @@ p2s_status p2s_init(const p2s_basis* basis, const p2s_mlp* mlp, p2s_handle** out
     stream[(base + (size_t)r * nks * hs + (size_t)ks * hs) / 2 + slab_idx(nl, kk)] = __float2half_rn(v);
   };
   const float* Wl[3] = {mlp->W1, mlp->W2, mlp->W3};
+  const float* bl[3] = {mlp->b1, mlp->b2, mlp->b3};
   const int outl[3] = {h->h1, h->h2, K}, inl[3] = {h->n_in, h->h1, h->h2};
-  for (int o = 0; o < h->n_ops; ++o) {
+  for (int o = 0; o < n_all_ops; ++o) {
     const MlpOp& op = h->ops[o];
+    const int l = op.layer;
     for (int ks = 0; ks < op.nks; ++ks)
       for (int n = 0; n < op.N; ++n)
         for (int kk = 0; kk < 16; ++kk) {
           const int row = op.n0 + n, k = ks * 16 + kk;
-          if (row < outl[op.layer] && k < inl[op.layer])
-            put(op_off[o], op.nks, op.N, ks, n, kk, Wl[op.layer][(size_t)row * inl[op.layer] + k]);
+          if (row < outl[l] && k < inl[l]) {
+            put(op_off[o], op.nks, op.N, ks, n, kk, Wl[l][(size_t)row * inl[l] + k]);
+          } else if (h->bias_folded && (k == inl[l] || k == inl[l] + 1)) {
+            // bias folding: input columns inl[l], inl[l]+1 of every layer are constant 1 (the
+            // Zernike tile's padding columns; the previous layer's padding units driven to 1)
+            // and carry the bias as an fp16 hi/lo pair (hi + lo = b to ~2^-22 relative: b3 is
+            // amplified by the tap sums in the centring term, plain fp16 costs accuracy)
+            if (row < outl[l]) {
+              const float bh = __half2float(__float2half_rn(bl[l][row]));
+              put(op_off[o], op.nks, op.N, ks, n, kk, k == inl[l] ? bh : bl[l][row] - bh);
+            } else if ((row == outl[l] || row == outl[l] + 1) && l < 2 && k == inl[l]) {
+              put(op_off[o], op.nks, op.N, ks, n, kk, 1.f);
+            }
+          }
         }
   }
   for (int g = 0; g < nconv; ++g)
@@ -476,8 +512,15 @@ p2s_status p2s_init(const p2s_basis* basis, const p2s_mlp* mlp, p2s_handle** out
   while (ci < conv_items.size()) full.push_back(conv_items[ci++]);
   // First tile of every CTA: all MLP ops before the conv stages (its first im2col views take
   // ~10 us of cold loads to build, longer than the MLP chain; interleaving measured slower).
+  // With whole-layer first-tile ops: [L1 (N1) | L2 (N2) | L3 (reads A2 only) | conv].
   std::vector<Item> first;
-  for (const Item& it : full) if (it.kind == 0) first.push_back(it);
+  if (h->n_fops > 0) {
+    for (int o = h->n_ops; o < h->n_ops + h->n_fops; ++o)
+      make_items(op_off[o], h->ops[o].nks, h->ops[o].N, 0, (uint8_t)o, first);
+    for (const Item& it : full) if (it.kind == 0 && h->ops[it.op].layer == 2) first.push_back(it);
+  } else {
+    for (const Item& it : full) if (it.kind == 0) first.push_back(it);
+  }
   for (const Item& it : full) if (it.kind == 1) first.push_back(it);
   h->n_items_full = (int)full.size();
   h->n_items_beta = (int)beta.size();
@@ -490,7 +533,7 @@ p2s_status p2s_init(const p2s_basis* basis, const p2s_mlp* mlp, p2s_handle** out
   h->items.insert(h->items.end(), beta.begin(), beta.end());
   h->items.insert(h->items.end(), first.begin(), first.end());
   // UMMA-side view of every item (precomputed so the issue loop does one LDS.128 per item)
-  auto mma_of = [&](const Item& it, int mode) {
+  auto mma_of = [&](const Item& it, int mode, bool first_tile) {
     MmaItem mi{};
     mi.first = it.first;
     mi.nslabs = (uint8_t)it.nslabs;
@@ -503,11 +546,13 @@ p2s_status p2s_init(const p2s_basis* basis, const p2s_mlp* mlp, p2s_handle** out
     mi.n16 = (uint8_t)(op.N / 16);
     uint32_t off, sbo;
     if (op.layer == 0) { off = h->off_a1 + it.first * 256; sbo = h->a1_sbo; }
-    else if (op.layer == 2 && h->l3_hold_ks > 0 && it.first >= h->hold_k0 && it.first < h->hold_k0 + h->l3_hold_ks) {
+    else if (op.layer == 2 && h->l3_hold_ks > 0 && it.first >= h->hold_k0 && it.first < h->hold_k0 + h->l3_hold_ks &&
+             !(first_tile && h->n_fops > 0)) {
       off = h->off_hold + (it.first - h->hold_k0) * 256; sbo = h->hold_sbo;
     } else { off = h->off_a2 + it.first * 256; sbo = h->a2_sbo; }
     mi.a_lo_rel = (off >> 4) | ((128u >> 4) << 16);
     mi.a_hi = (sbo >> 4) | (1u << 14);
+    mi.d_col = (uint16_t)op.d_col;
     uint16_t f = 0;
     if (it.flags & IT_BEGIN) f |= (op.layer == 0 && op.first_of_layer) ? MI_WAIT_A1 : MI_WAIT_SCR;
     if (it.flags & IT_END) {
@@ -518,9 +563,9 @@ p2s_status p2s_init(const p2s_basis* basis, const p2s_mlp* mlp, p2s_handle** out
     mi.flags = f;
     return mi;
   };
-  for (const Item& it : full) h->mma_items.push_back(mma_of(it, 0));
-  for (const Item& it : beta) h->mma_items.push_back(mma_of(it, 1));
-  for (const Item& it : first) h->mma_items.push_back(mma_of(it, 0));
+  for (const Item& it : full) h->mma_items.push_back(mma_of(it, 0, false));
+  for (const Item& it : beta) h->mma_items.push_back(mma_of(it, 1, false));
+  for (const Item& it : first) h->mma_items.push_back(mma_of(it, 0, true));
 
   // ---- constants: b1, b2 (kMaxN each), b3, svec (128 each), zero padded;
   //      svec[k] = sum of the taps of phi_k (centred-image identity)

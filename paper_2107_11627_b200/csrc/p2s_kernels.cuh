@@ -49,7 +49,7 @@ constexpr int kThreads = 32 * (kWarpEpi0 + kNumEpiWarps);  // 448
 constexpr int kBuildThreads = 32 * kNumBuildWarps;
 constexpr uint32_t kTmemCols = 512;
 constexpr int kMaxConvSteps = 512;
-constexpr int kMaxOps = 6;
+constexpr int kMaxOps = 8;
 constexpr int kMaxEy = 16, kMaxEx = 4;
 constexpr int kMaxN = 256;           // padded bias vectors
 
@@ -83,7 +83,7 @@ struct MmaItem {
   uint8_t nslabs;
   uint8_t n16;         // N / 16 (UMMA N; B half-slab = N rows/2 * 32 B = 16 N bytes)
   uint16_t flags;
-  uint16_t pad;
+  uint16_t d_col;      // MLP items: TMEM column of the accumulator
 };
 static_assert(sizeof(MmaItem) == 16, "MmaItem layout");
 
@@ -93,6 +93,8 @@ struct MlpOp {
   int n0, N;          // output columns [n0, n0+N) of the layer
   int nks;            // K-steps (input width / 16)
   int first_of_layer, last_of_layer;
+  int d_col;          // TMEM column of the accumulator (scratch; a CTA's first tile uses the
+                      // still-idle conv accumulator columns for whole-layer L1 / L2 ops)
 };
 
 constexpr int kMaxMaps = 6;
@@ -110,8 +112,9 @@ struct FusedParams {
   int n_items_full, n_items_beta, n_items_first;
   int tab_cap;                // entries of the shared-memory item tables
   int off_mma, off_steps;     // byte offsets of the MmaItem and conv-step tables
-  MlpOp ops[kMaxOps];
-  int n_ops;
+  MlpOp ops[kMaxOps];         // [0, n_ops): per-tile ops; then n_fops whole-layer L1/L2 ops
+  int n_ops, n_fops;          // drained in a CTA's first tile instead (mode 0)
+  int bias_folded;            // 1: b1..b3 ride in the packed weights (constant-1 padding inputs)
   int l3_hold_ks, hold_k0;    // L3 K-steps [hold_k0, hold_k0 + l3_hold_ks) read the hold buffer
   const MmaItem* mma_items;   // UMMA view of items (same order / modes as `items`)
   const uint32_t* conv_steps; // per conv K-step: descriptor low word (E-relative start>>4 | (LBO>>4)<<16)
@@ -181,6 +184,12 @@ __device__ __forceinline__ void tile_coords(const FusedParams& p, int t, int& b,
   x0 = s * kTileM;
 }
 
+// relu(a), relu(b) -> fp16x2 {lo = a, hi = b} in one cvt.rn.relu (RN; equals rn(relu(x)))
+__device__ __forceinline__ uint32_t cvt_relu_half2(float a, float b) {
+  uint32_t r;
+  asm("cvt.rn.relu.f16x2.f32 %0, %1, %2;" : "=r"(r) : "f"(b), "f"(a));
+  return r;
+}
 // fp32x2 -> fp16x2 (cvt.rn), then max(., 0) in fp16x2
 __device__ __forceinline__ uint32_t relu_half2(float2 a) {
   __half2 h = __hmax2(__float22half2_rn(a), __float2half2_rn(0.f));
@@ -318,7 +327,7 @@ __device__ __forceinline__ void build_E_all(const FusedParams& p, uint8_t* Eb, c
 template <int NC>
 __device__ __forceinline__ void conv_epi_group(uint32_t tl, int scr_col, int Nk, int gi, int C,
                                                const float* sB3, const float* sSv, float2 (&jc2)[3],
-                                               float2& bs2) {
+                                               float2& bs2, bool b3_folded) {
   float bv[NC], av[3][NC];
   tmem_ld_n<NC>(tl + scr_col + gi * 16, bv);
 #pragma unroll
@@ -336,8 +345,11 @@ __device__ __forceinline__ void conv_epi_group(uint32_t tl, int scr_col, int Nk,
     const float4 b3 = b34[i4], sv = sv4[i4];
 #endif
     const int i = 4 * i4;
-    const float2 be0 = __fadd2_rn(make_float2(bv[i], bv[i + 1]), make_float2(b3.x, b3.y));
-    const float2 be1 = __fadd2_rn(make_float2(bv[i + 2], bv[i + 3]), make_float2(b3.z, b3.w));
+    float2 be0 = make_float2(bv[i], bv[i + 1]), be1 = make_float2(bv[i + 2], bv[i + 3]);
+    if (!b3_folded) {
+      be0 = __fadd2_rn(be0, make_float2(b3.x, b3.y));
+      be1 = __fadd2_rn(be1, make_float2(b3.z, b3.w));
+    }
     bs2 = __ffma2_rn(be0, make_float2(sv.x, sv.y), bs2);
     bs2 = __ffma2_rn(be1, make_float2(sv.z, sv.w), bs2);
 #pragma unroll
@@ -462,7 +474,6 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads)
     const uint32_t ch16 = (uint32_t)p.chan_bytes >> 4;
     const uint32_t ebuf16 = 3u * ch16;
     const int C = p.C, nring = p.nring, ebufs = p.n_ebuf, mode = p.mode;
-    const uint32_t scr = tmem + (uint32_t)p.scr_col;
     const uint32_t acc1 = tmem + (uint32_t)p.Nk, acc2 = tmem + 2u * (uint32_t)p.Nk;
     const uint32_t smem_lo = smem_u32(smem) >> 4;
     const uint32_t id_base = idesc_f16(256, 0);
@@ -536,11 +547,12 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads)
         PROF_T0();
         const uint32_t idesc = id_base | ((uint32_t)cur.n16 << 18);  // N>>3 at bit 17
         const uint32_t a_lo0 = smem_lo + cur.a_lo_rel;
+        const uint32_t dacc = tmem + cur.d_col;
 #pragma unroll 2
         for (uint32_t j = 0; j < n; ++j) {
           const uint64_t ad = ((uint64_t)cur.a_hi << 32) | (a_lo0 + j * 16u);
           const uint64_t bd = ((uint64_t)hi_b << 32) | (b_lo0 + j * half16);
-          umma2_f16_elect(scr, ad, bd, idesc, (first + j) > 0);
+          umma2_f16_elect(dacc, ad, bd, idesc, (first + j) > 0);
           if (j == 0 && pending >= 0) { umma2_commit_elect(&ring_empty[pending]); pending = -1; }
         }
         PROF_ADD(6);
@@ -598,7 +610,9 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads)
         for (int k0 = 0; k0 < p.K1; k0 += 16) {
           float v[16];
 #pragma unroll
-          for (int i = 0; i < 16; ++i) v[i] = (k0 + i < p.n_in) ? __ldg(zp + (size_t)(k0 + i) * HW) : 0.f;
+          for (int i = 0; i < 16; ++i)
+            v[i] = (k0 + i < p.n_in) ? __ldg(zp + (size_t)(k0 + i) * HW)
+                                     : ((p.bias_folded && k0 + i < p.n_in + 2) ? 1.f : 0.f);
           *reinterpret_cast<uint4*>(dst + (k0 >> 3) * 128) = pack8(v);
           *reinterpret_cast<uint4*>(dst + ((k0 >> 3) + 1) * 128) = pack8(v + 8);
         }
@@ -670,12 +684,18 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads)
       const bool store = t_raw < p.ntiles;
       int b, y, x0;
       tile_coords(p, min(t_raw, p.ntiles - 1), b, y, x0);
-      for (int o = 0; o < p.n_ops; ++o) {
+      // a CTA's first tile (mode 0) runs L1 and L2 as whole-layer ops (p.ops[n_ops, +n_fops))
+      const bool fops = p.mode == 0 && it == 0 && p.n_fops > 0;
+      const int o_begin = fops ? p.n_ops : 0, o_end = fops ? p.n_ops + p.n_fops : p.n_ops;
+      for (int o = o_begin; o < o_end; ++o) {
         const MlpOp op = p.ops[o];
         if (op.layer == 2) continue;        // beta stays in TMEM for the conv epilogue
         { PROF_T0(); WAIT_EPI(&bars[BAR_MLP_DONE], mlp_waits & 1); PROF_ADD(13); }
         ++mlp_waits;
         tc_fence_after();
+#ifdef P2S_PROFILE
+        const long long td0 = clock64();
+#endif
         const float* bias = (op.layer == 0 ? sB1 : sB2) + op.n0;
         const int G = op.N >> 4;
         // L2 chunks other than the last go to the hold buffer (L3 reads them from there)
@@ -691,24 +711,30 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads)
           const int gi0 = wg + 4 * hp, gi1 = gi0 + 2;
           if (gi0 >= G) break;
           float v[2][16];
-          tmem_ld16(tl + p.scr_col + gi0 * 16, v[0]);
-          if (gi1 < G) tmem_ld16(tl + p.scr_col + gi1 * 16, v[1]);
+          tmem_ld16(tl + op.d_col + gi0 * 16, v[0]);
+          if (gi1 < G) tmem_ld16(tl + op.d_col + gi1 * 16, v[1]);
           tmem_ld_wait();
 #pragma unroll
           for (int u = 0; u < 2; ++u) {
             const int gi = gi0 + 2 * u;
             if (gi < G) {
-              // bias add in packed fp32x2, round to fp16x2 (RN), then ReLU in fp16x2: rounding is
-              // monotone and sign-preserving, so relu(rn(x)) == rn(relu(x))
-              const float4* b4 = reinterpret_cast<const float4*>(bias + gi * 16);
               uint32_t hv[8];
+              if (p.bias_folded) {
+                // bias already in the accumulator: one cvt.rn.relu.f16x2 per two values
 #pragma unroll
-              for (int i4 = 0; i4 < 4; ++i4) {
-                const float4 bb = b4[i4];
-                const float2 s0 = __fadd2_rn(make_float2(v[u][4 * i4 + 0], v[u][4 * i4 + 1]), make_float2(bb.x, bb.y));
-                const float2 s1 = __fadd2_rn(make_float2(v[u][4 * i4 + 2], v[u][4 * i4 + 3]), make_float2(bb.z, bb.w));
-                hv[2 * i4 + 0] = relu_half2(s0);
-                hv[2 * i4 + 1] = relu_half2(s1);
+                for (int i2 = 0; i2 < 8; ++i2) hv[i2] = cvt_relu_half2(v[u][2 * i2], v[u][2 * i2 + 1]);
+              } else {
+                // bias add in packed fp32x2, round to fp16x2 (RN), then ReLU in fp16x2: rounding
+                // is monotone and sign-preserving, so relu(rn(x)) == rn(relu(x))
+                const float4* b4 = reinterpret_cast<const float4*>(bias + gi * 16);
+#pragma unroll
+                for (int i4 = 0; i4 < 4; ++i4) {
+                  const float4 bb = b4[i4];
+                  const float2 s0 = __fadd2_rn(make_float2(v[u][4 * i4 + 0], v[u][4 * i4 + 1]), make_float2(bb.x, bb.y));
+                  const float2 s1 = __fadd2_rn(make_float2(v[u][4 * i4 + 2], v[u][4 * i4 + 3]), make_float2(bb.z, bb.w));
+                  hv[2 * i4 + 0] = relu_half2(s0);
+                  hv[2 * i4 + 1] = relu_half2(s1);
+                }
               }
               const int kc = kc0 + gi * 2;
 #ifndef P2S_ABL_NOA2
@@ -720,10 +746,17 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads)
             }
           }
         }
+#ifdef P2S_PROFILE
+        const long long td1 = clock64();
+#endif
         fence_proxy_async_smem();
         tc_fence_before();
         __syncwarp();
         if (lane == 0) mbar_arrive_remote(&bars[BAR_SCR_FREE], 0);
+#ifdef P2S_PROFILE
+        prof_acc[17] += (unsigned long long)(td1 - td0);
+        prof_acc[18] += (unsigned long long)(clock64() - td1);
+#endif
       }
       { PROF_T0(); WAIT_EPI(&bars[BAR_ACC_FULL], it & 1); PROF_ADD(15); }
       tc_fence_after();
@@ -740,7 +773,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads)
           tmem_ld_wait();
           if (store && x < p.W)
             for (int i = 0; i < 16 && gi * 16 + i < p.K; ++i)
-              p.beta_out[((size_t)b * p.K + gi * 16 + i) * HW + (size_t)y * p.W + x] = bv[i] + sB3[gi * 16 + i];
+              p.beta_out[((size_t)b * p.K + gi * 16 + i) * HW + (size_t)y * p.W + x] = bv[i] + (p.bias_folded ? 0.f : sB3[gi * 16 + i]);
         }
       } else {
         // packed fp32x2 accumulation: lane .x sums even k, .y odd k (combined after the loop)
@@ -753,8 +786,8 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads)
 #endif
           // a tail group with <= 4 real columns (K % 16 in 1..4, e.g. K = 100) reads only those:
           // the columns past K are zero padding (N % 16 == 0)
-          if (gi == GF && tail <= 4) conv_epi_group<4>(tl, p.scr_col, p.Nk, gi, C, sB3, sSv, jc2, bs2);
-          else conv_epi_group<16>(tl, p.scr_col, p.Nk, gi, C, sB3, sSv, jc2, bs2);
+          if (gi == GF && tail <= 4) conv_epi_group<4>(tl, p.scr_col, p.Nk, gi, C, sB3, sSv, jc2, bs2, p.bias_folded != 0);
+          else conv_epi_group<16>(tl, p.scr_col, p.Nk, gi, C, sB3, sSv, jc2, bs2, p.bias_folded != 0);
         }
         float jc[3] = {jc2[0].x + jc2[0].y, jc2[1].x + jc2[1].y, jc2[2].x + jc2[2].y};
         float bs = bs2.x + bs2.y;

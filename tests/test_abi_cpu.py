@@ -90,9 +90,13 @@ def test_sass_has_tcgen05_and_tma(lib):
     # no per-UMMA divergence/elect loops (a silent 1.5x slowdown when uniformity is lost)
     fused = sass[sass.index("k_fused_p2s"):]
     fused = fused[:fused.index("Function :")] if "Function :" in fused else fused
-    assert "BRA.DIV" not in fused
     ins = [l.split("*/", 1)[1].strip() for l in fused.split("\n") if l.strip().startswith("/*") and "*/" in l
            and not l.strip().startswith("/* 0x")]
-    for n, l in enumerate(ins):
-        if "UTCHMMA" in l:  # the 12 instructions feeding each UMMA must use uniform operands only
-            assert not any("R2UR.BROADCAST" in x for x in ins[max(0, n - 12):n]), ins[max(0, n - 12):n + 1]
+    mma = [n for n, l in enumerate(ins) if "UTCHMMA" in l]
+    assert mma
+    # the issue loop region: no divergence checks, no elect loops, no per-UMMA lane broadcasts
+    region = ins[max(0, mma[0] - 60):mma[-1] + 60]
+    for bad in ("BRA.DIV", "BRA.U.ANY", "R2UR.BROADCAST"):
+        assert not any(bad in x for x in region), bad
+    for n in mma:  # the 12 instructions feeding each UMMA must use uniform operands only
+        assert not any("R2UR.BROADCAST" in x for x in ins[max(0, n - 12):n]), ins[max(0, n - 12):n + 1]

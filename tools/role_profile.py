@@ -19,6 +19,8 @@ from paper_2107_11627_b200 import p2s, synth  # noqa: E402
 
 cfg = int(sys.argv[1]) if len(sys.argv) > 1 else 3
 spec = synth.CONFIGS[cfg]
+if os.environ.get("TRACE_H"):
+    spec = synth.custom("h", cfg, B=1, C=spec.C, H=int(os.environ["TRACE_H"]), W=spec.W, K=spec.K, S=spec.S, h1=spec.h1, h2=spec.h2)
 inp = synth.make_inputs(spec, frames=range(1))
 r = p2s.Renderer(inp.basis, inp.mlp)
 img, z, t = (torch.from_numpy(a).cuda() for a in (inp.image, inp.zernike, inp.tilt))
@@ -35,7 +37,7 @@ names = {0: {0: "wait A1_FULL", 1: "wait TMEM_FREE", 2: "wait SCR_FREE", 3: "wai
              4: "conv UMMA loops", 6: "MLP UMMA loops", 19: "total"},
          1: {7: "wait ring_empty", 19: "total"},
          2: {9: "wait A1_EMPTY", 11: "wait E_EMPTY", 12: "build E", 19: "total"},
-         3: {13: "wait MLP_DONE", 15: "wait ACC_FULL", 16: "conv epi to release", 19: "total"}}
+         3: {13: "wait MLP_DONE", 15: "wait ACC_FULL", 16: "conv epi to release", 17: "MLP drain work", 18: "drain fence+arrive", 19: "total"}}
 roles = ["MMA", "producer", "builder", "epilogue"]
 ntiles = spec.H * ((spec.W + 127) // 128)
 print(f"cfg{cfg}: {ntiles} tiles over 148 CTAs (~{ntiles / 148:.1f} tiles/CTA); cycles per CTA (mean / max)")
