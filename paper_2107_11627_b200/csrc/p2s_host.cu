@@ -217,6 +217,32 @@ p2s_status launch_fused(p2s_handle* h, const FusedParams& p, cudaStream_t st) {
   return P2S_OK;
 }
 
+// Tilt warp (step a3), launched as a programmatic dependent of the fused kernel on `st`
+// (its launch and tilt loads overlap the fused kernel's tail; it waits for J on the device).
+p2s_status launch_warp(const p2s_handle* h, const float* J, const float* tilt, float* out, int B, int C,
+                       int H, int W, cudaStream_t st) {
+  const size_t npx = (size_t)B * H * W;
+  const bool vec = (W % 4) == 0 && ((uintptr_t)J % 16) == 0 && ((uintptr_t)out % 16) == 0 &&
+                   ((uintptr_t)tilt % 16) == 0;
+  cudaLaunchConfig_t cfg{};
+  cudaLaunchAttribute attr[1];
+  attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  attr[0].val.programmaticStreamSerializationAllowed = 1;
+  cfg.attrs = attr;
+  cfg.numAttrs = 1;
+  cfg.blockDim = dim3(256);
+  cfg.dynamicSmemBytes = 0;
+  cfg.stream = st;
+  if (vec) {
+    cfg.gridDim = dim3((unsigned)((npx / 4 + 255) / 256));
+    P2S_CUDA(cudaLaunchKernelEx(&cfg, k_tilt_warp4, J, tilt, out, B, C, H, W));
+  } else {
+    cfg.gridDim = dim3((unsigned)std::min<size_t>((npx + 255) / 256, (size_t)h->sm_count * 16));
+    P2S_CUDA(cudaLaunchKernelEx(&cfg, k_tilt_warp, J, tilt, out, B, C, H, W));
+  }
+  return P2S_OK;
+}
+
 p2s_status check_image(const p2s_handle* h, const p2s_image& im) {
   if (!h || !im.data) return P2S_ERR_INVALID_ARG;
   if (im.B < 1 || im.H < 1 || im.W < 1 || im.C < 1) return P2S_ERR_INVALID_ARG;
@@ -661,10 +687,8 @@ static p2s_status render_impl(p2s_handle* h, p2s_image im, const float* z, const
   if (s != P2S_OK) return s;
   if (h->ev_end) P2S_CUDA(cudaEventRecord(h->ev_end, st));
   if (out) {
-    const size_t npx = (size_t)im.B * im.H * im.W;
-    const int grid = (int)std::min<size_t>((npx + 255) / 256, (size_t)h->sm_count * 16);
-    k_tilt_warp<<<grid, 256, 0, st>>>(J, tilt, out, im.B, im.C, im.H, im.W);
-    P2S_CUDA(cudaPeekAtLastError());
+    p2s_status sw = launch_warp(h, J, tilt, out, im.B, im.C, im.H, im.W, st);
+    if (sw != P2S_OK) return sw;
   }
   return P2S_OK;
 }
@@ -782,9 +806,8 @@ p2s_status p2s_render_host(p2s_handle* h, const float* image_host, int B, int C,
       mark("band rendered", st);
       y0 += ny;
     }
-    const int grid = (int)std::min<size_t>((HW + 255) / 256, (size_t)h->sm_count * 16);
-    k_tilt_warp<<<grid, 256, 0, st>>>(h->d_J, tilt_host ? h->h_t + fo_t : nullptr, h->h_out + fo_img, 1, C, H, W);
-    P2S_CUDA(cudaPeekAtLastError());
+    s = launch_warp(h, h->d_J, tilt_host ? h->h_t + fo_t : nullptr, h->h_out + fo_img, 1, C, H, W, st);
+    if (s != P2S_OK) return s;
     mark("warped", st);
     P2S_CUDA(cudaMemcpyAsync(out_host + fo_img, h->h_out + fo_img, (size_t)C * HW * 4, cudaMemcpyDeviceToHost, st));
     mark("out copied", st);

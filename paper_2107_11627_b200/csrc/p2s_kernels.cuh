@@ -833,6 +833,9 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads)
         if (prof_acc[i]) p.prof[((size_t)blockIdx.x * 4 + base) * 20 + i] = prof_acc[i];
   }
 #endif
+  // dependents (the warp kernel) may launch once every CTA got here; they still wait for this
+  // grid's completion (griddepcontrol.wait) before reading J
+  asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
   // ---- teardown: no CTA leaves while its pair may still touch its shared memory / TMEM
   tc_fence_before();
   __syncthreads();
@@ -842,8 +845,57 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads)
 }
 
 // Step a3: out(y,x) = bilinear J at (y - t1, x - t0), clamp-to-edge; all channels per thread.
+// Vectorised warp for W % 4 == 0: four consecutive pixels of a row per thread (float4 tilt
+// loads and output stores; the 4 x C gathers per pixel stay scalar). Launched as a programmatic
+// dependent of k_fused_p2s: the tilt (independent of J) is loaded before griddepcontrol.wait,
+// so its HBM latency and the launch overlap the fused kernel's tail.
+__global__ void __launch_bounds__(256) k_tilt_warp4(const float* __restrict__ J, const float* __restrict__ tilt,
+                                                    float* __restrict__ out, int B, int C, int H, int W) {
+  const size_t HW = (size_t)H * W;
+  const size_t nq = (size_t)B * HW / 4;
+  const size_t q = blockIdx.x * (size_t)blockDim.x + threadIdx.x;
+  float4 tx = make_float4(0.f, 0.f, 0.f, 0.f), ty = tx;
+  size_t b = 0, pix = 0;
+  if (q < nq) {
+    b = (q * 4) / HW;
+    pix = q * 4 - b * HW;
+    if (tilt) {
+      tx = __ldg(reinterpret_cast<const float4*>(tilt + (b * 2 + 0) * HW + pix));
+      ty = __ldg(reinterpret_cast<const float4*>(tilt + (b * 2 + 1) * HW + pix));
+    }
+  }
+  asm volatile("griddepcontrol.wait;" ::: "memory");  // J is complete past this point
+  if (q >= nq) return;
+  const int y = (int)(pix / W), x = (int)(pix - (size_t)y * W);
+  const float txs[4] = {tx.x, tx.y, tx.z, tx.w}, tys[4] = {ty.x, ty.y, ty.z, ty.w};
+  int o00[4], o01[4], o10[4], o11[4];
+  float w00[4], w01[4], w10[4], w11[4];
+#pragma unroll
+  for (int e = 0; e < 4; ++e) {
+    const float sy = fminf(fmaxf((float)y - tys[e], -1.f), (float)H);
+    const float sx = fminf(fmaxf((float)(x + e) - txs[e], -1.f), (float)W);
+    const float fy0 = floorf(sy), fx0 = floorf(sx);
+    const float fy = sy - fy0, fx = sx - fx0;
+    const int y0 = (int)fy0, x0 = (int)fx0;
+    const int ya = clampi(y0, 0, H - 1), yb = clampi(y0 + 1, 0, H - 1);
+    const int xa = clampi(x0, 0, W - 1), xb = clampi(x0 + 1, 0, W - 1);
+    o00[e] = ya * W + xa; o01[e] = ya * W + xb; o10[e] = yb * W + xa; o11[e] = yb * W + xb;
+    w00[e] = (1.f - fy) * (1.f - fx); w01[e] = (1.f - fy) * fx; w10[e] = fy * (1.f - fx); w11[e] = fy * fx;
+  }
+  for (int c = 0; c < C; ++c) {
+    const float* Jc = J + (b * C + c) * HW;
+    float v[4];
+#pragma unroll
+    for (int e = 0; e < 4; ++e)
+      v[e] = w00[e] * __ldg(Jc + o00[e]) + w01[e] * __ldg(Jc + o01[e]) + w10[e] * __ldg(Jc + o10[e]) +
+             w11[e] * __ldg(Jc + o11[e]);
+    *reinterpret_cast<float4*>(out + (b * C + c) * HW + pix) = make_float4(v[0], v[1], v[2], v[3]);
+  }
+}
+
 __global__ void __launch_bounds__(256) k_tilt_warp(const float* __restrict__ J, const float* __restrict__ tilt,
                                                    float* __restrict__ out, int B, int C, int H, int W) {
+  asm volatile("griddepcontrol.wait;" ::: "memory");
   const size_t HW = (size_t)H * W;
   const size_t n = (size_t)B * HW;
   for (size_t i = blockIdx.x * (size_t)blockDim.x + threadIdx.x; i < n; i += (size_t)gridDim.x * blockDim.x) {

@@ -34,7 +34,7 @@ ours = {k: v for k, v in tot.items() if k.startswith("p2s::")}
 step_ns = sum(ours.values()) / max(cnt.get("p2s::k_fused_p2s", 1), 1)
 with open(os.path.join(PROF, f"{tag}_launch_shares.txt"), "w") as f:
     f.write("ncu --metrics gpu__time_duration.sum --clock-control none (cold-cache, serialised launches)\n")
-    f.write("of: python bench.py --steps 5 --warmup 3 --no-cpu-baseline\n\n")
+    f.write("of: python bench.py --steps 5 --warmup 3 --no-cpu-baseline --no-e2e\n\n")
     for k in sorted(tot, key=lambda k: -tot[k]):
         f.write(f"{tot[k] / cnt[k] / 1e3:10.1f} us/launch x{cnt[k]:3d}  {k}\n")
     f.write("\nshare of one p2s_render (our kernels only):\n")
