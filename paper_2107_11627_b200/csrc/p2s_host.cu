@@ -325,14 +325,10 @@ p2s_status p2s_init(const p2s_basis* basis, const p2s_mlp* mlp, p2s_handle** out
       h->ops[h->n_ops++] = MlpOp{l, 0, w0, layer_K[l] / 16, 0, 1, h->scr_col};
     }
   }
-  // A CTA's first tile has no conv accumulator to protect yet: its L1 and L2 run as single
-  // whole-layer ops into TMEM columns [0, N1) and [N1, N1 + N2) (two drain round trips instead
-  // of four; L2's output goes straight to A2, L3 then reads all of it from A2).
+  // (Whole-layer L1/L2 ops for a CTA's first tile, in its still idle accumulator columns, were
+  // superseded by building that tile's E views in the epilogue warps and interleaving it like
+  // every other tile; the kernel keeps the n_fops hook, unused: n_fops = 0.)
   h->n_fops = 0;
-  if (h->N1 + h->N2 <= 512) {
-    h->ops[h->n_ops + h->n_fops++] = MlpOp{0, 0, h->N1, h->K1 / 16, 1, 1, 0};
-    h->ops[h->n_ops + h->n_fops++] = MlpOp{1, 0, h->N2, h->N1 / 16, 1, 1, h->N1};
-  }
 
   // The first-issued L2 chunk is parked in a "hold" buffer that L3 reads directly (the other
   // L2 chunk still reads A2); L3 K-steps [hold_k0, hold_k0 + hold_cols/16) come from it.
@@ -536,18 +532,10 @@ p2s_status p2s_init(const p2s_basis* basis, const p2s_mlp* mlp, p2s_handle** out
       for (int k = 0; k < per_gap && ci + 1 < conv_items.size(); ++k) full.push_back(conv_items[ci++]);
   }
   while (ci < conv_items.size()) full.push_back(conv_items[ci++]);
-  // First tile of every CTA: all MLP ops before the conv stages (its first im2col views take
-  // ~10 us of cold loads to build, longer than the MLP chain; interleaving measured slower).
-  // With whole-layer first-tile ops: [L1 (N1) | L2 (N2) | L3 (reads A2 only) | conv].
-  std::vector<Item> first;
-  if (h->n_fops > 0) {
-    for (int o = h->n_ops; o < h->n_ops + h->n_fops; ++o)
-      make_items(op_off[o], h->ops[o].nks, h->ops[o].N, 0, (uint8_t)o, first);
-    for (const Item& it : full) if (it.kind == 0 && h->ops[it.op].layer == 2) first.push_back(it);
-  } else {
-    for (const Item& it : full) if (it.kind == 0) first.push_back(it);
-  }
-  for (const Item& it : full) if (it.kind == 1) first.push_back(it);
+  // First tile of every CTA: the epilogue warps build its E views up front (they are idle until
+  // the first MLP chunk), so it uses the steady interleaved order too (MLP-first, or whole-layer
+  // first-tile MLP ops, measured slower: the builders' A1 + E chain of cold loads took ~10 us).
+  std::vector<Item> first = full;
   h->n_items_full = (int)full.size();
   h->n_items_beta = (int)beta.size();
   h->n_items_first = (int)first.size();

@@ -271,6 +271,7 @@ __device__ __forceinline__ void load_ex(const FusedParams& p, const float* img, 
     for (int q = 0; q < 12; ++q) v[q] = __ldg(row + clampi(col0 + q, 0, p.W - 1));
   }
 }
+template <int NT>
 __device__ __forceinline__ void build_E_all(const FusedParams& p, uint8_t* Eb, const float* img_b, int y, int x0,
                                             int tid) {
   const int cx0 = x0 - p.rr;
@@ -278,8 +279,8 @@ __device__ __forceinline__ void build_E_all(const FusedParams& p, uint8_t* Eb, c
   const size_t HW = (size_t)p.H * p.W;
   const int ngy = p.npos_y >> 2, per_c_y = p.n_ey * ngy;
   const int tot_y = p.C * per_c_y;
-  for (int w = tid; w < tot_y; w += 2 * kBuildThreads) {
-    const int w2 = w + kBuildThreads;
+  for (int w = tid; w < tot_y; w += 2 * NT) {
+    const int w2 = w + NT;
     const int c0 = w / per_c_y, r0 = w - c0 * per_c_y, blk0 = r0 / ngy, g0 = r0 - blk0 * ngy;
     float v0[4][8], v1[4][8];
     load_ey(p, img_b + c0 * HW, y, cx0, blk0, g0, vec, v0);
@@ -297,8 +298,8 @@ __device__ __forceinline__ void build_E_all(const FusedParams& p, uint8_t* Eb, c
   const int ngx = p.npos_x >> 2, per_c_x = p.n_ex * ngx;
   const int tot_x = p.C * per_c_x;
   const size_t xoff = (size_t)p.n_ey * p.npos_y * 16;
-  for (int w = tid; w < tot_x; w += 2 * kBuildThreads) {
-    const int w2 = w + kBuildThreads;
+  for (int w = tid; w < tot_x; w += 2 * NT) {
+    const int w2 = w + NT;
     const int c0 = w / per_c_x, r0 = w - c0 * per_c_x, e0 = r0 / ngx, g0 = r0 - e0 * ngx;
     float v0[12], v1[12];
     load_ex(p, img_b + c0 * HW, y, cx0, e0, g0, vec, v0);
@@ -621,15 +622,16 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads)
       __syncwarp();
       if (lane == 0) mbar_arrive_remote(&bars[BAR_A1_FULL], 0);
       if (p.mode != 0) continue;
-      // --- E views of every channel
+      // --- E views of every channel (the CTA's first tile: built by the idle epilogue warps)
       const int eb = p.n_ebuf == 2 ? (it & 1) : 0;
+      if (it == 0) { ++e_use0; continue; }
       { PROF_T0(); WAIT_BUILD(&bars[BAR_E_EMPTY0 + eb], ((eb ? e_use1 : e_use0) & 1) ^ 1); PROF_ADD(11); }
       if (eb) ++e_use1; else ++e_use0;
       uint8_t* Eb = sE + (size_t)eb * 3 * p.chan_bytes;  // buffers are sized for C = 3
       {
         PROF_T0();
 #ifndef P2S_ABL_NOE
-        build_E_all(p, Eb, p.image + (size_t)b * p.C * HW, y, x0, tid);
+        build_E_all<kBuildThreads>(p, Eb, p.image + (size_t)b * p.C * HW, y, x0, tid);
 #endif
         PROF_ADD(12);
       }
@@ -639,34 +641,22 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads)
     }
   } else if (warp >= kWarpEpi0) {
     // ================= epilogue: two warpgroups split every TMEM drain by 16-col groups =====
-    // ---- first tile's inputs -> L2 (the epilogue warps idle until its first MLP chunk): the
-    // builders' Zernike / image loads for it are otherwise a chain of cold HBM round trips.
-    // (Done here, not in the shared prologue: a tile_coords() there cost the UMMA issuer its
-    // convergence proof - ptxas then wraps every elect in a loop; test_abi_cpu checks the SASS.)
-    if (pr_begin < pr_end) {
+    // ---- the CTA's first tile: its E views (E buffer 0) come from the 8 epilogue warps, idle
+    // until the first MLP chunk, so the first conv stage does not wait for the builders' A1 + E
+    // chain of cold loads. (tile_coords() here, not in the shared prologue: there it cost the
+    // UMMA issuer its convergence proof - ptxas then wraps every elect in a loop; test_abi_cpu
+    // checks the SASS.)
+    if (pr_begin < pr_end && p.mode == 0) {
       int b0, y0, xs;
       tile_coords(p, min(2 * pr_begin + (int)rank, p.ntiles - 1), b0, y0, xs);
-      const int e0 = (warp - kWarpEpi0) * 32;
-      const size_t HW = (size_t)p.H * p.W;
-      const float* zt = p.zernike + (size_t)b0 * p.n_in * HW + (size_t)y0 * p.W;
-      const int nz = p.n_in * 5;
-      for (int i0 = e0; i0 < nz; i0 += 32 * kNumEpiWarps) {
-        const int i = i0 + lane;
-        if (i < nz) prefetch_l2(zt + (size_t)(i / 5) * HW + min(xs + (i % 5) * 32, p.W - 1));
-      }
-      if (p.mode == 0) {
-        const int S = 2 * p.r + 1;
-        const float* it0 = p.image + (size_t)b0 * p.C * HW;
-        const int ni = p.C * S * 7;
-        for (int i0 = e0; i0 < ni; i0 += 32 * kNumEpiWarps) {
-          const int i = i0 + lane;
-          if (i < ni) {
-            const int c = i / (S * 7), rr = (i / 7) % S, l = i % 7;
-            const int row = clampi(y0 - p.r + rr, 0, p.H - 1), col = clampi(xs - p.rr + l * 32, 0, p.W - 1);
-            prefetch_l2(it0 + (size_t)c * HW + (size_t)row * p.W + col);
-          }
-        }
-      }
+      const size_t HW0 = (size_t)p.H * p.W;
+#ifndef P2S_ABL_NOE
+      build_E_all<32 * kNumEpiWarps>(p, sE, p.image + (size_t)b0 * p.C * HW0, y0, xs,
+                                     (warp - kWarpEpi0) * 32 + lane);
+#endif
+      fence_proxy_async_smem();
+      named_bar_sync(2, 32 * kNumEpiWarps);
+      if (warp - kWarpEpi0 < kNumBuildWarps && lane == 0) mbar_arrive_remote(&bars[BAR_E_FULL0], 0);
     }
     const int ew = warp - kWarpEpi0;        // 0..7
     const int wg = ew >> 2;                 // warpgroup 0 / 1

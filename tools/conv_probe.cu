@@ -132,6 +132,62 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(128, 1) k_qdepth(uns
   if (warp_id() == 0) tmem_dealloc2<512>(tmem);
 }
 
+// Accumulator dependency: UMMAs (M=256, width N) rotating over NACC independent accumulators,
+// A descriptor fixed or walking (16-B steps, like the conv / MLP K-loops).
+template <int N, int NACC, bool WALK>
+__global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(128, 1) k_dep(int iters, unsigned long long* cyc) {
+  extern __shared__ __align__(1024) uint8_t smem[];
+  __shared__ uint64_t bar;
+  __shared__ uint32_t tslot;
+  for (int i = threadIdx.x * 16; i < 160 * 1024; i += 128 * 16) {
+    const uint32_t h = (uint32_t)i * 2654435761u;
+    *reinterpret_cast<int4*>(smem + i) = make_int4((int)(h & 0x3bff3bff), (int)((h >> 3) & 0x3bff3bff), 0, 0);
+  }
+  fence_proxy_async_smem();
+  if (threadIdx.x == 0) { mbar_init(&bar, 1); fence_mbar_init(); }
+  if (warp_id() == 0) tmem_alloc2<512>(&tslot);
+  tc_fence_before();
+  __syncthreads();
+  cluster_sync();
+  tc_fence_after();
+  const uint32_t tmem = tslot;
+  if (warp_id() == 0 && cluster_ctarank() == 0) {
+    const uint32_t id = idesc_f16(256, N);
+    const uint32_t a0 = smem_u32(smem) >> 4, b0 = (smem_u32(smem + 96 * 1024) >> 4) | ((128u >> 4) << 16);
+    const uint32_t hi_a = (3328u >> 4) | (1u << 14), hi_b = (256u >> 4) | (1u << 14);
+    long long t0 = clock64();
+    for (int it = 0; it < iters; ++it) {
+      const int acc = it % NACC;
+      const uint32_t alo = (a0 + (WALK ? (uint32_t)(it % 13) * 16u : 0u)) | ((128u >> 4) << 16);
+      const uint32_t blo = b0 + (uint32_t)(it % 13) * (uint32_t)(N * 16 / 16);
+      umma2_f16_elect(tmem + acc * 128, ((uint64_t)hi_a << 32) | alo, ((uint64_t)hi_b << 32) | blo, id, 1);
+    }
+    umma2_commit_elect(&bar);
+    mbar_wait(&bar, 0);
+    long long t1 = clock64();
+    if (lane_id() == 0) cyc[blockIdx.x] = (unsigned long long)(t1 - t0);
+  }
+  tc_fence_before();
+  __syncthreads();
+  cluster_sync();
+  if (warp_id() == 0) tmem_dealloc2<512>(tmem);
+}
+template <int N, int NACC, bool WALK>
+static void run_dep(int nsm) {
+  unsigned long long* dc; CK(cudaMalloc(&dc, 1024 * 8)); CK(cudaMemset(dc, 0, 1024 * 8));
+  auto k = k_dep<N, NACC, WALK>;
+  CK(cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, 160 * 1024));
+  const int iters = 3900;
+  for (int w = 0; w < 2; ++w) { k<<<nsm, 128, 160 * 1024>>>(iters, dc); CK(cudaGetLastError()); CK(cudaDeviceSynchronize()); }
+  std::vector<unsigned long long> c(nsm);
+  CK(cudaMemcpy(c.data(), dc, nsm * 8, cudaMemcpyDeviceToHost));
+  double mean = 0; int nl = 0;
+  for (int i = 0; i < nsm; i += 2) { mean += c[i]; ++nl; }
+  printf("dep N=%3d accumulators=%d A=%s: %.1f cyc/UMMA (floor %d)\n", N, NACC, WALK ? "walk " : "fixed",
+         mean / nl / iters, N / 2);
+  cudaFree(dc);
+}
+
 // TMEM -> register bandwidth: NW warps (quadrant = warp % 4), each loading NL x (32 lanes x
 // X columns) per tcgen05.wait::ld, for `iters` rounds over 448 columns.
 template <int X>
@@ -237,8 +293,10 @@ int main() {
     for (int j = 0; j < 64; ++j) printf("%s%llu", j % 16 ? " " : "\n  ", h[j]);
     printf("\n  all 64 complete at %llu\n", h[64]);
   }
-  for (int nw : {4, 8, 12, 16}) { run_tmem_bw<16, 1>(nw); run_tmem_bw<16, 2>(nw); run_tmem_bw<16, 4>(nw); }
-  run_tmem_bw<8, 4>(8); run_tmem_bw<4, 4>(8); run_tmem_bw<16, 6>(8);
+  run_dep<80, 1, false>(nsm); run_dep<80, 1, true>(nsm); run_dep<80, 2, true>(nsm); run_dep<80, 3, true>(nsm);
+  run_dep<112, 1, false>(nsm); run_dep<112, 1, true>(nsm); run_dep<112, 2, true>(nsm); run_dep<112, 3, true>(nsm);
+  run_dep<128, 1, true>(nsm); run_dep<128, 2, true>(nsm);
+  run_dep<208, 1, true>(nsm); run_dep<208, 2, true>(nsm);
   printf("PROBE DONE\n");
   return 0;
 }
