@@ -44,8 +44,9 @@ def _load():
         lib.p2s_oracle_render.argtypes = common + [i, i, d, d, i]
         lib.p2s_oracle_pixels.argtypes = common + [ctypes.POINTER(ctypes.c_int), i, d, d, i]
         lib.p2s_oracle_warp.argtypes = [d, i, i, i, i, f, d, i]
+        lib.p2s_oracle_interp_anchors.argtypes = [f, i, i, i, i, i, d]
         for fn in (lib.p2s_oracle_beta, lib.p2s_oracle_render, lib.p2s_oracle_pixels,
-                   lib.p2s_oracle_warp):
+                   lib.p2s_oracle_warp, lib.p2s_oracle_interp_anchors):
             fn.restype = i
         _lib = lib
     return _lib
@@ -141,5 +142,17 @@ def warp(J, tilt, threads=None) -> np.ndarray:
     rc = _load().p2s_oracle_warp(_dp(J), B, C, H, W,
                                  _fp(t) if t is not None else ctypes.POINTER(ctypes.c_float)(),
                                  _dp(out), threads or default_threads())
+    assert rc == 0
+    return out
+
+
+def interp_anchors(anchors, H, W) -> np.ndarray:
+    """Anchor grid [B][n_in][G][G] -> dense Zernike field [B][n_in][H][W] (fp64), bilinear per
+    mode with the corner / half-pixel registration of p2s_oracle.cpp."""
+    a = np.ascontiguousarray(anchors, np.float32)
+    B, n_in, G, G2 = a.shape
+    assert G == G2
+    out = np.zeros((B, n_in, H, W), np.float64)
+    rc = _load().p2s_oracle_interp_anchors(_fp(a), B, n_in, G, H, W, _dp(out))
     assert rc == 0
     return out

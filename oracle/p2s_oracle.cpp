@@ -28,6 +28,16 @@
 //          + fy (1-fx) J[cY(y0+1)][cX(x0)] + fy fx J[cY(y0+1)][cX(x0+1)]
 //    No output clamp (A12).
 //
+//  anchor grid (Sec. 3.4 "partition the image into a
+//    user-defined grid of anchor points ... interpolate the Zernike coefficients using
+//    bilinear interpolation"): a G x G grid of coefficient vectors, registered to the image
+//    corners with half-pixel alignment (reading N1): pixel (y, x) has continuous
+//    centre (y + 0.5, x + 0.5) in [0, H] x [0, W]; anchor (i, j) sits at (i H/(G-1), j W/(G-1)).
+//      u = (y + 0.5)(G-1)/H, i0 = min(floor(u), G-2), fy = u - i0   (v, j0, fx likewise)
+//      z_k(y,x) = (1-fy)(1-fx) A_k[i0][j0] + (1-fy) fx A_k[i0][j0+1]
+//               + fy (1-fx) A_k[i0+1][j0] + fy fx A_k[i0+1][j0+1]      (each mode k separately)
+//    G = 1: constant field. The dense field then feeds step a1 exactly as a given field does.
+//
 // Parity pins for every function live in tests/test_oracle_pins.py (closed forms,
 // invariants, library routines: torch nn.Linear, scipy.ndimage.convolve,
 // torch grid_sample, FFT convolution).
@@ -275,6 +285,28 @@ int p2s_oracle_warp(const double* J, int B, int C, int H, int W, const float* ti
       }
     });
   }
+  return 0;
+}
+
+// Anchor grid -> dense Zernike field (see the header): anchors [B][n_in][G][G] fp32,
+// field [B][n_in][H][W] fp64 (rounded to fp32 by the caller when it feeds the render).
+int p2s_oracle_interp_anchors(const float* anchors, int B, int n_in, int G, int H, int W, double* field) {
+  if (!anchors || !field || B < 1 || n_in < 1 || G < 1 || H < 1 || W < 1) return -1;
+  const size_t HW = (size_t)H * W, GG = (size_t)G * G;
+  for (int b = 0; b < B; ++b)
+    for (int k = 0; k < n_in; ++k) {
+      const float* A = anchors + ((size_t)b * n_in + k) * GG;
+      double* F = field + ((size_t)b * n_in + k) * HW;
+      for (int y = 0; y < H; ++y)
+        for (int x = 0; x < W; ++x) {
+          if (G == 1) { F[(size_t)y * W + x] = A[0]; continue; }
+          const double u = (y + 0.5) * (G - 1) / H, v = (x + 0.5) * (G - 1) / W;
+          const int i0 = std::min((int)std::floor(u), G - 2), j0 = std::min((int)std::floor(v), G - 2);
+          const double fy = u - i0, fx = v - j0;
+          F[(size_t)y * W + x] = (1 - fy) * (1 - fx) * A[(size_t)i0 * G + j0] + (1 - fy) * fx * A[(size_t)i0 * G + j0 + 1] +
+                                 fy * (1 - fx) * A[(size_t)(i0 + 1) * G + j0] + fy * fx * A[(size_t)(i0 + 1) * G + j0 + 1];
+        }
+    }
   return 0;
 }
 

@@ -289,3 +289,59 @@ def test_thread_count_does_not_change_results():
     a, _ = oracle.render(inp.image, inp.zernike, inp.tilt, inp.basis, inp.mlp, threads=1)
     b, _ = oracle.render(inp.image, inp.zernike, inp.tilt, inp.basis, inp.mlp, threads=5)
     np.testing.assert_array_equal(a, b)
+
+
+# ---- anchor grid -> dense Zernike field (Sec. 3.4;
+#      registration: DESIGN.md reading N1 — pixel centres at (y + 0.5, x + 0.5), anchors spanning
+#      the image corner to corner at (i H/(G-1), j W/(G-1)))
+
+def _anchor_coords(G, H, W):
+    return np.arange(G) * H / (G - 1), np.arange(G) * W / (G - 1)
+
+
+def test_anchor_interp_constant_and_single_anchor():
+    """Constant anchors give a constant field; G = 1 is a constant field (closed forms)."""
+    a = np.full((2, 3, 5, 5), 0.375, np.float32)
+    np.testing.assert_allclose(oracle.interp_anchors(a, 17, 23), 0.375, rtol=0, atol=1e-15)  # fp64 weights
+    a1 = np.array([[[[1.25]], [[-0.5]]]], np.float32)
+    f1 = oracle.interp_anchors(a1, 7, 9)
+    assert np.array_equal(f1[0, 0], np.full((7, 9), 1.25)) and np.array_equal(f1[0, 1], np.full((7, 9), -0.5))
+
+
+@pytest.mark.parametrize("G,H,W", [(2, 8, 8), (5, 37, 21), (16, 64, 96), (9, 512, 200)])
+def test_anchor_interp_reproduces_bilinear_functions(G, H, W):
+    """Bilinear interpolation reproduces any function a + b u + c v + d u v exactly, so with
+    anchors sampled from one the field must equal it at the pixel centres (y+0.5, x+0.5): a
+    shifted or scaled registration, a swapped axis or a wrong weight fails."""
+    u, v = _anchor_coords(G, H, W)
+    co = (0.25, -0.125, 0.0625, 0.001953125)  # dyadic: exact in fp32
+    f = lambda uu, vv: co[0] + co[1] * uu + co[2] * vv + co[3] * uu * vv  # noqa: E731
+    A = f(u[:, None], v[None, :]).astype(np.float32)[None, None]
+    yc, xc = np.arange(H) + 0.5, np.arange(W) + 0.5
+    ref = f(yc[:, None], xc[None, :])
+    got = oracle.interp_anchors(A.astype(np.float64).astype(np.float32), H, W)[0, 0]
+    # the anchors themselves are fp32-rounded samples of f: compare against interpolating those
+    np.testing.assert_allclose(got, ref, rtol=0, atol=1e-5 * (1 + np.abs(ref).max()))
+
+
+def test_anchor_interp_matches_scipy_regular_grid():
+    """Random anchors: equals scipy.interpolate.RegularGridInterpolator(linear) on the anchor
+    coordinates, evaluated at the pixel centres (library routine)."""
+    from scipy.interpolate import RegularGridInterpolator
+    rng = np.random.default_rng(7)
+    G, H, W = 6, 41, 29
+    A = rng.standard_normal((1, 4, G, G)).astype(np.float32)
+    got = oracle.interp_anchors(A, H, W)
+    u, v = _anchor_coords(G, H, W)
+    yy, xx = np.meshgrid(np.arange(H) + 0.5, np.arange(W) + 0.5, indexing="ij")
+    for k in range(4):
+        ref = RegularGridInterpolator((u, v), A[0, k].astype(np.float64))(np.stack([yy, xx], -1))
+        np.testing.assert_allclose(got[0, k], ref, rtol=0, atol=1e-12)
+
+
+def test_anchor_interp_exact_at_anchor_pixels():
+    """Where an anchor coincides with a pixel centre (H = W = 3, G = 3: anchor 1 at 1.5) the field
+    takes that anchor's value exactly (SPEC S:347 example)."""
+    A = np.arange(9, dtype=np.float32).reshape(1, 1, 3, 3) * 0.5 - 1.0
+    f = oracle.interp_anchors(A, 3, 3)
+    assert f[0, 0, 1, 1] == A[0, 0, 1, 1]
