@@ -162,6 +162,7 @@ def main():
     ap.add_argument("--cpu-budget", type=float, default=12.0, help="seconds of oracle work for cpu_baseline")
     ap.add_argument("--e2e-steps", type=int, default=None)
     ap.add_argument("--no-e2e", action="store_true", help="skip the host-path leg (profiler launch lists)")
+    ap.add_argument("--no-anchor-mode", action="store_true", help="skip the anchor-grid (NEXT-1) extra leg")
     args = ap.parse_args()
 
     rank, world, local_rank = pdist.env_rank_world()
@@ -275,6 +276,49 @@ def main():
     h2d = inp.image.nbytes + inp.zernike.nbytes + inp.tilt.nbytes
     d2h = h_out.nbytes
 
+    # ---- anchor-grid mode: the same frame with its Zernike coefficients
+    # given on a 16x16 anchor grid and interpolated inside the fused kernel (not the headline
+    # workload, which BASELINE.json defines on a dense field); same timing protocol
+    anchor_mode = None
+    if not args.no_anchor_mode:
+        G = 16
+        anc_h = synth.make_anchors(spec, G, frames=pdist.rank_frames(rank, 1))
+        anc = torch.from_numpy(anc_h).to(dev)
+        for _ in range(3):
+            r.render_anchors(img, anc, t, out=out)
+        n_a = max(10, min(args.steps, 100))
+        a0 = [torch.cuda.Event(enable_timing=True) for _ in range(n_a)]
+        a1 = [torch.cuda.Event(enable_timing=True) for _ in range(n_a)]
+        torch.cuda.synchronize()
+        for i in range(n_a):
+            flush.fill_(float(i))
+            a0[i].record(stream)
+            r.render_anchors(img, anc, t, out=out)
+            a1[i].record(stream)
+        torch.cuda.synchronize()
+        a_ms = pdist.max_over_ranks(float(sum(a0[i].elapsed_time(a1[i]) for i in range(n_a))), dist, dev)
+        h_anc = torch.from_numpy(anc_h).pin_memory().numpy()
+        ae = None
+        if e2e_steps:
+            for _ in range(2):
+                r.render_anchors_host(h_img, h_anc, h_t, h_out)
+            torch.cuda.synchronize()
+            for i in range(e2e_steps):
+                flush.fill_(float(i))
+                e0[i].record(stream)
+                r.render_anchors_host(h_img, h_anc, h_t, h_out)
+                e1[i].record(stream)
+            torch.cuda.synchronize()
+            ae_ms = pdist.max_over_ranks(float(sum(e0[i].elapsed_time(e1[i]) for i in range(e2e_steps))), dist, dev)
+            ae = {"value": pdist.throughput(B, world, e2e_steps, ae_ms), "unit": "frames/s",
+                  "h2d_bytes_per_step": int(inp.image.nbytes + anc_h.nbytes + inp.tilt.nbytes),
+                  "d2h_bytes_per_step": int(d2h), "steps": e2e_steps,
+                  "api": "p2s_render_anchors_host (pinned host buffers)"}
+        anchor_mode = {"G": G, "value": pdist.throughput(B, world, n_a, a_ms), "unit": "frames/s",
+                       "steps": n_a, "api": "p2s_render_anchors", "e2e": ae,
+                       "note": "SURVEY NEXT-1: Zernike coefficients on a 16x16 anchor grid (PAPER.md:285-288), "
+                               "bilinear per mode inside the fused kernel; same frame otherwise"}
+
     if dist:
         dist.barrier()
     if rank != 0:
@@ -314,6 +358,7 @@ def main():
                 "d2h_bytes_per_step": int(d2h), "steps": e2e_steps,
                 "api": "p2s_render_host (pinned host buffers)"},
         "gpu_launches": info["kernels_per_render"] * args.steps,
+        "anchor_mode": anchor_mode,
         "clocks": clk.summary(),
         "wall_s": t_wall,
         "plan": info,

@@ -99,6 +99,23 @@ P2S_API p2s_status p2s_render_host(p2s_handle* h, const float* image_host, int B
                            const float* zernike_host, const float* tilt_host, float* out_host,
                            p2s_stream_t stream);
 
+/* Anchor-grid input (Sec. 3.4: "partition the image
+ * into a user-defined grid of anchor points ... interpolate the Zernike coefficients using
+ * bilinear interpolation"). Instead of a dense [B][33][H][W] field the caller passes anchors
+ * DEVICE [B][n_in][G][G] fp32 (G >= 1; G = 1 is a constant field); the fused kernel
+ * interpolates them per pixel while staging the MLP input (phase-domain interpolation, then the
+ * P2S network per pixel: PAPER.md:293-299). Registration (reading N1): pixel (y, x)
+ * has centre (y + 0.5, x + 0.5); anchor (i, j) sits at (i H/(G-1), j W/(G-1)), i.e. the grid
+ * spans the image corner to corner. Otherwise identical to p2s_render (tilt, out, stream,
+ * ownership, errors; G outside [1, 4096] or NULL anchors -> P2S_ERR_INVALID_ARG). */
+P2S_API p2s_status p2s_render_anchors(p2s_handle* h, p2s_image image, const float* anchors, int G,
+                                      const float* tilt_field, float* out, p2s_stream_t stream);
+/* p2s_render_anchors with HOST buffers (image, anchors [B][n_in][G][G], tilt, out), copies
+ * inside, synchronous (the e2e path of the anchor mode). */
+P2S_API p2s_status p2s_render_anchors_host(p2s_handle* h, const float* image_host, int B, int C, int H,
+                                           int W, const float* anchors_host, int G,
+                                           const float* tilt_host, float* out_host, p2s_stream_t stream);
+
 /* Pre-sizes the workspace (and host-path staging) for frames up to B x C x H x W. */
 P2S_API p2s_status p2s_reserve(p2s_handle* h, int B, int C, int H, int W);
 
@@ -131,6 +148,9 @@ P2S_API const char* p2s_last_cuda_error(void);
  * p2s_debug_blur: steps a1+a2 only (no warp); J_out DEVICE [B][C][H][W] fp32. */
 P2S_API p2s_status p2s_debug_beta(p2s_handle* h, const float* zernike_field, int B, int H, int W,
                           float* beta_out, p2s_stream_t stream);
+/* p2s_debug_blur_anchors: steps a1+a2 from an anchor grid (as p2s_render_anchors), no warp. */
+P2S_API p2s_status p2s_debug_blur_anchors(p2s_handle* h, p2s_image image, const float* anchors, int G,
+                                          float* J_out, p2s_stream_t stream);
 P2S_API p2s_status p2s_debug_blur(p2s_handle* h, p2s_image image, const float* zernike_field,
                           float* J_out, p2s_stream_t stream);
 /* p2s_debug_profile_buffer: in a library built with -DP2S_PROFILE, later launches write per-CTA

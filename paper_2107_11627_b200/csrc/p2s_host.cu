@@ -120,6 +120,7 @@ struct p2s_handle {
   bool bias_folded = false;
   int stage_bytes, nring, smem_bytes, n_ebuf, scr_col;
   int off_ring, off_a1, off_a2, off_hold, off_e, off_tab, off_const, off_red, off_bar, a1_sbo, a2_sbo, hold_sbo;
+  int off_anc = 0, anc_cols = 0;
   int l3_hold_ks = 0, hold_k0 = 0;
   std::vector<MmaItem> mma_items;
   int sm_count;
@@ -131,6 +132,8 @@ struct p2s_handle {
   float* d_J = nullptr;
   size_t J_cap = 0;
   float *h_img = nullptr, *h_z = nullptr, *h_t = nullptr, *h_out = nullptr;  // device staging (host path)
+  float* h_anc = nullptr;  // anchor-grid staging (p2s_render_anchors_host)
+  size_t anc_cap = 0;
   size_t stage_px_cap = 0, stage_chw_cap = 0;
   cudaEvent_t ev_begin = nullptr, ev_end = nullptr;
   // host path (p2s_render_host): input-copy stream and its events
@@ -196,6 +199,8 @@ FusedParams make_params(const p2s_handle* h, int B, int C, int H, int W, int mod
   p.off_ring = h->off_ring; p.off_a1 = h->off_a1; p.off_a2 = h->off_a2; p.off_e = h->off_e;
   p.off_tab = h->off_tab; p.off_const = h->off_const; p.off_red = h->off_red; p.off_bar = h->off_bar;
   p.off_hold = h->off_hold;
+  p.off_anc = h->off_anc;
+  p.anc_cols = h->anc_cols;
   p.smem_bytes = h->smem_bytes;
   p.a1_sbo = h->a1_sbo; p.a2_sbo = h->a2_sbo; p.hold_sbo = h->hold_sbo;
   p.l3_hold_ks = h->l3_hold_ks;
@@ -347,6 +352,10 @@ p2s_status p2s_init(const p2s_basis* basis, const p2s_mlp* mlp, p2s_handle** out
   const int e1_bytes = 3 * P.chan_bytes;
   const int const_bytes = (2 * kMaxN + 256) * 4;
   const int red_bytes = 2 * 128 * 16;
+  // anchor-grid mode: y-interpolated anchor rows of one tile [n_in][kAncCols] (kernel falls back to
+  // direct gathers when a 128-px tile spans more anchor columns, e.g. G > ~80 at W = 512)
+  constexpr int kAncCols = 20;
+  const int anc_bytes = h->n_in * kAncCols * 4;
   auto al = [](int v) { return (v + 127) / 128 * 128; };
   const int bar_bytes = (BAR_RING + 2 * 4) * 8 + 16;  // BAR_RING fixed barriers + ring
   const bool red_in_hold = hold_bytes >= red_bytes;  // the J reduction buffer reuses the hold buffer
@@ -383,7 +392,7 @@ p2s_status p2s_init(const p2s_basis* basis, const p2s_mlp* mlp, p2s_handle** out
   for (int iter = 0; iter < 6; ++iter) {
     const int tab_all = tab_cap * (int)(sizeof(Item) + sizeof(MmaItem)) + nconv * 4;
     const int fixed = al(a1_bytes) + al(a2_bytes) + al(hold_bytes) + al(tab_all) + al(const_bytes) +
-                      (red_in_hold ? 0 : al(red_bytes)) + al(bar_bytes);
+                      (red_in_hold ? 0 : al(red_bytes)) + al(bar_bytes) + al(anc_bytes);
     int ring_avail = 0;
     for (h->n_ebuf = 2; h->n_ebuf >= 1; --h->n_ebuf) {
       ring_avail = kSmemLimit - fixed - al(h->n_ebuf * e1_bytes) - 1024;
@@ -421,6 +430,8 @@ p2s_status p2s_init(const p2s_basis* basis, const p2s_mlp* mlp, p2s_handle** out
   } else {
     h->off_red = off; off += al(red_bytes);
   }
+  h->off_anc = off; off += al(anc_bytes);
+  h->anc_cols = kAncCols;
   h->off_bar = off; off += (BAR_RING + 2 * nring) * 8 + 16;
   h->smem_bytes = off;
   h->a1_sbo = (h->K1 / 8) * 128;
@@ -652,9 +663,10 @@ p2s_status p2s_set_profile_events(p2s_handle* h, p2s_event_t ev_begin, p2s_event
 }
 
 static p2s_status render_impl(p2s_handle* h, p2s_image im, const float* z, const float* tilt, float* out,
-                              float* J_out, cudaStream_t st) {
+                              float* J_out, cudaStream_t st, const float* anchors = nullptr, int G = 0) {
   const size_t n_img = (size_t)im.B * im.C * im.H * im.W;
-  const size_t n_z = (size_t)im.B * h->n_in * im.H * im.W;
+  const size_t n_z = anchors ? (size_t)im.B * h->n_in * G * G : (size_t)im.B * h->n_in * im.H * im.W;
+  if (anchors) z = anchors;  // (aliasing check below covers whichever input is used)
   const size_t n_t = (size_t)im.B * 2 * im.H * im.W;
   float* dst = out ? out : J_out;
   if (overlaps(dst, n_img * 4, im.data, n_img * 4) || overlaps(dst, n_img * 4, z, n_z * 4) ||
@@ -668,7 +680,9 @@ static p2s_status render_impl(p2s_handle* h, p2s_image im, const float* z, const
   }
   FusedParams p = make_params(h, im.B, im.C, im.H, im.W, 0);
   p.image = im.data;
-  p.zernike = z;
+  p.zernike = anchors ? nullptr : z;
+  p.anchors = anchors;
+  p.G = G;
   p.J = J;
   if (h->ev_begin) P2S_CUDA(cudaEventRecord(h->ev_begin, st));
   p2s_status s = launch_fused(h, p, st);
@@ -687,6 +701,22 @@ p2s_status p2s_render(p2s_handle* h, p2s_image im, const float* zernike_field, c
   if (s != P2S_OK) return s;
   if (!zernike_field || !out) return P2S_ERR_INVALID_ARG;
   return render_impl(h, im, zernike_field, tilt_field, out, nullptr, (cudaStream_t)stream);
+}
+
+p2s_status p2s_render_anchors(p2s_handle* h, p2s_image im, const float* anchors, int G,
+                              const float* tilt_field, float* out, p2s_stream_t stream) {
+  p2s_status s = check_image(h, im);
+  if (s != P2S_OK) return s;
+  if (!anchors || !out || G < 1 || G > 4096) return P2S_ERR_INVALID_ARG;
+  return render_impl(h, im, nullptr, tilt_field, out, nullptr, (cudaStream_t)stream, anchors, G);
+}
+
+p2s_status p2s_debug_blur_anchors(p2s_handle* h, p2s_image im, const float* anchors, int G, float* J_out,
+                                  p2s_stream_t stream) {
+  p2s_status s = check_image(h, im);
+  if (s != P2S_OK) return s;
+  if (!anchors || !J_out || G < 1 || G > 4096) return P2S_ERR_INVALID_ARG;
+  return render_impl(h, im, nullptr, nullptr, nullptr, J_out, (cudaStream_t)stream, anchors, G);
 }
 
 p2s_status p2s_debug_blur(p2s_handle* h, p2s_image im, const float* zernike_field, float* J_out,
@@ -814,6 +844,74 @@ p2s_status p2s_render_host(p2s_handle* h, const float* image_host, int B, int C,
   return P2S_OK;
 }
 
+p2s_status p2s_render_anchors_host(p2s_handle* h, const float* image_host, int B, int C, int H, int W,
+                                   const float* anchors_host, int G, const float* tilt_host, float* out_host,
+                                   p2s_stream_t stream) {
+  if (!h || !image_host || !anchors_host || !out_host || G < 1 || G > 4096) return P2S_ERR_INVALID_ARG;
+  p2s_image im{image_host, B, C, H, W};
+  p2s_status s = check_image(h, im);
+  if (s != P2S_OK) return s;
+  cudaStream_t st = (cudaStream_t)stream;
+  const size_t HW = (size_t)H * W, px = (size_t)B * HW, chw = px * C, nanc = (size_t)h->n_in * G * G;
+  if (px > h->stage_px_cap || chw > h->stage_chw_cap) {
+    P2S_CUDA(cudaDeviceSynchronize());
+    cudaFree(h->h_img); cudaFree(h->h_z); cudaFree(h->h_t); cudaFree(h->h_out);
+    h->h_img = h->h_z = h->h_t = h->h_out = nullptr;
+    h->stage_px_cap = h->stage_chw_cap = 0;
+    P2S_CUDA(cudaMalloc(&h->h_img, chw * 4));
+    P2S_CUDA(cudaMalloc(&h->h_out, chw * 4));
+    P2S_CUDA(cudaMalloc(&h->h_z, px * h->n_in * 4));
+    P2S_CUDA(cudaMalloc(&h->h_t, px * 2 * 4));
+    h->stage_px_cap = px;
+    h->stage_chw_cap = chw;
+  }
+  if ((size_t)B * nanc > h->anc_cap) {
+    P2S_CUDA(cudaDeviceSynchronize());
+    cudaFree(h->h_anc);
+    h->h_anc = nullptr;
+    h->anc_cap = 0;
+    P2S_CUDA(cudaMalloc(&h->h_anc, (size_t)B * nanc * 4));
+    h->anc_cap = (size_t)B * nanc;
+  }
+  if (!h->s_in) {
+    P2S_CUDA(cudaStreamCreateWithFlags(&h->s_in, cudaStreamNonBlocking));
+    P2S_CUDA(cudaEventCreateWithFlags(&h->ev_entry, cudaEventDisableTiming));
+    P2S_CUDA(cudaEventCreateWithFlags(&h->ev_band, cudaEventDisableTiming));
+  }
+  s = ensure_J(h, chw);
+  if (s != P2S_OK) return s;
+  // Anchor-grid inputs are small (43 -> ~5 MB per 512^2 RGB frame): per frame the
+  // input stream copies image + anchors, the caller's stream renders the frame as soon as they
+  // land while the tilt copies behind them, then warps and copies the frame back.
+  P2S_CUDA(cudaEventRecord(h->ev_entry, st));
+  P2S_CUDA(cudaStreamWaitEvent(h->s_in, h->ev_entry, 0));
+  for (int f = 0; f < B; ++f) {
+    const size_t fo_img = (size_t)f * C * HW, fo_t = (size_t)f * 2 * HW, fo_a = (size_t)f * nanc;
+    P2S_CUDA(cudaMemcpyAsync(h->h_img + fo_img, image_host + fo_img, (size_t)C * HW * 4, cudaMemcpyHostToDevice, h->s_in));
+    P2S_CUDA(cudaMemcpyAsync(h->h_anc + fo_a, anchors_host + fo_a, nanc * 4, cudaMemcpyHostToDevice, h->s_in));
+    P2S_CUDA(cudaEventRecord(h->ev_band, h->s_in));
+    P2S_CUDA(cudaStreamWaitEvent(st, h->ev_band, 0));
+    FusedParams p = make_params(h, 1, C, H, W, 0);
+    p.image = h->h_img + fo_img;
+    p.zernike = nullptr;
+    p.anchors = h->h_anc + fo_a;
+    p.G = G;
+    p.J = h->d_J;
+    s = launch_fused(h, p, st);
+    if (s != P2S_OK) return s;
+    if (tilt_host) {
+      P2S_CUDA(cudaMemcpyAsync(h->h_t + fo_t, tilt_host + fo_t, 2 * HW * 4, cudaMemcpyHostToDevice, h->s_in));
+      P2S_CUDA(cudaEventRecord(h->ev_band, h->s_in));
+      P2S_CUDA(cudaStreamWaitEvent(st, h->ev_band, 0));
+    }
+    s = launch_warp(h, h->d_J, tilt_host ? h->h_t + fo_t : nullptr, h->h_out + fo_img, 1, C, H, W, st);
+    if (s != P2S_OK) return s;
+    P2S_CUDA(cudaMemcpyAsync(out_host + fo_img, h->h_out + fo_img, (size_t)C * HW * 4, cudaMemcpyDeviceToHost, st));
+  }
+  P2S_CUDA(cudaStreamSynchronize(st));
+  return P2S_OK;
+}
+
 p2s_status p2s_debug_profile_buffer(p2s_handle* h, void* device_counters) {
   if (!h) return P2S_ERR_INVALID_ARG;
 #ifdef P2S_PROFILE
@@ -840,7 +938,7 @@ void p2s_destroy(p2s_handle* h) {
   cudaDeviceSynchronize();
   cudaFree(h->d_stream); cudaFree(h->d_items); cudaFree(h->d_mma); cudaFree(h->d_steps); cudaFree(h->d_consts);
   cudaFree(h->d_J);
-  cudaFree(h->h_img); cudaFree(h->h_z); cudaFree(h->h_t); cudaFree(h->h_out);
+  cudaFree(h->h_img); cudaFree(h->h_z); cudaFree(h->h_t); cudaFree(h->h_out); cudaFree(h->h_anc);
   if (h->s_in) cudaStreamDestroy(h->s_in);
   if (h->ev_entry) cudaEventDestroy(h->ev_entry);
   if (h->ev_band) cudaEventDestroy(h->ev_band);

@@ -101,7 +101,10 @@ constexpr int kMaxMaps = 6;
 struct FusedParams {
   CUtensorMap maps[kMaxMaps];  // the packed B stream as uint8 [rows][256], box {256, N/16}
   const float* image;    // [B][C][H][W]
-  const float* zernike;  // [B][n_in][H][W]
+  const float* zernike;  // [B][n_in][H][W] (NULL when `anchors` is set)
+  const float* anchors;  // [B][n_in][G][G] anchor grid: A1 interpolates it
+  int G;
+  int off_anc, anc_cols;  // shared table of y-interpolated anchor rows [n_in][anc_cols] (per tile)
   float* J;              // [B][C][H][W] (mode 0)
   float* beta_out;       // [B][K][H][W] (mode 1)
   int B, C, H, W, n_in;
@@ -606,16 +609,82 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads)
       {
         const int m = tid;
         const int x = min(x0 + m, p.W - 1);
-        const float* zp = p.zernike + (size_t)b * p.n_in * HW + (size_t)y * p.W + x;
         uint8_t* dst = sA1 + (m & 7) * 16 + (m >> 3) * p.a1_sbo;
-        for (int k0 = 0; k0 < p.K1; k0 += 16) {
-          float v[16];
+        if (p.anchors == nullptr) {
+          const float* zp = p.zernike + (size_t)b * p.n_in * HW + (size_t)y * p.W + x;
+          for (int k0 = 0; k0 < p.K1; k0 += 16) {
+            float v[16];
 #pragma unroll
-          for (int i = 0; i < 16; ++i)
-            v[i] = (k0 + i < p.n_in) ? __ldg(zp + (size_t)(k0 + i) * HW)
-                                     : ((p.bias_folded && k0 + i < p.n_in + 2) ? 1.f : 0.f);
-          *reinterpret_cast<uint4*>(dst + (k0 >> 3) * 128) = pack8(v);
-          *reinterpret_cast<uint4*>(dst + ((k0 >> 3) + 1) * 128) = pack8(v + 8);
+            for (int i = 0; i < 16; ++i)
+              v[i] = (k0 + i < p.n_in) ? __ldg(zp + (size_t)(k0 + i) * HW)
+                                       : ((p.bias_folded && k0 + i < p.n_in + 2) ? 1.f : 0.f);
+            *reinterpret_cast<uint4*>(dst + (k0 >> 3) * 128) = pack8(v);
+            *reinterpret_cast<uint4*>(dst + ((k0 >> 3) + 1) * 128) = pack8(v + 8);
+          }
+        } else {
+          // anchor grid (registration DESIGN.md N1): pixel centre (y+.5, x+.5),
+          // anchors at (i H/(G-1), j W/(G-1)); bilinear per mode in fp32, then fp16 like the field
+          const int G = p.G;
+          int i0 = 0, j0 = 0;
+          float fy = 0.f, fx = 0.f;
+          if (G > 1) {
+            const float u = (y + 0.5f) * (float)(G - 1) / (float)p.H, vv = (x + 0.5f) * (float)(G - 1) / (float)p.W;
+            i0 = min((int)floorf(u), G - 2);
+            j0 = min((int)floorf(vv), G - 2);
+            fy = u - (float)i0;
+            fx = vv - (float)j0;
+          }
+          const int di = G > 1 ? G : 0, dj = G > 1 ? 1 : 0;
+          // anchor columns this tile spans (row weights are the same for the whole tile)
+          const int jlo = G > 1 ? min((int)floorf((x0 + 0.5f) * (float)(G - 1) / (float)p.W), G - 2) : 0;
+          const int xl = min(x0 + kTileM - 1, p.W - 1);
+          const int jhi = G > 1 ? min((int)floorf((xl + 0.5f) * (float)(G - 1) / (float)p.W), G - 2) + 1 : 0;
+          const int ncol = jhi - jlo + 1;
+          if (ncol <= p.anc_cols) {
+            // separable: the builders first form R_k[j] = (1-fy) A_k[i0][j] + fy A_k[i0+1][j] for
+            // those columns in shared memory, then each pixel needs 2 loads per mode, not 4
+            float* R = reinterpret_cast<float*>(smem + p.off_anc);
+            named_bar_sync(3, kBuildThreads);  // the previous tile's readers are done with R
+            const float* ab = p.anchors + (size_t)b * p.n_in * G * G + (size_t)i0 * G + jlo;
+            for (int e = tid; e < p.n_in * ncol; e += kBuildThreads) {
+              const int k = e / ncol, c = e - k * ncol;
+              const float* a = ab + (size_t)k * G * G + c;
+              R[e] = (1.f - fy) * __ldg(a) + fy * __ldg(a + di);
+            }
+            named_bar_sync(3, kBuildThreads);
+            const float* Rp = R + (j0 - jlo);
+            for (int k0 = 0; k0 < p.K1; k0 += 16) {
+              float v[16];
+#pragma unroll
+              for (int i = 0; i < 16; ++i) {
+                if (k0 + i < p.n_in) {
+                  const float* r0 = Rp + (k0 + i) * ncol;
+                  v[i] = (1.f - fx) * r0[0] + fx * r0[dj];
+                } else {
+                  v[i] = (p.bias_folded && k0 + i < p.n_in + 2) ? 1.f : 0.f;
+                }
+              }
+              *reinterpret_cast<uint4*>(dst + (k0 >> 3) * 128) = pack8(v);
+              *reinterpret_cast<uint4*>(dst + ((k0 >> 3) + 1) * 128) = pack8(v + 8);
+            }
+          } else {
+            const float w00 = (1.f - fy) * (1.f - fx), w01 = (1.f - fy) * fx, w10 = fy * (1.f - fx), w11 = fy * fx;
+            const float* ap = p.anchors + (size_t)b * p.n_in * G * G + (size_t)i0 * G + j0;
+            for (int k0 = 0; k0 < p.K1; k0 += 16) {
+              float v[16];
+#pragma unroll
+              for (int i = 0; i < 16; ++i) {
+                if (k0 + i < p.n_in) {
+                  const float* a = ap + (size_t)(k0 + i) * G * G;
+                  v[i] = w00 * __ldg(a) + w01 * __ldg(a + dj) + w10 * __ldg(a + di) + w11 * __ldg(a + di + dj);
+                } else {
+                  v[i] = (p.bias_folded && k0 + i < p.n_in + 2) ? 1.f : 0.f;
+                }
+              }
+              *reinterpret_cast<uint4*>(dst + (k0 >> 3) * 128) = pack8(v);
+              *reinterpret_cast<uint4*>(dst + ((k0 >> 3) + 1) * 128) = pack8(v + 8);
+            }
+          }
         }
       }
       fence_proxy_async_smem();

@@ -24,7 +24,8 @@ P2S_OK, P2S_ERR_INVALID_ARG, P2S_ERR_UNSUPPORTED, P2S_ERR_CUDA, P2S_ERR_OOM = ra
 
 EXPORTED = ("p2s_init", "p2s_render", "p2s_render_host", "p2s_reserve", "p2s_set_profile_events",
             "p2s_get_info", "p2s_destroy", "p2s_status_string", "p2s_last_cuda_error",
-            "p2s_debug_beta", "p2s_debug_blur", "p2s_debug_profile_buffer")
+            "p2s_debug_beta", "p2s_debug_blur", "p2s_debug_profile_buffer",
+            "p2s_render_anchors", "p2s_render_anchors_host", "p2s_debug_blur_anchors")
 
 
 class P2SError(RuntimeError):
@@ -87,8 +88,12 @@ def load_library(path: str = LIB_PATH) -> ctypes.CDLL:
     lib.p2s_debug_beta.argtypes = [v, v, i, i, i, v, v]
     lib.p2s_debug_blur.argtypes = [v, _Image, v, v, v]
     lib.p2s_debug_profile_buffer.argtypes = [v, v]
+    lib.p2s_render_anchors.argtypes = [v, _Image, v, i, v, v, v]
+    lib.p2s_render_anchors_host.argtypes = [v, v, i, i, i, i, v, i, v, v, v]
+    lib.p2s_debug_blur_anchors.argtypes = [v, _Image, v, i, v, v]
     for name in ("p2s_init", "p2s_render", "p2s_render_host", "p2s_reserve", "p2s_set_profile_events",
-                 "p2s_get_info", "p2s_debug_beta", "p2s_debug_blur", "p2s_debug_profile_buffer"):
+                 "p2s_get_info", "p2s_debug_beta", "p2s_debug_blur", "p2s_debug_profile_buffer",
+                 "p2s_render_anchors", "p2s_render_anchors_host", "p2s_debug_blur_anchors"):
         getattr(lib, name).restype = st
     _lib = lib
     return lib
@@ -172,6 +177,48 @@ class Renderer:
         _check(self._lib.p2s_debug_blur(self._h, im, _dev_ptr(zernike, "zernike_field", (B, self.n_in, H, W)),
                                         _dev_ptr(out, "J_out", (B, C, H, W)), _stream_handle(stream)),
                "p2s_debug_blur")
+        return out
+
+    def render_anchors(self, image, anchors, tilt=None, out=None, stream=None):
+        """p2s_render_anchors: Zernike coefficients from an anchor grid [B,n_in,G,G]."""
+        import torch
+        B, C, H, W = image.shape
+        G = anchors.shape[-1]
+        im = _Image(_dev_ptr(image, "image").value, B, C, H, W)
+        ap = _dev_ptr(anchors, "anchors", (B, self.n_in, G, G))
+        tp = _dev_ptr(tilt, "tilt_field", (B, 2, H, W)) if tilt is not None else ctypes.c_void_p()
+        if out is None:
+            out = torch.empty_like(image)
+        _check(self._lib.p2s_render_anchors(self._h, im, ap, G, tp, _dev_ptr(out, "out", (B, C, H, W)),
+                                            _stream_handle(stream)), "p2s_render_anchors")
+        return out
+
+    def debug_blur_anchors(self, image, anchors, out=None, stream=None):
+        import torch
+        B, C, H, W = image.shape
+        G = anchors.shape[-1]
+        if out is None:
+            out = torch.empty_like(image)
+        im = _Image(_dev_ptr(image, "image").value, B, C, H, W)
+        _check(self._lib.p2s_debug_blur_anchors(self._h, im, _dev_ptr(anchors, "anchors", (B, self.n_in, G, G)), G,
+                                                _dev_ptr(out, "J_out", (B, C, H, W)), _stream_handle(stream)),
+               "p2s_debug_blur_anchors")
+        return out
+
+    def render_anchors_host(self, image: np.ndarray, anchors: np.ndarray, tilt: Optional[np.ndarray],
+                            out: np.ndarray, stream=None) -> np.ndarray:
+        """p2s_render_anchors_host: host buffers in and out (copies inside), synchronous."""
+        B, C, H, W = image.shape
+        G = anchors.shape[-1]
+        for a, n in ((image, "image"), (anchors, "anchors"), (out, "out")):
+            if a.dtype != np.float32 or not a.flags.c_contiguous:
+                raise ValueError(f"{n} must be C-contiguous float32")
+        if anchors.shape != (B, self.n_in, G, G):
+            raise ValueError(f"anchors must be [B, n_in, G, G], got {anchors.shape}")
+        tp = tilt.ctypes.data if tilt is not None else None
+        _check(self._lib.p2s_render_anchors_host(self._h, image.ctypes.data, B, C, H, W, anchors.ctypes.data, G,
+                                                 tp, out.ctypes.data, _stream_handle(stream)),
+               "p2s_render_anchors_host")
         return out
 
     # -------------------------------------------------------------- host API (e2e)

@@ -29,7 +29,7 @@ from typing import Optional
 
 import numpy as np
 
-STREAM_IMAGE, STREAM_ZERNIKE, STREAM_TILT, STREAM_BASIS, STREAM_MLP, STREAM_RECT = range(6)
+STREAM_IMAGE, STREAM_ZERNIKE, STREAM_TILT, STREAM_BASIS, STREAM_MLP, STREAM_RECT, STREAM_ANCHORS = range(7)
 
 
 @dataclass(frozen=True)
@@ -131,6 +131,16 @@ def make_image(spec: Spec, frame: int) -> np.ndarray:
 def make_zernike(spec: Spec, frame: int) -> np.ndarray:
     return smooth_field(_rng(spec.cfg_id, frame, STREAM_ZERNIKE), spec.n_in, spec.H, spec.W,
                         spec.z_sigma, spec.z_std)
+
+
+def make_anchors(spec: Spec, G: int, frames: Optional[range] = None) -> np.ndarray:
+    """Anchor-grid Zernike coefficients [B][n_in][G][G] fp32:
+    per mode an N(0,1) G x G field, periodic-Gaussian smoothed over ~1 anchor spacing and scaled
+    to the config's Zernike std — a stand-in for the spatially correlated draws of P:293 (the
+    Takato covariance needs the missing supplementary parameters)."""
+    frames = range(spec.B) if frames is None else frames
+    return np.stack([smooth_field(_rng(spec.cfg_id, f, STREAM_ANCHORS), spec.n_in, G, G, 1.0, spec.z_std)
+                     for f in frames])
 
 
 def make_tilt(spec: Spec, frame: int) -> np.ndarray:

@@ -5,6 +5,8 @@ Bar (BASELINE.json north_star): max |gpu - oracle| <= 2e-3 and relative L2 <= 1e
 configs on sampled pixels the oracle computes one by one (oracle.pixels), at exactly the
 launch configuration bench.py times.
 """
+import ctypes
+
 import numpy as np
 import pytest
 
@@ -206,3 +208,86 @@ def test_invalid_arguments(p2s):
     with pytest.raises(p2s.P2SError) as e:
         p2s.Renderer(np.zeros((4, 4, 4), np.float32), {**inp.mlp})  # even S
     assert e.value.status in (p2s.P2S_ERR_INVALID_ARG, p2s.P2S_ERR_UNSUPPORTED)
+
+
+# ---- anchor-grid input: the GPU interpolates the
+#      anchors inside the fused kernel; the oracle interpolates them (oracle.interp_anchors, pinned
+#      in test_oracle_pins.py) and renders the dense field.
+
+def _anchors(spec, G, seed):
+    if G == 1:  # smooth_field removes the mean: draw constant fields directly
+        rng = np.random.default_rng(seed)
+        return (0.5 * rng.standard_normal((spec.B, spec.n_in, 1, 1))).astype(np.float32)
+    return synth.make_anchors(spec, G)
+
+
+ANCHOR_CASES = {
+    "rgb_S7_G5": (SMALL["ragged_rgb_S7"], 5),
+    "rgb_S7_G1": (SMALL["ragged_rgb_S7"], 1),
+    "S33_K100_G16": (SMALL["S33_K100_C2"], 16),
+    "S33_K100_G2": (SMALL["S33_K100_C2"], 2),
+}
+
+
+@pytest.mark.parametrize("name", list(ANCHOR_CASES))
+def test_anchor_grid_render_and_blur(p2s, name):
+    spec, G = ANCHOR_CASES[name]
+    inp = synth.make_inputs(spec)
+    anc = _anchors(spec, G, 11)
+    B, C, H, W = inp.image.shape
+    dense = oracle.interp_anchors(anc, H, W).astype(np.float32)
+    r = p2s.Renderer(inp.basis, inp.mlp)
+    J = r.debug_blur_anchors(_dev(inp.image), _dev(anc)).cpu().numpy()
+    out = r.render_anchors(_dev(inp.image), _dev(anc), _dev(inp.tilt)).cpu().numpy()
+    _, Jref = oracle.render(inp.image, dense, None, inp.basis, inp.mlp, want_blur=True)
+    ref, _ = oracle.render(inp.image, dense, inp.tilt, inp.basis, inp.mlp)
+    _cmp(J, Jref, f"blur_anchors[{name}]")
+    _cmp(out, ref, f"render_anchors[{name}]")
+
+
+@pytest.mark.parametrize("G", [16, 64])
+def test_anchor_grid_cfg3_sampled(p2s, G):
+    """The bench-size frame (512x512 RGB, K=100, 33x33) from a G x G anchor grid."""
+    spec = synth.CONFIGS[3]
+    inp = synth.make_inputs(spec)
+    anc = synth.make_anchors(spec, G)
+    B, C, H, W = inp.image.shape
+    dense = oracle.interp_anchors(anc, H, W).astype(np.float32)
+    r = p2s.Renderer(inp.basis, inp.mlp)
+    out = r.render_anchors(_dev(inp.image), _dev(anc), _dev(inp.tilt)).cpu().numpy()
+    rng = np.random.default_rng(5)
+    n = 256
+    bxy = np.stack([rng.integers(0, B, n), rng.integers(0, H, n), rng.integers(0, W, n)], 1)
+    edge = [[0, 0, 0], [0, H - 1, W - 1], [0, 0, W - 1], [0, H - 1, 0], [0, H // 2, 127], [0, H // 2, 128]]
+    bxy = np.concatenate([np.array(edge), bxy]).astype(np.int32)
+    _, oref = oracle.pixels(inp.image, dense, inp.tilt, inp.basis, inp.mlp, bxy)
+    _cmp(out[bxy[:, 0], :, bxy[:, 1], bxy[:, 2]], oref, f"render_anchors[cfg3 G={G} sampled]")
+
+
+def test_anchor_grid_host_matches_device(p2s):
+    spec, G = ANCHOR_CASES["rgb_S7_G5"]
+    inp = synth.make_inputs(spec)
+    anc = _anchors(spec, G, 11)
+    r = p2s.Renderer(inp.basis, inp.mlp)
+    dev = r.render_anchors(_dev(inp.image), _dev(anc), _dev(inp.tilt)).cpu().numpy()
+    host = np.empty_like(inp.image)
+    r.render_anchors_host(inp.image, anc, inp.tilt, host)
+    np.testing.assert_array_equal(host, dev)
+
+
+def test_anchor_grid_invalid_args(p2s):
+    spec, G = ANCHOR_CASES["rgb_S7_G5"]
+    inp = synth.make_inputs(spec)
+    r = p2s.Renderer(inp.basis, inp.mlp)
+    anc = _dev(_anchors(spec, G, 11))
+    img = _dev(inp.image)
+    with pytest.raises(p2s.P2SError) as e:  # out aliasing an input
+        r.render_anchors(img, anc, None, out=img)
+    assert e.value.status == p2s.P2S_ERR_INVALID_ARG
+    B, C, H, W = inp.image.shape
+    out = _dev(np.zeros_like(inp.image))
+    im = p2s._Image(img.data_ptr(), B, C, H, W)
+    for bad_g in (0, -3, 5000):  # G outside [1, 4096]
+        st = r._lib.p2s_render_anchors(r._h, im, ctypes.c_void_p(anc.data_ptr()), bad_g, ctypes.c_void_p(),
+                                       ctypes.c_void_p(out.data_ptr()), ctypes.c_void_p())
+        assert st == p2s.P2S_ERR_INVALID_ARG

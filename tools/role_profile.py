@@ -25,11 +25,17 @@ inp = synth.make_inputs(spec, frames=range(1))
 r = p2s.Renderer(inp.basis, inp.mlp)
 img, z, t = (torch.from_numpy(a).cuda() for a in (inp.image, inp.zernike, inp.tilt))
 out = torch.empty_like(img)
+ANCH = int(os.environ.get("ANCHOR_G", "0"))  # >0: anchor-grid mode (p2s_render_anchors) with this G
+if ANCH:
+    anc = torch.from_numpy(synth.make_anchors(spec, ANCH, frames=range(1))).cuda()
+    render = lambda: r.render_anchors(img, anc, t, out=out)  # noqa: E731
+else:
+    render = lambda: r.render(img, z, t, out=out)  # noqa: E731
 for _ in range(3):
-    r.render(img, z, t, out=out)
+    render()
 buf = torch.zeros(148 * 4 * 20 + 4 * 256, dtype=torch.int64, device="cuda")
 r.debug_profile_buffer(buf)
-r.render(img, z, t, out=out)
+render()
 torch.cuda.synchronize()
 r.debug_profile_buffer(None)
 c = buf[:148 * 4 * 20].view(148, 4, 20).cpu().numpy().astype(np.float64)
