@@ -131,6 +131,7 @@ typedef struct {
   int conv_steps;                    /* 16-tap K-slices per channel (sum of taps padded) */
   int smem_bytes;                    /* dynamic shared memory of the fused kernel */
   int kernels_per_render;            /* launches queued by one p2s_render */
+  int stage_bytes, nring;            /* B-operand ring: bytes per stage, stages */
 } p2s_info;
 P2S_API p2s_status p2s_get_info(const p2s_handle* h, p2s_info* info);
 

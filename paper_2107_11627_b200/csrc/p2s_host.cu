@@ -217,7 +217,8 @@ p2s_status launch_fused(p2s_handle* h, const FusedParams& p, cudaStream_t st) {
   // persistent grid of CTA pairs (clusters of 2): at most one CTA per SM
   const int npairs = (p.ntiles + 1) / 2;
   const int grid = 2 * std::max(1, std::min(h->sm_count / 2, npairs));
-  k_fused_p2s<<<grid, kThreads, h->smem_bytes, st>>>(p);
+  if (p.anchors) k_fused_p2s<true><<<grid, kThreads, h->smem_bytes, st>>>(p);
+  else k_fused_p2s<false><<<grid, kThreads, h->smem_bytes, st>>>(p);
   P2S_CUDA(cudaPeekAtLastError());
   return P2S_OK;
 }
@@ -350,7 +351,7 @@ p2s_status p2s_init(const p2s_basis* basis, const p2s_mlp* mlp, p2s_handle** out
   const int a2_bytes = kTileM * kh * 2;
   const int hold_bytes = kTileM * hold_cols * 2;
   const int e1_bytes = 3 * P.chan_bytes;
-  const int const_bytes = (2 * kMaxN + 256) * 4;
+  const int const_bytes = (h->bias_folded ? 256 : 256 + 2 * kMaxN) * 4;  // b1, b2 unused when folded
   const int red_bytes = 2 * 128 * 16;
   // anchor-grid mode: y-interpolated anchor rows of one tile [n_in][kAncCols] (kernel falls back to
   // direct gathers when a 128-px tile spans more anchor columns, e.g. G > ~80 at W = 512)
@@ -402,11 +403,11 @@ p2s_status p2s_init(const p2s_basis* basis, const p2s_mlp* mlp, p2s_handle** out
     ring_avail = kSmemLimit - fixed - al(h->n_ebuf * e1_bytes) - 1024;
     // prefer 3 large stages (fewer ring transitions for the UMMA issuer), else 4, else 2
     nring = 3;
-    sb = std::min(32768, (ring_avail / 3) / 512 * 512);
+    sb = std::min(32768, (ring_avail / 3) / 128 * 128);
     if (sb < 16384) {
       nring = 4;
-      sb = std::min(32768, (ring_avail / 4) / 512 * 512);
-      if (sb < 12288) { nring = 2; sb = std::min(32768, (ring_avail / 2) / 512 * 512); }
+      sb = std::min(32768, (ring_avail / 4) / 128 * 128);
+      if (sb < 12288) { nring = 2; sb = std::min(32768, (ring_avail / 2) / 128 * 128); }
     }
     if (sb < max_half_slab) { delete h; return P2S_ERR_UNSUPPORTED; }
     const int need = table_need(sb);
@@ -592,16 +593,16 @@ p2s_status p2s_init(const p2s_basis* basis, const p2s_mlp* mlp, p2s_handle** out
   for (const Item& it : beta) h->mma_items.push_back(mma_of(it, 1, false));
   for (const Item& it : first) h->mma_items.push_back(mma_of(it, 0, true));
 
-  // ---- constants: b1, b2 (kMaxN each), b3, svec (128 each), zero padded;
+  // ---- constants: b3, svec (128 each), b1, b2 (kMaxN each), zero padded;
   //      svec[k] = sum of the taps of phi_k (centred-image identity)
-  std::vector<float> consts(2 * kMaxN + 256, 0.f);
-  for (int i = 0; i < h->h1; ++i) consts[i] = mlp->b1[i];
-  for (int i = 0; i < h->h2; ++i) consts[kMaxN + i] = mlp->b2[i];
+  std::vector<float> consts(2 * kMaxN + 256, 0.f);  // [b3 | svec | b1 | b2]
+  for (int i = 0; i < h->h1; ++i) consts[256 + i] = mlp->b1[i];
+  for (int i = 0; i < h->h2; ++i) consts[256 + kMaxN + i] = mlp->b2[i];
   for (int i = 0; i < K; ++i) {
-    consts[2 * kMaxN + i] = mlp->b3[i];
+    consts[i] = mlp->b3[i];
     double sum = 0.0;
     for (int t = 0; t < S * S; ++t) sum += basis->taps[(size_t)i * S * S + t];
-    consts[2 * kMaxN + 128 + i] = (float)sum;
+    consts[128 + i] = (float)sum;
   }
   std::vector<uint32_t> steps(nconv);
   for (int g = 0; g < nconv; ++g) steps[g] = (P.steps[g].off >> 4) | ((P.steps[g].lbo >> 4) << 16);
@@ -643,8 +644,10 @@ p2s_status p2s_init(const p2s_basis* basis, const p2s_mlp* mlp, p2s_handle** out
   UP(h->d_steps, steps.data(), steps.size() * sizeof(uint32_t));
   UP(h->d_consts, consts.data(), consts.size() * 4);
 #undef UP
-  if ((e = cudaFuncSetAttribute(k_fused_p2s, cudaFuncAttributeMaxDynamicSharedMemorySize, kSmemLimit)) !=
-      cudaSuccess)
+  if ((e = cudaFuncSetAttribute(k_fused_p2s<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, kSmemLimit)) !=
+          cudaSuccess ||
+      (e = cudaFuncSetAttribute(k_fused_p2s<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, kSmemLimit)) !=
+          cudaSuccess)
     return fail(cuda_fail(e, "cudaFuncSetAttribute"));
   *out_handle = h;
   return P2S_OK;
@@ -930,6 +933,8 @@ p2s_status p2s_get_info(const p2s_handle* h, p2s_info* info) {
   info->conv_steps = (int)h->plan.steps.size();
   info->smem_bytes = h->smem_bytes;
   info->kernels_per_render = 2;
+  info->stage_bytes = h->stage_bytes;
+  info->nring = h->nring;
   return P2S_OK;
 }
 

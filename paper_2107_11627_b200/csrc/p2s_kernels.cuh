@@ -122,7 +122,7 @@ struct FusedParams {
   const MmaItem* mma_items;   // UMMA view of items (same order / modes as `items`)
   const uint32_t* conv_steps; // per conv K-step: descriptor low word (E-relative start>>4 | (LBO>>4)<<16)
   int nconv;
-  const float* consts;        // b1[kMaxN] b2[kMaxN] b3[128] svec[128] (zero padded)
+  const float* consts;        // b3[128] svec[128] b1[kMaxN] b2[kMaxN] (zero padded)
   int K, Nk, K1, N1, N2;
   int r, rr;                  // rr = r rounded up to a multiple of 4 (E column origin)
   int n_ey, n_ex, npos_y, npos_x;
@@ -365,6 +365,81 @@ __device__ __forceinline__ void conv_epi_group(uint32_t tl, int scr_col, int Nk,
   }
 }
 
+// A1 from an anchor grid (registration DESIGN.md N1): pixel
+// centre (y+.5, x+.5), anchors at (i H/(G-1), j W/(G-1)); bilinear per mode in fp32, then fp16
+// like a dense field. Out of line: it keeps the builders' (rarely used) anchor path from
+// costing the shared register allocation of the whole kernel.
+__device__ __noinline__ void build_A1_anchors(const FusedParams& p, uint8_t* dst, int b, int y, int x0, int x,
+                                              int tid, uint8_t* smem) {
+  // anchor grid (registration DESIGN.md N1): pixel centre (y+.5, x+.5),
+  // anchors at (i H/(G-1), j W/(G-1)); bilinear per mode in fp32, then fp16 like the field
+  const int G = p.G;
+  int i0 = 0, j0 = 0;
+  float fy = 0.f, fx = 0.f;
+  if (G > 1) {
+    const float u = (y + 0.5f) * (float)(G - 1) / (float)p.H, vv = (x + 0.5f) * (float)(G - 1) / (float)p.W;
+    i0 = min((int)floorf(u), G - 2);
+    j0 = min((int)floorf(vv), G - 2);
+    fy = u - (float)i0;
+    fx = vv - (float)j0;
+  }
+  const int di = G > 1 ? G : 0, dj = G > 1 ? 1 : 0;
+  // anchor columns this tile spans (row weights are the same for the whole tile)
+  const int jlo = G > 1 ? min((int)floorf((x0 + 0.5f) * (float)(G - 1) / (float)p.W), G - 2) : 0;
+  const int xl = min(x0 + kTileM - 1, p.W - 1);
+  const int jhi = G > 1 ? min((int)floorf((xl + 0.5f) * (float)(G - 1) / (float)p.W), G - 2) + 1 : 0;
+  const int ncol = jhi - jlo + 1;
+  if (ncol <= p.anc_cols) {
+    // separable: the builders first form R_k[j] = (1-fy) A_k[i0][j] + fy A_k[i0+1][j] for
+    // those columns in shared memory, then each pixel needs 2 loads per mode, not 4
+    float* R = reinterpret_cast<float*>(smem + p.off_anc);
+    named_bar_sync(3, kBuildThreads);  // the previous tile's readers are done with R
+    const float* ab = p.anchors + (size_t)b * p.n_in * G * G + (size_t)i0 * G + jlo;
+    for (int e = tid; e < p.n_in * ncol; e += kBuildThreads) {
+      const int k = e / ncol, c = e - k * ncol;
+      const float* a = ab + (size_t)k * G * G + c;
+      R[e] = (1.f - fy) * __ldg(a) + fy * __ldg(a + di);
+    }
+    named_bar_sync(3, kBuildThreads);
+    const float* Rp = R + (j0 - jlo);
+    for (int k0 = 0; k0 < p.K1; k0 += 16) {
+      float v[16];
+#pragma unroll
+      for (int i = 0; i < 16; ++i) {
+        if (k0 + i < p.n_in) {
+          const float* r0 = Rp + (k0 + i) * ncol;
+          v[i] = (1.f - fx) * r0[0] + fx * r0[dj];
+        } else {
+          v[i] = (p.bias_folded && k0 + i < p.n_in + 2) ? 1.f : 0.f;
+        }
+      }
+      *reinterpret_cast<uint4*>(dst + (k0 >> 3) * 128) = pack8(v);
+      *reinterpret_cast<uint4*>(dst + ((k0 >> 3) + 1) * 128) = pack8(v + 8);
+    }
+  } else {
+    const float w00 = (1.f - fy) * (1.f - fx), w01 = (1.f - fy) * fx, w10 = fy * (1.f - fx), w11 = fy * fx;
+    const float* ap = p.anchors + (size_t)b * p.n_in * G * G + (size_t)i0 * G + j0;
+    for (int k0 = 0; k0 < p.K1; k0 += 16) {
+      float v[16];
+#pragma unroll
+      for (int i = 0; i < 16; ++i) {
+        if (k0 + i < p.n_in) {
+          const float* a = ap + (size_t)(k0 + i) * G * G;
+          v[i] = w00 * __ldg(a) + w01 * __ldg(a + dj) + w10 * __ldg(a + di) + w11 * __ldg(a + di + dj);
+        } else {
+          v[i] = (p.bias_folded && k0 + i < p.n_in + 2) ? 1.f : 0.f;
+        }
+      }
+      *reinterpret_cast<uint4*>(dst + (k0 >> 3) * 128) = pack8(v);
+      *reinterpret_cast<uint4*>(dst + ((k0 >> 3) + 1) * 128) = pack8(v + 8);
+    }
+  }
+}
+
+// kAnchors: Zernike input from an anchor grid (p.anchors) instead of a dense field. A separate
+// instantiation: merely having the anchor path in the builders cost the dense kernel ~80 B of
+// register spills and ~1.5 % (measured).
+template <bool kAnchors>
 __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads)
     k_fused_p2s(const __grid_constant__ FusedParams p) {
   extern __shared__ __align__(1024) uint8_t smem[];
@@ -381,10 +456,11 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads)
   MmaItem* sMma = reinterpret_cast<MmaItem*>(smem + p.off_mma);
   uint32_t* sSteps = reinterpret_cast<uint32_t*>(smem + p.off_steps);
   float* sConst = reinterpret_cast<float*>(smem + p.off_const);
-  float* sB1 = sConst;
-  float* sB2 = sConst + kMaxN;
-  float* sB3 = sConst + 2 * kMaxN;
-  float* sSv = sConst + 2 * kMaxN + 128;
+  // [b3 | tap sums | b1 | b2]; with folded biases only the first 256 floats are staged
+  float* sB3 = sConst;
+  float* sSv = sConst + 128;
+  float* sB1 = sConst + 256;
+  float* sB2 = sConst + 256 + kMaxN;
   float4* sRed = reinterpret_cast<float4*>(smem + p.off_red);  // [2][128] partial J (WG1 -> WG0)
 
   const int warp = warp_id();
@@ -409,14 +485,27 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads)
   prof_acc[10] = globaltimer_ns();
 #endif
 
-  // ---- setup
-  for (int i = threadIdx.x; i < nA + nB; i += kThreads) {
-    const int src = i < nA ? offA + i : offB + (i - nA);
-    sItems[i] = p.items[src];
-    sMma[i] = p.mma_items[src];
+  // ---- setup: the item, step and constant tables -> shared memory as 4-byte async copies, all
+  // in flight at once (dependent load/store loops cost one global round trip per table)
+  {
+    constexpr int wi = (int)(sizeof(Item) / 4), wm = (int)(sizeof(MmaItem) / 4);
+    const uint32_t* gi = reinterpret_cast<const uint32_t*>(p.items);
+    const uint32_t* gm = reinterpret_cast<const uint32_t*>(p.mma_items);
+    uint32_t* si = reinterpret_cast<uint32_t*>(sItems);
+    uint32_t* sm = reinterpret_cast<uint32_t*>(sMma);
+    for (int w = threadIdx.x; w < (nA + nB) * wi; w += kThreads) {
+      const int i = w / wi, src = i < nA ? offA + i : offB + (i - nA);
+      cp_async4(si + w, gi + (size_t)src * wi + (w - i * wi));
+    }
+    for (int w = threadIdx.x; w < (nA + nB) * wm; w += kThreads) {
+      const int i = w / wm, src = i < nA ? offA + i : offB + (i - nA);
+      cp_async4(sm + w, gm + (size_t)src * wm + (w - i * wm));
+    }
+    for (int i = threadIdx.x; i < p.nconv; i += kThreads) cp_async4(sSteps + i, p.conv_steps + i);
+    const int n_const = p.bias_folded ? 256 : 256 + 2 * kMaxN;
+    for (int i = threadIdx.x; i < n_const; i += kThreads) cp_async4(sConst + i, p.consts + i);
+    cp_async_wait_all();
   }
-  for (int i = threadIdx.x; i < p.nconv; i += kThreads) sSteps[i] = p.conv_steps[i];
-  for (int i = threadIdx.x; i < 2 * kMaxN + 256; i += kThreads) sConst[i] = p.consts[i];
   if (threadIdx.x == 0) {
     mbar_init(&bars[BAR_A1_FULL], 2 * kNumBuildWarps);
     mbar_init(&bars[BAR_A1_EMPTY], 1);
@@ -610,7 +699,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads)
         const int m = tid;
         const int x = min(x0 + m, p.W - 1);
         uint8_t* dst = sA1 + (m & 7) * 16 + (m >> 3) * p.a1_sbo;
-        if (p.anchors == nullptr) {
+        if constexpr (!kAnchors) {
           const float* zp = p.zernike + (size_t)b * p.n_in * HW + (size_t)y * p.W + x;
           for (int k0 = 0; k0 < p.K1; k0 += 16) {
             float v[16];
@@ -622,69 +711,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads)
             *reinterpret_cast<uint4*>(dst + ((k0 >> 3) + 1) * 128) = pack8(v + 8);
           }
         } else {
-          // anchor grid (registration DESIGN.md N1): pixel centre (y+.5, x+.5),
-          // anchors at (i H/(G-1), j W/(G-1)); bilinear per mode in fp32, then fp16 like the field
-          const int G = p.G;
-          int i0 = 0, j0 = 0;
-          float fy = 0.f, fx = 0.f;
-          if (G > 1) {
-            const float u = (y + 0.5f) * (float)(G - 1) / (float)p.H, vv = (x + 0.5f) * (float)(G - 1) / (float)p.W;
-            i0 = min((int)floorf(u), G - 2);
-            j0 = min((int)floorf(vv), G - 2);
-            fy = u - (float)i0;
-            fx = vv - (float)j0;
-          }
-          const int di = G > 1 ? G : 0, dj = G > 1 ? 1 : 0;
-          // anchor columns this tile spans (row weights are the same for the whole tile)
-          const int jlo = G > 1 ? min((int)floorf((x0 + 0.5f) * (float)(G - 1) / (float)p.W), G - 2) : 0;
-          const int xl = min(x0 + kTileM - 1, p.W - 1);
-          const int jhi = G > 1 ? min((int)floorf((xl + 0.5f) * (float)(G - 1) / (float)p.W), G - 2) + 1 : 0;
-          const int ncol = jhi - jlo + 1;
-          if (ncol <= p.anc_cols) {
-            // separable: the builders first form R_k[j] = (1-fy) A_k[i0][j] + fy A_k[i0+1][j] for
-            // those columns in shared memory, then each pixel needs 2 loads per mode, not 4
-            float* R = reinterpret_cast<float*>(smem + p.off_anc);
-            named_bar_sync(3, kBuildThreads);  // the previous tile's readers are done with R
-            const float* ab = p.anchors + (size_t)b * p.n_in * G * G + (size_t)i0 * G + jlo;
-            for (int e = tid; e < p.n_in * ncol; e += kBuildThreads) {
-              const int k = e / ncol, c = e - k * ncol;
-              const float* a = ab + (size_t)k * G * G + c;
-              R[e] = (1.f - fy) * __ldg(a) + fy * __ldg(a + di);
-            }
-            named_bar_sync(3, kBuildThreads);
-            const float* Rp = R + (j0 - jlo);
-            for (int k0 = 0; k0 < p.K1; k0 += 16) {
-              float v[16];
-#pragma unroll
-              for (int i = 0; i < 16; ++i) {
-                if (k0 + i < p.n_in) {
-                  const float* r0 = Rp + (k0 + i) * ncol;
-                  v[i] = (1.f - fx) * r0[0] + fx * r0[dj];
-                } else {
-                  v[i] = (p.bias_folded && k0 + i < p.n_in + 2) ? 1.f : 0.f;
-                }
-              }
-              *reinterpret_cast<uint4*>(dst + (k0 >> 3) * 128) = pack8(v);
-              *reinterpret_cast<uint4*>(dst + ((k0 >> 3) + 1) * 128) = pack8(v + 8);
-            }
-          } else {
-            const float w00 = (1.f - fy) * (1.f - fx), w01 = (1.f - fy) * fx, w10 = fy * (1.f - fx), w11 = fy * fx;
-            const float* ap = p.anchors + (size_t)b * p.n_in * G * G + (size_t)i0 * G + j0;
-            for (int k0 = 0; k0 < p.K1; k0 += 16) {
-              float v[16];
-#pragma unroll
-              for (int i = 0; i < 16; ++i) {
-                if (k0 + i < p.n_in) {
-                  const float* a = ap + (size_t)(k0 + i) * G * G;
-                  v[i] = w00 * __ldg(a) + w01 * __ldg(a + dj) + w10 * __ldg(a + di) + w11 * __ldg(a + di + dj);
-                } else {
-                  v[i] = (p.bias_folded && k0 + i < p.n_in + 2) ? 1.f : 0.f;
-                }
-              }
-              *reinterpret_cast<uint4*>(dst + (k0 >> 3) * 128) = pack8(v);
-              *reinterpret_cast<uint4*>(dst + ((k0 >> 3) + 1) * 128) = pack8(v + 8);
-            }
-          }
+          build_A1_anchors(p, dst, b, y, x0, x, tid, smem);
         }
       }
       fence_proxy_async_smem();

@@ -69,6 +69,12 @@ P2S_DEV void tma2_load_2d(void* dst_smem, const void* tmap, int x, int y, uint32
       "l"(tmap), "r"(x), "r"(y), "r"(mbar_cluster)
       : "memory");
 }
+// 4-byte global -> shared asynchronous copy (LDGSTS); cp_async_wait_all() completes this
+// thread's copies (then a CTA barrier makes them visible).
+P2S_DEV void cp_async4(void* dst_smem, const void* src) {
+  asm volatile("cp.async.ca.shared.global [%0], [%1], 4;" ::"r"(smem_u32(dst_smem)), "l"(src) : "memory");
+}
+P2S_DEV void cp_async_wait_all() { asm volatile("cp.async.wait_all;" ::: "memory"); }
 // Fire-and-forget L2 prefetch of the 128-B line holding `ptr`.
 P2S_DEV void prefetch_l2(const void* ptr) { asm volatile("prefetch.global.L2 [%0];" ::"l"(ptr)); }
 P2S_DEV void prefetch_tmap(const void* tmap) {

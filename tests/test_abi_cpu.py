@@ -88,15 +88,16 @@ def test_sass_has_tcgen05_and_tma(lib):
     assert "HMMA" not in sass.replace("UTCHMMA", "")
     # the UMMA issue loop must stay on the uniform datapath: descriptors in uniform registers,
     # no per-UMMA divergence/elect loops (a silent 1.5x slowdown when uniformity is lost)
-    fused = sass[sass.index("k_fused_p2s"):]
-    fused = fused[:fused.index("Function :")] if "Function :" in fused else fused
-    ins = [l.split("*/", 1)[1].strip() for l in fused.split("\n") if l.strip().startswith("/*") and "*/" in l
-           and not l.strip().startswith("/* 0x")]
-    mma = [n for n, l in enumerate(ins) if "UTCHMMA" in l]
-    assert mma
-    # the issue loop region: no divergence checks, no elect loops, no per-UMMA lane broadcasts
-    region = ins[max(0, mma[0] - 60):mma[-1] + 60]
-    for bad in ("BRA.DIV", "BRA.U.ANY", "R2UR.BROADCAST"):
-        assert not any(bad in x for x in region), bad
-    for n in mma:  # the 12 instructions feeding each UMMA must use uniform operands only
-        assert not any("R2UR.BROADCAST" in x for x in ins[max(0, n - 12):n]), ins[max(0, n - 12):n + 1]
+    funcs = [f for f in sass.split("Function : ")[1:] if f.startswith("_ZN3p2s11k_fused_p2s")]
+    assert len(funcs) == 2  # dense-field and anchor-grid instantiations
+    for fused in funcs:
+        ins = [l.split("*/", 1)[1].strip() for l in fused.split("\n") if l.strip().startswith("/*") and "*/" in l
+               and not l.strip().startswith("/* 0x")]
+        mma = [n for n, l in enumerate(ins) if "UTCHMMA" in l]
+        assert mma
+        # the issue loop region: no divergence checks, no elect loops, no per-UMMA lane broadcasts
+        region = ins[max(0, mma[0] - 60):mma[-1] + 60]
+        for bad in ("BRA.DIV", "BRA.U.ANY", "R2UR.BROADCAST"):
+            assert not any(bad in x for x in region), bad
+        for n in mma:  # the 12 instructions feeding each UMMA must use uniform operands only
+            assert not any("R2UR.BROADCAST" in x for x in ins[max(0, n - 12):n]), ins[max(0, n - 12):n + 1]
