@@ -291,3 +291,32 @@ def test_anchor_grid_invalid_args(p2s):
         st = r._lib.p2s_render_anchors(r._h, im, ctypes.c_void_p(anc.data_ptr()), bad_g, ctypes.c_void_p(),
                                        ctypes.c_void_p(out.data_ptr()), ctypes.c_void_p())
         assert st == p2s.P2S_ERR_INVALID_ARG
+
+
+# ---- production use: graph capture and batched launches
+
+def test_render_is_cuda_graph_capturable(p2s):
+    """With the workspace reserved, p2s_render performs no host synchronisation or allocation, so
+    a CUDA graph can capture it once and replay it on new inputs (same buffers)."""
+    import torch
+    spec = SMALL["ragged_rgb_S7"]
+    inp = synth.make_inputs(spec)
+    r = p2s.Renderer(inp.basis, inp.mlp)
+    B, C, H, W = inp.image.shape
+    r.reserve(B, C, H, W)
+    img, z, t = _dev(inp.image), _dev(inp.zernike), _dev(inp.tilt)
+    out = torch.empty_like(img)
+    s = torch.cuda.Stream()
+    with torch.cuda.stream(s):
+        r.render(img, z, t, out=out, stream=s)  # warm-up outside capture
+    torch.cuda.synchronize()
+    g = torch.cuda.CUDAGraph()
+    with torch.cuda.graph(g, stream=s):
+        r.render(img, z, t, out=out, stream=s)
+    inp2 = synth.make_inputs(synth.custom("ragged_rgb_S7", 301, B=2, C=3, H=37, W=200, K=20, S=7, h1=48,
+                                          h2=40, t_std=1.7))
+    img.copy_(_dev(inp2.image)); z.copy_(_dev(inp2.zernike)); t.copy_(_dev(inp2.tilt))
+    g.replay()
+    torch.cuda.synchronize()
+    ref = r.render(_dev(inp2.image), _dev(inp2.zernike), _dev(inp2.tilt)).cpu().numpy()
+    np.testing.assert_array_equal(out.cpu().numpy(), ref)
