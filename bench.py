@@ -164,6 +164,7 @@ def main():
     ap.add_argument("--no-e2e", action="store_true", help="skip the host-path leg (profiler launch lists)")
     ap.add_argument("--no-anchor-mode", action="store_true", help="skip the anchor-grid (NEXT-1) extra leg")
     ap.add_argument("--no-batch-mode", action="store_true", help="skip the 16-frame batched-launch extra leg")
+    ap.add_argument("--no-sequence-mode", action="store_true", help="skip the 50-frame sequence extra leg")
     args = ap.parse_args()
 
     rank, world, local_rank = pdist.env_rank_world()
@@ -302,6 +303,34 @@ def main():
                       "calls": n_b, "note": "cfg4 shape: 16 frames (cfg3 recipe, per-frame seeds) per p2s_render"}
         del bimg, bz, bt, bout
 
+    # ---- sequence mode (50 degraded frames per image): one
+    # image, 50 Zernike fields / tilts; each tile's convolutions serve all 50 frames
+    sequence_mode = None
+    if not args.no_sequence_mode:
+        F = 50
+        sinp = synth.make_inputs(spec, frames=range(rank * F, (rank + 1) * F))
+        simg = torch.from_numpy(np.ascontiguousarray(sinp.image[:1])).to(dev)
+        sz, st_ = torch.from_numpy(sinp.zernike).to(dev), torch.from_numpy(sinp.tilt).to(dev)
+        sout = torch.empty((F, C, H, W), device=dev, dtype=torch.float32)
+        r.reserve(F, C, H, W)
+        for _ in range(2):
+            r.render_sequence(simg, sz, st_, out=sout)
+        n_s = 5
+        q0 = [torch.cuda.Event(enable_timing=True) for _ in range(n_s)]
+        q1 = [torch.cuda.Event(enable_timing=True) for _ in range(n_s)]
+        torch.cuda.synchronize()
+        for i in range(n_s):
+            q0[i].record(stream)
+            r.render_sequence(simg, sz, st_, out=sout)  # 50 x 35 MB of fields per call: > L2
+            q1[i].record(stream)
+        torch.cuda.synchronize()
+        s_ms = pdist.max_over_ranks(float(sum(q0[i].elapsed_time(q1[i]) for i in range(n_s))), dist, dev)
+        sequence_mode = {"frames_per_sequence": F, "value": pdist.throughput(F, world, n_s, s_ms),
+                         "unit": "frames/s", "calls": n_s, "api": "p2s_render_sequence",
+                         "note": "50 frames of one 512x512 RGB image (cfg3 recipe, per-frame Zernike/tilt); "
+                                 "the K convolutions are computed once per tile and shared by the frames"}
+        del simg, sz, st_, sout
+
     # ---- anchor-grid mode: the same frame with its Zernike coefficients
     # given on a 16x16 anchor grid and interpolated inside the fused kernel (not the headline
     # workload, which BASELINE.json defines on a dense field); same timing protocol
@@ -386,6 +415,7 @@ def main():
         "gpu_launches": info["kernels_per_render"] * args.steps,
         "anchor_mode": anchor_mode,
         "batch_mode": batch_mode,
+        "sequence_mode": sequence_mode,
         "clocks": clk.summary(),
         "wall_s": t_wall,
         "plan": info,

@@ -116,6 +116,18 @@ P2S_API p2s_status p2s_render_anchors_host(p2s_handle* h, const float* image_hos
                                            int W, const float* anchors_host, int G,
                                            const float* tilt_host, float* out_host, p2s_stream_t stream);
 
+/* Sequence mode: F degraded frames of ONE image, the way the paper's
+ * training data is made ("5000 simulated sequences, where each sequence contains
+ * 50 degraded frames" of one ground-truth image), each with its own Zernike field and tilt.
+ * out[f] = p2s_render(image, zernike[f], tilt[f]) for every f. The K basis convolutions of the
+ * image (83-93 % of the work) are computed once per tile and stay in tensor memory while the
+ * P2S network and the Eq. 5 reduction run for every frame.
+ * image DEVICE [1][C][H][W]; zernike_field DEVICE [F][n_in][H][W]; tilt_field DEVICE [F][2][H][W]
+ * or NULL; out DEVICE [F][C][H][W]. Errors as p2s_render; image.B != 1 or F outside [1, 65535]
+ * -> P2S_ERR_INVALID_ARG. */
+P2S_API p2s_status p2s_render_sequence(p2s_handle* h, p2s_image image, const float* zernike_field,
+                                       const float* tilt_field, int F, float* out, p2s_stream_t stream);
+
 /* Pre-sizes the workspace (and host-path staging) for frames up to B x C x H x W. */
 P2S_API p2s_status p2s_reserve(p2s_handle* h, int B, int C, int H, int W);
 

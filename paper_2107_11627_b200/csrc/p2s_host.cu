@@ -114,7 +114,7 @@ struct p2s_handle {
   int K, S, r, n_in, h1, h2, Nk, K1, N1, N2;
   ConvPlan plan;
   std::vector<Item> items;  // [items_full | items_beta]
-  int n_items_full = 0, n_items_beta = 0, n_items_first = 0, tab_cap = 0;
+  int n_items_full = 0, n_items_beta = 0, n_items_first = 0, n_items_seq = 0, tab_cap = 0;
   MlpOp ops[kMaxOps];  // [0, n_ops) per-tile ops, then n_fops first-tile whole-layer ops
   int n_ops = 0, n_fops = 0;
   bool bias_folded = false;
@@ -177,6 +177,8 @@ FusedParams make_params(const p2s_handle* h, int B, int C, int H, int W, int mod
   p.n_items_full = h->n_items_full;
   p.n_items_beta = h->n_items_beta;
   p.n_items_first = h->n_items_first;
+  p.n_items_seq = h->n_items_seq;
+  p.nfr = 1;
   p.tab_cap = h->tab_cap;
   p.off_mma = h->off_tab + h->tab_cap * (int)sizeof(Item);
   p.off_steps = p.off_mma + h->tab_cap * (int)sizeof(MmaItem);
@@ -387,7 +389,7 @@ p2s_status p2s_init(const p2s_basis* basis, const p2s_mlp* mlp, p2s_handle** out
       const bool in_first = h->n_fops > 0 ? (o >= h->n_ops || h->ops[o].layer == 2) : true;
       if (in_first) fst += count_stages(sb, h->ops[o].nks, h->ops[o].N, h->ops[o].layer == 2 && h->l3_hold_ks > 0);
     }
-    return std::max(mlp + conv + fst + conv, 2 * mlp);  // [first | steady] or [beta | beta]
+    return std::max(mlp + conv + fst + conv + mlp, 2 * mlp);  // [first | steady | seq] or [beta | beta]
   };
   int tab_cap = 48, sb = 0, nring = 3;
   for (int iter = 0; iter < 6; ++iter) {
@@ -551,13 +553,15 @@ p2s_status p2s_init(const p2s_basis* basis, const p2s_mlp* mlp, p2s_handle** out
   h->n_items_full = (int)full.size();
   h->n_items_beta = (int)beta.size();
   h->n_items_first = (int)first.size();
-  if (h->n_items_full + h->n_items_first > h->tab_cap || 2 * h->n_items_beta > h->tab_cap) {
+  h->n_items_seq = (int)beta.size();  // sequence mode: a frame after a tile's first = its MLP ops
+  if (h->n_items_full + h->n_items_first + h->n_items_seq > h->tab_cap || 2 * h->n_items_beta > h->tab_cap) {
     delete h;
     return P2S_ERR_UNSUPPORTED;
   }
   h->items = full;
   h->items.insert(h->items.end(), beta.begin(), beta.end());
   h->items.insert(h->items.end(), first.begin(), first.end());
+  h->items.insert(h->items.end(), beta.begin(), beta.end());  // seq list (same B stream)
   // UMMA-side view of every item (precomputed so the issue loop does one LDS.128 per item)
   auto mma_of = [&](const Item& it, int mode, bool first_tile) {
     MmaItem mi{};
@@ -580,11 +584,16 @@ p2s_status p2s_init(const p2s_basis* basis, const p2s_mlp* mlp, p2s_handle** out
     mi.a_hi = (sbo >> 4) | (1u << 14);
     mi.d_col = (uint16_t)op.d_col;
     uint16_t f = 0;
-    if (it.flags & IT_BEGIN) f |= (op.layer == 0 && op.first_of_layer) ? MI_WAIT_A1 : MI_WAIT_SCR;
+    // mode 2 = a sequence frame after the tile's first: its L1 waits for the previous frame's
+    // beta to leave the scratch (SCR_FREE), not for the conv accumulators (they stay)
+    if (it.flags & IT_BEGIN) {
+      if (op.layer == 0 && op.first_of_layer) f |= MI_WAIT_A1 | (mode == 2 ? MI_WAIT_SCR : MI_WAIT_TMEM);
+      else f |= MI_WAIT_SCR;
+    }
     if (it.flags & IT_END) {
       if (op.layer == 0 && op.last_of_layer) f |= MI_COMMIT_A1;
       if (op.layer < 2) f |= MI_COMMIT_MLP;
-      else if (mode == 1) f |= MI_COMMIT_ACC;
+      else if (mode >= 1) f |= MI_COMMIT_ACC;
     }
     mi.flags = f;
     return mi;
@@ -592,6 +601,7 @@ p2s_status p2s_init(const p2s_basis* basis, const p2s_mlp* mlp, p2s_handle** out
   for (const Item& it : full) h->mma_items.push_back(mma_of(it, 0, false));
   for (const Item& it : beta) h->mma_items.push_back(mma_of(it, 1, false));
   for (const Item& it : first) h->mma_items.push_back(mma_of(it, 0, true));
+  for (const Item& it : beta) h->mma_items.push_back(mma_of(it, 2, false));
 
   // ---- constants: b3, svec (128 each), b1, b2 (kMaxN each), zero padded;
   //      svec[k] = sum of the taps of phi_k (centred-image identity)
@@ -704,6 +714,31 @@ p2s_status p2s_render(p2s_handle* h, p2s_image im, const float* zernike_field, c
   if (s != P2S_OK) return s;
   if (!zernike_field || !out) return P2S_ERR_INVALID_ARG;
   return render_impl(h, im, zernike_field, tilt_field, out, nullptr, (cudaStream_t)stream);
+}
+
+p2s_status p2s_render_sequence(p2s_handle* h, p2s_image im, const float* zernike_field, const float* tilt_field,
+                               int F, float* out, p2s_stream_t stream) {
+  p2s_status s = check_image(h, im);
+  if (s != P2S_OK) return s;
+  if (!zernike_field || !out || im.B != 1 || F < 1 || F > 65535) return P2S_ERR_INVALID_ARG;
+  const size_t HW = (size_t)im.H * im.W, n_out = (size_t)F * im.C * HW;
+  if (overlaps(out, n_out * 4, im.data, (size_t)im.C * HW * 4) ||
+      overlaps(out, n_out * 4, zernike_field, (size_t)F * h->n_in * HW * 4) ||
+      overlaps(out, n_out * 4, tilt_field, (size_t)F * 2 * HW * 4))
+    return P2S_ERR_INVALID_ARG;
+  cudaStream_t st = (cudaStream_t)stream;
+  s = ensure_J(h, n_out);
+  if (s != P2S_OK) return s;
+  FusedParams p = make_params(h, 1, im.C, im.H, im.W, 0);
+  p.nfr = F;  // tiles of the one image; every tile serves all F frames (J / Zernike frame = fr)
+  p.image = im.data;
+  p.zernike = zernike_field;
+  p.J = h->d_J;
+  if (h->ev_begin) P2S_CUDA(cudaEventRecord(h->ev_begin, st));
+  s = launch_fused(h, p, st);
+  if (s != P2S_OK) return s;
+  if (h->ev_end) P2S_CUDA(cudaEventRecord(h->ev_end, st));
+  return launch_warp(h, h->d_J, tilt_field, out, F, im.C, im.H, im.W, st);
 }
 
 p2s_status p2s_render_anchors(p2s_handle* h, p2s_image im, const float* anchors, int G,

@@ -74,7 +74,7 @@ static_assert(sizeof(Item) == 24, "Item layout");
 // shared-memory base is added on the device), width, dependency waits and commits.
 enum MmaItemFlags : uint16_t {
   MI_CONV = 1, MI_WAIT_A1 = 2, MI_WAIT_SCR = 4, MI_WAIT_E = 8,
-  MI_COMMIT_A1 = 16, MI_COMMIT_MLP = 32, MI_COMMIT_ACC = 64
+  MI_COMMIT_A1 = 16, MI_COMMIT_MLP = 32, MI_COMMIT_ACC = 64, MI_WAIT_TMEM = 128
 };
 struct MmaItem {
   uint32_t a_lo_rel;   // (smem offset >> 4) | (LBO >> 4) << 16, without the smem base
@@ -111,8 +111,10 @@ struct FusedParams {
   int nstrips, ntiles, mode;  // mode 0: MLP + conv -> J ; mode 1: MLP only -> beta
   int y0, ny;                 // rows [y0, y0 + ny) of every frame (a band of the host path)
   const uint8_t* stream;
-  const Item* items;          // [items_full | items_beta | items_first]
-  int n_items_full, n_items_beta, n_items_first;
+  const Item* items;          // [items_full | items_beta | items_first | items_seq]
+  int n_items_full, n_items_beta, n_items_first, n_items_seq;
+  int nfr;                    // frames per tile: 1, or a sequence's length (sequence mode: frames
+                              // share the image, so each tile's convolutions serve all of them)
   int tab_cap;                // entries of the shared-memory item tables
   int off_mma, off_steps;     // byte offsets of the MmaItem and conv-step tables
   MlpOp ops[kMaxOps];         // [0, n_ops): per-tile ops; then n_fops whole-layer L1/L2 ops
@@ -477,6 +479,13 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads)
   const int nB = p.mode == 0 ? p.n_items_full : p.n_items_beta;
   const int offA = p.mode == 0 ? p.n_items_full + p.n_items_beta : p.n_items_full;
   const int offB = p.mode == 0 ? 0 : p.n_items_full;
+  // sequence mode: after a tile's first frame (list A / B), nfr - 1 MLP-only lists S
+  const int nS = p.nfr > 1 ? p.n_items_seq : 0;
+  const int offS = p.n_items_full + p.n_items_beta + p.n_items_first;
+  const int nfr = p.nfr;
+  // items of segment (tile it, frame fr) start at table index seg_base, n of them
+  auto seg_base = [&](int it, int fr) { return fr > 0 ? nA + nB : (it == 0 ? 0 : nA); };
+  auto seg_len = [&](int it, int fr) { return fr > 0 ? nS : (it == 0 ? nA : nB); };
 #ifdef P2S_PROFILE
   unsigned long long prof_acc[20];
 #pragma unroll
@@ -493,13 +502,14 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads)
     const uint32_t* gm = reinterpret_cast<const uint32_t*>(p.mma_items);
     uint32_t* si = reinterpret_cast<uint32_t*>(sItems);
     uint32_t* sm = reinterpret_cast<uint32_t*>(sMma);
-    for (int w = threadIdx.x; w < (nA + nB) * wi; w += kThreads) {
-      const int i = w / wi, src = i < nA ? offA + i : offB + (i - nA);
-      cp_async4(si + w, gi + (size_t)src * wi + (w - i * wi));
+    auto src_of = [&](int i) { return i < nA ? offA + i : (i < nA + nB ? offB + (i - nA) : offS + (i - nA - nB)); };
+    for (int w = threadIdx.x; w < (nA + nB + nS) * wi; w += kThreads) {
+      const int i = w / wi;
+      cp_async4(si + w, gi + (size_t)src_of(i) * wi + (w - i * wi));
     }
-    for (int w = threadIdx.x; w < (nA + nB) * wm; w += kThreads) {
-      const int i = w / wm, src = i < nA ? offA + i : offB + (i - nA);
-      cp_async4(sm + w, gm + (size_t)src * wm + (w - i * wm));
+    for (int w = threadIdx.x; w < (nA + nB + nS) * wm; w += kThreads) {
+      const int i = w / wm;
+      cp_async4(sm + w, gm + (size_t)src_of(i) * wm + (w - i * wm));
     }
     for (int i = threadIdx.x; i < p.nconv; i += kThreads) cp_async4(sSteps + i, p.conv_steps + i);
     const int n_const = p.bias_folded ? 256 : 256 + 2 * kMaxN;
@@ -538,8 +548,9 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads)
       for (int i = 0; i < kMaxMaps; ++i) prefetch_tmap(&p.maps[i]);
       int s = 0;
       uint32_t ph = 0;
-      for (int pr = pr_begin; pr < pr_end; ++pr) {
-        const int n_items = pr == pr_begin ? nA : nB, base = pr == pr_begin ? 0 : nA;
+      for (int pr = pr_begin; pr < pr_end; ++pr)
+      for (int fr = 0; fr < nfr; ++fr) {
+        const int n_items = seg_len(pr - pr_begin, fr), base = seg_base(pr - pr_begin, fr);
         for (int g = 0; g < n_items; ++g) {
           const Item it = sItems[base + g];
           { PROF_T0(); WAIT_PROD(&ring_empty[s], ph ^ 1); PROF_ADD(7); }
@@ -572,27 +583,29 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads)
     const uint32_t id_base = idesc_f16(256, 0);
     int s = 0;
     uint32_t ph = 0;
-    uint32_t scr_waits = 0;
+    uint32_t scr_waits = 0, a1_waits = 0;
     uint32_t e_use0 = 0, e_use1 = 0;
     int pending = -1;  // ring slot whose release commit is deferred behind the next UMMAs
 #ifdef P2S_PROFILE
     prof_acc[11] = globaltimer_ns();
 #endif
-    const int total = pr_end > pr_begin ? nA + (pr_end - pr_begin - 1) * nB : 0;
+    const int ntl = pr_end - pr_begin;
+    const int total = ntl > 0 ? nA + (ntl - 1) * nB + ntl * (nfr - 1) * nS : 0;
     MmaItem cur = sMma[0];
-    for (int step = 0, it = 0, g = 0; step < total; ++step) {
-      const int n_items = it == 0 ? nA : nB;
-      // prefetch the next item (sMma holds list A then list B)
-      const MmaItem nxt = sMma[g + 1 < n_items ? (it == 0 ? g + 1 : nA + g + 1) : nA];
+    for (int step = 0, it = 0, fr = 0, g = 0; step < total; ++step) {
+      const int n_items = seg_len(it, fr);
+      // prefetch the next item: same segment, else the next frame's (S) or the next tile's (B)
+      const MmaItem nxt = sMma[g + 1 < n_items ? seg_base(it, fr) + g + 1 : (fr + 1 < nfr ? nA + nB : nA)];
       const int eb = ebufs == 2 ? (it & 1) : 0;
       const uint32_t f = cur.flags;
 #ifdef P2S_PROFILE
       const long long tr_a = clock64();
 #endif
       if (f & MI_WAIT_A1) {
-        { PROF_T0(); mbar_wait(&bars[BAR_A1_FULL], it & 1); PROF_ADD(0); }
-        { PROF_T0(); mbar_wait(&bars[BAR_TMEM_FREE], (it & 1) ^ 1); PROF_ADD(1); }
+        { PROF_T0(); mbar_wait(&bars[BAR_A1_FULL], a1_waits & 1); PROF_ADD(0); }
+        ++a1_waits;
       }
+      if (f & MI_WAIT_TMEM) { PROF_T0(); mbar_wait(&bars[BAR_TMEM_FREE], (it & 1) ^ 1); PROF_ADD(1); }
       if (f & MI_WAIT_SCR) {
         { PROF_T0(); mbar_wait(&bars[BAR_SCR_FREE], scr_waits & 1); PROF_ADD(2); }
         ++scr_waits;
@@ -680,27 +693,33 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads)
 #endif
       if (++s == nring) { s = 0; ph ^= 1; }
       cur = nxt;
-      if (++g == n_items) { g = 0; ++it; }
+      if (++g == n_items) {
+        g = 0;
+        if (++fr == nfr) { fr = 0; ++it; }
+      }
     }
     if (pending >= 0) umma2_commit_elect(&ring_empty[pending]);
   } else if (builder_index(warp) >= 0) {
     // ================= builders: A1 (Zernike tile, fp16) and E views (fp16, centred) =====
     const int tid = builder_index(warp) * 32 + lane;
     const size_t HW = (size_t)p.H * p.W;
-    uint32_t e_use0 = 0, e_use1 = 0;
+    uint32_t e_use0 = 0, e_use1 = 0, a1_builds = 0;
     int it = 0;
-    for (int pr = pr_begin; pr < pr_end; ++pr, ++it) {
+    for (int pr = pr_begin; pr < pr_end; ++pr, ++it)
+    for (int fr = 0; fr < nfr; ++fr) {
       const int t = min(2 * pr + (int)rank, p.ntiles - 1);  // odd tail: duplicate, not stored
       int b, y, x0;
       tile_coords(p, t, b, y, x0);
-      // --- A1: row m = pixel x0+m, k = Zernike index (zero-padded to K1)
-      { PROF_T0(); WAIT_BUILD(&bars[BAR_A1_EMPTY], (it & 1) ^ 1); PROF_ADD(9); }
+      // --- A1 of frame b + fr (sequence mode: every frame of the image's sequence): row m =
+      //     pixel x0+m, k = Zernike index (zero-padded to K1)
+      { PROF_T0(); WAIT_BUILD(&bars[BAR_A1_EMPTY], (a1_builds & 1) ^ 1); PROF_ADD(9); }
+      ++a1_builds;
       {
         const int m = tid;
         const int x = min(x0 + m, p.W - 1);
         uint8_t* dst = sA1 + (m & 7) * 16 + (m >> 3) * p.a1_sbo;
         if constexpr (!kAnchors) {
-          const float* zp = p.zernike + (size_t)b * p.n_in * HW + (size_t)y * p.W + x;
+          const float* zp = p.zernike + (size_t)(b + fr) * p.n_in * HW + (size_t)y * p.W + x;
           for (int k0 = 0; k0 < p.K1; k0 += 16) {
             float v[16];
 #pragma unroll
@@ -711,13 +730,13 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads)
             *reinterpret_cast<uint4*>(dst + ((k0 >> 3) + 1) * 128) = pack8(v + 8);
           }
         } else {
-          build_A1_anchors(p, dst, b, y, x0, x, tid, smem);
+          build_A1_anchors(p, dst, b + fr, y, x0, x, tid, smem);
         }
       }
       fence_proxy_async_smem();
       __syncwarp();
       if (lane == 0) mbar_arrive_remote(&bars[BAR_A1_FULL], 0);
-      if (p.mode != 0) continue;
+      if (p.mode != 0 || fr > 0) continue;  // E views: once per tile (every frame shares the image)
       // --- E views of every channel (the CTA's first tile: built by the idle epilogue warps)
       const int eb = p.n_ebuf == 2 ? (it & 1) : 0;
       if (it == 0) { ++e_use0; continue; }
@@ -765,13 +784,15 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads)
     uint8_t* a2row = sA2 + (m & 7) * 16 + (m >> 3) * p.a2_sbo;
     uint8_t* hrow = sHold + (m & 7) * 16 + (m >> 3) * p.hold_sbo;
     int it = 0;
-    for (int pr = pr_begin; pr < pr_end; ++pr, ++it) {
+    uint32_t acc_waits = 0, red_i = 0;
+    for (int pr = pr_begin; pr < pr_end; ++pr, ++it)
+    for (int fr = 0; fr < nfr; ++fr) {  // sequence mode: every frame of the tile's image
       const int t_raw = 2 * pr + (int)rank;
       const bool store = t_raw < p.ntiles;
       int b, y, x0;
       tile_coords(p, min(t_raw, p.ntiles - 1), b, y, x0);
       // a CTA's first tile (mode 0) runs L1 and L2 as whole-layer ops (p.ops[n_ops, +n_fops))
-      const bool fops = p.mode == 0 && it == 0 && p.n_fops > 0;
+      const bool fops = p.mode == 0 && it == 0 && fr == 0 && p.n_fops > 0;
       const int o_begin = fops ? p.n_ops : 0, o_end = fops ? p.n_ops + p.n_fops : p.n_ops;
       for (int o = o_begin; o < o_end; ++o) {
         const MlpOp op = p.ops[o];
@@ -844,7 +865,8 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads)
         prof_acc[18] += (unsigned long long)(clock64() - td1);
 #endif
       }
-      { PROF_T0(); WAIT_EPI(&bars[BAR_ACC_FULL], it & 1); PROF_ADD(15); }
+      { PROF_T0(); WAIT_EPI(&bars[BAR_ACC_FULL], acc_waits & 1); PROF_ADD(15); }
+      ++acc_waits;
       tc_fence_after();
 #ifdef P2S_PROFILE
       const long long te0 = clock64();
@@ -877,14 +899,15 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads)
         }
         float jc[3] = {jc2[0].x + jc2[0].y, jc2[1].x + jc2[1].y, jc2[2].x + jc2[2].y};
         float bs = bs2.x + bs2.y;
-        // every TMEM read of this tile is done: release TMEM before combining / storing J
+        // every TMEM read of this tile is done: release TMEM before combining / storing J (in a
+        // sequence, frames before the last release only beta's scratch: the accumulators stay)
         tc_fence_before();
         __syncwarp();
-        if (lane == 0) mbar_arrive_remote(&bars[BAR_TMEM_FREE], 0);
+        if (lane == 0) mbar_arrive_remote(&bars[fr == nfr - 1 ? BAR_TMEM_FREE : BAR_SCR_FREE], 0);
 #ifdef P2S_PROFILE
         prof_acc[16] += (unsigned long long)(clock64() - te0);
 #endif
-        float4* red = sRed + (it & 1) * 128;
+        float4* red = sRed + (red_i++ & 1) * 128;
         if (wg == 1) red[m] = make_float4(jc[0], jc[1], jc[2], bs);
         named_bar_sync(1, 32 * kNumEpiWarps);
         if (wg == 0) {
@@ -894,7 +917,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads)
           if (store && x < p.W) {
 #pragma unroll
             for (int c = 0; c < 3; ++c)
-              if (c < C) p.J[((size_t)b * C + c) * HW + (size_t)y * p.W + x] = fmaf(0.5f, bs, jc[c]);
+              if (c < C) p.J[((size_t)(b + fr) * C + c) * HW + (size_t)y * p.W + x] = fmaf(0.5f, bs, jc[c]);
           }
         }
       }

@@ -25,7 +25,8 @@ P2S_OK, P2S_ERR_INVALID_ARG, P2S_ERR_UNSUPPORTED, P2S_ERR_CUDA, P2S_ERR_OOM = ra
 EXPORTED = ("p2s_init", "p2s_render", "p2s_render_host", "p2s_reserve", "p2s_set_profile_events",
             "p2s_get_info", "p2s_destroy", "p2s_status_string", "p2s_last_cuda_error",
             "p2s_debug_beta", "p2s_debug_blur", "p2s_debug_profile_buffer",
-            "p2s_render_anchors", "p2s_render_anchors_host", "p2s_debug_blur_anchors")
+            "p2s_render_anchors", "p2s_render_anchors_host", "p2s_debug_blur_anchors",
+            "p2s_render_sequence")
 
 
 class P2SError(RuntimeError):
@@ -92,9 +93,11 @@ def load_library(path: str = LIB_PATH) -> ctypes.CDLL:
     lib.p2s_render_anchors.argtypes = [v, _Image, v, i, v, v, v]
     lib.p2s_render_anchors_host.argtypes = [v, v, i, i, i, i, v, i, v, v, v]
     lib.p2s_debug_blur_anchors.argtypes = [v, _Image, v, i, v, v]
+    lib.p2s_render_sequence.argtypes = [v, _Image, v, v, i, v, v]
     for name in ("p2s_init", "p2s_render", "p2s_render_host", "p2s_reserve", "p2s_set_profile_events",
                  "p2s_get_info", "p2s_debug_beta", "p2s_debug_blur", "p2s_debug_profile_buffer",
-                 "p2s_render_anchors", "p2s_render_anchors_host", "p2s_debug_blur_anchors"):
+                 "p2s_render_anchors", "p2s_render_anchors_host", "p2s_debug_blur_anchors",
+                 "p2s_render_sequence"):
         getattr(lib, name).restype = st
     _lib = lib
     return lib
@@ -192,6 +195,20 @@ class Renderer:
             out = torch.empty_like(image)
         _check(self._lib.p2s_render_anchors(self._h, im, ap, G, tp, _dev_ptr(out, "out", (B, C, H, W)),
                                             _stream_handle(stream)), "p2s_render_anchors")
+        return out
+
+    def render_sequence(self, image, zernike, tilt=None, out=None, stream=None):
+        """p2s_render_sequence: one image [1,C,H,W], F frames of Zernike [F,n_in,H,W] / tilt [F,2,H,W]."""
+        import torch
+        _, C, H, W = image.shape
+        F = zernike.shape[0]
+        im = _Image(_dev_ptr(image, "image", (1, C, H, W)).value, 1, C, H, W)
+        zp = _dev_ptr(zernike, "zernike_field", (F, self.n_in, H, W))
+        tp = _dev_ptr(tilt, "tilt_field", (F, 2, H, W)) if tilt is not None else ctypes.c_void_p()
+        if out is None:
+            out = torch.empty((F, C, H, W), device=image.device, dtype=torch.float32)
+        _check(self._lib.p2s_render_sequence(self._h, im, zp, tp, F, _dev_ptr(out, "out", (F, C, H, W)),
+                                             _stream_handle(stream)), "p2s_render_sequence")
         return out
 
     def debug_blur_anchors(self, image, anchors, out=None, stream=None):

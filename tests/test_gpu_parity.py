@@ -320,3 +320,76 @@ def test_render_is_cuda_graph_capturable(p2s):
     torch.cuda.synchronize()
     ref = r.render(_dev(inp2.image), _dev(inp2.zernike), _dev(inp2.tilt)).cpu().numpy()
     np.testing.assert_array_equal(out.cpu().numpy(), ref)
+
+
+# ---- sequence mode (sequences of 50 degraded frames of one
+#      image): one image, F Zernike fields / tilts; convolutions shared across the frames
+
+SEQ_CASES = {
+    "rgb_S7_F3": (SMALL["ragged_rgb_S7"], 3),
+    "S33_K100_C2_F4": (SMALL["S33_K100_C2"], 4),
+    "many_tiles_F2": (SMALL["many_tiles_C2"], 2),
+    "F1": (SMALL["ragged_rgb_S7"], 1),
+}
+
+
+def _seq_inputs(spec, F):
+    inp = synth.make_inputs(spec, frames=range(F))
+    return inp, np.ascontiguousarray(inp.image[:1])  # every frame uses frame 0's image
+
+
+@pytest.mark.parametrize("name", list(SEQ_CASES))
+def test_sequence_matches_replicated_batch(p2s, name):
+    """p2s_render_sequence == p2s_render on the image replicated F times, bit for bit (each tile's
+    arithmetic is the same; the convolutions are just not recomputed per frame)."""
+    import torch
+    spec, F = SEQ_CASES[name]
+    inp, img1 = _seq_inputs(spec, F)
+    r = p2s.Renderer(inp.basis, inp.mlp)
+    seq = r.render_sequence(_dev(img1), _dev(inp.zernike), _dev(inp.tilt)).cpu().numpy()
+    rep = np.ascontiguousarray(np.repeat(img1, F, axis=0))
+    ref = r.render(_dev(rep), _dev(inp.zernike), _dev(inp.tilt)).cpu().numpy()
+    np.testing.assert_array_equal(seq, ref)
+    torch.cuda.synchronize()
+
+
+def test_sequence_vs_oracle(p2s):
+    spec, F = SEQ_CASES["S33_K100_C2_F4"]
+    inp, img1 = _seq_inputs(spec, F)
+    r = p2s.Renderer(inp.basis, inp.mlp)
+    seq = r.render_sequence(_dev(img1), _dev(inp.zernike), _dev(inp.tilt)).cpu().numpy()
+    rep = np.ascontiguousarray(np.repeat(img1, F, axis=0))
+    ref, _ = oracle.render(rep, inp.zernike, inp.tilt, inp.basis, inp.mlp)
+    _cmp(seq, ref, "render_sequence[S33_K100_C2_F4]")
+
+
+def test_sequence_cfg3_sampled(p2s):
+    """Bench-size frames (512x512 RGB, K=100, 33x33), a 4-frame sequence, sampled outputs."""
+    spec, F = synth.CONFIGS[3], 4
+    inp, img1 = _seq_inputs(spec, F)
+    r = p2s.Renderer(inp.basis, inp.mlp)
+    seq = r.render_sequence(_dev(img1), _dev(inp.zernike), _dev(inp.tilt)).cpu().numpy()
+    _, C, H, W = img1.shape
+    rng = np.random.default_rng(9)
+    n = 256
+    bxy = np.stack([rng.integers(0, F, n), rng.integers(0, H, n), rng.integers(0, W, n)], 1)
+    edge = [[0, 0, 0], [F - 1, H - 1, W - 1], [1, 0, W - 1], [2, H // 2, 127], [3, H // 2, 128]]
+    bxy = np.concatenate([np.array(edge), bxy]).astype(np.int32)
+    rep = np.ascontiguousarray(np.repeat(img1, F, axis=0))
+    _, oref = oracle.pixels(rep, inp.zernike, inp.tilt, inp.basis, inp.mlp, bxy)
+    _cmp(seq[bxy[:, 0], :, bxy[:, 1], bxy[:, 2]], oref, "render_sequence[cfg3 F=4 sampled]")
+
+
+def test_sequence_invalid_args(p2s):
+    spec, F = SEQ_CASES["rgb_S7_F3"]
+    inp, img1 = _seq_inputs(spec, F)
+    r = p2s.Renderer(inp.basis, inp.mlp)
+    img2 = _dev(np.ascontiguousarray(np.repeat(img1, 2, axis=0)))
+    z = _dev(inp.zernike)
+    out = _dev(np.zeros((F,) + img1.shape[1:], np.float32))
+    _, C, H, W = img1.shape
+    for im, f in ((p2s._Image(img2.data_ptr(), 2, C, H, W), F),   # the image must be one frame
+                  (p2s._Image(img2.data_ptr(), 1, C, H, W), 0)):  # F >= 1
+        st = r._lib.p2s_render_sequence(r._h, im, ctypes.c_void_p(z.data_ptr()), ctypes.c_void_p(), f,
+                                        ctypes.c_void_p(out.data_ptr()), ctypes.c_void_p())
+        assert st == p2s.P2S_ERR_INVALID_ARG
