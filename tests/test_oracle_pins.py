@@ -345,3 +345,52 @@ def test_anchor_interp_exact_at_anchor_pixels():
     A = np.arange(9, dtype=np.float32).reshape(1, 1, 3, 3) * 0.5 - 1.0
     f = oracle.interp_anchors(A, 3, 3)
     assert f[0, 0, 1, 1] == A[0, 0, 1, 1]
+
+
+# ---- correlated anchor sampling (stand-in covariance:
+#      DESIGN.md reading N3) — oracle/sampler.py
+
+def test_philox_known_answers():
+    """Philox4x32-10 reproduces the Random123 known-answer vectors (Salmon et al., SC'11)."""
+    from oracle import sampler
+    out = sampler.philox4x32_10([[0, 0, 0, 0], [0x243f6a88, 0x85a308d3, 0x13198a2e, 0x03707344]],
+                                [[0, 0], [0xa4093822, 0x299f31d0]])
+    assert [int(v) for v in out[0]] == [0x6627e8d5, 0xe169c58d, 0xbc57ac4c, 0x9b00dbd8]
+    assert [int(v) for v in out[1]] == [0xd16cfe09, 0x94fdcceb, 0x5001e420, 0x24126ea1]
+
+
+def test_sampler_normals_are_standard_normal():
+    """Box-Muller on Philox words: mean 0, variance 1, Kolmogorov-Smirnov vs N(0,1)."""
+    import scipy.stats
+    from oracle import sampler
+    z = np.concatenate([sampler.normals(1234, f, 64, 33).ravel() for f in range(4)])  # 540k draws
+    n = z.size
+    assert abs(z.mean()) < 5 / np.sqrt(n)
+    assert abs(z.var() - 1) < 5 * np.sqrt(2 / n)
+    assert scipy.stats.kstest(z, "norm").pvalue > 1e-3
+    # different frames / seeds give different streams
+    assert not np.allclose(sampler.normals(1234, 0, 4, 3), sampler.normals(1234, 1, 4, 3))
+    assert not np.allclose(sampler.normals(1234, 0, 4, 3), sampler.normals(1235, 0, 4, 3))
+
+
+def test_sampler_identity_covariance_returns_the_normals():
+    """corr_len 0 (s = identity up to the 1e-6 jitter) and R = I: the anchors are z itself."""
+    from oracle import sampler
+    A = sampler.sample(7, 3, 2, 5, 4, corr_len=0.0, mode_cov=np.eye(4))
+    for f in range(2):
+        z = sampler.normals(7, 3 + f, 5, 4).reshape(5, 5, 4).transpose(2, 0, 1)
+        np.testing.assert_allclose(A[f], z * (1 + 1e-6), rtol=1e-12, atol=1e-12)  # two spatial factors
+
+
+def test_sampler_empirical_covariance():
+    """Across many frames the anchors' covariance is R (x) s (x) s (Monte-Carlo, 4000 frames)."""
+    from oracle import sampler
+    G, n_in, L = 3, 2, 1.5
+    rng = np.random.default_rng(3)
+    M = rng.standard_normal((n_in, n_in))
+    R = M @ M.T / n_in + 0.5 * np.eye(n_in)
+    A = sampler.sample(99, 0, 4000, G, n_in, corr_len=L, mode_cov=R).reshape(4000, -1)
+    emp = A.T @ A / A.shape[0]
+    s = sampler.spatial_cov(G, L)
+    ref = np.kron(R, np.kron(s, s))
+    assert np.abs(emp - ref).max() < 6 * np.sqrt(2 / 4000) * np.abs(ref).max()
