@@ -352,6 +352,20 @@ def main():
             a1[i].record(stream)
         torch.cuda.synchronize()
         a_ms = pdist.max_over_ranks(float(sum(a0[i].elapsed_time(a1[i]) for i in range(n_a))), dist, dev)
+        # the whole simulator from a seed (NEXT-3 + NEXT-1): correlated anchors, then the frame
+        smp = p2s.Sampler(G, spec.n_in, 2.0)
+        for _ in range(2):
+            r.render_anchors(img, smp.sample(1000 + rank, 0, 1, out=anc), t, out=out)
+        torch.cuda.synchronize()
+        for i in range(n_a):
+            flush.fill_(float(i))
+            a0[i].record(stream)
+            smp.sample(1000 + rank, i, 1, out=anc)
+            r.render_anchors(img, anc, t, out=out)
+            a1[i].record(stream)
+        torch.cuda.synchronize()
+        sa_ms = pdist.max_over_ranks(float(sum(a0[i].elapsed_time(a1[i]) for i in range(n_a))), dist, dev)
+        smp.close()
         h_anc = torch.from_numpy(anc_h).pin_memory().numpy()
         ae = None
         if e2e_steps:
@@ -370,6 +384,9 @@ def main():
                   "d2h_bytes_per_step": int(d2h), "steps": e2e_steps,
                   "api": "p2s_render_anchors_host (pinned host buffers)"}
         anchor_mode = {"G": G, "value": pdist.throughput(B, world, n_a, a_ms), "unit": "frames/s",
+                       "sampled_value": pdist.throughput(B, world, n_a, sa_ms),
+                       "sampled_note": "NEXT-3: p2s_sample_anchors (correlated anchors from a seed, stand-in "
+                                       "covariance, corr_len 2) + p2s_render_anchors per frame",
                        "steps": n_a, "api": "p2s_render_anchors", "e2e": ae,
                        "note": "SURVEY NEXT-1: Zernike coefficients on a 16x16 anchor grid (PAPER.md:285-288), "
                                "bilinear per mode inside the fused kernel; same frame otherwise"}

@@ -128,6 +128,25 @@ P2S_API p2s_status p2s_render_anchors_host(p2s_handle* h, const float* image_hos
 P2S_API p2s_status p2s_render_sequence(p2s_handle* h, p2s_image image, const float* zernike_field,
                                        const float* tilt_field, int F, float* out, p2s_stream_t stream);
 
+/* ---- correlated anchor sampling (Sec. 3.4: anchor
+ * coefficient sets "drawn from the correlation matrix", which "can be pre-computed") ----
+ * Stand-in covariance (reading N3; the paper's Takato-formula parameters are absent):
+ * separable over anchor row a, anchor column b and mode j:
+ *   Cov[A_j(a,b), A_j'(a',b')] = R[j][j'] s(a-a') s(b-b'), s(d) = exp(-d^2/(2 l^2)) + 1e-6 [d = 0]
+ * with l = corr_len in anchor spacings (0: independent anchors) and R = mode_cov (HOST fp64
+ * [n_in][n_in], symmetric positive definite; NULL: 0.25 I). p2s_sampler_init factors both
+ * (Cholesky, fp64, once); p2s_sample_anchors writes F frames A_f = (L_R (x) L_s (x) L_s) z_f to
+ * anchors (DEVICE [F][n_in][G][G] fp32, the layout p2s_render_anchors reads), z_f ~ N(0, I) from
+ * Philox4x32-10 (key = seed, counter = (frame0 + f, a G + b, j, 0)) + Box-Muller: every frame is
+ * reproducible on its own. G in [1, 64], n_in in [1, 64]; a non-SPD mode_cov, a bad size or NULL
+ * pointers -> P2S_ERR_INVALID_ARG. Asynchronous on `stream`. */
+typedef struct p2s_sampler p2s_sampler;
+P2S_API p2s_status p2s_sampler_init(int G, int n_in, double corr_len, const double* mode_cov,
+                                    p2s_sampler** out_sampler);
+P2S_API p2s_status p2s_sample_anchors(p2s_sampler* s, unsigned long long seed, int frame0, int F,
+                                      float* anchors, p2s_stream_t stream);
+P2S_API void p2s_sampler_destroy(p2s_sampler* s);
+
 /* Pre-sizes the workspace (and host-path staging) for frames up to B x C x H x W. */
 P2S_API p2s_status p2s_reserve(p2s_handle* h, int B, int C, int H, int W);
 

@@ -74,6 +74,9 @@ def sample(seed: int, frame0: int, F: int, G: int, n_in: int, corr_len: float, m
     LR = np.linalg.cholesky(R)
     out = np.empty((F, n_in, G, G))
     for f in range(F):
-        z = normals(seed, frame0 + f, G, n_in).reshape(G, G, n_in)  # [a][b][j]
-        out[f] = np.einsum("jk,ac,bd,cdk->jab", LR, Ls, Ls, z)
+        z = normals(seed, frame0 + f, G, n_in).reshape(G, G, n_in)  # [a][b][k]
+        t = z @ LR.T                                  # modes:   t[a][b][j] = sum_k L_R[j][k] z[a][b][k]
+        t = np.einsum("ac,cbj->abj", Ls, t)           # rows:    sum_c L_s[a][c] t[c][b][j]
+        t = np.einsum("bd,adj->abj", Ls, t)           # columns: sum_d L_s[b][d] t[a][d][j]
+        out[f] = t.transpose(2, 0, 1)
     return out

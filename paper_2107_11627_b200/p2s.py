@@ -26,7 +26,7 @@ EXPORTED = ("p2s_init", "p2s_render", "p2s_render_host", "p2s_reserve", "p2s_set
             "p2s_get_info", "p2s_destroy", "p2s_status_string", "p2s_last_cuda_error",
             "p2s_debug_beta", "p2s_debug_blur", "p2s_debug_profile_buffer",
             "p2s_render_anchors", "p2s_render_anchors_host", "p2s_debug_blur_anchors",
-            "p2s_render_sequence")
+            "p2s_render_sequence", "p2s_sampler_init", "p2s_sample_anchors", "p2s_sampler_destroy")
 
 
 class P2SError(RuntimeError):
@@ -94,10 +94,14 @@ def load_library(path: str = LIB_PATH) -> ctypes.CDLL:
     lib.p2s_render_anchors_host.argtypes = [v, v, i, i, i, i, v, i, v, v, v]
     lib.p2s_debug_blur_anchors.argtypes = [v, _Image, v, i, v, v]
     lib.p2s_render_sequence.argtypes = [v, _Image, v, v, i, v, v]
+    lib.p2s_sampler_init.argtypes = [i, i, ctypes.c_double, v, ctypes.POINTER(v)]
+    lib.p2s_sample_anchors.argtypes = [v, ctypes.c_ulonglong, i, i, v, v]
+    lib.p2s_sampler_destroy.argtypes = [v]
+    lib.p2s_sampler_destroy.restype = None
     for name in ("p2s_init", "p2s_render", "p2s_render_host", "p2s_reserve", "p2s_set_profile_events",
                  "p2s_get_info", "p2s_debug_beta", "p2s_debug_blur", "p2s_debug_profile_buffer",
                  "p2s_render_anchors", "p2s_render_anchors_host", "p2s_debug_blur_anchors",
-                 "p2s_render_sequence"):
+                 "p2s_render_sequence", "p2s_sampler_init", "p2s_sample_anchors"):
         getattr(lib, name).restype = st
     _lib = lib
     return lib
@@ -277,6 +281,47 @@ class Renderer:
     def close(self):
         if getattr(self, "_h", None):
             self._lib.p2s_destroy(self._h)
+            self._h = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+
+class Sampler:
+    """Correlated anchor-grid sampler (include/p2s.h p2s_sampler_*): stand-in
+    separable covariance R (x) s (x) s (reading N3), Philox4x32-10 + Box-Muller normals."""
+
+    def __init__(self, G: int, n_in: int, corr_len: float, mode_cov: Optional[np.ndarray] = None):
+        lib = load_library()
+        self._lib = lib
+        self.G, self.n_in = G, n_in
+        self._h = None
+        mp = ctypes.c_void_p()
+        if mode_cov is not None:
+            self._keep = np.ascontiguousarray(mode_cov, np.float64)
+            if self._keep.shape != (n_in, n_in):
+                raise ValueError("mode_cov must be [n_in, n_in]")
+            mp = ctypes.c_void_p(self._keep.ctypes.data)
+        h = ctypes.c_void_p()
+        _check(lib.p2s_sampler_init(G, n_in, float(corr_len), mp, ctypes.byref(h)), "p2s_sampler_init")
+        self._h = h
+
+    def sample(self, seed: int, frame0: int, F: int, out=None, stream=None):
+        """Anchors [F, n_in, G, G] (CUDA fp32) of frames frame0 .. frame0 + F - 1."""
+        import torch
+        if out is None:
+            out = torch.empty((F, self.n_in, self.G, self.G), device="cuda", dtype=torch.float32)
+        _check(self._lib.p2s_sample_anchors(self._h, seed, frame0, F,
+                                            _dev_ptr(out, "anchors", (F, self.n_in, self.G, self.G)),
+                                            _stream_handle(stream)), "p2s_sample_anchors")
+        return out
+
+    def close(self):
+        if self._h:
+            self._lib.p2s_sampler_destroy(self._h)
             self._h = None
 
     def __del__(self):
