@@ -394,3 +394,65 @@ def test_sampler_empirical_covariance():
     s = sampler.spatial_cov(G, L)
     ref = np.kron(R, np.kron(s, s))
     assert np.abs(emp - ref).max() < 6 * np.sqrt(2 / 4000) * np.abs(ref).max()
+
+
+# ---- adjoint of steps a2-a3 ("differentiable module") —
+#      oracle/adjoint.py, pinned by finite differences of its independent forward
+
+def _adj_problem(seed=0, C=2, H=5, W=7, K=3, S=3, t_std=0.8):
+    rng = np.random.default_rng(seed)
+    image = rng.random((C, H, W))
+    basis = rng.standard_normal((K, S, S))
+    beta = rng.standard_normal((K, H, W))
+    tilt = t_std * rng.standard_normal((2, H, W))
+    g = rng.standard_normal((C, H, W))
+    return image, basis, beta, tilt, g
+
+
+def test_adjoint_beta_matches_finite_differences():
+    from oracle import adjoint
+    image, basis, beta, tilt, g = _adj_problem(1)
+    _, gbeta, _ = adjoint.backward(image, beta, tilt, basis, g)
+    rng = np.random.default_rng(2)
+    for _ in range(12):
+        k, y, x = rng.integers(0, beta.shape[0]), rng.integers(0, beta.shape[1]), rng.integers(0, beta.shape[2])
+        e = np.zeros_like(beta)
+        e[k, y, x] = 1e-3
+        lp = np.sum(g * adjoint.forward_from_beta(image, beta + e, tilt, basis)[0])
+        lm = np.sum(g * adjoint.forward_from_beta(image, beta - e, tilt, basis)[0])
+        assert abs((lp - lm) / 2e-3 - gbeta[k, y, x]) < 1e-9 * (1 + abs(gbeta[k, y, x]))  # linear in beta
+
+
+def test_adjoint_tilt_matches_finite_differences():
+    from oracle import adjoint
+    image, basis, beta, tilt, g = _adj_problem(3, t_std=1.3)
+    _, _, gt = adjoint.backward(image, beta, tilt, basis, g)
+    rng = np.random.default_rng(4)
+    for _ in range(16):
+        ch, y, x = rng.integers(0, 2), rng.integers(0, tilt.shape[1]), rng.integers(0, tilt.shape[2])
+        e = np.zeros_like(tilt)
+        e[ch, y, x] = 1e-7
+        lp = np.sum(g * adjoint.forward_from_beta(image, beta, tilt + e, basis)[0])
+        lm = np.sum(g * adjoint.forward_from_beta(image, beta, tilt - e, basis)[0])
+        assert abs((lp - lm) / 2e-7 - gt[ch, y, x]) < 1e-5 * (1 + abs(gt[ch, y, x]))
+
+
+def test_adjoint_warp_dot_product_identity():
+    """<g, warp(J)> = <dL/dJ, J>: the scattered bilinear weights are the exact transpose."""
+    from oracle import adjoint
+    image, basis, beta, tilt, g = _adj_problem(5, H=9, W=11, t_std=2.5)  # tilts reach the clamp
+    out, J, _ = adjoint.forward_from_beta(image, beta, tilt, basis)
+    gJ, _, _ = adjoint.backward(image, beta, tilt, basis, g)
+    assert abs(np.sum(g * out) - np.sum(gJ * J)) < 1e-10 * np.sum(np.abs(g * out))
+
+
+def test_adjoint_forward_matches_render_oracle():
+    """forward_from_beta with the MLP's beta reproduces p2s_oracle_render (two independent codes)."""
+    from oracle import adjoint
+    spec = synth.custom("adjf", 401, B=1, C=2, H=6, W=9, K=5, S=5, h1=16, h2=16, t_std=1.2)
+    inp = synth.make_inputs(spec)
+    beta = oracle.beta(inp.image, inp.zernike, inp.basis, inp.mlp)[0]
+    out, J, _ = adjoint.forward_from_beta(inp.image[0], beta, inp.tilt[0], inp.basis)
+    ref, Jref = oracle.render(inp.image, inp.zernike, inp.tilt, inp.basis, inp.mlp, want_blur=True)
+    np.testing.assert_allclose(J, Jref[0], rtol=0, atol=1e-12)
+    np.testing.assert_allclose(out, ref[0], rtol=0, atol=1e-12)
