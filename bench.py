@@ -165,6 +165,7 @@ def main():
     ap.add_argument("--no-anchor-mode", action="store_true", help="skip the anchor-grid (NEXT-1) extra leg")
     ap.add_argument("--no-batch-mode", action="store_true", help="skip the 16-frame batched-launch extra leg")
     ap.add_argument("--no-sequence-mode", action="store_true", help="skip the 50-frame sequence extra leg")
+    ap.add_argument("--no-adjoint-mode", action="store_true", help="skip the adjoint (NEXT-4) extra leg")
     args = ap.parse_args()
 
     rank, world, local_rank = pdist.env_rank_world()
@@ -331,6 +332,35 @@ def main():
                                  "the K convolutions are computed once per tile and shared by the frames"}
         del simg, sz, st_, sout
 
+    # ---- adjoint: dL/dbeta and dL/dt of one cfg3 frame for an upstream
+    # gradient (p2s_backward: forward recompute for J, warp-transpose scatter, conv-only fused pass)
+    adjoint_mode = None
+    if not args.no_adjoint_mode:
+        ainp = synth.make_inputs(spec, frames=pdist.rank_frames(rank, 1))
+        aimg, az, at = (torch.from_numpy(a).to(dev) for a in (ainp.image, ainp.zernike, ainp.tilt))
+        ag = torch.from_numpy(synth.make_upstream_grad(spec, frames=pdist.rank_frames(rank, 1))).to(dev)
+        res = {}
+        for key, wb, wt in (("value", True, True), ("beta_only", True, False)):
+            for _ in range(3):
+                r.backward(aimg, az, at, ag, want_beta=wb, want_tilt=wt)
+            n_a = max(5, min(args.steps // 4, 50))
+            a0 = [torch.cuda.Event(enable_timing=True) for _ in range(n_a)]
+            a1 = [torch.cuda.Event(enable_timing=True) for _ in range(n_a)]
+            torch.cuda.synchronize()
+            for i in range(n_a):
+                flush.fill_(float(i))
+                a0[i].record(stream)
+                r.backward(aimg, az, at, ag, want_beta=wb, want_tilt=wt)
+                a1[i].record(stream)
+            torch.cuda.synchronize()
+            a_ms = pdist.max_over_ranks(float(sum(a0[i].elapsed_time(a1[i]) for i in range(n_a))), dist, dev)
+            res[key] = pdist.throughput(1, world, n_a, a_ms)
+        adjoint_mode = {"value": res["value"], "unit": "frames/s", "beta_only": res["beta_only"],
+                        "api": "p2s_backward",
+                        "note": "dL/dbeta [K,H,W] + dL/dt [2,H,W] of one cfg3 frame (L2 flushed per call); "
+                                "includes the forward recompute needed for dL/dt; beta_only skips it"}
+        del aimg, az, at, ag
+
     # ---- anchor-grid mode: the same frame with its Zernike coefficients
     # given on a 16x16 anchor grid and interpolated inside the fused kernel (not the headline
     # workload, which BASELINE.json defines on a dense field); same timing protocol
@@ -433,6 +463,7 @@ def main():
         "anchor_mode": anchor_mode,
         "batch_mode": batch_mode,
         "sequence_mode": sequence_mode,
+        "adjoint_mode": adjoint_mode,
         "clocks": clk.summary(),
         "wall_s": t_wall,
         "plan": info,

@@ -128,6 +128,21 @@ P2S_API p2s_status p2s_render_anchors_host(p2s_handle* h, const float* image_hos
 P2S_API p2s_status p2s_render_sequence(p2s_handle* h, p2s_image image, const float* zernike_field,
                                        const float* tilt_field, int F, float* out, p2s_stream_t stream);
 
+/* Adjoint of steps a2-a3 ("differentiable module"): for the
+ * frames p2s_render would produce and an upstream gradient grad_out = dL/dout (DEVICE
+ * [B][C][H][W] fp32), writes
+ *   grad_beta (DEVICE [B][K][H][W] or NULL) = dL/dbeta_k(p) = sum_c dL/dJ_c(p) C_kc(p)
+ *   grad_tilt (DEVICE [B][2][H][W] or NULL) = dL/dt(p) through the bilinear warp (0 where the
+ *     coordinate clamp is active)
+ * where dL/dJ scatters grad_out through the warp's bilinear weights (float atomics: the
+ * summation order, hence the last bits, vary run to run). The image gradient (a scatter-order
+ * transpose convolution) is not provided yet. grad_beta recomputes the K convolutions on the
+ * tensor cores; grad_tilt also recomputes J (one forward). Errors as p2s_render; both outputs
+ * NULL -> P2S_ERR_INVALID_ARG. */
+P2S_API p2s_status p2s_backward(p2s_handle* h, p2s_image image, const float* zernike_field,
+                                const float* tilt_field, const float* grad_out, float* grad_beta,
+                                float* grad_tilt, p2s_stream_t stream);
+
 /* ---- correlated anchor sampling (Sec. 3.4: anchor
  * coefficient sets "drawn from the correlation matrix", which "can be pre-computed") ----
  * Stand-in covariance (reading N3; the paper's Takato-formula parameters are absent):

@@ -43,10 +43,14 @@ def conv_all(image: np.ndarray, basis: np.ndarray) -> np.ndarray:
     return out
 
 
-def _warp_coords(tilt, H, W):
-    y, x = np.meshgrid(np.arange(H, dtype=np.float64), np.arange(W, dtype=np.float64), indexing="ij")
-    sy_raw = y - tilt[1].astype(np.float64)
-    sx_raw = x - tilt[0].astype(np.float64)
+def _warp_coords(tilt, H, W, coord_dtype=np.float64):
+    """Source coordinates s = p - t(p) and their bilinear cell. coord_dtype is the precision s is
+    formed in: the cell (an integer) is decided there, and d out/d s jumps across cell edges, so
+    the GPU parity tests pass np.float32 -- the kernel's precision (reading N4). The
+    weights and everything after them stay fp64."""
+    y, x = np.meshgrid(np.arange(H), np.arange(W), indexing="ij")
+    sy_raw = (y.astype(coord_dtype) - tilt[1].astype(coord_dtype)).astype(np.float64)
+    sx_raw = (x.astype(coord_dtype) - tilt[0].astype(coord_dtype)).astype(np.float64)
     sy, sx = _clamp(sy_raw, -1.0, float(H)), _clamp(sx_raw, -1.0, float(W))
     y0, x0 = np.floor(sy), np.floor(sx)
     fy, fx = sy - y0, sx - x0
@@ -69,17 +73,40 @@ def forward_from_beta(image, beta, tilt, basis):
     return out, J, Ck
 
 
-def backward(image, beta, tilt, basis, g):
-    """(dL/dJ [C][H][W], dL/dbeta [K][H][W], dL/dt [2][H][W]) for upstream g [C][H][W]."""
-    _, J, Ck = forward_from_beta(image, beta, tilt, basis)
-    C_, H, W = J.shape
+def conv_at(image, basis, yx):
+    """C_kc at the listed pixels only: [n][K][C] (fp64), the sum of conv_all's definition."""
+    C_, H, W = image.shape
+    K, S, _ = basis.shape
+    r = (S - 1) // 2
+    out = np.zeros((len(yx), K, C_))
+    for n, (y, x) in enumerate(yx):
+        yy = _clamp(y - (np.arange(S) - r), 0, H - 1)
+        xx = _clamp(x - (np.arange(S) - r), 0, W - 1)
+        patch = image[:, yy][:, :, xx].astype(np.float64)  # [C][i][j] = I_c[cY(y-(i-r))][cX(x-(j-r))]
+        out[n] = np.einsum("kij,cij->kc", basis.astype(np.float64), patch)
+    return out
+
+
+def grad_J(tilt, g, coord_dtype=np.float64):
+    """dL/dJ [C][H][W]: g scattered through the warp's bilinear weights (the transpose of step a3)."""
+    C_, H, W = g.shape
     g = g.astype(np.float64)
-    ya, yb, xa, xb, fy, fx, in_y, in_x = _warp_coords(tilt, H, W)
-    gJ = np.zeros_like(J)
+    ya, yb, xa, xb, fy, fx, _, _ = _warp_coords(tilt, H, W, coord_dtype)
+    gJ = np.zeros((C_, H, W))
     for (yy, xx, w) in ((ya, xa, (1 - fy) * (1 - fx)), (ya, xb, (1 - fy) * fx),
                         (yb, xa, fy * (1 - fx)), (yb, xb, fy * fx)):
         for c in range(C_):
             np.add.at(gJ[c], (yy, xx), g[c] * w)
+    return gJ
+
+
+def backward(image, beta, tilt, basis, g, coord_dtype=np.float64):
+    """(dL/dJ [C][H][W], dL/dbeta [K][H][W], dL/dt [2][H][W]) for upstream g [C][H][W]."""
+    _, J, Ck = forward_from_beta(image, beta, tilt, basis)
+    C_, H, W = J.shape
+    g = g.astype(np.float64)
+    ya, yb, xa, xb, fy, fx, in_y, in_x = _warp_coords(tilt, H, W, coord_dtype)
+    gJ = grad_J(tilt, g, coord_dtype)
     gbeta = np.einsum("chw,kchw->khw", gJ, Ck)
     # d out / d sx = (1-fy)(J[ya][xb] - J[ya][xa]) + fy (J[yb][xb] - J[yb][xa]); sx = x - t_x
     dsx = (1 - fy) * (J[:, ya, xb] - J[:, ya, xa]) + fy * (J[:, yb, xb] - J[:, yb, xa])
@@ -88,3 +115,26 @@ def backward(image, beta, tilt, basis, g):
     gt[0] = -np.where(in_x, (g * dsx).sum(0), 0.0)
     gt[1] = -np.where(in_y, (g * dsy).sum(0), 0.0)
     return gJ, gbeta, gt
+
+
+def backward_at(image, beta, tilt, basis, g, yx, coord_dtype=np.float64):
+    """backward's dL/dbeta [n][K] and dL/dt [n][2] at the listed pixels only (full-size frames):
+    dL/dJ over the whole frame (cheap), C_kc and J only where the listed pixels need them."""
+    C_, H, W = image.shape
+    g = g.astype(np.float64)
+    gJ = grad_J(tilt, g, coord_dtype)
+    ya, yb, xa, xb, fy, fx, in_y, in_x = _warp_coords(tilt, H, W, coord_dtype)
+    gbeta = np.zeros((len(yx), beta.shape[0]))
+    gt = np.zeros((len(yx), 2))
+    for n, (y, x) in enumerate(yx):
+        gbeta[n] = conv_at(image, basis, [(y, x)])[0] @ gJ[:, y, x]
+        corners = [(ya[y, x], xa[y, x]), (ya[y, x], xb[y, x]), (yb[y, x], xa[y, x]), (yb[y, x], xb[y, x])]
+        Ck = conv_at(image, basis, corners)                                  # [4][K][C]
+        Jc = np.einsum("nk,nkc->nc", np.stack([beta[:, q, p] for q, p in corners]), Ck)  # J_c at corners
+        j00, j01, j10, j11 = Jc
+        a, b = fy[y, x], fx[y, x]
+        dsx = (1 - a) * (j01 - j00) + a * (j11 - j10)
+        dsy = (1 - b) * (j10 - j00) + b * (j11 - j01)
+        gt[n, 0] = -(g[:, y, x] @ dsx) if in_x[y, x] else 0.0
+        gt[n, 1] = -(g[:, y, x] @ dsy) if in_y[y, x] else 0.0
+    return gbeta, gt

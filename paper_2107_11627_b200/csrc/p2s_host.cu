@@ -114,7 +114,9 @@ struct p2s_handle {
   int K, S, r, n_in, h1, h2, Nk, K1, N1, N2;
   ConvPlan plan;
   std::vector<Item> items;  // [items_full | items_beta]
-  int n_items_full = 0, n_items_beta = 0, n_items_first = 0, n_items_seq = 0, tab_cap = 0;
+  int n_items_full = 0, n_items_beta = 0, n_items_first = 0, n_items_seq = 0, n_items_conv = 0, tab_cap = 0;
+  float* d_gJ = nullptr;  // adjoint workspace dL/dJ
+  size_t gJ_cap = 0;
   MlpOp ops[kMaxOps];  // [0, n_ops) per-tile ops, then n_fops first-tile whole-layer ops
   int n_ops = 0, n_fops = 0;
   bool bias_folded = false;
@@ -178,6 +180,7 @@ FusedParams make_params(const p2s_handle* h, int B, int C, int H, int W, int mod
   p.n_items_beta = h->n_items_beta;
   p.n_items_first = h->n_items_first;
   p.n_items_seq = h->n_items_seq;
+  p.n_items_conv = h->n_items_conv;
   p.nfr = 1;
   p.tab_cap = h->tab_cap;
   p.off_mma = h->off_tab + h->tab_cap * (int)sizeof(Item);
@@ -219,7 +222,8 @@ p2s_status launch_fused(p2s_handle* h, const FusedParams& p, cudaStream_t st) {
   // persistent grid of CTA pairs (clusters of 2): at most one CTA per SM
   const int npairs = (p.ntiles + 1) / 2;
   const int grid = 2 * std::max(1, std::min(h->sm_count / 2, npairs));
-  if (p.anchors) k_fused_p2s<true><<<grid, kThreads, h->smem_bytes, st>>>(p);
+  if (p.mode == 2) k_fused_p2s<false, true><<<grid, kThreads, h->smem_bytes, st>>>(p);
+  else if (p.anchors) k_fused_p2s<true><<<grid, kThreads, h->smem_bytes, st>>>(p);
   else k_fused_p2s<false><<<grid, kThreads, h->smem_bytes, st>>>(p);
   P2S_CUDA(cudaPeekAtLastError());
   return P2S_OK;
@@ -562,6 +566,8 @@ p2s_status p2s_init(const p2s_basis* basis, const p2s_mlp* mlp, p2s_handle** out
   h->items.insert(h->items.end(), beta.begin(), beta.end());
   h->items.insert(h->items.end(), first.begin(), first.end());
   h->items.insert(h->items.end(), beta.begin(), beta.end());  // seq list (same B stream)
+  h->n_items_conv = (int)conv_items.size();  // adjoint (mode 2): conv stages only
+  h->items.insert(h->items.end(), conv_items.begin(), conv_items.end());
   // UMMA-side view of every item (precomputed so the issue loop does one LDS.128 per item)
   auto mma_of = [&](const Item& it, int mode, bool first_tile) {
     MmaItem mi{};
@@ -569,7 +575,9 @@ p2s_status p2s_init(const p2s_basis* basis, const p2s_mlp* mlp, p2s_handle** out
     mi.nslabs = (uint8_t)it.nslabs;
     if (it.kind == 1) {
       mi.n16 = (uint8_t)(h->Nk / 16);
-      mi.flags = MI_CONV | ((it.flags & IT_BEGIN) ? MI_WAIT_E : 0) | ((it.flags & IT_END) ? MI_COMMIT_ACC : 0);
+      // mode 3 = the adjoint's conv-only list: its first stage also waits for the accumulators
+      mi.flags = MI_CONV | ((it.flags & IT_BEGIN) ? (MI_WAIT_E | (mode == 3 ? MI_WAIT_TMEM : 0)) : 0) |
+                 ((it.flags & IT_END) ? MI_COMMIT_ACC : 0);
       return mi;
     }
     const MlpOp& op = h->ops[it.op];
@@ -602,6 +610,7 @@ p2s_status p2s_init(const p2s_basis* basis, const p2s_mlp* mlp, p2s_handle** out
   for (const Item& it : beta) h->mma_items.push_back(mma_of(it, 1, false));
   for (const Item& it : first) h->mma_items.push_back(mma_of(it, 0, true));
   for (const Item& it : beta) h->mma_items.push_back(mma_of(it, 2, false));
+  for (const Item& it : conv_items) h->mma_items.push_back(mma_of(it, 3, false));
 
   // ---- constants: b3, svec (128 each), b1, b2 (kMaxN each), zero padded;
   //      svec[k] = sum of the taps of phi_k (centred-image identity)
@@ -657,7 +666,9 @@ p2s_status p2s_init(const p2s_basis* basis, const p2s_mlp* mlp, p2s_handle** out
   if ((e = cudaFuncSetAttribute(k_fused_p2s<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, kSmemLimit)) !=
           cudaSuccess ||
       (e = cudaFuncSetAttribute(k_fused_p2s<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, kSmemLimit)) !=
-          cudaSuccess)
+          cudaSuccess ||
+      (e = cudaFuncSetAttribute(k_fused_p2s<false, true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                kSmemLimit)) != cudaSuccess)
     return fail(cuda_fail(e, "cudaFuncSetAttribute"));
   *out_handle = h;
   return P2S_OK;
@@ -739,6 +750,47 @@ p2s_status p2s_render_sequence(p2s_handle* h, p2s_image im, const float* zernike
   if (s != P2S_OK) return s;
   if (h->ev_end) P2S_CUDA(cudaEventRecord(h->ev_end, st));
   return launch_warp(h, h->d_J, tilt_field, out, F, im.C, im.H, im.W, st);
+}
+
+p2s_status p2s_backward(p2s_handle* h, p2s_image im, const float* zernike_field, const float* tilt_field,
+                        const float* grad_out, float* grad_beta, float* grad_tilt, p2s_stream_t stream) {
+  p2s_status s = check_image(h, im);
+  if (s != P2S_OK) return s;
+  if (!zernike_field || !grad_out || (!grad_beta && !grad_tilt)) return P2S_ERR_INVALID_ARG;
+  cudaStream_t st = (cudaStream_t)stream;
+  const size_t HW = (size_t)im.H * im.W, chw = (size_t)im.B * im.C * HW;
+  s = ensure_J(h, chw);
+  if (s != P2S_OK) return s;
+  if (chw > h->gJ_cap) {
+    P2S_CUDA(cudaDeviceSynchronize());
+    cudaFree(h->d_gJ);
+    h->d_gJ = nullptr;
+    h->gJ_cap = 0;
+    P2S_CUDA(cudaMalloc(&h->d_gJ, chw * sizeof(float)));
+    h->gJ_cap = chw;
+  }
+  if (grad_tilt) {  // J (the forward blur) is needed only for dL/dt
+    FusedParams p = make_params(h, im.B, im.C, im.H, im.W, 0);
+    p.image = im.data;
+    p.zernike = zernike_field;
+    p.J = h->d_J;
+    s = launch_fused(h, p, st);
+    if (s != P2S_OK) return s;
+  }
+  P2S_CUDA(cudaMemsetAsync(h->d_gJ, 0, chw * sizeof(float), st));
+  const size_t npx = (size_t)im.B * HW;
+  const int grid = (int)std::min<size_t>((npx + 255) / 256, (size_t)h->sm_count * 16);
+  k_warp_backward<<<grid, 256, 0, st>>>(h->d_J, tilt_field, grad_out, h->d_gJ, grad_tilt, im.B, im.C, im.H, im.W);
+  P2S_CUDA(cudaPeekAtLastError());
+  if (grad_beta) {  // dL/dbeta_k = sum_c dL/dJ_c C_kc: the K convolutions again, another epilogue
+    FusedParams p = make_params(h, im.B, im.C, im.H, im.W, 2);
+    p.image = im.data;
+    p.gJ = h->d_gJ;
+    p.beta_out = grad_beta;
+    s = launch_fused(h, p, st);
+    if (s != P2S_OK) return s;
+  }
+  return P2S_OK;
 }
 
 p2s_status p2s_render_anchors(p2s_handle* h, p2s_image im, const float* anchors, int G,
@@ -979,6 +1031,7 @@ void p2s_destroy(p2s_handle* h) {
   cudaFree(h->d_stream); cudaFree(h->d_items); cudaFree(h->d_mma); cudaFree(h->d_steps); cudaFree(h->d_consts);
   cudaFree(h->d_J);
   cudaFree(h->h_img); cudaFree(h->h_z); cudaFree(h->h_t); cudaFree(h->h_out); cudaFree(h->h_anc);
+  cudaFree(h->d_gJ);
   if (h->s_in) cudaStreamDestroy(h->s_in);
   if (h->ev_entry) cudaEventDestroy(h->ev_entry);
   if (h->ev_band) cudaEventDestroy(h->ev_band);

@@ -106,13 +106,15 @@ struct FusedParams {
   int G;
   int off_anc, anc_cols;  // shared table of y-interpolated anchor rows [n_in][anc_cols] (per tile)
   float* J;              // [B][C][H][W] (mode 0)
-  float* beta_out;       // [B][K][H][W] (mode 1)
+  float* beta_out;       // [B][K][H][W] (mode 1: beta; mode 2: dL/dbeta)
+  const float* gJ;       // [B][C][H][W] dL/dJ (mode 2, the adjoint: SURVEY NEXT-4)
   int B, C, H, W, n_in;
-  int nstrips, ntiles, mode;  // mode 0: MLP + conv -> J ; mode 1: MLP only -> beta
+  int nstrips, ntiles, mode;  // mode 0: MLP + conv -> J ; mode 1: MLP only -> beta ;
+                              // mode 2: conv only -> dL/dbeta = sum_c dL/dJ_c C_kc (adjoint)
   int y0, ny;                 // rows [y0, y0 + ny) of every frame (a band of the host path)
   const uint8_t* stream;
   const Item* items;          // [items_full | items_beta | items_first | items_seq]
-  int n_items_full, n_items_beta, n_items_first, n_items_seq;
+  int n_items_full, n_items_beta, n_items_first, n_items_seq, n_items_conv;
   int nfr;                    // frames per tile: 1, or a sequence's length (sequence mode: frames
                               // share the image, so each tile's convolutions serve all of them)
   int tab_cap;                // entries of the shared-memory item tables
@@ -330,6 +332,38 @@ __device__ __forceinline__ void build_E_all(const FusedParams& p, uint8_t* Eb, c
 // One 16-column group of the conv epilogue (Eq. 5 reduction): NC real columns of beta (scratch)
 // and of each channel's accumulator, fp32x2 FMAs into jc2 (sum_k beta_k C_k) and bs2
 // (sum_k beta_k s_k for the centring term).
+// adjoint epilogue (mode 2) for NC channels: dL/dbeta_k = sum_c dL/dJ_c C_kc over this warp
+// group's 16-column groups; C_kc = C'_kc + 0.5 s_k (C' convolves the centred image, s_k = tap sum)
+// (s_k is read through L1 from the global table: using the shared copy here made ptxas drop the
+// MMA warp's uniformity in this instantiation -- R2UR.BROADCAST before every UMMA, SASS-checked)
+template <int NC>
+__device__ __forceinline__ void adj_epi(uint32_t tl, int Nk, int K, int wg, int GK, const float* gJ, size_t HW,
+                                        const float* __restrict__ sv, float* out, bool st) {
+  float gj[NC], gsum = 0.f;
+#pragma unroll
+  for (int c = 0; c < NC; ++c) {
+    gj[c] = st ? __ldg(gJ + c * HW) : 0.f;
+    gsum += gj[c];
+  }
+  for (int gi = wg; gi < GK; gi += 2) {
+    float av[NC][16];
+#pragma unroll
+    for (int c = 0; c < NC; ++c) tmem_ld16(tl + c * Nk + gi * 16, av[c]);
+    tmem_ld_wait();
+    if (st)
+#pragma unroll
+      for (int i = 0; i < 16; ++i) {
+        const int k = gi * 16 + i;
+        if (k < K) {
+          float v = 0.5f * __ldg(sv + k) * gsum;
+#pragma unroll
+          for (int c = 0; c < NC; ++c) v = fmaf(gj[c], av[c][i], v);
+          out[(size_t)k * HW] = v;
+        }
+      }
+  }
+}
+
 template <int NC>
 __device__ __forceinline__ void conv_epi_group(uint32_t tl, int scr_col, int Nk, int gi, int C,
                                                const float* sB3, const float* sSv, float2 (&jc2)[3],
@@ -440,8 +474,9 @@ __device__ __noinline__ void build_A1_anchors(const FusedParams& p, uint8_t* dst
 
 // kAnchors: Zernike input from an anchor grid (p.anchors) instead of a dense field. A separate
 // instantiation: merely having the anchor path in the builders cost the dense kernel ~80 B of
-// register spills and ~1.5 % (measured).
-template <bool kAnchors>
+// register spills and ~1.5 % (measured). kAdjoint: mode 2 (conv-only lists, dL/dbeta epilogue),
+// likewise its own instantiation; the render instantiations see mode & 1 only (0 or 1).
+template <bool kAnchors, bool kAdjoint = false>
 __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads)
     k_fused_p2s(const __grid_constant__ FusedParams p) {
   extern __shared__ __align__(1024) uint8_t smem[];
@@ -474,11 +509,13 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads)
   const int ncl = gridDim.x >> 1, cl = blockIdx.x >> 1;
   const int pr_begin = (int)(((long long)cl * npairs) / ncl);
   const int pr_end = (int)(((long long)(cl + 1) * npairs) / ncl);
+  const int pmode = kAdjoint ? 2 : (p.mode & 1);
   // per-tile item lists: tile 0 of this CTA uses list A (MLP first), later tiles list B
-  const int nA = p.mode == 0 ? p.n_items_first : p.n_items_beta;
-  const int nB = p.mode == 0 ? p.n_items_full : p.n_items_beta;
-  const int offA = p.mode == 0 ? p.n_items_full + p.n_items_beta : p.n_items_full;
-  const int offB = p.mode == 0 ? 0 : p.n_items_full;
+  const int offC = p.n_items_full + p.n_items_beta + p.n_items_first + p.n_items_seq;  // conv-only list
+  const int nA = pmode == 0 ? p.n_items_first : (pmode == 1 ? p.n_items_beta : p.n_items_conv);
+  const int nB = pmode == 0 ? p.n_items_full : (pmode == 1 ? p.n_items_beta : p.n_items_conv);
+  const int offA = pmode == 0 ? p.n_items_full + p.n_items_beta : (pmode == 1 ? p.n_items_full : offC);
+  const int offB = pmode == 0 ? 0 : (pmode == 1 ? p.n_items_full : offC);
   // sequence mode: after a tile's first frame (list A / B), nfr - 1 MLP-only lists S
   const int nS = p.nfr > 1 ? p.n_items_seq : 0;
   const int offS = p.n_items_full + p.n_items_beta + p.n_items_first;
@@ -577,7 +614,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads)
     const uint32_t stage16 = (uint32_t)p.stage_bytes >> 4;
     const uint32_t ch16 = (uint32_t)p.chan_bytes >> 4;
     const uint32_t ebuf16 = 3u * ch16;
-    const int C = p.C, nring = p.nring, ebufs = p.n_ebuf, mode = p.mode;
+    const int C = p.C, nring = p.nring, ebufs = p.n_ebuf, mode = pmode;
     const uint32_t acc1 = tmem + (uint32_t)p.Nk, acc2 = tmem + 2u * (uint32_t)p.Nk;
     const uint32_t smem_lo = smem_u32(smem) >> 4;
     const uint32_t id_base = idesc_f16(256, 0);
@@ -601,12 +638,12 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads)
 #ifdef P2S_PROFILE
       const long long tr_a = clock64();
 #endif
-      if (f & MI_WAIT_A1) {
+      if (!kAdjoint && (f & MI_WAIT_A1)) {
         { PROF_T0(); mbar_wait(&bars[BAR_A1_FULL], a1_waits & 1); PROF_ADD(0); }
         ++a1_waits;
       }
       if (f & MI_WAIT_TMEM) { PROF_T0(); mbar_wait(&bars[BAR_TMEM_FREE], (it & 1) ^ 1); PROF_ADD(1); }
-      if (f & MI_WAIT_SCR) {
+      if (!kAdjoint && (f & MI_WAIT_SCR)) {
         { PROF_T0(); mbar_wait(&bars[BAR_SCR_FREE], scr_waits & 1); PROF_ADD(2); }
         ++scr_waits;
       }
@@ -625,7 +662,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads)
 #if defined(P2S_ABL_NOCONVMMA)
       if ((f & MI_CONV) && n == 0) {
 #else
-      if (f & MI_CONV) {
+      if (kAdjoint || (f & MI_CONV)) {  // (the adjoint's lists hold conv stages only)
 #endif
         PROF_T0();
         const uint32_t e0 = e_lo + (uint32_t)eb * ebuf16;
@@ -673,7 +710,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads)
         if (f & MI_COMMIT_A1) umma2_commit_elect(&bars[BAR_A1_EMPTY]);
         if (f & MI_COMMIT_MLP) umma2_commit_elect(&bars[BAR_MLP_DONE]);
         if (f & MI_COMMIT_ACC) {
-          if ((f & MI_CONV) && mode == 0) {
+          if ((f & MI_CONV) && mode != 1) {
             umma2_commit_elect(&bars[BAR_E_EMPTY0 + eb]);
             if (eb) ++e_use1; else ++e_use0;
           }
@@ -710,33 +747,35 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads)
       const int t = min(2 * pr + (int)rank, p.ntiles - 1);  // odd tail: duplicate, not stored
       int b, y, x0;
       tile_coords(p, t, b, y, x0);
-      // --- A1 of frame b + fr (sequence mode: every frame of the image's sequence): row m =
-      //     pixel x0+m, k = Zernike index (zero-padded to K1)
-      { PROF_T0(); WAIT_BUILD(&bars[BAR_A1_EMPTY], (a1_builds & 1) ^ 1); PROF_ADD(9); }
-      ++a1_builds;
-      {
-        const int m = tid;
-        const int x = min(x0 + m, p.W - 1);
-        uint8_t* dst = sA1 + (m & 7) * 16 + (m >> 3) * p.a1_sbo;
-        if constexpr (!kAnchors) {
-          const float* zp = p.zernike + (size_t)(b + fr) * p.n_in * HW + (size_t)y * p.W + x;
-          for (int k0 = 0; k0 < p.K1; k0 += 16) {
-            float v[16];
-#pragma unroll
-            for (int i = 0; i < 16; ++i)
-              v[i] = (k0 + i < p.n_in) ? __ldg(zp + (size_t)(k0 + i) * HW)
-                                       : ((p.bias_folded && k0 + i < p.n_in + 2) ? 1.f : 0.f);
-            *reinterpret_cast<uint4*>(dst + (k0 >> 3) * 128) = pack8(v);
-            *reinterpret_cast<uint4*>(dst + ((k0 >> 3) + 1) * 128) = pack8(v + 8);
+      if (pmode != 2) {  // (mode 2, the adjoint, needs only the E views)
+        // --- A1 of frame b + fr (sequence mode: every frame of the image's sequence): row m =
+        //     pixel x0+m, k = Zernike index (zero-padded to K1)
+        { PROF_T0(); WAIT_BUILD(&bars[BAR_A1_EMPTY], (a1_builds & 1) ^ 1); PROF_ADD(9); }
+        ++a1_builds;
+        {
+          const int m = tid;
+          const int x = min(x0 + m, p.W - 1);
+          uint8_t* dst = sA1 + (m & 7) * 16 + (m >> 3) * p.a1_sbo;
+          if constexpr (!kAnchors) {
+            const float* zp = p.zernike + (size_t)(b + fr) * p.n_in * HW + (size_t)y * p.W + x;
+            for (int k0 = 0; k0 < p.K1; k0 += 16) {
+              float v[16];
+  #pragma unroll
+              for (int i = 0; i < 16; ++i)
+                v[i] = (k0 + i < p.n_in) ? __ldg(zp + (size_t)(k0 + i) * HW)
+                                         : ((p.bias_folded && k0 + i < p.n_in + 2) ? 1.f : 0.f);
+              *reinterpret_cast<uint4*>(dst + (k0 >> 3) * 128) = pack8(v);
+              *reinterpret_cast<uint4*>(dst + ((k0 >> 3) + 1) * 128) = pack8(v + 8);
+            }
+          } else {
+            build_A1_anchors(p, dst, b + fr, y, x0, x, tid, smem);
           }
-        } else {
-          build_A1_anchors(p, dst, b + fr, y, x0, x, tid, smem);
         }
+        fence_proxy_async_smem();
+        __syncwarp();
+        if (lane == 0) mbar_arrive_remote(&bars[BAR_A1_FULL], 0);
       }
-      fence_proxy_async_smem();
-      __syncwarp();
-      if (lane == 0) mbar_arrive_remote(&bars[BAR_A1_FULL], 0);
-      if (p.mode != 0 || fr > 0) continue;  // E views: once per tile (every frame shares the image)
+      if (pmode == 1 || fr > 0) continue;  // E views: once per tile (every frame shares the image)
       // --- E views of every channel (the CTA's first tile: built by the idle epilogue warps)
       const int eb = p.n_ebuf == 2 ? (it & 1) : 0;
       if (it == 0) { ++e_use0; continue; }
@@ -761,7 +800,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads)
     // chain of cold loads. (tile_coords() here, not in the shared prologue: there it cost the
     // UMMA issuer its convergence proof - ptxas then wraps every elect in a loop; test_abi_cpu
     // checks the SASS.)
-    if (pr_begin < pr_end && p.mode == 0) {
+    if (pr_begin < pr_end && pmode != 1) {
       int b0, y0, xs;
       tile_coords(p, min(2 * pr_begin + (int)rank, p.ntiles - 1), b0, y0, xs);
       const size_t HW0 = (size_t)p.H * p.W;
@@ -792,8 +831,8 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads)
       int b, y, x0;
       tile_coords(p, min(t_raw, p.ntiles - 1), b, y, x0);
       // a CTA's first tile (mode 0) runs L1 and L2 as whole-layer ops (p.ops[n_ops, +n_fops))
-      const bool fops = p.mode == 0 && it == 0 && fr == 0 && p.n_fops > 0;
-      const int o_begin = fops ? p.n_ops : 0, o_end = fops ? p.n_ops + p.n_fops : p.n_ops;
+      const bool fops = pmode == 0 && it == 0 && fr == 0 && p.n_fops > 0;
+      const int o_begin = fops ? p.n_ops : 0, o_end = pmode == 2 ? 0 : (fops ? p.n_ops + p.n_fops : p.n_ops);
       for (int o = o_begin; o < o_end; ++o) {
         const MlpOp op = p.ops[o];
         if (op.layer == 2) continue;        // beta stays in TMEM for the conv epilogue
@@ -874,7 +913,20 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads)
       const int x = x0 + m;
       const int GK = p.Nk >> 4;
       const int GF = p.K >> 4, tail = p.K & 15;  // full 16-column groups, real columns after them
-      if (p.mode == 1) {
+      if (pmode == 2) {
+        // adjoint: dL/dbeta_k = sum_c dL/dJ_c C_kc, with C_kc = C'_kc + 0.5 s_k
+        // (C' convolves the centred image; s_k = tap sum of phi_k)
+        const bool st = store && x < p.W;
+        const size_t pix = (size_t)y * p.W + x;
+        const float* gJb = p.gJ + (size_t)b * C * HW + pix;
+        float* ob = p.beta_out + (size_t)b * p.K * HW + pix;
+        if (C == 3) adj_epi<3>(tl, p.Nk, p.K, wg, GK, gJb, HW, p.consts + 128, ob, st);
+        else if (C == 2) adj_epi<2>(tl, p.Nk, p.K, wg, GK, gJb, HW, p.consts + 128, ob, st);
+        else adj_epi<1>(tl, p.Nk, p.K, wg, GK, gJb, HW, p.consts + 128, ob, st);
+        tc_fence_before();
+        __syncwarp();
+        if (lane == 0) mbar_arrive_remote(&bars[BAR_TMEM_FREE], 0);
+      } else if (pmode == 1) {
         for (int gi = wg; gi < GK; gi += 2) {
           float bv[16];
           tmem_ld16(tl + p.scr_col + gi * 16, bv);
@@ -921,7 +973,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads)
           }
         }
       }
-      if (p.mode == 1) {
+      if (pmode == 1) {
         tc_fence_before();
         __syncwarp();
         if (lane == 0) mbar_arrive_remote(&bars[BAR_TMEM_FREE], 0);
@@ -1028,6 +1080,53 @@ __global__ void __launch_bounds__(256) k_tilt_warp(const float* __restrict__ J, 
       const float v = w00 * __ldg(Jc + (size_t)ya * W + xa) + w01 * __ldg(Jc + (size_t)ya * W + xb) +
                       w10 * __ldg(Jc + (size_t)yb * W + xa) + w11 * __ldg(Jc + (size_t)yb * W + xb);
       out[(b * C + c) * HW + pix] = v;
+    }
+  }
+}
+
+// Adjoint of the tilt warp (oracle/adjoint.py): per output pixel p, the
+// bilinear weights scatter g_c(p) into dL/dJ (atomicAdd, gJ zeroed by the caller) and
+// dL/dt(p) = -sum_c g_c(p) d out_c / d s (0 where the coordinate clamp is active).
+__global__ void __launch_bounds__(256) k_warp_backward(const float* __restrict__ J, const float* __restrict__ tilt,
+                                                       const float* __restrict__ g, float* __restrict__ gJ,
+                                                       float* __restrict__ gt, int B, int C, int H, int W) {
+  const size_t HW = (size_t)H * W;
+  const size_t n = (size_t)B * HW;
+  for (size_t i = blockIdx.x * (size_t)blockDim.x + threadIdx.x; i < n; i += (size_t)gridDim.x * blockDim.x) {
+    const size_t b = i / HW, pix = i - b * HW;
+    const int y = (int)(pix / W), x = (int)(pix - (size_t)y * W);
+    float tx = 0.f, ty = 0.f;
+    if (tilt) {
+      tx = __ldg(tilt + (b * 2 + 0) * HW + pix);
+      ty = __ldg(tilt + (b * 2 + 1) * HW + pix);
+    }
+    const float syr = (float)y - ty, sxr = (float)x - tx;
+    const float sy = fminf(fmaxf(syr, -1.f), (float)H), sx = fminf(fmaxf(sxr, -1.f), (float)W);
+    const float fy0 = floorf(sy), fx0 = floorf(sx);
+    const float fy = sy - fy0, fx = sx - fx0;
+    const int y0 = (int)fy0, x0 = (int)fx0;
+    const int ya = clampi(y0, 0, H - 1), yb = clampi(y0 + 1, 0, H - 1);
+    const int xa = clampi(x0, 0, W - 1), xb = clampi(x0 + 1, 0, W - 1);
+    const float w00 = (1.f - fy) * (1.f - fx), w01 = (1.f - fy) * fx, w10 = fy * (1.f - fx), w11 = fy * fx;
+    float dsx = 0.f, dsy = 0.f;
+    for (int c = 0; c < C; ++c) {
+      const float gc = __ldg(g + (b * C + c) * HW + pix);
+      float* gJc = gJ + (b * C + c) * HW;
+      atomicAdd(gJc + (size_t)ya * W + xa, gc * w00);
+      atomicAdd(gJc + (size_t)ya * W + xb, gc * w01);
+      atomicAdd(gJc + (size_t)yb * W + xa, gc * w10);
+      atomicAdd(gJc + (size_t)yb * W + xb, gc * w11);
+      if (gt) {
+        const float* Jc = J + (b * C + c) * HW;
+        const float j00 = __ldg(Jc + (size_t)ya * W + xa), j01 = __ldg(Jc + (size_t)ya * W + xb);
+        const float j10 = __ldg(Jc + (size_t)yb * W + xa), j11 = __ldg(Jc + (size_t)yb * W + xb);
+        dsx = fmaf(gc, (1.f - fy) * (j01 - j00) + fy * (j11 - j10), dsx);
+        dsy = fmaf(gc, (1.f - fx) * (j10 - j00) + fx * (j11 - j01), dsy);
+      }
+    }
+    if (gt) {
+      gt[(b * 2 + 0) * HW + pix] = (sxr > -1.f && sxr < (float)W) ? -dsx : 0.f;
+      gt[(b * 2 + 1) * HW + pix] = (syr > -1.f && syr < (float)H) ? -dsy : 0.f;
     }
   }
 }

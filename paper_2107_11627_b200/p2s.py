@@ -26,7 +26,8 @@ EXPORTED = ("p2s_init", "p2s_render", "p2s_render_host", "p2s_reserve", "p2s_set
             "p2s_get_info", "p2s_destroy", "p2s_status_string", "p2s_last_cuda_error",
             "p2s_debug_beta", "p2s_debug_blur", "p2s_debug_profile_buffer",
             "p2s_render_anchors", "p2s_render_anchors_host", "p2s_debug_blur_anchors",
-            "p2s_render_sequence", "p2s_sampler_init", "p2s_sample_anchors", "p2s_sampler_destroy")
+            "p2s_render_sequence", "p2s_sampler_init", "p2s_sample_anchors", "p2s_sampler_destroy",
+            "p2s_backward")
 
 
 class P2SError(RuntimeError):
@@ -97,11 +98,12 @@ def load_library(path: str = LIB_PATH) -> ctypes.CDLL:
     lib.p2s_sampler_init.argtypes = [i, i, ctypes.c_double, v, ctypes.POINTER(v)]
     lib.p2s_sample_anchors.argtypes = [v, ctypes.c_ulonglong, i, i, v, v]
     lib.p2s_sampler_destroy.argtypes = [v]
+    lib.p2s_backward.argtypes = [v, _Image, v, v, v, v, v, v]
     lib.p2s_sampler_destroy.restype = None
     for name in ("p2s_init", "p2s_render", "p2s_render_host", "p2s_reserve", "p2s_set_profile_events",
                  "p2s_get_info", "p2s_debug_beta", "p2s_debug_blur", "p2s_debug_profile_buffer",
                  "p2s_render_anchors", "p2s_render_anchors_host", "p2s_debug_blur_anchors",
-                 "p2s_render_sequence", "p2s_sampler_init", "p2s_sample_anchors"):
+                 "p2s_render_sequence", "p2s_sampler_init", "p2s_sample_anchors", "p2s_backward"):
         getattr(lib, name).restype = st
     _lib = lib
     return lib
@@ -165,6 +167,23 @@ class Renderer:
         op = _dev_ptr(out, "out", (B, C, H, W))
         _check(self._lib.p2s_render(self._h, im, zp, tp, op, _stream_handle(stream)), "p2s_render")
         return out
+
+    def backward(self, image, zernike, tilt, grad_out, want_beta=True, want_tilt=True, stream=None):
+        """p2s_backward: (dL/dbeta [B,K,H,W] | None, dL/dt [B,2,H,W] | None) of the
+        frames render(image, zernike, tilt) gives, for upstream grad_out [B,C,H,W]."""
+        import torch
+        B, C, H, W = image.shape
+        im = _Image(_dev_ptr(image, "image").value, B, C, H, W)
+        zp = _dev_ptr(zernike, "zernike_field", (B, self.n_in, H, W))
+        tp = _dev_ptr(tilt, "tilt_field", (B, 2, H, W)) if tilt is not None else ctypes.c_void_p()
+        gp = _dev_ptr(grad_out, "grad_out", (B, C, H, W))
+        gb = torch.empty((B, self.K, H, W), device=image.device, dtype=torch.float32) if want_beta else None
+        gt = torch.empty((B, 2, H, W), device=image.device, dtype=torch.float32) if want_tilt else None
+        _check(self._lib.p2s_backward(self._h, im, zp, tp, gp,
+                                      _dev_ptr(gb, "grad_beta") if gb is not None else ctypes.c_void_p(),
+                                      _dev_ptr(gt, "grad_tilt") if gt is not None else ctypes.c_void_p(),
+                                      _stream_handle(stream)), "p2s_backward")
+        return gb, gt
 
     def debug_beta(self, zernike, out=None, stream=None):
         import torch

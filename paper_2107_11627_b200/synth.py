@@ -29,7 +29,7 @@ from typing import Optional
 
 import numpy as np
 
-STREAM_IMAGE, STREAM_ZERNIKE, STREAM_TILT, STREAM_BASIS, STREAM_MLP, STREAM_RECT, STREAM_ANCHORS = range(7)
+STREAM_IMAGE, STREAM_ZERNIKE, STREAM_TILT, STREAM_BASIS, STREAM_MLP, STREAM_RECT, STREAM_ANCHORS, STREAM_GRAD = range(8)
 
 
 @dataclass(frozen=True)
@@ -141,6 +141,14 @@ def make_anchors(spec: Spec, G: int, frames: Optional[range] = None) -> np.ndarr
     frames = range(spec.B) if frames is None else frames
     return np.stack([smooth_field(_rng(spec.cfg_id, f, STREAM_ANCHORS), spec.n_in, G, G, 1.0, spec.z_std)
                      for f in frames])
+
+
+def make_upstream_grad(spec: Spec, frames: Optional[range] = None) -> np.ndarray:
+    """dL/dout [B][C][H][W] fp32 for the adjoint: i.i.d. U(-1, 1), the gradient of
+    a loss on the rendered frames (no structure assumed)."""
+    frames = range(spec.B) if frames is None else frames
+    return np.stack([_rng(spec.cfg_id, f, STREAM_GRAD).uniform(-1.0, 1.0, (spec.C, spec.H, spec.W))
+                     for f in frames]).astype(np.float32)
 
 
 def make_tilt(spec: Spec, frame: int) -> np.ndarray:

@@ -452,3 +452,90 @@ def test_sampled_anchors_render_end_to_end(p2s):
     dense = oracle.interp_anchors(a_ref, H, W).astype(np.float32)
     ref, _ = oracle.render(inp.image, dense, inp.tilt, inp.basis, inp.mlp)
     _cmp(out, ref, "render[sampled anchors G=6]")
+
+
+# ---- adjoint of steps a2-a3 vs oracle/adjoint.py (pinned by finite
+#      differences). beta for the oracle comes from oracle.beta (never from the GPU).
+#      Tolerances: dL/dbeta = sum_c dL/dJ_c C_kc has the forward blur's arithmetic (fp16 operands,
+#      fp32 accumulation) -> the render bar relative to its scale: max abs <= 2e-3 max|ref|,
+#      rel L2 <= 1e-3. dL/dt differences J at the warp corners: with |J_gpu - J| <= e = 2e-3 (the
+#      forward bar) each channel's d out/d s errs by <= 2e, so max abs <= 2 e C max|g|.
+#      The bilinear cell (an integer decided by s = p - t) is taken in fp32 on both sides (reading N4).
+
+ADJ_CASES = ["ragged_rgb_S7", "S33_K100_C2", "many_tiles_C2", "S1_K1", "W1_H1", "S65_K100_h256",
+             "many_tiles_C1_S9"]
+
+
+def _adj_ref(inp, g, with_tilt):
+    from oracle import adjoint
+    beta = oracle.beta(inp.image, inp.zernike, inp.basis, inp.mlp)
+    gb, gt = [], []
+    for b in range(inp.image.shape[0]):
+        t = inp.tilt[b] if with_tilt else np.zeros_like(inp.tilt[b])
+        _, gbb, gtb = adjoint.backward(inp.image[b], beta[b], t, inp.basis, g[b], coord_dtype=np.float32)
+        gb.append(gbb)
+        gt.append(gtb)
+    return np.stack(gb), np.stack(gt)
+
+
+@pytest.mark.parametrize("with_tilt", [True, False])
+@pytest.mark.parametrize("name", ADJ_CASES)
+def test_backward_parity(p2s, name, with_tilt):
+    spec = SMALL[name]
+    inp = synth.make_inputs(spec)
+    g = synth.make_upstream_grad(spec)
+    r = p2s.Renderer(inp.basis, inp.mlp)
+    gb, gt = r.backward(_dev(inp.image), _dev(inp.zernike), _dev(inp.tilt) if with_tilt else None, _dev(g))
+    gb, gt = gb.cpu().numpy(), gt.cpu().numpy()
+    rb, rt = _adj_ref(inp, g, with_tilt)
+    _cmp(gb, rb, f"dL/dbeta[{name}]", max_abs=2e-3 * np.abs(rb).max())
+    C = inp.image.shape[1]
+    err = np.abs(gt - rt).max()
+    print(f"dL/dt[{name}]: max_abs={err:.3e} (ref max {np.abs(rt).max():.3f})")
+    assert err <= 2 * 2e-3 * C * np.abs(g).max()
+    # either output alone == the same output of the joint call (dL/dJ scatter order aside)
+    gb1, none_t = r.backward(_dev(inp.image), _dev(inp.zernike), _dev(inp.tilt) if with_tilt else None, _dev(g),
+                             want_tilt=False)
+    none_b, gt1 = r.backward(_dev(inp.image), _dev(inp.zernike), _dev(inp.tilt) if with_tilt else None, _dev(g),
+                             want_beta=False)
+    assert none_t is None and none_b is None
+    np.testing.assert_allclose(gb1.cpu().numpy(), gb, rtol=1e-5, atol=1e-5 * np.abs(rb).max())
+    np.testing.assert_allclose(gt1.cpu().numpy(), gt, rtol=0, atol=1e-6 * (1 + np.abs(rt).max()))
+    r.close()
+
+
+def test_backward_cfg3_sampled(p2s):
+    """Bench-size frames (512x512 RGB, K=100, 33x33), sampled pixels (seams and borders included)."""
+    from oracle import adjoint
+    spec = synth.CONFIGS[3]
+    inp = synth.make_inputs(spec)
+    g = synth.make_upstream_grad(spec)
+    r = p2s.Renderer(inp.basis, inp.mlp)
+    gb, gt = r.backward(_dev(inp.image), _dev(inp.zernike), _dev(inp.tilt), _dev(g))
+    gb, gt = gb.cpu().numpy(), gt.cpu().numpy()
+    B, C, H, W = inp.image.shape
+    rng = np.random.default_rng(11)
+    yx = [(0, 0), (H - 1, W - 1), (0, W - 1), (H // 2, 127), (H // 2, 128), (H - 1, 0)]
+    yx += [(int(y), int(x)) for y, x in zip(rng.integers(0, H, 60), rng.integers(0, W, 60))]
+    beta = oracle.beta(inp.image[:1], inp.zernike[:1], inp.basis, inp.mlp)[0]
+    rb, rt = adjoint.backward_at(inp.image[0], beta, inp.tilt[0], inp.basis, g[0], yx, coord_dtype=np.float32)
+    ys, xs = np.array(yx).T
+    _cmp(gb[0][:, ys, xs].T, rb, "dL/dbeta[cfg3 sampled]", max_abs=2e-3 * np.abs(rb).max())
+    err = np.abs(gt[0][:, ys, xs].T - rt).max()
+    print(f"dL/dt[cfg3 sampled]: max_abs={err:.3e} (ref max {np.abs(rt).max():.3f})")
+    assert err <= 2 * 2e-3 * C * np.abs(g).max()
+
+
+def test_backward_invalid_args(p2s):
+    spec = SMALL["ragged_rgb_S7"]
+    inp = synth.make_inputs(spec)
+    r = p2s.Renderer(inp.basis, inp.mlp)
+    img, z, g = _dev(inp.image), _dev(inp.zernike), _dev(synth.make_upstream_grad(spec))
+    B, C, H, W = inp.image.shape
+    im = p2s._Image(img.data_ptr(), B, C, H, W)
+    buf = _dev(np.zeros((B, spec.K, H, W), np.float32))
+    vp = ctypes.c_void_p
+    for args in ((vp(z.data_ptr()), vp(), vp(g.data_ptr()), vp(), vp()),              # no output
+                 (vp(), vp(), vp(g.data_ptr()), vp(buf.data_ptr()), vp()),             # no zernike
+                 (vp(z.data_ptr()), vp(), vp(), vp(buf.data_ptr()), vp())):            # no grad_out
+        assert r._lib.p2s_backward(r._h, im, *args, vp()) == p2s.P2S_ERR_INVALID_ARG

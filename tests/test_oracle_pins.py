@@ -456,3 +456,56 @@ def test_adjoint_forward_matches_render_oracle():
     ref, Jref = oracle.render(inp.image, inp.zernike, inp.tilt, inp.basis, inp.mlp, want_blur=True)
     np.testing.assert_allclose(J, Jref[0], rtol=0, atol=1e-12)
     np.testing.assert_allclose(out, ref[0], rtol=0, atol=1e-12)
+
+
+def test_adjoint_conv_at_brute_force():
+    """conv_at (the sampled-pixel form the full-size GPU test uses) == the convolution written as
+    four nested loops over the definition, and == conv_all at the same pixels."""
+    from oracle import adjoint
+    rng = np.random.default_rng(6)
+    C, H, W, K, S = 2, 6, 8, 3, 5
+    image, basis = rng.random((C, H, W)), rng.standard_normal((K, S, S))
+    r = S // 2
+    yx = [(0, 0), (H - 1, W - 1), (2, 3), (5, 0), (0, 7)]
+    got = adjoint.conv_at(image, basis, yx)
+    full = adjoint.conv_all(image, basis)
+    for n, (y, x) in enumerate(yx):
+        for k in range(K):
+            for c in range(C):
+                ref = 0.0
+                for i in range(S):
+                    for j in range(S):
+                        yy = min(max(y - (i - r), 0), H - 1)
+                        xx = min(max(x - (j - r), 0), W - 1)
+                        ref += basis[k, i, j] * image[c, yy, xx]
+                assert abs(got[n, k, c] - ref) < 1e-12
+                assert abs(full[k, c, y, x] - ref) < 1e-12
+
+
+def test_adjoint_backward_at_matches_backward():
+    """The sampled-pixel form agrees with the whole-frame backward (pinned above by finite
+    differences), clamp-active pixels included."""
+    from oracle import adjoint
+    image, basis, beta, tilt, g = _adj_problem(7, H=9, W=11, t_std=2.5)
+    _, gbeta, gt = adjoint.backward(image, beta, tilt, basis, g)
+    yx = [(y, x) for y in range(9) for x in range(11)]
+    gb_at, gt_at = adjoint.backward_at(image, beta, tilt, basis, g, yx)
+    ys, xs = np.array(yx).T
+    np.testing.assert_allclose(gb_at, gbeta[:, ys, xs].T, rtol=0, atol=1e-11)
+    np.testing.assert_allclose(gt_at, gt[:, ys, xs].T, rtol=0, atol=1e-11)
+
+
+def test_adjoint_fp32_cells_agree_away_from_cell_edges():
+    """coord_dtype=float32 only moves the cell decision: where fp64 and fp32 s = p - t pick the
+    same cell, dL/dt and dL/dJ agree to fp32 rounding of s."""
+    from oracle import adjoint
+    image, basis, beta, tilt, g = _adj_problem(8, H=9, W=11, t_std=2.5)
+    tilt = tilt.astype(np.float32)
+    gJ64, gb64, gt64 = adjoint.backward(image, beta, tilt, basis, g)
+    gJ32, gb32, gt32 = adjoint.backward(image, beta, tilt, basis, g, coord_dtype=np.float32)
+    c64 = adjoint._warp_coords(tilt, 9, 11)
+    c32 = adjoint._warp_coords(tilt, 9, 11, np.float32)
+    same = np.all([np.array_equal(a, b) for a, b in zip(c64[:4], c32[:4])])
+    assert same  # no fp32/fp64 cell flips on this problem: the two forms must then agree
+    np.testing.assert_allclose(gt32, gt64, rtol=0, atol=1e-5 * (1 + np.abs(gt64).max()))
+    np.testing.assert_allclose(gJ32, gJ64, rtol=0, atol=1e-5 * (1 + np.abs(gJ64).max()))
