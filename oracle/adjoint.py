@@ -11,6 +11,7 @@ and an upstream gradient g = dL/dout, the adjoint quantities are
 
     dL/dJ_c(q)    = sum_p g_c(p) w_q(p)       (w_q(p): the bilinear weight out_c(p) gives J_c(q))
     dL/dbeta_k(p) = sum_c dL/dJ_c(p) C_kc(p)
+    dL/dI_c(q)    = sum_{p,k,i,j: cY(p_y-(i-r)) = q_y, cX(p_x-(j-r)) = q_x} phi_k[i][j] beta_k(p) dL/dJ_c(p)
     dL/dt_x(p)    = -sum_c g_c(p) d bilinear / d sx, likewise y (0 where the coordinate clamp is
                     active; the derivative of the bilinear weights inside the cell)
 
@@ -100,21 +101,74 @@ def grad_J(tilt, g, coord_dtype=np.float64):
     return gJ
 
 
+def grad_image(beta, basis, gJ):
+    """dL/dI [C][H][W]: the transpose of step a2 (the beta-weighted convolution, scatter order):
+    every term phi_k[i][j] I[cY(y-(i-r))][cX(x-(j-r))] of J_c(y,x) sends
+    phi_k[i][j] beta_k(y,x) dL/dJ_c(y,x) back to the (clamped) pixel it read."""
+    C_, H, W = gJ.shape
+    K, S, _ = basis.shape
+    r = (S - 1) // 2
+    out = np.zeros((C_, H, W))
+    ys, xs = np.arange(H), np.arange(W)
+    for i in range(S):
+        yy = _clamp(ys - (i - r), 0, H - 1)
+        for j in range(S):
+            xx = _clamp(xs - (j - r), 0, W - 1)
+            v = np.einsum("k,khw->hw", basis[:, i, j].astype(np.float64), beta.astype(np.float64))
+            for c in range(C_):
+                np.add.at(out[c], (yy[:, None], xx[None, :]), v * gJ[c])
+    return out
+
+
+def _preimage(q, d, n):
+    """{p in [0, n) : clamp(p - d, 0, n - 1) == q}: the pixels whose tap at offset d read q."""
+    if q == 0:
+        return np.arange(0, max(0, min(n - 1, d) + 1))
+    if q == n - 1:
+        return np.arange(min(n, max(0, n - 1 + d)), n)
+    p = q + d
+    return np.array([p]) if 0 <= p < n else np.arange(0)
+
+
+def grad_image_at(beta, basis, gJ, yx):
+    """grad_image at the listed pixels only: [n][C] (fp64), by the same definition (each tap's
+    preimage under the clamp is a rectangle of output pixels)."""
+    C_, H, W = gJ.shape
+    K, S, _ = basis.shape
+    r = (S - 1) // 2
+    out = np.zeros((len(yx), C_))
+    for n, (y, x) in enumerate(yx):
+        for i in range(S):
+            rows = _preimage(y, i - r, H)
+            if rows.size == 0:
+                continue
+            for j in range(S):
+                cols = _preimage(x, j - r, W)
+                if cols.size == 0:
+                    continue
+                bsum = beta[:, rows][:, :, cols].astype(np.float64)          # [K][h][w]
+                gsum = gJ[:, rows][:, :, cols].astype(np.float64)            # [C][h][w]
+                out[n] += np.einsum("k,khw,chw->c", basis[:, i, j].astype(np.float64), bsum, gsum)
+    return out
+
+
 def backward(image, beta, tilt, basis, g, coord_dtype=np.float64):
-    """(dL/dJ [C][H][W], dL/dbeta [K][H][W], dL/dt [2][H][W]) for upstream g [C][H][W]."""
+    """(dL/dJ [C][H][W], dL/dbeta [K][H][W], dL/dt [2][H][W], dL/dI [C][H][W]) for upstream
+    g [C][H][W]."""
     _, J, Ck = forward_from_beta(image, beta, tilt, basis)
     C_, H, W = J.shape
     g = g.astype(np.float64)
     ya, yb, xa, xb, fy, fx, in_y, in_x = _warp_coords(tilt, H, W, coord_dtype)
     gJ = grad_J(tilt, g, coord_dtype)
     gbeta = np.einsum("chw,kchw->khw", gJ, Ck)
+    gimage = grad_image(beta, basis, gJ)
     # d out / d sx = (1-fy)(J[ya][xb] - J[ya][xa]) + fy (J[yb][xb] - J[yb][xa]); sx = x - t_x
     dsx = (1 - fy) * (J[:, ya, xb] - J[:, ya, xa]) + fy * (J[:, yb, xb] - J[:, yb, xa])
     dsy = (1 - fx) * (J[:, yb, xa] - J[:, ya, xa]) + fx * (J[:, yb, xb] - J[:, ya, xb])
     gt = np.zeros((2, H, W))
     gt[0] = -np.where(in_x, (g * dsx).sum(0), 0.0)
     gt[1] = -np.where(in_y, (g * dsy).sum(0), 0.0)
-    return gJ, gbeta, gt
+    return gJ, gbeta, gt, gimage
 
 
 def backward_at(image, beta, tilt, basis, g, yx, coord_dtype=np.float64):

@@ -472,7 +472,7 @@ def _adj_ref(inp, g, with_tilt):
     gb, gt = [], []
     for b in range(inp.image.shape[0]):
         t = inp.tilt[b] if with_tilt else np.zeros_like(inp.tilt[b])
-        _, gbb, gtb = adjoint.backward(inp.image[b], beta[b], t, inp.basis, g[b], coord_dtype=np.float32)
+        _, gbb, gtb, _ = adjoint.backward(inp.image[b], beta[b], t, inp.basis, g[b], coord_dtype=np.float32)
         gb.append(gbb)
         gt.append(gtb)
     return np.stack(gb), np.stack(gt)

@@ -412,7 +412,7 @@ def _adj_problem(seed=0, C=2, H=5, W=7, K=3, S=3, t_std=0.8):
 def test_adjoint_beta_matches_finite_differences():
     from oracle import adjoint
     image, basis, beta, tilt, g = _adj_problem(1)
-    _, gbeta, _ = adjoint.backward(image, beta, tilt, basis, g)
+    _, gbeta, _, _ = adjoint.backward(image, beta, tilt, basis, g)
     rng = np.random.default_rng(2)
     for _ in range(12):
         k, y, x = rng.integers(0, beta.shape[0]), rng.integers(0, beta.shape[1]), rng.integers(0, beta.shape[2])
@@ -426,7 +426,7 @@ def test_adjoint_beta_matches_finite_differences():
 def test_adjoint_tilt_matches_finite_differences():
     from oracle import adjoint
     image, basis, beta, tilt, g = _adj_problem(3, t_std=1.3)
-    _, _, gt = adjoint.backward(image, beta, tilt, basis, g)
+    _, _, gt, _ = adjoint.backward(image, beta, tilt, basis, g)
     rng = np.random.default_rng(4)
     for _ in range(16):
         ch, y, x = rng.integers(0, 2), rng.integers(0, tilt.shape[1]), rng.integers(0, tilt.shape[2])
@@ -442,7 +442,7 @@ def test_adjoint_warp_dot_product_identity():
     from oracle import adjoint
     image, basis, beta, tilt, g = _adj_problem(5, H=9, W=11, t_std=2.5)  # tilts reach the clamp
     out, J, _ = adjoint.forward_from_beta(image, beta, tilt, basis)
-    gJ, _, _ = adjoint.backward(image, beta, tilt, basis, g)
+    gJ, _, _, _ = adjoint.backward(image, beta, tilt, basis, g)
     assert abs(np.sum(g * out) - np.sum(gJ * J)) < 1e-10 * np.sum(np.abs(g * out))
 
 
@@ -487,7 +487,7 @@ def test_adjoint_backward_at_matches_backward():
     differences), clamp-active pixels included."""
     from oracle import adjoint
     image, basis, beta, tilt, g = _adj_problem(7, H=9, W=11, t_std=2.5)
-    _, gbeta, gt = adjoint.backward(image, beta, tilt, basis, g)
+    _, gbeta, gt, _ = adjoint.backward(image, beta, tilt, basis, g)
     yx = [(y, x) for y in range(9) for x in range(11)]
     gb_at, gt_at = adjoint.backward_at(image, beta, tilt, basis, g, yx)
     ys, xs = np.array(yx).T
@@ -501,11 +501,44 @@ def test_adjoint_fp32_cells_agree_away_from_cell_edges():
     from oracle import adjoint
     image, basis, beta, tilt, g = _adj_problem(8, H=9, W=11, t_std=2.5)
     tilt = tilt.astype(np.float32)
-    gJ64, gb64, gt64 = adjoint.backward(image, beta, tilt, basis, g)
-    gJ32, gb32, gt32 = adjoint.backward(image, beta, tilt, basis, g, coord_dtype=np.float32)
+    gJ64, gb64, gt64, _ = adjoint.backward(image, beta, tilt, basis, g)
+    gJ32, gb32, gt32, _ = adjoint.backward(image, beta, tilt, basis, g, coord_dtype=np.float32)
     c64 = adjoint._warp_coords(tilt, 9, 11)
     c32 = adjoint._warp_coords(tilt, 9, 11, np.float32)
     same = np.all([np.array_equal(a, b) for a, b in zip(c64[:4], c32[:4])])
     assert same  # no fp32/fp64 cell flips on this problem: the two forms must then agree
     np.testing.assert_allclose(gt32, gt64, rtol=0, atol=1e-5 * (1 + np.abs(gt64).max()))
     np.testing.assert_allclose(gJ32, gJ64, rtol=0, atol=1e-5 * (1 + np.abs(gJ64).max()))
+
+
+
+def test_adjoint_image_matches_finite_differences():
+    """dL/dI by central differences of the forward (J is linear in I: differences are exact up to
+    rounding), borders and corners included (S = 5 on a 5x7 frame: every pixel is near one)."""
+    from oracle import adjoint
+    image, basis, beta, tilt, g = _adj_problem(9, K=3, S=5)
+    *_, gI = adjoint.backward(image, beta, tilt, basis, g)
+    C, H, W = image.shape
+    for c in range(C):
+        for y in range(H):
+            for x in range(W):
+                e = np.zeros_like(image)
+                e[c, y, x] = 1e-3
+                lp = np.sum(g * adjoint.forward_from_beta(image + e, beta, tilt, basis)[0])
+                lm = np.sum(g * adjoint.forward_from_beta(image - e, beta, tilt, basis)[0])
+                assert abs((lp - lm) / 2e-3 - gI[c, y, x]) < 1e-9 * (1 + abs(gI[c, y, x]))
+
+
+def test_adjoint_image_dot_product_and_sampled_form():
+    """<dL/dJ, J(I)> = <dL/dI, I> (J is linear in I), and grad_image_at (per-pixel preimage
+    rectangles, the full-size GPU test's form) == grad_image at every pixel, S > frame included."""
+    from oracle import adjoint
+    for seed, H, W, S in ((10, 9, 11, 5), (11, 6, 4, 9)):
+        image, basis, beta, tilt, g = _adj_problem(seed, H=H, W=W, K=4, S=S)
+        gJ, _, _, gI = adjoint.backward(image, beta, tilt, basis, g)
+        _, J, _ = adjoint.forward_from_beta(image, beta, tilt, basis)
+        assert abs(np.sum(gJ * J) - np.sum(gI * image)) < 1e-10 * np.sum(np.abs(gJ * J))
+        yx = [(y, x) for y in range(H) for x in range(W)]
+        at = adjoint.grad_image_at(beta, basis, gJ, yx)
+        ys, xs = np.array(yx).T
+        np.testing.assert_allclose(at, gI[:, ys, xs].T, rtol=0, atol=1e-11)
