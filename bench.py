@@ -340,9 +340,10 @@ def main():
         aimg, az, at = (torch.from_numpy(a).to(dev) for a in (ainp.image, ainp.zernike, ainp.tilt))
         ag = torch.from_numpy(synth.make_upstream_grad(spec, frames=pdist.rank_frames(rank, 1))).to(dev)
         res = {}
-        for key, wb, wt in (("value", True, True), ("beta_only", True, False)):
+        for key, wb, wt, wi in (("value", True, True, False), ("beta_only", True, False, False),
+                                ("image_only", False, False, True), ("all", True, True, True)):
             for _ in range(3):
-                r.backward(aimg, az, at, ag, want_beta=wb, want_tilt=wt)
+                r.backward(aimg, az, at, ag, want_beta=wb, want_tilt=wt, want_image=wi)
             n_a = max(5, min(args.steps // 4, 50))
             a0 = [torch.cuda.Event(enable_timing=True) for _ in range(n_a)]
             a1 = [torch.cuda.Event(enable_timing=True) for _ in range(n_a)]
@@ -350,15 +351,17 @@ def main():
             for i in range(n_a):
                 flush.fill_(float(i))
                 a0[i].record(stream)
-                r.backward(aimg, az, at, ag, want_beta=wb, want_tilt=wt)
+                r.backward(aimg, az, at, ag, want_beta=wb, want_tilt=wt, want_image=wi)
                 a1[i].record(stream)
             torch.cuda.synchronize()
             a_ms = pdist.max_over_ranks(float(sum(a0[i].elapsed_time(a1[i]) for i in range(n_a))), dist, dev)
             res[key] = pdist.throughput(1, world, n_a, a_ms)
         adjoint_mode = {"value": res["value"], "unit": "frames/s", "beta_only": res["beta_only"],
-                        "api": "p2s_backward",
-                        "note": "dL/dbeta [K,H,W] + dL/dt [2,H,W] of one cfg3 frame (L2 flushed per call); "
-                                "includes the forward recompute needed for dL/dt; beta_only skips it"}
+                        "image_only": res["image_only"], "all": res["all"], "api": "p2s_backward",
+                        "note": "value: dL/dbeta [K,H,W] + dL/dt [2,H,W] of one cfg3 frame (L2 flushed per "
+                                "call), including the forward recompute dL/dt needs; beta_only skips it; "
+                                "image_only: dL/dI [C,H,W] (MLP pass for beta, U prep, k_adjoint_image); "
+                                "all: the three gradients"}
         del aimg, az, at, ag
 
     # ---- anchor-grid mode: the same frame with its Zernike coefficients

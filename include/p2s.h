@@ -134,14 +134,19 @@ P2S_API p2s_status p2s_render_sequence(p2s_handle* h, p2s_image image, const flo
  *   grad_beta (DEVICE [B][K][H][W] or NULL) = dL/dbeta_k(p) = sum_c dL/dJ_c(p) C_kc(p)
  *   grad_tilt (DEVICE [B][2][H][W] or NULL) = dL/dt(p) through the bilinear warp (0 where the
  *     coordinate clamp is active)
+ *   grad_image (DEVICE [B][C][H][W] or NULL) = dL/dI_c(q) = sum over the taps that read q (after
+ *     the replicate clamp) of phi_k[i][j] beta_k(p) dL/dJ_c(p): the transpose of Eq. 5's
+ *     beta-weighted convolution ("scatter order"), on the tensor cores with U = beta dL/dJ
+ *     rounded to fp16 (|beta dL/dJ| must stay below 65504)
  * where dL/dJ scatters grad_out through the warp's bilinear weights (float atomics: the
- * summation order, hence the last bits, vary run to run). The image gradient (a scatter-order
- * transpose convolution) is not provided yet. grad_beta recomputes the K convolutions on the
- * tensor cores; grad_tilt also recomputes J (one forward). Errors as p2s_render; both outputs
- * NULL -> P2S_ERR_INVALID_ARG. */
+ * summation order, hence the last bits, vary run to run; grad_image's border pixels likewise).
+ * grad_beta recomputes the K convolutions on the tensor cores; grad_tilt also recomputes J (one
+ * forward); grad_image recomputes beta (one MLP pass) and needs workspace for beta [B][K][H][W]
+ * fp32 and U [B][C][K][W][ceil8(H)] fp16 (grown on first use: synchronising, like p2s_render's).
+ * Errors as p2s_render; all three outputs NULL -> P2S_ERR_INVALID_ARG. */
 P2S_API p2s_status p2s_backward(p2s_handle* h, p2s_image image, const float* zernike_field,
                                 const float* tilt_field, const float* grad_out, float* grad_beta,
-                                float* grad_tilt, p2s_stream_t stream);
+                                float* grad_tilt, float* grad_image, p2s_stream_t stream);
 
 /* ---- correlated anchor sampling (Sec. 3.4: anchor
  * coefficient sets "drawn from the correlation matrix", which "can be pre-computed") ----

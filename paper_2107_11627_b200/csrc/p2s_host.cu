@@ -15,6 +15,7 @@
 
 #include "p2s.h"
 #include "p2s_kernels.cuh"
+#include "p2s_adjoint.cuh"
 
 using namespace p2s;
 
@@ -117,6 +118,13 @@ struct p2s_handle {
   int n_items_full = 0, n_items_beta = 0, n_items_first = 0, n_items_seq = 0, n_items_conv = 0, tab_cap = 0;
   float* d_gJ = nullptr;  // adjoint workspace dL/dJ
   size_t gJ_cap = 0;
+  // dL/dI (k_adjoint_image): plan, phi table, workspaces beta [B][K][H][W] fp32 and U_T fp16
+  int di_R = 0, di_nchunk = 0, di_kg = 0, di_ngroups = 0, di_Nh = 0, di_OW = 0, di_nring = 0, di_smem = 0;
+  int di_a_bytes = 0, di_b_bytes = 0, di_off_p = 0, di_off_bar = 0;
+  uint8_t* d_dib = nullptr;
+  __half* d_ut = nullptr;
+  size_t ut_cap = 0;
+  PFN_cuTensorMapEncodeTiled encode = nullptr;
   MlpOp ops[kMaxOps];  // [0, n_ops) per-tile ops, then n_fops first-tile whole-layer ops
   int n_ops = 0, n_fops = 0;
   bool bias_folded = false;
@@ -222,7 +230,8 @@ p2s_status launch_fused(p2s_handle* h, const FusedParams& p, cudaStream_t st) {
   // persistent grid of CTA pairs (clusters of 2): at most one CTA per SM
   const int npairs = (p.ntiles + 1) / 2;
   const int grid = 2 * std::max(1, std::min(h->sm_count / 2, npairs));
-  if (p.mode == 2) k_fused_p2s<false, true><<<grid, kThreads, h->smem_bytes, st>>>(p);
+  if (p.mode == 2) k_fused_p2s<false, 1><<<grid, kThreads, h->smem_bytes, st>>>(p);
+  else if (p.mode == 3) k_fused_p2s<false, 2><<<grid, kThreads, h->smem_bytes, st>>>(p);
   else if (p.anchors) k_fused_p2s<true><<<grid, kThreads, h->smem_bytes, st>>>(p);
   else k_fused_p2s<false><<<grid, kThreads, h->smem_bytes, st>>>(p);
   P2S_CUDA(cudaPeekAtLastError());
@@ -641,6 +650,7 @@ p2s_status p2s_init(const p2s_basis* basis, const p2s_mlp* mlp, p2s_handle** out
         q != cudaDriverEntryPointSuccess || !fn)
       return fail(cuda_fail(e != cudaSuccess ? e : cudaErrorUnknown, "cuTensorMapEncodeTiled entry point"));
     auto encode = reinterpret_cast<PFN_cuTensorMapEncodeTiled>(fn);
+    h->encode = encode;
     std::memset(h->maps, 0, sizeof(h->maps));
     for (size_t i = 0; i < map_rows.size(); ++i) {
       // the stream viewed as uint8 [total/256][256]; one box = one half slab
@@ -667,9 +677,65 @@ p2s_status p2s_init(const p2s_basis* basis, const p2s_mlp* mlp, p2s_handle** out
           cudaSuccess ||
       (e = cudaFuncSetAttribute(k_fused_p2s<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, kSmemLimit)) !=
           cudaSuccess ||
-      (e = cudaFuncSetAttribute(k_fused_p2s<false, true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+      (e = cudaFuncSetAttribute(k_fused_p2s<false, 1>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                kSmemLimit)) != cudaSuccess ||
+      (e = cudaFuncSetAttribute(k_fused_p2s<false, 2>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                 kSmemLimit)) != cudaSuccess)
     return fail(cuda_fail(e, "cudaFuncSetAttribute"));
+  {
+    // ---- dL/dI plan (p2s_adjoint.cuh): R output rows per band, WR8 8-row U chunks per basis
+    // function, N = R x S in two halves of Nh columns; k-groups of kg functions make every stage
+    // an even number of chunks (UMMA K = 16 = two chunks), else the window is padded by a chunk
+    // R = 8 rows per band when N = 4 S fits one UMMA and >= 2 ring stages fit, else R = 4
+    int R = 0, hr = 0, Nh = 0, wr8 = 0, kg = 1, nchunk = 0, wpad = 0, stage = 0, nring = 0;
+    const int sp_bytes = S * 128 * 4, bar_bytes = 256;
+    const int avail = kSmemLimit - sp_bytes - bar_bytes;
+    for (int Rt : {8, 4}) {
+      R = Rt; hr = R / 2;
+      Nh = (hr * S + 15) / 16 * 16;
+      if (Nh > 256) continue;
+      wr8 = (S + R - 1 + 7) / 8;  // window rows s + i < R + S - 1
+      auto stage_of = [&](int nch) { return nch * 2048 + 2 * nch * Nh * 16; };
+      kg = 1; nchunk = wr8; wpad = wr8;
+      if (wr8 % 2) {
+        if (3 * stage_of(2 * wr8) <= avail) { kg = 2; nchunk = 2 * wr8; }
+        else { wpad = wr8 + 1; nchunk = wpad; }
+      }
+      stage = stage_of(nchunk);
+      nring = std::min(6, avail / stage);
+      if (nring >= 2) break;
+    }
+    if (nring < 2) return fail(P2S_ERR_UNSUPPORTED);  // not reached for S <= 65
+    h->di_R = R; h->di_Nh = Nh; h->di_kg = kg; h->di_nchunk = nchunk; h->di_nring = nring;
+    h->di_ngroups = (K + kg - 1) / kg;
+    h->di_OW = (128 - (S - 1)) / 8 * 8;  // strips start at multiples of 8 columns (TMA x/8 view)
+    h->di_a_bytes = nchunk * 2048;
+    h->di_b_bytes = 2 * nchunk * Nh * 16;
+    h->di_off_p = nring * stage;
+    h->di_off_bar = h->di_off_p + sp_bytes;
+    // >= 120 KB so that one CTA (and one 512-column TMEM allocation) occupies an SM
+    h->di_smem = std::max(h->di_off_bar + bar_bytes, 120 * 1024);
+    const int cpk = nchunk / kg;  // chunks per basis function (wr8, or wr8 + 1 when padded)
+    std::vector<__half> tab((size_t)h->di_ngroups * h->di_b_bytes / 2, __float2half(0.f));
+    for (int g = 0; g < h->di_ngroups; ++g)
+      for (int hf = 0; hf < 2; ++hf)
+        for (int c = 0; c < nchunk; ++c)
+          for (int n = 0; n < Nh; ++n)
+            for (int e8 = 0; e8 < 8; ++e8) {
+              const int kl = c / cpk, w = (c - kl * cpk) * 8 + e8, k = g * kg + kl;
+              const int sr = hf * hr + n / S, j = n % S, i = w - sr;
+              if (n >= hr * S || k >= K || i < 0 || i >= S) continue;
+              const size_t at = ((((size_t)g * 2 + hf) * nchunk + c) * Nh + n) * 8 + e8;
+              tab[at] = __float2half_rn(basis->taps[((size_t)k * S + i) * S + j]);
+            }
+    if ((e = cudaMalloc(&h->d_dib, tab.size() * sizeof(__half))) != cudaSuccess ||
+        (e = cudaMemcpy(h->d_dib, tab.data(), tab.size() * sizeof(__half), cudaMemcpyHostToDevice)) != cudaSuccess)
+      return fail(cuda_fail(e, "dI table"));
+    if ((e = cudaFuncSetAttribute(k_adjoint_image, cudaFuncAttributeMaxDynamicSharedMemorySize, h->di_smem)) !=
+        cudaSuccess)
+      return fail(cuda_fail(e, "cudaFuncSetAttribute(k_adjoint_image)"));
+    (void)wpad;
+  }
   *out_handle = h;
   return P2S_OK;
 }
@@ -753,10 +819,11 @@ p2s_status p2s_render_sequence(p2s_handle* h, p2s_image im, const float* zernike
 }
 
 p2s_status p2s_backward(p2s_handle* h, p2s_image im, const float* zernike_field, const float* tilt_field,
-                        const float* grad_out, float* grad_beta, float* grad_tilt, p2s_stream_t stream) {
+                        const float* grad_out, float* grad_beta, float* grad_tilt, float* grad_image,
+                        p2s_stream_t stream) {
   p2s_status s = check_image(h, im);
   if (s != P2S_OK) return s;
-  if (!zernike_field || !grad_out || (!grad_beta && !grad_tilt)) return P2S_ERR_INVALID_ARG;
+  if (!zernike_field || !grad_out || (!grad_beta && !grad_tilt && !grad_image)) return P2S_ERR_INVALID_ARG;
   cudaStream_t st = (cudaStream_t)stream;
   const size_t HW = (size_t)im.H * im.W, chw = (size_t)im.B * im.C * HW;
   s = ensure_J(h, chw);
@@ -782,13 +849,60 @@ p2s_status p2s_backward(p2s_handle* h, p2s_image im, const float* zernike_field,
   const int grid = (int)std::min<size_t>((npx + 255) / 256, (size_t)h->sm_count * 16);
   k_warp_backward<<<grid, 256, 0, st>>>(h->d_J, tilt_field, grad_out, h->d_gJ, grad_tilt, im.B, im.C, im.H, im.W);
   P2S_CUDA(cudaPeekAtLastError());
-  if (grad_beta) {  // dL/dbeta_k = sum_c dL/dJ_c C_kc: the K convolutions again, another epilogue
-    FusedParams p = make_params(h, im.B, im.C, im.H, im.W, 2);
+  const int Ws = (im.W + 7) / 8 * 8;
+  if (grad_image) {
+    const size_t nu = (size_t)im.B * im.C * h->K * im.H * Ws;
+    if (nu > h->ut_cap) {
+      P2S_CUDA(cudaDeviceSynchronize());
+      cudaFree(h->d_ut);
+      h->d_ut = nullptr;
+      h->ut_cap = 0;
+      P2S_CUDA(cudaMalloc(&h->d_ut, nu * sizeof(__half)));
+      h->ut_cap = nu;
+    }
+  }
+  if (grad_beta || grad_image) {
+    // dL/dbeta_k = sum_c dL/dJ_c C_kc (the K convolutions again, another epilogue); with dL/dI the
+    // render flow (MLP + convolutions) whose epilogue also writes U = beta dL/dJ (fp16)
+    FusedParams p = make_params(h, im.B, im.C, im.H, im.W, grad_image ? 3 : 2);
     p.image = im.data;
+    p.zernike = zernike_field;
     p.gJ = h->d_gJ;
     p.beta_out = grad_beta;
+    p.u_out = grad_image ? h->d_ut : nullptr;
+    p.Ws = Ws;
     s = launch_fused(h, p, st);
     if (s != P2S_OK) return s;
+  }
+  if (grad_image) {  // dL/dI: the transpose convolution on the tensor cores (k_adjoint_image)
+    P2S_CUDA(cudaMemsetAsync(grad_image, 0, chw * sizeof(float), st));
+    DiParams d{};
+    {
+      cuuint64_t gdim[4] = {8, (cuuint64_t)im.H, (cuuint64_t)Ws / 8, (cuuint64_t)im.B * im.C * h->K};
+      cuuint64_t gstride[3] = {(cuuint64_t)Ws * 2, 16, (cuuint64_t)im.H * Ws * 2};
+      cuuint32_t box[4] = {8, 8, 16, 1};
+      cuuint32_t estr[4] = {1, 1, 1, 1};
+      CUresult cr = h->encode(&d.umap, CU_TENSOR_MAP_DATA_TYPE_FLOAT16, 4, h->d_ut, gdim, gstride, box, estr,
+                              CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE,
+                              CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+      if (cr != CUDA_SUCCESS) {
+        g_last_cuda_error = "cuTensorMapEncodeTiled (U) failed (" + std::to_string((int)cr) + ")";
+        return P2S_ERR_CUDA;
+      }
+    }
+    d.btab = h->d_dib;
+    d.gI = grad_image;
+    d.BC = im.B * im.C; d.K = h->K; d.H = im.H; d.W = im.W; d.S = h->S; d.r = h->r;
+    d.R = h->di_R; d.nchunk = h->di_nchunk; d.kg = h->di_kg; d.ngroups = h->di_ngroups; d.Nh = h->di_Nh;
+    d.OW = h->di_OW;
+    d.xs0 = -8 * ((2 * h->r + 7) / 8);  // <= -2r: the first strip's outputs start at or before -r
+    d.nbands = (im.H + 2 * h->r + d.R - 1) / d.R;
+    d.nstrips = (im.W - d.xs0 + d.OW - 1) / d.OW;
+    d.ntiles = d.BC * d.nbands * d.nstrips;
+    d.a_bytes = h->di_a_bytes; d.b_bytes = h->di_b_bytes; d.nring = h->di_nring;
+    d.off_p = h->di_off_p; d.off_bar = h->di_off_bar;
+    k_adjoint_image<<<std::min(d.ntiles, h->sm_count), kDiThreads, h->di_smem, st>>>(d);
+    P2S_CUDA(cudaPeekAtLastError());
   }
   return P2S_OK;
 }
@@ -1032,6 +1146,7 @@ void p2s_destroy(p2s_handle* h) {
   cudaFree(h->d_J);
   cudaFree(h->h_img); cudaFree(h->h_z); cudaFree(h->h_t); cudaFree(h->h_out); cudaFree(h->h_anc);
   cudaFree(h->d_gJ);
+  cudaFree(h->d_dib); cudaFree(h->d_ut);
   if (h->s_in) cudaStreamDestroy(h->s_in);
   if (h->ev_entry) cudaEventDestroy(h->ev_entry);
   if (h->ev_band) cudaEventDestroy(h->ev_band);

@@ -107,7 +107,9 @@ struct FusedParams {
   int off_anc, anc_cols;  // shared table of y-interpolated anchor rows [n_in][anc_cols] (per tile)
   float* J;              // [B][C][H][W] (mode 0)
   float* beta_out;       // [B][K][H][W] (mode 1: beta; mode 2: dL/dbeta)
-  const float* gJ;       // [B][C][H][W] dL/dJ (mode 2, the adjoint: SURVEY NEXT-4)
+  const float* gJ;  // [B][C][H][W] dL/dJ (the adjoint)
+  __half* u_out;    // kAdj = 2: U = beta dL/dJ, fp16 [B][C][K][H][Ws]
+  int Ws;           // U row pitch (ceil8(W))
   int B, C, H, W, n_in;
   int nstrips, ntiles, mode;  // mode 0: MLP + conv -> J ; mode 1: MLP only -> beta ;
                               // mode 2: conv only -> dL/dbeta = sum_c dL/dJ_c C_kc (adjoint)
@@ -364,6 +366,47 @@ __device__ __forceinline__ void adj_epi(uint32_t tl, int Nk, int K, int wg, int 
   }
 }
 
+// adjoint epilogue with U (kAdj = 2): beta_k (MLP output, + b3 unless folded) and the NC
+// channels' conv accumulators per 16-column group ->
+//   dL/dbeta_k = sum_c dL/dJ_c (C'_kc + 0.5 s_k)      (if dbeta != nullptr)
+//   U_kc       = fp16(beta_k dL/dJ_c)                   (plane (c, k) of the pixel's frame)
+// consts: the global [b3 | s] table (read through L1, as adj_epi). real = x < W (pitch columns
+// beyond W store zero U so the TMA view reads zeros there).
+template <int NC>
+__device__ __forceinline__ void adj_u_epi(uint32_t tl, int scr_col, int Nk, int K, int wg, int GK, const float* gJ,
+                                          size_t HW, const float* __restrict__ consts, bool b3_folded, float* dbeta,
+                                          __half* u, size_t plane, bool st, bool real) {
+  float gj[NC], gsum = 0.f;
+#pragma unroll
+  for (int c = 0; c < NC; ++c) {
+    gj[c] = (st && real) ? __ldg(gJ + c * HW) : 0.f;
+    gsum += gj[c];
+  }
+  for (int gi = wg; gi < GK; gi += 2) {
+    float bv[16], av[NC][16];
+    tmem_ld16(tl + scr_col + gi * 16, bv);
+#pragma unroll
+    for (int c = 0; c < NC; ++c) tmem_ld16(tl + c * Nk + gi * 16, av[c]);
+    tmem_ld_wait();
+    if (st)
+#pragma unroll
+      for (int i = 0; i < 16; ++i) {
+        const int k = gi * 16 + i;
+        if (k < K) {
+          const float beta = bv[i] + (b3_folded ? 0.f : __ldg(consts + k));
+#pragma unroll
+          for (int c = 0; c < NC; ++c) u[((size_t)c * K + k) * plane] = __float2half_rn(beta * gj[c]);
+          if (dbeta && real) {
+            float v = 0.5f * __ldg(consts + 128 + k) * gsum;
+#pragma unroll
+            for (int c = 0; c < NC; ++c) v = fmaf(gj[c], av[c][i], v);
+            dbeta[(size_t)k * HW] = v;
+          }
+        }
+      }
+  }
+}
+
 template <int NC>
 __device__ __forceinline__ void conv_epi_group(uint32_t tl, int scr_col, int Nk, int gi, int C,
                                                const float* sB3, const float* sSv, float2 (&jc2)[3],
@@ -476,7 +519,7 @@ __device__ __noinline__ void build_A1_anchors(const FusedParams& p, uint8_t* dst
 // instantiation: merely having the anchor path in the builders cost the dense kernel ~80 B of
 // register spills and ~1.5 % (measured). kAdjoint: mode 2 (conv-only lists, dL/dbeta epilogue),
 // likewise its own instantiation; the render instantiations see mode & 1 only (0 or 1).
-template <bool kAnchors, bool kAdjoint = false>
+template <bool kAnchors, int kAdj = 0>
 __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads)
     k_fused_p2s(const __grid_constant__ FusedParams p) {
   extern __shared__ __align__(1024) uint8_t smem[];
@@ -509,7 +552,9 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads)
   const int ncl = gridDim.x >> 1, cl = blockIdx.x >> 1;
   const int pr_begin = (int)(((long long)cl * npairs) / ncl);
   const int pr_end = (int)(((long long)(cl + 1) * npairs) / ncl);
-  const int pmode = kAdjoint ? 2 : (p.mode & 1);
+  // kAdj 1: dL/dbeta only (conv-only lists, mode 2); kAdj 2: dL/dbeta + U = beta dL/dJ (the
+  // render flow, mode 0, with the adjoint epilogue)
+  const int pmode = kAdj == 1 ? 2 : (kAdj == 2 ? 0 : (p.mode & 1));
   // per-tile item lists: tile 0 of this CTA uses list A (MLP first), later tiles list B
   const int offC = p.n_items_full + p.n_items_beta + p.n_items_first + p.n_items_seq;  // conv-only list
   const int nA = pmode == 0 ? p.n_items_first : (pmode == 1 ? p.n_items_beta : p.n_items_conv);
@@ -638,12 +683,12 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads)
 #ifdef P2S_PROFILE
       const long long tr_a = clock64();
 #endif
-      if (!kAdjoint && (f & MI_WAIT_A1)) {
+      if (kAdj != 1 && (f & MI_WAIT_A1)) {
         { PROF_T0(); mbar_wait(&bars[BAR_A1_FULL], a1_waits & 1); PROF_ADD(0); }
         ++a1_waits;
       }
       if (f & MI_WAIT_TMEM) { PROF_T0(); mbar_wait(&bars[BAR_TMEM_FREE], (it & 1) ^ 1); PROF_ADD(1); }
-      if (!kAdjoint && (f & MI_WAIT_SCR)) {
+      if (kAdj != 1 && (f & MI_WAIT_SCR)) {
         { PROF_T0(); mbar_wait(&bars[BAR_SCR_FREE], scr_waits & 1); PROF_ADD(2); }
         ++scr_waits;
       }
@@ -662,7 +707,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads)
 #if defined(P2S_ABL_NOCONVMMA)
       if ((f & MI_CONV) && n == 0) {
 #else
-      if (kAdjoint || (f & MI_CONV)) {  // (the adjoint's lists hold conv stages only)
+      if (kAdj == 1 || (f & MI_CONV)) {  // (the kAdj = 1 lists hold conv stages only)
 #endif
         PROF_T0();
         const uint32_t e0 = e_lo + (uint32_t)eb * ebuf16;
@@ -935,6 +980,22 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads)
             for (int i = 0; i < 16 && gi * 16 + i < p.K; ++i)
               p.beta_out[((size_t)b * p.K + gi * 16 + i) * HW + (size_t)y * p.W + x] = bv[i] + (p.bias_folded ? 0.f : sB3[gi * 16 + i]);
         }
+      } else if (kAdj == 2) {
+        const bool st = store && x < p.Ws;  // pitch columns [W, Ws) get zeros
+        const size_t pix = (size_t)y * p.W + x;
+        const float* gJb = p.gJ + (size_t)b * C * HW + pix;
+        float* ob = p.beta_out ? p.beta_out + (size_t)b * p.K * HW + pix : nullptr;
+        __half* ub = p.u_out + (size_t)b * C * p.K * p.H * p.Ws + (size_t)y * p.Ws + x;
+        const bool real = x < p.W;
+        if (C == 3) adj_u_epi<3>(tl, p.scr_col, p.Nk, p.K, wg, GK, gJb, HW, p.consts, p.bias_folded != 0, ob, ub,
+                                 (size_t)p.H * p.Ws, st, real);
+        else if (C == 2) adj_u_epi<2>(tl, p.scr_col, p.Nk, p.K, wg, GK, gJb, HW, p.consts, p.bias_folded != 0, ob, ub,
+                                      (size_t)p.H * p.Ws, st, real);
+        else adj_u_epi<1>(tl, p.scr_col, p.Nk, p.K, wg, GK, gJb, HW, p.consts, p.bias_folded != 0, ob, ub,
+                          (size_t)p.H * p.Ws, st, real);
+        tc_fence_before();
+        __syncwarp();
+        if (lane == 0) mbar_arrive_remote(&bars[BAR_TMEM_FREE], 0);
       } else {
         // packed fp32x2 accumulation: lane .x sums even k, .y odd k (combined after the loop)
         float2 jc2[3] = {make_float2(0.f, 0.f), make_float2(0.f, 0.f), make_float2(0.f, 0.f)};

@@ -98,7 +98,7 @@ def load_library(path: str = LIB_PATH) -> ctypes.CDLL:
     lib.p2s_sampler_init.argtypes = [i, i, ctypes.c_double, v, ctypes.POINTER(v)]
     lib.p2s_sample_anchors.argtypes = [v, ctypes.c_ulonglong, i, i, v, v]
     lib.p2s_sampler_destroy.argtypes = [v]
-    lib.p2s_backward.argtypes = [v, _Image, v, v, v, v, v, v]
+    lib.p2s_backward.argtypes = [v, _Image, v, v, v, v, v, v, v]
     lib.p2s_sampler_destroy.restype = None
     for name in ("p2s_init", "p2s_render", "p2s_render_host", "p2s_reserve", "p2s_set_profile_events",
                  "p2s_get_info", "p2s_debug_beta", "p2s_debug_blur", "p2s_debug_profile_buffer",
@@ -168,9 +168,11 @@ class Renderer:
         _check(self._lib.p2s_render(self._h, im, zp, tp, op, _stream_handle(stream)), "p2s_render")
         return out
 
-    def backward(self, image, zernike, tilt, grad_out, want_beta=True, want_tilt=True, stream=None):
+    def backward(self, image, zernike, tilt, grad_out, want_beta=True, want_tilt=True, want_image=False,
+                 stream=None):
         """p2s_backward: (dL/dbeta [B,K,H,W] | None, dL/dt [B,2,H,W] | None) of the
-        frames render(image, zernike, tilt) gives, for upstream grad_out [B,C,H,W]."""
+        frames render(image, zernike, tilt) gives, for upstream grad_out [B,C,H,W]; with
+        want_image=True a third entry dL/dI [B,C,H,W]."""
         import torch
         B, C, H, W = image.shape
         im = _Image(_dev_ptr(image, "image").value, B, C, H, W)
@@ -179,11 +181,13 @@ class Renderer:
         gp = _dev_ptr(grad_out, "grad_out", (B, C, H, W))
         gb = torch.empty((B, self.K, H, W), device=image.device, dtype=torch.float32) if want_beta else None
         gt = torch.empty((B, 2, H, W), device=image.device, dtype=torch.float32) if want_tilt else None
+        gi = torch.empty((B, C, H, W), device=image.device, dtype=torch.float32) if want_image else None
         _check(self._lib.p2s_backward(self._h, im, zp, tp, gp,
                                       _dev_ptr(gb, "grad_beta") if gb is not None else ctypes.c_void_p(),
                                       _dev_ptr(gt, "grad_tilt") if gt is not None else ctypes.c_void_p(),
+                                      _dev_ptr(gi, "grad_image") if gi is not None else ctypes.c_void_p(),
                                       _stream_handle(stream)), "p2s_backward")
-        return gb, gt
+        return (gb, gt, gi) if want_image else (gb, gt)
 
     def debug_beta(self, zernike, out=None, stream=None):
         import torch

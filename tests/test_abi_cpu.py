@@ -89,7 +89,7 @@ def test_sass_has_tcgen05_and_tma(lib):
     # the UMMA issue loop must stay on the uniform datapath: descriptors in uniform registers,
     # no per-UMMA divergence/elect loops (a silent 1.5x slowdown when uniformity is lost)
     funcs = [f for f in sass.split("Function : ")[1:] if f.startswith("_ZN3p2s11k_fused_p2s")]
-    assert len(funcs) == 3  # dense-field, anchor-grid and adjoint instantiations
+    assert len(funcs) == 4  # dense-field, anchor-grid and the two adjoint instantiations
     for fused in funcs:
         ins = [l.split("*/", 1)[1].strip() for l in fused.split("\n") if l.strip().startswith("/*") and "*/" in l
                and not l.strip().startswith("/* 0x")]

@@ -469,13 +469,14 @@ ADJ_CASES = ["ragged_rgb_S7", "S33_K100_C2", "many_tiles_C2", "S1_K1", "W1_H1", 
 def _adj_ref(inp, g, with_tilt):
     from oracle import adjoint
     beta = oracle.beta(inp.image, inp.zernike, inp.basis, inp.mlp)
-    gb, gt = [], []
+    gb, gt, gi = [], [], []
     for b in range(inp.image.shape[0]):
         t = inp.tilt[b] if with_tilt else np.zeros_like(inp.tilt[b])
-        _, gbb, gtb, _ = adjoint.backward(inp.image[b], beta[b], t, inp.basis, g[b], coord_dtype=np.float32)
+        _, gbb, gtb, gib = adjoint.backward(inp.image[b], beta[b], t, inp.basis, g[b], coord_dtype=np.float32)
         gb.append(gbb)
         gt.append(gtb)
-    return np.stack(gb), np.stack(gt)
+        gi.append(gib)
+    return np.stack(gb), np.stack(gt), np.stack(gi)
 
 
 @pytest.mark.parametrize("with_tilt", [True, False])
@@ -485,10 +486,24 @@ def test_backward_parity(p2s, name, with_tilt):
     inp = synth.make_inputs(spec)
     g = synth.make_upstream_grad(spec)
     r = p2s.Renderer(inp.basis, inp.mlp)
-    gb, gt = r.backward(_dev(inp.image), _dev(inp.zernike), _dev(inp.tilt) if with_tilt else None, _dev(g))
-    gb, gt = gb.cpu().numpy(), gt.cpu().numpy()
-    rb, rt = _adj_ref(inp, g, with_tilt)
+    gb, gt, gi = r.backward(_dev(inp.image), _dev(inp.zernike), _dev(inp.tilt) if with_tilt else None, _dev(g),
+                            want_image=True)
+    gb, gt, gi = gb.cpu().numpy(), gt.cpu().numpy(), gi.cpu().numpy()
+    rb, rt, ri = _adj_ref(inp, g, with_tilt)
     _cmp(gb, rb, f"dL/dbeta[{name}]", max_abs=2e-3 * np.abs(rb).max())
+    if name in REL_TO_INPUT:
+        # 1x1 frame: dL/dI = dL/dJ sum_k beta_k s_k cancels like J does (see REL_TO_INPUT); the fp16
+        # rounding error follows the terms' absolute sum, so the scale is that sum (the oracle on
+        # |beta|, |phi|, |dL/dJ|)
+        from oracle import adjoint
+        beta = oracle.beta(inp.image, inp.zernike, inp.basis, inp.mlp)
+        scale = np.stack([adjoint.grad_image(np.abs(beta[b]), np.abs(inp.basis),
+                                             np.abs(adjoint.grad_J(inp.tilt[b] if with_tilt else 0 * inp.tilt[b],
+                                                                   g[b], np.float32)))
+                          for b in range(inp.image.shape[0])])
+        _cmp(gi, ri, f"dL/dI[{name}]", max_abs=2e-3 * scale.max(), norm_ref=scale)
+    else:
+        _cmp(gi, ri, f"dL/dI[{name}]", max_abs=2e-3 * np.abs(ri).max())
     C = inp.image.shape[1]
     err = np.abs(gt - rt).max()
     print(f"dL/dt[{name}]: max_abs={err:.3e} (ref max {np.abs(rt).max():.3f})")
@@ -511,8 +526,8 @@ def test_backward_cfg3_sampled(p2s):
     inp = synth.make_inputs(spec)
     g = synth.make_upstream_grad(spec)
     r = p2s.Renderer(inp.basis, inp.mlp)
-    gb, gt = r.backward(_dev(inp.image), _dev(inp.zernike), _dev(inp.tilt), _dev(g))
-    gb, gt = gb.cpu().numpy(), gt.cpu().numpy()
+    gb, gt, gi = r.backward(_dev(inp.image), _dev(inp.zernike), _dev(inp.tilt), _dev(g), want_image=True)
+    gb, gt, gi = gb.cpu().numpy(), gt.cpu().numpy(), gi.cpu().numpy()
     B, C, H, W = inp.image.shape
     rng = np.random.default_rng(11)
     yx = [(0, 0), (H - 1, W - 1), (0, W - 1), (H // 2, 127), (H // 2, 128), (H - 1, 0)]
@@ -524,6 +539,14 @@ def test_backward_cfg3_sampled(p2s):
     err = np.abs(gt[0][:, ys, xs].T - rt).max()
     print(f"dL/dt[cfg3 sampled]: max_abs={err:.3e} (ref max {np.abs(rt).max():.3f})")
     assert err <= 2 * 2e-3 * C * np.abs(g).max()
+    # dL/dI at sampled pixels: the strip/band seams of k_adjoint_image (96-column strips and
+    # 8-row bands on the extended grid start at -16) and the clamp-collecting borders
+    gJ = adjoint.grad_J(inp.tilt[0], g[0], coord_dtype=np.float32)
+    yxi = [(0, 0), (H - 1, W - 1), (0, 200), (300, W - 1), (7, 79), (8, 80), (H // 2, 175), (H // 2, 176)]
+    yxi += [(int(y), int(x)) for y, x in zip(rng.integers(1, H - 1, 40), rng.integers(1, W - 1, 40))]
+    ri = adjoint.grad_image_at(beta, inp.basis, gJ, yxi)
+    yi, xi = np.array(yxi).T
+    _cmp(gi[0][:, yi, xi].T, ri, "dL/dI[cfg3 sampled]", max_abs=2e-3 * np.abs(ri).max())
 
 
 def test_backward_invalid_args(p2s):
@@ -538,4 +561,4 @@ def test_backward_invalid_args(p2s):
     for args in ((vp(z.data_ptr()), vp(), vp(g.data_ptr()), vp(), vp()),              # no output
                  (vp(), vp(), vp(g.data_ptr()), vp(buf.data_ptr()), vp()),             # no zernike
                  (vp(z.data_ptr()), vp(), vp(), vp(buf.data_ptr()), vp())):            # no grad_out
-        assert r._lib.p2s_backward(r._h, im, *args, vp()) == p2s.P2S_ERR_INVALID_ARG
+        assert r._lib.p2s_backward(r._h, im, *args, vp(), vp()) == p2s.P2S_ERR_INVALID_ARG
