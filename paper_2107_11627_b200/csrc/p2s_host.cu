@@ -683,40 +683,41 @@ p2s_status p2s_init(const p2s_basis* basis, const p2s_mlp* mlp, p2s_handle** out
                                 kSmemLimit)) != cudaSuccess)
     return fail(cuda_fail(e, "cudaFuncSetAttribute"));
   {
-    // ---- dL/dI plan (p2s_adjoint.cuh): R output rows per band, WR8 8-row U chunks per basis
-    // function, N = R x S in two halves of Nh columns; k-groups of kg functions make every stage
-    // an even number of chunks (UMMA K = 16 = two chunks), else the window is padded by a chunk
-    // R = 8 rows per band when N = 4 S fits one UMMA and >= 2 ring stages fit, else R = 4
+    // ---- dL/dI plan (p2s_adjoint.cuh): one basis function per ring stage; its U window of
+    // nchunk 8-row chunks (even: UMMA K = 16) and N = R x S in two halves of Nh columns
+    // R output rows per band share one window of R + S - 1 rows: the R minimising the staged
+    // bytes per output row (this CTA's A window + its half of B) such that each half of
+    // N = R x S fits one UMMA (<= 256) and >= 3 ring stages fit (measured: the kernel is bound
+    // by L2 -> SM delivery, so bytes per output decide)
     int R = 0, hr = 0, Nh = 0, wr8 = 0, kg = 1, nchunk = 0, wpad = 0, stage = 0, nring = 0;
     const int sp_bytes = S * 128 * 4, bar_bytes = 256;
     const int avail = kSmemLimit - sp_bytes - bar_bytes;
-    for (int Rt : {8, 4}) {
-      R = Rt; hr = R / 2;
-      Nh = (hr * S + 15) / 16 * 16;
-      if (Nh > 256) continue;
-      wr8 = (S + R - 1 + 7) / 8;  // window rows s + i < R + S - 1
-      auto stage_of = [&](int nch) { return nch * 2048 + 2 * nch * Nh * 16; };
-      kg = 1; nchunk = wr8; wpad = wr8;
-      if (wr8 % 2) {
-        if (3 * stage_of(2 * wr8) <= avail) { kg = 2; nchunk = 2 * wr8; }
-        else { wpad = wr8 + 1; nchunk = wpad; }
+    double best = 1e30;
+    for (int Rt = 2; Rt <= 32; Rt += 2) {
+      const int Nht = (Rt / 2 * S + 15) / 16 * 16;
+      if (Nht > 256) break;
+      const int w8 = (S + Rt - 1 + 7) / 8, nch = w8 + (w8 & 1);  // even chunk count: UMMA K = 16
+      const int stg = nch * 2048 + nch * Nht * 16;
+      const int nr = std::min(6, avail / stg);
+      if (nr < 3 || nch * 8 > 256) continue;
+      const double cost = (double)stg / Rt;
+      if (cost < best) {
+        best = cost;
+        R = Rt; hr = Rt / 2; Nh = Nht; wr8 = w8; nchunk = nch; wpad = nch; stage = stg; nring = nr;
       }
-      stage = stage_of(nchunk);
-      nring = std::min(6, avail / stage);
-      if (nring >= 2) break;
     }
     if (nring < 2) return fail(P2S_ERR_UNSUPPORTED);  // not reached for S <= 65
     h->di_R = R; h->di_Nh = Nh; h->di_kg = kg; h->di_nchunk = nchunk; h->di_nring = nring;
     h->di_ngroups = (K + kg - 1) / kg;
     h->di_OW = (128 - (S - 1)) / 8 * 8;  // strips start at multiples of 8 columns (TMA x/8 view)
     h->di_a_bytes = nchunk * 2048;
-    h->di_b_bytes = 2 * nchunk * Nh * 16;
+    h->di_b_bytes = nchunk * Nh * 16;  // per CTA: two halves x Nh/2 rows
     h->di_off_p = nring * stage;
     h->di_off_bar = h->di_off_p + sp_bytes;
     // >= 120 KB so that one CTA (and one 512-column TMEM allocation) occupies an SM
     h->di_smem = std::max(h->di_off_bar + bar_bytes, 120 * 1024);
     const int cpk = nchunk / kg;  // chunks per basis function (wr8, or wr8 + 1 when padded)
-    std::vector<__half> tab((size_t)h->di_ngroups * h->di_b_bytes / 2, __float2half(0.f));
+    std::vector<__half> tab((size_t)h->di_ngroups * 2 * h->di_b_bytes / 2, __float2half(0.f));
     for (int g = 0; g < h->di_ngroups; ++g)
       for (int hf = 0; hf < 2; ++hf)
         for (int c = 0; c < nchunk; ++c)
@@ -725,7 +726,9 @@ p2s_status p2s_init(const p2s_basis* basis, const p2s_mlp* mlp, p2s_handle** out
               const int kl = c / cpk, w = (c - kl * cpk) * 8 + e8, k = g * kg + kl;
               const int sr = hf * hr + n / S, j = n % S, i = w - sr;
               if (n >= hr * S || k >= K || i < 0 || i >= S) continue;
-              const size_t at = ((((size_t)g * 2 + hf) * nchunk + c) * Nh + n) * 8 + e8;
+              // [g][CTA rho][half][chunk][Nh/2 rows][8]: CTA rho stages rows [rho Nh/2, +Nh/2)
+              const int rho = n / (Nh / 2), nl = n % (Nh / 2);
+              const size_t at = (((((size_t)g * 2 + rho) * 2 + hf) * nchunk + c) * (Nh / 2) + nl) * 8 + e8;
               tab[at] = __float2half_rn(basis->taps[((size_t)k * S + i) * S + j]);
             }
     if ((e = cudaMalloc(&h->d_dib, tab.size() * sizeof(__half))) != cudaSuccess ||
@@ -880,7 +883,7 @@ p2s_status p2s_backward(p2s_handle* h, p2s_image im, const float* zernike_field,
     {
       cuuint64_t gdim[4] = {8, (cuuint64_t)im.H, (cuuint64_t)Ws / 8, (cuuint64_t)im.B * im.C * h->K};
       cuuint64_t gstride[3] = {(cuuint64_t)Ws * 2, 16, (cuuint64_t)im.H * Ws * 2};
-      cuuint32_t box[4] = {8, 8, 16, 1};
+      cuuint32_t box[4] = {8, (cuuint32_t)h->di_nchunk * 8, 16, 1};
       cuuint32_t estr[4] = {1, 1, 1, 1};
       CUresult cr = h->encode(&d.umap, CU_TENSOR_MAP_DATA_TYPE_FLOAT16, 4, h->d_ut, gdim, gstride, box, estr,
                               CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE,
@@ -890,7 +893,20 @@ p2s_status p2s_backward(p2s_handle* h, p2s_image im, const float* zernike_field,
         return P2S_ERR_CUDA;
       }
     }
-    d.btab = h->d_dib;
+    {
+      const cuuint64_t rows = (cuuint64_t)h->di_ngroups * 2 * h->di_b_bytes / 256;
+      cuuint64_t gdim[2] = {256, rows};
+      cuuint64_t gstride[1] = {256};
+      cuuint32_t box[2] = {256, (cuuint32_t)(h->di_b_bytes / 256)};
+      cuuint32_t estr[2] = {1, 1};
+      CUresult cr = h->encode(&d.bmap, CU_TENSOR_MAP_DATA_TYPE_UINT8, 2, h->d_dib, gdim, gstride, box, estr,
+                              CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE,
+                              CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+      if (cr != CUDA_SUCCESS) {
+        g_last_cuda_error = "cuTensorMapEncodeTiled (dI table) failed (" + std::to_string((int)cr) + ")";
+        return P2S_ERR_CUDA;
+      }
+    }
     d.gI = grad_image;
     d.BC = im.B * im.C; d.K = h->K; d.H = im.H; d.W = im.W; d.S = h->S; d.r = h->r;
     d.R = h->di_R; d.nchunk = h->di_nchunk; d.kg = h->di_kg; d.ngroups = h->di_ngroups; d.Nh = h->di_Nh;
@@ -898,10 +914,11 @@ p2s_status p2s_backward(p2s_handle* h, p2s_image im, const float* zernike_field,
     d.xs0 = -8 * ((2 * h->r + 7) / 8);  // <= -2r: the first strip's outputs start at or before -r
     d.nbands = (im.H + 2 * h->r + d.R - 1) / d.R;
     d.nstrips = (im.W - d.xs0 + d.OW - 1) / d.OW;
-    d.ntiles = d.BC * d.nbands * d.nstrips;
+    d.npairs = (d.nstrips + 1) / 2;
+    d.ntiles = d.BC * d.nbands * d.npairs;
     d.a_bytes = h->di_a_bytes; d.b_bytes = h->di_b_bytes; d.nring = h->di_nring;
     d.off_p = h->di_off_p; d.off_bar = h->di_off_bar;
-    k_adjoint_image<<<std::min(d.ntiles, h->sm_count), kDiThreads, h->di_smem, st>>>(d);
+    k_adjoint_image<<<2 * std::min(d.ntiles, h->sm_count / 2), kDiThreads, h->di_smem, st>>>(d);
     P2S_CUDA(cudaPeekAtLastError());
   }
   return P2S_OK;
