@@ -359,9 +359,9 @@ def main():
         adjoint_mode = {"value": res["value"], "unit": "frames/s", "beta_only": res["beta_only"],
                         "image_only": res["image_only"], "all": res["all"], "api": "p2s_backward",
                         "note": "value: dL/dbeta [K,H,W] + dL/dt [2,H,W] of one cfg3 frame (L2 flushed per "
-                                "call), including the forward recompute dL/dt needs; beta_only skips it; "
-                                "image_only: dL/dI [C,H,W] (MLP pass for beta, U prep, k_adjoint_image); "
-                                "all: the three gradients"}
+                                "call): dL/dJ scatter, one fused pass (MLP + convolutions -> J, dL/dbeta), "
+                                "dL/dt; beta_only: scatter + conv-only pass; image_only: dL/dI [C,H,W] "
+                                "(scatter, fused pass -> U = beta dL/dJ, k_adjoint_image); all: the three"}
         del aimg, az, at, ag
 
     # ---- anchor-grid mode: the same frame with its Zernike coefficients

@@ -839,18 +839,11 @@ p2s_status p2s_backward(p2s_handle* h, p2s_image im, const float* zernike_field,
     P2S_CUDA(cudaMalloc(&h->d_gJ, chw * sizeof(float)));
     h->gJ_cap = chw;
   }
-  if (grad_tilt) {  // J (the forward blur) is needed only for dL/dt
-    FusedParams p = make_params(h, im.B, im.C, im.H, im.W, 0);
-    p.image = im.data;
-    p.zernike = zernike_field;
-    p.J = h->d_J;
-    s = launch_fused(h, p, st);
-    if (s != P2S_OK) return s;
-  }
+  // dL/dJ: dL/dout scattered through the warp's bilinear weights (needs no J)
   P2S_CUDA(cudaMemsetAsync(h->d_gJ, 0, chw * sizeof(float), st));
   const size_t npx = (size_t)im.B * HW;
   const int grid = (int)std::min<size_t>((npx + 255) / 256, (size_t)h->sm_count * 16);
-  k_warp_backward<<<grid, 256, 0, st>>>(h->d_J, tilt_field, grad_out, h->d_gJ, grad_tilt, im.B, im.C, im.H, im.W);
+  k_warp_backward<<<grid, 256, 0, st>>>(nullptr, tilt_field, grad_out, h->d_gJ, nullptr, im.B, im.C, im.H, im.W);
   P2S_CUDA(cudaPeekAtLastError());
   const int Ws = (im.W + 7) / 8 * 8;
   if (grad_image) {
@@ -864,18 +857,24 @@ p2s_status p2s_backward(p2s_handle* h, p2s_image im, const float* zernike_field,
       h->ut_cap = nu;
     }
   }
-  if (grad_beta || grad_image) {
-    // dL/dbeta_k = sum_c dL/dJ_c C_kc (the K convolutions again, another epilogue); with dL/dI the
-    // render flow (MLP + convolutions) whose epilogue also writes U = beta dL/dJ (fp16)
-    FusedParams p = make_params(h, im.B, im.C, im.H, im.W, grad_image ? 3 : 2);
+  {
+    // one pass over the K convolutions: dL/dbeta_k = sum_c dL/dJ_c C_kc; with dL/dt or dL/dI the
+    // render flow (MLP + convolutions, kAdj = 2) whose epilogue also forms J and U = beta dL/dJ
+    const bool full = grad_tilt || grad_image;
+    FusedParams p = make_params(h, im.B, im.C, im.H, im.W, full ? 3 : 2);
     p.image = im.data;
     p.zernike = zernike_field;
     p.gJ = h->d_gJ;
     p.beta_out = grad_beta;
     p.u_out = grad_image ? h->d_ut : nullptr;
+    p.J = grad_tilt ? h->d_J : nullptr;
     p.Ws = Ws;
     s = launch_fused(h, p, st);
     if (s != P2S_OK) return s;
+  }
+  if (grad_tilt) {  // dL/dt from J's bilinear corners
+    k_warp_backward<<<grid, 256, 0, st>>>(h->d_J, tilt_field, grad_out, nullptr, grad_tilt, im.B, im.C, im.H, im.W);
+    P2S_CUDA(cudaPeekAtLastError());
   }
   if (grad_image) {  // dL/dI: the transpose convolution on the tensor cores (k_adjoint_image)
     P2S_CUDA(cudaMemsetAsync(grad_image, 0, chw * sizeof(float), st));

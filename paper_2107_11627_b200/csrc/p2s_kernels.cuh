@@ -369,13 +369,14 @@ __device__ __forceinline__ void adj_epi(uint32_t tl, int Nk, int K, int wg, int 
 // adjoint epilogue with U (kAdj = 2): beta_k (MLP output, + b3 unless folded) and the NC
 // channels' conv accumulators per 16-column group ->
 //   dL/dbeta_k = sum_c dL/dJ_c (C'_kc + 0.5 s_k)      (if dbeta != nullptr)
-//   U_kc       = fp16(beta_k dL/dJ_c)                   (plane (c, k) of the pixel's frame)
+//   U_kc       = fp16(beta_k dL/dJ_c)                   (plane (c, k) of the pixel's frame; if u)
+//   jc[c] += beta_k C'_kc, bs += beta_k s_k            (this warpgroup's part of J, Eq. 5)
 // consts: the global [b3 | s] table (read through L1, as adj_epi). real = x < W (pitch columns
 // beyond W store zero U so the TMA view reads zeros there).
 template <int NC>
 __device__ __forceinline__ void adj_u_epi(uint32_t tl, int scr_col, int Nk, int K, int wg, int GK, const float* gJ,
                                           size_t HW, const float* __restrict__ consts, bool b3_folded, float* dbeta,
-                                          __half* u, size_t plane, bool st, bool real) {
+                                          __half* u, size_t plane, bool st, bool real, float (&jc)[3], float& bs) {
   float gj[NC], gsum = 0.f;
 #pragma unroll
   for (int c = 0; c < NC; ++c) {
@@ -394,10 +395,16 @@ __device__ __forceinline__ void adj_u_epi(uint32_t tl, int scr_col, int Nk, int 
         const int k = gi * 16 + i;
         if (k < K) {
           const float beta = bv[i] + (b3_folded ? 0.f : __ldg(consts + k));
+          const float sk = __ldg(consts + 128 + k);
+          bs = fmaf(beta, sk, bs);
 #pragma unroll
-          for (int c = 0; c < NC; ++c) u[((size_t)c * K + k) * plane] = __float2half_rn(beta * gj[c]);
+          for (int c = 0; c < NC; ++c) jc[c] = fmaf(beta, av[c][i], jc[c]);
+          if (u) {
+#pragma unroll
+            for (int c = 0; c < NC; ++c) u[((size_t)c * K + k) * plane] = __float2half_rn(beta * gj[c]);
+          }
           if (dbeta && real) {
-            float v = 0.5f * __ldg(consts + 128 + k) * gsum;
+            float v = 0.5f * sk * gsum;
 #pragma unroll
             for (int c = 0; c < NC; ++c) v = fmaf(gj[c], av[c][i], v);
             dbeta[(size_t)k * HW] = v;
@@ -985,17 +992,32 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads)
         const size_t pix = (size_t)y * p.W + x;
         const float* gJb = p.gJ + (size_t)b * C * HW + pix;
         float* ob = p.beta_out ? p.beta_out + (size_t)b * p.K * HW + pix : nullptr;
-        __half* ub = p.u_out + (size_t)b * C * p.K * p.H * p.Ws + (size_t)y * p.Ws + x;
+        __half* ub = p.u_out ? p.u_out + (size_t)b * C * p.K * p.H * p.Ws + (size_t)y * p.Ws + x : nullptr;
         const bool real = x < p.W;
+        const size_t plane = (size_t)p.H * p.Ws;
+        float jc[3] = {0.f, 0.f, 0.f}, bs = 0.f;
         if (C == 3) adj_u_epi<3>(tl, p.scr_col, p.Nk, p.K, wg, GK, gJb, HW, p.consts, p.bias_folded != 0, ob, ub,
-                                 (size_t)p.H * p.Ws, st, real);
+                                 plane, st, real, jc, bs);
         else if (C == 2) adj_u_epi<2>(tl, p.scr_col, p.Nk, p.K, wg, GK, gJb, HW, p.consts, p.bias_folded != 0, ob, ub,
-                                      (size_t)p.H * p.Ws, st, real);
-        else adj_u_epi<1>(tl, p.scr_col, p.Nk, p.K, wg, GK, gJb, HW, p.consts, p.bias_folded != 0, ob, ub,
-                          (size_t)p.H * p.Ws, st, real);
+                                      plane, st, real, jc, bs);
+        else adj_u_epi<1>(tl, p.scr_col, p.Nk, p.K, wg, GK, gJb, HW, p.consts, p.bias_folded != 0, ob, ub, plane,
+                          st, real, jc, bs);
         tc_fence_before();
         __syncwarp();
         if (lane == 0) mbar_arrive_remote(&bars[BAR_TMEM_FREE], 0);
+        if (p.J) {  // the forward blur J as well (dL/dt needs it): the two warpgroups' halves
+          float4* red = sRed + (red_i++ & 1) * 128;
+          if (wg == 1) red[m] = make_float4(jc[0], jc[1], jc[2], bs);
+          named_bar_sync(1, 32 * kNumEpiWarps);
+          if (wg == 0 && store && x < p.W) {
+            const float4 o = red[m];
+            const float bt = bs + o.w;
+            const float jt[3] = {jc[0] + o.x, jc[1] + o.y, jc[2] + o.z};
+#pragma unroll
+            for (int c = 0; c < 3; ++c)
+              if (c < C) p.J[((size_t)b * C + c) * HW + (size_t)y * p.W + x] = fmaf(0.5f, bt, jt[c]);
+          }
+        }
       } else {
         // packed fp32x2 accumulation: lane .x sums even k, .y odd k (combined after the loop)
         float2 jc2[3] = {make_float2(0.f, 0.f), make_float2(0.f, 0.f), make_float2(0.f, 0.f)};
@@ -1148,6 +1170,7 @@ __global__ void __launch_bounds__(256) k_tilt_warp(const float* __restrict__ J, 
 // Adjoint of the tilt warp (oracle/adjoint.py): per output pixel p, the
 // bilinear weights scatter g_c(p) into dL/dJ (atomicAdd, gJ zeroed by the caller) and
 // dL/dt(p) = -sum_c g_c(p) d out_c / d s (0 where the coordinate clamp is active).
+// gJ != nullptr: scatter dL/dout into dL/dJ (needs no J); gt != nullptr: dL/dt from J's corners
 __global__ void __launch_bounds__(256) k_warp_backward(const float* __restrict__ J, const float* __restrict__ tilt,
                                                        const float* __restrict__ g, float* __restrict__ gJ,
                                                        float* __restrict__ gt, int B, int C, int H, int W) {
@@ -1172,11 +1195,13 @@ __global__ void __launch_bounds__(256) k_warp_backward(const float* __restrict__
     float dsx = 0.f, dsy = 0.f;
     for (int c = 0; c < C; ++c) {
       const float gc = __ldg(g + (b * C + c) * HW + pix);
-      float* gJc = gJ + (b * C + c) * HW;
-      atomicAdd(gJc + (size_t)ya * W + xa, gc * w00);
-      atomicAdd(gJc + (size_t)ya * W + xb, gc * w01);
-      atomicAdd(gJc + (size_t)yb * W + xa, gc * w10);
-      atomicAdd(gJc + (size_t)yb * W + xb, gc * w11);
+      if (gJ) {
+        float* gJc = gJ + (b * C + c) * HW;
+        atomicAdd(gJc + (size_t)ya * W + xa, gc * w00);
+        atomicAdd(gJc + (size_t)ya * W + xb, gc * w01);
+        atomicAdd(gJc + (size_t)yb * W + xa, gc * w10);
+        atomicAdd(gJc + (size_t)yb * W + xb, gc * w11);
+      }
       if (gt) {
         const float* Jc = J + (b * C + c) * HW;
         const float j00 = __ldg(Jc + (size_t)ya * W + xa), j01 = __ldg(Jc + (size_t)ya * W + xb);
