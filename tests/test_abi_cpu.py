@@ -101,3 +101,17 @@ def test_sass_has_tcgen05_and_tma(lib):
             assert not any(bad in x for x in region), bad
         for n in mma:  # the 12 instructions feeding each UMMA must use uniform operands only
             assert not any("R2UR.BROADCAST" in x for x in ins[max(0, n - 12):n]), ins[max(0, n - 12):n + 1]
+
+
+def test_sass_adjoint_image_kernel(lib):
+    """dL/dI (k_adjoint_image): pair UMMAs fed by TMA, a uniform issue loop (SASS evidence)."""
+    sass = os.popen(f"cuobjdump -sass {lib._name}").read()
+    funcs = [f for f in sass.split("Function : ")[1:] if f.startswith("_ZN3p2s15k_adjoint_image")]
+    assert len(funcs) == 1
+    ins = [l.split("*/", 1)[1].strip() for l in funcs[0].split("\n") if l.strip().startswith("/*") and "*/" in l
+           and not l.strip().startswith("/* 0x")]
+    mma = [n for n, l in enumerate(ins) if "UTCHMMA.2CTA" in l]
+    assert len(mma) == 2 and any("UTMALDG.4D" in l for l in ins) and any("UTMALDG.2D" in l for l in ins)
+    region = ins[max(0, mma[0] - 40):mma[-1] + 20]
+    for bad in ("BRA.DIV", "BRA.U.ANY", "R2UR.BROADCAST"):
+        assert not any(bad in x for x in region), bad
