@@ -166,6 +166,7 @@ def main():
     ap.add_argument("--no-batch-mode", action="store_true", help="skip the 16-frame batched-launch extra leg")
     ap.add_argument("--no-sequence-mode", action="store_true", help="skip the 50-frame sequence extra leg")
     ap.add_argument("--no-adjoint-mode", action="store_true", help="skip the adjoint (NEXT-4) extra leg")
+    ap.add_argument("--no-color-mode", action="store_true", help="skip the per-channel beta (row 5) extra leg")
     args = ap.parse_args()
 
     rank, world, local_rank = pdist.env_rank_world()
@@ -364,6 +365,33 @@ def main():
                                 "(scatter, fused pass -> U = beta dL/dJ, k_adjoint_image); all: the three"}
         del aimg, az, at, ag
 
+    # ---- colour mode: per-channel Zernike fields (the
+    # frame's field at 570/540/450 nm) -> per-channel beta; one fused launch per frame
+    color_mode = None
+    if not args.no_color_mode:
+        cinp = synth.make_inputs(spec, frames=pdist.rank_frames(rank, 1))
+        cimg, ct = (torch.from_numpy(a).to(dev) for a in (cinp.image, cinp.tilt))
+        cz = torch.from_numpy(synth.make_zernike_color(spec, frames=pdist.rank_frames(rank, 1))).to(dev)
+        cout = torch.empty_like(cimg)
+        for _ in range(3):
+            r.render_color(cimg, cz, ct, out=cout)
+        n_c = max(5, min(args.steps // 4, 50))
+        c0 = [torch.cuda.Event(enable_timing=True) for _ in range(n_c)]
+        c1 = [torch.cuda.Event(enable_timing=True) for _ in range(n_c)]
+        torch.cuda.synchronize()
+        for i in range(n_c):
+            flush.fill_(float(i))
+            c0[i].record(stream)
+            r.render_color(cimg, cz, ct, out=cout)
+            c1[i].record(stream)
+        torch.cuda.synchronize()
+        c_ms = pdist.max_over_ranks(float(sum(c0[i].elapsed_time(c1[i]) for i in range(n_c))), dist, dev)
+        color_mode = {"value": pdist.throughput(1, world, n_c, c_ms), "unit": "frames/s", "calls": n_c,
+                      "api": "p2s_render_color",
+                      "note": "cfg3 frame, per-channel Zernike fields (z * 540/lambda, lambda = 570/540/450 nm) "
+                              "-> per-channel beta; the convolutions once per tile, 3 MLP + J passes"}
+        del cimg, ct, cz, cout
+
     # ---- anchor-grid mode: the same frame with its Zernike coefficients
     # given on a 16x16 anchor grid and interpolated inside the fused kernel (not the headline
     # workload, which BASELINE.json defines on a dense field); same timing protocol
@@ -467,6 +495,7 @@ def main():
         "batch_mode": batch_mode,
         "sequence_mode": sequence_mode,
         "adjoint_mode": adjoint_mode,
+        "color_mode": color_mode,
         "clocks": clk.summary(),
         "wall_s": t_wall,
         "plan": info,

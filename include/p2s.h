@@ -128,6 +128,17 @@ P2S_API p2s_status p2s_render_anchors_host(p2s_handle* h, const float* image_hos
 P2S_API p2s_status p2s_render_sequence(p2s_handle* h, p2s_image image, const float* zernike_field,
                                        const float* tilt_field, int F, float* out, p2s_stream_t stream);
 
+/* Wavelength-dependent colour ("3 PSFs with wavelengths
+ * 450nm, 540nm, and 570nm ... requires 3x computation"): every channel c of frame b has its own
+ * Zernike field, hence its own beta (PSF field):
+ *   out[b][c] = warp(J_c, tilt[b]),  J_c(p) = sum_k beta_k(z[b][c](p)) (I[b][c] * phi_k)(p)
+ * zernike_field: DEVICE [B][C][n_in][H][W] fp32 (channel-major per frame); image, tilt and out as
+ * p2s_render. The K convolutions of each tile are computed once and serve the C MLP passes
+ * (one fused launch; the channel passes reuse the sequence-mode schedule). With every channel's
+ * field equal this is p2s_render. Errors as p2s_render. */
+P2S_API p2s_status p2s_render_color(p2s_handle* h, p2s_image image, const float* zernike_field,
+                                    const float* tilt_field, float* out, p2s_stream_t stream);
+
 /* Adjoint of steps a2-a3 ("differentiable module"): for the
  * frames p2s_render would produce and an upstream gradient grad_out = dL/dout (DEVICE
  * [B][C][H][W] fp32), writes

@@ -116,6 +116,24 @@ def render(image, zernike, tilt, basis, mlp, rows=None, want_blur=False, threads
     return out, J
 
 
+def render_color(image, zernike_c, tilt, basis, mlp, rows=None, want_blur=False, threads=None):
+    """Wavelength-dependent colour ("3 PSFs with wavelengths
+    450nm, 540nm, and 570nm ... requires 3x computation"): channel c of every frame is rendered as a
+    one-channel image with its own Zernike field zernike_c[b][c] -- its own beta, so its own PSF
+    field -- and the frame's tilt. zernike_c: [B][C][n_in][H][W]. Returns (out, J) like render."""
+    image = np.asarray(image)
+    B, C, H, W = image.shape
+    out = np.zeros((B, C, H, W), np.float64)
+    J = np.zeros((B, C, H, W), np.float64) if want_blur else None
+    for c in range(C):
+        o, j = render(np.ascontiguousarray(image[:, c:c + 1]), np.ascontiguousarray(zernike_c[:, c]), tilt, basis,
+                      mlp, rows=rows, want_blur=want_blur, threads=threads)
+        out[:, c] = o[:, 0]
+        if want_blur:
+            J[:, c] = j[:, 0]
+    return out, J
+
+
 def pixels(image, zernike, tilt, basis, mlp, bxy, want_blur=True, want_out=True, threads=None):
     """Sampled outputs, one by one: (J[n][C], out[n][C]) fp64 at the (b, y, x) triples."""
     a = _Args(image, zernike, tilt, basis, mlp)

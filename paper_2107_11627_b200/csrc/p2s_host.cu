@@ -821,6 +821,32 @@ p2s_status p2s_render_sequence(p2s_handle* h, p2s_image im, const float* zernike
   return launch_warp(h, h->d_J, tilt_field, out, F, im.C, im.H, im.W, st);
 }
 
+p2s_status p2s_render_color(p2s_handle* h, p2s_image im, const float* zernike_field, const float* tilt_field,
+                            float* out, p2s_stream_t stream) {
+  p2s_status s = check_image(h, im);
+  if (s != P2S_OK) return s;
+  if (!zernike_field || !out) return P2S_ERR_INVALID_ARG;
+  const size_t HW = (size_t)im.H * im.W, n_out = (size_t)im.B * im.C * HW;
+  if (overlaps(out, n_out * 4, im.data, n_out * 4) ||
+      overlaps(out, n_out * 4, zernike_field, n_out * h->n_in * 4) ||
+      overlaps(out, n_out * 4, tilt_field, (size_t)im.B * 2 * HW * 4))
+    return P2S_ERR_INVALID_ARG;
+  cudaStream_t st = (cudaStream_t)stream;
+  s = ensure_J(h, n_out);
+  if (s != P2S_OK) return s;
+  FusedParams p = make_params(h, im.B, im.C, im.H, im.W, 0);
+  p.nfr = im.C;  // per tile: the C channels' convolutions once, then one MLP + J pass per channel
+  p.color = 1;
+  p.image = im.data;
+  p.zernike = zernike_field;
+  p.J = h->d_J;
+  if (h->ev_begin) P2S_CUDA(cudaEventRecord(h->ev_begin, st));
+  s = launch_fused(h, p, st);
+  if (s != P2S_OK) return s;
+  if (h->ev_end) P2S_CUDA(cudaEventRecord(h->ev_end, st));
+  return launch_warp(h, h->d_J, tilt_field, out, im.B, im.C, im.H, im.W, st);
+}
+
 p2s_status p2s_backward(p2s_handle* h, p2s_image im, const float* zernike_field, const float* tilt_field,
                         const float* grad_out, float* grad_beta, float* grad_tilt, float* grad_image,
                         p2s_stream_t stream) {

@@ -119,6 +119,8 @@ struct FusedParams {
   int n_items_full, n_items_beta, n_items_first, n_items_seq, n_items_conv;
   int nfr;                    // frames per tile: 1, or a sequence's length (sequence mode: frames
                               // share the image, so each tile's convolutions serve all of them)
+  int color;                  // colour mode (per-channel beta): nfr = C passes per tile, pass c
+                              // uses Zernike frame b C + c and writes J channel c only
   int tab_cap;                // entries of the shared-memory item tables
   int off_mma, off_steps;     // byte offsets of the MmaItem and conv-step tables
   MlpOp ops[kMaxOps];         // [0, n_ops): per-tile ops; then n_fops whole-layer L1/L2 ops
@@ -383,34 +385,55 @@ __device__ __forceinline__ void adj_u_epi(uint32_t tl, int scr_col, int Nk, int 
     gj[c] = (st && real) ? __ldg(gJ + c * HW) : 0.f;
     gsum += gj[c];
   }
+  const float4* b34 = reinterpret_cast<const float4*>(consts);
+  const float4* sv4 = reinterpret_cast<const float4*>(consts + 128);
   for (int gi = wg; gi < GK; gi += 2) {
-    float bv[16], av[NC][16];
+    float bv[16], av[NC][16], sv[16];
     tmem_ld16(tl + scr_col + gi * 16, bv);
 #pragma unroll
     for (int c = 0; c < NC; ++c) tmem_ld16(tl + c * Nk + gi * 16, av[c]);
+#pragma unroll
+    for (int i4 = 0; i4 < 4; ++i4) {  // tap sums (and b3) for the 16 columns, zero past K
+      const float4 s4 = __ldg(sv4 + gi * 4 + i4);
+      sv[4 * i4] = s4.x; sv[4 * i4 + 1] = s4.y; sv[4 * i4 + 2] = s4.z; sv[4 * i4 + 3] = s4.w;
+    }
     tmem_ld_wait();
-    if (st)
+    if (!b3_folded) {
+#pragma unroll
+      for (int i4 = 0; i4 < 4; ++i4) {
+        const float4 b4 = __ldg(b34 + gi * 4 + i4);
+        bv[4 * i4] += b4.x; bv[4 * i4 + 1] += b4.y; bv[4 * i4 + 2] += b4.z; bv[4 * i4 + 3] += b4.w;
+      }
+    }
+    // J parts: the columns past K carry beta = 0 and s = 0 (zero-padded weights and tables)
+#pragma unroll
+    for (int i = 0; i < 16; ++i) {
+      bs = fmaf(bv[i], sv[i], bs);
+#pragma unroll
+      for (int c = 0; c < NC; ++c) jc[c] = fmaf(bv[i], av[c][i], jc[c]);
+    }
+    if (st && u) {
 #pragma unroll
       for (int i = 0; i < 16; ++i) {
         const int k = gi * 16 + i;
         if (k < K) {
-          const float beta = bv[i] + (b3_folded ? 0.f : __ldg(consts + k));
-          const float sk = __ldg(consts + 128 + k);
-          bs = fmaf(beta, sk, bs);
 #pragma unroll
-          for (int c = 0; c < NC; ++c) jc[c] = fmaf(beta, av[c][i], jc[c]);
-          if (u) {
-#pragma unroll
-            for (int c = 0; c < NC; ++c) u[((size_t)c * K + k) * plane] = __float2half_rn(beta * gj[c]);
-          }
-          if (dbeta && real) {
-            float v = 0.5f * sk * gsum;
-#pragma unroll
-            for (int c = 0; c < NC; ++c) v = fmaf(gj[c], av[c][i], v);
-            dbeta[(size_t)k * HW] = v;
-          }
+          for (int c = 0; c < NC; ++c) u[((size_t)c * K + k) * plane] = __float2half_rn(bv[i] * gj[c]);
         }
       }
+    }
+    if (st && real && dbeta) {
+#pragma unroll
+      for (int i = 0; i < 16; ++i) {
+        const int k = gi * 16 + i;
+        if (k < K) {
+          float v = 0.5f * sv[i] * gsum;
+#pragma unroll
+          for (int c = 0; c < NC; ++c) v = fmaf(gj[c], av[c][i], v);
+          dbeta[(size_t)k * HW] = v;
+        }
+      }
+    }
   }
 }
 
@@ -800,7 +823,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads)
       int b, y, x0;
       tile_coords(p, t, b, y, x0);
       if (pmode != 2) {  // (mode 2, the adjoint, needs only the E views)
-        // --- A1 of frame b + fr (sequence mode: every frame of the image's sequence): row m =
+        // --- A1 of Zernike frame b nfr + fr (sequence mode: b = 0; colour mode: channel fr): row m =
         //     pixel x0+m, k = Zernike index (zero-padded to K1)
         { PROF_T0(); WAIT_BUILD(&bars[BAR_A1_EMPTY], (a1_builds & 1) ^ 1); PROF_ADD(9); }
         ++a1_builds;
@@ -809,7 +832,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads)
           const int x = min(x0 + m, p.W - 1);
           uint8_t* dst = sA1 + (m & 7) * 16 + (m >> 3) * p.a1_sbo;
           if constexpr (!kAnchors) {
-            const float* zp = p.zernike + (size_t)(b + fr) * p.n_in * HW + (size_t)y * p.W + x;
+            const float* zp = p.zernike + (size_t)(b * nfr + fr) * p.n_in * HW + (size_t)y * p.W + x;
             for (int k0 = 0; k0 < p.K1; k0 += 16) {
               float v[16];
   #pragma unroll
@@ -820,7 +843,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads)
               *reinterpret_cast<uint4*>(dst + ((k0 >> 3) + 1) * 128) = pack8(v + 8);
             }
           } else {
-            build_A1_anchors(p, dst, b + fr, y, x0, x, tid, smem);
+            build_A1_anchors(p, dst, b * nfr + fr, y, x0, x, tid, smem);
           }
         }
         fence_proxy_async_smem();
@@ -1050,9 +1073,13 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads)
           bs += o.w;
           jc[0] += o.x; jc[1] += o.y; jc[2] += o.z;
           if (store && x < p.W) {
+            // sequence mode: frame b + fr, every channel; colour mode (per-channel beta): frame b,
+            // channel fr only (the pass of channel fr's Zernike field)
+            const int c0 = p.color ? fr : 0, c1 = p.color ? fr + 1 : C;
+            float* jo = p.J + (p.color ? ((size_t)b * C + fr) : (size_t)(b + fr) * C) * HW + (size_t)y * p.W + x;
 #pragma unroll
             for (int c = 0; c < 3; ++c)
-              if (c < C) p.J[((size_t)(b + fr) * C + c) * HW + (size_t)y * p.W + x] = fmaf(0.5f, bs, jc[c]);
+              if (c >= c0 && c < c1) jo[(size_t)(c - c0) * HW] = fmaf(0.5f, bs, jc[c]);
           }
         }
       }

@@ -27,7 +27,7 @@ EXPORTED = ("p2s_init", "p2s_render", "p2s_render_host", "p2s_reserve", "p2s_set
             "p2s_debug_beta", "p2s_debug_blur", "p2s_debug_profile_buffer",
             "p2s_render_anchors", "p2s_render_anchors_host", "p2s_debug_blur_anchors",
             "p2s_render_sequence", "p2s_sampler_init", "p2s_sample_anchors", "p2s_sampler_destroy",
-            "p2s_backward")
+            "p2s_backward", "p2s_render_color")
 
 
 class P2SError(RuntimeError):
@@ -99,11 +99,13 @@ def load_library(path: str = LIB_PATH) -> ctypes.CDLL:
     lib.p2s_sample_anchors.argtypes = [v, ctypes.c_ulonglong, i, i, v, v]
     lib.p2s_sampler_destroy.argtypes = [v]
     lib.p2s_backward.argtypes = [v, _Image, v, v, v, v, v, v, v]
+    lib.p2s_render_color.argtypes = [v, _Image, v, v, v, v]
     lib.p2s_sampler_destroy.restype = None
     for name in ("p2s_init", "p2s_render", "p2s_render_host", "p2s_reserve", "p2s_set_profile_events",
                  "p2s_get_info", "p2s_debug_beta", "p2s_debug_blur", "p2s_debug_profile_buffer",
                  "p2s_render_anchors", "p2s_render_anchors_host", "p2s_debug_blur_anchors",
-                 "p2s_render_sequence", "p2s_sampler_init", "p2s_sample_anchors", "p2s_backward"):
+                 "p2s_render_sequence", "p2s_sampler_init", "p2s_sample_anchors", "p2s_backward",
+                 "p2s_render_color"):
         getattr(lib, name).restype = st
     _lib = lib
     return lib
@@ -222,6 +224,19 @@ class Renderer:
             out = torch.empty_like(image)
         _check(self._lib.p2s_render_anchors(self._h, im, ap, G, tp, _dev_ptr(out, "out", (B, C, H, W)),
                                             _stream_handle(stream)), "p2s_render_anchors")
+        return out
+
+    def render_color(self, image, zernike, tilt=None, out=None, stream=None):
+        """p2s_render_color: per-channel Zernike fields zernike [B,C,n_in,H,W]."""
+        import torch
+        B, C, H, W = image.shape
+        im = _Image(_dev_ptr(image, "image").value, B, C, H, W)
+        zp = _dev_ptr(zernike, "zernike_field", (B, C, self.n_in, H, W))
+        tp = _dev_ptr(tilt, "tilt_field", (B, 2, H, W)) if tilt is not None else ctypes.c_void_p()
+        if out is None:
+            out = torch.empty_like(image)
+        _check(self._lib.p2s_render_color(self._h, im, zp, tp, _dev_ptr(out, "out", (B, C, H, W)),
+                                          _stream_handle(stream)), "p2s_render_color")
         return out
 
     def render_sequence(self, image, zernike, tilt=None, out=None, stream=None):

@@ -143,6 +143,20 @@ def make_anchors(spec: Spec, G: int, frames: Optional[range] = None) -> np.ndarr
                      for f in frames])
 
 
+WAVELENGTHS_NM = (570.0, 540.0, 450.0)  # R, G, B as in PAPER.md:318 ("450nm, 540nm, and 570nm")
+
+
+def make_zernike_color(spec: Spec, frames: Optional[range] = None, ref_nm: float = 540.0) -> np.ndarray:
+    """Per-channel Zernike fields [B][C][n_in][H][W] fp32 for the colour mode: the
+    frame's field (make_zernike, defined at ref_nm) seen at each channel's wavelength -- a phase
+    aberration in radians scales as 1/lambda, so z_c = z * ref_nm / lambda_c (C = 3: R, G, B at
+    570, 540, 450 nm; other C: wavelengths spread evenly over 450..570 nm)."""
+    frames = range(spec.B) if frames is None else frames
+    lam = WAVELENGTHS_NM if spec.C == 3 else tuple(np.linspace(570.0, 450.0, spec.C))
+    return np.stack([np.stack([make_zernike(spec, f) * np.float32(ref_nm / l) for l in lam])
+                     for f in frames]).astype(np.float32)
+
+
 def make_upstream_grad(spec: Spec, frames: Optional[range] = None) -> np.ndarray:
     """dL/dout [B][C][H][W] fp32 for the adjoint: i.i.d. U(-1, 1), the gradient of
     a loss on the rendered frames (no structure assumed)."""

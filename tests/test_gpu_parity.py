@@ -562,3 +562,52 @@ def test_backward_invalid_args(p2s):
                  (vp(), vp(), vp(g.data_ptr()), vp(buf.data_ptr()), vp()),             # no zernike
                  (vp(z.data_ptr()), vp(), vp(), vp(buf.data_ptr()), vp())):            # no grad_out
         assert r._lib.p2s_backward(r._h, im, *args, vp(), vp()) == p2s.P2S_ERR_INVALID_ARG
+
+
+# ---- wavelength-dependent colour: per-channel Zernike fields -> per-channel
+#      beta, vs oracle.render_color (each channel rendered alone with its own field)
+
+COLOR_CASES = ["ragged_rgb_S7", "S33_K100_C2", "many_tiles_C2", "S65_K100_h256", "W1_H1", "many_tiles_C1_S9"]
+
+
+@pytest.mark.parametrize("name", COLOR_CASES)
+def test_render_color_parity(p2s, name):
+    spec = SMALL[name]
+    inp = synth.make_inputs(spec)
+    zc = synth.make_zernike_color(spec)
+    r = p2s.Renderer(inp.basis, inp.mlp)
+    out = r.render_color(_dev(inp.image), _dev(zc), _dev(inp.tilt)).cpu().numpy()
+    ref, _ = oracle.render_color(inp.image, zc, inp.tilt, inp.basis, inp.mlp)
+    _cmp(out, ref, f"render_color[{name}]", norm_ref=inp.image if name in REL_TO_INPUT else None)
+    r.close()
+
+
+@pytest.mark.parametrize("name", ["ragged_rgb_S7", "S33_K100_C2"])
+def test_render_color_equal_fields_is_render(p2s, name):
+    """Every channel given the frame's one field: bit for bit p2s_render (same beta, same sums)."""
+    spec = SMALL[name]
+    inp = synth.make_inputs(spec)
+    same = np.ascontiguousarray(np.repeat(inp.zernike[:, None], spec.C, axis=1))
+    r = p2s.Renderer(inp.basis, inp.mlp)
+    a = r.render_color(_dev(inp.image), _dev(same), _dev(inp.tilt)).cpu().numpy()
+    b = r.render(_dev(inp.image), _dev(inp.zernike), _dev(inp.tilt)).cpu().numpy()
+    np.testing.assert_array_equal(a, b)
+
+
+def test_render_color_cfg3_sampled(p2s):
+    """Bench-size frames (512x512 RGB, K=100, 33x33), 2 frames, sampled pixels per channel."""
+    spec = synth.CONFIGS[3]
+    inp = synth.make_inputs(spec, frames=range(2))
+    zc = synth.make_zernike_color(spec, frames=range(2))
+    r = p2s.Renderer(inp.basis, inp.mlp)
+    out = r.render_color(_dev(inp.image), _dev(zc), _dev(inp.tilt)).cpu().numpy()
+    B, C, H, W = inp.image.shape
+    rng = np.random.default_rng(13)
+    n = 128
+    bxy = np.stack([rng.integers(0, B, n), rng.integers(0, H, n), rng.integers(0, W, n)], 1)
+    edge = [[0, 0, 0], [B - 1, H - 1, W - 1], [0, H // 2, 127], [1, H // 2, 128]]
+    bxy = np.concatenate([np.array(edge), bxy]).astype(np.int32)
+    for c in range(C):
+        _, oref = oracle.pixels(np.ascontiguousarray(inp.image[:, c:c + 1]), np.ascontiguousarray(zc[:, c]),
+                                inp.tilt, inp.basis, inp.mlp, bxy)
+        _cmp(out[bxy[:, 0], c, bxy[:, 1], bxy[:, 2]], oref[:, 0], f"render_color[cfg3 sampled, c={c}]")

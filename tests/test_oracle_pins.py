@@ -542,3 +542,23 @@ def test_adjoint_image_dot_product_and_sampled_form():
         at = adjoint.grad_image_at(beta, basis, gJ, yx)
         ys, xs = np.array(yx).T
         np.testing.assert_allclose(at, gI[:, ys, xs].T, rtol=0, atol=1e-11)
+
+
+# ---- wavelength-dependent colour
+
+def test_render_color_reduces_to_shared_beta():
+    """One Zernike field for every channel (the paper's 'simulate the RGB channels identically',
+    P:320, reading A13) makes render_color == render exactly; and channel c of render_color
+    depends only on channel c's field (swapping another channel's field leaves it unchanged)."""
+    spec = synth.custom("col", 501, B=2, C=3, H=7, W=9, K=5, S=5, h1=16, h2=16, t_std=1.2)
+    inp = synth.make_inputs(spec)
+    same = np.repeat(inp.zernike[:, None], 3, axis=1)
+    o1, J1 = oracle.render_color(inp.image, same, inp.tilt, inp.basis, inp.mlp, want_blur=True)
+    o0, J0 = oracle.render(inp.image, inp.zernike, inp.tilt, inp.basis, inp.mlp, want_blur=True)
+    np.testing.assert_array_equal(o1, o0)
+    np.testing.assert_array_equal(J1, J0)
+    other = same.copy()
+    other[:, 2] = 1.7 * same[:, 2] + 0.3
+    o2, _ = oracle.render_color(inp.image, other, inp.tilt, inp.basis, inp.mlp)
+    np.testing.assert_array_equal(o2[:, :2], o0[:, :2])
+    assert np.abs(o2[:, 2] - o0[:, 2]).max() > 1e-3
