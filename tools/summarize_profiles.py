@@ -77,3 +77,34 @@ json.dump({"dram_bytes_per_launch": dram, "source": f"profiles/{tag}_ncu_fused.t
 print(open(os.path.join(PROF, f"{tag}_launch_shares.txt")).read())
 print("\n".join(lines))
 print("dram bytes/launch", dram)
+
+# ---- the adjoint: launch list of one p2s_backward (all three gradients) and one
+#      --set full capture of k_adjoint_image (tools/ncu_adjoint_run.sh)
+adj_csv = os.path.join(OUT, "adj_launches.csv")
+adj_rep = os.path.join(OUT, "prof_adjoint.ncu-rep")
+if os.path.exists(adj_csv) and os.path.exists(adj_rep):
+    rows = list(csv.reader(open(adj_csv)))
+    start = next(i for i, r in enumerate(rows) if r and r[0] == "ID")
+    hdr = rows[start]
+    ki, vi = hdr.index("Kernel Name"), hdr.index("Metric Value")
+    seq = [(r[ki].split("(")[0], float(r[vi].replace(",", ""))) for r in rows[start + 1:]]
+    # the last p2s_backward call of the run (warm-up calls precede it): its kernels in order
+    last = seq[-4:]  # dL/dJ scatter, fused pass (J, dL/dbeta, U), dL/dt, k_adjoint_image
+    raw = subprocess.run(["ncu", "-i", adj_rep, "--page", "raw", "--csv"], capture_output=True, text=True).stdout
+    rr = list(csv.reader(raw.splitlines()))
+    m = {a: (c, b) for a, b, c in zip(rr[0], rr[1], rr[2])}
+    want = ["gpu__time_duration.sum", "sm__cycles_elapsed.avg.per_second", "dram__bytes_read.sum",
+            "dram__bytes_write.sum", "lts__t_bytes.sum", "lts__throughput.avg.pct_of_peak_sustained_elapsed",
+            "sm__pipe_tensor_cycles_active.avg.pct_of_peak_sustained_elapsed", "launch__grid_size",
+            "launch__cluster_dim_x", "launch__registers_per_thread", "launch__shared_mem_per_block_dynamic"]
+    with open(os.path.join(PROF, f"{tag}_ncu_adjoint.txt"), "w") as f:
+        f.write("adjoint (p2s_backward, all three gradients, cfg3): ncu --metrics gpu__time_duration.sum "
+                "--clock-control none (cold-cache, serialised); last call's launches:\n")
+        for name, ns in last:
+            f.write(f"  {ns / 1e3:9.1f} us  {name}\n")
+        f.write("\nncu --set full --clock-control none -k regex:k_adjoint_image -c 1 (dL/dI of one cfg3 frame)\n\n")
+        for k in want:
+            if k in m:
+                f.write(f"{k:80s} {m[k][0]:>16s} {m[k][1]}\n")
+    shutil.copy(adj_csv, os.path.join(PROF, f"{tag}_adjoint_launches.csv"))
+    print(open(os.path.join(PROF, f"{tag}_ncu_adjoint.txt")).read())
