@@ -417,9 +417,11 @@ p2s_status p2s_init(const p2s_basis* basis, const p2s_mlp* mlp, p2s_handle** out
     if (h->n_ebuf < 1) h->n_ebuf = 1;
     ring_avail = kSmemLimit - fixed - al(h->n_ebuf * e1_bytes) - 1024;
     // prefer 3 large stages (fewer ring transitions for the UMMA issuer), else 4, else 2
+    // (P2S_NRING overrides the stage count for tuning experiments)
     nring = 3;
-    sb = std::min(32768, (ring_avail / 3) / 128 * 128);
-    if (sb < 16384) {
+    if (const char* e = std::getenv("P2S_NRING")) nring = std::max(2, std::min(8, std::atoi(e)));
+    sb = std::min(32768, (ring_avail / nring) / 128 * 128);
+    if (sb < 16384 && !std::getenv("P2S_NRING")) {
       nring = 4;
       sb = std::min(32768, (ring_avail / 4) / 128 * 128);
       if (sb < 12288) { nring = 2; sb = std::min(32768, (ring_avail / 2) / 128 * 128); }

@@ -26,7 +26,7 @@ hdr = rows[start]
 ki, vi = hdr.index("Kernel Name"), hdr.index("Metric Value")
 tot, cnt = defaultdict(float), defaultdict(int)
 for r in rows[start + 1:]:
-    name = r[ki].split("(")[0].split("<")[0]  # (template instantiations folded)
+    name = r[ki].split("(")[0].split("<")[0].removeprefix("void ")  # (template instantiations folded)
     tot[name] += float(r[vi].replace(",", ""))
     cnt[name] += 1
 shutil.copy(os.path.join(OUT, "launches.csv"), os.path.join(PROF, f"{tag}_launches.csv"))
