@@ -410,7 +410,8 @@ p2s_status p2s_init(const p2s_basis* basis, const p2s_mlp* mlp, p2s_handle** out
     const int fixed = al(a1_bytes) + al(a2_bytes) + al(hold_bytes) + al(tab_all) + al(const_bytes) +
                       (red_in_hold ? 0 : al(red_bytes)) + al(bar_bytes) + al(anc_bytes);
     int ring_avail = 0;
-    for (h->n_ebuf = 2; h->n_ebuf >= 1; --h->n_ebuf) {
+    const int ebuf_max = std::getenv("P2S_NEBUF") ? std::max(1, std::min(2, std::atoi(std::getenv("P2S_NEBUF")))) : 2;
+    for (h->n_ebuf = ebuf_max; h->n_ebuf >= 1; --h->n_ebuf) {
       ring_avail = kSmemLimit - fixed - al(h->n_ebuf * e1_bytes) - 1024;
       if (ring_avail >= 3 * 12288) break;
     }
