@@ -611,3 +611,51 @@ def test_render_color_cfg3_sampled(p2s):
         _, oref = oracle.pixels(np.ascontiguousarray(inp.image[:, c:c + 1]), np.ascontiguousarray(zc[:, c]),
                                 inp.tilt, inp.basis, inp.mlp, bxy)
         _cmp(out[bxy[:, 0], c, bxy[:, 1], bxy[:, 2]], oref[:, 0], f"render_color[cfg3 sampled, c={c}]")
+
+
+# ---- guard bands: every output written through the C ABI lands in the middle of a larger buffer
+#      whose margins hold a sentinel; no entry point may touch them (out-of-bounds write check)
+
+def _guarded(shape, pad=4096):
+    n = int(np.prod(shape))
+    buf = torch.full((n + 2 * pad,), 12345.0, dtype=torch.float32, device="cuda")
+    return buf, buf[pad:pad + n].view(*shape), pad
+
+
+def _margins_ok(buf, pad):
+    b = buf.cpu().numpy()
+    return bool(np.all(b[:pad] == 12345.0) and np.all(b[-pad:] == 12345.0))
+
+
+@pytest.mark.parametrize("name", ["ragged_rgb_S7", "S33_K100_C2", "W1_H1", "S65_K100_h256"])
+def test_outputs_stay_in_bounds(p2s, name):
+    spec = SMALL[name]
+    inp = synth.make_inputs(spec)
+    B, C, H, W = inp.image.shape
+    r = p2s.Renderer(inp.basis, inp.mlp)
+    img, z, t = _dev(inp.image), _dev(inp.zernike), _dev(inp.tilt)
+    vp = ctypes.c_void_p
+    im = p2s._Image(img.data_ptr(), B, C, H, W)
+    checks = []
+    buf, out, pad = _guarded((B, C, H, W))
+    r.render(img, z, t, out=out)
+    checks.append(("render", buf, pad))
+    buf2, out2, pad2 = _guarded((B, C, H, W))
+    r.render_color(img, _dev(synth.make_zernike_color(spec)), t, out=out2)
+    checks.append(("render_color", buf2, pad2))
+    gb_buf, gb, pb = _guarded((B, spec.K, H, W))
+    gt_buf, gt, pt = _guarded((B, 2, H, W))
+    gi_buf, gi, pi = _guarded((B, C, H, W))
+    g = _dev(synth.make_upstream_grad(spec))
+    st = r._lib.p2s_backward(r._h, im, vp(z.data_ptr()), vp(t.data_ptr()), vp(g.data_ptr()), vp(gb.data_ptr()),
+                             vp(gt.data_ptr()), vp(gi.data_ptr()), vp())
+    assert st == p2s.P2S_OK
+    checks += [("dL/dbeta", gb_buf, pb), ("dL/dt", gt_buf, pt), ("dL/dI", gi_buf, pi)]
+    bb, beta, pbb = _guarded((B, spec.K, H, W))
+    r.debug_beta(z, out=beta)
+    checks.append(("debug_beta", bb, pbb))
+    torch.cuda.synchronize()
+    for what, b, p in checks:
+        assert _margins_ok(b, p), f"{what} wrote outside its buffer"
+        inner = b[p:-p].cpu().numpy()
+        assert np.all(np.isfinite(inner)), f"{what}: non-finite values"
