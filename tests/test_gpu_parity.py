@@ -659,3 +659,51 @@ def test_outputs_stay_in_bounds(p2s, name):
         assert _margins_ok(b, p), f"{what} wrote outside its buffer"
         inner = b[p:-p].cpu().numpy()
         assert np.all(np.isfinite(inner)), f"{what}: non-finite values"
+
+
+def test_empty_and_out_of_envelope_dims(p2s):
+    """Zero-sized frames are argument errors, C > 3 is outside the envelope (include/p2s.h)."""
+    inp = synth.make_inputs(SMALL["ragged_rgb_S7"])
+    r = p2s.Renderer(inp.basis, inp.mlp)
+    img, z = _dev(inp.image), _dev(inp.zernike)
+    out = torch.empty_like(img)
+    vp = ctypes.c_void_p
+    B, C, H, W = inp.image.shape
+    for dims, want in (((0, C, H, W), p2s.P2S_ERR_INVALID_ARG), ((B, C, 0, W), p2s.P2S_ERR_INVALID_ARG),
+                       ((B, C, H, 0), p2s.P2S_ERR_INVALID_ARG), ((B, 0, H, W), p2s.P2S_ERR_INVALID_ARG),
+                       ((1, 4, H, W), p2s.P2S_ERR_UNSUPPORTED)):
+        im = p2s._Image(img.data_ptr(), *dims)
+        assert r._lib.p2s_render(r._h, im, vp(z.data_ptr()), vp(), vp(out.data_ptr()), vp()) == want, dims
+        assert r._lib.p2s_render_color(r._h, im, vp(z.data_ptr()), vp(), vp(out.data_ptr()), vp()) == want, dims
+
+
+def test_full_envelope_at_once(p2s):
+    """K = 128, S = 65, h1 = h2 = 256, n_in = 48 together: renders within the bar or is refused
+    as UNSUPPORTED at init (never a wrong frame)."""
+    spec = synth.custom("envmax", 213, B=1, C=3, H=10, W=140, K=128, S=65, n_in=48, h1=256, h2=256, t_std=2.0)
+    inp = synth.make_inputs(spec)
+    try:
+        r = p2s.Renderer(inp.basis, inp.mlp)
+    except p2s.P2SError as e:
+        assert e.status == p2s.P2S_ERR_UNSUPPORTED
+        pytest.skip("envelope corner refused at init (UNSUPPORTED)")
+    out = r.render(_dev(inp.image), _dev(inp.zernike), _dev(inp.tilt)).cpu().numpy()
+    ref, _ = oracle.render(inp.image, inp.zernike, inp.tilt, inp.basis, inp.mlp)
+    _cmp(out, ref, "render[envelope corner]")
+
+
+def test_large_ragged_frame_sampled(p2s):
+    """A 2048 x 2000 RGB frame (K = 100, 33 x 33): 64-bit index paths, a ragged last strip,
+    sampled pixels against the oracle."""
+    spec = synth.custom("big", 214, B=1, C=3, H=2048, W=2000, K=100, S=33, h1=200, h2=200, t_std=2.0)
+    inp = synth.make_inputs(spec)
+    r = p2s.Renderer(inp.basis, inp.mlp)
+    out = r.render(_dev(inp.image), _dev(inp.zernike), _dev(inp.tilt)).cpu().numpy()
+    B, C, H, W = inp.image.shape
+    rng = np.random.default_rng(17)
+    n = 160
+    bxy = np.stack([np.zeros(n, int), rng.integers(0, H, n), rng.integers(0, W, n)], 1)
+    edge = [[0, 0, 0], [0, H - 1, W - 1], [0, H - 1, 1919], [0, H - 1, 1920], [0, 1024, 1999], [0, 2047, 0]]
+    bxy = np.concatenate([np.array(edge), bxy]).astype(np.int32)
+    _, oref = oracle.pixels(inp.image, inp.zernike, inp.tilt, inp.basis, inp.mlp, bxy)
+    _cmp(out[bxy[:, 0], :, bxy[:, 1], bxy[:, 2]], oref, "render[2048x2000 sampled]")
