@@ -1,6 +1,7 @@
 """Per-item UMMA issue timeline of leader CTA 0 (needs a -DP2S_PROFILE build).
 
 Usage: P2S_LIB=paper_2107_11627_b200/libp2s_prof.so python tools/mma_trace.py [cfg] [first] [count]
+(TRACE_SEQ=F traces a p2s_render_sequence of F frames; TRACE_H=h a frame of h rows)
 Columns: item, kind (conv/mlp + flags), slabs, N, start (cycles since kernel entry), wait cycles,
 issue cycles (waits end -> commits done), cycles since the previous item start, and the ideal
 tensor time of that item (56 cyc per M=256 N=112 UMMA, scaled by N).
@@ -21,15 +22,25 @@ spec = synth.CONFIGS[cfg]
 if os.environ.get("TRACE_H"):  # e.g. TRACE_H=16: one tile per CTA (launch-latency view)
     spec = synth.custom("h", cfg, B=1, C=spec.C, H=int(os.environ["TRACE_H"]), W=spec.W, K=spec.K, S=spec.S,
                         h1=spec.h1, h2=spec.h2)
-inp = synth.make_inputs(spec, frames=range(1))
+SEQ = int(os.environ.get("TRACE_SEQ", "0"))  # > 0: a p2s_render_sequence of SEQ frames instead
+inp = synth.make_inputs(spec, frames=range(max(1, SEQ)))
 r = p2s.Renderer(inp.basis, inp.mlp)
-img, z, t = (torch.from_numpy(a).cuda() for a in (inp.image, inp.zernike, inp.tilt))
-out = torch.empty_like(img)
+img, z, t = (torch.from_numpy(np.ascontiguousarray(a)).cuda() for a in (inp.image[:1], inp.zernike, inp.tilt))
+out = torch.empty((max(1, SEQ),) + tuple(img.shape[1:]), device="cuda")
+
+
+def call():
+    if SEQ:
+        r.render_sequence(img, z, t, out=out)
+    else:
+        r.render(img, z, t, out=out)
+
+
 for _ in range(3):
-    r.render(img, z, t, out=out)
+    call()
 buf = torch.zeros(148 * 4 * 20 + 4 * 256, dtype=torch.int64, device="cuda")
 r.debug_profile_buffer(buf)
-r.render(img, z, t, out=out)
+call()
 torch.cuda.synchronize()
 r.debug_profile_buffer(None)
 tr = buf[148 * 4 * 20:].view(256, 4).cpu().numpy().astype(np.int64)
