@@ -192,3 +192,35 @@ def backward_at(image, beta, tilt, basis, g, yx, coord_dtype=np.float64):
         gt[n, 0] = -(g[:, y, x] @ dsx) if in_x[y, x] else 0.0
         gt[n, 1] = -(g[:, y, x] @ dsy) if in_y[y, x] else 0.0
     return gbeta, gt
+
+
+def _f16(a):
+    return np.asarray(a, np.float32).astype(np.float16).astype(np.float64)
+
+
+def mlp_backward(zernike, gbeta, mlp, mask_precision="fp64"):
+    """dL/dz [n_in][H][W] (fp64) of one frame through the P2S MLP (step a1, PAPER.md:280-283,
+    reading A11: ReLU after layers 1-2, linear output), for dL/dbeta [K][H][W]:
+
+        pre1 = W1 z + b1,  a1 = ReLU(pre1),  pre2 = W2 a1 + b2,  (beta = W3 ReLU(pre2) + b3)
+        g2 = (W3^T dL/dbeta) [pre2 > 0],  g1 = (W2^T g2) [pre1 > 0],  dL/dz = W1^T g1
+
+    The masks are integers decided by floats: mask_precision="fp16" decides them the way the GPU
+    does (fp16-rounded z, weights and a1; reading N5), "fp64" from exact values (the
+    finite-difference pins). The gradient values are fp64 either way."""
+    z = np.asarray(zernike, np.float64)
+    n_in, H, W = z.shape
+    Z = z.reshape(n_in, -1)
+    G3 = np.asarray(gbeta, np.float64).reshape(gbeta.shape[0], -1)
+    W1, W2, W3 = (np.asarray(mlp[k], np.float64) for k in ("W1", "W2", "W3"))
+    b1, b2 = (np.asarray(mlp[k], np.float64) for k in ("b1", "b2"))
+    if mask_precision == "fp16":
+        pre1 = _f16(mlp["W1"]) @ _f16(Z.T.astype(np.float32)).T + b1[:, None]
+        a1 = np.maximum(pre1, 0.0)
+        pre2 = _f16(mlp["W2"]) @ _f16(a1.astype(np.float32)) + b2[:, None]
+    else:
+        pre1 = W1 @ Z + b1[:, None]
+        pre2 = W2 @ np.maximum(pre1, 0.0) + b2[:, None]
+    g2 = (W3.T @ G3) * (pre2 > 0)
+    g1 = (W2.T @ g2) * (pre1 > 0)
+    return (W1.T @ g1).reshape(n_in, H, W)

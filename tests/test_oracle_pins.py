@@ -562,3 +562,25 @@ def test_render_color_reduces_to_shared_beta():
     o2, _ = oracle.render_color(inp.image, other, inp.tilt, inp.basis, inp.mlp)
     np.testing.assert_array_equal(o2[:, :2], o0[:, :2])
     assert np.abs(o2[:, 2] - o0[:, 2]).max() > 1e-3
+
+
+def test_mlp_backward_matches_finite_differences():
+    """dL/dz through the P2S MLP: central differences of the C oracle's beta (an independent
+    forward) for L = <g, beta(z)>; and the fp16-mask form equals the exact one when no
+    pre-activation is near zero (checked on this input)."""
+    from oracle import adjoint
+    spec = synth.custom("mlpb", 402, B=1, C=1, H=3, W=4, K=6, S=3, h1=12, h2=10)
+    inp = synth.make_inputs(spec)
+    z = inp.zernike.astype(np.float64)
+    g = np.random.default_rng(3).standard_normal((6, 3, 4))
+    dz = adjoint.mlp_backward(z[0], g, inp.mlp)
+    loss = lambda zz: np.sum(g * oracle.beta(inp.image, zz.astype(np.float32), inp.basis, inp.mlp)[0])  # noqa: E731
+    rng = np.random.default_rng(4)
+    for _ in range(10):
+        i, y, x = rng.integers(0, z.shape[1]), rng.integers(0, 3), rng.integers(0, 4)
+        e = np.zeros_like(z)
+        e[0, i, y, x] = 1e-2   # fp32 inputs to the oracle: a step well above their rounding
+        fd = (loss(z + e) - loss(z - e)) / 2e-2
+        assert abs(fd - dz[i, y, x]) < 1e-4 * (1 + abs(dz[i, y, x])), (fd, dz[i, y, x])
+    # masks decided in fp16 agree here (no pre-activation within rounding of 0)
+    np.testing.assert_allclose(adjoint.mlp_backward(z[0], g, inp.mlp, "fp16"), dz, rtol=0, atol=1e-12)
