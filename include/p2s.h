@@ -159,6 +159,22 @@ P2S_API p2s_status p2s_backward(p2s_handle* h, p2s_image image, const float* zer
                                 const float* tilt_field, const float* grad_out, float* grad_beta,
                                 float* grad_tilt, float* grad_image, p2s_stream_t stream);
 
+/* dL/dz through the P2S MLP (the adjoint of step a1; "three fully connected
+ * layers", reading A11: ReLU after layers 1-2, linear output; "differentiable
+ * module"). For the Zernike field zernike_field (DEVICE [B][n_in][H][W] fp32, the p2s_render
+ * input) and grad_beta = dL/dbeta (DEVICE [B][K][H][W] fp32, e.g. p2s_backward's grad_beta), writes
+ *   grad_zernike (DEVICE [B][n_in][H][W] fp32) = W1^T ((W2^T ((W3^T grad_beta) [pre2 > 0])) [pre1 > 0])
+ * per pixel, pre1 = W1 z + b1, pre2 = W2 ReLU(pre1) + b2 (the forward masks are recomputed).
+ * Tensor cores with fp16 operands and fp32 accumulation; grad_beta is scaled per pixel by a power
+ * of two before rounding (any finite range); the masks are decided on the fp16-operand fp32
+ * accumulators (reading N5), so a pre-activation within rounding of 0 may take
+ * either side. Asynchronous on `stream`; no allocation. Errors: NULL pointers, B/H/W < 1 or
+ * grad_zernike overlapping an input -> P2S_ERR_INVALID_ARG; weights that do not fit one SM's
+ * shared memory next to a [128][max width] activation tile (e.g. 33-256-256-100) ->
+ * P2S_ERR_UNSUPPORTED; launch failure -> P2S_ERR_CUDA. */
+P2S_API p2s_status p2s_mlp_backward(p2s_handle* h, const float* zernike_field, const float* grad_beta, int B,
+                                    int H, int W, float* grad_zernike, p2s_stream_t stream);
+
 /* ---- correlated anchor sampling (Sec. 3.4: anchor
  * coefficient sets "drawn from the correlation matrix", which "can be pre-computed") ----
  * Stand-in covariance (reading N3; the paper's Takato-formula parameters are absent):

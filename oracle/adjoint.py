@@ -198,7 +198,25 @@ def _f16(a):
     return np.asarray(a, np.float32).astype(np.float16).astype(np.float64)
 
 
-def mlp_backward(zernike, gbeta, mlp, mask_precision="fp64"):
+def mlp_preactivations(zernike, mlp, mask_precision="fp64"):
+    """(pre1 [h1][H*W], pre2 [h2][H*W]) of one frame's MLP layers 1-2 (reading
+    A11), fp64 values: "fp64" from exact operands; "fp16" from the fp16-rounded z, W1, W2 and a1
+    the GPU multiplies (reading N5), biases exact."""
+    z = np.asarray(zernike, np.float64)
+    Z = z.reshape(z.shape[0], -1)
+    b1, b2 = (np.asarray(mlp[k], np.float64) for k in ("b1", "b2"))
+    if mask_precision == "fp16":
+        pre1 = _f16(mlp["W1"]) @ _f16(Z.T.astype(np.float32)).T + b1[:, None]
+        a1 = np.maximum(pre1, 0.0)
+        pre2 = _f16(mlp["W2"]) @ _f16(a1.astype(np.float32)) + b2[:, None]
+    else:
+        W1, W2 = (np.asarray(mlp[k], np.float64) for k in ("W1", "W2"))
+        pre1 = W1 @ Z + b1[:, None]
+        pre2 = W2 @ np.maximum(pre1, 0.0) + b2[:, None]
+    return pre1, pre2
+
+
+def mlp_backward(zernike, gbeta, mlp, mask_precision="fp64", masks=None):
     """dL/dz [n_in][H][W] (fp64) of one frame through the P2S MLP (step a1, PAPER.md:280-283,
     reading A11: ReLU after layers 1-2, linear output), for dL/dbeta [K][H][W]:
 
@@ -207,20 +225,18 @@ def mlp_backward(zernike, gbeta, mlp, mask_precision="fp64"):
 
     The masks are integers decided by floats: mask_precision="fp16" decides them the way the GPU
     does (fp16-rounded z, weights and a1; reading N5), "fp64" from exact values (the
-    finite-difference pins). The gradient values are fp64 either way."""
+    finite-difference pins); masks=(m1 [h1][H*W], m2 [h2][H*W]) imposes them (the tests' check
+    of the other valid answer where a pre-activation is within rounding of 0). The gradient
+    values are fp64 either way."""
     z = np.asarray(zernike, np.float64)
     n_in, H, W = z.shape
-    Z = z.reshape(n_in, -1)
     G3 = np.asarray(gbeta, np.float64).reshape(gbeta.shape[0], -1)
     W1, W2, W3 = (np.asarray(mlp[k], np.float64) for k in ("W1", "W2", "W3"))
-    b1, b2 = (np.asarray(mlp[k], np.float64) for k in ("b1", "b2"))
-    if mask_precision == "fp16":
-        pre1 = _f16(mlp["W1"]) @ _f16(Z.T.astype(np.float32)).T + b1[:, None]
-        a1 = np.maximum(pre1, 0.0)
-        pre2 = _f16(mlp["W2"]) @ _f16(a1.astype(np.float32)) + b2[:, None]
+    if masks is None:
+        pre1, pre2 = mlp_preactivations(z, mlp, mask_precision)
+        m1, m2 = pre1 > 0, pre2 > 0
     else:
-        pre1 = W1 @ Z + b1[:, None]
-        pre2 = W2 @ np.maximum(pre1, 0.0) + b2[:, None]
-    g2 = (W3.T @ G3) * (pre2 > 0)
-    g1 = (W2.T @ g2) * (pre1 > 0)
+        m1, m2 = masks
+    g2 = (W3.T @ G3) * m2
+    g1 = (W2.T @ g2) * m1
     return (W1.T @ g1).reshape(n_in, H, W)

@@ -16,6 +16,7 @@
 #include "p2s.h"
 #include "p2s_kernels.cuh"
 #include "p2s_adjoint.cuh"
+#include "p2s_mlp_backward.cuh"
 
 using namespace p2s;
 
@@ -125,6 +126,10 @@ struct p2s_handle {
   __half* d_ut = nullptr;
   size_t ut_cap = 0;
   PFN_cuTensorMapEncodeTiled encode = nullptr;
+  // dL/dz (k_mlp_backward): resident weight pack and its shared-memory plan (mb_ok = it fits)
+  uint8_t* d_mlpb = nullptr;
+  int mb_ok = 0, mb_fold = 0, mb_smem = 0, mb_off_w2 = 0, mb_off_w3 = 0, mb_off_bias = 0, mb_wbytes = 0, mb_off_act = 0,
+      mb_off_bar = 0;
   MlpOp ops[kMaxOps];  // [0, n_ops) per-tile ops, then n_fops first-tile whole-layer ops
   int n_ops = 0, n_fops = 0;
   bool bias_folded = false;
@@ -742,6 +747,68 @@ p2s_status p2s_init(const p2s_basis* basis, const p2s_mlp* mlp, p2s_handle** out
       return fail(cuda_fail(e, "cudaFuncSetAttribute(k_adjoint_image)"));
     (void)wpad;
   }
+  {
+    // ---- dL/dz plan (p2s_mlp_backward.cuh): W1 [N1][K1], W2 [N2][N1], W3^T [N2][Nk] as K-major
+    // fp16 tiles + fp32 biases, resident in shared memory with one [128][max K] activation buffer.
+    // MLPs too large for that (e.g. 33-256-256-100) leave mb_ok = 0: p2s_mlp_backward returns
+    // P2S_ERR_UNSUPPORTED for them.
+    const int K1 = h->K1, N1 = h->N1, N2 = h->N2, Nk = h->Nk;
+    const int w1 = N1 * K1 * 2, w2 = N2 * N1 * 2, w3 = N2 * Nk * 2, bb = (N1 + N2) * 4;
+    const int wbytes = w1 + w2 + w3 + bb;
+    const int kact = std::max(std::max(K1, N1), std::max(N2, Nk));
+    const int off_act = (wbytes + 127) / 128 * 128, off_bar = off_act + 128 * kact * 2;
+    const int smem = off_bar + 32 + 4 * 128 * 4;
+    // biases as fp16 hi/lo pairs on constant-1 inputs when each layer input has 2 spare columns
+    const bool fold = h->n_in + 2 <= K1 && h->h1 + 2 <= N1;
+    if (smem <= kSmemLimit && K1 <= 64) {
+      std::vector<uint8_t> pk((size_t)wbytes, 0);
+      __half* hp = reinterpret_cast<__half*>(pk.data());
+      // element (n, k) of a K-major tile [rows][kd]: (n%8)*16 + (n/8)*kd*16 + (k%8)*2 + (k/8)*128 bytes
+      auto at = [](int n, int k, int kd) { return ((n % 8) * 16 + (n / 8) * kd * 16 + (k % 8) * 2 + (k / 8) * 128) / 2; };
+      for (int j = 0; j < h->h1; ++j)
+        for (int i = 0; i < h->n_in; ++i) hp[at(j, i, K1)] = __float2half_rn(mlp->W1[(size_t)j * h->n_in + i]);
+      for (int j = 0; j < h->h2; ++j)
+        for (int i = 0; i < h->h1; ++i) hp[w1 / 2 + at(j, i, N1)] = __float2half_rn(mlp->W2[(size_t)j * h->h1 + i]);
+      for (int j = 0; j < h->h2; ++j)
+        for (int k = 0; k < K; ++k) hp[(w1 + w2) / 2 + at(j, k, Nk)] = __float2half_rn(mlp->W3[(size_t)k * h->h2 + j]);
+      float* bp = reinterpret_cast<float*>(pk.data() + w1 + w2 + w3);
+      for (int j = 0; j < h->h1; ++j) bp[j] = mlp->b1[j];
+      for (int j = 0; j < h->h2; ++j) bp[N1 + j] = mlp->b2[j];
+      if (fold) {
+        // z columns n_in, n_in + 1 are 1: W1 carries b1 there as hi + lo; W1 rows h1, h1 + 1 turn
+        // them into a1 columns h1, h1 + 1 = 1, where W2 carries b2 as hi + lo
+        auto hi = [](float v) { return __float2half_rn(v); };
+        auto lo = [](float v) { return __float2half_rn(v - __half2float(__float2half_rn(v))); };
+        for (int j = 0; j < h->h1; ++j) {
+          hp[at(j, h->n_in, K1)] = hi(mlp->b1[j]);
+          hp[at(j, h->n_in + 1, K1)] = lo(mlp->b1[j]);
+        }
+        hp[at(h->h1, h->n_in, K1)] = __float2half_rn(1.f);
+        hp[at(h->h1 + 1, h->n_in, K1)] = __float2half_rn(1.f);
+        for (int j = 0; j < h->h2; ++j) {
+          hp[w1 / 2 + at(j, h->h1, N1)] = hi(mlp->b2[j]);
+          hp[w1 / 2 + at(j, h->h1 + 1, N1)] = lo(mlp->b2[j]);
+        }
+      }
+      if ((e = cudaMalloc(&h->d_mlpb, pk.size())) != cudaSuccess ||
+          (e = cudaMemcpy(h->d_mlpb, pk.data(), pk.size(), cudaMemcpyHostToDevice)) != cudaSuccess)
+        return fail(cuda_fail(e, "dz weight pack"));
+      if ((e = cudaFuncSetAttribute(k_mlp_backward<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem)) !=
+              cudaSuccess ||
+          (e = cudaFuncSetAttribute(k_mlp_backward<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem)) !=
+              cudaSuccess)
+        return fail(cuda_fail(e, "cudaFuncSetAttribute(k_mlp_backward)"));
+      h->mb_ok = 1;
+      h->mb_fold = fold ? 1 : 0;
+      h->mb_smem = smem;
+      h->mb_off_w2 = w1;
+      h->mb_off_w3 = w1 + w2;
+      h->mb_off_bias = w1 + w2 + w3;
+      h->mb_wbytes = wbytes;
+      h->mb_off_act = off_act;
+      h->mb_off_bar = off_bar;
+    }
+  }
   *out_handle = h;
   return P2S_OK;
 }
@@ -949,6 +1016,32 @@ p2s_status p2s_backward(p2s_handle* h, p2s_image im, const float* zernike_field,
     k_adjoint_image<<<2 * std::min(d.ntiles, h->sm_count / 2), kDiThreads, h->di_smem, st>>>(d);
     P2S_CUDA(cudaPeekAtLastError());
   }
+  return P2S_OK;
+}
+
+p2s_status p2s_mlp_backward(p2s_handle* h, const float* zernike_field, const float* grad_beta, int B, int H, int W,
+                            float* grad_zernike, p2s_stream_t stream) {
+  if (!h || !zernike_field || !grad_beta || !grad_zernike || B < 1 || H < 1 || W < 1) return P2S_ERR_INVALID_ARG;
+  const size_t HW = (size_t)H * W, nz = (size_t)B * h->n_in * HW, nb = (size_t)B * h->K * HW;
+  if (overlaps(grad_zernike, nz * 4, zernike_field, nz * 4) || overlaps(grad_zernike, nz * 4, grad_beta, nb * 4))
+    return P2S_ERR_INVALID_ARG;
+  if (!h->mb_ok) return P2S_ERR_UNSUPPORTED;
+  const long long tpf = ((long long)HW + 127) / 128;
+  // the kernel addresses a frame's channels by 32-bit offsets
+  if (tpf * B > 0x7fffffffLL || (unsigned long long)std::max(h->K, h->n_in + 2) * HW > 0x7fffffffULL)
+    return P2S_ERR_UNSUPPORTED;
+  MlpbParams p{};
+  p.z = zernike_field; p.gb = grad_beta; p.gz = grad_zernike; p.wpack = h->d_mlpb;
+  p.B = B; p.HW = (int)HW; p.n_in = h->n_in; p.K = h->K;
+  p.K1 = h->K1; p.N1 = h->N1; p.N2 = h->N2; p.Nk = h->Nk;
+  p.tiles_per_frame = (int)tpf;
+  p.ntiles = (int)(tpf * B);
+  p.off_w2 = h->mb_off_w2; p.off_w3 = h->mb_off_w3; p.off_bias = h->mb_off_bias; p.wbytes = h->mb_wbytes;
+  p.off_act = h->mb_off_act; p.off_bar = h->mb_off_bar;
+  const int grid = std::min(p.ntiles, h->sm_count);
+  if (h->mb_fold) k_mlp_backward<true><<<grid, kMbThreads, h->mb_smem, (cudaStream_t)stream>>>(p);
+  else k_mlp_backward<false><<<grid, kMbThreads, h->mb_smem, (cudaStream_t)stream>>>(p);
+  P2S_CUDA(cudaPeekAtLastError());
   return P2S_OK;
 }
 
@@ -1192,6 +1285,7 @@ void p2s_destroy(p2s_handle* h) {
   cudaFree(h->h_img); cudaFree(h->h_z); cudaFree(h->h_t); cudaFree(h->h_out); cudaFree(h->h_anc);
   cudaFree(h->d_gJ);
   cudaFree(h->d_dib); cudaFree(h->d_ut);
+  cudaFree(h->d_mlpb);
   if (h->s_in) cudaStreamDestroy(h->s_in);
   if (h->ev_entry) cudaEventDestroy(h->ev_entry);
   if (h->ev_band) cudaEventDestroy(h->ev_band);

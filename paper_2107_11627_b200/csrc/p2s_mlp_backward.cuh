@@ -1,0 +1,351 @@
+// p2s_mlp_backward.cuh — dL/dz through the P2S MLP: the adjoint of step a1 (PAPER.md:280-283
+// "three fully connected layers", reading A11: ReLU after layers 1-2, linear output; the
+// simulator "as a differentiable module").
+//
+// Per pixel, for z in R^n_in and g3 = dL/dbeta in R^K:
+//     pre1 = W1 z + b1,  a1 = ReLU(pre1),  pre2 = W2 a1 + b2
+//     g2 = (W3^T g3) [pre2 > 0],  g1 = (W2^T g2) [pre1 > 0],  dL/dz = W1^T g1
+// Five tensor-core GEMMs per tile of M = 128 pixels (tcgen05, kind::f16, fp32 accumulators in
+// TMEM), all operands in shared memory:
+//     F1: D1 = Z  W1^T     (K = K1, N = N1)     drain: a1 = relu(D1 + b1) -> ACT, mask1 -> regs
+//     F2: D2 = A1 W2^T     (K = N1, N = N2)
+//     B1: D3 = G3 W3       (K = Nk, N = N2)     drain: g2 = (D2 + b2 > 0) ? D3 : 0 -> ACT
+//     B2: D4 = G2 W2       (K = N2, N = N1)     drain: g1 = mask1 ? D4 : 0 -> ACT
+//     B3: D5 = G1 W1       (K = N1, N = K1)     drain: dL/dz -> global
+// The weights are resident in shared memory for the whole persistent launch, each stored ONCE as
+// a K-major fp16 tile; B2 and B3 read W2 and W1 transposed through the descriptor's B-major bit
+// (an 8x8 core matrix that is K-major for W is MN-major for W^T: LBO and SBO swap roles). One
+// activation buffer (ACT, [128][max K] fp16) carries z, a1, g3, g2 and g1 in turn (each GEMM
+// completes before its A operand is overwritten). The forward masks are recomputed (two of the
+// five GEMMs) rather than stored by the forward pass.
+//
+// Biases: when every layer input has two spare padding columns (n_in + 2 <= K1, h1 + 2 <= N1),
+// they ride in the GEMMs as fp16 hi/lo pairs on constant-1 inputs, as in the render kernel
+// (kFold: z columns n_in, n_in + 1 = 1; W1 rows h1, h1 + 1 make a1 columns h1, h1 + 1 = 1). The
+// transposed products then also carry those columns (D4 at h1, h1 + 1 and D5 at n_in, n_in + 1):
+// they land in dL/dz channels >= n_in only, which are never stored. Otherwise the drains add
+// the fp32 biases.
+// 512 threads: 4 per pixel row (TMEM lane), each owning every 4th 16-column group.
+// Precision (reading N5): fp16 operands (RN), fp32 accumulation, as the render kernel.
+// dL/dbeta is scaled per pixel by an exact power of two before the fp16 rounding (the chain is
+// linear in g3 and the masks do not depend on it), so its range never under- or overflows fp16;
+// dL/dz is scaled back by the inverse power. The ReLU masks are decided on fp32 accumulators of
+// fp16 operands (pre > 0), as the oracle's mask_precision="fp16" mode decides them.
+#pragma once
+
+#include <cuda_fp16.h>
+#include <cuda_runtime.h>
+
+#include <cstdint>
+
+#include "sm100.cuh"
+
+namespace p2s {
+
+struct MlpbParams {
+  const float* z;       // [B][n_in][HW] fp32 (the zernike field)
+  const float* gb;      // [B][K][HW] fp32 dL/dbeta
+  float* gz;            // [B][n_in][HW] fp32 dL/dz (output)
+  const uint8_t* wpack; // [W1 | W2 | W3^T | b1 (N1 fp32) | b2 (N2 fp32)], copied to smem offset 0
+  int B, HW, n_in, K;
+  int K1, N1, N2, Nk;   // padded (multiples of 16) input / hidden / hidden / output widths
+  int tiles_per_frame, ntiles;
+  int off_w2, off_w3, off_bias, wbytes;  // byte offsets in wpack (= in shared memory)
+  int off_act, off_bar;
+};
+
+constexpr int kMbThreads = 512;
+
+namespace mlpb {
+
+// D[128 x N] = A[128 x 16 nks] * B^T, A = ACT (K-major, kd = 16 nks), B at b_s:
+//   K-major B [N][16 nks]:            lbo = 128,       sbo = 16 * 16 nks, kstep = 256
+//   transposed B (stored [16 nks][N]): lbo = 16 * N,    sbo = 128,         kstep = 32 * N, idesc bit 16
+P2S_DEV void gemm(uint32_t d, uint32_t a_s, int nks, uint32_t b_s, uint32_t b_lbo, uint32_t b_sbo,
+                  uint32_t b_kstep, uint32_t idesc) {
+  const uint32_t a_sbo = (uint32_t)nks * 256u;
+  for (int ks = 0; ks < nks; ++ks)
+    umma_f16_elect(d, sdesc(a_s + (uint32_t)ks * 256u, 128u, a_sbo),
+                   sdesc(b_s + (uint32_t)ks * b_kstep, b_lbo, b_sbo), idesc, ks > 0 ? 1u : 0u);
+}
+
+// this thread's row of a K-major [128][kd] fp16 tile: element (m, k) at
+// (m%8)*16 + (m/8)*kd*16 + (k%8)*2 + (k/8)*128
+P2S_DEV uint8_t* row_of(uint8_t* act, int m, int kd) { return act + (m & 7) * 16 + (m >> 3) * kd * 16; }
+
+P2S_DEV void st8(uint8_t* row, int kchunk, uint32_t a, uint32_t b, uint32_t c, uint32_t d) {
+  *reinterpret_cast<uint4*>(row + kchunk * 128) = make_uint4(a, b, c, d);
+}
+P2S_DEV void st8f(uint8_t* row, int kchunk, const float* v) {
+  st8(row, kchunk, pack_half2(v[0], v[1]), pack_half2(v[2], v[3]), pack_half2(v[4], v[5]), pack_half2(v[6], v[7]));
+}
+P2S_DEV uint32_t relu2(float a, float b) {  // fp16x2 {lo = relu(a), hi = relu(b)}, RN
+  uint32_t r;
+  asm("cvt.rn.relu.f16x2.f32 %0, %1, %2;" : "=r"(r) : "f"(b), "f"(a));
+  return r;
+}
+P2S_DEV float exp2i(int e) { return __int_as_float((e + 127) << 23); }  // 2^e, e in [-126, 127]
+
+// the CTA's generic-proxy writes to ACT / its TMEM reads are ordered before the next UMMA
+P2S_DEV void publish() {
+  fence_proxy_async_smem();
+  tc_fence_before();
+  __syncthreads();
+}
+
+}  // namespace mlpb
+
+// this thread's z values of tile t (chunks 4i + q of 8 channels). Loads clamp the pixel into the
+// frame (a ragged tile's extra rows are never stored) and address channels by 32-bit offsets
+// from the frame base (host: (n_in + 2) HW, K HW < 2^31).
+P2S_DEV void load_z(const MlpbParams& p, int t, int m, int q, float (&zv)[2][8]) {
+  const int b = t / p.tiles_per_frame;
+  const int px = min((t - b * p.tiles_per_frame) * 128 + m, p.HW - 1);
+  const float* zb = p.z + (size_t)b * p.n_in * (size_t)p.HW + px;
+#pragma unroll
+  for (int i = 0; i < 2; ++i) {
+    const int c = 4 * i + q;
+    uint32_t off = (uint32_t)(c * 8) * (uint32_t)p.HW;
+#pragma unroll
+    for (int j = 0; j < 8; ++j, off += (uint32_t)p.HW) zv[i][j] = (c * 8 + j < p.n_in) ? __ldcs(zb + off) : 0.f;
+  }
+}
+
+template <bool kFold>
+__global__ void __launch_bounds__(kMbThreads, 1) k_mlp_backward(const __grid_constant__ MlpbParams p) {
+  using namespace mlpb;
+  extern __shared__ __align__(1024) uint8_t smem[];
+  const uint32_t sbase = smem_u32(smem);
+  uint64_t* bar_w = reinterpret_cast<uint64_t*>(smem + p.off_bar);
+  uint64_t* bar_mma = bar_w + 1;
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bar_mma + 1);
+  float* s_max = reinterpret_cast<float*>(smem + p.off_bar + 32);  // [4][128]
+  const float* s_b1 = reinterpret_cast<const float*>(smem + p.off_bias);
+  const float* s_b2 = s_b1 + p.N1;
+  uint8_t* act = smem + p.off_act;
+  const uint32_t act_s = sbase + (uint32_t)p.off_act;
+  const int tid = (int)threadIdx.x, warp = (int)warp_id();
+  const int m = tid & 127, q = tid >> 7;  // pixel row (TMEM lane) and column quarter
+
+  if (tid == 0) {
+    mbar_init(bar_w, 1);
+    mbar_init(bar_mma, 1);
+    fence_mbar_init();
+  }
+  if (warp == 0) tmem_alloc<512>(tmem_slot);
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
+  const uint32_t tmem = *tmem_slot;
+  const uint32_t tq = tmem + ((uint32_t)(32 * (warp & 3)) << 16);  // this warp's lane quadrant
+  if (tid == 0 && (int)blockIdx.x < p.ntiles) {
+    mbar_arrive_expect_tx(bar_w, (uint32_t)p.wbytes);
+    for (int off = 0; off < p.wbytes; off += 32768)
+      bulk_g2s(smem + off, p.wpack + off, (uint32_t)min(32768, p.wbytes - off), bar_w);
+  }
+
+  const uint32_t id_f1 = idesc_f16(128, (uint32_t)p.N1), id_f2 = idesc_f16(128, (uint32_t)p.N2);
+  const uint32_t id_b2 = idesc_f16(128, (uint32_t)p.N1) | (1u << 16);
+  const uint32_t id_b3 = idesc_f16(128, (uint32_t)p.K1) | (1u << 16);
+  const uint32_t w1_s = sbase, w2_s = sbase + (uint32_t)p.off_w2, w3_s = sbase + (uint32_t)p.off_w3;
+  const size_t HW = (size_t)p.HW;
+  uint8_t* const row_k1 = row_of(act, m, p.K1);
+  uint8_t* const row_n1 = row_of(act, m, p.N1);
+  uint8_t* const row_n2 = row_of(act, m, p.N2);
+  uint8_t* const row_nk = row_of(act, m, p.Nk);
+  uint32_t ph = 0;
+  bool first = true;
+  float zv[2][8];
+  if ((int)blockIdx.x < p.ntiles) load_z(p, (int)blockIdx.x, m, q, zv);
+
+  for (int t = (int)blockIdx.x; t < p.ntiles; t += (int)gridDim.x) {
+    const int b = t / p.tiles_per_frame;
+    const int px = (t - b * p.tiles_per_frame) * 128 + m;
+    const bool valid = px < p.HW;
+    {  // L2 prefetch of the next tile's dL/dbeta rows (4 lines of 128 B per channel)
+      const int tn = t + (int)gridDim.x;
+      if (tn < p.ntiles) {
+        const int bn = tn / p.tiles_per_frame, p0 = (tn - bn * p.tiles_per_frame) * 128;
+        for (int r = tid; r < 4 * p.K; r += kMbThreads) {
+          const int qq = p0 + (r & 3) * 32;
+          if (qq < p.HW) prefetch_l2(p.gb + ((size_t)bn * p.K + (r >> 2)) * HW + qq);
+        }
+      }
+    }
+    const int pxc = valid ? px : p.HW - 1;
+    // ---- z (loaded into zv one tile ahead) -> ACT (fp16, K1 columns; kFold: columns n_in,
+    //      n_in + 1 = 1; other padding zeros)
+#pragma unroll
+    for (int i = 0; i < 2; ++i) {
+      const int c = 4 * i + q;
+      if (c * 8 < p.K1) {
+        float v[8];
+#pragma unroll
+        for (int j = 0; j < 8; ++j) {
+          const int ch = c * 8 + j;
+          v[j] = ch < p.n_in ? zv[i][j] : ((kFold && ch < p.n_in + 2) ? 1.f : 0.f);
+        }
+        st8f(row_k1, c, v);
+      }
+    }
+    publish();
+    if (first) {  // resident weights and biases
+      mbar_wait(bar_w, 0);
+      first = false;
+    }
+    if (warp == 0) {
+      tc_fence_after();
+      gemm(tmem, act_s, p.K1 / 16, w1_s, 128u, (uint32_t)p.K1 * 16u, 256u, id_f1);
+      umma_commit_elect(bar_mma);
+    }
+    // ---- dL/dbeta of this tile into registers (in flight during F1 / F2)
+    float gv[4][8];
+    {
+      const float* gbb = p.gb + (size_t)b * p.K * HW + pxc;
+#pragma unroll
+      for (int i = 0; i < 4; ++i) {
+        const int c = 4 * i + q;
+        uint32_t off = (uint32_t)(c * 8) * (uint32_t)p.HW;
+#pragma unroll
+        for (int j = 0; j < 8; ++j, off += (uint32_t)p.HW) gv[i][j] = (c * 8 + j < p.K) ? __ldcs(gbb + off) : 0.f;
+      }
+    }
+    mbar_wait(bar_mma, ph);
+    ph ^= 1;
+    tc_fence_after();
+    // ---- drain D1: a1 = relu(pre1) -> ACT (N1 columns), mask1 = [pre1 > 0] bits
+    uint32_t mask1[2] = {0u, 0u};
+#pragma unroll
+    for (int i = 0; i < 4; ++i) {
+      const int g = 4 * i + q;
+      if (g * 16 < p.N1) {
+        float v[16];
+        tmem_ld16(tq + (uint32_t)(g * 16), v);
+        tmem_ld_wait();
+        if (!kFold) {
+#pragma unroll
+          for (int j = 0; j < 16; ++j) v[j] += s_b1[g * 16 + j];
+        }
+        uint32_t bits = 0;
+#pragma unroll
+        for (int j = 0; j < 16; ++j) bits |= (v[j] > 0.f ? 1u : 0u) << j;
+        mask1[i >> 1] |= bits << ((i & 1) * 16);
+        st8(row_n1, 2 * g, relu2(v[0], v[1]), relu2(v[2], v[3]), relu2(v[4], v[5]), relu2(v[6], v[7]));
+        st8(row_n1, 2 * g + 1, relu2(v[8], v[9]), relu2(v[10], v[11]), relu2(v[12], v[13]), relu2(v[14], v[15]));
+      }
+    }
+    publish();
+    if (warp == 0) {
+      tc_fence_after();
+      gemm(tmem + 256u, act_s, p.N1 / 16, w2_s, 128u, (uint32_t)p.N1 * 16u, 256u, id_f2);
+      umma_commit_elect(bar_mma);
+    }
+    // per-pixel power-of-two scale of dL/dbeta (the four quarters agree through s_max)
+    float mx = 0.f;
+#pragma unroll
+    for (int i = 0; i < 4; ++i)
+#pragma unroll
+      for (int j = 0; j < 8; ++j) mx = fmaxf(mx, fabsf(gv[i][j]));
+    s_max[q * 128 + m] = mx;
+    mbar_wait(bar_mma, ph);  // F2 done: ACT is free
+    ph ^= 1;
+    tc_fence_after();
+    __syncthreads();
+    mx = fmaxf(fmaxf(s_max[m], s_max[128 + m]), fmaxf(s_max[256 + m], s_max[384 + m]));
+    // mx = f 2^ex with f in [0.5, 1) (normal mx; 0 and subnormals take ex = -126, inf/NaN 129):
+    // scale by 2^-ex and back by 2^ex, each as two in-range power-of-two factors (exact)
+    const int ex = (int)((__float_as_uint(mx) >> 23) & 0xffu) - 126;
+    const int e1 = (-ex) / 2, e2 = -ex - e1;
+    const float s1 = exp2i(e1), s2 = exp2i(e2);
+    // ---- scaled dL/dbeta -> ACT (Nk columns)
+#pragma unroll
+    for (int i = 0; i < 4; ++i) {
+      const int c = 4 * i + q;
+      if (c * 8 < p.Nk) {
+        float v[8];
+#pragma unroll
+        for (int j = 0; j < 8; ++j) v[j] = gv[i][j] * s1 * s2;
+        st8f(row_nk, c, v);
+      }
+    }
+    publish();
+    if (warp == 0) {
+      tc_fence_after();
+      gemm(tmem, act_s, p.Nk / 16, w3_s, 128u, (uint32_t)p.Nk * 16u, 256u, id_f2);
+      umma_commit_elect(bar_mma);
+    }
+    mbar_wait(bar_mma, ph);
+    ph ^= 1;
+    tc_fence_after();
+    // ---- drain D2 (pre2) and D3 (W3^T g3): g2 = (pre2 > 0) ? D3 : 0 -> ACT (N2 columns)
+#pragma unroll
+    for (int i = 0; i < 4; ++i) {
+      const int g = 4 * i + q;
+      if (g * 16 < p.N2) {
+        float v2[16], v3[16];
+        tmem_ld16(tq + 256u + (uint32_t)(g * 16), v2);
+        tmem_ld16(tq + (uint32_t)(g * 16), v3);
+        tmem_ld_wait();
+#pragma unroll
+        for (int j = 0; j < 16; ++j) v3[j] = (v2[j] + (kFold ? 0.f : s_b2[g * 16 + j]) > 0.f) ? v3[j] : 0.f;
+        st8f(row_n2, 2 * g, v3);
+        st8f(row_n2, 2 * g + 1, v3 + 8);
+      }
+    }
+    publish();
+    if (warp == 0) {
+      tc_fence_after();
+      gemm(tmem + 256u, act_s, p.N2 / 16, w2_s, (uint32_t)p.N1 * 16u, 128u, (uint32_t)p.N1 * 32u, id_b2);
+      umma_commit_elect(bar_mma);
+    }
+    mbar_wait(bar_mma, ph);
+    ph ^= 1;
+    tc_fence_after();
+    // ---- drain D4 (W2^T g2): g1 = mask1 ? D4 : 0 -> ACT (N1 columns)
+#pragma unroll
+    for (int i = 0; i < 4; ++i) {
+      const int g = 4 * i + q;
+      if (g * 16 < p.N1) {
+        float v[16];
+        tmem_ld16(tq + 256u + (uint32_t)(g * 16), v);
+        tmem_ld_wait();
+        const uint32_t bits = mask1[i >> 1] >> ((i & 1) * 16);
+#pragma unroll
+        for (int j = 0; j < 16; ++j) v[j] = ((bits >> j) & 1u) ? v[j] : 0.f;
+        st8f(row_n1, 2 * g, v);
+        st8f(row_n1, 2 * g + 1, v + 8);
+      }
+    }
+    publish();
+    if (warp == 0) {
+      tc_fence_after();
+      gemm(tmem, act_s, p.N1 / 16, w1_s, (uint32_t)p.K1 * 16u, 128u, (uint32_t)p.K1 * 32u, id_b3);
+      umma_commit_elect(bar_mma);
+    }
+    if (t + (int)gridDim.x < p.ntiles) load_z(p, t + (int)gridDim.x, m, q, zv);  // next tile's z
+    mbar_wait(bar_mma, ph);
+    ph ^= 1;
+    tc_fence_after();
+    // ---- drain D5 (W1^T g1) -> dL/dz, unscaled (coalesced: lanes are consecutive pixels)
+    if (q * 16 < p.K1) {
+      const float u1 = exp2i(-e1), u2 = exp2i(-e2);
+      float* gzb = p.gz + (size_t)b * p.n_in * HW + px;
+      float v[16];
+      tmem_ld16(tq + (uint32_t)(q * 16), v);
+      tmem_ld_wait();
+      if (valid) {
+        uint32_t off = (uint32_t)(q * 16) * (uint32_t)p.HW;
+#pragma unroll
+        for (int j = 0; j < 16; ++j, off += (uint32_t)p.HW)
+          if (q * 16 + j < p.n_in) __stcs(gzb + off, v[j] * u1 * u2);
+      }
+    }
+    tc_fence_before();  // TMEM reads before the next tile's F1 (ordered by its publish())
+  }
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
+  if (warp == 0) tmem_dealloc<512>(tmem);
+}
+
+}  // namespace p2s

@@ -27,7 +27,7 @@ EXPORTED = ("p2s_init", "p2s_render", "p2s_render_host", "p2s_reserve", "p2s_set
             "p2s_debug_beta", "p2s_debug_blur", "p2s_debug_profile_buffer",
             "p2s_render_anchors", "p2s_render_anchors_host", "p2s_debug_blur_anchors",
             "p2s_render_sequence", "p2s_sampler_init", "p2s_sample_anchors", "p2s_sampler_destroy",
-            "p2s_backward", "p2s_render_color")
+            "p2s_backward", "p2s_render_color", "p2s_mlp_backward")
 
 
 class P2SError(RuntimeError):
@@ -100,12 +100,13 @@ def load_library(path: str = LIB_PATH) -> ctypes.CDLL:
     lib.p2s_sampler_destroy.argtypes = [v]
     lib.p2s_backward.argtypes = [v, _Image, v, v, v, v, v, v, v]
     lib.p2s_render_color.argtypes = [v, _Image, v, v, v, v]
+    lib.p2s_mlp_backward.argtypes = [v, v, v, i, i, i, v, v]
     lib.p2s_sampler_destroy.restype = None
     for name in ("p2s_init", "p2s_render", "p2s_render_host", "p2s_reserve", "p2s_set_profile_events",
                  "p2s_get_info", "p2s_debug_beta", "p2s_debug_blur", "p2s_debug_profile_buffer",
                  "p2s_render_anchors", "p2s_render_anchors_host", "p2s_debug_blur_anchors",
                  "p2s_render_sequence", "p2s_sampler_init", "p2s_sample_anchors", "p2s_backward",
-                 "p2s_render_color"):
+                 "p2s_render_color", "p2s_mlp_backward"):
         getattr(lib, name).restype = st
     _lib = lib
     return lib
@@ -171,17 +172,19 @@ class Renderer:
         return out
 
     def backward(self, image, zernike, tilt, grad_out, want_beta=True, want_tilt=True, want_image=False,
-                 stream=None):
+                 want_zernike=False, stream=None):
         """p2s_backward: (dL/dbeta [B,K,H,W] | None, dL/dt [B,2,H,W] | None) of the
         frames render(image, zernike, tilt) gives, for upstream grad_out [B,C,H,W]; with
-        want_image=True a third entry dL/dI [B,C,H,W]."""
+        want_image=True a third entry dL/dI [B,C,H,W]; with want_zernike=True a fourth entry
+        dL/dz [B,n_in,H,W] (p2s_mlp_backward on dL/dbeta)."""
         import torch
         B, C, H, W = image.shape
         im = _Image(_dev_ptr(image, "image").value, B, C, H, W)
         zp = _dev_ptr(zernike, "zernike_field", (B, self.n_in, H, W))
         tp = _dev_ptr(tilt, "tilt_field", (B, 2, H, W)) if tilt is not None else ctypes.c_void_p()
         gp = _dev_ptr(grad_out, "grad_out", (B, C, H, W))
-        gb = torch.empty((B, self.K, H, W), device=image.device, dtype=torch.float32) if want_beta else None
+        gb = torch.empty((B, self.K, H, W), device=image.device, dtype=torch.float32) \
+            if (want_beta or want_zernike) else None
         gt = torch.empty((B, 2, H, W), device=image.device, dtype=torch.float32) if want_tilt else None
         gi = torch.empty((B, C, H, W), device=image.device, dtype=torch.float32) if want_image else None
         _check(self._lib.p2s_backward(self._h, im, zp, tp, gp,
@@ -189,7 +192,22 @@ class Renderer:
                                       _dev_ptr(gt, "grad_tilt") if gt is not None else ctypes.c_void_p(),
                                       _dev_ptr(gi, "grad_image") if gi is not None else ctypes.c_void_p(),
                                       _stream_handle(stream)), "p2s_backward")
+        if want_zernike:
+            gz = self.mlp_backward(zernike, gb, stream=stream)
+            return (gb if want_beta else None), gt, gi, gz
         return (gb, gt, gi) if want_image else (gb, gt)
+
+    def mlp_backward(self, zernike, grad_beta, out=None, stream=None):
+        """p2s_mlp_backward: dL/dz [B,n_in,H,W] through the P2S MLP for dL/dbeta [B,K,H,W]."""
+        import torch
+        B, n_in, H, W = zernike.shape
+        zp = _dev_ptr(zernike, "zernike_field", (B, self.n_in, H, W))
+        bp = _dev_ptr(grad_beta, "grad_beta", (B, self.K, H, W))
+        if out is None:
+            out = torch.empty_like(zernike)
+        _check(self._lib.p2s_mlp_backward(self._h, zp, bp, B, H, W, _dev_ptr(out, "grad_zernike", (B, n_in, H, W)),
+                                          _stream_handle(stream)), "p2s_mlp_backward")
+        return out
 
     def debug_beta(self, zernike, out=None, stream=None):
         import torch

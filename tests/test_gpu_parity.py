@@ -707,3 +707,186 @@ def test_large_ragged_frame_sampled(p2s):
     bxy = np.concatenate([np.array(edge), bxy]).astype(np.int32)
     _, oref = oracle.pixels(inp.image, inp.zernike, inp.tilt, inp.basis, inp.mlp, bxy)
     _cmp(out[bxy[:, 0], :, bxy[:, 1], bxy[:, 2]], oref, "render[2048x2000 sampled]")
+
+
+# ---- dL/dz through the P2S MLP (p2s_mlp_backward; the adjoint of step a1), vs
+#      oracle.adjoint.mlp_backward with the masks decided in the GPU's fp16 precision (reading N5)
+
+DZ_CASES = ["cfg1", "ragged_rgb_S7", "S33_K100_C2", "S1_K1", "S17_K128_n64", "S25", "W1_H1", "many_tiles_C1_S9"]
+
+
+def _dz_ref(inp, gbeta, amb_rel=(2e-5, 2e-4)):
+    """Oracle dL/dz per frame, and the pixels where a pre-activation lies within the rounding
+    envelope of 0 (amb_rel x the abs-sum of its terms: layer 1 differs from the GPU only by fp32
+    accumulation order and the fp32 bias, ~n 2^-24; layer 2 also by the odd a1 element rounded
+    to the other fp16 neighbour): there either side of the ReLU mask is a correct answer, and the
+    valid alternatives (every flip of the ambiguous units, <= 4) are returned for the comparison."""
+    from oracle import adjoint
+    f16 = lambda a: np.asarray(a, np.float32).astype(np.float16).astype(np.float64)  # noqa: E731
+    m = inp.mlp
+    refs, alts = [], []
+    for b in range(inp.zernike.shape[0]):
+        z = inp.zernike[b].astype(np.float64)
+        n_in, H, W = z.shape
+        p1, p2 = adjoint.mlp_preactivations(z, m, "fp16")
+        Z = f16(z.reshape(n_in, -1))
+        s1 = np.abs(f16(m["W1"])) @ np.abs(Z) + np.abs(m["b1"].astype(np.float64))[:, None]
+        s2 = np.abs(f16(m["W2"])) @ f16(np.maximum(p1, 0)) + np.abs(m["b2"].astype(np.float64))[:, None]
+        a1, a2 = np.abs(p1) <= amb_rel[0] * s1, np.abs(p2) <= amb_rel[1] * s2
+        refs.append(adjoint.mlp_backward(z, gbeta[b], m, "fp16"))
+        alt = {}
+        for q in np.nonzero(a1.any(0) | a2.any(0))[0]:
+            u1, u2 = np.nonzero(a1[:, q])[0], np.nonzero(a2[:, q])[0]
+            n = len(u1) + len(u2)
+            if n > 4:
+                alt[q] = None  # too ambiguous to enumerate: excluded (counted below)
+                continue
+            y, x = divmod(int(q), W)
+            zq, gq = z[:, y:y + 1, x:x + 1], gbeta[b][:, y:y + 1, x:x + 1]
+            outs = []
+            for bits in range(1 << n):
+                m1, m2 = (p1[:, q:q + 1] > 0).copy(), (p2[:, q:q + 1] > 0).copy()
+                for i, u in enumerate(u1):
+                    m1[u, 0] = bool((bits >> i) & 1)
+                for i, u in enumerate(u2):
+                    m2[u, 0] = bool((bits >> (len(u1) + i)) & 1)
+                outs.append(adjoint.mlp_backward(zq, gq, m, masks=(m1, m2))[:, 0, 0])
+            alt[q] = outs
+        alts.append(alt)
+    return np.stack(refs), alts
+
+
+def _dz_check(gz, ref, alts, what, scale=None):
+    """Element-wise parity off the ambiguous pixels; at an ambiguous pixel the GPU result must equal
+    one of its valid alternatives. Tolerance: 2e-3 x max|ref|, or x scale[b, 0, pixel] (a per-pixel
+    error envelope) when given."""
+    B, n_in, H, W = ref.shape
+    g = gz.reshape(B, n_in, -1).astype(np.float64)
+    r = ref.reshape(B, n_in, -1).copy()
+    assert np.all(np.isfinite(g)), f"{what}: non-finite"
+    per_pixel = scale is not None
+    if not per_pixel:
+        scale = np.full((B, 1, r.shape[2]), np.abs(r).max())
+    keep = np.ones((B, r.shape[2]), bool)
+    n_amb = n_skip = 0
+    for b, alt in enumerate(alts):
+        for q, outs in alt.items():
+            keep[b, q] = False
+            n_amb += 1
+            if outs is None:
+                n_skip += 1
+                continue
+            tol = 2e-3 * max(np.abs(np.stack(outs)).max(), scale[b, 0, q])
+            assert min(np.abs(g[b, :, q] - o).max() for o in outs) <= tol, f"{what}: ambiguous pixel {b},{q}"
+    err = np.abs(g - r) / np.maximum(scale, 1e-300)
+    err = err.transpose(0, 2, 1)[keep]
+    mx = float(err.max()) if err.size else 0.0
+    gk, rk = g.transpose(0, 2, 1)[keep], r.transpose(0, 2, 1)[keep]
+    rl2 = float(np.linalg.norm(gk - rk) / max(np.linalg.norm(rk), 1e-300)) if not per_pixel else 0.0
+    print(f"{what}: max_err/scale={mx:.3e} rel_l2={rl2:.3e} ambiguous={n_amb} (skipped {n_skip}) of {keep.size}")
+    assert n_skip <= max(1, keep.size // 1000)
+    assert mx <= 2e-3, f"{what}: {mx:.3e}"
+    assert rl2 <= 1e-3, f"{what}: rel L2 {rl2:.3e}"
+
+
+def _gbeta(spec, shape, seed, wide=False):
+    rng = np.random.default_rng([seed, 17])
+    g = rng.standard_normal(shape)
+    if wide:  # per-pixel magnitudes over 24 decades: the per-pixel power-of-two scaling
+        B, K, H, W = shape
+        g *= 10.0 ** rng.uniform(-12, 12, (B, 1, H, W))
+    return g.astype(np.float32)
+
+
+@pytest.mark.parametrize("name", DZ_CASES)
+def test_mlp_backward_parity(p2s, name):
+    spec = SMALL[name]
+    inp = synth.make_inputs(spec)
+    B, n_in, H, W = inp.zernike.shape
+    gbeta = _gbeta(spec, (B, spec.K, H, W), 31)
+    r = p2s.Renderer(inp.basis, inp.mlp)
+    gz = r.mlp_backward(_dev(inp.zernike), _dev(gbeta)).cpu().numpy()
+    ref, alts = _dz_ref(inp, gbeta.astype(np.float64))
+    _dz_check(gz, ref, alts, f"dL/dz[{name}]")
+    r.close()
+
+
+@pytest.mark.parametrize("name", ["ragged_rgb_S7", "S33_K100_C2"])
+def test_mlp_backward_wide_range(p2s, name):
+    """dL/dbeta spanning 1e-12 ... 1e12 across pixels (beyond fp16's range both ways)."""
+    spec = SMALL[name]
+    inp = synth.make_inputs(spec)
+    B, n_in, H, W = inp.zernike.shape
+    gbeta = _gbeta(spec, (B, spec.K, H, W), 32, wide=True)
+    r = p2s.Renderer(inp.basis, inp.mlp)
+    gz = r.mlp_backward(_dev(inp.zernike), _dev(gbeta)).cpu().numpy()
+    ref, alts = _dz_ref(inp, gbeta.astype(np.float64))
+    # per-pixel envelope: the same chain on |W| and |dL/dbeta| (fp16 rounding errors of every term
+    # add up to at most ~2^-11 of it), as the dL/dI test scales its 1x1 case
+    from oracle import adjoint
+    absm = {k: np.abs(np.asarray(v, np.float64)) for k, v in inp.mlp.items()}
+    env = []
+    for b in range(B):
+        p1, p2 = adjoint.mlp_preactivations(inp.zernike[b].astype(np.float64), inp.mlp, "fp16")
+        e = adjoint.mlp_backward(inp.zernike[b].astype(np.float64), np.abs(gbeta[b].astype(np.float64)), absm,
+                                 masks=(p1 > 0, p2 > 0))
+        env.append(e.reshape(n_in, -1).max(0)[None])
+    _dz_check(gz, ref, alts, f"dL/dz wide[{name}]", scale=np.stack(env))
+    # zero upstream gradient -> exactly zero
+    z0 = r.mlp_backward(_dev(inp.zernike), _dev(np.zeros_like(gbeta))).cpu().numpy()
+    assert not np.any(z0)
+    r.close()
+
+
+def test_mlp_backward_cfg3_full_frame(p2s):
+    """Bench-size frame (512x512, MLP 33-200-200-100), every pixel, dL/dbeta from p2s_backward
+    (the chained dL/dz of the whole simulator)."""
+    from oracle import adjoint
+    spec = synth.CONFIGS[3]
+    inp = synth.make_inputs(spec)
+    g = synth.make_upstream_grad(spec)
+    r = p2s.Renderer(inp.basis, inp.mlp)
+    gb, gt, gi, gz = r.backward(_dev(inp.image), _dev(inp.zernike), _dev(inp.tilt), _dev(g), want_beta=True,
+                                want_tilt=False, want_zernike=True)
+    assert gt is None and gi is None
+    gb = gb.cpu().numpy()
+    ref, alts = _dz_ref(inp, gb.astype(np.float64))
+    _dz_check(gz.cpu().numpy(), ref, alts, "dL/dz[cfg3 chained]")
+    # the chained call equals the standalone call on the same dL/dbeta
+    gz2 = r.mlp_backward(_dev(inp.zernike), _dev(gb)).cpu().numpy()
+    np.testing.assert_array_equal(gz.cpu().numpy(), gz2)
+    # and the GPU's dL/dbeta feeding it matches the oracle at sampled pixels (as test_backward_cfg3_sampled)
+    rng = np.random.default_rng(12)
+    yx = [(int(y), int(x)) for y, x in zip(rng.integers(0, 512, 24), rng.integers(0, 512, 24))]
+    beta = oracle.beta(inp.image[:1], inp.zernike[:1], inp.basis, inp.mlp)[0]
+    rb, _ = adjoint.backward_at(inp.image[0], beta, inp.tilt[0], inp.basis, g[0], yx, coord_dtype=np.float32)
+    ys, xs = np.array(yx).T
+    _cmp(gb[0][:, ys, xs].T, rb, "dL/dbeta[cfg3 chained]", max_abs=2e-3 * np.abs(rb).max())
+    r.close()
+
+
+def test_mlp_backward_invalid_and_unsupported(p2s):
+    spec = SMALL["ragged_rgb_S7"]
+    inp = synth.make_inputs(spec)
+    B, n_in, H, W = inp.zernike.shape
+    r = p2s.Renderer(inp.basis, inp.mlp)
+    z, gb = _dev(inp.zernike), _dev(_gbeta(spec, (B, spec.K, H, W), 33))
+    out = torch.empty_like(z)
+    vp = ctypes.c_void_p
+    lib, st = r._lib, vp(torch.cuda.current_stream().cuda_stream)
+    assert lib.p2s_mlp_backward(r._h, vp(), vp(gb.data_ptr()), B, H, W, vp(out.data_ptr()), st) == p2s.P2S_ERR_INVALID_ARG
+    assert lib.p2s_mlp_backward(r._h, vp(z.data_ptr()), vp(), B, H, W, vp(out.data_ptr()), st) == p2s.P2S_ERR_INVALID_ARG
+    assert lib.p2s_mlp_backward(r._h, vp(z.data_ptr()), vp(gb.data_ptr()), B, H, W, vp(), st) == p2s.P2S_ERR_INVALID_ARG
+    assert lib.p2s_mlp_backward(r._h, vp(z.data_ptr()), vp(gb.data_ptr()), 0, H, W, vp(out.data_ptr()), st) == p2s.P2S_ERR_INVALID_ARG
+    # output aliasing an input
+    assert lib.p2s_mlp_backward(r._h, vp(z.data_ptr()), vp(gb.data_ptr()), B, H, W, vp(z.data_ptr()), st) == p2s.P2S_ERR_INVALID_ARG
+    assert lib.p2s_mlp_backward(r._h, vp(z.data_ptr()), vp(gb.data_ptr()), B, H, W, vp(gb.data_ptr()), st) == p2s.P2S_ERR_INVALID_ARG
+    r.close()
+    # an MLP whose weights do not fit one SM next to the activation tile: unsupported, not wrong
+    big = synth.make_inputs(SMALL["S65_K100_h256"])
+    r = p2s.Renderer(big.basis, big.mlp)
+    B, n_in, H, W = big.zernike.shape
+    with pytest.raises(p2s.P2SError) as ei:
+        r.mlp_backward(_dev(big.zernike), _dev(np.zeros((B, 100, H, W), np.float32)))
+    assert ei.value.status == p2s.P2S_ERR_UNSUPPORTED
+    r.close()

@@ -584,3 +584,22 @@ def test_mlp_backward_matches_finite_differences():
         assert abs(fd - dz[i, y, x]) < 1e-4 * (1 + abs(dz[i, y, x])), (fd, dz[i, y, x])
     # masks decided in fp16 agree here (no pre-activation within rounding of 0)
     np.testing.assert_allclose(adjoint.mlp_backward(z[0], g, inp.mlp, "fp16"), dz, rtol=0, atol=1e-12)
+
+
+def test_mlp_preactivations_reproduce_c_oracle_beta():
+    """The layer-1/2 pre-activations the dL/dz masks are decided on: W3 ReLU(pre2) + b3 equals the
+    independent C oracle's beta (fp64 mode), and the fp16-operand form stays within the fp16
+    rounding of it; imposing the computed masks reproduces mlp_backward."""
+    from oracle import adjoint
+    spec = synth.custom("mlpp", 403, B=1, C=1, H=5, W=7, K=9, S=3, h1=24, h2=20)
+    inp = synth.make_inputs(spec)
+    z = inp.zernike[0].astype(np.float64)
+    ref = oracle.beta(inp.image, inp.zernike, inp.basis, inp.mlp)[0].reshape(9, -1)
+    for prec, tol in (("fp64", 1e-12), ("fp16", 5e-3)):
+        p1, p2 = adjoint.mlp_preactivations(z, inp.mlp, prec)
+        beta = inp.mlp["W3"].astype(np.float64) @ np.maximum(p2, 0) + inp.mlp["b3"].astype(np.float64)[:, None]
+        assert np.abs(beta - ref).max() <= tol * (1 + np.abs(ref).max()), prec
+    g = np.random.default_rng(5).standard_normal((9, 5, 7))
+    p1, p2 = adjoint.mlp_preactivations(z, inp.mlp, "fp16")
+    np.testing.assert_array_equal(adjoint.mlp_backward(z, g, inp.mlp, masks=(p1 > 0, p2 > 0)),
+                                  adjoint.mlp_backward(z, g, inp.mlp, "fp16"))
