@@ -357,10 +357,15 @@ def main():
         aimg, az, at = (torch.from_numpy(a).to(dev) for a in (ainp.image, ainp.zernike, ainp.tilt))
         ag = torch.from_numpy(synth.make_upstream_grad(spec, frames=pdist.rank_frames(rank, 1))).to(dev)
         res = {}
-        for key, wb, wt, wi in (("value", True, True, False), ("beta_only", True, False, False),
-                                ("image_only", False, False, True), ("all", True, True, True)):
+        for key, wb, wt, wi, wz in (("value", True, True, False, False), ("beta_only", True, False, False, False),
+                                    ("image_only", False, False, True, False),
+                                    ("all", True, True, True, False), ("zernike_only", False, False, False, True),
+                                    ("all_with_zernike", True, True, True, True)):
+            if wz and not r.info()["mlp_backward"]:
+                res[key] = None
+                continue
             for _ in range(3):
-                r.backward(aimg, az, at, ag, want_beta=wb, want_tilt=wt, want_image=wi)
+                r.backward(aimg, az, at, ag, want_beta=wb, want_tilt=wt, want_image=wi, want_zernike=wz)
             n_a = max(5, min(args.steps // 4, 50))
             a0 = [torch.cuda.Event(enable_timing=True) for _ in range(n_a)]
             a1 = [torch.cuda.Event(enable_timing=True) for _ in range(n_a)]
@@ -368,17 +373,21 @@ def main():
             for i in range(n_a):
                 flush.fill_(float(i))
                 a0[i].record(stream)
-                r.backward(aimg, az, at, ag, want_beta=wb, want_tilt=wt, want_image=wi)
+                r.backward(aimg, az, at, ag, want_beta=wb, want_tilt=wt, want_image=wi, want_zernike=wz)
                 a1[i].record(stream)
             torch.cuda.synchronize()
             a_ms = pdist.max_over_ranks(float(sum(a0[i].elapsed_time(a1[i]) for i in range(n_a))), dist, dev)
             res[key] = pdist.throughput(1, world, n_a, a_ms)
         adjoint_mode = {"value": res["value"], "unit": "frames/s", "beta_only": res["beta_only"],
-                        "image_only": res["image_only"], "all": res["all"], "api": "p2s_backward",
+                        "image_only": res["image_only"], "all": res["all"],
+                        "zernike_only": res["zernike_only"], "all_with_zernike": res["all_with_zernike"],
+                        "api": "p2s_backward + p2s_mlp_backward",
                         "note": "value: dL/dbeta [K,H,W] + dL/dt [2,H,W] of one cfg3 frame (L2 flushed per "
                                 "call): dL/dJ scatter, one fused pass (MLP + convolutions -> J, dL/dbeta), "
                                 "dL/dt; beta_only: scatter + conv-only pass; image_only: dL/dI [C,H,W] "
-                                "(scatter, fused pass -> U = beta dL/dJ, k_adjoint_image); all: the three"}
+                                "(scatter, fused pass -> U = beta dL/dJ, k_adjoint_image); all: the three; zernike_only: "
+                                "dL/dz [n_in,H,W] (beta_only's pass, then k_mlp_backward through the MLP); "
+                                "all_with_zernike: the four"}
         del aimg, az, at, ag
 
     # ---- colour mode: per-channel Zernike fields (the

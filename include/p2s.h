@@ -210,6 +210,7 @@ typedef struct {
   int smem_bytes;                    /* dynamic shared memory of the fused kernel */
   int kernels_per_render;            /* launches queued by one p2s_render */
   int stage_bytes, nring;            /* B-operand ring: bytes per stage, stages */
+  int mlp_backward;                  /* 1: p2s_mlp_backward supports this MLP (weights fit one SM) */
 } p2s_info;
 P2S_API p2s_status p2s_get_info(const p2s_handle* h, p2s_info* info);
 

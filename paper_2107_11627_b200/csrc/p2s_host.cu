@@ -1274,6 +1274,7 @@ p2s_status p2s_get_info(const p2s_handle* h, p2s_info* info) {
   info->kernels_per_render = 2;
   info->stage_bytes = h->stage_bytes;
   info->nring = h->nring;
+  info->mlp_backward = h->mb_ok;
   return P2S_OK;
 }
 

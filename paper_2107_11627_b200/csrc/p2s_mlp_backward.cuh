@@ -136,7 +136,9 @@ __global__ void __launch_bounds__(kMbThreads, 1) k_mlp_backward(const __grid_con
   tc_fence_before();
   __syncthreads();
   tc_fence_after();
-  const uint32_t tmem = *tmem_slot;
+  // broadcast from lane 0 so that ptxas keeps the UMMA operands on the uniform datapath (no
+  // per-UMMA elect loops; tests/test_abi_cpu.py checks the SASS)
+  const uint32_t tmem = __shfl_sync(0xffffffffu, *tmem_slot, 0);
   const uint32_t tq = tmem + ((uint32_t)(32 * (warp & 3)) << 16);  // this warp's lane quadrant
   if (tid == 0 && (int)blockIdx.x < p.ntiles) {
     mbar_arrive_expect_tx(bar_w, (uint32_t)p.wbytes);

@@ -57,7 +57,7 @@ class _Image(ctypes.Structure):
 class Info(ctypes.Structure):
     _fields_ = [(n, ctypes.c_int) for n in ("K", "S", "n_in", "h1", "h2", "n_pad", "h1_pad", "h2_pad",
                                             "in_pad", "conv_steps", "smem_bytes", "kernels_per_render",
-                                            "stage_bytes", "nring")]
+                                            "stage_bytes", "nring", "mlp_backward")]
 
     def as_dict(self):
         return {n: getattr(self, n) for n, _ in self._fields_}

@@ -115,3 +115,15 @@ def test_sass_adjoint_image_kernel(lib):
     region = ins[max(0, mma[0] - 40):mma[-1] + 20]
     for bad in ("BRA.DIV", "BRA.U.ANY", "R2UR.BROADCAST"):
         assert not any(bad in x for x in region), bad
+
+
+def test_sass_mlp_backward_kernel(lib):
+    """dL/dz (k_mlp_backward, both bias modes): 1-CTA UMMAs (kind::f16), TMEM loads, the resident
+    weights brought in by bulk async copies, and no HMMA (SASS evidence)."""
+    sass = os.popen(f"cuobjdump -sass {lib._name}").read()
+    funcs = [f for f in sass.split("Function : ")[1:] if f.startswith("_ZN3p2s14k_mlp_backward")]
+    assert len(funcs) == 2
+    for f in funcs:
+        assert "UTCHMMA" in f and "UTCHMMA.2CTA" not in f
+        assert "LDTM" in f and "UBLKCP" in f
+        assert "HMMA" not in f.replace("UTCHMMA", "")
