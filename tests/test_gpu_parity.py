@@ -712,7 +712,8 @@ def test_large_ragged_frame_sampled(p2s):
 # ---- dL/dz through the P2S MLP (p2s_mlp_backward; the adjoint of step a1), vs
 #      oracle.adjoint.mlp_backward with the masks decided in the GPU's fp16 precision (reading N5)
 
-DZ_CASES = ["cfg1", "ragged_rgb_S7", "S33_K100_C2", "S1_K1", "S17_K128_n64", "S25", "W1_H1", "many_tiles_C1_S9"]
+DZ_CASES = ["cfg1", "ragged_rgb_S7", "narrow_S15_K16", "S33_K100_C2", "S1_K1", "S17_K128_n64", "S25", "W1_H1",
+            "many_tiles_C1_S9"]
 
 
 def _dz_ref(inp, gbeta, amb_rel=(2e-5, 2e-4)):
