@@ -654,6 +654,10 @@ def test_outputs_stay_in_bounds(p2s, name):
     bb, beta, pbb = _guarded((B, spec.K, H, W))
     r.debug_beta(z, out=beta)
     checks.append(("debug_beta", bb, pbb))
+    if r.info()["mlp_backward"]:
+        gz_buf, gz, pz = _guarded((B, spec.n_in, H, W))
+        r.mlp_backward(z, gb, out=gz)
+        checks.append(("dL/dz", gz_buf, pz))
     torch.cuda.synchronize()
     for what, b, p in checks:
         assert _margins_ok(b, p), f"{what} wrote outside its buffer"

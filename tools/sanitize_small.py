@@ -1,5 +1,5 @@
 """Small invocations of every device entry point (for compute-sanitizer runs): render, anchors,
-sequence, colour, sampler, backward (all three gradients) on ragged shapes."""
+sequence, colour, sampler, backward (all three gradients, and dL/dz) on ragged shapes."""
 import sys
 
 import numpy as np
@@ -24,6 +24,7 @@ for spec in (synth.custom("san1", 601, B=2, C=3, H=21, W=150, K=20, S=7, h1=48, 
     g = d(synth.make_upstream_grad(spec))
     r.backward(img, z, t, g, want_image=True)
     r.backward(img, z, None, g, want_tilt=False)
+    r.backward(img, z, t, g, want_zernike=True)
     smp = p2s.Sampler(6, spec.n_in, 1.5)
     smp.sample(7, 0, 2)
     torch.cuda.synchronize()
