@@ -895,3 +895,51 @@ def test_mlp_backward_invalid_and_unsupported(p2s):
         r.mlp_backward(_dev(big.zernike), _dev(np.zeros((B, 100, H, W), np.float32)))
     assert ei.value.status == p2s.P2S_ERR_UNSUPPORTED
     r.close()
+
+
+# ---- properties at the bench size (hold at any size; SPEC S:272, S:280 test ideas; north-star b)
+
+def test_cfg3_beta_pixel_permutation_equivariance(p2s):
+    """The P2S MLP acts per pixel: permuting the Zernike field's pixels permutes
+    beta the same way, bit for bit, at the full 512x512 size (every tile position, both CTA
+    ranks, the ragged-free bench launch)."""
+    spec = synth.CONFIGS[3]
+    inp = synth.make_inputs(spec)
+    r = p2s.Renderer(inp.basis, inp.mlp)
+    z = inp.zernike[:1]
+    _, n_in, H, W = z.shape
+    perm = np.random.default_rng(21).permutation(H * W)
+    zp = np.ascontiguousarray(z.reshape(1, n_in, -1)[:, :, perm].reshape(z.shape))
+    b0 = r.debug_beta(_dev(z)).cpu().numpy().reshape(1, spec.K, -1)
+    b1 = r.debug_beta(_dev(zp)).cpu().numpy().reshape(1, spec.K, -1)
+    np.testing.assert_array_equal(b1, b0[:, :, perm])
+    r.close()
+
+
+def test_cfg3_zero_mlp_gives_zero_frame(p2s):
+    """W = 0, b = 0 -> beta = 0 -> J = 0 -> out = 0 exactly, whatever the image and tilt."""
+    spec = synth.CONFIGS[3]
+    inp = synth.make_inputs(spec)
+    zero = {k: np.zeros_like(v) for k, v in inp.mlp.items()}
+    r = p2s.Renderer(inp.basis, zero)
+    out = r.render(_dev(inp.image), _dev(inp.zernike), _dev(inp.tilt)).cpu().numpy()
+    assert not np.any(out)
+    r.close()
+
+
+def test_cfg3_linearity_in_the_image(p2s):
+    """north-star (b) at the bench size: out(a I1 + b I2) = a out(I1) + b out(I2) with fixed
+    Zernike and tilt fields, within the render bar on every output (the fp16 rounding of each
+    image is the only difference)."""
+    spec = synth.CONFIGS[3]
+    i1 = synth.make_inputs(spec, frames=[0])
+    i2 = synth.make_inputs(spec, frames=[1])
+    r = p2s.Renderer(i1.basis, i1.mlp)
+    z, t = _dev(i1.zernike), _dev(i1.tilt)
+    a, b = 0.625, 0.375  # a + b = 1 keeps the mix in [0, 1], as the inputs
+    mix = (a * i1.image.astype(np.float64) + b * i2.image.astype(np.float64)).astype(np.float32)
+    o1 = r.render(_dev(i1.image), z, t).cpu().numpy().astype(np.float64)
+    o2 = r.render(_dev(i2.image), z, t).cpu().numpy().astype(np.float64)
+    om = r.render(_dev(mix), z, t).cpu().numpy().astype(np.float64)
+    _cmp(om, a * o1 + b * o2, "render linearity[cfg3 full frame]")
+    r.close()

@@ -1,5 +1,5 @@
 """Time p2s_backward's pieces on cfg3 (GPU only; for ncu launch lists and quick A/B):
-python tools/adjoint_time.py [iters] [image|beta|tilt|all]"""
+python tools/adjoint_time.py [iters] [image|beta|tilt|zernike|all|all4]  (all4: all + dL/dz)"""
 import sys
 
 import numpy as np
@@ -16,7 +16,8 @@ g = synth.make_upstream_grad(spec)
 r = p2s.Renderer(inp.basis, inp.mlp)
 d = lambda a: torch.from_numpy(np.ascontiguousarray(a)).cuda()  # noqa: E731
 img, z, t, gg = d(inp.image), d(inp.zernike), d(inp.tilt), d(g)
-kw = dict(want_beta=what in ("beta", "all"), want_tilt=what in ("tilt", "all"), want_image=what in ("image", "all"))
+kw = dict(want_beta=what in ("beta", "all", "all4"), want_tilt=what in ("tilt", "all", "all4"),
+          want_image=what in ("image", "all", "all4"), want_zernike=what in ("zernike", "all4"))
 for _ in range(3):
     r.backward(img, z, t, gg, **kw)
 torch.cuda.synchronize()
