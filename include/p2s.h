@@ -169,9 +169,10 @@ P2S_API p2s_status p2s_backward(p2s_handle* h, p2s_image image, const float* zer
  * of two before rounding (any finite range); the masks are decided on the fp16-operand fp32
  * accumulators (reading N5), so a pre-activation within rounding of 0 may take
  * either side. Asynchronous on `stream`; no allocation. Errors: NULL pointers, B/H/W < 1 or
- * grad_zernike overlapping an input -> P2S_ERR_INVALID_ARG; weights that do not fit one SM's
- * shared memory next to a [128][max width] activation tile (e.g. 33-256-256-100) ->
- * P2S_ERR_UNSUPPORTED; launch failure -> P2S_ERR_CUDA. */
+ * grad_zernike overlapping an input -> P2S_ERR_INVALID_ARG; frames whose channel planes exceed
+ * 2^31 elements -> P2S_ERR_UNSUPPORTED; launch failure -> P2S_ERR_CUDA. MLPs whose weights do not
+ * all fit one SM next to the activation tile (e.g. 33-256-256-100) run a variant that streams
+ * W1 / W3 from L2; every MLP p2s_init accepts is supported (p2s_info.mlp_backward = 1). */
 P2S_API p2s_status p2s_mlp_backward(p2s_handle* h, const float* zernike_field, const float* grad_beta, int B,
                                     int H, int W, float* grad_zernike, p2s_stream_t stream);
 
@@ -210,7 +211,7 @@ typedef struct {
   int smem_bytes;                    /* dynamic shared memory of the fused kernel */
   int kernels_per_render;            /* launches queued by one p2s_render */
   int stage_bytes, nring;            /* B-operand ring: bytes per stage, stages */
-  int mlp_backward;                  /* 1: p2s_mlp_backward supports this MLP (weights fit one SM) */
+  int mlp_backward;                  /* 1: p2s_mlp_backward supports this MLP (all p2s_init accepts) */
 } p2s_info;
 P2S_API p2s_status p2s_get_info(const p2s_handle* h, p2s_info* info);
 

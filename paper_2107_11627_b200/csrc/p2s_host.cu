@@ -128,7 +128,7 @@ struct p2s_handle {
   PFN_cuTensorMapEncodeTiled encode = nullptr;
   // dL/dz (k_mlp_backward): resident weight pack and its shared-memory plan (mb_ok = it fits)
   uint8_t* d_mlpb = nullptr;
-  int mb_ok = 0, mb_fold = 0, mb_smem = 0, mb_off_w2 = 0, mb_off_w3 = 0, mb_off_bias = 0, mb_wbytes = 0, mb_off_act = 0,
+  int mb_ok = 0, mb_fold = 0, mb_ring = 0, mb_g3 = 1, mb_nring = 0, mb_slab = 0, mb_off_ring = 0, mb_ring_src_off = 0, mb_smem = 0, mb_off_w2 = 0, mb_off_w3 = 0, mb_off_bias = 0, mb_wbytes = 0, mb_off_act = 0,
       mb_off_bar = 0;
   MlpOp ops[kMaxOps];  // [0, n_ops) per-tile ops, then n_fops first-tile whole-layer ops
   int n_ops = 0, n_fops = 0;
@@ -750,63 +750,117 @@ p2s_status p2s_init(const p2s_basis* basis, const p2s_mlp* mlp, p2s_handle** out
   {
     // ---- dL/dz plan (p2s_mlp_backward.cuh): W1 [N1][K1], W2 [N2][N1], W3^T [N2][Nk] as K-major
     // fp16 tiles + fp32 biases, resident in shared memory with one [128][max K] activation buffer.
-    // MLPs too large for that (e.g. 33-256-256-100) leave mb_ok = 0: p2s_mlp_backward returns
-    // P2S_ERR_UNSUPPORTED for them.
+    // When all three do not fit (e.g. 33-256-256-100), the ring variant keeps W2 resident and
+    // streams W1 / W3^T / W1^T slabs through a 3-slot ring; if even that does not fit, mb_ok = 0
+    // and p2s_mlp_backward returns P2S_ERR_UNSUPPORTED.
     const int K1 = h->K1, N1 = h->N1, N2 = h->N2, Nk = h->Nk;
     const int w1 = N1 * K1 * 2, w2 = N2 * N1 * 2, w3 = N2 * Nk * 2, bb = (N1 + N2) * 4;
-    const int wbytes = w1 + w2 + w3 + bb;
     const int kact = std::max(std::max(K1, N1), std::max(N2, Nk));
-    const int off_act = (wbytes + 127) / 128 * 128, off_bar = off_act + 128 * kact * 2;
-    const int smem = off_bar + 32 + 4 * 128 * 4;
+    const int act_bytes = 128 * kact * 2, bar_bytes = 32 + 4 * 128 * 4 + 16 * 8;
+    auto al128 = [](int v) { return (v + 127) / 128 * 128; };
+    const int smem_res = al128(w1 + w2 + w3 + bb) + act_bytes + bar_bytes;
+    const int slab = std::max(std::max(N1, N2), K1) * 32, nring_mb = 3;
+    const int smem_ring = al128(w2 + bb) + al128(nring_mb * slab) + act_bytes + bar_bytes;
+    // (P2S_MB_RING=1 forces the ring variant: tests cover it on MLPs that would fit resident)
+    const bool ring = smem_res > kSmemLimit || (std::getenv("P2S_MB_RING") && std::atoi(std::getenv("P2S_MB_RING")) != 0);
+    const int smem = ring ? smem_ring : smem_res;
     // biases as fp16 hi/lo pairs on constant-1 inputs when each layer input has 2 spare columns
     const bool fold = h->n_in + 2 <= K1 && h->h1 + 2 <= N1;
     if (smem <= kSmemLimit && K1 <= 64) {
-      std::vector<uint8_t> pk((size_t)wbytes, 0);
-      __half* hp = reinterpret_cast<__half*>(pk.data());
-      // element (n, k) of a K-major tile [rows][kd]: (n%8)*16 + (n/8)*kd*16 + (k%8)*2 + (k/8)*128 bytes
+      // standard K-major tiles: element (n, k) of [rows][kd] at (n%8)*16 + (n/8)*kd*16 + (k%8)*2 + (k/8)*128
       auto at = [](int n, int k, int kd) { return ((n % 8) * 16 + (n / 8) * kd * 16 + (k % 8) * 2 + (k / 8) * 128) / 2; };
+      std::vector<__half> W1h((size_t)N1 * K1, __float2half(0.f)), W2h((size_t)N2 * N1, __float2half(0.f)),
+          W3h((size_t)N2 * Nk, __float2half(0.f));
       for (int j = 0; j < h->h1; ++j)
-        for (int i = 0; i < h->n_in; ++i) hp[at(j, i, K1)] = __float2half_rn(mlp->W1[(size_t)j * h->n_in + i]);
+        for (int i = 0; i < h->n_in; ++i) W1h[at(j, i, K1)] = __float2half_rn(mlp->W1[(size_t)j * h->n_in + i]);
       for (int j = 0; j < h->h2; ++j)
-        for (int i = 0; i < h->h1; ++i) hp[w1 / 2 + at(j, i, N1)] = __float2half_rn(mlp->W2[(size_t)j * h->h1 + i]);
+        for (int i = 0; i < h->h1; ++i) W2h[at(j, i, N1)] = __float2half_rn(mlp->W2[(size_t)j * h->h1 + i]);
       for (int j = 0; j < h->h2; ++j)
-        for (int k = 0; k < K; ++k) hp[(w1 + w2) / 2 + at(j, k, Nk)] = __float2half_rn(mlp->W3[(size_t)k * h->h2 + j]);
-      float* bp = reinterpret_cast<float*>(pk.data() + w1 + w2 + w3);
-      for (int j = 0; j < h->h1; ++j) bp[j] = mlp->b1[j];
-      for (int j = 0; j < h->h2; ++j) bp[N1 + j] = mlp->b2[j];
+        for (int k = 0; k < K; ++k) W3h[at(j, k, Nk)] = __float2half_rn(mlp->W3[(size_t)k * h->h2 + j]);
       if (fold) {
         // z columns n_in, n_in + 1 are 1: W1 carries b1 there as hi + lo; W1 rows h1, h1 + 1 turn
         // them into a1 columns h1, h1 + 1 = 1, where W2 carries b2 as hi + lo
         auto hi = [](float v) { return __float2half_rn(v); };
         auto lo = [](float v) { return __float2half_rn(v - __half2float(__float2half_rn(v))); };
         for (int j = 0; j < h->h1; ++j) {
-          hp[at(j, h->n_in, K1)] = hi(mlp->b1[j]);
-          hp[at(j, h->n_in + 1, K1)] = lo(mlp->b1[j]);
+          W1h[at(j, h->n_in, K1)] = hi(mlp->b1[j]);
+          W1h[at(j, h->n_in + 1, K1)] = lo(mlp->b1[j]);
         }
-        hp[at(h->h1, h->n_in, K1)] = __float2half_rn(1.f);
-        hp[at(h->h1 + 1, h->n_in, K1)] = __float2half_rn(1.f);
+        W1h[at(h->h1, h->n_in, K1)] = __float2half_rn(1.f);
+        W1h[at(h->h1 + 1, h->n_in, K1)] = __float2half_rn(1.f);
         for (int j = 0; j < h->h2; ++j) {
-          hp[w1 / 2 + at(j, h->h1, N1)] = hi(mlp->b2[j]);
-          hp[w1 / 2 + at(j, h->h1 + 1, N1)] = lo(mlp->b2[j]);
+          W2h[at(j, h->h1, N1)] = hi(mlp->b2[j]);
+          W2h[at(j, h->h1 + 1, N1)] = lo(mlp->b2[j]);
         }
       }
-      if ((e = cudaMalloc(&h->d_mlpb, pk.size())) != cudaSuccess ||
-          (e = cudaMemcpy(h->d_mlpb, pk.data(), pk.size(), cudaMemcpyHostToDevice)) != cudaSuccess)
+      std::vector<float> bias((size_t)N1 + N2, 0.f);
+      for (int j = 0; j < h->h1; ++j) bias[j] = mlp->b1[j];
+      for (int j = 0; j < h->h2; ++j) bias[N1 + j] = mlp->b2[j];
+      // resident pack [W1 | W2 | W3^T | b1 | b2], or (ring) [W2 | b1 | b2] + the slab table
+      std::vector<uint8_t> pk;
+      auto append = [&](const void* src, size_t n) {
+        const size_t o = pk.size();
+        pk.resize(o + n);
+        std::memcpy(pk.data() + o, src, n);
+      };
+      if (!ring) {
+        append(W1h.data(), w1);
+        append(W2h.data(), w2);
+        append(W3h.data(), w3);
+      } else {
+        append(W2h.data(), w2);
+      }
+      append(bias.data(), bb);
+      std::vector<uint8_t> slabs;
+      if (ring) {
+        // per-tile order [F1: W1 K-slabs | B1: W3^T K-slabs | B3: W1 row pairs (= W1^T K'-slabs)],
+        // K-slabs re-laid [N][16] (lbo 128, sbo 256), W1 row pairs as stored (2 x 8 rows x K1)
+        const int g3 = std::max(1, slab / (K1 * 32)), nb3 = N1 / 16;
+        const int nsl = K1 / 16 + Nk / 16 + (nb3 + g3 - 1) / g3;
+        slabs.assign((size_t)nsl * slab, 0);
+        int i = 0;
+        auto kslab = [&](const std::vector<__half>& Wt, int N, int kd, int ks) {
+          __half* d = reinterpret_cast<__half*>(slabs.data() + (size_t)i * slab);
+          for (int n = 0; n < N; ++n)
+            for (int kk = 0; kk < 16; ++kk)
+              d[((n % 8) * 16 + (n / 8) * 256 + (kk % 8) * 2 + (kk / 8) * 128) / 2] = Wt[at(n, 16 * ks + kk, kd)];
+          ++i;
+        };
+        for (int ks = 0; ks < K1 / 16; ++ks) kslab(W1h, N1, K1, ks);
+        for (int ks = 0; ks < Nk / 16; ++ks) kslab(W3h, N2, Nk, ks);
+        for (int ks = 0; ks < nb3; ks += g3, ++i)  // g3 W1 row pairs per slot
+          std::memcpy(slabs.data() + (size_t)i * slab, reinterpret_cast<const uint8_t*>(W1h.data()) + (size_t)ks * K1 * 32,
+                      (size_t)std::min(g3, nb3 - ks) * K1 * 32);
+        h->mb_g3 = g3;
+      }
+      if ((e = cudaMalloc(&h->d_mlpb, pk.size() + slabs.size())) != cudaSuccess ||
+          (e = cudaMemcpy(h->d_mlpb, pk.data(), pk.size(), cudaMemcpyHostToDevice)) != cudaSuccess ||
+          (ring && (e = cudaMemcpy(h->d_mlpb + pk.size(), slabs.data(), slabs.size(), cudaMemcpyHostToDevice)) !=
+                       cudaSuccess))
         return fail(cuda_fail(e, "dz weight pack"));
-      if ((e = cudaFuncSetAttribute(k_mlp_backward<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem)) !=
+      if ((e = cudaFuncSetAttribute(k_mlp_backward<true, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem)) !=
               cudaSuccess ||
-          (e = cudaFuncSetAttribute(k_mlp_backward<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem)) !=
+          (e = cudaFuncSetAttribute(k_mlp_backward<false, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem)) !=
+              cudaSuccess ||
+          (e = cudaFuncSetAttribute(k_mlp_backward<true, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem)) !=
+              cudaSuccess ||
+          (e = cudaFuncSetAttribute(k_mlp_backward<false, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem)) !=
               cudaSuccess)
         return fail(cuda_fail(e, "cudaFuncSetAttribute(k_mlp_backward)"));
       h->mb_ok = 1;
       h->mb_fold = fold ? 1 : 0;
+      h->mb_ring = ring ? 1 : 0;
       h->mb_smem = smem;
-      h->mb_off_w2 = w1;
-      h->mb_off_w3 = w1 + w2;
-      h->mb_off_bias = w1 + w2 + w3;
-      h->mb_wbytes = wbytes;
-      h->mb_off_act = off_act;
-      h->mb_off_bar = off_bar;
+      h->mb_off_w2 = ring ? 0 : w1;
+      h->mb_off_w3 = ring ? 0 : w1 + w2;
+      h->mb_off_bias = ring ? w2 : w1 + w2 + w3;
+      h->mb_wbytes = (int)pk.size();
+      h->mb_off_ring = al128((int)pk.size());
+      h->mb_off_act = ring ? h->mb_off_ring + al128(nring_mb * slab) : al128((int)pk.size());
+      h->mb_off_bar = h->mb_off_act + act_bytes;
+      h->mb_nring = nring_mb;
+      h->mb_slab = slab;
+      h->mb_ring_src_off = (int)pk.size();
     }
   }
   *out_handle = h;
@@ -1038,9 +1092,17 @@ p2s_status p2s_mlp_backward(p2s_handle* h, const float* zernike_field, const flo
   p.ntiles = (int)(tpf * B);
   p.off_w2 = h->mb_off_w2; p.off_w3 = h->mb_off_w3; p.off_bias = h->mb_off_bias; p.wbytes = h->mb_wbytes;
   p.off_act = h->mb_off_act; p.off_bar = h->mb_off_bar;
+  p.ring_src = h->d_mlpb + h->mb_ring_src_off;
+  p.off_ring = h->mb_off_ring; p.nring = h->mb_nring; p.slab_stride = h->mb_slab; p.g3 = h->mb_g3;
   const int grid = std::min(p.ntiles, h->sm_count);
-  if (h->mb_fold) k_mlp_backward<true><<<grid, kMbThreads, h->mb_smem, (cudaStream_t)stream>>>(p);
-  else k_mlp_backward<false><<<grid, kMbThreads, h->mb_smem, (cudaStream_t)stream>>>(p);
+  cudaStream_t st = (cudaStream_t)stream;
+  if (h->mb_ring) {
+    if (h->mb_fold) k_mlp_backward<true, true><<<grid, kMbThreadsRing, h->mb_smem, st>>>(p);
+    else k_mlp_backward<false, true><<<grid, kMbThreadsRing, h->mb_smem, st>>>(p);
+  } else {
+    if (h->mb_fold) k_mlp_backward<true, false><<<grid, kMbThreads, h->mb_smem, st>>>(p);
+    else k_mlp_backward<false, false><<<grid, kMbThreads, h->mb_smem, st>>>(p);
+  }
   P2S_CUDA(cudaPeekAtLastError());
   return P2S_OK;
 }

@@ -52,9 +52,17 @@ struct MlpbParams {
   int tiles_per_frame, ntiles;
   int off_w2, off_w3, off_bias, wbytes;  // byte offsets in wpack (= in shared memory)
   int off_act, off_bar;
+  // kRing (MLPs whose three weight matrices do not all fit, e.g. 33-256-256-100): only W2 (used
+  // twice per tile) is resident; the F1 / B1 / B3 operands (W1 slabs, W3^T slabs, W1^T slabs)
+  // stream from an L2-resident table through a ring of nring slots of slab_stride bytes, fed by
+  // a producer warp, in the fixed per-tile order [F1: K1/16 | B1: Nk/16 | B3: N1/16 slabs]
+  // (B3's W1^T K'-steps are small, K1 x 32 B: g3 of them share one slot, contiguous in W1's layout)
+  const uint8_t* ring_src;
+  int off_ring, nring, slab_stride, g3;
 };
 
-constexpr int kMbThreads = 512;
+constexpr int kMbThreads = 512;      // drain/staging threads (16 warps)
+constexpr int kMbThreadsRing = 544;  // + one producer warp in the ring variant
 
 namespace mlpb {
 
@@ -68,6 +76,30 @@ P2S_DEV void gemm(uint32_t d, uint32_t a_s, int nks, uint32_t b_s, uint32_t b_lb
     umma_f16_elect(d, sdesc(a_s + (uint32_t)ks * 256u, 128u, a_sbo),
                    sdesc(b_s + (uint32_t)ks * b_kstep, b_lbo, b_sbo), idesc, ks > 0 ? 1u : 0u);
 }
+
+// D[128 x N] = ACT * B^T with each 16-wide K-step of B taken from the next ring slot
+// (K-major slabs: lbo 128, sbo 256; W1^T slabs: lbo 16 K1, sbo 128); each slot is released to the
+// producer by a commit once the UMMA reading it completes
+// (per_slot K-steps per ring slot, kstep bytes apart inside it)
+P2S_DEV void gemm_ring(uint32_t d, uint32_t a_s, int nks, uint32_t ring_s, uint32_t stride, uint32_t b_lbo,
+                       uint32_t b_sbo, uint32_t idesc, uint64_t* full, uint64_t* empty, int nring, int& s,
+                       uint32_t& ph, int per_slot = 1, uint32_t kstep = 0) {
+  const uint32_t a_sbo = (uint32_t)nks * 256u;
+  for (int k0 = 0; k0 < nks; k0 += per_slot) {
+    mbar_wait(&full[s], ph);
+    tc_fence_after();
+    const int k1 = min(nks, k0 + per_slot);
+    for (int ks = k0; ks < k1; ++ks)
+      umma_f16_elect(d, sdesc(a_s + (uint32_t)ks * 256u, 128u, a_sbo),
+                     sdesc(ring_s + (uint32_t)s * stride + (uint32_t)(ks - k0) * kstep, b_lbo, b_sbo), idesc,
+                     ks > 0 ? 1u : 0u);
+    umma_commit_elect(&empty[s]);
+    if (++s == nring) { s = 0; ph ^= 1; }
+  }
+}
+
+// the 512 drain threads' barrier (the ring variant's producer warp does not take part)
+P2S_DEV void drain_sync() { asm volatile("bar.sync 1, 512;" ::: "memory"); }
 
 // this thread's row of a K-major [128][kd] fp16 tile: element (m, k) at
 // (m%8)*16 + (m/8)*kd*16 + (k%8)*2 + (k/8)*128
@@ -90,7 +122,7 @@ P2S_DEV float exp2i(int e) { return __int_as_float((e + 127) << 23); }  // 2^e, 
 P2S_DEV void publish() {
   fence_proxy_async_smem();
   tc_fence_before();
-  __syncthreads();
+  drain_sync();
 }
 
 }  // namespace mlpb
@@ -111,8 +143,9 @@ P2S_DEV void load_z(const MlpbParams& p, int t, int m, int q, float (&zv)[2][8])
   }
 }
 
-template <bool kFold>
-__global__ void __launch_bounds__(kMbThreads, 1) k_mlp_backward(const __grid_constant__ MlpbParams p) {
+template <bool kFold, bool kRing>
+__global__ void __launch_bounds__(kRing ? kMbThreadsRing : kMbThreads, 1)
+    k_mlp_backward(const __grid_constant__ MlpbParams p) {
   using namespace mlpb;
   extern __shared__ __align__(1024) uint8_t smem[];
   const uint32_t sbase = smem_u32(smem);
@@ -127,9 +160,16 @@ __global__ void __launch_bounds__(kMbThreads, 1) k_mlp_backward(const __grid_con
   const int tid = (int)threadIdx.x, warp = (int)warp_id();
   const int m = tid & 127, q = tid >> 7;  // pixel row (TMEM lane) and column quarter
 
+  uint64_t* ring_full = reinterpret_cast<uint64_t*>(smem + p.off_bar + 32 + 2048);
+  uint64_t* ring_empty = ring_full + 8;
   if (tid == 0) {
     mbar_init(bar_w, 1);
     mbar_init(bar_mma, 1);
+    if (kRing)
+      for (int i = 0; i < p.nring; ++i) {
+        mbar_init(&ring_full[i], 1);
+        mbar_init(&ring_empty[i], 1);
+      }
     fence_mbar_init();
   }
   if (warp == 0) tmem_alloc<512>(tmem_slot);
@@ -146,6 +186,28 @@ __global__ void __launch_bounds__(kMbThreads, 1) k_mlp_backward(const __grid_con
       bulk_g2s(smem + off, p.wpack + off, (uint32_t)min(32768, p.wbytes - off), bar_w);
   }
 
+  if (kRing && warp == 16) {
+    // ---- producer (ring variant): the per-tile slab sequence, one bulk copy per slab
+    if (lane_id() == 0) {
+      const int n_f1 = p.K1 / 16, n_b1 = p.Nk / 16, nb3 = p.N1 / 16, nsl = n_f1 + n_b1 + (nb3 + p.g3 - 1) / p.g3;
+      int s = 0;
+      uint32_t ph = 0;
+      for (int t = (int)blockIdx.x; t < p.ntiles; t += (int)gridDim.x)
+        for (int i = 0; i < nsl; ++i) {
+          mbar_wait(&ring_empty[s], ph ^ 1);
+          const int i3 = i - n_f1 - n_b1;  // B3 item: K'-steps [g3 i3, min(nb3, g3 (i3 + 1)))
+          const uint32_t bytes = (uint32_t)(i < n_f1 ? p.N1 * 32
+                                                     : (i3 < 0 ? p.N2 * 32 : min(p.g3, nb3 - p.g3 * i3) * p.K1 * 32));
+          mbar_arrive_expect_tx(&ring_full[s], bytes);
+          bulk_g2s(smem + p.off_ring + s * p.slab_stride, p.ring_src + (size_t)i * p.slab_stride, bytes, &ring_full[s]);
+          if (++s == p.nring) { s = 0; ph ^= 1; }
+        }
+    }
+    __syncwarp();
+  } else {
+  const uint32_t ring_s = sbase + (uint32_t)p.off_ring, stride = (uint32_t)p.slab_stride;
+  int rs = 0;
+  uint32_t rph = 0;
   const uint32_t id_f1 = idesc_f16(128, (uint32_t)p.N1), id_f2 = idesc_f16(128, (uint32_t)p.N2);
   const uint32_t id_b2 = idesc_f16(128, (uint32_t)p.N1) | (1u << 16);
   const uint32_t id_b3 = idesc_f16(128, (uint32_t)p.K1) | (1u << 16);
@@ -197,7 +259,8 @@ __global__ void __launch_bounds__(kMbThreads, 1) k_mlp_backward(const __grid_con
     }
     if (warp == 0) {
       tc_fence_after();
-      gemm(tmem, act_s, p.K1 / 16, w1_s, 128u, (uint32_t)p.K1 * 16u, 256u, id_f1);
+      if (kRing) gemm_ring(tmem, act_s, p.K1 / 16, ring_s, stride, 128u, 256u, id_f1, ring_full, ring_empty, p.nring, rs, rph);
+      else gemm(tmem, act_s, p.K1 / 16, w1_s, 128u, (uint32_t)p.K1 * 16u, 256u, id_f1);
       umma_commit_elect(bar_mma);
     }
     // ---- dL/dbeta of this tile into registers (in flight during F1 / F2)
@@ -252,7 +315,7 @@ __global__ void __launch_bounds__(kMbThreads, 1) k_mlp_backward(const __grid_con
     mbar_wait(bar_mma, ph);  // F2 done: ACT is free
     ph ^= 1;
     tc_fence_after();
-    __syncthreads();
+    drain_sync();
     mx = fmaxf(fmaxf(s_max[m], s_max[128 + m]), fmaxf(s_max[256 + m], s_max[384 + m]));
     // mx = f 2^ex with f in [0.5, 1) (normal mx; 0 and subnormals take ex = -126, inf/NaN 129):
     // scale by 2^-ex and back by 2^ex, each as two in-range power-of-two factors (exact)
@@ -273,7 +336,8 @@ __global__ void __launch_bounds__(kMbThreads, 1) k_mlp_backward(const __grid_con
     publish();
     if (warp == 0) {
       tc_fence_after();
-      gemm(tmem, act_s, p.Nk / 16, w3_s, 128u, (uint32_t)p.Nk * 16u, 256u, id_f2);
+      if (kRing) gemm_ring(tmem, act_s, p.Nk / 16, ring_s, stride, 128u, 256u, id_f2, ring_full, ring_empty, p.nring, rs, rph);
+      else gemm(tmem, act_s, p.Nk / 16, w3_s, 128u, (uint32_t)p.Nk * 16u, 256u, id_f2);
       umma_commit_elect(bar_mma);
     }
     mbar_wait(bar_mma, ph);
@@ -321,7 +385,10 @@ __global__ void __launch_bounds__(kMbThreads, 1) k_mlp_backward(const __grid_con
     publish();
     if (warp == 0) {
       tc_fence_after();
-      gemm(tmem, act_s, p.N1 / 16, w1_s, (uint32_t)p.K1 * 16u, 128u, (uint32_t)p.K1 * 32u, id_b3);
+      if (kRing)
+        gemm_ring(tmem, act_s, p.N1 / 16, ring_s, stride, (uint32_t)p.K1 * 16u, 128u, id_b3, ring_full, ring_empty, p.nring,
+                  rs, rph, p.g3, (uint32_t)p.K1 * 32u);
+      else gemm(tmem, act_s, p.N1 / 16, w1_s, (uint32_t)p.K1 * 16u, 128u, (uint32_t)p.K1 * 32u, id_b3);
       umma_commit_elect(bar_mma);
     }
     if (t + (int)gridDim.x < p.ntiles) load_z(p, t + (int)gridDim.x, m, q, zv);  // next tile's z
@@ -344,6 +411,7 @@ __global__ void __launch_bounds__(kMbThreads, 1) k_mlp_backward(const __grid_con
     }
     tc_fence_before();  // TMEM reads before the next tile's F1 (ordered by its publish())
   }
+  }  // drain / issue warps
   tc_fence_before();
   __syncthreads();
   tc_fence_after();

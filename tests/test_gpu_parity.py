@@ -694,6 +694,12 @@ def test_full_envelope_at_once(p2s):
     out = r.render(_dev(inp.image), _dev(inp.zernike), _dev(inp.tilt)).cpu().numpy()
     ref, _ = oracle.render(inp.image, inp.zernike, inp.tilt, inp.basis, inp.mlp)
     _cmp(out, ref, "render[envelope corner]")
+    # dL/dz at the envelope corner (ring variant: W2 resident, the other weights streamed)
+    assert r.info()["mlp_backward"] == 1
+    gbeta = _gbeta(spec, (1, 128, 10, 140), 35)
+    gz = r.mlp_backward(_dev(inp.zernike), _dev(gbeta)).cpu().numpy()
+    zref, alts = _dz_ref(inp, gbeta.astype(np.float64))
+    _dz_check(gz, zref, alts, "dL/dz[envelope corner]")
 
 
 def test_large_ragged_frame_sampled(p2s):
@@ -816,6 +822,24 @@ def test_mlp_backward_parity(p2s, name):
     r.close()
 
 
+@pytest.mark.parametrize("name", ["S65_K100_h256", "cfg1", "S33_K100_C2", "W1_H1", "many_tiles_C1_S9"])
+def test_mlp_backward_ring_variant(p2s, name, monkeypatch):
+    """The ring variant (W2 resident, W1 / W3^T / W1^T slabs streamed by a producer warp): chosen
+    for 33-256-256-100 (cfg5's MLP), forced by P2S_MB_RING=1 for MLPs that would fit resident."""
+    spec = SMALL[name]
+    if name != "S65_K100_h256":
+        monkeypatch.setenv("P2S_MB_RING", "1")
+    inp = synth.make_inputs(spec)
+    B, n_in, H, W = inp.zernike.shape
+    gbeta = _gbeta(spec, (B, spec.K, H, W), 34)
+    r = p2s.Renderer(inp.basis, inp.mlp)
+    assert r.info()["mlp_backward"] == 1
+    gz = r.mlp_backward(_dev(inp.zernike), _dev(gbeta)).cpu().numpy()
+    ref, alts = _dz_ref(inp, gbeta.astype(np.float64))
+    _dz_check(gz, ref, alts, f"dL/dz ring[{name}]")
+    r.close()
+
+
 @pytest.mark.parametrize("name", ["ragged_rgb_S7", "S33_K100_C2"])
 def test_mlp_backward_wide_range(p2s, name):
     """dL/dbeta spanning 1e-12 ... 1e12 across pixels (beyond fp16's range both ways)."""
@@ -886,14 +910,6 @@ def test_mlp_backward_invalid_and_unsupported(p2s):
     # output aliasing an input
     assert lib.p2s_mlp_backward(r._h, vp(z.data_ptr()), vp(gb.data_ptr()), B, H, W, vp(z.data_ptr()), st) == p2s.P2S_ERR_INVALID_ARG
     assert lib.p2s_mlp_backward(r._h, vp(z.data_ptr()), vp(gb.data_ptr()), B, H, W, vp(gb.data_ptr()), st) == p2s.P2S_ERR_INVALID_ARG
-    r.close()
-    # an MLP whose weights do not fit one SM next to the activation tile: unsupported, not wrong
-    big = synth.make_inputs(SMALL["S65_K100_h256"])
-    r = p2s.Renderer(big.basis, big.mlp)
-    B, n_in, H, W = big.zernike.shape
-    with pytest.raises(p2s.P2SError) as ei:
-        r.mlp_backward(_dev(big.zernike), _dev(np.zeros((B, 100, H, W), np.float32)))
-    assert ei.value.status == p2s.P2S_ERR_UNSUPPORTED
     r.close()
 
 

@@ -1,6 +1,9 @@
-"""Times p2s_mlp_backward (dL/dz through the P2S MLP) on one cfg3 frame and a 16-frame batch
-(CUDA events, L2 warm and flushed). Tools only: no oracle, synthetic inputs."""
+"""Times p2s_mlp_backward (dL/dz through the P2S MLP): one cfg3 frame and a 16-frame batch
+(resident weights), cfg3 with the ring variant forced (P2S_MB_RING=1), and one cfg5 frame
+(33-256-256-100: the ring variant). CUDA events, L2 warm and flushed. Tools only: synthetic
+inputs, no oracle."""
 import json
+import os
 import sys
 
 import numpy as np
@@ -10,15 +13,19 @@ sys.path.insert(0, ".")
 from paper_2107_11627_b200 import p2s, synth  # noqa: E402
 
 
-def main():
-    spec = synth.CONFIGS[3]
-    inp = synth.make_inputs(spec)
+def run(cfg, Bs, ring, res):
+    spec = synth.CONFIGS[cfg]
+    inp = synth.make_inputs(spec, frames=[0])
+    if ring:
+        os.environ["P2S_MB_RING"] = "1"
     r = p2s.Renderer(inp.basis, inp.mlp)
-    res = {}
+    os.environ.pop("P2S_MB_RING", None)
     flush = torch.empty(256 << 20, dtype=torch.uint8, device="cuda")
-    for B in (1, 16):
+    n_in, H, W = inp.zernike.shape[1:]
+    h1, h2, K = inp.mlp["W1"].shape[0], inp.mlp["W2"].shape[0], spec.K
+    for B in Bs:
         z = torch.from_numpy(np.ascontiguousarray(np.repeat(inp.zernike, B, 0))).cuda()
-        gb = torch.randn((B, spec.K, 512, 512), device="cuda")
+        gb = torch.randn((B, K, H, W), device="cuda")
         out = torch.empty_like(z)
         for _ in range(3):
             r.mlp_backward(z, gb, out)
@@ -34,11 +41,19 @@ def main():
                 torch.cuda.synchronize()
                 ts.append(e0.elapsed_time(e1) * 1e3)
             us = float(np.median(ts))
-            px = B * 512 * 512
-            macs = px * (33 * 200 + 200 * 200 + 100 * 200 + 200 * 200 + 200 * 33)
-            byts = px * (33 + 100 + 33) * 4
-            res[f"B{B}_{mode}"] = {"us": us, "us_per_frame": us / B, "tflops": 2 * macs / us / 1e6,
-                                   "gbs": byts / us / 1e3}
+            px = B * H * W
+            macs = px * (n_in * h1 + h1 * h2 + K * h2 + h2 * h1 + h1 * n_in)
+            byts = px * (2 * n_in + K) * 4
+            res[f"cfg{cfg}{'_ring' if ring else ''}_B{B}_{mode}"] = {
+                "us": us, "us_per_frame": us / B, "tflops": 2 * macs / us / 1e6, "gbs": byts / us / 1e3}
+    r.close()
+
+
+def main():
+    res = {}
+    run(3, (1, 16), False, res)
+    run(3, (1,), True, res)
+    run(5, (1,), False, res)
     print(json.dumps(res))
 
 
