@@ -240,3 +240,30 @@ def mlp_backward(zernike, gbeta, mlp, mask_precision="fp64", masks=None):
     g2 = (W3.T @ G3) * m2
     g1 = (W2.T @ g2) * m1
     return (W1.T @ g1).reshape(n_in, H, W)
+
+
+def anchor_weights(n, G):
+    """[n][G] fp64 matrix of the 1-D linear weights the anchor interpolation gives pixel index
+    t (0..n-1) from anchor index a (reading N1: pixel centre t + 0.5,
+    anchors at a n / (G - 1)): u = (t + 0.5)(G - 1)/n, i0 = min(floor(u), G - 2), weights
+    1 - (u - i0) on i0 and u - i0 on i0 + 1; G = 1: all weight on the single anchor."""
+    w = np.zeros((n, G))
+    if G == 1:
+        w[:, 0] = 1.0
+        return w
+    for t in range(n):
+        u = (t + 0.5) * (G - 1) / n
+        i0 = min(int(np.floor(u)), G - 2)
+        f = u - i0
+        w[t, i0] += 1.0 - f
+        w[t, i0 + 1] += f
+    return w
+
+
+def anchors_backward(gfield, G):
+    """dL/dA [B][n_in][G][G] (fp64) for dL/dz = gfield [B][n_in][H][W]: the transpose of the
+    separable bilinear anchor interpolation z = Wy A Wx^T (per frame and mode), dL/dA = Wy^T dL/dz Wx."""
+    g = np.asarray(gfield, np.float64)
+    B, n_in, H, W = g.shape
+    Wy, Wx = anchor_weights(H, G), anchor_weights(W, G)
+    return np.einsum("ya,bkyx,xc->bkac", Wy, g, Wx)

@@ -603,3 +603,24 @@ def test_mlp_preactivations_reproduce_c_oracle_beta():
     p1, p2 = adjoint.mlp_preactivations(z, inp.mlp, "fp16")
     np.testing.assert_array_equal(adjoint.mlp_backward(z, g, inp.mlp, masks=(p1 > 0, p2 > 0)),
                                   adjoint.mlp_backward(z, g, inp.mlp, "fp16"))
+
+
+def test_anchors_backward_is_the_transpose_of_the_c_interpolation():
+    """dL/dA = Wy^T dL/dz Wx is pinned against the independent C oracle of the forward
+    interpolation (p2s_oracle_interp_anchors) by the dot-product identity <g, interp(A)> =
+    <interp^T(g), A>, for several G (1, 2, 5, 16) and ragged H, W; plus closed forms: each pixel's
+    weights sum to 1, so sum(dL/dA) = sum(dL/dz), and a constant dL/dz = 1 gives
+    dL/dA[a][b] = (sum_y Wy[y][a]) (sum_x Wx[x][b])."""
+    from oracle import adjoint
+    rng = np.random.default_rng(8)
+    for G, H, W in ((1, 7, 9), (2, 5, 13), (5, 37, 29), (16, 64, 40)):
+        A = rng.standard_normal((2, 3, G, G)).astype(np.float32)
+        g = rng.standard_normal((2, 3, H, W))
+        z = oracle.interp_anchors(A, H, W)
+        gA = adjoint.anchors_backward(g, G)
+        lhs, rhs = np.sum(g * z), np.sum(gA * A.astype(np.float64))
+        assert abs(lhs - rhs) <= 1e-10 * (1 + abs(lhs)), (G, lhs, rhs)
+        np.testing.assert_allclose(gA.sum(axis=(2, 3)), g.sum(axis=(2, 3)), rtol=1e-12, atol=1e-9)
+        ones = adjoint.anchors_backward(np.ones((1, 1, H, W)), G)[0, 0]
+        wy, wx = adjoint.anchor_weights(H, G).sum(0), adjoint.anchor_weights(W, G).sum(0)
+        np.testing.assert_allclose(ones, np.outer(wy, wx), rtol=1e-12)
