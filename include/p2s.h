@@ -176,6 +176,21 @@ P2S_API p2s_status p2s_backward(p2s_handle* h, p2s_image image, const float* zer
 P2S_API p2s_status p2s_mlp_backward(p2s_handle* h, const float* zernike_field, const float* grad_beta, int B,
                                     int H, int W, float* grad_zernike, p2s_stream_t stream);
 
+/* The anchor-grid interpolation ("anchor points ... interpolated"; registration
+ * DESIGN.md reading N1 — pixel centre (t + 0.5), anchors at a n / (G - 1)) as a standalone op and
+ * its adjoint, so the anchor pipeline is differentiable end to end:
+ *   p2s_interp_anchors:  anchors (DEVICE [B][n_in][G][G] fp32) -> zernike_field (DEVICE
+ *     [B][n_in][H][W] fp32), z = Wy A Wx^T per frame and mode, the fp32 arithmetic of
+ *     p2s_render_anchors' staging (p2s_render on this field equals p2s_render_anchors);
+ *   p2s_anchors_backward: grad_zernike (DEVICE [B][n_in][H][W]) -> grad_anchors (DEVICE
+ *     [B][n_in][G][G]) = Wy^T grad_zernike Wx (deterministic: a fixed reduction order).
+ * Handle-free; asynchronous on `stream`; NULL pointers, B/n_in/H/W < 1, G outside [1, 4096] or
+ * an output overlapping the input -> P2S_ERR_INVALID_ARG; launch failure -> P2S_ERR_CUDA. */
+P2S_API p2s_status p2s_interp_anchors(const float* anchors, int B, int n_in, int G, int H, int W,
+                                      float* zernike_field, p2s_stream_t stream);
+P2S_API p2s_status p2s_anchors_backward(const float* grad_zernike, int B, int n_in, int G, int H, int W,
+                                        float* grad_anchors, p2s_stream_t stream);
+
 /* ---- correlated anchor sampling (Sec. 3.4: anchor
  * coefficient sets "drawn from the correlation matrix", which "can be pre-computed") ----
  * Stand-in covariance (reading N3; the paper's Takato-formula parameters are absent):

@@ -10,7 +10,7 @@ ROOT = os.path.dirname(PKG)
 CSRC = os.path.join(PKG, "csrc")
 LIB = os.path.join(PKG, "libp2s.so")
 LIB_PROF = os.path.join(PKG, "libp2s_prof.so")  # -DP2S_PROFILE variant (tools only)
-SOURCES = [os.path.join(CSRC, "p2s_host.cu"), os.path.join(CSRC, "p2s_sampler.cu")]
+SOURCES = [os.path.join(CSRC, "p2s_host.cu"), os.path.join(CSRC, "p2s_sampler.cu"), os.path.join(CSRC, "p2s_anchor.cu")]
 DEPS = SOURCES + [os.path.join(CSRC, f) for f in ("p2s_kernels.cuh", "sm100.cuh", "p2s_adjoint.cuh", "p2s_mlp_backward.cuh")] + \
     [os.path.join(ROOT, "include", "p2s.h")]
 NVCC = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")

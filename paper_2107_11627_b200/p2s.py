@@ -27,7 +27,8 @@ EXPORTED = ("p2s_init", "p2s_render", "p2s_render_host", "p2s_reserve", "p2s_set
             "p2s_debug_beta", "p2s_debug_blur", "p2s_debug_profile_buffer",
             "p2s_render_anchors", "p2s_render_anchors_host", "p2s_debug_blur_anchors",
             "p2s_render_sequence", "p2s_sampler_init", "p2s_sample_anchors", "p2s_sampler_destroy",
-            "p2s_backward", "p2s_render_color", "p2s_mlp_backward")
+            "p2s_backward", "p2s_render_color", "p2s_mlp_backward", "p2s_interp_anchors",
+            "p2s_anchors_backward")
 
 
 class P2SError(RuntimeError):
@@ -101,12 +102,14 @@ def load_library(path: str = LIB_PATH) -> ctypes.CDLL:
     lib.p2s_backward.argtypes = [v, _Image, v, v, v, v, v, v, v]
     lib.p2s_render_color.argtypes = [v, _Image, v, v, v, v]
     lib.p2s_mlp_backward.argtypes = [v, v, v, i, i, i, v, v]
+    lib.p2s_interp_anchors.argtypes = [v, i, i, i, i, i, v, v]
+    lib.p2s_anchors_backward.argtypes = [v, i, i, i, i, i, v, v]
     lib.p2s_sampler_destroy.restype = None
     for name in ("p2s_init", "p2s_render", "p2s_render_host", "p2s_reserve", "p2s_set_profile_events",
                  "p2s_get_info", "p2s_debug_beta", "p2s_debug_blur", "p2s_debug_profile_buffer",
                  "p2s_render_anchors", "p2s_render_anchors_host", "p2s_debug_blur_anchors",
                  "p2s_render_sequence", "p2s_sampler_init", "p2s_sample_anchors", "p2s_backward",
-                 "p2s_render_color", "p2s_mlp_backward"):
+                 "p2s_render_color", "p2s_mlp_backward", "p2s_interp_anchors", "p2s_anchors_backward"):
         getattr(lib, name).restype = st
     _lib = lib
     return lib
@@ -134,6 +137,34 @@ def _stream_handle(stream):
     import torch
     s = stream if stream is not None else torch.cuda.current_stream()
     return ctypes.c_void_p(s.cuda_stream)
+
+
+def interp_anchors(anchors, H: int, W: int, out=None, stream=None):
+    """p2s_interp_anchors: anchor grid [B,n_in,G,G] -> dense Zernike field [B,n_in,H,W] (CUDA)."""
+    import torch
+    lib = load_library()
+    B, n_in, G, G2 = anchors.shape
+    if G != G2:
+        raise ValueError("anchors must be [B, n_in, G, G]")
+    ap = _dev_ptr(anchors, "anchors")
+    if out is None:
+        out = torch.empty((B, n_in, H, W), device=anchors.device, dtype=torch.float32)
+    _check(lib.p2s_interp_anchors(ap, B, n_in, G, H, W, _dev_ptr(out, "zernike_field", (B, n_in, H, W)),
+                                  _stream_handle(stream)), "p2s_interp_anchors")
+    return out
+
+
+def anchors_backward(grad_zernike, G: int, out=None, stream=None):
+    """p2s_anchors_backward: dL/dz [B,n_in,H,W] -> dL/dA [B,n_in,G,G] (CUDA)."""
+    import torch
+    lib = load_library()
+    B, n_in, H, W = grad_zernike.shape
+    gp = _dev_ptr(grad_zernike, "grad_zernike")
+    if out is None:
+        out = torch.empty((B, n_in, G, G), device=grad_zernike.device, dtype=torch.float32)
+    _check(lib.p2s_anchors_backward(gp, B, n_in, G, H, W, _dev_ptr(out, "grad_anchors", (B, n_in, G, G)),
+                                    _stream_handle(stream)), "p2s_anchors_backward")
+    return out
 
 
 class Renderer:
@@ -196,6 +227,17 @@ class Renderer:
             gz = self.mlp_backward(zernike, gb, stream=stream)
             return (gb if want_beta else None), gt, gi, gz
         return (gb, gt, gi) if want_image else (gb, gt)
+
+    def backward_anchors(self, image, anchors, tilt, grad_out, want_tilt=True, want_image=False, stream=None):
+        """The adjoint of render_anchors: (dL/dA [B,n_in,G,G], dL/dt | None, dL/dI | None) for upstream
+        grad_out [B,C,H,W] — interp_anchors -> p2s_backward (dL/dbeta) -> p2s_mlp_backward ->
+        p2s_anchors_backward, all on the device."""
+        B, C, H, W = image.shape
+        G = anchors.shape[-1]
+        z = interp_anchors(anchors, H, W, stream=stream)
+        gb, gt, gi, gz = self.backward(image, z, tilt, grad_out, want_beta=False, want_tilt=want_tilt,
+                                       want_image=want_image, want_zernike=True, stream=stream)
+        return anchors_backward(gz, G, stream=stream), gt, gi
 
     def mlp_backward(self, zernike, grad_beta, out=None, stream=None):
         """p2s_mlp_backward: dL/dz [B,n_in,H,W] through the P2S MLP for dL/dbeta [B,K,H,W]."""

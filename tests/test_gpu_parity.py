@@ -959,3 +959,91 @@ def test_cfg3_linearity_in_the_image(p2s):
     om = r.render(_dev(mix), z, t).cpu().numpy().astype(np.float64)
     _cmp(om, a * o1 + b * o2, "render linearity[cfg3 full frame]")
     r.close()
+
+
+# ---- the anchor interpolation as a standalone op and its adjoint (p2s_interp_anchors /
+#      p2s_anchors_backward), and the whole anchor-mode chain dL/dout -> dL/dA
+
+ANCHOR_ADJ_CASES = [("ragged_rgb_S7", 5), ("ragged_rgb_S7", 1), ("S33_K100_C2", 16), ("narrow_S15_K16", 2),
+                    ("many_tiles_C1_S9", 64), ("W1_H1", 3)]
+
+
+@pytest.mark.parametrize("name,G", ANCHOR_ADJ_CASES)
+def test_interp_anchors_and_adjoint(p2s, name, G):
+    from oracle import adjoint
+    spec = SMALL[name]
+    A = _anchors(spec, G, 41)
+    B, n_in = A.shape[:2]
+    H, W = spec.H, spec.W
+    # both kernels form the weights in fp32 as the fused kernel's staging: u = (t + 0.5)(G - 1)/n
+    # carries ~u 2^-24 <= G 2^-24 of absolute error into each weight
+    tol = 1e-6 + 2 * G * 2.0 ** -24
+    z = p2s.interp_anchors(_dev(A), H, W).cpu().numpy()
+    zref = oracle.interp_anchors(A, H, W)
+    assert np.abs(z - zref).max() <= tol * max(1.0, np.abs(A).max())
+    g = np.random.default_rng([G, 42]).standard_normal((B, n_in, H, W)).astype(np.float32)
+    gA = p2s.anchors_backward(_dev(g), G).cpu().numpy()
+    ref = adjoint.anchors_backward(g, G)
+    env = adjoint.anchors_backward(np.abs(g.astype(np.float64)), G)  # the terms' absolute sum
+    err = np.abs(gA - ref)
+    print(f"dL/dA[{name}, G={G}]: max err / envelope = {np.max(err / np.maximum(env, 1e-30)):.2e}")
+    assert np.all(err <= tol * env + 1e-30)
+    # deterministic (fixed reduction order)
+    np.testing.assert_array_equal(p2s.anchors_backward(_dev(g), G).cpu().numpy(), gA)
+
+
+@pytest.mark.parametrize("G", [16, 64])
+def test_render_on_interpolated_field_is_render_anchors(p2s, G):
+    """p2s_render on p2s_interp_anchors' field == p2s_render_anchors, bit for bit (the same fp32
+    interpolation feeds the same fp16 staging), at the bench size."""
+    spec = synth.CONFIGS[3]
+    inp = synth.make_inputs(spec)
+    A = synth.make_anchors(spec, G)
+    r = p2s.Renderer(inp.basis, inp.mlp)
+    img, t = _dev(inp.image), _dev(inp.tilt)
+    z = p2s.interp_anchors(_dev(A), 512, 512)
+    o1 = r.render(img, z, t).cpu().numpy()
+    o2 = r.render_anchors(img, _dev(A), t).cpu().numpy()
+    np.testing.assert_array_equal(o1, o2)
+    r.close()
+
+
+@pytest.mark.parametrize("name,G", [("ragged_rgb_S7", 5), ("S33_K100_C2", 16)])
+def test_backward_anchors_chain(p2s, name, G):
+    """dL/dA of render_anchors for an upstream gradient, against the oracle chain (interpolation,
+    beta, dL/dbeta, dL/dz with fp16-decided masks, dL/dA). Where a ReLU unit is ambiguous (reading
+    N5) the bar widens by that pixel's largest alternative change of dL/dz carried through the
+    interpolation's adjoint."""
+    from oracle import adjoint
+    spec = SMALL[name]
+    inp = synth.make_inputs(spec)
+    A = _anchors(spec, G, 43)
+    B, C, H, W = inp.image.shape
+    g = synth.make_upstream_grad(spec)
+    r = p2s.Renderer(inp.basis, inp.mlp)
+    gA, gt, gi = r.backward_anchors(_dev(inp.image), _dev(A), _dev(inp.tilt), _dev(g), want_tilt=True)
+    gA = gA.cpu().numpy()
+    # oracle chain
+    z32 = oracle.interp_anchors(A, H, W).astype(np.float32)
+    beta = oracle.beta(inp.image, z32, inp.basis, inp.mlp)
+    gb = np.stack([adjoint.backward(inp.image[b], beta[b], inp.tilt[b], inp.basis, g[b], coord_dtype=np.float32)[1]
+                   for b in range(B)])
+
+    class _In:
+        zernike, mlp = z32, inp.mlp
+    dz, alts = _dz_ref(_In, gb)
+    dev = np.zeros_like(dz)
+    for b, alt in enumerate(alts):
+        for q, outs in alt.items():
+            y, x = divmod(int(q), W)
+            dev[b, :, y, x] = np.max([np.abs(o - dz[b, :, y, x]) for o in outs], axis=0) if outs else np.inf
+    ref = adjoint.anchors_backward(dz, G)
+    amb = adjoint.anchors_backward(dev, G)
+    # dL/dz's own bar (2e-3 of its max) carried through the adjoint, plus the ambiguity envelope
+    bar = 2e-3 * np.abs(dz).max() * adjoint.anchors_backward(np.ones_like(dz), G) + amb
+    err = np.abs(gA - ref)
+    print(f"dL/dA chain[{name}, G={G}]: max err {err.max():.3e}, ref max {np.abs(ref).max():.3e}, "
+          f"max err / bar {np.max(err / np.maximum(bar, 1e-30)):.2e}")
+    assert np.all(err <= bar)
+    assert np.linalg.norm(gA - ref) <= 2e-3 * np.linalg.norm(ref) + np.linalg.norm(amb)
+    r.close()
