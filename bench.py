@@ -378,16 +378,38 @@ def main():
             torch.cuda.synchronize()
             a_ms = pdist.max_over_ranks(float(sum(a0[i].elapsed_time(a1[i]) for i in range(n_a))), dist, dev)
             res[key] = pdist.throughput(1, world, n_a, a_ms)
+        # the anchor-mode chain (NEXT-1 + NEXT-4): dL/dA (G = 16) + dL/dt through interp ->
+        # p2s_backward -> p2s_mlp_backward -> p2s_anchors_backward
+        res["anchor_chain"] = None
+        if r.info()["mlp_backward"]:
+            aanc = torch.from_numpy(synth.make_anchors(spec, 16, frames=pdist.rank_frames(rank, 1))).to(dev)
+            for _ in range(3):
+                r.backward_anchors(aimg, aanc, at, ag)
+            n_a = max(5, min(args.steps // 4, 50))
+            a0 = [torch.cuda.Event(enable_timing=True) for _ in range(n_a)]
+            a1 = [torch.cuda.Event(enable_timing=True) for _ in range(n_a)]
+            torch.cuda.synchronize()
+            for i in range(n_a):
+                flush.fill_(float(i))
+                a0[i].record(stream)
+                r.backward_anchors(aimg, aanc, at, ag)
+                a1[i].record(stream)
+            torch.cuda.synchronize()
+            a_ms = pdist.max_over_ranks(float(sum(a0[i].elapsed_time(a1[i]) for i in range(n_a))), dist, dev)
+            res["anchor_chain"] = pdist.throughput(1, world, n_a, a_ms)
+            del aanc
         adjoint_mode = {"value": res["value"], "unit": "frames/s", "beta_only": res["beta_only"],
                         "image_only": res["image_only"], "all": res["all"],
                         "zernike_only": res["zernike_only"], "all_with_zernike": res["all_with_zernike"],
+                        "anchor_chain": res["anchor_chain"],
                         "api": "p2s_backward + p2s_mlp_backward",
                         "note": "value: dL/dbeta [K,H,W] + dL/dt [2,H,W] of one cfg3 frame (L2 flushed per "
                                 "call): dL/dJ scatter, one fused pass (MLP + convolutions -> J, dL/dbeta), "
                                 "dL/dt; beta_only: scatter + conv-only pass; image_only: dL/dI [C,H,W] "
                                 "(scatter, fused pass -> U = beta dL/dJ, k_adjoint_image); all: the three; zernike_only: "
                                 "dL/dz [n_in,H,W] (beta_only's pass, then k_mlp_backward through the MLP); "
-                                "all_with_zernike: the four"}
+                                "all_with_zernike: the four; anchor_chain: dL/dA (G = 16) + dL/dt of render_anchors "
+                                "(interp -> p2s_backward -> p2s_mlp_backward -> p2s_anchors_backward)"}
         del aimg, az, at, ag
 
     # ---- colour mode: per-channel Zernike fields (the
