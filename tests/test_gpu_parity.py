@@ -1047,3 +1047,41 @@ def test_backward_anchors_chain(p2s, name, G):
     assert np.all(err <= bar)
     assert np.linalg.norm(gA - ref) <= 2e-3 * np.linalg.norm(ref) + np.linalg.norm(amb)
     r.close()
+
+
+def test_two_handles_on_two_streams_concurrently(p2s):
+    """One handle per stream (include/p2s.h): two handles with different assets render and
+    back-propagate concurrently on two streams; every output equals the same call made alone."""
+    import torch
+    specs = [SMALL["ragged_rgb_S7"], SMALL["S33_K100_C2"]]
+    inps = [synth.make_inputs(s) for s in specs]
+    rs = [p2s.Renderer(i.basis, i.mlp) for i in inps]
+    dev = [(_dev(i.image), _dev(i.zernike), _dev(i.tilt), _dev(synth.make_upstream_grad(s)))
+           for i, s in zip(inps, specs)]
+    alone = []
+    for r, (img, z, t, g) in zip(rs, dev):
+        out = r.render(img, z, t)
+        gb, _ = r.backward(img, z, t, g, want_tilt=False)
+        gz = r.mlp_backward(z, gb)
+        torch.cuda.synchronize()
+        alone.append((out.cpu().numpy(), gb.cpu().numpy(), gz.cpu().numpy()))
+    streams = [torch.cuda.Stream(), torch.cuda.Stream()]
+    res = [None, None]
+    for _ in range(3):
+        for k in range(2):
+            r, (img, z, t, g), s = rs[k], dev[k], streams[k]
+            with torch.cuda.stream(s):
+                out = r.render(img, z, t, stream=s)
+                gb, _ = r.backward(img, z, t, g, want_tilt=False, stream=s)
+                gz = r.mlp_backward(z, gb, stream=s)
+                res[k] = (out, gb, gz)
+        torch.cuda.synchronize()
+        for k in range(2):
+            np.testing.assert_array_equal(res[k][0].cpu().numpy(), alone[k][0])
+            # dL/dbeta reduces dL/dJ, whose scatter uses float atomics (order-dependent last bits)
+            np.testing.assert_allclose(res[k][1].cpu().numpy(), alone[k][1], rtol=1e-5,
+                                       atol=1e-5 * np.abs(alone[k][1]).max())
+            np.testing.assert_allclose(res[k][2].cpu().numpy(), alone[k][2], rtol=1e-3,
+                                       atol=1e-3 * np.abs(alone[k][2]).max())
+    for r in rs:
+        r.close()
