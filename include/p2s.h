@@ -172,7 +172,8 @@ P2S_API p2s_status p2s_backward(p2s_handle* h, p2s_image image, const float* zer
  * grad_zernike overlapping an input -> P2S_ERR_INVALID_ARG; frames whose channel planes exceed
  * 2^31 elements -> P2S_ERR_UNSUPPORTED; launch failure -> P2S_ERR_CUDA. MLPs whose weights do not
  * all fit one SM next to the activation tile (e.g. 33-256-256-100) run a variant that streams
- * W1 / W3 from L2; every MLP p2s_init accepts is supported (p2s_info.mlp_backward = 1). */
+ * the weights from L2, two CTAs per SM; every MLP p2s_init accepts is supported
+ * (p2s_info.mlp_backward = 1). */
 P2S_API p2s_status p2s_mlp_backward(p2s_handle* h, const float* zernike_field, const float* grad_beta, int B,
                                     int H, int W, float* grad_zernike, p2s_stream_t stream);
 

@@ -128,8 +128,8 @@ struct p2s_handle {
   PFN_cuTensorMapEncodeTiled encode = nullptr;
   // dL/dz (k_mlp_backward): resident weight pack and its shared-memory plan (mb_ok = it fits)
   uint8_t* d_mlpb = nullptr;
-  int mb_ok = 0, mb_fold = 0, mb_ring = 0, mb_g3 = 1, mb_nring = 0, mb_slab = 0, mb_off_ring = 0, mb_ring_src_off = 0, mb_smem = 0, mb_off_w2 = 0, mb_off_w3 = 0, mb_off_bias = 0, mb_wbytes = 0, mb_off_act = 0,
-      mb_off_bar = 0;
+  int mb_ok = 0, mb_fold = 0, mb_stream = 0, mb_g3 = 1, mb_nring = 0, mb_slot = 0, mb_off_ring = 0, mb_ring_src_off = 0,
+      mb_smem = 0, mb_off_w2 = 0, mb_off_w3 = 0, mb_off_bias = 0, mb_wbytes = 0, mb_off_act = 0, mb_off_bar = 0;
   MlpOp ops[kMaxOps];  // [0, n_ops) per-tile ops, then n_fops first-tile whole-layer ops
   int n_ops = 0, n_fops = 0;
   bool bias_folded = false;
@@ -748,25 +748,20 @@ p2s_status p2s_init(const p2s_basis* basis, const p2s_mlp* mlp, p2s_handle** out
     (void)wpad;
   }
   {
-    // ---- dL/dz plan (p2s_mlp_backward.cuh): W1 [N1][K1], W2 [N2][N1], W3^T [N2][Nk] as K-major
-    // fp16 tiles + fp32 biases, resident in shared memory with one [128][max K] activation buffer.
-    // When all three do not fit (e.g. 33-256-256-100), the ring variant keeps W2 resident and
-    // streams W1 / W3^T / W1^T slabs through a 3-slot ring; if even that does not fit, mb_ok = 0
-    // and p2s_mlp_backward returns P2S_ERR_UNSUPPORTED.
+    // ---- dL/dz plan (p2s_mlp_backward.cuh). W1 [N1][K1], W2 [N2][N1], W3^T [N2][Nk] as K-major
+    // fp16 tiles (+ fp32 biases, or biases folded as hi/lo pairs). Resident variant when the three
+    // and one [128][max K] activation tile fit one SM; otherwise (e.g. 33-256-256-100) the
+    // streamed variant: two CTAs per SM, every GEMM's weight slabs through a ring from an
+    // L2-resident table (P2S_MB_MODE=stream forces it; tests cover both).
     const int K1 = h->K1, N1 = h->N1, N2 = h->N2, Nk = h->Nk;
     const int w1 = N1 * K1 * 2, w2 = N2 * N1 * 2, w3 = N2 * Nk * 2, bb = (N1 + N2) * 4;
     const int kact = std::max(std::max(K1, N1), std::max(N2, Nk));
-    const int act_bytes = 128 * kact * 2, bar_bytes = 32 + 4 * 128 * 4 + 16 * 8;
+    const int act_bytes = 128 * kact * 2;
     auto al128 = [](int v) { return (v + 127) / 128 * 128; };
-    const int smem_res = al128(w1 + w2 + w3 + bb) + act_bytes + bar_bytes;
-    const int slab = std::max(std::max(N1, N2), K1) * 32, nring_mb = 3;
-    const int smem_ring = al128(w2 + bb) + al128(nring_mb * slab) + act_bytes + bar_bytes;
-    // (P2S_MB_RING=1 forces the ring variant: tests cover it on MLPs that would fit resident)
-    const bool ring = smem_res > kSmemLimit || (std::getenv("P2S_MB_RING") && std::atoi(std::getenv("P2S_MB_RING")) != 0);
-    const int smem = ring ? smem_ring : smem_res;
+    const int smem_res = al128(w1 + w2 + w3 + bb) + act_bytes + 32 + 4 * 128 * 4;
     // biases as fp16 hi/lo pairs on constant-1 inputs when each layer input has 2 spare columns
     const bool fold = h->n_in + 2 <= K1 && h->h1 + 2 <= N1;
-    if (smem <= kSmemLimit && K1 <= 64) {
+    if (K1 <= 64) {
       // standard K-major tiles: element (n, k) of [rows][kd] at (n%8)*16 + (n/8)*kd*16 + (k%8)*2 + (k/8)*128
       auto at = [](int n, int k, int kd) { return ((n % 8) * 16 + (n / 8) * kd * 16 + (k % 8) * 2 + (k / 8) * 128) / 2; };
       std::vector<__half> W1h((size_t)N1 * K1, __float2half(0.f)), W2h((size_t)N2 * N1, __float2half(0.f)),
@@ -796,71 +791,80 @@ p2s_status p2s_init(const p2s_basis* basis, const p2s_mlp* mlp, p2s_handle** out
       std::vector<float> bias((size_t)N1 + N2, 0.f);
       for (int j = 0; j < h->h1; ++j) bias[j] = mlp->b1[j];
       for (int j = 0; j < h->h2; ++j) bias[N1 + j] = mlp->b2[j];
-      // resident pack [W1 | W2 | W3^T | b1 | b2], or (ring) [W2 | b1 | b2] + the slab table
-      std::vector<uint8_t> pk;
-      auto append = [&](const void* src, size_t n) {
-        const size_t o = pk.size();
-        pk.resize(o + n);
-        std::memcpy(pk.data() + o, src, n);
-      };
-      if (!ring) {
-        append(W1h.data(), w1);
-        append(W2h.data(), w2);
-        append(W3h.data(), w3);
+      const char* mode = std::getenv("P2S_MB_MODE");
+      const bool stream = smem_res > kSmemLimit || (mode && std::strcmp(mode, "stream") == 0);
+      if (!stream) {
+        // resident pack [W1 | W2 | W3^T | b1 | b2], copied to shared memory offset 0
+        std::vector<uint8_t> pk((size_t)w1 + w2 + w3 + bb);
+        std::memcpy(pk.data(), W1h.data(), w1);
+        std::memcpy(pk.data() + w1, W2h.data(), w2);
+        std::memcpy(pk.data() + w1 + w2, W3h.data(), w3);
+        std::memcpy(pk.data() + w1 + w2 + w3, bias.data(), bb);
+        if ((e = cudaMalloc(&h->d_mlpb, pk.size())) != cudaSuccess ||
+            (e = cudaMemcpy(h->d_mlpb, pk.data(), pk.size(), cudaMemcpyHostToDevice)) != cudaSuccess)
+          return fail(cuda_fail(e, "dz weight pack"));
+        if ((e = cudaFuncSetAttribute(k_mlp_backward<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem_res)) !=
+                cudaSuccess ||
+            (e = cudaFuncSetAttribute(k_mlp_backward<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem_res)) !=
+                cudaSuccess)
+          return fail(cuda_fail(e, "cudaFuncSetAttribute(k_mlp_backward)"));
+        h->mb_smem = smem_res;
+        h->mb_off_w2 = w1;
+        h->mb_off_w3 = w1 + w2;
+        h->mb_off_bias = w1 + w2 + w3;
+        h->mb_wbytes = (int)pk.size();
+        h->mb_off_act = al128((int)pk.size());
+        h->mb_off_bar = h->mb_off_act + act_bytes;
       } else {
-        append(W2h.data(), w2);
-      }
-      append(bias.data(), bb);
-      std::vector<uint8_t> slabs;
-      if (ring) {
-        // per-tile order [F1: W1 K-slabs | B1: W3^T K-slabs | B3: W1 row pairs (= W1^T K'-slabs)],
-        // K-slabs re-laid [N][16] (lbo 128, sbo 256), W1 row pairs as stored (2 x 8 rows x K1)
-        const int g3 = std::max(1, slab / (K1 * 32)), nb3 = N1 / 16;
-        const int nsl = K1 / 16 + Nk / 16 + (nb3 + g3 - 1) / g3;
-        slabs.assign((size_t)nsl * slab, 0);
+        // slab table, per tile: [F1: W1 K-slabs | F2: W2 K-slabs | B1: W3^T K-slabs | B2: W2 row
+        // pairs (W2^T K'-slabs) | B3: W1 row pairs, g3 per slot]; K-slabs re-laid [N][16]
+        // (lbo 128, sbo 256), row pairs as stored (lbo 16 kd, sbo 128)
+        const int slot = std::max(std::max(N1, N2), K1) * 32, g3 = std::max(1, slot / (K1 * 32)), nring = 4;
+        const int nb3 = N1 / 16;
+        const int nsl = K1 / 16 + N1 / 16 + Nk / 16 + N2 / 16 + (nb3 + g3 - 1) / g3;
+        std::vector<uint8_t> st((size_t)bb + (size_t)nsl * slot, 0);
+        std::memcpy(st.data(), bias.data(), bb);  // [b1 | b2] first
+        uint8_t* tab = st.data() + bb;
         int i = 0;
         auto kslab = [&](const std::vector<__half>& Wt, int N, int kd, int ks) {
-          __half* d = reinterpret_cast<__half*>(slabs.data() + (size_t)i * slab);
+          __half* d = reinterpret_cast<__half*>(tab + (size_t)i * slot);
           for (int n = 0; n < N; ++n)
             for (int kk = 0; kk < 16; ++kk)
               d[((n % 8) * 16 + (n / 8) * 256 + (kk % 8) * 2 + (kk / 8) * 128) / 2] = Wt[at(n, 16 * ks + kk, kd)];
           ++i;
         };
         for (int ks = 0; ks < K1 / 16; ++ks) kslab(W1h, N1, K1, ks);
+        for (int ks = 0; ks < N1 / 16; ++ks) kslab(W2h, N2, N1, ks);
         for (int ks = 0; ks < Nk / 16; ++ks) kslab(W3h, N2, Nk, ks);
-        for (int ks = 0; ks < nb3; ks += g3, ++i)  // g3 W1 row pairs per slot
-          std::memcpy(slabs.data() + (size_t)i * slab, reinterpret_cast<const uint8_t*>(W1h.data()) + (size_t)ks * K1 * 32,
+        for (int ks = 0; ks < N2 / 16; ++ks, ++i)
+          std::memcpy(tab + (size_t)i * slot, reinterpret_cast<const uint8_t*>(W2h.data()) + (size_t)ks * N1 * 32,
+                      (size_t)N1 * 32);
+        for (int ks = 0; ks < nb3; ks += g3, ++i)
+          std::memcpy(tab + (size_t)i * slot, reinterpret_cast<const uint8_t*>(W1h.data()) + (size_t)ks * K1 * 32,
                       (size_t)std::min(g3, nb3 - ks) * K1 * 32);
+        const int off_ring = al128(bb), off_act = off_ring + al128(nring * slot), off_bar = off_act + act_bytes;
+        const int smem = off_bar + 160 + 2 * 128 * 4;
+        if ((e = cudaMalloc(&h->d_mlpb, st.size())) != cudaSuccess ||
+            (e = cudaMemcpy(h->d_mlpb, st.data(), st.size(), cudaMemcpyHostToDevice)) != cudaSuccess)
+          return fail(cuda_fail(e, "dz slab table"));
+        if ((e = cudaFuncSetAttribute(k_mlp_backward_s<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem)) !=
+                cudaSuccess ||
+            (e = cudaFuncSetAttribute(k_mlp_backward_s<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem)) !=
+                cudaSuccess)
+          return fail(cuda_fail(e, "cudaFuncSetAttribute(k_mlp_backward_s)"));
+        h->mb_stream = 1;
+        h->mb_smem = smem;
+        h->mb_off_bias = 0;
+        h->mb_off_ring = off_ring;
+        h->mb_off_act = off_act;
+        h->mb_off_bar = off_bar;
+        h->mb_slot = slot;
         h->mb_g3 = g3;
+        h->mb_nring = nring;
+        h->mb_ring_src_off = bb;
       }
-      if ((e = cudaMalloc(&h->d_mlpb, pk.size() + slabs.size())) != cudaSuccess ||
-          (e = cudaMemcpy(h->d_mlpb, pk.data(), pk.size(), cudaMemcpyHostToDevice)) != cudaSuccess ||
-          (ring && (e = cudaMemcpy(h->d_mlpb + pk.size(), slabs.data(), slabs.size(), cudaMemcpyHostToDevice)) !=
-                       cudaSuccess))
-        return fail(cuda_fail(e, "dz weight pack"));
-      if ((e = cudaFuncSetAttribute(k_mlp_backward<true, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem)) !=
-              cudaSuccess ||
-          (e = cudaFuncSetAttribute(k_mlp_backward<false, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem)) !=
-              cudaSuccess ||
-          (e = cudaFuncSetAttribute(k_mlp_backward<true, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem)) !=
-              cudaSuccess ||
-          (e = cudaFuncSetAttribute(k_mlp_backward<false, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem)) !=
-              cudaSuccess)
-        return fail(cuda_fail(e, "cudaFuncSetAttribute(k_mlp_backward)"));
       h->mb_ok = 1;
       h->mb_fold = fold ? 1 : 0;
-      h->mb_ring = ring ? 1 : 0;
-      h->mb_smem = smem;
-      h->mb_off_w2 = ring ? 0 : w1;
-      h->mb_off_w3 = ring ? 0 : w1 + w2;
-      h->mb_off_bias = ring ? w2 : w1 + w2 + w3;
-      h->mb_wbytes = (int)pk.size();
-      h->mb_off_ring = al128((int)pk.size());
-      h->mb_off_act = ring ? h->mb_off_ring + al128(nring_mb * slab) : al128((int)pk.size());
-      h->mb_off_bar = h->mb_off_act + act_bytes;
-      h->mb_nring = nring_mb;
-      h->mb_slab = slab;
-      h->mb_ring_src_off = (int)pk.size();
     }
   }
   *out_handle = h;
@@ -1092,16 +1096,17 @@ p2s_status p2s_mlp_backward(p2s_handle* h, const float* zernike_field, const flo
   p.ntiles = (int)(tpf * B);
   p.off_w2 = h->mb_off_w2; p.off_w3 = h->mb_off_w3; p.off_bias = h->mb_off_bias; p.wbytes = h->mb_wbytes;
   p.off_act = h->mb_off_act; p.off_bar = h->mb_off_bar;
-  p.ring_src = h->d_mlpb + h->mb_ring_src_off;
-  p.off_ring = h->mb_off_ring; p.nring = h->mb_nring; p.slab_stride = h->mb_slab; p.g3 = h->mb_g3;
-  const int grid = std::min(p.ntiles, h->sm_count);
   cudaStream_t st = (cudaStream_t)stream;
-  if (h->mb_ring) {
-    if (h->mb_fold) k_mlp_backward<true, true><<<grid, kMbThreadsRing, h->mb_smem, st>>>(p);
-    else k_mlp_backward<false, true><<<grid, kMbThreadsRing, h->mb_smem, st>>>(p);
+  if (h->mb_stream) {
+    p.ring_src = h->d_mlpb + h->mb_ring_src_off;
+    p.off_ring = h->mb_off_ring; p.nring = h->mb_nring; p.slab_stride = h->mb_slot; p.g3 = h->mb_g3;
+    const int grid = std::min(p.ntiles, 2 * h->sm_count);  // two CTAs per SM
+    if (h->mb_fold) k_mlp_backward_s<true><<<grid, kMbsThreads, h->mb_smem, st>>>(p);
+    else k_mlp_backward_s<false><<<grid, kMbsThreads, h->mb_smem, st>>>(p);
   } else {
-    if (h->mb_fold) k_mlp_backward<true, false><<<grid, kMbThreads, h->mb_smem, st>>>(p);
-    else k_mlp_backward<false, false><<<grid, kMbThreads, h->mb_smem, st>>>(p);
+    const int grid = std::min(p.ntiles, h->sm_count);
+    if (h->mb_fold) k_mlp_backward<true><<<grid, kMbThreads, h->mb_smem, st>>>(p);
+    else k_mlp_backward<false><<<grid, kMbThreads, h->mb_smem, st>>>(p);
   }
   P2S_CUDA(cudaPeekAtLastError());
   return P2S_OK;

@@ -12,12 +12,14 @@
 //     B1: D3 = G3 W3       (K = Nk, N = N2)     drain: g2 = (D2 + b2 > 0) ? D3 : 0 -> ACT
 //     B2: D4 = G2 W2       (K = N2, N = N1)     drain: g1 = mask1 ? D4 : 0 -> ACT
 //     B3: D5 = G1 W1       (K = N1, N = K1)     drain: dL/dz -> global
-// The weights are resident in shared memory for the whole persistent launch, each stored ONCE as
+// Two variants. k_mlp_backward (resident, one CTA per SM, used when everything fits):
+// the weights are resident in shared memory for the whole persistent launch, each stored ONCE as
 // a K-major fp16 tile; B2 and B3 read W2 and W1 transposed through the descriptor's B-major bit
 // (an 8x8 core matrix that is K-major for W is MN-major for W^T: LBO and SBO swap roles). One
 // activation buffer (ACT, [128][max K] fp16) carries z, a1, g3, g2 and g1 in turn (each GEMM
 // completes before its A operand is overwritten). The forward masks are recomputed (two of the
-// five GEMMs) rather than stored by the forward pass.
+// five GEMMs) rather than stored by the forward pass. k_mlp_backward_s (streamed, two CTAs per
+// SM, any MLP the render accepts — e.g. 33-256-256-100): see its comment below.
 //
 // Biases: when every layer input has two spare padding columns (n_in + 2 <= K1, h1 + 2 <= N1),
 // they ride in the GEMMs as fp16 hi/lo pairs on constant-1 inputs, as in the render kernel
@@ -52,17 +54,13 @@ struct MlpbParams {
   int tiles_per_frame, ntiles;
   int off_w2, off_w3, off_bias, wbytes;  // byte offsets in wpack (= in shared memory)
   int off_act, off_bar;
-  // kRing (MLPs whose three weight matrices do not all fit, e.g. 33-256-256-100): only W2 (used
-  // twice per tile) is resident; the F1 / B1 / B3 operands (W1 slabs, W3^T slabs, W1^T slabs)
-  // stream from an L2-resident table through a ring of nring slots of slab_stride bytes, fed by
-  // a producer warp, in the fixed per-tile order [F1: K1/16 | B1: Nk/16 | B3: N1/16 slabs]
-  // (B3's W1^T K'-steps are small, K1 x 32 B: g3 of them share one slot, contiguous in W1's layout)
+  // streamed variant (k_mlp_backward_s): the slab table and the ring (B3's W1^T K'-steps are
+  // small, K1 x 32 B: g3 of them share one slot, contiguous in W1's layout)
   const uint8_t* ring_src;
   int off_ring, nring, slab_stride, g3;
 };
 
-constexpr int kMbThreads = 512;      // drain/staging threads (16 warps)
-constexpr int kMbThreadsRing = 544;  // + one producer warp in the ring variant
+constexpr int kMbThreads = 512;
 
 namespace mlpb {
 
@@ -76,6 +74,23 @@ P2S_DEV void gemm(uint32_t d, uint32_t a_s, int nks, uint32_t b_s, uint32_t b_lb
     umma_f16_elect(d, sdesc(a_s + (uint32_t)ks * 256u, 128u, a_sbo),
                    sdesc(b_s + (uint32_t)ks * b_kstep, b_lbo, b_sbo), idesc, ks > 0 ? 1u : 0u);
 }
+
+// this thread's row of a K-major [128][kd] fp16 tile: element (m, k) at
+// (m%8)*16 + (m/8)*kd*16 + (k%8)*2 + (k/8)*128
+P2S_DEV uint8_t* row_of(uint8_t* act, int m, int kd) { return act + (m & 7) * 16 + (m >> 3) * kd * 16; }
+
+P2S_DEV void st8(uint8_t* row, int kchunk, uint32_t a, uint32_t b, uint32_t c, uint32_t d) {
+  *reinterpret_cast<uint4*>(row + kchunk * 128) = make_uint4(a, b, c, d);
+}
+P2S_DEV void st8f(uint8_t* row, int kchunk, const float* v) {
+  st8(row, kchunk, pack_half2(v[0], v[1]), pack_half2(v[2], v[3]), pack_half2(v[4], v[5]), pack_half2(v[6], v[7]));
+}
+P2S_DEV uint32_t relu2(float a, float b) {  // fp16x2 {lo = relu(a), hi = relu(b)}, RN
+  uint32_t r;
+  asm("cvt.rn.relu.f16x2.f32 %0, %1, %2;" : "=r"(r) : "f"(b), "f"(a));
+  return r;
+}
+P2S_DEV float exp2i(int e) { return __int_as_float((e + 127) << 23); }  // 2^e, e in [-126, 127]
 
 // D[128 x N] = ACT * B^T with each 16-wide K-step of B taken from the next ring slot
 // (K-major slabs: lbo 128, sbo 256; W1^T slabs: lbo 16 K1, sbo 128); each slot is released to the
@@ -98,31 +113,11 @@ P2S_DEV void gemm_ring(uint32_t d, uint32_t a_s, int nks, uint32_t ring_s, uint3
   }
 }
 
-// the 512 drain threads' barrier (the ring variant's producer warp does not take part)
-P2S_DEV void drain_sync() { asm volatile("bar.sync 1, 512;" ::: "memory"); }
-
-// this thread's row of a K-major [128][kd] fp16 tile: element (m, k) at
-// (m%8)*16 + (m/8)*kd*16 + (k%8)*2 + (k/8)*128
-P2S_DEV uint8_t* row_of(uint8_t* act, int m, int kd) { return act + (m & 7) * 16 + (m >> 3) * kd * 16; }
-
-P2S_DEV void st8(uint8_t* row, int kchunk, uint32_t a, uint32_t b, uint32_t c, uint32_t d) {
-  *reinterpret_cast<uint4*>(row + kchunk * 128) = make_uint4(a, b, c, d);
-}
-P2S_DEV void st8f(uint8_t* row, int kchunk, const float* v) {
-  st8(row, kchunk, pack_half2(v[0], v[1]), pack_half2(v[2], v[3]), pack_half2(v[4], v[5]), pack_half2(v[6], v[7]));
-}
-P2S_DEV uint32_t relu2(float a, float b) {  // fp16x2 {lo = relu(a), hi = relu(b)}, RN
-  uint32_t r;
-  asm("cvt.rn.relu.f16x2.f32 %0, %1, %2;" : "=r"(r) : "f"(b), "f"(a));
-  return r;
-}
-P2S_DEV float exp2i(int e) { return __int_as_float((e + 127) << 23); }  // 2^e, e in [-126, 127]
-
 // the CTA's generic-proxy writes to ACT / its TMEM reads are ordered before the next UMMA
 P2S_DEV void publish() {
   fence_proxy_async_smem();
   tc_fence_before();
-  drain_sync();
+  __syncthreads();
 }
 
 }  // namespace mlpb
@@ -143,9 +138,8 @@ P2S_DEV void load_z(const MlpbParams& p, int t, int m, int q, float (&zv)[2][8])
   }
 }
 
-template <bool kFold, bool kRing>
-__global__ void __launch_bounds__(kRing ? kMbThreadsRing : kMbThreads, 1)
-    k_mlp_backward(const __grid_constant__ MlpbParams p) {
+template <bool kFold>
+__global__ void __launch_bounds__(kMbThreads, 1) k_mlp_backward(const __grid_constant__ MlpbParams p) {
   using namespace mlpb;
   extern __shared__ __align__(1024) uint8_t smem[];
   const uint32_t sbase = smem_u32(smem);
@@ -160,16 +154,9 @@ __global__ void __launch_bounds__(kRing ? kMbThreadsRing : kMbThreads, 1)
   const int tid = (int)threadIdx.x, warp = (int)warp_id();
   const int m = tid & 127, q = tid >> 7;  // pixel row (TMEM lane) and column quarter
 
-  uint64_t* ring_full = reinterpret_cast<uint64_t*>(smem + p.off_bar + 32 + 2048);
-  uint64_t* ring_empty = ring_full + 8;
   if (tid == 0) {
     mbar_init(bar_w, 1);
     mbar_init(bar_mma, 1);
-    if (kRing)
-      for (int i = 0; i < p.nring; ++i) {
-        mbar_init(&ring_full[i], 1);
-        mbar_init(&ring_empty[i], 1);
-      }
     fence_mbar_init();
   }
   if (warp == 0) tmem_alloc<512>(tmem_slot);
@@ -186,28 +173,6 @@ __global__ void __launch_bounds__(kRing ? kMbThreadsRing : kMbThreads, 1)
       bulk_g2s(smem + off, p.wpack + off, (uint32_t)min(32768, p.wbytes - off), bar_w);
   }
 
-  if (kRing && warp == 16) {
-    // ---- producer (ring variant): the per-tile slab sequence, one bulk copy per slab
-    if (lane_id() == 0) {
-      const int n_f1 = p.K1 / 16, n_b1 = p.Nk / 16, nb3 = p.N1 / 16, nsl = n_f1 + n_b1 + (nb3 + p.g3 - 1) / p.g3;
-      int s = 0;
-      uint32_t ph = 0;
-      for (int t = (int)blockIdx.x; t < p.ntiles; t += (int)gridDim.x)
-        for (int i = 0; i < nsl; ++i) {
-          mbar_wait(&ring_empty[s], ph ^ 1);
-          const int i3 = i - n_f1 - n_b1;  // B3 item: K'-steps [g3 i3, min(nb3, g3 (i3 + 1)))
-          const uint32_t bytes = (uint32_t)(i < n_f1 ? p.N1 * 32
-                                                     : (i3 < 0 ? p.N2 * 32 : min(p.g3, nb3 - p.g3 * i3) * p.K1 * 32));
-          mbar_arrive_expect_tx(&ring_full[s], bytes);
-          bulk_g2s(smem + p.off_ring + s * p.slab_stride, p.ring_src + (size_t)i * p.slab_stride, bytes, &ring_full[s]);
-          if (++s == p.nring) { s = 0; ph ^= 1; }
-        }
-    }
-    __syncwarp();
-  } else {
-  const uint32_t ring_s = sbase + (uint32_t)p.off_ring, stride = (uint32_t)p.slab_stride;
-  int rs = 0;
-  uint32_t rph = 0;
   const uint32_t id_f1 = idesc_f16(128, (uint32_t)p.N1), id_f2 = idesc_f16(128, (uint32_t)p.N2);
   const uint32_t id_b2 = idesc_f16(128, (uint32_t)p.N1) | (1u << 16);
   const uint32_t id_b3 = idesc_f16(128, (uint32_t)p.K1) | (1u << 16);
@@ -259,8 +224,7 @@ __global__ void __launch_bounds__(kRing ? kMbThreadsRing : kMbThreads, 1)
     }
     if (warp == 0) {
       tc_fence_after();
-      if (kRing) gemm_ring(tmem, act_s, p.K1 / 16, ring_s, stride, 128u, 256u, id_f1, ring_full, ring_empty, p.nring, rs, rph);
-      else gemm(tmem, act_s, p.K1 / 16, w1_s, 128u, (uint32_t)p.K1 * 16u, 256u, id_f1);
+      gemm(tmem, act_s, p.K1 / 16, w1_s, 128u, (uint32_t)p.K1 * 16u, 256u, id_f1);
       umma_commit_elect(bar_mma);
     }
     // ---- dL/dbeta of this tile into registers (in flight during F1 / F2)
@@ -315,7 +279,7 @@ __global__ void __launch_bounds__(kRing ? kMbThreadsRing : kMbThreads, 1)
     mbar_wait(bar_mma, ph);  // F2 done: ACT is free
     ph ^= 1;
     tc_fence_after();
-    drain_sync();
+    __syncthreads();
     mx = fmaxf(fmaxf(s_max[m], s_max[128 + m]), fmaxf(s_max[256 + m], s_max[384 + m]));
     // mx = f 2^ex with f in [0.5, 1) (normal mx; 0 and subnormals take ex = -126, inf/NaN 129):
     // scale by 2^-ex and back by 2^ex, each as two in-range power-of-two factors (exact)
@@ -336,8 +300,7 @@ __global__ void __launch_bounds__(kRing ? kMbThreadsRing : kMbThreads, 1)
     publish();
     if (warp == 0) {
       tc_fence_after();
-      if (kRing) gemm_ring(tmem, act_s, p.Nk / 16, ring_s, stride, 128u, 256u, id_f2, ring_full, ring_empty, p.nring, rs, rph);
-      else gemm(tmem, act_s, p.Nk / 16, w3_s, 128u, (uint32_t)p.Nk * 16u, 256u, id_f2);
+      gemm(tmem, act_s, p.Nk / 16, w3_s, 128u, (uint32_t)p.Nk * 16u, 256u, id_f2);
       umma_commit_elect(bar_mma);
     }
     mbar_wait(bar_mma, ph);
@@ -385,10 +348,7 @@ __global__ void __launch_bounds__(kRing ? kMbThreadsRing : kMbThreads, 1)
     publish();
     if (warp == 0) {
       tc_fence_after();
-      if (kRing)
-        gemm_ring(tmem, act_s, p.N1 / 16, ring_s, stride, (uint32_t)p.K1 * 16u, 128u, id_b3, ring_full, ring_empty, p.nring,
-                  rs, rph, p.g3, (uint32_t)p.K1 * 32u);
-      else gemm(tmem, act_s, p.N1 / 16, w1_s, (uint32_t)p.K1 * 16u, 128u, (uint32_t)p.K1 * 32u, id_b3);
+      gemm(tmem, act_s, p.N1 / 16, w1_s, (uint32_t)p.K1 * 16u, 128u, (uint32_t)p.K1 * 32u, id_b3);
       umma_commit_elect(bar_mma);
     }
     if (t + (int)gridDim.x < p.ntiles) load_z(p, t + (int)gridDim.x, m, q, zv);  // next tile's z
@@ -411,11 +371,288 @@ __global__ void __launch_bounds__(kRing ? kMbThreadsRing : kMbThreads, 1)
     }
     tc_fence_before();  // TMEM reads before the next tile's F1 (ordered by its publish())
   }
-  }  // drain / issue warps
   tc_fence_before();
   __syncthreads();
   tc_fence_after();
   if (warp == 0) tmem_dealloc<512>(tmem);
+}
+
+// ================================================================================================
+// k_mlp_backward_s: the streamed variant — no resident weights, TWO CTAs per SM. Each CTA keeps one
+// 256-column TMEM region (the layer-2 mask is taken to bits when D2 is drained, so D3 can reuse the
+// region), one activation tile, and a ring fed by a producer warp with every GEMM's weight slabs
+// in the fixed per-tile order
+//     [F1: W1 K-slabs | F2: W2 K-slabs | B1: W3^T K-slabs | B2: W2 row pairs (W2^T K'-slabs) |
+//      B3: W1 row pairs (W1^T K'-slabs), g3 per slot]
+// from an L2-resident table. The serial GEMM -> drain chain of one CTA overlaps the other CTA's.
+// 288 threads: 8 drain warps (2 threads per TMEM lane, each half of the 16-column groups) + the
+// producer (warp 8). Slabs: K-slabs [N][16] (lbo 128, sbo 256); row pairs as stored in the K-major
+// [rows][kd] layout (lbo 16 kd, sbo 128, B-major bit).
+constexpr int kMbsThreads = 288;
+
+template <bool kFold>
+__global__ void __launch_bounds__(kMbsThreads, 2) k_mlp_backward_s(const __grid_constant__ MlpbParams p) {
+  using namespace mlpb;
+  extern __shared__ __align__(1024) uint8_t smem[];
+  const uint32_t sbase = smem_u32(smem);
+  uint64_t* bar_mma = reinterpret_cast<uint64_t*>(smem + p.off_bar);
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bar_mma + 1);
+  uint64_t* ring_full = bar_mma + 2;
+  uint64_t* ring_empty = ring_full + 8;
+  float* s_max = reinterpret_cast<float*>(smem + p.off_bar + 160);  // [2][128]
+  const float* s_b1 = reinterpret_cast<const float*>(smem + p.off_bias);
+  const float* s_b2 = s_b1 + p.N1;
+  uint8_t* act = smem + p.off_act;
+  const uint32_t act_s = sbase + (uint32_t)p.off_act;
+  const int tid = (int)threadIdx.x, warp = (int)warp_id();
+  const int m = tid & 127, hh = (tid >> 7) & 1;  // pixel row (TMEM lane) and column half
+
+  if (tid == 0) {
+    mbar_init(bar_mma, 1);
+    for (int i = 0; i < p.nring; ++i) {
+      mbar_init(&ring_full[i], 1);
+      mbar_init(&ring_empty[i], 1);
+    }
+    fence_mbar_init();
+  }
+  if (!kFold)  // fp32 biases for the drains (folded biases ride in the GEMMs)
+    for (int i = tid; i < p.N1 + p.N2; i += kMbsThreads)
+      const_cast<float*>(s_b1)[i] = reinterpret_cast<const float*>(p.wpack)[i];
+  if (warp == 0) tmem_alloc<256>(tmem_slot);
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
+  const uint32_t tmem = __shfl_sync(0xffffffffu, *tmem_slot, 0);
+
+  if (warp == 8) {
+    // ---- producer: every tile's slab sequence, one bulk copy per slot
+    if (lane_id() == 0) {
+      const int n1 = p.K1 / 16, n2 = n1 + p.N1 / 16, n3 = n2 + p.Nk / 16, n4 = n3 + p.N2 / 16, nb3 = p.N1 / 16;
+      const int nsl = n4 + (nb3 + p.g3 - 1) / p.g3;
+      int s = 0;
+      uint32_t ph = 0;
+      for (int t = (int)blockIdx.x; t < p.ntiles; t += (int)gridDim.x)
+        for (int i = 0; i < nsl; ++i) {
+          mbar_wait(&ring_empty[s], ph ^ 1);
+          const uint32_t bytes =
+              (uint32_t)(i < n1 ? p.N1 * 32
+                                : (i < n3 ? p.N2 * 32 : (i < n4 ? p.N1 * 32 : min(p.g3, nb3 - p.g3 * (i - n4)) * p.K1 * 32)));
+          mbar_arrive_expect_tx(&ring_full[s], bytes);
+          bulk_g2s(smem + p.off_ring + s * p.slab_stride, p.ring_src + (size_t)i * p.slab_stride, bytes, &ring_full[s]);
+          if (++s == p.nring) { s = 0; ph ^= 1; }
+        }
+    }
+    __syncwarp();
+  } else {
+    const uint32_t tq = tmem + ((uint32_t)(32 * (warp & 3)) << 16);
+    const uint32_t ring_s = sbase + (uint32_t)p.off_ring, stride = (uint32_t)p.slab_stride;
+    const uint32_t id_f1 = idesc_f16(128, (uint32_t)p.N1), id_f2 = idesc_f16(128, (uint32_t)p.N2);
+    const uint32_t id_b2 = idesc_f16(128, (uint32_t)p.N1) | (1u << 16);
+    const uint32_t id_b3 = idesc_f16(128, (uint32_t)p.K1) | (1u << 16);
+    const size_t HW = (size_t)p.HW;
+    uint8_t* const row_k1 = row_of(act, m, p.K1);
+    uint8_t* const row_n1 = row_of(act, m, p.N1);
+    uint8_t* const row_n2 = row_of(act, m, p.N2);
+    uint8_t* const row_nk = row_of(act, m, p.Nk);
+    int rs = 0;
+    uint32_t rph = 0, ph = 0;
+    auto sync8 = [] { asm volatile("bar.sync 1, 256;" ::: "memory"); };
+    auto publish8 = [&] {
+      fence_proxy_async_smem();
+      tc_fence_before();
+      sync8();
+    };
+    auto wait_mma = [&] {
+      mbar_wait(bar_mma, ph);
+      ph ^= 1;
+      tc_fence_after();
+    };
+    for (int t = (int)blockIdx.x; t < p.ntiles; t += (int)gridDim.x) {
+      const int b = t / p.tiles_per_frame;
+      const int px = (t - b * p.tiles_per_frame) * 128 + m;
+      const bool valid = px < p.HW;
+      const int pxc = valid ? px : p.HW - 1;
+      // ---- z -> ACT (K1 columns; kFold: columns n_in, n_in + 1 = 1)
+      {
+        const float* zb = p.z + (size_t)b * p.n_in * HW + pxc;
+#pragma unroll
+        for (int i = 0; i < 4; ++i) {
+          const int c = 2 * i + hh;
+          if (c * 8 < p.K1) {
+            float v[8];
+            uint32_t off = (uint32_t)(c * 8) * (uint32_t)p.HW;
+#pragma unroll
+            for (int j = 0; j < 8; ++j, off += (uint32_t)p.HW) {
+              const int ch = c * 8 + j;
+              v[j] = ch < p.n_in ? __ldcs(zb + off) : ((kFold && ch < p.n_in + 2) ? 1.f : 0.f);
+            }
+            st8f(row_k1, c, v);
+          }
+        }
+      }
+      publish8();
+      if (warp == 0) {
+        tc_fence_after();
+        gemm_ring(tmem, act_s, p.K1 / 16, ring_s, stride, 128u, 256u, id_f1, ring_full, ring_empty, p.nring, rs, rph);
+        umma_commit_elect(bar_mma);
+      }
+      wait_mma();
+      // ---- D1: a1 = relu(pre1) -> ACT (N1), mask1 = [pre1 > 0]
+      uint32_t mask1[4] = {0u, 0u, 0u, 0u};
+#pragma unroll
+      for (int i = 0; i < 8; ++i) {
+        const int g = 2 * i + hh;
+        if (g * 16 < p.N1) {
+          float v[16];
+          tmem_ld16(tq + (uint32_t)(g * 16), v);
+          tmem_ld_wait();
+          if (!kFold) {
+#pragma unroll
+            for (int j = 0; j < 16; ++j) v[j] += s_b1[g * 16 + j];
+          }
+          uint32_t bits = 0;
+#pragma unroll
+          for (int j = 0; j < 16; ++j) bits |= (v[j] > 0.f ? 1u : 0u) << j;
+          mask1[i >> 1] |= bits << ((i & 1) * 16);
+          st8(row_n1, 2 * g, relu2(v[0], v[1]), relu2(v[2], v[3]), relu2(v[4], v[5]), relu2(v[6], v[7]));
+          st8(row_n1, 2 * g + 1, relu2(v[8], v[9]), relu2(v[10], v[11]), relu2(v[12], v[13]), relu2(v[14], v[15]));
+        }
+      }
+      publish8();
+      if (warp == 0) {
+        tc_fence_after();
+        gemm_ring(tmem, act_s, p.N1 / 16, ring_s, stride, 128u, 256u, id_f2, ring_full, ring_empty, p.nring, rs, rph);
+        umma_commit_elect(bar_mma);
+      }
+      // dL/dbeta of this tile (in flight during F2) and its per-pixel exponent
+      float gv[8][8];
+      {
+        const float* gbb = p.gb + (size_t)b * p.K * HW + pxc;
+#pragma unroll
+        for (int i = 0; i < 8; ++i) {
+          const int c = 2 * i + hh;
+          uint32_t off = (uint32_t)(c * 8) * (uint32_t)p.HW;
+#pragma unroll
+          for (int j = 0; j < 8; ++j, off += (uint32_t)p.HW) gv[i][j] = (c * 8 + j < p.K) ? __ldcs(gbb + off) : 0.f;
+        }
+      }
+      float mx = 0.f;
+#pragma unroll
+      for (int i = 0; i < 8; ++i)
+#pragma unroll
+        for (int j = 0; j < 8; ++j) mx = fmaxf(mx, fabsf(gv[i][j]));
+      s_max[hh * 128 + m] = mx;
+      wait_mma();  // F2 done: ACT is free, D2 in the region
+      // ---- D2: mask2 = [pre2 > 0] bits (the region is then free for D3)
+      uint32_t mask2[4] = {0u, 0u, 0u, 0u};
+#pragma unroll
+      for (int i = 0; i < 8; ++i) {
+        const int g = 2 * i + hh;
+        if (g * 16 < p.N2) {
+          float v[16];
+          tmem_ld16(tq + (uint32_t)(g * 16), v);
+          tmem_ld_wait();
+          uint32_t bits = 0;
+#pragma unroll
+          for (int j = 0; j < 16; ++j) bits |= (v[j] + (kFold ? 0.f : s_b2[g * 16 + j]) > 0.f ? 1u : 0u) << j;
+          mask2[i >> 1] |= bits << ((i & 1) * 16);
+        }
+      }
+      sync8();  // s_max of both halves
+      mx = fmaxf(s_max[m], s_max[128 + m]);
+      const int ex = (int)((__float_as_uint(mx) >> 23) & 0xffu) - 126;
+      const int e1 = (-ex) / 2;
+      {
+        const float s1 = exp2i(e1), s2 = exp2i(-ex - e1);
+#pragma unroll
+        for (int i = 0; i < 8; ++i) {
+          const int c = 2 * i + hh;
+          if (c * 8 < p.Nk) {
+            float v[8];
+#pragma unroll
+            for (int j = 0; j < 8; ++j) v[j] = gv[i][j] * s1 * s2;
+            st8f(row_nk, c, v);
+          }
+        }
+      }
+      publish8();
+      if (warp == 0) {
+        tc_fence_after();
+        gemm_ring(tmem, act_s, p.Nk / 16, ring_s, stride, 128u, 256u, id_f2, ring_full, ring_empty, p.nring, rs, rph);
+        umma_commit_elect(bar_mma);
+      }
+      wait_mma();
+      // ---- D3 (W3^T g3): g2 = mask2 ? D3 : 0 -> ACT (N2)
+#pragma unroll
+      for (int i = 0; i < 8; ++i) {
+        const int g = 2 * i + hh;
+        if (g * 16 < p.N2) {
+          float v[16];
+          tmem_ld16(tq + (uint32_t)(g * 16), v);
+          tmem_ld_wait();
+          const uint32_t bits = mask2[i >> 1] >> ((i & 1) * 16);
+#pragma unroll
+          for (int j = 0; j < 16; ++j) v[j] = ((bits >> j) & 1u) ? v[j] : 0.f;
+          st8f(row_n2, 2 * g, v);
+          st8f(row_n2, 2 * g + 1, v + 8);
+        }
+      }
+      publish8();
+      if (warp == 0) {
+        tc_fence_after();
+        gemm_ring(tmem, act_s, p.N2 / 16, ring_s, stride, (uint32_t)p.N1 * 16u, 128u, id_b2, ring_full, ring_empty,
+                  p.nring, rs, rph);
+        umma_commit_elect(bar_mma);
+      }
+      wait_mma();
+      // ---- D4 (W2^T g2): g1 = mask1 ? D4 : 0 -> ACT (N1)
+#pragma unroll
+      for (int i = 0; i < 8; ++i) {
+        const int g = 2 * i + hh;
+        if (g * 16 < p.N1) {
+          float v[16];
+          tmem_ld16(tq + (uint32_t)(g * 16), v);
+          tmem_ld_wait();
+          const uint32_t bits = mask1[i >> 1] >> ((i & 1) * 16);
+#pragma unroll
+          for (int j = 0; j < 16; ++j) v[j] = ((bits >> j) & 1u) ? v[j] : 0.f;
+          st8f(row_n1, 2 * g, v);
+          st8f(row_n1, 2 * g + 1, v + 8);
+        }
+      }
+      publish8();
+      if (warp == 0) {
+        tc_fence_after();
+        gemm_ring(tmem, act_s, p.N1 / 16, ring_s, stride, (uint32_t)p.K1 * 16u, 128u, id_b3, ring_full, ring_empty,
+                  p.nring, rs, rph, p.g3, (uint32_t)p.K1 * 32u);
+        umma_commit_elect(bar_mma);
+      }
+      wait_mma();
+      // ---- D5 (W1^T g1) -> dL/dz, unscaled
+#pragma unroll
+      for (int i = 0; i < 2; ++i) {
+        const int g = 2 * i + hh;
+        if (g * 16 < p.K1) {
+          float v[16];
+          tmem_ld16(tq + (uint32_t)(g * 16), v);
+          tmem_ld_wait();
+          if (valid) {
+            const float u1 = exp2i(-e1), u2 = exp2i(ex + e1);
+            float* gzb = p.gz + (size_t)b * p.n_in * HW + px;
+            uint32_t off = (uint32_t)(g * 16) * (uint32_t)p.HW;
+#pragma unroll
+            for (int j = 0; j < 16; ++j, off += (uint32_t)p.HW)
+              if (g * 16 + j < p.n_in) __stcs(gzb + off, v[j] * u1 * u2);
+          }
+        }
+      }
+      tc_fence_before();  // TMEM reads before the next tile's F1 (ordered by its publish)
+    }
+  }
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
+  if (warp == 0) tmem_dealloc<256>(tmem);
 }
 
 }  // namespace p2s

@@ -118,10 +118,11 @@ def test_sass_adjoint_image_kernel(lib):
 
 
 def test_sass_mlp_backward_kernel(lib):
-    """dL/dz (k_mlp_backward: both bias modes x resident / ring weights): 1-CTA UMMAs (kind::f16),
-    TMEM loads, weights brought in by bulk async copies, and no HMMA (SASS evidence)."""
+    """dL/dz (k_mlp_backward resident and k_mlp_backward_s streamed, both bias modes): 1-CTA UMMAs
+    (kind::f16), TMEM loads, weights brought in by bulk async copies, and no HMMA (SASS evidence)."""
     sass = os.popen(f"cuobjdump -sass {lib._name}").read()
-    funcs = [f for f in sass.split("Function : ")[1:] if f.startswith("_ZN3p2s14k_mlp_backward")]
+    funcs = [f for f in sass.split("Function : ")[1:] if f.startswith("_ZN3p2s14k_mlp_backward")
+             or f.startswith("_ZN3p2s16k_mlp_backward_s")]
     assert len(funcs) == 4
     for f in funcs:
         assert "UTCHMMA" in f and "UTCHMMA.2CTA" not in f

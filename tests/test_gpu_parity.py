@@ -694,7 +694,7 @@ def test_full_envelope_at_once(p2s):
     out = r.render(_dev(inp.image), _dev(inp.zernike), _dev(inp.tilt)).cpu().numpy()
     ref, _ = oracle.render(inp.image, inp.zernike, inp.tilt, inp.basis, inp.mlp)
     _cmp(out, ref, "render[envelope corner]")
-    # dL/dz at the envelope corner (ring variant: W2 resident, the other weights streamed)
+    # dL/dz at the envelope corner (the streamed variant)
     assert r.info()["mlp_backward"] == 1
     gbeta = _gbeta(spec, (1, 128, 10, 140), 35)
     gz = r.mlp_backward(_dev(inp.zernike), _dev(gbeta)).cpu().numpy()
@@ -822,13 +822,15 @@ def test_mlp_backward_parity(p2s, name):
     r.close()
 
 
-@pytest.mark.parametrize("name", ["S65_K100_h256", "cfg1", "S33_K100_C2", "W1_H1", "many_tiles_C1_S9"])
-def test_mlp_backward_ring_variant(p2s, name, monkeypatch):
-    """The ring variant (W2 resident, W1 / W3^T / W1^T slabs streamed by a producer warp): chosen
-    for 33-256-256-100 (cfg5's MLP), forced by P2S_MB_RING=1 for MLPs that would fit resident."""
+@pytest.mark.parametrize("name", ["S65_K100_h256", "cfg1", "S33_K100_C2", "W1_H1", "many_tiles_C1_S9", "S1_K1",
+                                  "S17_K128_n64", "narrow_S15_K16"])
+def test_mlp_backward_streamed_variant(p2s, name, monkeypatch):
+    """The streamed variant (two CTAs per SM, every weight slab through a ring fed by a producer
+    warp): chosen for 33-256-256-100 (cfg5's MLP), forced by P2S_MB_MODE=stream for MLPs that
+    would fit resident."""
     spec = SMALL[name]
     if name != "S65_K100_h256":
-        monkeypatch.setenv("P2S_MB_RING", "1")
+        monkeypatch.setenv("P2S_MB_MODE", "stream")
     inp = synth.make_inputs(spec)
     B, n_in, H, W = inp.zernike.shape
     gbeta = _gbeta(spec, (B, spec.K, H, W), 34)
@@ -836,7 +838,7 @@ def test_mlp_backward_ring_variant(p2s, name, monkeypatch):
     assert r.info()["mlp_backward"] == 1
     gz = r.mlp_backward(_dev(inp.zernike), _dev(gbeta)).cpu().numpy()
     ref, alts = _dz_ref(inp, gbeta.astype(np.float64))
-    _dz_check(gz, ref, alts, f"dL/dz ring[{name}]")
+    _dz_check(gz, ref, alts, f"dL/dz streamed[{name}]")
     r.close()
 
 

@@ -1,6 +1,6 @@
 """Times p2s_mlp_backward (dL/dz through the P2S MLP): one cfg3 frame and a 16-frame batch
-(resident weights), cfg3 with the ring variant forced (P2S_MB_RING=1), and one cfg5 frame
-(33-256-256-100: the ring variant). CUDA events, L2 warm and flushed. Tools only: synthetic
+(resident weights), cfg3 with the streamed variant forced (P2S_MB_MODE=stream), and one cfg5 frame
+(33-256-256-100: the streamed variant). CUDA events, L2 warm and flushed. Tools only: synthetic
 inputs, no oracle."""
 import json
 import os
@@ -17,9 +17,9 @@ def run(cfg, Bs, ring, res):
     spec = synth.CONFIGS[cfg]
     inp = synth.make_inputs(spec, frames=[0])
     if ring:
-        os.environ["P2S_MB_RING"] = "1"
+        os.environ["P2S_MB_MODE"] = "stream"
     r = p2s.Renderer(inp.basis, inp.mlp)
-    os.environ.pop("P2S_MB_RING", None)
+    os.environ.pop("P2S_MB_MODE", None)
     flush = torch.empty(256 << 20, dtype=torch.uint8, device="cuda")
     n_in, H, W = inp.zernike.shape[1:]
     h1, h2, K = inp.mlp["W1"].shape[0], inp.mlp["W2"].shape[0], spec.K
@@ -44,7 +44,7 @@ def run(cfg, Bs, ring, res):
             px = B * H * W
             macs = px * (n_in * h1 + h1 * h2 + K * h2 + h2 * h1 + h1 * n_in)
             byts = px * (2 * n_in + K) * 4
-            res[f"cfg{cfg}{'_ring' if ring else ''}_B{B}_{mode}"] = {
+            res[f"cfg{cfg}{'_stream' if ring else ''}_B{B}_{mode}"] = {
                 "us": us, "us_per_frame": us / B, "tflops": 2 * macs / us / 1e6, "gbs": byts / us / 1e3}
     r.close()
 
