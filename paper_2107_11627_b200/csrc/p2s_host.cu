@@ -819,7 +819,13 @@ p2s_status p2s_init(const p2s_basis* basis, const p2s_mlp* mlp, p2s_handle** out
         // slab table, per tile: [F1: W1 K-slabs | F2: W2 K-slabs | B1: W3^T K-slabs | B2: W2 row
         // pairs (W2^T K'-slabs) | B3: W1 row pairs, g3 per slot]; K-slabs re-laid [N][16]
         // (lbo 128, sbo 256), row pairs as stored (lbo 16 kd, sbo 128)
-        const int slot = std::max(std::max(N1, N2), K1) * 32, g3 = std::max(1, slot / (K1 * 32)), nring = 4;
+        // ring depth: as many slots as two CTAs per SM leave room for (a slot refill is an L2 round
+        // trip, so the depth sets the slab throughput), at most 16
+        const int slot = std::max(std::max(N1, N2), K1) * 32, g3 = std::max(1, slot / (K1 * 32));
+        const int per_cta = 233472 / 2 - 1024, fixed = al128(bb) + act_bytes + 288 + 2 * 128 * 4;
+        int nring = std::min(16, (per_cta - fixed) / slot);
+        if (const char* e = std::getenv("P2S_MB_NRING")) nring = std::max(2, std::min(nring, std::atoi(e)));
+        if (nring < 2) return fail(P2S_ERR_UNSUPPORTED);  // not reached inside the envelope
         const int nb3 = N1 / 16;
         const int nsl = K1 / 16 + N1 / 16 + Nk / 16 + N2 / 16 + (nb3 + g3 - 1) / g3;
         std::vector<uint8_t> st((size_t)bb + (size_t)nsl * slot, 0);
@@ -843,7 +849,7 @@ p2s_status p2s_init(const p2s_basis* basis, const p2s_mlp* mlp, p2s_handle** out
           std::memcpy(tab + (size_t)i * slot, reinterpret_cast<const uint8_t*>(W1h.data()) + (size_t)ks * K1 * 32,
                       (size_t)std::min(g3, nb3 - ks) * K1 * 32);
         const int off_ring = al128(bb), off_act = off_ring + al128(nring * slot), off_bar = off_act + act_bytes;
-        const int smem = off_bar + 160 + 2 * 128 * 4;
+        const int smem = off_bar + 288 + 2 * 128 * 4;
         if ((e = cudaMalloc(&h->d_mlpb, st.size())) != cudaSuccess ||
             (e = cudaMemcpy(h->d_mlpb, st.data(), st.size(), cudaMemcpyHostToDevice)) != cudaSuccess)
           return fail(cuda_fail(e, "dz slab table"));

@@ -397,9 +397,9 @@ __global__ void __launch_bounds__(kMbsThreads, 2) k_mlp_backward_s(const __grid_
   const uint32_t sbase = smem_u32(smem);
   uint64_t* bar_mma = reinterpret_cast<uint64_t*>(smem + p.off_bar);
   uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bar_mma + 1);
-  uint64_t* ring_full = bar_mma + 2;
-  uint64_t* ring_empty = ring_full + 8;
-  float* s_max = reinterpret_cast<float*>(smem + p.off_bar + 160);  // [2][128]
+  uint64_t* ring_full = bar_mma + 2;  // [<= 16]
+  uint64_t* ring_empty = ring_full + 16;
+  float* s_max = reinterpret_cast<float*>(smem + p.off_bar + 288);  // [2][128]
   const float* s_b1 = reinterpret_cast<const float*>(smem + p.off_bias);
   const float* s_b2 = s_b1 + p.N1;
   uint8_t* act = smem + p.off_act;
