@@ -548,7 +548,7 @@ def main():
         "plan": info,
         "context": PAPER_CONTEXT,
     }
-    if not args.no_cpu_baseline:
+    if not args.no_cpu_baseline and world == 1:  # the oracle baseline: rank 0 at N = 1 only
         import oracle
         threads = oracle.default_threads()
         fps, tcpu, rows, sample = cpu_reference(spec, inp, args.cpu_budget, threads)
