@@ -37,5 +37,22 @@ def build(force: bool = False, verbose: bool = False, profile: bool = False) -> 
     return lib
 
 
+EXAMPLE_SRC = os.path.join(ROOT, "examples", "render_c_abi.c")
+EXAMPLE_BIN = os.path.join(ROOT, "examples", "render_c_abi")
+
+
+def build_example() -> str:
+    """Compiles examples/render_c_abi.c, a plain-C client of the C ABI (gcc, no C++/PyTorch)."""
+    cuda = os.path.dirname(os.path.dirname(NVCC))
+    cmd = ["gcc", "-O2", "-std=c99", "-Wall", f"-I{os.path.join(ROOT, 'include')}", f"-I{cuda}/include",
+           EXAMPLE_SRC, f"-L{PKG}", "-lp2s", f"-L{cuda}/lib64", "-lcudart", "-lm",
+           "-Wl,-rpath,$ORIGIN/../paper_2107_11627_b200", f"-Wl,-rpath,{cuda}/lib64", "-o", EXAMPLE_BIN]
+    r = subprocess.run(cmd, capture_output=True, text=True)
+    if r.returncode != 0:
+        sys.stderr.write(r.stdout + r.stderr)
+        raise RuntimeError("gcc failed building examples/render_c_abi")
+    return EXAMPLE_BIN
+
+
 if __name__ == "__main__":
     print(build(force="--force" in sys.argv, verbose=True, profile="--profile" in sys.argv))

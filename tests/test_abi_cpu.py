@@ -128,3 +128,13 @@ def test_sass_mlp_backward_kernel(lib):
         assert "UTCHMMA" in f and "UTCHMMA.2CTA" not in f
         assert "LDTM" in f and "UBLKCP" in f
         assert "HMMA" not in f.replace("UTCHMMA", "")
+
+
+def test_plain_c_client_builds_against_the_abi(lib):
+    """examples/render_c_abi.c (C99, gcc, no C++ or PyTorch) compiles and links against the header
+    and libp2s.so alone: the boundary is a C ABI."""
+    from paper_2107_11627_b200 import build
+    exe = build.build_example()
+    assert os.path.exists(exe)
+    deps = os.popen(f"ldd {exe}").read()
+    assert "libp2s.so" in deps and "torch" not in deps

@@ -1087,3 +1087,15 @@ def test_two_handles_on_two_streams_concurrently(p2s):
                                        atol=1e-3 * np.abs(alone[k][2]).max())
     for r in rs:
         r.close()
+
+
+def test_plain_c_client_runs(p2s):
+    """examples/render_c_abi: a C program renders through the ABI (delta basis, integer tilt ->
+    the closed-form shift) and back-propagates; it checks its own result (exit 0)."""
+    import subprocess
+    from paper_2107_11627_b200 import build
+    exe = build.build_example()
+    r = subprocess.run([exe], capture_output=True, text=True, timeout=120)
+    print(r.stdout)
+    assert r.returncode == 0, r.stdout + r.stderr
+    assert "render_c_abi: ok" in r.stdout
