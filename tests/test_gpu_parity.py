@@ -1099,3 +1099,37 @@ def test_plain_c_client_runs(p2s):
     print(r.stdout)
     assert r.returncode == 0, r.stdout + r.stderr
     assert "render_c_abi: ok" in r.stdout
+
+
+def test_adjoint_chain_is_cuda_graph_capturable(p2s):
+    """After one eager call has sized the workspace, the whole adjoint chain of the anchor path
+    (interp -> p2s_backward with dL/dt and dL/dI -> p2s_mlp_backward -> p2s_anchors_backward) is
+    captured in one CUDA graph and replayed on new inputs; it matches the eager call (dL/dJ's float
+    atomics make the last bits order-dependent)."""
+    import torch
+    spec = SMALL["ragged_rgb_S7"]
+    inp = synth.make_inputs(spec)
+    r = p2s.Renderer(inp.basis, inp.mlp)
+    G = 5
+    img, t, g = _dev(inp.image), _dev(inp.tilt), _dev(synth.make_upstream_grad(spec))
+    A = _dev(_anchors(spec, G, 51))
+    s = torch.cuda.Stream()
+    with torch.cuda.stream(s):
+        r.backward_anchors(img, A, t, g, want_image=True, stream=s)  # sizes the workspace
+    torch.cuda.synchronize()
+    graph = torch.cuda.CUDAGraph()
+    with torch.cuda.graph(graph, stream=s):
+        outs = r.backward_anchors(img, A, t, g, want_image=True, stream=s)
+    spec2 = synth.custom("ragged_rgb_S7", 302, B=2, C=3, H=37, W=200, K=20, S=7, h1=48, h2=40, t_std=1.7)
+    inp2 = synth.make_inputs(spec2)
+    img.copy_(_dev(inp2.image)); t.copy_(_dev(inp2.tilt)); g.copy_(_dev(synth.make_upstream_grad(spec2)))
+    A.copy_(_dev(_anchors(spec2, G, 52)))
+    graph.replay()
+    torch.cuda.synchronize()
+    eager = r.backward_anchors(_dev(inp2.image), _dev(_anchors(spec2, G, 52)), _dev(inp2.tilt),
+                               _dev(synth.make_upstream_grad(spec2)), want_image=True)
+    torch.cuda.synchronize()
+    for what, a, b in zip(("dL/dA", "dL/dt", "dL/dI"), outs, eager):
+        a, b = a.cpu().numpy(), b.cpu().numpy()
+        np.testing.assert_allclose(a, b, rtol=1e-4, atol=1e-4 * np.abs(b).max(), err_msg=what)
+    r.close()
