@@ -1,6 +1,7 @@
 """Per-role cycle breakdown of k_fused_p2s (needs libp2s_prof.so, built with -DP2S_PROFILE).
 
 Usage: P2S_LIB=paper_2107_11627_b200/libp2s_prof.so python tools/role_profile.py [cfg]
+       (ADJ=image: the adjoint's fused pass instead of the render; ANCHOR_G=G: anchor mode)
 Counters (clock64 cycles, averaged over CTAs), per role:
   MMA issuer : 0 wait A1_FULL, 1 wait BETA_FREE, 2 wait SCR_FREE, 3 wait E_FULL,
                4 wait ring (MLP), 5 wait ring (conv), 6 wait ACC_FREE (first conv stage), 19 total
@@ -26,7 +27,11 @@ r = p2s.Renderer(inp.basis, inp.mlp)
 img, z, t = (torch.from_numpy(a).cuda() for a in (inp.image, inp.zernike, inp.tilt))
 out = torch.empty_like(img)
 ANCH = int(os.environ.get("ANCHOR_G", "0"))  # >0: anchor-grid mode (p2s_render_anchors) with this G
-if ANCH:
+ADJ = os.environ.get("ADJ")  # "image": the adjoint's fused pass (mode 3: J + U = beta dL/dJ)
+if ADJ:
+    gg = torch.from_numpy(synth.make_upstream_grad(spec, frames=range(1))).cuda()
+    render = lambda: r.backward(img, z, t, gg, want_beta=False, want_tilt=False, want_image=True)  # noqa: E731
+elif ANCH:
     anc = torch.from_numpy(synth.make_anchors(spec, ANCH, frames=range(1))).cuda()
     render = lambda: r.render_anchors(img, anc, t, out=out)  # noqa: E731
 else:
