@@ -64,6 +64,9 @@ SMALL = {
     "S31": synth.custom("s31", 207, B=1, C=3, H=12, W=100, K=40, S=31, h1=64, h2=64, t_std=1.0),
     "S25": synth.custom("s25", 208, B=1, C=1, H=12, W=129, K=60, S=25, h1=100, h2=150, t_std=1.0),
     "W1_H1": synth.custom("w1h1", 209, B=3, C=3, H=1, W=1, K=8, S=5, h1=16, h2=16, t_std=0.7),
+    # degenerate widths: one Zernike input, one hidden unit per layer, one basis function
+    # (seed 215: both units active on ~78 % of the pixels, so beta varies and the masks matter)
+    "tiny_widths": synth.custom("tiny", 215, B=2, C=2, H=19, W=133, K=1, S=3, n_in=1, h1=1, h2=1, t_std=1.1),
     # many tiles per CTA (both E buffers, ring wrap-around) with C = 2 and C = 1
     "many_tiles_C2": synth.custom("mt2", 211, B=2, C=2, H=300, W=130, K=32, S=17, h1=64, h2=96,
                                   t_std=1.2),
@@ -723,7 +726,7 @@ def test_large_ragged_frame_sampled(p2s):
 #      oracle.adjoint.mlp_backward with the masks decided in the GPU's fp16 precision (reading N5)
 
 DZ_CASES = ["cfg1", "ragged_rgb_S7", "narrow_S15_K16", "S33_K100_C2", "S1_K1", "S17_K128_n64", "S25", "W1_H1",
-            "many_tiles_C1_S9"]
+            "many_tiles_C1_S9", "tiny_widths"]
 
 
 def _dz_ref(inp, gbeta, amb_rel=(2e-5, 2e-4)):
