@@ -465,7 +465,7 @@ def test_sampled_anchors_render_end_to_end(p2s):
 #      forward bar) each channel's d out/d s errs by <= 2e, so max abs <= 2 e C max|g|.
 #      The bilinear cell (an integer decided by s = p - t) is taken in fp32 on both sides (reading N4).
 
-ADJ_CASES = ["ragged_rgb_S7", "S33_K100_C2", "many_tiles_C2", "S1_K1", "W1_H1", "S65_K100_h256",
+ADJ_CASES = ["ragged_rgb_S7", "S33_K100_C2", "many_tiles_C2", "S1_K1", "W1_H1", "S65_K100_h256", "tiny_widths",
              "many_tiles_C1_S9"]
 
 
@@ -570,7 +570,8 @@ def test_backward_invalid_args(p2s):
 # ---- wavelength-dependent colour: per-channel Zernike fields -> per-channel
 #      beta, vs oracle.render_color (each channel rendered alone with its own field)
 
-COLOR_CASES = ["ragged_rgb_S7", "S33_K100_C2", "many_tiles_C2", "S65_K100_h256", "W1_H1", "many_tiles_C1_S9"]
+COLOR_CASES = ["ragged_rgb_S7", "S33_K100_C2", "many_tiles_C2", "S65_K100_h256", "W1_H1", "many_tiles_C1_S9",
+               "tiny_widths"]
 
 
 @pytest.mark.parametrize("name", COLOR_CASES)
