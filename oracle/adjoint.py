@@ -267,3 +267,26 @@ def anchors_backward(gfield, G):
     B, n_in, H, W = g.shape
     Wy, Wx = anchor_weights(H, G), anchor_weights(W, G)
     return np.einsum("ya,bkyx,xc->bkac", Wy, g, Wx)
+
+
+def backward_color(image, zernike_c, tilt, basis, mlp, g, coord_dtype=np.float64, mask_precision="fp64"):
+    """Adjoint of the wavelength-dependent colour render (oracle.render_color):
+    channel c of a frame is a one-channel render with its own beta_c = P2S(z_c), so for one frame
+    (image [C][H][W], zernike_c [C][n_in][H][W], tilt [2][H][W], g = dL/dout [C][H][W]):
+        dL/dbeta_c = backward(I_c, beta_c, t, g_c).dbeta,   dL/dI_c = backward(...).dI,
+        dL/dt = sum_c backward(...).dt,                       dL/dz_c = mlp_backward(z_c, dL/dbeta_c)
+    Returns (dbeta [C][K][H][W], dt [2][H][W], dI [C][H][W], dz [C][n_in][H][W]), fp64."""
+    from oracle import beta as _beta  # the C oracle's beta (forward of step a1)
+    image = np.asarray(image)
+    C = image.shape[0]
+    gb, gi, gz = [], [], []
+    gt = None
+    for c in range(C):
+        zc = np.ascontiguousarray(zernike_c[c], np.float32)
+        bc = _beta(image[None, c:c + 1], zc[None], basis, mlp)[0]
+        _, gbc, gtc, gic = backward(image[c:c + 1], bc, tilt, basis, g[c:c + 1], coord_dtype=coord_dtype)
+        gb.append(gbc)
+        gi.append(gic[0])
+        gt = gtc if gt is None else gt + gtc
+        gz.append(mlp_backward(zc.astype(np.float64), gbc, mlp, mask_precision))
+    return np.stack(gb), gt, np.stack(gi), np.stack(gz)

@@ -624,3 +624,48 @@ def test_anchors_backward_is_the_transpose_of_the_c_interpolation():
         ones = adjoint.anchors_backward(np.ones((1, 1, H, W)), G)[0, 0]
         wy, wx = adjoint.anchor_weights(H, G).sum(0), adjoint.anchor_weights(W, G).sum(0)
         np.testing.assert_allclose(ones, np.outer(wy, wx), rtol=1e-12)
+
+
+def test_backward_color_reduces_to_shared_and_matches_finite_differences():
+    """Adjoint of the wavelength-dependent colour render (oracle.adjoint.backward_color): with every
+    channel's field equal it is the shared-beta adjoint (dL/dbeta = sum_c dL/dbeta_c, dL/dt and
+    dL/dI equal, dL/dz = sum_c dL/dz_c); with different fields, central differences of
+    oracle.render_color (an independent forward) match dL/dz_c, dL/dI and dL/dt at sampled entries."""
+    from oracle import adjoint
+    spec = synth.custom("bcol", 404, B=1, C=3, H=6, W=7, K=4, S=3, h1=10, h2=9, t_std=0.6)
+    inp = synth.make_inputs(spec)
+    img, t = inp.image[0].astype(np.float64), inp.tilt[0]
+    g = np.random.default_rng(6).standard_normal((3, 6, 7))
+    z = inp.zernike[0]
+    zc_eq = np.stack([z] * 3)
+    gb, gt, gi, gz = adjoint.backward_color(img, zc_eq, t, inp.basis, inp.mlp, g)
+    beta = oracle.beta(inp.image, inp.zernike, inp.basis, inp.mlp)[0]
+    _, gb_s, gt_s, gi_s = adjoint.backward(img, beta, t, inp.basis, g)
+    np.testing.assert_allclose(gb.sum(0), gb_s, rtol=1e-10, atol=1e-12)
+    np.testing.assert_allclose(gt, gt_s, rtol=1e-10, atol=1e-12)
+    np.testing.assert_allclose(gi, gi_s, rtol=1e-10, atol=1e-12)
+    np.testing.assert_allclose(gz.sum(0), adjoint.mlp_backward(z.astype(np.float64), gb_s, inp.mlp), rtol=1e-9,
+                               atol=1e-12)
+    # different fields per channel: finite differences of the colour render
+    zc = np.stack([z * s for s in (1.0, 0.8, 1.3)]).astype(np.float32)
+    gb, gt, gi, gz = adjoint.backward_color(img, zc, t, inp.basis, inp.mlp, g)
+
+    def loss(im, zz, tt):
+        o, _ = oracle.render_color(im[None].astype(np.float32), zz[None].astype(np.float32), tt[None].astype(np.float32),
+                                   inp.basis, inp.mlp)
+        return np.sum(g * o[0])
+    rng = np.random.default_rng(7)
+    for _ in range(6):
+        c, j, y, x = rng.integers(0, 3), rng.integers(0, spec.n_in), rng.integers(0, 6), rng.integers(0, 7)
+        e = np.zeros_like(zc)
+        e[c, j, y, x] = 1e-2
+        fd = (loss(img, zc + e, t) - loss(img, zc - e, t)) / 2e-2
+        assert abs(fd - gz[c, j, y, x]) < 2e-4 * (1 + abs(gz[c, j, y, x])), ("z", fd, gz[c, j, y, x])
+        e = np.zeros_like(img)
+        e[c, y, x] = 1e-2
+        fd = (loss(img + e, zc, t) - loss(img - e, zc, t)) / 2e-2
+        assert abs(fd - gi[c, y, x]) < 2e-4 * (1 + abs(gi[c, y, x])), ("I", fd, gi[c, y, x])
+        e = np.zeros(t.shape, np.float64)
+        e[c % 2, y, x] = 1e-3
+        fd = (loss(img, zc, t + e) - loss(img, zc, t - e)) / 2e-3
+        assert abs(fd - gt[c % 2, y, x]) < 1e-3 * (1 + abs(gt[c % 2, y, x])), ("t", fd, gt[c % 2, y, x])
