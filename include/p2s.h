@@ -177,6 +177,22 @@ P2S_API p2s_status p2s_backward(p2s_handle* h, p2s_image image, const float* zer
 P2S_API p2s_status p2s_mlp_backward(p2s_handle* h, const float* zernike_field, const float* grad_beta, int B,
                                     int H, int W, float* grad_zernike, p2s_stream_t stream);
 
+/* Adjoint of p2s_render_color (SURVEY §8(f) row 5 with NEXT-4): channel c
+ * of frame b is a one-channel render with its own field z[b][c], so for grad_out = dL/dout
+ * (DEVICE [B][C][H][W]) it writes
+ *   grad_beta    (DEVICE [B][C][K][H][W] or NULL)     dL/dbeta_c of each channel's own beta
+ *   grad_tilt    (DEVICE [B][2][H][W] or NULL)        summed over the channels
+ *   grad_image   (DEVICE [B][C][H][W] or NULL)
+ *   grad_zernike (DEVICE [B][C][n_in][H][W] or NULL)  dL/dz_c through the MLP (p2s_mlp_backward)
+ * each (frame, channel) as p2s_backward / p2s_mlp_backward on that channel's plane (their
+ * precision notes apply). zernike_field as p2s_render_color. Workspace (one channel's dL/dt, and
+ * dL/dbeta when only dL/dz is wanted) grows on first use (synchronising). Errors as p2s_backward;
+ * all four outputs NULL -> P2S_ERR_INVALID_ARG. */
+P2S_API p2s_status p2s_backward_color(p2s_handle* h, p2s_image image, const float* zernike_field,
+                                      const float* tilt_field, const float* grad_out, float* grad_beta,
+                                      float* grad_tilt, float* grad_image, float* grad_zernike,
+                                      p2s_stream_t stream);
+
 /* The anchor-grid interpolation ("anchor points ... interpolated"; registration
  * DESIGN.md reading N1 — pixel centre (t + 0.5), anchors at a n / (G - 1)) as a standalone op and
  * its adjoint, so the anchor pipeline is differentiable end to end:

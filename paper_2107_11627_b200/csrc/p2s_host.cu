@@ -118,6 +118,8 @@ struct p2s_handle {
   std::vector<Item> items;  // [items_full | items_beta]
   int n_items_full = 0, n_items_beta = 0, n_items_first = 0, n_items_seq = 0, n_items_conv = 0, tab_cap = 0;
   float* d_gJ = nullptr;  // adjoint workspace dL/dJ
+  float* d_col_ws = nullptr;  // colour adjoint: per-channel dL/dt and (if needed) dL/dbeta planes
+  size_t col_ws_cap = 0;
   size_t gJ_cap = 0;
   // dL/dI (k_adjoint_image): plan, phi table, workspaces beta [B][K][H][W] fp32 and U_T fp16
   int di_R = 0, di_nchunk = 0, di_kg = 0, di_ngroups = 0, di_Nh = 0, di_OW = 0, di_nring = 0, di_smem = 0;
@@ -1118,6 +1120,69 @@ p2s_status p2s_mlp_backward(p2s_handle* h, const float* zernike_field, const flo
   return P2S_OK;
 }
 
+}  // extern "C"
+
+namespace {
+__global__ void __launch_bounds__(256) k_accumulate(float* __restrict__ dst, const float* __restrict__ src, size_t n) {
+  for (size_t i = (size_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (size_t)gridDim.x * blockDim.x)
+    dst[i] += src[i];
+}
+}  // namespace
+
+extern "C" {
+
+p2s_status p2s_backward_color(p2s_handle* h, p2s_image im, const float* zernike_field, const float* tilt_field,
+                              const float* grad_out, float* grad_beta, float* grad_tilt, float* grad_image,
+                              float* grad_zernike, p2s_stream_t stream) {
+  p2s_status s = check_image(h, im);
+  if (s != P2S_OK) return s;
+  if (!zernike_field || !grad_out || (!grad_beta && !grad_tilt && !grad_image && !grad_zernike))
+    return P2S_ERR_INVALID_ARG;
+  if (grad_zernike && !h->mb_ok) return P2S_ERR_UNSUPPORTED;
+  cudaStream_t st = (cudaStream_t)stream;
+  const int B = im.B, C = im.C, H = im.H, W = im.W, K = h->K, n_in = h->n_in;
+  const size_t HW = (size_t)H * W;
+  // workspace: one channel's dL/dt [2][H][W] (channels > 0 are accumulated) and, when dL/dz is
+  // wanted without dL/dbeta, one channel's dL/dbeta [K][H][W]
+  const size_t need = 2 * HW + (grad_zernike && !grad_beta ? (size_t)K * HW : 0);
+  if (need > h->col_ws_cap) {
+    P2S_CUDA(cudaDeviceSynchronize());
+    cudaFree(h->d_col_ws);
+    h->d_col_ws = nullptr;
+    h->col_ws_cap = 0;
+    P2S_CUDA(cudaMalloc(&h->d_col_ws, need * sizeof(float)));
+    h->col_ws_cap = need;
+  }
+  float* gt_tmp = h->d_col_ws;
+  float* gb_tmp = h->d_col_ws + 2 * HW;
+  // channel c of frame b is a one-channel render with its own beta: its
+  // adjoint is p2s_backward on that channel's plane and field, dL/dt summed over the channels
+  for (int b = 0; b < B; ++b)
+    for (int c = 0; c < C; ++c) {
+      const size_t bc = (size_t)b * C + c;
+      p2s_image ic{im.data + bc * HW, 1, 1, H, W};
+      const float* zc = zernike_field + bc * n_in * HW;
+      float* gb = grad_beta ? grad_beta + bc * K * HW : (grad_zernike ? gb_tmp : nullptr);
+      float* gt = grad_tilt ? (c == 0 ? grad_tilt + (size_t)b * 2 * HW : gt_tmp) : nullptr;
+      float* gi = grad_image ? grad_image + bc * HW : nullptr;
+      if (gb || gt || gi) {
+        s = p2s_backward(h, ic, zc, tilt_field ? tilt_field + (size_t)b * 2 * HW : nullptr, grad_out + bc * HW, gb, gt,
+                         gi, stream);
+        if (s != P2S_OK) return s;
+      }
+      if (grad_tilt && c > 0) {
+        k_accumulate<<<(int)std::min<size_t>((2 * HW + 255) / 256, (size_t)h->sm_count * 8), 256, 0, st>>>(
+            grad_tilt + (size_t)b * 2 * HW, gt_tmp, 2 * HW);
+        P2S_CUDA(cudaPeekAtLastError());
+      }
+      if (grad_zernike) {
+        s = p2s_mlp_backward(h, zc, gb, 1, H, W, grad_zernike + bc * n_in * HW, stream);
+        if (s != P2S_OK) return s;
+      }
+    }
+  return P2S_OK;
+}
+
 p2s_status p2s_render_anchors(p2s_handle* h, p2s_image im, const float* anchors, int G,
                               const float* tilt_field, float* out, p2s_stream_t stream) {
   p2s_status s = check_image(h, im);
@@ -1360,6 +1425,7 @@ void p2s_destroy(p2s_handle* h) {
   cudaFree(h->d_gJ);
   cudaFree(h->d_dib); cudaFree(h->d_ut);
   cudaFree(h->d_mlpb);
+  cudaFree(h->d_col_ws);
   if (h->s_in) cudaStreamDestroy(h->s_in);
   if (h->ev_entry) cudaEventDestroy(h->ev_entry);
   if (h->ev_band) cudaEventDestroy(h->ev_band);

@@ -28,7 +28,7 @@ EXPORTED = ("p2s_init", "p2s_render", "p2s_render_host", "p2s_reserve", "p2s_set
             "p2s_render_anchors", "p2s_render_anchors_host", "p2s_debug_blur_anchors",
             "p2s_render_sequence", "p2s_sampler_init", "p2s_sample_anchors", "p2s_sampler_destroy",
             "p2s_backward", "p2s_render_color", "p2s_mlp_backward", "p2s_interp_anchors",
-            "p2s_anchors_backward")
+            "p2s_anchors_backward", "p2s_backward_color")
 
 
 class P2SError(RuntimeError):
@@ -104,12 +104,14 @@ def load_library(path: str = LIB_PATH) -> ctypes.CDLL:
     lib.p2s_mlp_backward.argtypes = [v, v, v, i, i, i, v, v]
     lib.p2s_interp_anchors.argtypes = [v, i, i, i, i, i, v, v]
     lib.p2s_anchors_backward.argtypes = [v, i, i, i, i, i, v, v]
+    lib.p2s_backward_color.argtypes = [v, _Image, v, v, v, v, v, v, v, v]
     lib.p2s_sampler_destroy.restype = None
     for name in ("p2s_init", "p2s_render", "p2s_render_host", "p2s_reserve", "p2s_set_profile_events",
                  "p2s_get_info", "p2s_debug_beta", "p2s_debug_blur", "p2s_debug_profile_buffer",
                  "p2s_render_anchors", "p2s_render_anchors_host", "p2s_debug_blur_anchors",
                  "p2s_render_sequence", "p2s_sampler_init", "p2s_sample_anchors", "p2s_backward",
-                 "p2s_render_color", "p2s_mlp_backward", "p2s_interp_anchors", "p2s_anchors_backward"):
+                 "p2s_render_color", "p2s_mlp_backward", "p2s_interp_anchors", "p2s_anchors_backward",
+                 "p2s_backward_color"):
         getattr(lib, name).restype = st
     _lib = lib
     return lib
@@ -238,6 +240,27 @@ class Renderer:
         gb, gt, gi, gz = self.backward(image, z, tilt, grad_out, want_beta=False, want_tilt=want_tilt,
                                        want_image=want_image, want_zernike=True, stream=stream)
         return anchors_backward(gz, G, stream=stream), gt, gi
+
+    def backward_color(self, image, zernike_color, tilt, grad_out, want_beta=True, want_tilt=True, want_image=False,
+                       want_zernike=False, stream=None):
+        """p2s_backward_color: (dL/dbeta [B,C,K,H,W], dL/dt [B,2,H,W], dL/dI [B,C,H,W], dL/dz [B,C,n_in,H,W])
+        of render_color (entries None when not wanted)."""
+        import torch
+        B, C, H, W = image.shape
+        im = _Image(_dev_ptr(image, "image").value, B, C, H, W)
+        zp = _dev_ptr(zernike_color, "zernike_field", (B, C, self.n_in, H, W))
+        tp = _dev_ptr(tilt, "tilt_field", (B, 2, H, W)) if tilt is not None else ctypes.c_void_p()
+        gp = _dev_ptr(grad_out, "grad_out", (B, C, H, W))
+        kw = dict(device=image.device, dtype=torch.float32)
+        gb = torch.empty((B, C, self.K, H, W), **kw) if want_beta else None
+        gt = torch.empty((B, 2, H, W), **kw) if want_tilt else None
+        gi = torch.empty((B, C, H, W), **kw) if want_image else None
+        gz = torch.empty((B, C, self.n_in, H, W), **kw) if want_zernike else None
+        ptr = lambda t, n: _dev_ptr(t, n) if t is not None else ctypes.c_void_p()  # noqa: E731
+        _check(self._lib.p2s_backward_color(self._h, im, zp, tp, gp, ptr(gb, "grad_beta"), ptr(gt, "grad_tilt"),
+                                            ptr(gi, "grad_image"), ptr(gz, "grad_zernike"), _stream_handle(stream)),
+               "p2s_backward_color")
+        return gb, gt, gi, gz
 
     def mlp_backward(self, zernike, grad_beta, out=None, stream=None):
         """p2s_mlp_backward: dL/dz [B,n_in,H,W] through the P2S MLP for dL/dbeta [B,K,H,W]."""
