@@ -433,11 +433,30 @@ def main():
             c1[i].record(stream)
         torch.cuda.synchronize()
         c_ms = pdist.max_over_ranks(float(sum(c0[i].elapsed_time(c1[i]) for i in range(n_c))), dist, dev)
+        # its adjoint (p2s_backward_color): dL/dbeta_c, dL/dt, dL/dI and dL/dz_c of the same frame
+        cg = torch.from_numpy(synth.make_upstream_grad(spec, frames=pdist.rank_frames(rank, 1))).to(dev)
+        adj_v = None
+        if r.info()["mlp_backward"]:
+            for _ in range(2):
+                r.backward_color(cimg, cz, ct, cg, want_image=True, want_zernike=True)
+            n_ca = max(3, min(args.steps // 20, 20))
+            c0 = [torch.cuda.Event(enable_timing=True) for _ in range(n_ca)]
+            c1 = [torch.cuda.Event(enable_timing=True) for _ in range(n_ca)]
+            torch.cuda.synchronize()
+            for i in range(n_ca):
+                flush.fill_(float(i))
+                c0[i].record(stream)
+                r.backward_color(cimg, cz, ct, cg, want_image=True, want_zernike=True)
+                c1[i].record(stream)
+            torch.cuda.synchronize()
+            ca_ms = pdist.max_over_ranks(float(sum(c0[i].elapsed_time(c1[i]) for i in range(n_ca))), dist, dev)
+            adj_v = pdist.throughput(1, world, n_ca, ca_ms)
         color_mode = {"value": pdist.throughput(1, world, n_c, c_ms), "unit": "frames/s", "calls": n_c,
                       "api": "p2s_render_color",
+                      "adjoint_value": adj_v, "adjoint_api": "p2s_backward_color (all four gradients)",
                       "note": "cfg3 frame, per-channel Zernike fields (z * 540/lambda, lambda = 570/540/450 nm) "
                               "-> per-channel beta; the convolutions once per tile, 3 MLP + J passes"}
-        del cimg, ct, cz, cout
+        del cimg, ct, cz, cout, cg
 
     # ---- anchor-grid mode: the same frame with its Zernike coefficients
     # given on a 16x16 anchor grid and interpolated inside the fused kernel (not the headline
