@@ -30,7 +30,7 @@ from paper_2107_11627_b200 import dist as pdist  # noqa: E402
 from paper_2107_11627_b200 import synth  # noqa: E402
 
 CFG_ID = 3
-FUSED_EVERY = 4  # steps per fused-kernel event pair (roofline timing; see the timed loop)
+FUSED_EVERY = 10  # steps per fused-kernel event pair (roofline timing; see the timed loop)
 METRIC = "frames/s and output Mpix/s (512x512 RGB, K=100); tensor-pipe % of peak"
 PAPER_CONTEXT = ("Paper: 0.026 s per 256x256 frame (whole simulator, Tesla V100, precision not "
                  "stated; PAPER.md:514/500). Hardie et al. split-step: 24.36 s per frame (PAPER.md:511).")
