@@ -184,10 +184,11 @@ P2S_API p2s_status p2s_mlp_backward(p2s_handle* h, const float* zernike_field, c
  *   grad_tilt    (DEVICE [B][2][H][W] or NULL)        summed over the channels
  *   grad_image   (DEVICE [B][C][H][W] or NULL)
  *   grad_zernike (DEVICE [B][C][n_in][H][W] or NULL)  dL/dz_c through the MLP (p2s_mlp_backward)
- * each (frame, channel) as p2s_backward / p2s_mlp_backward on that channel's plane (their
- * precision notes apply). zernike_field as p2s_render_color. Workspace (one channel's dL/dt, and
- * dL/dbeta when only dL/dz is wanted) grows on first use (synchronising). Errors as p2s_backward;
- * all four outputs NULL -> P2S_ERR_INVALID_ARG. */
+ * as ONE p2s_backward over the B*C one-channel frames the colour layouts already are (tilt
+ * replicated per channel) and one p2s_mlp_backward (their precision notes apply). zernike_field
+ * as p2s_render_color. Workspace (replicated tilt and per-channel dL/dt [B*C][2][H][W]; dL/dbeta
+ * [B*C][K][H][W] when only dL/dz is wanted) grows on first use (synchronising). Errors as
+ * p2s_backward; all four outputs NULL -> P2S_ERR_INVALID_ARG. */
 P2S_API p2s_status p2s_backward_color(p2s_handle* h, p2s_image image, const float* zernike_field,
                                       const float* tilt_field, const float* grad_out, float* grad_beta,
                                       float* grad_tilt, float* grad_image, float* grad_zernike,

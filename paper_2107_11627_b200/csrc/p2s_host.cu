@@ -1123,9 +1123,16 @@ p2s_status p2s_mlp_backward(p2s_handle* h, const float* zernike_field, const flo
 }  // extern "C"
 
 namespace {
-__global__ void __launch_bounds__(256) k_accumulate(float* __restrict__ dst, const float* __restrict__ src, size_t n) {
-  for (size_t i = (size_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (size_t)gridDim.x * blockDim.x)
-    dst[i] += src[i];
+// grad_tilt[b] = sum_c part[b C + c] over planes of n floats (the colour adjoint's dL/dt)
+__global__ void __launch_bounds__(256) k_sum_channels(float* __restrict__ dst, const float* __restrict__ part, int B,
+                                                      int C, size_t n) {
+  const size_t tot = (size_t)B * n;
+  for (size_t i = (size_t)blockIdx.x * blockDim.x + threadIdx.x; i < tot; i += (size_t)gridDim.x * blockDim.x) {
+    const size_t b = i / n, e = i - b * n;
+    float acc = 0.f;
+    for (int c = 0; c < C; ++c) acc += part[((size_t)b * C + c) * n + e];
+    dst[i] = acc;
+  }
 }
 }  // namespace
 
@@ -1140,11 +1147,17 @@ p2s_status p2s_backward_color(p2s_handle* h, p2s_image im, const float* zernike_
     return P2S_ERR_INVALID_ARG;
   if (grad_zernike && !h->mb_ok) return P2S_ERR_UNSUPPORTED;
   cudaStream_t st = (cudaStream_t)stream;
-  const int B = im.B, C = im.C, H = im.H, W = im.W, K = h->K, n_in = h->n_in;
-  const size_t HW = (size_t)H * W;
-  // workspace: one channel's dL/dt [2][H][W] (channels > 0 are accumulated) and, when dL/dz is
-  // wanted without dL/dbeta, one channel's dL/dbeta [K][H][W]
-  const size_t need = 2 * HW + (grad_zernike && !grad_beta ? (size_t)K * HW : 0);
+  const int B = im.B, C = im.C, H = im.H, W = im.W, K = h->K;
+  const size_t HW = (size_t)H * W, BC = (size_t)B * C;
+  // Channel c of frame b is a one-channel render with its own beta, and the
+  // colour layouts are exactly B*C one-channel frames: image [B][C][H][W] = [BC][1][H][W], fields
+  // [B][C][n_in][H][W] = [BC][n_in][H][W], dL/dbeta [BC][K][H][W]. So the adjoint is ONE
+  // p2s_backward over BC frames (the tilt replicated per channel), dL/dt summed over the channels
+  // afterwards, and one p2s_mlp_backward. Workspace: the replicated tilt and per-channel dL/dt
+  // [BC][2][H][W], and dL/dbeta [BC][K][H][W] when only dL/dz is wanted (grown on first use).
+  const size_t n_t = tilt_field ? BC * 2 * HW : 0, n_gt = grad_tilt ? BC * 2 * HW : 0;
+  const size_t n_gb = (grad_zernike && !grad_beta) ? BC * K * HW : 0;
+  const size_t need = n_t + n_gt + n_gb;
   if (need > h->col_ws_cap) {
     P2S_CUDA(cudaDeviceSynchronize());
     cudaFree(h->d_col_ws);
@@ -1153,33 +1166,27 @@ p2s_status p2s_backward_color(p2s_handle* h, p2s_image im, const float* zernike_
     P2S_CUDA(cudaMalloc(&h->d_col_ws, need * sizeof(float)));
     h->col_ws_cap = need;
   }
-  float* gt_tmp = h->d_col_ws;
-  float* gb_tmp = h->d_col_ws + 2 * HW;
-  // channel c of frame b is a one-channel render with its own beta: its
-  // adjoint is p2s_backward on that channel's plane and field, dL/dt summed over the channels
-  for (int b = 0; b < B; ++b)
-    for (int c = 0; c < C; ++c) {
-      const size_t bc = (size_t)b * C + c;
-      p2s_image ic{im.data + bc * HW, 1, 1, H, W};
-      const float* zc = zernike_field + bc * n_in * HW;
-      float* gb = grad_beta ? grad_beta + bc * K * HW : (grad_zernike ? gb_tmp : nullptr);
-      float* gt = grad_tilt ? (c == 0 ? grad_tilt + (size_t)b * 2 * HW : gt_tmp) : nullptr;
-      float* gi = grad_image ? grad_image + bc * HW : nullptr;
-      if (gb || gt || gi) {
-        s = p2s_backward(h, ic, zc, tilt_field ? tilt_field + (size_t)b * 2 * HW : nullptr, grad_out + bc * HW, gb, gt,
-                         gi, stream);
-        if (s != P2S_OK) return s;
-      }
-      if (grad_tilt && c > 0) {
-        k_accumulate<<<(int)std::min<size_t>((2 * HW + 255) / 256, (size_t)h->sm_count * 8), 256, 0, st>>>(
-            grad_tilt + (size_t)b * 2 * HW, gt_tmp, 2 * HW);
-        P2S_CUDA(cudaPeekAtLastError());
-      }
-      if (grad_zernike) {
-        s = p2s_mlp_backward(h, zc, gb, 1, H, W, grad_zernike + bc * n_in * HW, stream);
-        if (s != P2S_OK) return s;
-      }
-    }
+  float* t_rep = tilt_field ? h->d_col_ws : nullptr;
+  float* gt_rep = grad_tilt ? h->d_col_ws + n_t : nullptr;
+  float* gb = grad_beta ? grad_beta : (n_gb ? h->d_col_ws + n_t + n_gt : nullptr);
+  if (tilt_field)
+    for (size_t bc = 0; bc < BC; ++bc)
+      P2S_CUDA(cudaMemcpyAsync(t_rep + bc * 2 * HW, tilt_field + bc / C * 2 * HW, 2 * HW * sizeof(float),
+                               cudaMemcpyDeviceToDevice, st));
+  p2s_image one{im.data, (int)BC, 1, H, W};
+  if (gb || gt_rep || grad_image) {
+    s = p2s_backward(h, one, zernike_field, t_rep, grad_out, gb, gt_rep, grad_image, stream);
+    if (s != P2S_OK) return s;
+  }
+  if (grad_tilt) {
+    k_sum_channels<<<(int)std::min<size_t>(((size_t)B * 2 * HW + 255) / 256, (size_t)h->sm_count * 8), 256, 0, st>>>(
+        grad_tilt, gt_rep, B, C, 2 * HW);
+    P2S_CUDA(cudaPeekAtLastError());
+  }
+  if (grad_zernike) {
+    s = p2s_mlp_backward(h, zernike_field, gb, (int)BC, H, W, grad_zernike, stream);
+    if (s != P2S_OK) return s;
+  }
   return P2S_OK;
 }
 
