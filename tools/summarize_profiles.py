@@ -78,8 +78,8 @@ print(open(os.path.join(PROF, f"{tag}_launch_shares.txt")).read())
 print("\n".join(lines))
 print("dram bytes/launch", dram)
 
-# ---- the adjoint: launch list of one p2s_backward (all three gradients) and one
-#      --set full capture of k_adjoint_image (tools/ncu_adjoint_run.sh)
+# ---- the adjoint: launch list of one p2s_backward + p2s_mlp_backward (all four
+#      gradients) and one --set full capture of k_adjoint_image (tools/ncu_adjoint_run.sh)
 adj_csv = os.path.join(OUT, "adj_launches.csv")
 adj_rep = os.path.join(OUT, "prof_adjoint.ncu-rep")
 if os.path.exists(adj_csv) and os.path.exists(adj_rep):
@@ -89,7 +89,9 @@ if os.path.exists(adj_csv) and os.path.exists(adj_rep):
     ki, vi = hdr.index("Kernel Name"), hdr.index("Metric Value")
     seq = [(r[ki].split("(")[0], float(r[vi].replace(",", ""))) for r in rows[start + 1:]]
     # the last p2s_backward call of the run (warm-up calls precede it): its kernels in order
-    last = seq[-4:]  # dL/dJ scatter, fused pass (J, dL/dbeta, U), dL/dt, k_adjoint_image
+    roles = ["(dL/dJ scatter)", "(MLP + convolutions -> J, dL/dbeta, U = beta dL/dJ)", "(dL/dt)", "(dL/dI)",
+             "(dL/dz)"]
+    last = seq[-5:]  # dL/dJ scatter, fused pass (J, dL/dbeta, U), dL/dt, k_adjoint_image, k_mlp_backward
     raw = subprocess.run(["ncu", "-i", adj_rep, "--page", "raw", "--csv"], capture_output=True, text=True).stdout
     rr = list(csv.reader(raw.splitlines()))
     m = {a: (c, b) for a, b, c in zip(rr[0], rr[1], rr[2])}
@@ -98,10 +100,11 @@ if os.path.exists(adj_csv) and os.path.exists(adj_rep):
             "sm__pipe_tensor_cycles_active.avg.pct_of_peak_sustained_elapsed", "launch__grid_size",
             "launch__cluster_dim_x", "launch__registers_per_thread", "launch__shared_mem_per_block_dynamic"]
     with open(os.path.join(PROF, f"{tag}_ncu_adjoint.txt"), "w") as f:
-        f.write("adjoint (p2s_backward, all three gradients, cfg3): ncu --metrics gpu__time_duration.sum "
-                "--clock-control none (cold-cache, serialised); last call's launches:\n")
-        for name, ns in last:
-            f.write(f"  {ns / 1e3:9.1f} us  {name}\n")
+        f.write("adjoint (p2s_backward + p2s_mlp_backward, all four gradients, cfg3): ncu --metrics "
+                "gpu__time_duration.sum --clock-control none (cold-cache, serialised); last call's launches "
+                "(tools/adjoint_time.py 1 all4; full list in " + f"{tag}_adjoint_launches.csv):\n")
+        for (name, ns), role in zip(last, roles):
+            f.write(f"  {ns / 1e3:9.1f} us  {name.removeprefix('void '):24s} {role}\n")
         f.write("\nncu --set full --clock-control none -k regex:k_adjoint_image -c 1 (dL/dI of one cfg3 frame)\n\n")
         for k in want:
             if k in m:
