@@ -99,7 +99,7 @@ P2S_API p2s_status p2s_render_host(p2s_handle* h, const float* image_host, int B
                            const float* zernike_host, const float* tilt_host, float* out_host,
                            p2s_stream_t stream);
 
-/* Anchor-grid input (SURVEY.md §8(f) NEXT-1; PAPER.md:285-288, Sec. 3.4: "partition the image
+/* Anchor-grid input (SURVEY.md §8(f) NEXT-1; PAPER.md:293, Sec. 3.4: "partition the image
  * into a user-defined grid of anchor points ... interpolate the Zernike coefficients using
  * bilinear interpolation"). Instead of a dense [B][33][H][W] field the caller passes anchors
  * DEVICE [B][n_in][G][G] fp32 (G >= 1; G = 1 is a constant field); the fused kernel
@@ -194,7 +194,7 @@ P2S_API p2s_status p2s_backward_color(p2s_handle* h, p2s_image image, const floa
                                       float* grad_tilt, float* grad_image, float* grad_zernike,
                                       p2s_stream_t stream);
 
-/* The anchor-grid interpolation (PAPER.md:285-288 "anchor points ... interpolated"; registration
+/* The anchor-grid interpolation (PAPER.md:293 "anchor points ... interpolated"; registration
  * DESIGN.md reading N1 — pixel centre (t + 0.5), anchors at a n / (G - 1)) as a standalone op and
  * its adjoint, so the anchor pipeline is differentiable end to end:
  *   p2s_interp_anchors:  anchors (DEVICE [B][n_in][G][G] fp32) -> zernike_field (DEVICE
@@ -209,7 +209,7 @@ P2S_API p2s_status p2s_interp_anchors(const float* anchors, int B, int n_in, int
 P2S_API p2s_status p2s_anchors_backward(const float* grad_zernike, int B, int n_in, int G, int H, int W,
                                         float* grad_anchors, p2s_stream_t stream);
 
-/* ---- correlated anchor sampling (SURVEY.md §8(f) NEXT-3; PAPER.md:285-290, Sec. 3.4: anchor
+/* ---- correlated anchor sampling (SURVEY.md §8(f) NEXT-3; PAPER.md:293-295, Sec. 3.4: anchor
  * coefficient sets "drawn from the correlation matrix", which "can be pre-computed") ----
  * Stand-in covariance (reading N3; the paper's Takato-formula parameters are absent):
  * separable over anchor row a, anchor column b and mode j:

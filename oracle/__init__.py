@@ -166,7 +166,7 @@ def warp(J, tilt, threads=None) -> np.ndarray:
 
 def interp_anchors(anchors, H, W) -> np.ndarray:
     """Anchor grid [B][n_in][G][G] -> dense Zernike field [B][n_in][H][W] (fp64), bilinear per
-    mode with the corner / half-pixel registration of p2s_oracle.cpp (PAPER.md:285-288)."""
+    mode with the corner / half-pixel registration of p2s_oracle.cpp (PAPER.md:293)."""
     a = np.ascontiguousarray(anchors, np.float32)
     B, n_in, G, G2 = a.shape
     assert G == G2

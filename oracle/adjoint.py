@@ -152,22 +152,39 @@ def grad_image_at(beta, basis, gJ, yx):
     return out
 
 
+def grad_tilt(J, tilt, g, coord_dtype=np.float64, absolute=False):
+    """dL/dt [2][H][W] (fp64) of the warp out_c(p) = bilinear(J_c, p - t(p)) for a given blur J
+    [C][H][W] and upstream g [C][H][W]: the derivative of the bilinear weights inside the cell,
+    0 where the coordinate clamp is active. absolute=True returns the same sums over |terms|
+    (the scale of their rounding error)."""
+    J = np.asarray(J, np.float64)
+    C_, H, W = J.shape
+    g = np.asarray(g, np.float64)
+    ya, yb, xa, xb, fy, fx, in_y, in_x = _warp_coords(tilt, H, W, coord_dtype)
+    # d out / d sx = (1-fy)(J[ya][xb] - J[ya][xa]) + fy (J[yb][xb] - J[yb][xa]); sx = x - t_x
+    if absolute:
+        dsx = (1 - fy) * (abs(J[:, ya, xb]) + abs(J[:, ya, xa])) + fy * (abs(J[:, yb, xb]) + abs(J[:, yb, xa]))
+        dsy = (1 - fx) * (abs(J[:, yb, xa]) + abs(J[:, ya, xa])) + fx * (abs(J[:, yb, xb]) + abs(J[:, ya, xb]))
+        g = np.abs(g)
+    else:
+        dsx = (1 - fy) * (J[:, ya, xb] - J[:, ya, xa]) + fy * (J[:, yb, xb] - J[:, yb, xa])
+        dsy = (1 - fx) * (J[:, yb, xa] - J[:, ya, xa]) + fx * (J[:, yb, xb] - J[:, ya, xb])
+    sgn = 1.0 if absolute else -1.0
+    gt = np.zeros((2, H, W))
+    gt[0] = sgn * np.where(in_x, (g * dsx).sum(0), 0.0)
+    gt[1] = sgn * np.where(in_y, (g * dsy).sum(0), 0.0)
+    return gt
+
+
 def backward(image, beta, tilt, basis, g, coord_dtype=np.float64):
     """(dL/dJ [C][H][W], dL/dbeta [K][H][W], dL/dt [2][H][W], dL/dI [C][H][W]) for upstream
     g [C][H][W]."""
     _, J, Ck = forward_from_beta(image, beta, tilt, basis)
-    C_, H, W = J.shape
     g = g.astype(np.float64)
-    ya, yb, xa, xb, fy, fx, in_y, in_x = _warp_coords(tilt, H, W, coord_dtype)
     gJ = grad_J(tilt, g, coord_dtype)
     gbeta = np.einsum("chw,kchw->khw", gJ, Ck)
     gimage = grad_image(beta, basis, gJ)
-    # d out / d sx = (1-fy)(J[ya][xb] - J[ya][xa]) + fy (J[yb][xb] - J[yb][xa]); sx = x - t_x
-    dsx = (1 - fy) * (J[:, ya, xb] - J[:, ya, xa]) + fy * (J[:, yb, xb] - J[:, yb, xa])
-    dsy = (1 - fx) * (J[:, yb, xa] - J[:, ya, xa]) + fx * (J[:, yb, xb] - J[:, ya, xb])
-    gt = np.zeros((2, H, W))
-    gt[0] = -np.where(in_x, (g * dsx).sum(0), 0.0)
-    gt[1] = -np.where(in_y, (g * dsy).sum(0), 0.0)
+    gt = grad_tilt(J, tilt, g, coord_dtype)
     return gJ, gbeta, gt, gimage
 
 
@@ -244,7 +261,7 @@ def mlp_backward(zernike, gbeta, mlp, mask_precision="fp64", masks=None):
 
 def anchor_weights(n, G):
     """[n][G] fp64 matrix of the 1-D linear weights the anchor interpolation gives pixel index
-    t (0..n-1) from anchor index a (PAPER.md:285-288; DESIGN.md reading N1: pixel centre t + 0.5,
+    t (0..n-1) from anchor index a (PAPER.md:293; DESIGN.md reading N1: pixel centre t + 0.5,
     anchors at a n / (G - 1)): u = (t + 0.5)(G - 1)/n, i0 = min(floor(u), G - 2), weights
     1 - (u - i0) on i0 and u - i0 on i0 + 1; G = 1: all weight on the single anchor."""
     w = np.zeros((n, G))

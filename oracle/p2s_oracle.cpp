@@ -28,7 +28,7 @@
 //          + fy (1-fx) J[cY(y0+1)][cX(x0)] + fy fx J[cY(y0+1)][cX(x0+1)]
 //    No output clamp (A12).
 //
-//  anchor grid (SURVEY §8(f) NEXT-1; PAPER.md:285-288, Sec. 3.4 "partition the image into a
+//  anchor grid (SURVEY §8(f) NEXT-1; PAPER.md:293, Sec. 3.4 "partition the image into a
 //    user-defined grid of anchor points ... interpolate the Zernike coefficients using
 //    bilinear interpolation"): a G x G grid of coefficient vectors, registered to the image
 //    corners with half-pixel alignment (reading N1): pixel (y, x) has continuous

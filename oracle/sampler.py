@@ -1,10 +1,10 @@
 """Oracle for correlated anchor-grid sampling. TEST INFRASTRUCTURE ONLY
 (imported by tests/ and bench.py's reference leg; never by the product package).
 
-PAPER.md:285-290 (Sec. 3.4): "partition the image into a user-defined grid of anchor points ...
+PAPER.md:293-295 (Sec. 3.4): "partition the image into a user-defined grid of anchor points ...
 This grid corresponds to a correlation matrix ... which can be pre-computed ... sets of Zernike
 coefficients are drawn from the correlation matrix". The paper's correlation (Takato 1995 angle
-of arrival statistics, P:289) needs parameters the paper does not give, so the stand-in
+of arrival statistics, P:295) needs parameters the paper does not give, so the stand-in
 covariance is separable (reading N3):
 
     Cov[A_j(a, b), A_j'(a', b')] = R[j][j'] * s(a - a') * s(b - b'),

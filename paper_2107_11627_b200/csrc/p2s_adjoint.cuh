@@ -34,6 +34,7 @@
 #include <cstdint>
 
 #include "sm100.cuh"
+#include "p2s_kernels.cuh"  // u_scale_exp / exp2i (U's range scale)
 
 namespace p2s {
 
@@ -41,6 +42,7 @@ struct alignas(64) DiParams {
   CUtensorMap umap;        // U fp16 [B*C*K][H][Ws] viewed as (x%8, y, x/8, plane)
   CUtensorMap bmap;        // B table as uint8 [rows][256]
   float* gI;               // [B][C][H][W] fp32, zeroed by the caller; RED targets
+  const uint32_t* u_maxbits;  // [B*C] U's per-plane range scale (u_scale_exp, p2s_kernels.cuh)
   int BC, K, H, W, S, r;
   int R, nchunk, kg, ngroups, Nh, OW;
   int xs0, nbands, nstrips, npairs, ntiles;  // strip t reads U columns [xs0 + OW t, + 128)
@@ -184,6 +186,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kDiThreads, 1)
         if (m < p.OW && strip < p.nstrips && qy < p.H + p.r && qx >= -p.r && qx < p.W + p.r) {
           float acc = 0.f;
           for (int j = 0; j < p.S; ++j) acc += sP[j * 128 + m + j];
+          acc *= exp2i(-u_scale_exp(__ldg(p.u_maxbits + bc)));  // undo U's range scale (exact)
           const int y = qy < 0 ? 0 : (qy >= p.H ? p.H - 1 : qy);
           const int x = qx < 0 ? 0 : (qx >= p.W ? p.W - 1 : qx);
           atomicAdd(p.gI + (size_t)bc * HW + (size_t)y * p.W + x, acc);

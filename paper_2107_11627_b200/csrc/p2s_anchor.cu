@@ -1,5 +1,5 @@
 // p2s_anchor.cu — the anchor-grid interpolation as a standalone op and its adjoint (SURVEY
-// §8(f) NEXT-1 with NEXT-4: the paper's own input path, PAPER.md:285-288 "anchor points ...
+// §8(f) NEXT-1 with NEXT-4: the paper's own input path, PAPER.md:293 "anchor points ...
 // interpolated", made differentiable). Registration (reading N1): pixel
 // centre (t + 0.5), anchors at a n / (G - 1); per mode
 //     z[y][x] = sum_{a,b} wy[y][a] wx[x][b] A[a][b]        (bilinear, separable: z = Wy A Wx^T)

@@ -127,6 +127,8 @@ struct p2s_handle {
   uint8_t* d_dib = nullptr;
   __half* d_ut = nullptr;
   size_t ut_cap = 0;
+  uint32_t* d_umax = nullptr;  // [B*C] max |dL/dJ| bits per plane (U's fp16 range scale)
+  size_t umax_cap = 0;
   PFN_cuTensorMapEncodeTiled encode = nullptr;
   // dL/dz (k_mlp_backward): resident weight pack and its shared-memory plan (mb_ok = it fits)
   uint8_t* d_mlpb = nullptr;
@@ -744,7 +746,7 @@ p2s_status p2s_init(const p2s_basis* basis, const p2s_mlp* mlp, p2s_handle** out
     if ((e = cudaMalloc(&h->d_dib, tab.size() * sizeof(__half))) != cudaSuccess ||
         (e = cudaMemcpy(h->d_dib, tab.data(), tab.size() * sizeof(__half), cudaMemcpyHostToDevice)) != cudaSuccess)
       return fail(cuda_fail(e, "dI table"));
-    if ((e = cudaFuncSetAttribute(k_adjoint_image, cudaFuncAttributeMaxDynamicSharedMemorySize, h->di_smem)) !=
+    if ((e = cudaFuncSetAttribute(k_adjoint_image, cudaFuncAttributeMaxDynamicSharedMemorySize, kSmemLimit)) !=
         cudaSuccess)
       return fail(cuda_fail(e, "cudaFuncSetAttribute(k_adjoint_image)"));
     (void)wpad;
@@ -805,9 +807,9 @@ p2s_status p2s_init(const p2s_basis* basis, const p2s_mlp* mlp, p2s_handle** out
         if ((e = cudaMalloc(&h->d_mlpb, pk.size())) != cudaSuccess ||
             (e = cudaMemcpy(h->d_mlpb, pk.data(), pk.size(), cudaMemcpyHostToDevice)) != cudaSuccess)
           return fail(cuda_fail(e, "dz weight pack"));
-        if ((e = cudaFuncSetAttribute(k_mlp_backward<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem_res)) !=
+        if ((e = cudaFuncSetAttribute(k_mlp_backward<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, kSmemLimit)) !=
                 cudaSuccess ||
-            (e = cudaFuncSetAttribute(k_mlp_backward<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem_res)) !=
+            (e = cudaFuncSetAttribute(k_mlp_backward<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, kSmemLimit)) !=
                 cudaSuccess)
           return fail(cuda_fail(e, "cudaFuncSetAttribute(k_mlp_backward)"));
         h->mb_smem = smem_res;
@@ -855,9 +857,9 @@ p2s_status p2s_init(const p2s_basis* basis, const p2s_mlp* mlp, p2s_handle** out
         if ((e = cudaMalloc(&h->d_mlpb, st.size())) != cudaSuccess ||
             (e = cudaMemcpy(h->d_mlpb, st.data(), st.size(), cudaMemcpyHostToDevice)) != cudaSuccess)
           return fail(cuda_fail(e, "dz slab table"));
-        if ((e = cudaFuncSetAttribute(k_mlp_backward_s<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem)) !=
+        if ((e = cudaFuncSetAttribute(k_mlp_backward_s<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, kSmemLimit)) !=
                 cudaSuccess ||
-            (e = cudaFuncSetAttribute(k_mlp_backward_s<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem)) !=
+            (e = cudaFuncSetAttribute(k_mlp_backward_s<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, kSmemLimit)) !=
                 cudaSuccess)
           return fail(cuda_fail(e, "cudaFuncSetAttribute(k_mlp_backward_s)"));
         h->mb_stream = 1;
@@ -1018,6 +1020,22 @@ p2s_status p2s_backward(p2s_handle* h, p2s_image im, const float* zernike_field,
       P2S_CUDA(cudaMalloc(&h->d_ut, nu * sizeof(__half)));
       h->ut_cap = nu;
     }
+    const size_t nbc = (size_t)im.B * im.C;
+    if (nbc > h->umax_cap) {
+      P2S_CUDA(cudaDeviceSynchronize());
+      cudaFree(h->d_umax);
+      h->d_umax = nullptr;
+      h->umax_cap = 0;
+      P2S_CUDA(cudaMalloc(&h->d_umax, nbc * sizeof(uint32_t)));
+      h->umax_cap = nbc;
+    }
+    // per-(frame, channel) max |dL/dJ|: U = beta dL/dJ is stored in fp16 scaled by a power of two
+    // chosen from it, and k_adjoint_image scales its sums back (any finite dL/dout range)
+    P2S_CUDA(cudaMemsetAsync(h->d_umax, 0, nbc * sizeof(uint32_t), st));
+    const unsigned bpp = (unsigned)std::max<size_t>(1, std::min<size_t>((HW + 4095) / 4096,
+                                                                        (size_t)(4 * h->sm_count + nbc - 1) / nbc));
+    k_absmax_planes<<<dim3(bpp, (unsigned)nbc), 256, 0, st>>>(h->d_gJ, HW, h->d_umax);
+    P2S_CUDA(cudaPeekAtLastError());
   }
   {
     // one pass over the K convolutions: dL/dbeta_k = sum_c dL/dJ_c C_kc; with dL/dt or dL/dI the
@@ -1029,6 +1047,7 @@ p2s_status p2s_backward(p2s_handle* h, p2s_image im, const float* zernike_field,
     p.gJ = h->d_gJ;
     p.beta_out = grad_beta;
     p.u_out = grad_image ? h->d_ut : nullptr;
+    p.u_maxbits = grad_image ? h->d_umax : nullptr;
     p.J = grad_tilt ? h->d_J : nullptr;
     p.Ws = Ws;
     s = launch_fused(h, p, st);
@@ -1069,6 +1088,7 @@ p2s_status p2s_backward(p2s_handle* h, p2s_image im, const float* zernike_field,
       }
     }
     d.gI = grad_image;
+    d.u_maxbits = h->d_umax;
     d.BC = im.B * im.C; d.K = h->K; d.H = im.H; d.W = im.W; d.S = h->S; d.r = h->r;
     d.R = h->di_R; d.nchunk = h->di_nchunk; d.kg = h->di_kg; d.ngroups = h->di_ngroups; d.Nh = h->di_Nh;
     d.OW = h->di_OW;
@@ -1430,7 +1450,7 @@ void p2s_destroy(p2s_handle* h) {
   cudaFree(h->d_J);
   cudaFree(h->h_img); cudaFree(h->h_z); cudaFree(h->h_t); cudaFree(h->h_out); cudaFree(h->h_anc);
   cudaFree(h->d_gJ);
-  cudaFree(h->d_dib); cudaFree(h->d_ut);
+  cudaFree(h->d_dib); cudaFree(h->d_ut); cudaFree(h->d_umax);
   cudaFree(h->d_mlpb);
   cudaFree(h->d_col_ws);
   if (h->s_in) cudaStreamDestroy(h->s_in);

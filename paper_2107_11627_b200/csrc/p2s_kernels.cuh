@@ -108,7 +108,8 @@ struct FusedParams {
   float* J;              // [B][C][H][W] (mode 0)
   float* beta_out;       // [B][K][H][W] (mode 1: beta; mode 2: dL/dbeta)
   const float* gJ;  // [B][C][H][W] dL/dJ (the adjoint)
-  __half* u_out;    // kAdj = 2: U = beta dL/dJ, fp16 [B][C][K][H][Ws]
+  __half* u_out;    // kAdj = 2: U = beta dL/dJ, fp16 [B][C][K][H][Ws], scaled per (frame, channel)
+  const uint32_t* u_maxbits;  // [B][C] float bits of max |dL/dJ| over the plane (k_absmax_planes)
   int Ws;           // U row pitch (ceil8(W))
   int B, C, H, W, n_in;
   int nstrips, ntiles, mode;  // mode 0: MLP + conv -> J ; mode 1: MLP only -> beta ;
@@ -336,6 +337,38 @@ __device__ __forceinline__ void build_E_all(const FusedParams& p, uint8_t* Eb, c
 // One 16-column group of the conv epilogue (Eq. 5 reduction): NC real columns of beta (scratch)
 // and of each channel's accumulator, fp32x2 FMAs into jc2 (sum_k beta_k C_k) and bs2
 // (sum_k beta_k s_k for the centring term).
+// Range of U = beta dL/dJ in fp16: each (frame, channel) plane of U is scaled by 2^s,
+// s = 7 - floor(log2 max|dL/dJ|), so the plane's largest |dL/dJ| lands in [128, 256): a loss
+// reduced over a frame (dL/dout ~ 1e-7) no longer flushes to fp16 zero and dL/dout ~ 1e5 no
+// longer overflows (|U| < 65504 while |beta| < 256); k_adjoint_image multiplies its sums by 2^-s.
+// maxbits = the float bits of max|dL/dJ| (0: an all-zero plane, scale 1). Exact powers of two.
+P2S_DEV float exp2i(int e) { return __int_as_float((e + 127) << 23); }  // 2^e, e in [-126, 127]
+__device__ __forceinline__ int u_scale_exp(uint32_t maxbits) {
+  if (maxbits == 0u) return 0;
+  const int E = (int)((maxbits >> 23) & 0xffu) - 127;  // floor(log2 max) (subnormals: -127)
+  const int s = 7 - E;
+  return s < -126 ? -126 : (s > 126 ? 126 : s);  // 2^s and 2^-s both normal floats
+}
+
+// max |x| of each of n_planes planes of n floats, as float bits (|x| >= 0 orders like uint32);
+// out zeroed by the caller. grid (blocks per plane, n_planes).
+__global__ void __launch_bounds__(256) k_absmax_planes(const float* __restrict__ x, size_t n,
+                                                        uint32_t* __restrict__ out) {
+  const float* xp = x + (size_t)blockIdx.y * n;
+  uint32_t m = 0u;
+  for (size_t i = (size_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (size_t)gridDim.x * blockDim.x)
+    m = max(m, __float_as_uint(fabsf(__ldg(xp + i))));
+  m = __reduce_max_sync(0xffffffffu, m);
+  __shared__ uint32_t red[8];
+  if ((threadIdx.x & 31) == 0) red[threadIdx.x >> 5] = m;
+  __syncthreads();
+  if (threadIdx.x < 32) {
+    m = threadIdx.x < (blockDim.x >> 5) ? red[threadIdx.x] : 0u;
+    m = __reduce_max_sync(0xffffffffu, m);
+    if (threadIdx.x == 0 && m) atomicMax(out + blockIdx.y, m);
+  }
+}
+
 // adjoint epilogue (mode 2) for NC channels: dL/dbeta_k = sum_c dL/dJ_c C_kc over this warp
 // group's 16-column groups; C_kc = C'_kc + 0.5 s_k (C' convolves the centred image, s_k = tap sum)
 // (s_k is read through L1 from the global table: using the shared copy here made ptxas drop the
@@ -378,11 +411,13 @@ __device__ __forceinline__ void adj_epi(uint32_t tl, int Nk, int K, int wg, int 
 template <int NC>
 __device__ __forceinline__ void adj_u_epi(uint32_t tl, int scr_col, int Nk, int K, int wg, int GK, const float* gJ,
                                           size_t HW, const float* __restrict__ consts, bool b3_folded, float* dbeta,
-                                          __half* u, size_t plane, bool st, bool real, float (&jc)[3], float& bs) {
-  float gj[NC], gsum = 0.f;
+                                          __half* u, const uint32_t* umax, size_t plane, bool st, bool real,
+                                          float (&jc)[3], float& bs) {
+  float gj[NC], gu[NC], gsum = 0.f;
 #pragma unroll
   for (int c = 0; c < NC; ++c) {
     gj[c] = (st && real) ? __ldg(gJ + c * HW) : 0.f;
+    gu[c] = u ? gj[c] * exp2i(u_scale_exp(__ldg(umax + c))) : 0.f;  // U's per-plane range scale
     gsum += gj[c];
   }
   const float4* b34 = reinterpret_cast<const float4*>(consts);
@@ -418,7 +453,7 @@ __device__ __forceinline__ void adj_u_epi(uint32_t tl, int scr_col, int Nk, int 
         const int k = gi * 16 + i;
         if (k < K) {
 #pragma unroll
-          for (int c = 0; c < NC; ++c) u[((size_t)c * K + k) * plane] = __float2half_rn(bv[i] * gj[c]);
+          for (int c = 0; c < NC; ++c) u[((size_t)c * K + k) * plane] = __float2half_rn(bv[i] * gu[c]);
         }
       }
     }
@@ -474,13 +509,13 @@ __device__ __forceinline__ void conv_epi_group(uint32_t tl, int scr_col, int Nk,
   }
 }
 
-// A1 from an anchor grid (SURVEY NEXT-1; PAPER.md:285-288; registration DESIGN.md N1): pixel
+// A1 from an anchor grid (SURVEY NEXT-1; PAPER.md:293; registration DESIGN.md N1): pixel
 // centre (y+.5, x+.5), anchors at (i H/(G-1), j W/(G-1)); bilinear per mode in fp32, then fp16
 // like a dense field. Out of line: it keeps the builders' (rarely used) anchor path from
 // costing the shared register allocation of the whole kernel.
 __device__ __noinline__ void build_A1_anchors(const FusedParams& p, uint8_t* dst, int b, int y, int x0, int x,
                                               int tid, uint8_t* smem) {
-  // anchor grid (PAPER.md:285-288; registration DESIGN.md N1): pixel centre (y+.5, x+.5),
+  // anchor grid (PAPER.md:293; registration DESIGN.md N1): pixel centre (y+.5, x+.5),
   // anchors at (i H/(G-1), j W/(G-1)); bilinear per mode in fp32, then fp16 like the field
   const int G = p.G;
   int i0 = 0, j0 = 0;
@@ -1018,12 +1053,13 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads)
         __half* ub = p.u_out ? p.u_out + (size_t)b * C * p.K * p.H * p.Ws + (size_t)y * p.Ws + x : nullptr;
         const bool real = x < p.W;
         const size_t plane = (size_t)p.H * p.Ws;
+        const uint32_t* umb = p.u_maxbits + (size_t)b * C;
         float jc[3] = {0.f, 0.f, 0.f}, bs = 0.f;
         if (C == 3) adj_u_epi<3>(tl, p.scr_col, p.Nk, p.K, wg, GK, gJb, HW, p.consts, p.bias_folded != 0, ob, ub,
-                                 plane, st, real, jc, bs);
+                                 umb, plane, st, real, jc, bs);
         else if (C == 2) adj_u_epi<2>(tl, p.scr_col, p.Nk, p.K, wg, GK, gJb, HW, p.consts, p.bias_folded != 0, ob, ub,
-                                      plane, st, real, jc, bs);
-        else adj_u_epi<1>(tl, p.scr_col, p.Nk, p.K, wg, GK, gJb, HW, p.consts, p.bias_folded != 0, ob, ub, plane,
+                                      umb, plane, st, real, jc, bs);
+        else adj_u_epi<1>(tl, p.scr_col, p.Nk, p.K, wg, GK, gJb, HW, p.consts, p.bias_folded != 0, ob, ub, umb, plane,
                           st, real, jc, bs);
         tc_fence_before();
         __syncwarp();

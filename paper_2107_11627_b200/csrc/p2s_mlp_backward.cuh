@@ -90,7 +90,6 @@ P2S_DEV uint32_t relu2(float a, float b) {  // fp16x2 {lo = relu(a), hi = relu(b
   asm("cvt.rn.relu.f16x2.f32 %0, %1, %2;" : "=r"(r) : "f"(b), "f"(a));
   return r;
 }
-P2S_DEV float exp2i(int e) { return __int_as_float((e + 127) << 23); }  // 2^e, e in [-126, 127]
 
 // D[128 x N] = ACT * B^T with each 16-wide K-step of B taken from the next ring slot
 // (K-major slabs: lbo 128, sbo 256; W1^T slabs: lbo 16 K1, sbo 128); each slot is released to the

@@ -1,5 +1,5 @@
 // p2s_sampler.cu — correlated anchor-grid sampling, the step upstream of
-// p2s_render_anchors (NEXT-1). PAPER.md:285-290 (Sec. 3.4): anchor coefficients "drawn from the
+// p2s_render_anchors (NEXT-1). PAPER.md:293-295 (Sec. 3.4): anchor coefficients "drawn from the
 // correlation matrix", which "can be pre-computed". Stand-in covariance (reading N3;
 // the Takato-formula parameters are not in the paper): separable over anchor row, anchor column
 // and Zernike mode,

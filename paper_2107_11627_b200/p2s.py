@@ -135,6 +135,29 @@ def _dev_ptr(t, name, shape=None):
     return ctypes.c_void_p(t.data_ptr())
 
 
+def _on(stream):
+    """Allocations made for a call on `stream` come from that stream's caching-allocator pool, so
+    a tensor the queued kernels still use is not handed to another stream when it is freed."""
+    import contextlib
+    import torch
+    return torch.cuda.stream(stream) if stream is not None else contextlib.nullcontext()
+
+
+def _empty(stream, shape, device):
+    """torch.empty on `stream`'s allocator pool (see _on)."""
+    import torch
+    with _on(stream):
+        return torch.empty(shape, device=device, dtype=torch.float32)
+
+
+def _host_f32(a, name, shape):
+    if not isinstance(a, np.ndarray) or a.dtype != np.float32 or not a.flags.c_contiguous:
+        raise ValueError(f"{name} must be a C-contiguous float32 numpy array")
+    if tuple(a.shape) != tuple(shape):
+        raise ValueError(f"{name} has shape {tuple(a.shape)}, expected {tuple(shape)}")
+    return a.ctypes.data
+
+
 def _stream_handle(stream):
     import torch
     s = stream if stream is not None else torch.cuda.current_stream()
@@ -150,7 +173,7 @@ def interp_anchors(anchors, H: int, W: int, out=None, stream=None):
         raise ValueError("anchors must be [B, n_in, G, G]")
     ap = _dev_ptr(anchors, "anchors")
     if out is None:
-        out = torch.empty((B, n_in, H, W), device=anchors.device, dtype=torch.float32)
+        out = _empty(stream, (B, n_in, H, W), anchors.device)
     _check(lib.p2s_interp_anchors(ap, B, n_in, G, H, W, _dev_ptr(out, "zernike_field", (B, n_in, H, W)),
                                   _stream_handle(stream)), "p2s_interp_anchors")
     return out
@@ -163,7 +186,7 @@ def anchors_backward(grad_zernike, G: int, out=None, stream=None):
     B, n_in, H, W = grad_zernike.shape
     gp = _dev_ptr(grad_zernike, "grad_zernike")
     if out is None:
-        out = torch.empty((B, n_in, G, G), device=grad_zernike.device, dtype=torch.float32)
+        out = _empty(stream, (B, n_in, G, G), grad_zernike.device)
     _check(lib.p2s_anchors_backward(gp, B, n_in, G, H, W, _dev_ptr(out, "grad_anchors", (B, n_in, G, G)),
                                     _stream_handle(stream)), "p2s_anchors_backward")
     return out
@@ -199,7 +222,7 @@ class Renderer:
         zp = _dev_ptr(zernike, "zernike_field", (B, self.n_in, H, W))
         tp = _dev_ptr(tilt, "tilt_field", (B, 2, H, W)) if tilt is not None else ctypes.c_void_p()
         if out is None:
-            out = torch.empty_like(image)
+            out = _empty(stream, image.shape, image.device)
         op = _dev_ptr(out, "out", (B, C, H, W))
         _check(self._lib.p2s_render(self._h, im, zp, tp, op, _stream_handle(stream)), "p2s_render")
         return out
@@ -216,10 +239,10 @@ class Renderer:
         zp = _dev_ptr(zernike, "zernike_field", (B, self.n_in, H, W))
         tp = _dev_ptr(tilt, "tilt_field", (B, 2, H, W)) if tilt is not None else ctypes.c_void_p()
         gp = _dev_ptr(grad_out, "grad_out", (B, C, H, W))
-        gb = torch.empty((B, self.K, H, W), device=image.device, dtype=torch.float32) \
+        gb = _empty(stream, (B, self.K, H, W), image.device) \
             if (want_beta or want_zernike) else None
-        gt = torch.empty((B, 2, H, W), device=image.device, dtype=torch.float32) if want_tilt else None
-        gi = torch.empty((B, C, H, W), device=image.device, dtype=torch.float32) if want_image else None
+        gt = _empty(stream, (B, 2, H, W), image.device) if want_tilt else None
+        gi = _empty(stream, (B, C, H, W), image.device) if want_image else None
         _check(self._lib.p2s_backward(self._h, im, zp, tp, gp,
                                       _dev_ptr(gb, "grad_beta") if gb is not None else ctypes.c_void_p(),
                                       _dev_ptr(gt, "grad_tilt") if gt is not None else ctypes.c_void_p(),
@@ -251,11 +274,10 @@ class Renderer:
         zp = _dev_ptr(zernike_color, "zernike_field", (B, C, self.n_in, H, W))
         tp = _dev_ptr(tilt, "tilt_field", (B, 2, H, W)) if tilt is not None else ctypes.c_void_p()
         gp = _dev_ptr(grad_out, "grad_out", (B, C, H, W))
-        kw = dict(device=image.device, dtype=torch.float32)
-        gb = torch.empty((B, C, self.K, H, W), **kw) if want_beta else None
-        gt = torch.empty((B, 2, H, W), **kw) if want_tilt else None
-        gi = torch.empty((B, C, H, W), **kw) if want_image else None
-        gz = torch.empty((B, C, self.n_in, H, W), **kw) if want_zernike else None
+        gb = _empty(stream, (B, C, self.K, H, W), image.device) if want_beta else None
+        gt = _empty(stream, (B, 2, H, W), image.device) if want_tilt else None
+        gi = _empty(stream, (B, C, H, W), image.device) if want_image else None
+        gz = _empty(stream, (B, C, self.n_in, H, W), image.device) if want_zernike else None
         ptr = lambda t, n: _dev_ptr(t, n) if t is not None else ctypes.c_void_p()  # noqa: E731
         _check(self._lib.p2s_backward_color(self._h, im, zp, tp, gp, ptr(gb, "grad_beta"), ptr(gt, "grad_tilt"),
                                             ptr(gi, "grad_image"), ptr(gz, "grad_zernike"), _stream_handle(stream)),
@@ -269,7 +291,7 @@ class Renderer:
         zp = _dev_ptr(zernike, "zernike_field", (B, self.n_in, H, W))
         bp = _dev_ptr(grad_beta, "grad_beta", (B, self.K, H, W))
         if out is None:
-            out = torch.empty_like(zernike)
+            out = _empty(stream, zernike.shape, zernike.device)
         _check(self._lib.p2s_mlp_backward(self._h, zp, bp, B, H, W, _dev_ptr(out, "grad_zernike", (B, n_in, H, W)),
                                           _stream_handle(stream)), "p2s_mlp_backward")
         return out
@@ -278,7 +300,7 @@ class Renderer:
         import torch
         B, n_in, H, W = zernike.shape
         if out is None:
-            out = torch.empty((B, self.K, H, W), device=zernike.device, dtype=torch.float32)
+            out = _empty(stream, (B, self.K, H, W), zernike.device)
         _check(self._lib.p2s_debug_beta(self._h, _dev_ptr(zernike, "zernike_field", (B, self.n_in, H, W)),
                                         B, H, W, _dev_ptr(out, "beta_out", (B, self.K, H, W)),
                                         _stream_handle(stream)), "p2s_debug_beta")
@@ -288,7 +310,7 @@ class Renderer:
         import torch
         B, C, H, W = image.shape
         if out is None:
-            out = torch.empty_like(image)
+            out = _empty(stream, image.shape, image.device)
         im = _Image(_dev_ptr(image, "image").value, B, C, H, W)
         _check(self._lib.p2s_debug_blur(self._h, im, _dev_ptr(zernike, "zernike_field", (B, self.n_in, H, W)),
                                         _dev_ptr(out, "J_out", (B, C, H, W)), _stream_handle(stream)),
@@ -304,7 +326,7 @@ class Renderer:
         ap = _dev_ptr(anchors, "anchors", (B, self.n_in, G, G))
         tp = _dev_ptr(tilt, "tilt_field", (B, 2, H, W)) if tilt is not None else ctypes.c_void_p()
         if out is None:
-            out = torch.empty_like(image)
+            out = _empty(stream, image.shape, image.device)
         _check(self._lib.p2s_render_anchors(self._h, im, ap, G, tp, _dev_ptr(out, "out", (B, C, H, W)),
                                             _stream_handle(stream)), "p2s_render_anchors")
         return out
@@ -317,7 +339,7 @@ class Renderer:
         zp = _dev_ptr(zernike, "zernike_field", (B, C, self.n_in, H, W))
         tp = _dev_ptr(tilt, "tilt_field", (B, 2, H, W)) if tilt is not None else ctypes.c_void_p()
         if out is None:
-            out = torch.empty_like(image)
+            out = _empty(stream, image.shape, image.device)
         _check(self._lib.p2s_render_color(self._h, im, zp, tp, _dev_ptr(out, "out", (B, C, H, W)),
                                           _stream_handle(stream)), "p2s_render_color")
         return out
@@ -331,7 +353,7 @@ class Renderer:
         zp = _dev_ptr(zernike, "zernike_field", (F, self.n_in, H, W))
         tp = _dev_ptr(tilt, "tilt_field", (F, 2, H, W)) if tilt is not None else ctypes.c_void_p()
         if out is None:
-            out = torch.empty((F, C, H, W), device=image.device, dtype=torch.float32)
+            out = _empty(stream, (F, C, H, W), image.device)
         _check(self._lib.p2s_render_sequence(self._h, im, zp, tp, F, _dev_ptr(out, "out", (F, C, H, W)),
                                              _stream_handle(stream)), "p2s_render_sequence")
         return out
@@ -341,7 +363,7 @@ class Renderer:
         B, C, H, W = image.shape
         G = anchors.shape[-1]
         if out is None:
-            out = torch.empty_like(image)
+            out = _empty(stream, image.shape, image.device)
         im = _Image(_dev_ptr(image, "image").value, B, C, H, W)
         _check(self._lib.p2s_debug_blur_anchors(self._h, im, _dev_ptr(anchors, "anchors", (B, self.n_in, G, G)), G,
                                                 _dev_ptr(out, "J_out", (B, C, H, W)), _stream_handle(stream)),
@@ -353,14 +375,11 @@ class Renderer:
         """p2s_render_anchors_host: host buffers in and out (copies inside), synchronous."""
         B, C, H, W = image.shape
         G = anchors.shape[-1]
-        for a, n in ((image, "image"), (anchors, "anchors"), (out, "out")):
-            if a.dtype != np.float32 or not a.flags.c_contiguous:
-                raise ValueError(f"{n} must be C-contiguous float32")
-        if anchors.shape != (B, self.n_in, G, G):
-            raise ValueError(f"anchors must be [B, n_in, G, G], got {anchors.shape}")
-        tp = tilt.ctypes.data if tilt is not None else None
-        _check(self._lib.p2s_render_anchors_host(self._h, image.ctypes.data, B, C, H, W, anchors.ctypes.data, G,
-                                                 tp, out.ctypes.data, _stream_handle(stream)),
+        ip = _host_f32(image, "image", (B, C, H, W))
+        ap = _host_f32(anchors, "anchors", (B, self.n_in, G, G))
+        tp = _host_f32(tilt, "tilt", (B, 2, H, W)) if tilt is not None else None
+        op = _host_f32(out, "out", (B, C, H, W))
+        _check(self._lib.p2s_render_anchors_host(self._h, ip, B, C, H, W, ap, G, tp, op, _stream_handle(stream)),
                "p2s_render_anchors_host")
         return out
 
@@ -369,12 +388,12 @@ class Renderer:
                     out: np.ndarray, stream=None) -> np.ndarray:
         """p2s_render_host: host buffers in and out (copies inside), synchronous."""
         B, C, H, W = image.shape
-        for a, n in ((image, "image"), (zernike, "zernike"), (out, "out")):
-            if a.dtype != np.float32 or not a.flags.c_contiguous:
-                raise ValueError(f"{n} must be C-contiguous float32")
-        tp = tilt.ctypes.data if tilt is not None else None
-        _check(self._lib.p2s_render_host(self._h, image.ctypes.data, B, C, H, W, zernike.ctypes.data, tp,
-                                         out.ctypes.data, _stream_handle(stream)), "p2s_render_host")
+        ip = _host_f32(image, "image", (B, C, H, W))
+        zp = _host_f32(zernike, "zernike", (B, self.n_in, H, W))
+        tp = _host_f32(tilt, "tilt", (B, 2, H, W)) if tilt is not None else None
+        op = _host_f32(out, "out", (B, C, H, W))
+        _check(self._lib.p2s_render_host(self._h, ip, B, C, H, W, zp, tp, op, _stream_handle(stream)),
+               "p2s_render_host")
         return out
 
     def reserve(self, B, C, H, W):
@@ -434,7 +453,7 @@ class Sampler:
         """Anchors [F, n_in, G, G] (CUDA fp32) of frames frame0 .. frame0 + F - 1."""
         import torch
         if out is None:
-            out = torch.empty((F, self.n_in, self.G, self.G), device="cuda", dtype=torch.float32)
+            out = _empty(stream, (F, self.n_in, self.G, self.G), "cuda")
         _check(self._lib.p2s_sample_anchors(self._h, seed, frame0, F,
                                             _dev_ptr(out, "anchors", (F, self.n_in, self.G, self.G)),
                                             _stream_handle(stream)), "p2s_sample_anchors")

@@ -134,7 +134,7 @@ def make_zernike(spec: Spec, frame: int) -> np.ndarray:
 
 
 def make_anchors(spec: Spec, G: int, frames: Optional[range] = None) -> np.ndarray:
-    """Anchor-grid Zernike coefficients [B][n_in][G][G] fp32 (SURVEY NEXT-1, PAPER.md:285-288):
+    """Anchor-grid Zernike coefficients [B][n_in][G][G] fp32 (SURVEY NEXT-1, PAPER.md:293):
     per mode an N(0,1) G x G field, periodic-Gaussian smoothed over ~1 anchor spacing and scaled
     to the config's Zernike std — a stand-in for the spatially correlated draws of P:293 (the
     Takato covariance needs the missing supplementary parameters)."""

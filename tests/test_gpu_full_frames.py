@@ -1,0 +1,160 @@
+"""Whole-output GPU-vs-oracle parity at the configs the metric and BASELINE are quoted on.
+
+Every element of J (steps a1+a2, Eq. 5) and of the rendered frame (a1-a3,
+the blur then the tilt shift of PAPER.md:172) is compared with the CPU oracle
+(oracle/p2s_oracle.cpp, fp64, all host cores) on the same seeded inputs, in the launch
+configuration bench.py times:
+
+  * cfg3  one 512x512 RGB frame (K=100, 33x33, MLP 33-200-200-100)  -- the bench workload
+  * cfg4  the 16-frame batch, one p2s_render call; every frame is reported and the worst
+          frame is asserted on (SURVEY.md §8(c) precision plan: "report the worst frame")
+  * cfg5  one 1024x1024 RGB frame (K=100, 65x65, MLP 33-256-256-100) -- the tightest margin
+          the survey predicts (max-abs 1.46e-3 vs the 2e-3 bar)
+  * the cfg3 4-frame sequence (p2s_render_sequence) and the cfg3 colour frame
+    (p2s_render_color, per-channel beta), every element.
+
+Bar (BASELINE.json north_star): max |gpu - oracle| <= 2e-3 and relative L2 <= 1e-3, over the
+whole tensor AND for every frame on its own. Per-frame numbers are written as JSON to
+$P2S_PARITY_OUT (default gpurun_out/parity_full.json when gpurun_out/ exists) so they can be
+committed under profiles/.
+"""
+import json
+import os
+import time
+
+import numpy as np
+import pytest
+
+import oracle
+from paper_2107_11627_b200 import synth
+
+torch = pytest.importorskip("torch")
+pytestmark = pytest.mark.gpu
+
+MAX_ABS = 2e-3
+REL_L2 = 1e-3
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+_RESULTS = {}
+
+
+@pytest.fixture(scope="module")
+def p2s():
+    if not torch.cuda.is_available():
+        pytest.fail("GPU tests need a CUDA device (run them on the B200 box)")
+    from paper_2107_11627_b200 import p2s as mod
+    mod.load_library()
+    yield mod
+    path = os.environ.get("P2S_PARITY_OUT")
+    if not path and os.path.isdir(os.path.join(ROOT, "gpurun_out")):
+        path = os.path.join(ROOT, "gpurun_out", "parity_full.json")
+    if path and _RESULTS:
+        old = {}
+        if os.path.exists(path):
+            try:
+                with open(path) as f:
+                    old = json.load(f)
+            except Exception:
+                old = {}
+        old.update(_RESULTS)
+        with open(path, "w") as f:
+            json.dump(old, f, indent=1)
+
+
+def _dev(a):
+    return torch.from_numpy(np.ascontiguousarray(a)).cuda()
+
+
+def _per_frame(gpu, ref, what, frame_axis=0):
+    """Compares every element; returns (whole-tensor stats, per-frame stats) and asserts the bar
+    on the whole tensor and on every frame."""
+    gpu = np.asarray(gpu, np.float64)
+    ref = np.asarray(ref, np.float64)
+    assert gpu.shape == ref.shape, (gpu.shape, ref.shape)
+    assert np.all(np.isfinite(gpu)), f"{what}: non-finite GPU output"
+    frames = []
+    for f in range(gpu.shape[frame_axis]):
+        g = np.take(gpu, f, axis=frame_axis)
+        r = np.take(ref, f, axis=frame_axis)
+        d = g - r
+        frames.append({"max_abs": float(np.abs(d).max()),
+                       "rel_l2": float(np.linalg.norm(d) / max(np.linalg.norm(r), 1e-30)),
+                       "argmax": [int(v) for v in np.unravel_index(int(np.abs(d).argmax()), d.shape)],
+                       "ref_rms": float(np.sqrt(np.mean(r ** 2)))})
+    d = gpu - ref
+    whole = {"max_abs": float(np.abs(d).max()), "rel_l2": float(np.linalg.norm(d) / np.linalg.norm(ref)),
+             "elements": int(d.size), "frames": len(frames),
+             "worst_frame_max_abs": int(np.argmax([f["max_abs"] for f in frames])),
+             "worst_frame_rel_l2": int(np.argmax([f["rel_l2"] for f in frames])),
+             "bar": {"max_abs": MAX_ABS, "rel_l2": REL_L2}}
+    _RESULTS[what] = {"whole": whole, "per_frame": frames}
+    w = frames[whole["worst_frame_max_abs"]]
+    print(f"{what}: {d.size} elements, max_abs={whole['max_abs']:.3e} rel_l2={whole['rel_l2']:.3e}; "
+          f"worst frame {whole['worst_frame_max_abs']}: max_abs={w['max_abs']:.3e} "
+          f"rel_l2={frames[whole['worst_frame_rel_l2']]['rel_l2']:.3e}")
+    for i, fr in enumerate(frames):
+        assert fr["max_abs"] <= MAX_ABS, f"{what} frame {i}: max abs err {fr['max_abs']:.3e} at {fr['argmax']}"
+        assert fr["rel_l2"] <= REL_L2, f"{what} frame {i}: rel L2 {fr['rel_l2']:.3e}"
+    assert whole["max_abs"] <= MAX_ABS and whole["rel_l2"] <= REL_L2
+    return whole, frames
+
+
+def _full(p2s, cfg, frames=None):
+    spec = synth.CONFIGS[cfg]
+    inp = synth.make_inputs(spec, frames=frames)
+    r = p2s.Renderer(inp.basis, inp.mlp)
+    B, C, H, W = inp.image.shape
+    r.reserve(B, C, H, W)
+    img, z, t = _dev(inp.image), _dev(inp.zernike), _dev(inp.tilt)
+    out = r.render(img, z, t).cpu().numpy()
+    J = r.debug_blur(img, z).cpu().numpy()
+    r.close()
+    del img, z, t
+    torch.cuda.empty_cache()
+    t0 = time.perf_counter()
+    oref, Jref = oracle.render(inp.image, inp.zernike, inp.tilt, inp.basis, inp.mlp, want_blur=True)
+    print(f"oracle cfg{cfg}: {time.perf_counter() - t0:.1f} s on {oracle.default_threads()} threads")
+    _per_frame(J, Jref, f"blur[cfg{cfg} full]")
+    _per_frame(out, oref, f"render[cfg{cfg} full]")
+
+
+def test_cfg3_full_frame(p2s):
+    """The bench workload: every element of J and out of one 512x512 RGB frame."""
+    _full(p2s, 3)
+
+
+def test_cfg4_all_16_frames(p2s):
+    """cfg4: the 16-frame batch in ONE p2s_render call (the persistent (frame, tile) schedule),
+    every element of all 16 frames; the worst frame is reported and asserted."""
+    _full(p2s, 4)
+
+
+def test_cfg5_full_frame(p2s):
+    """cfg5: 1024x1024 RGB, K=100, 65x65 taps, MLP 33-256-256-100, every element."""
+    _full(p2s, 5)
+
+
+def test_sequence_cfg3_full(p2s):
+    """p2s_render_sequence on a 4-frame cfg3 sequence (one image, per-frame Zernike/tilt;
+    PAPER.md:474) vs the oracle rendering each frame of the replicated image, every element."""
+    spec, F = synth.CONFIGS[3], 4
+    inp = synth.make_inputs(spec, frames=range(F))
+    img1 = np.ascontiguousarray(inp.image[:1])
+    r = p2s.Renderer(inp.basis, inp.mlp)
+    seq = r.render_sequence(_dev(img1), _dev(inp.zernike), _dev(inp.tilt)).cpu().numpy()
+    r.close()
+    rep = np.ascontiguousarray(np.repeat(img1, F, axis=0))
+    ref, _ = oracle.render(rep, inp.zernike, inp.tilt, inp.basis, inp.mlp)
+    _per_frame(seq, ref, "render_sequence[cfg3 F=4 full]")
+
+
+def test_color_cfg3_full(p2s):
+    """p2s_render_color on a cfg3 frame with per-channel Zernike fields, every
+    element of every channel (each channel reported as a 'frame')."""
+    spec = synth.CONFIGS[3]
+    inp = synth.make_inputs(spec, frames=range(1))
+    zc = synth.make_zernike_color(spec, frames=range(1))
+    r = p2s.Renderer(inp.basis, inp.mlp)
+    out = r.render_color(_dev(inp.image), _dev(zc), _dev(inp.tilt)).cpu().numpy()
+    r.close()
+    ref, _ = oracle.render_color(inp.image, zc, inp.tilt, inp.basis, inp.mlp)
+    _per_frame(out[0], ref[0], "render_color[cfg3 full, per channel]")

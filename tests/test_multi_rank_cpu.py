@@ -56,3 +56,21 @@ def test_single_process_defaults():
     assert list(pdist.rank_frames(0, 1)) == [0]
     with pytest.raises(ValueError):
         pdist.throughput(1, 1, 1, 0.0)
+
+
+def test_bench_gpus_flag_launches_ranks_dry_run():
+    """`python bench.py --gpus 2 --dry-run` (no torchrun around it) re-launches itself as two ranks
+    (torch.distributed.run, gloo, 127.0.0.1) and rank 0 prints n_gpus = 2 with disjoint frame blocks."""
+    import json
+    import subprocess
+    import sys
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    env = {k: v for k, v in os.environ.items() if k not in ("WORLD_SIZE", "RANK", "LOCAL_RANK")}
+    r = subprocess.run([sys.executable, os.path.join(root, "bench.py"), "--gpus", "2", "--dry-run", "--steps", "3"],
+                       capture_output=True, text=True, timeout=300, env=env)
+    assert r.returncode == 0, r.stderr[-2000:]
+    lines = [ln for ln in r.stdout.splitlines() if ln.startswith("{")]
+    assert len(lines) == 1, r.stdout  # rank 0 only
+    d = json.loads(lines[0])
+    assert d["n_gpus"] == 2 and d["dry_run"] and d["rank_frames"] == [[0], [1]]
+    assert d["max_over_ranks_probe"] == 2.0 and d["scaling"] == "weak"

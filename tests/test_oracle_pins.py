@@ -291,7 +291,7 @@ def test_thread_count_does_not_change_results():
     np.testing.assert_array_equal(a, b)
 
 
-# ---- anchor grid -> dense Zernike field (SURVEY §8(f) NEXT-1; PAPER.md:285-288, Sec. 3.4;
+# ---- anchor grid -> dense Zernike field (SURVEY §8(f) NEXT-1; PAPER.md:293, Sec. 3.4;
 #      registration: DESIGN.md reading N1 — pixel centres at (y + 0.5, x + 0.5), anchors spanning
 #      the image corner to corner at (i H/(G-1), j W/(G-1)))
 
@@ -347,7 +347,7 @@ def test_anchor_interp_exact_at_anchor_pixels():
     assert f[0, 0, 1, 1] == A[0, 0, 1, 1]
 
 
-# ---- correlated anchor sampling (SURVEY §8(f) NEXT-3; PAPER.md:285-290; stand-in covariance:
+# ---- correlated anchor sampling (SURVEY §8(f) NEXT-3; PAPER.md:293-295; stand-in covariance:
 #      DESIGN.md reading N3) — oracle/sampler.py
 
 def test_philox_known_answers():
