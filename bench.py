@@ -508,6 +508,33 @@ def main():
                 fs()
             sa_ms = tm.calls(fs, 50)
             smp.close()
+            # NEXT-3 with a dense pre-computed 4096 x 4096 correlation (G = 64, the
+            # non-separable exponential stand-in): 50 frames per call on the tensor cores, and the
+            # whole simulator per frame (draw + render_anchors at G = 64)
+            GD, FD = 64, 50
+            dsmp = p2s.Sampler(GD, spec.n_in, spatial_cov=synth.anchor_cov_exp(GD, 6.0))
+            danc = torch.empty((FD, spec.n_in, GD, GD), device=dev, dtype=torch.float32)
+            fd = lambda: dsmp.sample(7 + rank, 0, FD, out=danc)  # noqa: E731
+            for _ in range(2):
+                fd()
+            d_ms = tm.calls(fd, 10)
+            d1 = danc[:1]
+            fdr = lambda: (dsmp.sample(7 + rank, 0, 1, out=d1), r.render_anchors(img, d1, t, out=out))  # noqa: E731
+            for _ in range(2):
+                fdr()
+            dr_ms = tm.calls(fdr, 20)
+            GG2 = GD * GD
+            dflops = 2.0 * GG2 * (GG2 + 1) / 2 * FD * spec.n_in  # L's lower triangle x (frame, mode) columns
+            dense_sampler = {
+                "G": GD, "frames_per_call": FD, "ms_per_call": float(np.median(d_ms)),
+                "frames_per_s": pdist.throughput(FD, world, 10, pdist.max_over_ranks(float(d_ms.sum()), dist, dev)),
+                "gemm_tflops_algorithmic": dflops / (np.median(d_ms) / 1e3) / 1e12,
+                "frac_of_peak": dflops / (np.median(d_ms) / 1e3) / 1e12 / peak,
+                "note": "k_draw_y (Philox + mode mixing, fp64) + k_sample_dense (tcgen05, 3 fp16 products per "
+                        "K-step: executed MMA = 3x the algorithmic triangle FLOPs)",
+                "sample_and_render_fps": pdist.throughput(1, world, 20, pdist.max_over_ranks(float(dr_ms.sum()), dist, dev))}
+            dsmp.close()
+            del danc, d1
             ae = None
             if e2e_steps:
                 h_anc = torch.from_numpy(anc_h).pin_memory().numpy()
@@ -524,7 +551,7 @@ def main():
                            "sampled_value": pdist.throughput(B, world, 50, pdist.max_over_ranks(float(sa_ms.sum()), dist, dev)),
                            "sampled_note": "NEXT-3: p2s_sample_anchors (separable stand-in covariance, corr_len 2) + "
                                            "p2s_render_anchors per frame",
-                           "steps": 50, "api": "p2s_render_anchors", "e2e": ae,
+                           "steps": 50, "api": "p2s_render_anchors", "e2e": ae, "dense_sampler": dense_sampler,
                            "note": "Zernike coefficients on a 16x16 anchor grid (PAPER.md:292-295), bilinear per "
                                    "mode inside the fused kernel; same frame otherwise"}
             del anc

@@ -224,6 +224,23 @@ P2S_API p2s_status p2s_anchors_backward(const float* grad_zernike, int B, int n_
 typedef struct p2s_sampler p2s_sampler;
 P2S_API p2s_status p2s_sampler_init(int G, int n_in, double corr_len, const double* mode_cov,
                                     p2s_sampler** out_sampler);
+/* Dense pre-computed correlation ("This grid corresponds to a correlation matrix of
+ * size 64^2 x 64^2 = 4096 x 4096 which can be pre-computed ... 4096 sets of Zernike coefficients
+ * are drawn from the correlation matrix"; the Takato-formula entries of P:295 need parameters the
+ * paper does not give, reading N6):
+ *   Cov[A_j(p), A_j'(p')] = R[j][j'] C[p][p'],  p = a G + b (anchor row a, column b),
+ * spatial_cov = C: HOST fp64 [G^2][G^2] row-major, symmetric positive definite, factored once here
+ * (fp64 Cholesky on the host, threaded; ~1 s at G = 64); or, with is_factor != 0, its lower
+ * Cholesky factor L (the upper triangle is ignored, the diagonal must be > 0). mode_cov as
+ * p2s_sampler_init. The sampler owns device copies of L (fp16 hi/lo tiles, ~33 MB at G = 64) and a
+ * workspace; p2s_sample_anchors then draws A_f = (L_R (x) L) z_f with the same Philox normals z_f
+ * as the separable sampler (so C = s (x) s reproduces it up to rounding), the product L Y as a
+ * tcgen05 GEMM over L's lower triangle with fp16 hi/lo operand splits and fp32 accumulation:
+ * |error| <= ~2^-19 x sum_q |L[p][q]| |Y[q]| per anchor. Errors: NULL
+ * spatial_cov / out, G outside [1, 64], n_in outside [1, 64], a non-symmetric or non-SPD matrix
+ * -> P2S_ERR_INVALID_ARG; not an sm_100 device -> P2S_ERR_UNSUPPORTED; allocation -> P2S_ERR_OOM. */
+P2S_API p2s_status p2s_sampler_init_dense(int G, int n_in, const double* spatial_cov, int is_factor,
+                                          const double* mode_cov, p2s_sampler** out_sampler);
 P2S_API p2s_status p2s_sample_anchors(p2s_sampler* s, unsigned long long seed, int frame0, int F,
                                       float* anchors, p2s_stream_t stream);
 P2S_API void p2s_sampler_destroy(p2s_sampler* s);

@@ -80,3 +80,34 @@ def sample(seed: int, frame0: int, F: int, G: int, n_in: int, corr_len: float, m
         t = np.einsum("bd,adj->abj", Ls, t)           # columns: sum_d L_s[b][d] t[a][d][j]
         out[f] = t.transpose(2, 0, 1)
     return out
+
+
+def sample_dense(seed: int, frame0: int, F: int, G: int, n_in: int, spatial_cov, mode_cov=None,
+                 is_factor: bool = False) -> np.ndarray:
+    """Anchors [F][n_in][G][G] (fp64) from a DENSE pre-computed spatial correlation over the G^2
+    anchors ("a correlation matrix of size 64^2 x 64^2 = 4096 x 4096 which can be
+    pre-computed ... 4096 sets of Zernike coefficients are drawn from the correlation matrix"):
+
+        Cov[A_j(p), A_j'(p')] = R[j][j'] C[p][p'],  p = a G + b (anchor row a, column b)
+        A_f = (L_R (x) L) z_f,  L = cholesky(C) [G^2][G^2],  L_R = cholesky(R)
+
+    with the same normals z_f as `sample` (so C = s (x) s reproduces it). spatial_cov [G^2][G^2];
+    is_factor=True: spatial_cov already is the lower Cholesky factor L (upper part ignored)."""
+    R = default_mode_cov(n_in) if mode_cov is None else np.asarray(mode_cov, np.float64)
+    C = np.asarray(spatial_cov, np.float64)
+    L = np.tril(C) if is_factor else np.linalg.cholesky(C)
+    LR = np.linalg.cholesky(R)
+    out = np.empty((F, n_in, G, G))
+    for f in range(F):
+        z = normals(seed, frame0 + f, G, n_in)   # [p][k]
+        y = z @ LR.T                              # modes:  y[p][j] = sum_k L_R[j][k] z[p][k]
+        a = L @ y                                 # space:  a[p][j] = sum_q L[p][q] y[q][j]
+        out[f] = a.T.reshape(n_in, G, G)
+    return out
+
+
+def mixed_normals(seed: int, frame: int, G: int, n_in: int, mode_cov=None) -> np.ndarray:
+    """y [G^2][n_in] = z L_R^T of one frame (the right-hand side sample_dense multiplies by L)."""
+    R = default_mode_cov(n_in) if mode_cov is None else np.asarray(mode_cov, np.float64)
+    return normals(seed, frame, G, n_in) @ np.linalg.cholesky(R).T
+

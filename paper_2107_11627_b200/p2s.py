@@ -28,7 +28,7 @@ EXPORTED = ("p2s_init", "p2s_render", "p2s_render_host", "p2s_reserve", "p2s_set
             "p2s_render_anchors", "p2s_render_anchors_host", "p2s_debug_blur_anchors",
             "p2s_render_sequence", "p2s_sampler_init", "p2s_sample_anchors", "p2s_sampler_destroy",
             "p2s_backward", "p2s_render_color", "p2s_mlp_backward", "p2s_interp_anchors",
-            "p2s_anchors_backward", "p2s_backward_color")
+            "p2s_anchors_backward", "p2s_backward_color", "p2s_sampler_init_dense")
 
 
 class P2SError(RuntimeError):
@@ -98,6 +98,7 @@ def load_library(path: str = LIB_PATH) -> ctypes.CDLL:
     lib.p2s_render_sequence.argtypes = [v, _Image, v, v, i, v, v]
     lib.p2s_sampler_init.argtypes = [i, i, ctypes.c_double, v, ctypes.POINTER(v)]
     lib.p2s_sample_anchors.argtypes = [v, ctypes.c_ulonglong, i, i, v, v]
+    lib.p2s_sampler_init_dense.argtypes = [i, i, v, i, v, ctypes.POINTER(v)]
     lib.p2s_sampler_destroy.argtypes = [v]
     lib.p2s_backward.argtypes = [v, _Image, v, v, v, v, v, v, v]
     lib.p2s_render_color.argtypes = [v, _Image, v, v, v, v]
@@ -111,7 +112,7 @@ def load_library(path: str = LIB_PATH) -> ctypes.CDLL:
                  "p2s_render_anchors", "p2s_render_anchors_host", "p2s_debug_blur_anchors",
                  "p2s_render_sequence", "p2s_sampler_init", "p2s_sample_anchors", "p2s_backward",
                  "p2s_render_color", "p2s_mlp_backward", "p2s_interp_anchors", "p2s_anchors_backward",
-                 "p2s_backward_color"):
+                 "p2s_backward_color", "p2s_sampler_init_dense"):
         getattr(lib, name).restype = st
     _lib = lib
     return lib
@@ -434,7 +435,11 @@ class Sampler:
     """Correlated anchor-grid sampler (include/p2s.h p2s_sampler_*): stand-in
     separable covariance R (x) s (x) s (reading N3), Philox4x32-10 + Box-Muller normals."""
 
-    def __init__(self, G: int, n_in: int, corr_len: float, mode_cov: Optional[np.ndarray] = None):
+    def __init__(self, G: int, n_in: int, corr_len: float = 0.0, mode_cov: Optional[np.ndarray] = None,
+                 spatial_cov: Optional[np.ndarray] = None, is_factor: bool = False):
+        """Separable stand-in (corr_len; p2s_sampler_init), or -- with spatial_cov [G^2, G^2] fp64 --
+        a dense pre-computed spatial correlation (or its lower Cholesky factor when is_factor;
+        p2s_sampler_init_dense, the tensor-core path)."""
         lib = load_library()
         self._lib = lib
         self.G, self.n_in = G, n_in
@@ -446,7 +451,14 @@ class Sampler:
                 raise ValueError("mode_cov must be [n_in, n_in]")
             mp = ctypes.c_void_p(self._keep.ctypes.data)
         h = ctypes.c_void_p()
-        _check(lib.p2s_sampler_init(G, n_in, float(corr_len), mp, ctypes.byref(h)), "p2s_sampler_init")
+        if spatial_cov is not None:
+            c = np.ascontiguousarray(spatial_cov, np.float64)
+            if c.shape != (G * G, G * G):
+                raise ValueError("spatial_cov must be [G*G, G*G]")
+            _check(lib.p2s_sampler_init_dense(G, n_in, ctypes.c_void_p(c.ctypes.data), int(bool(is_factor)), mp,
+                                              ctypes.byref(h)), "p2s_sampler_init_dense")
+        else:
+            _check(lib.p2s_sampler_init(G, n_in, float(corr_len), mp, ctypes.byref(h)), "p2s_sampler_init")
         self._h = h
 
     def sample(self, seed: int, frame0: int, F: int, out=None, stream=None):

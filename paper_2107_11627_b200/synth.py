@@ -143,6 +143,28 @@ def make_anchors(spec: Spec, G: int, frames: Optional[range] = None) -> np.ndarr
                      for f in frames])
 
 
+def anchor_cov_exp(G: int, corr_len: float, jitter: float = 1e-6) -> np.ndarray:
+    """A dense, NON-separable spatial correlation over the G x G anchor grid (fp64 [G^2][G^2],
+    p = a G + b): exp(-|p - p'| / corr_len) of the Euclidean anchor distance (in anchor
+    spacings) + jitter I. Stand-in for the pre-computed Takato/Chimitt correlation matrix of
+    PAPER.md:293-295, whose turbulence parameters the paper does not give (reading N6).
+    The exponential (Matern nu = 1/2) kernel is positive definite in 2-D; it is not a Kronecker
+    product, so only the dense sampler can draw from it."""
+    a, b = np.divmod(np.arange(G * G), G)
+    d = np.hypot(a[:, None] - a[None, :], b[:, None] - b[None, :]).astype(np.float64)
+    c = np.exp(-d / corr_len) if corr_len > 0 else (d == 0).astype(np.float64)
+    return c + jitter * np.eye(G * G)
+
+
+def anchor_cov_separable(G: int, corr_len: float) -> np.ndarray:
+    """The separable stand-in s (x) s of p2s_sampler_init written as a dense [G^2][G^2] matrix
+    (s(d) = exp(-d^2 / (2 l^2)) + 1e-6 [d = 0], reading N3)."""
+    d = np.arange(G)[:, None] - np.arange(G)[None, :]
+    s = np.exp(-d.astype(np.float64) ** 2 / (2.0 * corr_len ** 2)) if corr_len > 0 else (d == 0).astype(np.float64)
+    s = s + 1e-6 * np.eye(G)
+    return np.kron(s, s)
+
+
 WAVELENGTHS_NM = (570.0, 540.0, 450.0)  # R, G, B as in PAPER.md:318 ("450nm, 540nm, and 570nm")
 
 

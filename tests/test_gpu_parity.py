@@ -452,6 +452,83 @@ def test_sampler_matches_oracle(p2s, name):
     np.testing.assert_array_equal(one[0], got[1])
 
 
+DENSE_CASES = {  # G, n_in, covariance, corr_len, mode-cov seed, frames
+    "G64_exp_F3": (64, 33, "exp", 3.0, 1, 3),
+    "G64_exp_F70": (64, 33, "exp", 6.0, None, 70),   # two GEMM launches (2048-column chunks), ragged N
+    "G16_exp": (16, 33, "exp", 2.0, 2, 5),
+    "G5_n3": (5, 3, "exp", 1.0, 3, 4),
+    "G1": (1, 7, "exp", 1.0, None, 2),
+    "G12_sep": (12, 33, "sep", 2.0, None, 3),
+}
+
+
+def _dense_cov(kind, G, L):
+    return synth.anchor_cov_exp(G, L) if kind == "exp" else synth.anchor_cov_separable(G, L)
+
+
+@pytest.mark.parametrize("name", list(DENSE_CASES))
+def test_dense_sampler_matches_oracle(p2s, name):
+    """NEXT-3 with the paper's structure (a dense pre-computed G^2 x G^2 correlation):
+    A = L Y on the tensor cores (fp16 hi/lo splits, fp32 accumulation) vs oracle.sampler.sample_dense
+    (numpy fp64 Cholesky and L @ y). Bar per anchor: |err| <= 2^-18 sum_q |L[p][q]| |Y[q]| (three
+    fp16 products drop the lo x lo term, ~2^-22 relative, and fp32 accumulation adds ~2^-24 per
+    term; 4x margin) and rel-L2 <= 1e-6."""
+    from oracle import sampler as osamp
+    G, n_in, kind, L, spd, F = DENSE_CASES[name]
+    R = _spd(n_in, spd) if spd else None
+    C = _dense_cov(kind, G, L)
+    smp = p2s.Sampler(G, n_in, mode_cov=R, spatial_cov=C)
+    seed, f0 = 0x0BAD_CAFE_1234, 11
+    got = smp.sample(seed, f0, F).cpu().numpy().astype(np.float64)
+    ref = osamp.sample_dense(seed, f0, F, G, n_in, C, R)
+    Lf = np.abs(np.linalg.cholesky(C))
+    worst, num, den = 0.0, 0.0, 0.0
+    for f in range(F):
+        y = np.abs(osamp.mixed_normals(seed, f0 + f, G, n_in, R))            # [G^2][n_in]
+        bar = 2.0 ** -18 * (Lf @ y).T.reshape(n_in, G, G) + 1e-30
+        d = np.abs(got[f] - ref[f])
+        assert np.all(d <= bar), f"dense sampler[{name}] frame {f}: {(d / bar).max():.2f} x bar"
+        worst = max(worst, float((d / bar).max()))
+        num += float((d ** 2).sum())
+        den += float((ref[f] ** 2).sum())
+    rl2 = np.sqrt(num / den)
+    print(f"dense sampler[{name}]: max_abs={np.abs(got - ref).max():.3e} rel_l2={rl2:.3e} bar use {worst:.3f}")
+    assert rl2 <= 1e-6
+    # counter-based: a frame drawn alone equals the same frame of the batch
+    one = smp.sample(seed, f0 + F - 1, 1).cpu().numpy()
+    np.testing.assert_array_equal(one[0], got[F - 1].astype(np.float32))
+    smp.close()
+
+
+def test_dense_sampler_is_the_separable_one_for_a_kronecker_covariance(p2s):
+    """With C = s (x) s written out densely, the tensor-core sampler draws the separable sampler's
+    anchors (same Philox normals; equal up to the GEMM's rounding), and passing the Cholesky factor
+    directly (is_factor) gives the same draw as passing C."""
+    G, n_in, L = 16, 33, 2.0
+    sep = p2s.Sampler(G, n_in, L).sample(77, 0, 4).cpu().numpy()
+    C = synth.anchor_cov_separable(G, L)
+    den = p2s.Sampler(G, n_in, spatial_cov=C).sample(77, 0, 4).cpu().numpy()
+    fac = p2s.Sampler(G, n_in, spatial_cov=np.linalg.cholesky(C), is_factor=True).sample(77, 0, 4).cpu().numpy()
+    err = np.abs(den - sep).max()
+    print(f"dense vs separable (G={G}): max_abs={err:.3e} (rms {np.sqrt((sep ** 2).mean()):.3f})")
+    assert err <= 2e-5 * np.abs(sep).max()
+    assert np.abs(fac - den).max() <= 2e-6 * np.abs(sep).max()
+
+
+def test_dense_sampler_invalid_args(p2s):
+    C = synth.anchor_cov_exp(4, 1.0)
+    notsym = C.copy()
+    notsym[0, 1] += 0.1
+    notpd = C - 2.0 * np.eye(16)
+    for G, cov, fac in ((4, notsym, False), (4, notpd, False), (0, np.zeros((0, 0)), False),
+                        (4, -np.eye(16), True)):
+        with pytest.raises(p2s.P2SError) as e:
+            p2s.Sampler(G, 3, spatial_cov=cov, is_factor=fac)
+        assert e.value.status == p2s.P2S_ERR_INVALID_ARG
+    with pytest.raises(ValueError):
+        p2s.Sampler(4, 3, spatial_cov=np.eye(15))
+
+
 def test_sampler_invalid_args(p2s):
     bad = np.array([[1.0, 2.0], [2.0, 1.0]])  # symmetric, not positive definite
     for args in ((16, 2, 1.0, bad), (0, 33, 1.0, None), (65, 33, 1.0, None), (8, 33, -1.0, None)):
@@ -506,8 +583,9 @@ def _adj_ref(inp, g, with_tilt):
 def _check_dt(r, inp, g, gt, rt, with_tilt, name, J_ref=None):
     """dL/dt bars (tight, with a rel-L2). (1) The kernel's warp-derivative
     arithmetic: the GPU's dL/dt against oracle.adjoint.grad_tilt applied to the GPU's own blur J
-    (p2s_debug_blur) -- only fp32 rounding separates them: |err| <= 1e-5 x the sum of the terms'
-    absolute values. (2) Against the full oracle: every d out/d s differences two J values, so per
+    (p2s_debug_blur) -- only fp32 rounding separates them (the adjoint pass re-forms J in its own
+    epilogue, a different fp32 summation order of the K x C terms): |err| <= 1e-5 x the sum of the
+    terms' absolute values + 2 x 4e-6 max|J| sum_c |g_c|. (2) Against the full oracle: every d out/d s differences two J values, so per
     pixel |err| <= 2 max|J_gpu - J_oracle| sum_c |g_c| (+ the rounding of (1)); rel-L2 <= 1e-2
     (J's own rel-L2 bar is 1e-3, and neighbour differences of a blurred J are ~10x smaller than J)."""
     from oracle import adjoint
@@ -521,15 +599,16 @@ def _check_dt(r, inp, g, gt, rt, with_tilt, name, J_ref=None):
         tg = adjoint.grad_tilt(Jg[b], tilt[b], g[b], np.float32)
         ta = adjoint.grad_tilt(Jg[b], tilt[b], g[b], np.float32, absolute=True)
         d1 = np.abs(gt[b] - tg)
-        assert np.all(d1 <= 1e-5 * ta + 1e-30), f"dL/dt[{name}] vs grad_tilt(J_gpu): {d1.max():.3e}"
-        worst1 = max(worst1, float((d1 / np.maximum(ta, 1e-30)).max()))
-        bar = 2 * eJ * np.abs(g[b].astype(np.float64)).sum(0)[None] + 1e-5 * ta + 1e-30
+        b1 = 1e-5 * ta + 8e-6 * np.abs(Jg[b]).max() * np.abs(g[b].astype(np.float64)).sum(0)[None] + 1e-30
+        assert np.all(d1 <= b1), f"dL/dt[{name}] vs grad_tilt(J_gpu): {d1.max():.3e} ({(d1 / b1).max():.2f} x bar)"
+        worst1 = max(worst1, float((d1 / b1).max()))
+        bar = 2 * eJ * np.abs(g[b].astype(np.float64)).sum(0)[None] + b1
         d2 = np.abs(gt[b] - rt[b])
         assert np.all(d2 <= bar), f"dL/dt[{name}] vs oracle: {d2.max():.3e} > its J-error bound"
         worst2 = max(worst2, float((d2 / bar).max()))
     rl2 = float(np.linalg.norm(gt - rt) / max(np.linalg.norm(rt), 1e-30))
     print(f"dL/dt[{name}]: max_abs={np.abs(gt - rt).max():.3e} rel_l2={rl2:.3e} (ref max {np.abs(rt).max():.3f}); "
-          f"vs grad_tilt(J_gpu) max rel {worst1:.2e}; J-error bound use {worst2:.2f}")
+          f"vs grad_tilt(J_gpu) bar use {worst1:.2f}; J-error bound use {worst2:.2f}")
     assert rl2 <= 1e-2, f"dL/dt[{name}]: rel L2 {rl2:.3e}"
 
 

@@ -396,6 +396,45 @@ def test_sampler_empirical_covariance():
     assert np.abs(emp - ref).max() < 6 * np.sqrt(2 / 4000) * np.abs(ref).max()
 
 
+def test_dense_sampler_reduces_to_the_separable_one():
+    """A dense spatial correlation equal to s (x) s (the separable stand-in written out) gives the
+    separable sampler's anchors: the Kronecker product of the Cholesky factors is the Cholesky
+    factor of the Kronecker product (both lower triangular with a positive diagonal)."""
+    from oracle import sampler
+    rng = np.random.default_rng(5)
+    M = rng.standard_normal((3, 3))
+    R = M @ M.T / 3 + 0.3 * np.eye(3)
+    for G, L in ((1, 0.0), (4, 1.5), (6, 0.0), (7, 2.5)):
+        sep = sampler.sample(11, 2, 3, G, 3, corr_len=L, mode_cov=R)
+        den = sampler.sample_dense(11, 2, 3, G, 3, synth.anchor_cov_separable(G, L), mode_cov=R)
+        # (equal up to rounding amplified by the condition number: the Gaussian s with a 1e-6
+        # jitter has cond ~ 1e6, so the two factorisations agree to ~1e-9)
+        np.testing.assert_allclose(den, sep, rtol=0, atol=1e-7)
+        # the factor passed directly (is_factor) is the same draw
+        Lf = np.linalg.cholesky(synth.anchor_cov_separable(G, L))
+        Lf_up = Lf + np.triu(np.ones_like(Lf), 1) * 7.0  # upper part ignored
+        np.testing.assert_allclose(sampler.sample_dense(11, 2, 3, G, 3, Lf_up, mode_cov=R, is_factor=True), den,
+                                   rtol=0, atol=1e-12)
+
+
+def test_dense_sampler_empirical_covariance_nonseparable():
+    """Across 4000 frames the anchors' covariance is R (x) C for the NON-separable exponential
+    correlation C (Monte-Carlo), which no Kronecker-factored sampler can produce."""
+    from oracle import sampler
+    G, n_in = 3, 2
+    rng = np.random.default_rng(4)
+    M = rng.standard_normal((n_in, n_in))
+    R = M @ M.T / n_in + 0.5 * np.eye(n_in)
+    Cs = synth.anchor_cov_exp(G, 1.2)
+    # C is not separable: it differs from the Kronecker product of its own row/column marginals
+    assert np.abs(Cs - np.kron(Cs[::G, ::G], Cs[:G, :G])).max() > 1e-2
+    A = sampler.sample_dense(99, 0, 4000, G, n_in, Cs, mode_cov=R).reshape(4000, -1)
+    emp = A.T @ A / A.shape[0]
+    ref = np.kron(R, Cs)
+    assert np.abs(emp - ref).max() < 6 * np.sqrt(2 / 4000) * np.abs(ref).max()
+    assert np.all(np.linalg.eigvalsh(synth.anchor_cov_exp(8, 3.0)) > 0)  # positive definite at G = 8
+
+
 # ---- adjoint of steps a2-a3 (SURVEY §8(f) NEXT-4; PAPER.md:524 "differentiable module") —
 #      oracle/adjoint.py, pinned by finite differences of its independent forward
 
