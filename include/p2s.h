@@ -235,8 +235,9 @@ P2S_API p2s_status p2s_sampler_init(int G, int n_in, double corr_len, const doub
  * p2s_sampler_init. The sampler owns device copies of L (fp16 hi/lo tiles, ~33 MB at G = 64) and a
  * workspace; p2s_sample_anchors then draws A_f = (L_R (x) L) z_f with the same Philox normals z_f
  * as the separable sampler (so C = s (x) s reproduces it up to rounding), the product L Y as a
- * tcgen05 GEMM over L's lower triangle with fp16 hi/lo operand splits and fp32 accumulation:
- * |error| <= ~2^-19 x sum_q |L[p][q]| |Y[q]| per anchor. Errors: NULL
+ * tcgen05 GEMM over L's lower triangle with fp16 hi/lo operand splits (lo parts scaled by 2^11, L
+ * by 2^14) and fp32 accumulation:
+ * |error| <= ~2^-20 x sum_q |L[p][q]| |Y[q]| per anchor. Errors: NULL
  * spatial_cov / out, G outside [1, 64], n_in outside [1, 64], a non-symmetric or non-SPD matrix
  * -> P2S_ERR_INVALID_ARG; not an sm_100 device -> P2S_ERR_UNSUPPORTED; allocation -> P2S_ERR_OOM. */
 P2S_API p2s_status p2s_sampler_init_dense(int G, int n_in, const double* spatial_cov, int is_factor,

@@ -45,8 +45,9 @@ def _load():
         lib.p2s_oracle_pixels.argtypes = common + [ctypes.POINTER(ctypes.c_int), i, d, d, i]
         lib.p2s_oracle_warp.argtypes = [d, i, i, i, i, f, d, i]
         lib.p2s_oracle_interp_anchors.argtypes = [f, i, i, i, i, i, d]
+        lib.p2s_oracle_adjoint_blur.argtypes = [f, i, i, i, i, f, i, i, d, d, d, d, i]
         for fn in (lib.p2s_oracle_beta, lib.p2s_oracle_render, lib.p2s_oracle_pixels,
-                   lib.p2s_oracle_warp, lib.p2s_oracle_interp_anchors):
+                   lib.p2s_oracle_warp, lib.p2s_oracle_interp_anchors, lib.p2s_oracle_adjoint_blur):
             fn.restype = i
         _lib = lib
     return _lib
@@ -174,3 +175,25 @@ def interp_anchors(anchors, H, W) -> np.ndarray:
     rc = _load().p2s_oracle_interp_anchors(_fp(a), B, n_in, G, H, W, _dp(out))
     assert rc == 0
     return out
+
+
+def adjoint_blur(image, basis, beta, gJ, want_beta=True, want_image=True, threads=None):
+    """Adjoint of step a2 (Eq. 5 transposed) in the C oracle:
+    (dL/dbeta [B][K][H][W] | None, dL/dI [B][C][H][W] | None), fp64, for beta [B][K][H][W] and
+    dL/dJ = gJ [B][C][H][W] (see p2s_oracle.cpp)."""
+    image = np.ascontiguousarray(image, np.float32)
+    basis = np.ascontiguousarray(basis, np.float32)
+    beta = np.ascontiguousarray(beta, np.float64)
+    gJ = np.ascontiguousarray(gJ, np.float64)
+    B, C, H, W = image.shape
+    K, S, _ = basis.shape
+    assert beta.shape == (B, K, H, W) and gJ.shape == (B, C, H, W)
+    gb = np.zeros((B, K, H, W)) if want_beta else None
+    gi = np.zeros((B, C, H, W)) if want_image else None
+    nul = ctypes.POINTER(ctypes.c_double)()
+    rc = _load().p2s_oracle_adjoint_blur(_fp(image), B, C, H, W, _fp(basis), K, S, _dp(beta), _dp(gJ),
+                                         _dp(gb) if gb is not None else nul, _dp(gi) if gi is not None else nul,
+                                         threads or default_threads())
+    assert rc == 0
+    return gb, gi
+

@@ -38,6 +38,13 @@
 //               + fy (1-fx) A_k[i0+1][j0] + fy fx A_k[i0+1][j0+1]      (each mode k separately)
 //    G = 1: constant field. The dense field then feeds step a1 exactly as a given field does.
 //
+//  adjoint of step a2 ("differentiable module"), for a given
+//    beta [K] per pixel and upstream dL/dJ = gJ [C] per pixel (fp64 inputs):
+//      dL/dbeta_k(y,x) = sum_c gJ_c(y,x) C_kc(y,x)                     (C_kc as in step a2)
+//      dL/dI_c(q)      = sum over pixels p and taps (i,j) with (cY(p_y-(i-r)), cX(p_x-(j-r))) = q
+//                        of phi_k[i][j] beta_k(p) gJ_c(p)               (the transpose of Eq. 5:
+//                        every term of J_c(p) sends its weight back to the pixel it read)
+//
 // Parity pins for every function live in tests/test_oracle_pins.py (closed forms,
 // invariants, library routines: torch nn.Linear, scipy.ndimage.convolve,
 // torch grid_sample, FFT convolution).
@@ -307,6 +314,80 @@ int p2s_oracle_interp_anchors(const float* anchors, int B, int n_in, int G, int 
                                  fy * (1 - fx) * A[(size_t)(i0 + 1) * G + j0] + fy * fx * A[(size_t)(i0 + 1) * G + j0 + 1];
         }
     }
+  return 0;
+}
+
+// Adjoint of step a2 (see the header) for beta [B][K][H][W] and gJ [B][C][H][W] (fp64):
+// gbeta_out [B][K][H][W] and / or gimage_out [B][C][H][W] (fp64, either may be NULL). dL/dI is
+// accumulated per thread in private frames (scatter order, no atomics) and then summed.
+int p2s_oracle_adjoint_blur(const float* image, int B, int C, int H, int W, const float* taps, int K, int S,
+                            const double* beta, const double* gJ, double* gbeta_out, double* gimage_out,
+                            int nthreads) {
+  if (!image || !taps || !beta || !gJ || B < 1 || C < 1 || H < 1 || W < 1 || K < 1 || S < 1 || (S % 2) == 0)
+    return -1;
+  const int r = (S - 1) / 2;
+  const size_t HW = (size_t)H * W;
+  nthreads = std::max(1, nthreads);
+  for (int b = 0; b < B; ++b) {
+    const double* bb = beta + (size_t)b * K * HW;
+    const double* gj = gJ + (size_t)b * C * HW;
+    if (gbeta_out)
+      parallel_rows(H, nthreads, [&](int y) {
+        std::vector<double> patch((size_t)S * S);
+        for (int x = 0; x < W; ++x) {
+          for (int k = 0; k < K; ++k) gbeta_out[((size_t)b * K + k) * HW + (size_t)y * W + x] = 0.0;
+          for (int c = 0; c < C; ++c) {
+            const float* img = image + ((size_t)b * C + c) * HW;
+            for (int i = 0; i < S; ++i) {
+              const int yy = clampi(y - (i - r), 0, H - 1);
+              for (int j = 0; j < S; ++j) patch[(size_t)i * S + j] = img[(size_t)yy * W + clampi(x - (j - r), 0, W - 1)];
+            }
+            const double g = gj[(size_t)c * HW + (size_t)y * W + x];
+            for (int k = 0; k < K; ++k) {
+              const float* phi = taps + (size_t)k * S * S;
+              double ck = 0.0;
+              for (int t = 0; t < S * S; ++t) ck += (double)phi[t] * patch[t];
+              gbeta_out[((size_t)b * K + k) * HW + (size_t)y * W + x] += g * ck;
+            }
+          }
+        }
+      });
+    if (gimage_out) {
+      std::vector<std::vector<double>> part(nthreads, std::vector<double>((size_t)C * HW, 0.0));
+      std::vector<std::thread> th;
+      std::atomic_int next{0};
+      for (int t = 0; t < nthreads; ++t)
+        th.emplace_back([&, t]() {
+          std::vector<double> h((size_t)S * S);
+          double* acc = part[t].data();
+          for (int y; (y = next.fetch_add(1)) < H;)
+            for (int x = 0; x < W; ++x) {
+              // h[i][j] = sum_k beta_k(y,x) phi_k[i][j]: the pixel's own PSF (Eq. 3/4)
+              std::fill(h.begin(), h.end(), 0.0);
+              for (int k = 0; k < K; ++k) {
+                const double bk = bb[(size_t)k * HW + (size_t)y * W + x];
+                const float* phi = taps + (size_t)k * S * S;
+                for (int t2 = 0; t2 < S * S; ++t2) h[t2] += bk * (double)phi[t2];
+              }
+              for (int c = 0; c < C; ++c) {
+                const double g = gj[(size_t)c * HW + (size_t)y * W + x];
+                double* ac = acc + (size_t)c * HW;
+                for (int i = 0; i < S; ++i) {
+                  const int yy = clampi(y - (i - r), 0, H - 1);
+                  for (int j = 0; j < S; ++j) ac[(size_t)yy * W + clampi(x - (j - r), 0, W - 1)] += h[(size_t)i * S + j] * g;
+                }
+              }
+            }
+        });
+      for (auto& t : th) t.join();
+      double* o = gimage_out + (size_t)b * C * HW;
+      for (size_t e = 0; e < (size_t)C * HW; ++e) {
+        double s = 0.0;
+        for (int t = 0; t < nthreads; ++t) s += part[t][e];
+        o[e] = s;
+      }
+    }
+  }
   return 0;
 }
 

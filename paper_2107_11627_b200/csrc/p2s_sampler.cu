@@ -15,8 +15,11 @@
 // with L = chol(C) computed once on the host (fp64, blocked, threaded). Per call the mode-mixed
 // normals Y = z L_R^T (fp64, split into fp16 hi + lo) are drawn by k_draw_y and the product L Y is
 // a tcgen05 GEMM (k_sample_dense): M = 128 anchors x N = 128 (frame, mode) columns per tile, K
-// over the anchors of L's lower triangle only, three fp16 products per K-step
-// (L_hi Y_hi + L_hi Y_lo + L_lo Y_hi, fp32 accumulation in TMEM) -- ~2^-21 relative per term.
+// over the anchors of L's lower triangle only, three fp16 products per K-step, fp32 accumulation
+// in TMEM: L_hi Y_hi into one accumulator, L_hi Y_lo' + L_lo' Y_hi into a second, where the lo
+// parts are stored scaled by 2^11 (lo' = fp16((v - hi) 2^11): no subnormal lo parts) and L by
+// 2^14 (entries down to ~4e-9 stay normal); the epilogue forms 2^-14 (D_hi + 2^-11 D_lo) --
+// the dropped lo x lo term is ~2^-22 relative.
 #include <cuda_fp16.h>
 #include <cuda_runtime.h>
 
@@ -115,6 +118,8 @@ constexpr int kDenseStages = 3;
 constexpr int kDenseThreads = 192;                   // w0 bulk-copy producer, w1 UMMA, w2-5 epilogue
 constexpr int kDenseSmem = kDenseStages * kDenseStage + 256;
 constexpr int kDenseMaxCols = 2048;                  // (frame, mode) columns per GEMM launch
+constexpr double kDenseLScale = 16384.0;             // L stored x 2^14
+constexpr double kDenseLoScale = 2048.0;             // lo parts stored x 2^11
 
 __host__ __device__ __forceinline__ uint32_t core_off(int row, int k) {
   return (uint32_t)((row % 8) * 16 + (row / 8) * 1024 + (k % 8) * 2 + (k / 8) * 128);
@@ -129,7 +134,7 @@ struct DenseParams {
 
 // Y = z L_R^T for frames [frame0, frame0 + F), all anchors p < Np (zero for p >= G^2): block
 // (anchor block of 128, frame); normals once per (p, k) into shared memory, then per thread (one
-// anchor) the n_in mixed values, fp64, split into fp16 hi and lo = fp16(y - hi).
+// anchor) the n_in mixed values, fp64, split into fp16 hi and lo' = fp16((y - hi) 2^11).
 __global__ void __launch_bounds__(128) k_draw_y(const double* __restrict__ LR, int G, int n_in, uint32_t k0,
                                                 uint32_t k1, int frame0, int KB, uint8_t* __restrict__ Yp) {
   extern __shared__ double zs[];  // [n_in][128]
@@ -144,15 +149,15 @@ __global__ void __launch_bounds__(128) k_draw_y(const double* __restrict__ LR, i
     const int n = f * n_in + j, nb = n / kDenseBN, row = n % kDenseBN;
     uint8_t* t = Yp + ((size_t)nb * KB + kb) * kDensePair + core_off(row, kk);
     const __half hi = __double2half(y);
-    const __half lo = __double2half(y - (double)__half2float(hi));
+    const __half lo = __double2half((y - (double)__half2float(hi)) * kDenseLoScale);
     *reinterpret_cast<__half*>(t) = hi;
     *reinterpret_cast<__half*>(t + kDenseTile) = lo;
   }
 }
 
 // A[p][(f, j)] = sum_q L[p][q] Y[q][(f, j)], persistent over (mb, nb) tiles, longest (largest mb)
-// first; TMEM double-buffered (2 x 128 columns) so one tile's epilogue overlaps the next tile's
-// UMMAs.
+// first; per tile two accumulators (hi x hi, and the two lo' products), TMEM double-buffered
+// (2 x 256 columns) so one tile's epilogue overlaps the next tile's UMMAs.
 __global__ void __launch_bounds__(kDenseThreads, 1) k_sample_dense(const DenseParams p) {
   using namespace p2s;
   extern __shared__ __align__(1024) uint8_t smem[];
@@ -173,7 +178,7 @@ __global__ void __launch_bounds__(kDenseThreads, 1) k_sample_dense(const DensePa
     }
     fence_mbar_init();
   }
-  if (warp == 1) tmem_alloc<256>(tmem_slot);
+  if (warp == 1) tmem_alloc<512>(tmem_slot);
   tc_fence_before();
   __syncthreads();
   tc_fence_after();
@@ -201,7 +206,7 @@ __global__ void __launch_bounds__(kDenseThreads, 1) k_sample_dense(const DensePa
       const int buf = tl & 1;
       mbar_wait(&acc_empty[buf], ((tl >> 1) & 1) ^ 1);
       tc_fence_after();
-      const uint32_t d = tmem + (uint32_t)(buf * kDenseBN);
+      const uint32_t d = tmem + (uint32_t)(buf * 2 * kDenseBN), dlo = d + kDenseBN;
       for (int kb = 0; kb <= 2 * mb + 1; ++kb, ++it) {
         const int s = it % kDenseStages;
         mbar_wait(&full[s], (it / kDenseStages) & 1);
@@ -212,9 +217,10 @@ __global__ void __launch_bounds__(kDenseThreads, 1) k_sample_dense(const DensePa
           const uint32_t o = base + (uint32_t)k16 * 256;
           const uint64_t ahi = sdesc(o, 128, 1024), alo = sdesc(o + kDenseTile, 128, 1024);
           const uint64_t bhi = sdesc(o + kDensePair, 128, 1024), blo = sdesc(o + kDensePair + kDenseTile, 128, 1024);
-          umma_f16_elect(d, ahi, bhi, idesc, (kb | k16) != 0 ? 1u : 0u);
-          umma_f16_elect(d, ahi, blo, idesc, 1u);
-          umma_f16_elect(d, alo, bhi, idesc, 1u);
+          const uint32_t acc = (kb | k16) != 0 ? 1u : 0u;
+          umma_f16_elect(d, ahi, bhi, idesc, acc);
+          umma_f16_elect(dlo, ahi, blo, idesc, acc);
+          umma_f16_elect(dlo, alo, bhi, idesc, 1u);
         }
         umma_commit_elect(&empty[s]);  // the stage is free once these UMMAs have read it
       }
@@ -229,16 +235,18 @@ __global__ void __launch_bounds__(kDenseThreads, 1) k_sample_dense(const DensePa
       mbar_wait(&acc_full[buf], (tl >> 1) & 1);
       tc_fence_after();
       const int a = mb * kDenseBM + row;
-      const uint32_t tl_addr = tmem + ((uint32_t)(32 * q) << 16) + (uint32_t)(buf * kDenseBN);
+      const uint32_t tl_addr = tmem + ((uint32_t)(32 * q) << 16) + (uint32_t)(buf * 2 * kDenseBN);
       for (int cg = 0; cg < kDenseBN / 16; ++cg) {
-        float v[16];
+        float v[16], w[16];
         tmem_ld16(tl_addr + (uint32_t)cg * 16, v);
+        tmem_ld16(tl_addr + (uint32_t)(kDenseBN + cg * 16), w);
         tmem_ld_wait();
         if (a < p.GG) {
 #pragma unroll
           for (int i = 0; i < 16; ++i) {
             const int n = nb * kDenseBN + cg * 16 + i;
-            if (n < p.ncols) p.out[(size_t)n * p.GG + a] = v[i];  // n = f n_in + j: [f][j][a]
+            // 2^-14 (D_hi + 2^-11 D_lo); n = f n_in + j: anchors [f][j][a]
+            if (n < p.ncols) p.out[(size_t)n * p.GG + a] = fmaf(w[i], 0x1p-25f, v[i] * 0x1p-14f);
           }
         }
       }
@@ -249,7 +257,7 @@ __global__ void __launch_bounds__(kDenseThreads, 1) k_sample_dense(const DensePa
   tc_fence_before();
   __syncthreads();
   tc_fence_after();
-  if (warp == 1) tmem_dealloc<256>(tmem);
+  if (warp == 1) tmem_dealloc<512>(tmem);
 }
 
 // Lower Cholesky factor of an n x n row-major SPD matrix in place (fp64), right-looking with
@@ -398,8 +406,8 @@ p2s_status p2s_sampler_init_dense(int G, int n_in, const double* spatial_cov, in
         for (int k = 0; k < kDenseBK; ++k) {
           const int i = mb * kDenseBM + r, j = kb * kDenseBK + k;
           if (i >= GG || j >= GG || j > i) continue;
-          const double v = L[(size_t)i * GG + j];
-          const __half hi = __double2half(v), lo = __double2half(v - (double)__half2float(hi));
+          const double v = L[(size_t)i * GG + j] * kDenseLScale;
+          const __half hi = __double2half(v), lo = __double2half((v - (double)__half2float(hi)) * kDenseLoScale);
           std::memcpy(t + core_off(r, k), &hi, 2);
           std::memcpy(t + kDenseTile + core_off(r, k), &lo, 2);
         }

@@ -10,8 +10,9 @@ configuration bench.py times:
           frame is asserted on (SURVEY.md §8(c) precision plan: "report the worst frame")
   * cfg5  one 1024x1024 RGB frame (K=100, 65x65, MLP 33-256-256-100) -- the tightest margin
           the survey predicts (max-abs 1.46e-3 vs the 2e-3 bar)
-  * the cfg3 4-frame sequence (p2s_render_sequence) and the cfg3 colour frame
-    (p2s_render_color, per-channel beta), every element.
+  * the cfg3 4-frame sequence (p2s_render_sequence), the cfg3 colour frame (p2s_render_color,
+    per-channel beta) and the cfg3 anchor-grid frame (p2s_render_anchors, G = 16), every element;
+  * the adjoint of a cfg3 frame (p2s_backward): every element of dL/dbeta and dL/dI.
 
 Bar (BASELINE.json north_star): max |gpu - oracle| <= 2e-3 and relative L2 <= 1e-3, over the
 whole tensor AND for every frame on its own. Per-frame numbers are written as JSON to
@@ -158,3 +159,50 @@ def test_color_cfg3_full(p2s):
     r.close()
     ref, _ = oracle.render_color(inp.image, zc, inp.tilt, inp.basis, inp.mlp)
     _per_frame(out[0], ref[0], "render_color[cfg3 full, per channel]")
+
+
+def test_adjoint_cfg3_full_frame(p2s):
+    """The adjoint of a whole cfg3 frame: every element of
+    dL/dbeta [K][H][W] and dL/dI [C][H][W] against the C oracle's adjoint of Eq. 5
+    (oracle.adjoint_blur, pinned against oracle/adjoint.py and by the dot-product identities)
+    fed with the oracle's beta and dL/dJ (the warp's transpose, oracle/adjoint.py grad_J, cells
+    decided in fp32 as the kernel: DESIGN.md reading N4). Bars: max-abs 2e-3 x max|ref| and
+    rel-L2 1e-3 (the forward's bar, relative to the gradient's scale)."""
+    from oracle import adjoint
+    spec = synth.CONFIGS[3]
+    inp = synth.make_inputs(spec)
+    g = synth.make_upstream_grad(spec)
+    r = p2s.Renderer(inp.basis, inp.mlp)
+    gb, gt, gi = r.backward(_dev(inp.image), _dev(inp.zernike), _dev(inp.tilt), _dev(g), want_image=True)
+    gb, gi = gb.cpu().numpy().astype(np.float64), gi.cpu().numpy().astype(np.float64)
+    r.close()
+    beta = oracle.beta(inp.image, inp.zernike, inp.basis, inp.mlp)
+    gJ = adjoint.grad_J(inp.tilt[0], g[0], coord_dtype=np.float32)[None]
+    t0 = time.perf_counter()
+    rb, ri = oracle.adjoint_blur(inp.image, inp.basis, beta, gJ)
+    print(f"oracle adjoint cfg3: {time.perf_counter() - t0:.1f} s")
+    for got, ref, what in ((gb, rb, "dL/dbeta[cfg3 full]"), (gi, ri, "dL/dI[cfg3 full]")):
+        d = got - ref
+        mx, rl = float(np.abs(d).max()), float(np.linalg.norm(d) / np.linalg.norm(ref))
+        _RESULTS[what] = {"whole": {"max_abs": mx, "rel_l2": rl, "elements": int(d.size),
+                                    "ref_max": float(np.abs(ref).max()),
+                                    "bar": {"max_abs": f"2e-3 x max|ref| = {2e-3 * np.abs(ref).max():.3e}",
+                                            "rel_l2": REL_L2}}, "per_frame": []}
+        print(f"{what}: {d.size} elements, max_abs={mx:.3e} (ref max {np.abs(ref).max():.3f}) rel_l2={rl:.3e}")
+        assert mx <= 2e-3 * np.abs(ref).max() and rl <= REL_L2
+
+
+def test_anchor_grid_cfg3_full_frame(p2s):
+    """p2s_render_anchors (a G x G anchor grid interpolated
+    bilinearly to every pixel) on a whole cfg3 frame at G = 16, every element, vs the oracle chain
+    (oracle.interp_anchors -> the field rounded to fp32 as a caller would pass it -> oracle.render)."""
+    spec = synth.CONFIGS[3]
+    inp = synth.make_inputs(spec)
+    G = 16
+    anc = synth.make_anchors(spec, G)
+    r = p2s.Renderer(inp.basis, inp.mlp)
+    out = r.render_anchors(_dev(inp.image), _dev(anc), _dev(inp.tilt)).cpu().numpy()
+    r.close()
+    dense = oracle.interp_anchors(anc, spec.H, spec.W).astype(np.float32)
+    ref, _ = oracle.render(inp.image, dense, inp.tilt, inp.basis, inp.mlp)
+    _per_frame(out, ref, f"render_anchors[cfg3 G={G} full]")

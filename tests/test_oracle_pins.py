@@ -435,6 +435,39 @@ def test_dense_sampler_empirical_covariance_nonseparable():
     assert np.all(np.linalg.eigvalsh(synth.anchor_cov_exp(8, 3.0)) > 0)  # positive definite at G = 8
 
 
+@pytest.mark.parametrize("shape", [dict(B=1, C=3, H=9, W=11, K=4, S=5), dict(B=2, C=1, H=6, W=5, K=3, S=7),
+                                   dict(B=1, C=2, H=1, W=1, K=2, S=3), dict(B=1, C=1, H=4, W=13, K=1, S=1)])
+def test_c_adjoint_blur_matches_numpy_adjoint(shape):
+    """The C oracle's adjoint of Eq. 5 (dL/dbeta, dL/dI: the whole-frame reference of the GPU's
+    cfg3 adjoint) equals oracle/adjoint.py's (pinned above by central finite differences)."""
+    from oracle import adjoint
+    rng = np.random.default_rng(sum(shape.values()))
+    B, C, H, W, K, S = (shape[k] for k in "BCHWKS")
+    image = rng.random((B, C, H, W)).astype(np.float32)
+    basis = rng.standard_normal((K, S, S)).astype(np.float32)
+    beta = rng.standard_normal((B, K, H, W))
+    gJ = rng.standard_normal((B, C, H, W))
+    gb, gi = oracle.adjoint_blur(image, basis, beta, gJ, threads=3)
+    for b in range(B):
+        Ck = adjoint.conv_all(image[b], basis)
+        np.testing.assert_allclose(gb[b], np.einsum("chw,kchw->khw", gJ[b], Ck), rtol=1e-12, atol=1e-12)
+        np.testing.assert_allclose(gi[b], adjoint.grad_image(beta[b], basis, gJ[b]), rtol=1e-12, atol=1e-12)
+
+
+def test_c_adjoint_blur_dot_product_identities():
+    """<dL/dJ, J> = <dL/dbeta, beta> = <dL/dI, I> with J the C oracle's own forward blur (J is
+    linear in I and in beta for fixed beta / I), on a ragged 3-channel frame with replicate borders."""
+    spec = synth.custom("adjid", 321, B=1, C=3, H=21, W=34, K=6, S=9, h1=16, h2=16, t_std=0.0)
+    inp = synth.make_inputs(spec)
+    beta = oracle.beta(inp.image, inp.zernike, inp.basis, inp.mlp)
+    _, J = oracle.render(inp.image, inp.zernike, None, inp.basis, inp.mlp, want_blur=True)
+    gJ = np.random.default_rng(8).standard_normal(J.shape)
+    gb, gi = oracle.adjoint_blur(inp.image, inp.basis, beta, gJ)
+    lhs = float((gJ * J).sum())
+    assert abs(lhs - float((gb * beta).sum())) <= 1e-10 * np.abs(gJ * J).sum()
+    assert abs(lhs - float((gi * inp.image).sum())) <= 1e-10 * np.abs(gJ * J).sum()
+
+
 # ---- adjoint of steps a2-a3 (SURVEY §8(f) NEXT-4; PAPER.md:524 "differentiable module") —
 #      oracle/adjoint.py, pinned by finite differences of its independent forward
 
