@@ -613,6 +613,12 @@ def main():
         v = len(times) / sum(times)
         line["cpu_baseline"] = {"value": v, "unit": "frames/s", "cores": threads, "kind": "oracle",
                                 "sample": sample, "s_per_frame": [round(x, 3) for x in times]}
+        # cfg1 and cfg2 (the paper's 256x256 timing shape) also on one thread
+        single = {}
+        for cid in (1, 2):
+            st, _ = oracle_full_frames(synth.CONFIGS[cid], range(1), 1)
+            single[synth.CONFIGS[cid].name] = {"s_per_frame": round(st[0], 4), "threads": 1}
+        line["cpu_baseline"]["single_thread_full_frames"] = single
     print(json.dumps(line))
     pdist.shutdown(dist)
 

@@ -123,7 +123,7 @@ struct p2s_handle {
   size_t gJ_cap = 0;
   // dL/dI (k_adjoint_image): plan, phi table, workspaces beta [B][K][H][W] fp32 and U_T fp16
   int di_R = 0, di_nchunk = 0, di_kg = 0, di_ngroups = 0, di_Nh = 0, di_OW = 0, di_nring = 0, di_smem = 0;
-  int di_a_bytes = 0, di_b_bytes = 0, di_off_p = 0, di_off_bar = 0;
+  int di_a_bytes = 0, di_b_bytes = 0, di_off_p = 0, di_off_bar = 0, di_egroups = 1;
   uint8_t* d_dib = nullptr;
   __half* d_ut = nullptr;
   size_t ut_cap = 0;
@@ -701,15 +701,21 @@ p2s_status p2s_init(const p2s_basis* basis, const p2s_mlp* mlp, p2s_handle** out
     // bytes per output row (this CTA's A window + its half of B) such that each half of
     // N = R x S fits one UMMA (<= 256) and >= 3 ring stages fit (measured: the kernel is bound
     // by L2 -> SM delivery, so bytes per output decide)
-    int R = 0, hr = 0, Nh = 0, wr8 = 0, kg = 1, nchunk = 0, wpad = 0, stage = 0, nring = 0;
-    const int sp_bytes = S * 128 * 4, bar_bytes = 256;
+    // The epilogue runs in up to kDiGroups groups of four warps (each with an S x 128 fp32 P buffer):
+    // as many as leave room for the ring (S = 65 takes fewer).
+    int R = 0, hr = 0, Nh = 0, wr8 = 0, kg = 1, nchunk = 0, wpad = 0, stage = 0, nring = 0, egroups = 0;
+    const int bar_bytes = 256;
+    int sp_bytes = 0;
+    for (int eg = kDiGroups; eg >= 1 && nring < 3; --eg) {
+    sp_bytes = eg * S * 128 * 4;
     const int avail = kSmemLimit - sp_bytes - bar_bytes;
     double best = 1e30;
+    egroups = eg;
     for (int Rt = 2; Rt <= 32; Rt += 2) {
       const int Nht = (Rt / 2 * S + 15) / 16 * 16;
       if (Nht > 256) break;
       const int w8 = (S + Rt - 1 + 7) / 8, nch = w8 + (w8 & 1);  // even chunk count: UMMA K = 16
-      const int stg = nch * 2048 + nch * Nht * 16;
+      const int stg = (nch * 2048 + nch * Nht * 16 + 1023) / 1024 * 1024;  // 1 KB: SWIZZLE_128B U tiles
       const int nr = std::min(6, avail / stg);
       if (nr < 3 || nch * 8 > 256) continue;
       const double cost = (double)stg / Rt;
@@ -718,10 +724,15 @@ p2s_status p2s_init(const p2s_basis* basis, const p2s_mlp* mlp, p2s_handle** out
         R = Rt; hr = Rt / 2; Nh = Nht; wr8 = w8; nchunk = nch; wpad = nch; stage = stg; nring = nr;
       }
     }
-    if (nring < 2) return fail(P2S_ERR_UNSUPPORTED);  // not reached for S <= 65
+    }
+    if (nring < 3) return fail(P2S_ERR_UNSUPPORTED);  // not reached for S <= 65
+    {  // every group gets >= 1 output row (an empty group would never release TMEM)
+      const int per = (R + egroups - 1) / egroups;
+      h->di_egroups = (R + per - 1) / per;
+    }
     h->di_R = R; h->di_Nh = Nh; h->di_kg = kg; h->di_nchunk = nchunk; h->di_nring = nring;
     h->di_ngroups = (K + kg - 1) / kg;
-    h->di_OW = (128 - (S - 1)) / 8 * 8;  // strips start at multiples of 8 columns (TMA x/8 view)
+    h->di_OW = 128;  // strip stride: strips tile U, partial diagonal sums meet in RED.ADD
     h->di_a_bytes = nchunk * 2048;
     h->di_b_bytes = nchunk * Nh * 16;  // per CTA: two halves x Nh/2 rows
     h->di_off_p = nring * stage;
@@ -1061,12 +1072,13 @@ p2s_status p2s_backward(p2s_handle* h, p2s_image im, const float* zernike_field,
     P2S_CUDA(cudaMemsetAsync(grad_image, 0, chw * sizeof(float), st));
     DiParams d{};
     {
-      cuuint64_t gdim[4] = {8, (cuuint64_t)im.H, (cuuint64_t)Ws / 8, (cuuint64_t)im.B * im.C * h->K};
-      cuuint64_t gstride[3] = {(cuuint64_t)Ws * 2, 16, (cuuint64_t)im.H * Ws * 2};
-      cuuint32_t box[4] = {8, (cuuint32_t)h->di_nchunk * 8, 16, 1};
-      cuuint32_t estr[4] = {1, 1, 1, 1};
-      CUresult cr = h->encode(&d.umap, CU_TENSOR_MAP_DATA_TYPE_FLOAT16, 4, h->d_ut, gdim, gstride, box, estr,
-                              CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE,
+      // U [planes][H][Ws] fp16; box = 64 columns (128 B) x the window's rows x 1 plane, 128B swizzle
+      cuuint64_t gdim[3] = {(cuuint64_t)Ws, (cuuint64_t)im.H, (cuuint64_t)im.B * im.C * h->K};
+      cuuint64_t gstride[2] = {(cuuint64_t)Ws * 2, (cuuint64_t)im.H * Ws * 2};
+      cuuint32_t box[3] = {64, (cuuint32_t)h->di_nchunk * 8, 1};
+      cuuint32_t estr[3] = {1, 1, 1};
+      CUresult cr = h->encode(&d.umap, CU_TENSOR_MAP_DATA_TYPE_FLOAT16, 3, h->d_ut, gdim, gstride, box, estr,
+                              CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B,
                               CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
       if (cr != CUDA_SUCCESS) {
         g_last_cuda_error = "cuTensorMapEncodeTiled (U) failed (" + std::to_string((int)cr) + ")";
@@ -1092,14 +1104,16 @@ p2s_status p2s_backward(p2s_handle* h, p2s_image im, const float* zernike_field,
     d.BC = im.B * im.C; d.K = h->K; d.H = im.H; d.W = im.W; d.S = h->S; d.r = h->r;
     d.R = h->di_R; d.nchunk = h->di_nchunk; d.kg = h->di_kg; d.ngroups = h->di_ngroups; d.Nh = h->di_Nh;
     d.OW = h->di_OW;
-    d.xs0 = -8 * ((2 * h->r + 7) / 8);  // <= -2r: the first strip's outputs start at or before -r
+    d.xs0 = 0;  // strip 0 = U columns [0, 128); its outputs start at -r
     d.nbands = (im.H + 2 * h->r + d.R - 1) / d.R;
     d.nstrips = (im.W - d.xs0 + d.OW - 1) / d.OW;
     d.npairs = (d.nstrips + 1) / 2;
     d.ntiles = d.BC * d.nbands * d.npairs;
     d.a_bytes = h->di_a_bytes; d.b_bytes = h->di_b_bytes; d.nring = h->di_nring;
+    d.stage_bytes = (h->di_a_bytes + h->di_b_bytes + 1023) / 1024 * 1024;
     d.off_p = h->di_off_p; d.off_bar = h->di_off_bar;
-    k_adjoint_image<<<2 * std::min(d.ntiles, h->sm_count / 2), kDiThreads, h->di_smem, st>>>(d);
+    d.egroups = h->di_egroups;
+    k_adjoint_image<<<2 * std::min(d.ntiles, h->sm_count / 2), 64 + 128 * d.egroups, h->di_smem, st>>>(d);
     P2S_CUDA(cudaPeekAtLastError());
   }
   return P2S_OK;

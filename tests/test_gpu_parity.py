@@ -690,10 +690,12 @@ def test_backward_cfg3_sampled(p2s):
     rt_full = adjoint.grad_tilt(Jref[0], inp.tilt[0], g[0], np.float32)[None]
     np.testing.assert_allclose(rt_full[0][:, ys, xs].T, rt, rtol=1e-9, atol=1e-9)  # = backward_at's
     _check_dt(r, inp, g, gt, rt_full, True, "cfg3 full frame", J_ref=Jref)
-    # dL/dI at sampled pixels: the strip/band seams of k_adjoint_image (96-column strips and
-    # 8-row bands on the extended grid start at -16) and the clamp-collecting borders
+    # dL/dI at sampled pixels: the strip/band seams of k_adjoint_image (128-column strips whose
+    # partial diagonal sums overlap on [128 s - r, 128 s + r); 14-row bands from -16) and the
+    # clamp-collecting borders
     gJ = adjoint.grad_J(inp.tilt[0], g[0], coord_dtype=np.float32)
-    yxi = [(0, 0), (H - 1, W - 1), (0, 200), (300, W - 1), (7, 79), (8, 80), (H // 2, 175), (H // 2, 176)]
+    yxi = [(0, 0), (H - 1, W - 1), (0, 200), (300, W - 1), (7, 79), (8, 80), (H // 2, 175), (H // 2, 176),
+           (5, 111), (5, 112), (5, 127), (5, 128), (5, 143), (5, 144), (12, 383), (13, 384)]
     yxi += [(int(y), int(x)) for y, x in zip(rng.integers(1, H - 1, 40), rng.integers(1, W - 1, 40))]
     ri = adjoint.grad_image_at(beta, inp.basis, gJ, yxi)
     yi, xi = np.array(yxi).T
@@ -919,6 +921,42 @@ def _dz_ref(inp, gbeta, amb_rel=(2e-5, 2e-4)):
     return np.stack(refs), alts
 
 
+def _dz_check_fp64_masks(gz, inp, gbeta, what, band=(2.0 ** -10, 2.0 ** -9)):
+    """dL/dz against the oracle with its ReLU masks decided in fp64 (exact operands,
+    the paper's MLP) rather than in the kernel's precision. A unit whose exact pre-activation lies
+    within the fp16 rounding envelope of 0 may take either side on the GPU: |pre_fp16 - pre| <=
+    ~2^-11 sum|terms| per layer (each operand rounded to fp16, 2^-12 relative; layer 2 also
+    inherits layer 1's), so band = (2^-10, 2^-9) x the abs-sums. A flipped unit changes dL/dz by at
+    most its own term: layer 1 unit u -> |W1[u,:]| |(W2^T g2)_u|, layer 2 unit v ->
+    |W1|^T |W2[v,:]| |(W3^T g3)_v|. Per pixel: |gpu - ref64| <= 2e-3 max|ref64| + those terms
+    summed over the pixel's ambiguous units (no enumeration needed)."""
+    from oracle import adjoint
+    m = inp.mlp
+    W1, W2, W3 = (np.asarray(m[k], np.float64) for k in ("W1", "W2", "W3"))
+    worst, n_amb = 0.0, 0
+    for b in range(inp.zernike.shape[0]):
+        z = inp.zernike[b].astype(np.float64)
+        n_in, H, W = z.shape
+        Z = z.reshape(n_in, -1)
+        G3 = np.asarray(gbeta[b], np.float64).reshape(gbeta.shape[1], -1)
+        ref = adjoint.mlp_backward(z, gbeta[b], m, "fp64").reshape(n_in, -1)
+        p1, p2 = adjoint.mlp_preactivations(z, m, "fp64")
+        s1 = np.abs(W1) @ np.abs(Z) + np.abs(m["b1"].astype(np.float64))[:, None]
+        s2 = np.abs(W2) @ np.maximum(p1, 0) + np.abs(m["b2"].astype(np.float64))[:, None]
+        a1, a2 = np.abs(p1) <= band[0] * s1, np.abs(p2) <= band[1] * s2
+        h3 = W3.T @ G3                                   # (W3^T g3) per layer-2 unit
+        g2 = h3 * (p2 > 0)
+        h2 = np.abs(W2).T @ np.abs(g2)                   # >= |(W2^T g2)_u| per layer-1 unit
+        env = np.abs(W1).T @ (a1 * h2)                   # layer-1 flips
+        env += np.abs(W1).T @ (np.abs(W2).T @ (a2 * np.abs(h3)))  # layer-2 flips
+        d = np.abs(gz[b].reshape(n_in, -1).astype(np.float64) - ref)
+        bar = 2e-3 * np.abs(ref).max() + env
+        assert np.all(d <= bar), f"{what} (fp64 masks): {(d / bar).max():.2f} x bar"
+        worst = max(worst, float((d / bar).max()))
+        n_amb += int((a1.any(0) | a2.any(0)).sum())
+    print(f"{what} (fp64 masks): bar use {worst:.3f}, pixels with an fp16-ambiguous unit {n_amb}")
+
+
 def _dz_check(gz, ref, alts, what, scale=None):
     """Element-wise parity off the ambiguous pixels; at an ambiguous pixel the GPU result must equal
     one of its valid alternatives. Tolerance: 2e-3 x max|ref|, or x scale[b, 0, pixel] (a per-pixel
@@ -974,6 +1012,7 @@ def test_mlp_backward_parity(p2s, name):
     gz = r.mlp_backward(_dev(inp.zernike), _dev(gbeta)).cpu().numpy()
     ref, alts = _dz_ref(inp, gbeta.astype(np.float64))
     _dz_check(gz, ref, alts, f"dL/dz[{name}]")
+    _dz_check_fp64_masks(gz, inp, gbeta, f"dL/dz[{name}]")
     r.close()
 
 
@@ -1038,6 +1077,7 @@ def test_mlp_backward_cfg3_full_frame(p2s):
     gb = gb.cpu().numpy()
     ref, alts = _dz_ref(inp, gb.astype(np.float64))
     _dz_check(gz.cpu().numpy(), ref, alts, "dL/dz[cfg3 chained]")
+    _dz_check_fp64_masks(gz.cpu().numpy(), inp, gb, "dL/dz[cfg3 chained]")
     # the chained call equals the standalone call on the same dL/dbeta
     gz2 = r.mlp_backward(_dev(inp.zernike), _dev(gb)).cpu().numpy()
     np.testing.assert_array_equal(gz.cpu().numpy(), gz2)
