@@ -111,7 +111,8 @@ def test_sass_adjoint_image_kernel(lib):
     ins = [l.split("*/", 1)[1].strip() for l in funcs[0].split("\n") if l.strip().startswith("/*") and "*/" in l
            and not l.strip().startswith("/* 0x")]
     mma = [n for n, l in enumerate(ins) if "UTCHMMA.2CTA" in l]
-    assert len(mma) == 2 and any("UTMALDG.4D" in l for l in ins) and any("UTMALDG.2D" in l for l in ins)
+    # U comes in as 64-column 128B-swizzled boxes (3-D map), the basis taps as a 2-D map
+    assert len(mma) == 2 and any("UTMALDG.3D" in l for l in ins) and any("UTMALDG.2D" in l for l in ins)
     region = ins[max(0, mma[0] - 40):mma[-1] + 20]
     for bad in ("BRA.DIV", "BRA.U.ANY", "R2UR.BROADCAST"):
         assert not any(bad in x for x in region), bad

@@ -1,5 +1,6 @@
 # scratch driver for one gpurun call (edited per call)
-timeout 300 python tools/adjoint_time.py 50 image; python tools/adjoint_time.py 50 all
-timeout 900 python -m pytest tests/test_gpu_parity.py tests/test_gpu_full_frames.py -m gpu -q -p no:cacheprovider -x -k "backward_parity or image_gradient or backward_cfg3 or adjoint_cfg3 or backward_color or two_handles or adjoint_chain or mlp_backward_parity or mlp_backward_cfg3" > gpurun_out/t7.log 2>&1; tail -3 gpurun_out/t7.log; grep -E "dL/dI|fp64 masks" gpurun_out/t7.log | head -30
-ncu --metrics gpu__time_duration.sum,lts__t_bytes.sum --clock-control none --csv --log-file gpurun_out/adj_launches.csv python tools/adjoint_time.py 3 image > /dev/null 2>&1
-grep k_adjoint_image gpurun_out/adj_launches.csv | tail -2
+mkdir -p gpurun_out
+timeout 1500 python -m pytest tests -m gpu -q -p no:cacheprovider -x > gpurun_out/gputest.log 2>&1; tail -3 gpurun_out/gputest.log
+timeout 300 python bench.py > gpurun_out/bench.log 2>gpurun_out/bench.err; tail -c 3000 gpurun_out/bench.log
+timeout 300 python bench.py --impl reference > gpurun_out/bench_ref.log 2>&1; tail -c 1500 gpurun_out/bench_ref.log
+timeout 120 python -c "import __graft_entry__ as g; g.smoke()" > gpurun_out/smoke.log 2>&1; tail -2 gpurun_out/smoke.log
