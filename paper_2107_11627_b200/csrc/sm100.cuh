@@ -182,6 +182,24 @@ P2S_DEV void umma_commit_elect(uint64_t* bar) {
       " @e tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];\n}" ::"r"(
           smem_u32(bar)) : "memory");
 }
+// A from TMEM: D[tmem] (+)= A[tmem] * B[smem]^T. A's 128 rows are TMEM lanes 0-127; one K-step
+// (16 fp16) occupies 8 columns from a_tmem, column c holding the pair (k = 2c, 2c + 1) as
+// {lo, hi} (verified on hardware: tools/tmem_a_probe.cu). Warp-collective like umma_f16_elect.
+P2S_DEV void umma_f16_tA_elect(uint32_t d_tmem, uint32_t a_tmem, uint64_t bdesc, uint32_t idesc,
+                               uint32_t accumulate) {
+  asm volatile(
+      "{\n .reg .pred e, p;\n elect.sync _|e, 0xffffffff;\n setp.ne.b32 p, %4, 0;\n"
+      " @e tcgen05.mma.cta_group::1.kind::f16 [%0], [%1], %2, %3, p;\n}" ::"r"(d_tmem),
+      "r"(a_tmem), "l"(bdesc), "r"(idesc), "r"(accumulate));
+}
+// 32 lanes x 8 consecutive 32-bit columns from registers (warp-collective; lane quadrant in taddr)
+P2S_DEV void tmem_st8(uint32_t taddr, uint32_t r0, uint32_t r1, uint32_t r2, uint32_t r3, uint32_t r4,
+                      uint32_t r5, uint32_t r6, uint32_t r7) {
+  asm volatile("tcgen05.st.sync.aligned.32x32b.x8.b32 [%0], {%1,%2,%3,%4,%5,%6,%7,%8};" ::"r"(taddr), "r"(r0),
+               "r"(r1), "r"(r2), "r"(r3), "r"(r4), "r"(r5), "r"(r6), "r"(r7)
+               : "memory");
+}
+P2S_DEV void tmem_st_wait() { asm volatile("tcgen05.wait::st.sync.aligned;" ::: "memory"); }
 // Arrive (once) on `bar` when all previously issued tcgen05.mma of this thread complete.
 P2S_DEV void umma_commit(uint64_t* bar) {
   asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];" ::"r"(
