@@ -201,15 +201,27 @@ def reference_arm(args, rank, world):
 
 class Timer:
     """CUDA-event timing of calls on the render stream, L2 flushed (256 MiB write) before each
-    call outside the events."""
+    call outside the events.
+
+    The B200 comes out of even a few milliseconds of idle (a host synchronize, host-side work)
+    at a lower effective speed and needs ~3-4 ms of back-to-back work to settle: the first ~15
+    cfg3 renders after a pause run 227 -> 175 us (measured, P2S_BENCH_DEBUG). So `pre` untimed
+    calls are enqueued right before the timed ones, with no host synchronisation in between."""
 
     def __init__(self, torch, stream, flush):
         self.torch, self.stream, self.flush = torch, stream, flush
 
-    def calls(self, fn, n, flush=True):
+    def warm(self, fn, pre, flush=True):
+        for i in range(pre):
+            if flush:
+                self.flush.fill_(float(i))
+            fn()
+
+    def calls(self, fn, n, flush=True, pre=3):
         ev0 = [self.torch.cuda.Event(enable_timing=True) for _ in range(n)]
         ev1 = [self.torch.cuda.Event(enable_timing=True) for _ in range(n)]
         self.torch.cuda.synchronize()
+        self.warm(fn, pre, flush)
         for i in range(n):
             if flush:
                 self.flush.fill_(float(i))
@@ -219,7 +231,7 @@ class Timer:
         self.torch.cuda.synchronize()
         return np.array([ev0[i].elapsed_time(ev1[i]) for i in range(n)])
 
-    def fused(self, r, fn, n):
+    def fused(self, r, fn, n, pre=16, defer=False):
         """The fused MLP+convolution kernel alone: the library records two events right around
         that launch on its stream (p2s_set_profile_events); an outer pair brackets the whole
         render. Events are created (first record) before the loop, so no lazy creation sits
@@ -230,6 +242,7 @@ class Timer:
             for e in e4:
                 e.record(self.stream)
         self.torch.cuda.synchronize()
+        self.warm(fn, pre)
         for i in range(n):
             self.flush.fill_(float(i))
             r.set_profile_events(ev[i][1], ev[i][2])
@@ -237,8 +250,13 @@ class Timer:
             fn()
             ev[i][3].record(self.stream)
         r.set_profile_events(None, None)
-        self.torch.cuda.synchronize()
-        return (np.array([e[1].elapsed_time(e[2]) for e in ev]), np.array([e[0].elapsed_time(e[3]) for e in ev]))
+
+        def result():
+            self.torch.cuda.synchronize()
+            return (np.array([e[1].elapsed_time(e[2]) for e in ev]), np.array([e[0].elapsed_time(e[3]) for e in ev]))
+        if defer:  # the caller keeps the GPU busy and reads the times later
+            return result
+        return result()
 
 
 def executed_macs_per_px(info, C):
@@ -323,16 +341,18 @@ def main():
     ev_s0 = [torch.cuda.Event(enable_timing=True) for _ in range(args.steps)]
     ev_s1 = [torch.cuda.Event(enable_timing=True) for _ in range(args.steps)]
 
-    for _ in range(args.warmup):
-        flush.fill_(1.0)
-        r.render(img, z, t, out=out)
+    r.render(img, z, t, out=out)  # first call (allocations, lazy init)
     torch.cuda.synchronize()
-    # the fused kernel alone (roofline): half of the dedicated loop before the timed steps, half
-    # after, so both halves bracket the same thermal/clock window as the steps
-    fused_pre, evstep_pre = tm.fused(r, lambda: r.render(img, z, t, out=out), N_FUSED // 2)
 
     with ClockSampler(torch.cuda.current_device()) as clk:
         t_all0 = time.time()
+        # the fused kernel alone (roofline): half of the dedicated loop (after its own pre-warm)
+        # before the timed steps, half after them
+        fused_pre_res = tm.fused(r, lambda: r.render(img, z, t, out=out), N_FUSED // 2, defer=True)
+        # W untimed warm-up steps, enqueued back to back right behind the fused loop's work
+        for _ in range(args.warmup):
+            flush.fill_(1.0)
+            r.render(img, z, t, out=out)
         # ---- the timed steps: one p2s_render per step (MLP + conv kernel, then the warp kernel as
         # its programmatic dependent), L2 flushed before each step outside the events
         if dist:
@@ -349,6 +369,7 @@ def main():
             dist.barrier()
         tr1 = time.time()
         step_ms = np.array([ev_s0[i].elapsed_time(ev_s1[i]) for i in range(args.steps)])
+        fused_pre, evstep_pre = fused_pre_res()
         tot_ms = pdist.max_over_ranks(float(step_ms.sum()), dist, dev)
         value = pdist.throughput(B, world, args.steps, tot_ms)
         ms_per_step = tot_ms / args.steps
@@ -356,6 +377,9 @@ def main():
         # ---- the fused kernel alone: the second half of the dedicated loop
         fused_post, evstep_post = tm.fused(r, lambda: r.render(img, z, t, out=out), N_FUSED - N_FUSED // 2)
         fused_ms = np.concatenate([fused_pre, fused_post])
+        if os.environ.get("P2S_BENCH_DEBUG"):
+            print("fused_pre", np.round(fused_pre * 1e3, 1).tolist(), "\nfused_post", np.round(fused_post * 1e3, 1).tolist(),
+                  "\nsteps", np.round(step_ms[:40] * 1e3, 1).tolist(), file=sys.stderr)
         evstep_ms = np.concatenate([evstep_pre, evstep_post])
 
         # ---- e2e: same metric through p2s_render_host (pinned host buffers, copies inside the step)
@@ -391,8 +415,8 @@ def main():
                 for _ in range(3):
                     fn()
                 n = 100 if cid == 2 else 20
-                c_ms = tm.calls(fn, n)
-                cf_ms, _ = tm.fused(cr, fn, max(30, n // 2))
+                c_ms = tm.calls(fn, n, pre=40 if cid == 2 else 3)
+                cf_ms, _ = tm.fused(cr, fn, max(30, n // 2), pre=60 if cid == 2 else 3)
                 cv = pdist.throughput(1, world, n, pdist.max_over_ranks(float(c_ms.sum()), dist, dev))
                 configs[cs.name] = {
                     "value": cv, "unit": "frames/s", "mpix_per_s": cv * cs.H * cs.W / 1e6,
@@ -422,7 +446,7 @@ def main():
                 fn()
             n_b = 10
             b_ms = tm.calls(fn, n_b, flush=False)
-            fb_ms, _ = tm.fused(r, fn, 10)
+            fb_ms, _ = tm.fused(r, fn, 10, pre=2)
             rl = roofline_entry(spec, info, fb_ms, peak, peak_src, frames=nb)
             rl["frac_sustained"] = rl["achieved"] / peak_sust if peak_sust else None
             rl["note"] = ("frac against the burst peak (a ~2.6 ms launch is a short kernel); frac_sustained "
@@ -446,7 +470,7 @@ def main():
             fn = lambda: r.render_sequence(simg, sz, st_, out=sout)  # noqa: E731  50 x 35 MB: > L2
             for _ in range(2):
                 fn()
-            s_ms = tm.calls(fn, 5, flush=False)
+            s_ms = tm.calls(fn, 5, flush=False, pre=2)
             sequence_mode = {"frames_per_sequence": F, "value": pdist.throughput(F, world, 5, pdist.max_over_ranks(
                 float(s_ms.sum()), dist, dev)), "unit": "frames/s", "calls": 5, "api": "p2s_render_sequence",
                 "note": "50 frames of one 512x512 RGB image (per-frame Zernike/tilt); the K convolutions "
@@ -468,13 +492,13 @@ def main():
                                                                     want_image=wi, want_zernike=wz))
                 for _ in range(3):
                     fn()
-                a_ms = tm.calls(fn, 20)
+                a_ms = tm.calls(fn, 20, pre=8)
                 res[key] = pdist.throughput(1, world, 20, pdist.max_over_ranks(float(a_ms.sum()), dist, dev))
             aanc = torch.from_numpy(synth.make_anchors(spec, 16, frames=pdist.rank_frames(rank, 1))).to(dev)
             fn = lambda: r.backward_anchors(aimg, aanc, at, ag)  # noqa: E731
             for _ in range(3):
                 fn()
-            a_ms = tm.calls(fn, 20)
+            a_ms = tm.calls(fn, 20, pre=8)
             res["anchor_chain"] = pdist.throughput(1, world, 20, pdist.max_over_ranks(float(a_ms.sum()), dist, dev))
             adjoint_mode = dict(res, unit="frames/s", api="p2s_backward + p2s_mlp_backward",
                                 note="value: dL/dbeta [K,H,W] + dL/dt [2,H,W] of one cfg3 frame (L2 flushed per "
@@ -490,7 +514,7 @@ def main():
             fn = lambda: r.render_color(img, cz, t, out=out)  # noqa: E731
             for _ in range(3):
                 fn()
-            c_ms = tm.calls(fn, 20)
+            c_ms = tm.calls(fn, 20, pre=10)
             cg = torch.from_numpy(synth.make_upstream_grad(spec, frames=pdist.rank_frames(rank, 1))).to(dev)
             fa = lambda: r.backward_color(img, cz, t, cg, want_image=True, want_zernike=True)  # noqa: E731
             for _ in range(2):
@@ -513,12 +537,12 @@ def main():
             fn = lambda: r.render_anchors(img, anc, t, out=out)  # noqa: E731
             for _ in range(3):
                 fn()
-            a_ms = tm.calls(fn, 50)
+            a_ms = tm.calls(fn, 50, pre=20)
             smp = p2s.Sampler(G, spec.n_in, 2.0)
             fs = lambda: (smp.sample(1000 + rank, 0, 1, out=anc), r.render_anchors(img, anc, t, out=out))  # noqa
             for _ in range(2):
                 fs()
-            sa_ms = tm.calls(fs, 50)
+            sa_ms = tm.calls(fs, 50, pre=20)
             smp.close()
             # NEXT-3 with a dense pre-computed 4096 x 4096 correlation (G = 64, the
             # non-separable exponential stand-in): 50 frames per call on the tensor cores, and the
@@ -534,7 +558,7 @@ def main():
             fdr = lambda: (dsmp.sample(7 + rank, 0, 1, out=d1), r.render_anchors(img, d1, t, out=out))  # noqa: E731
             for _ in range(2):
                 fdr()
-            dr_ms = tm.calls(fdr, 20)
+            dr_ms = tm.calls(fdr, 20, pre=20)
             GG2 = GD * GD
             dflops = 2.0 * GG2 * (GG2 + 1) / 2 * FD * spec.n_in  # L's lower triangle x (frame, mode) columns
             dense_sampler = {

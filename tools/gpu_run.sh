@@ -1,1 +1,1 @@
-P2S_LIB=paper_2107_11627_b200/abl_mbprof.so python tools/dz_trace.py
+P2S_BENCH_DEBUG=1 python bench.py --steps 20 --warmup 3 --no-cpu-baseline --no-extra 2>&1 | tail -4 | cut -c1-600

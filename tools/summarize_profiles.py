@@ -71,8 +71,19 @@ with open(os.path.join(PROF, f"{tag}_ncu_fused.txt"), "w") as f:
     f.write("ncu --set full --clock-control none -k regex:k_fused -s 1 -c 1 (cfg3, one frame)\n\n")
     f.write("\n".join(lines) + "\n")
     f.write(f"\nDRAM bytes per launch (read+write): {dram:.0f}\n")
+def num(k):
+    return float(m[k][0].replace(",", "")) if k in m else None
+
+
+clk = num("sm__cycles_elapsed.avg.per_second")  # the capture's own clock record (GHz)
 json.dump({"dram_bytes_per_launch": dram, "source": f"profiles/{tag}_ncu_fused.txt",
-           "kernel": "k_fused_p2s", "workload": "cfg3_512_rgb_K100_S33"},
+           "kernel": "k_fused_p2s", "workload": "cfg3_512_rgb_K100_S33",
+           "tensor_pipe_active_pct": num("sm__pipe_tensor_cycles_active.avg.pct_of_peak_sustained_elapsed"),
+           "tc_smem_pipe_pct": num("l1tex__data_pipe_tc_wavefronts_mem_shared.sum.pct_of_peak_sustained_elapsed"),
+           "sm_clock_ghz": clk, "gpu_time_us": num("gpu__time_duration.sum"),
+           "note": "ncu --set full --clock-control none (replayed ~40x); sm_clock_ghz = sm__cycles_elapsed."
+                   "avg.per_second of the capture: the tensor-pipe % is a fraction of elapsed cycles at that "
+                   "clock, the duration is not comparable to bench timings at a different clock"},
           open(os.path.join(PROF, "ncu_fused_summary.json"), "w"), indent=1)
 print(open(os.path.join(PROF, f"{tag}_launch_shares.txt")).read())
 print("\n".join(lines))
