@@ -51,29 +51,62 @@ def _peaks():
 
 
 class ClockSampler:
-    """nvidia-smi clocks/throttle reasons sampled every 20 ms (B200_PROFILING.md).
-
-    Samples are kept with host timestamps; `summary(t0, t1)` summarises a window (the main
-    timed region, or every leg of the run)."""
+    """SM clocks, power and clock-event (throttle) reasons sampled every ~2 ms during the run
+    (NVML, the library nvidia-smi reads; B200_PROFILING.md's clocks line), with host timestamps;
+    `summary(t0, t1)` summarises a window (the main timed region, or every leg of the run).
+    Falls back to `nvidia-smi -lms 20` when NVML is unavailable."""
 
     Q = ("timestamp,index,clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
          "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
          "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+    NAMES = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
 
-    def __init__(self, gpu_index: int):
-        self.idx = gpu_index
+    def __init__(self, gpu_index: int, pci_bus_id: str | None = None, period_s: float = 0.002):
+        self.idx, self.pci, self.period = gpu_index, pci_bus_id, period_s
         self.proc = None
-        self.lines = []
+        self.nvml = None
+        self.stop = threading.Event()
+        self.samples = []  # (host time, sm MHz, max sm MHz, power W, set of reason names)
+        self.source = None
 
     def __enter__(self):
         try:
+            import pynvml as nv
+            nv.nvmlInit()
+            h = nv.nvmlDeviceGetHandleByPciBusId(self.pci) if self.pci else nv.nvmlDeviceGetHandleByIndex(self.idx)
+            bits = {"hw_slowdown": nv.nvmlClocksEventReasonHwSlowdown,
+                    "hw_thermal_slowdown": nv.nvmlClocksEventReasonHwThermalSlowdown,
+                    "sw_thermal_slowdown": nv.nvmlClocksEventReasonSwThermalSlowdown,
+                    "sw_power_cap": nv.nvmlClocksEventReasonSwPowerCap}
+            mx = nv.nvmlDeviceGetMaxClockInfo(h, nv.NVML_CLOCK_SM)
+
+            def poll():
+                while not self.stop.is_set():
+                    try:
+                        sm = nv.nvmlDeviceGetClockInfo(h, nv.NVML_CLOCK_SM)
+                        pw = nv.nvmlDeviceGetPowerUsage(h) / 1e3
+                        rs = nv.nvmlDeviceGetCurrentClocksEventReasons(h)
+                        self.samples.append((time.time(), float(sm), float(mx), pw,
+                                             {n for n, b in bits.items() if rs & b}))
+                    except Exception:
+                        pass
+                    time.sleep(self.period)
+            self.nvml = nv
+            self.t = threading.Thread(target=poll, daemon=True)
+            self.t.start()
+            self.source = f"NVML every {self.period * 1e3:.0f} ms"
+            return self
+        except Exception:
+            self.nvml = None
+        try:  # fallback: nvidia-smi every 20 ms
             self.proc = subprocess.Popen(["nvidia-smi", "-i", str(self.idx), f"--query-gpu={self.Q}",
                                           "--format=csv,noheader,nounits", "-lms", "20"],
                                          stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
             self.t = threading.Thread(target=self._read, daemon=True)
             self.t.start()
+            self.source = "nvidia-smi -lms 20"
             deadline = time.time() + 5
-            while not self.lines and time.time() < deadline:
+            while not self.samples and time.time() < deadline:
                 time.sleep(0.02)
         except Exception:
             self.proc = None
@@ -81,9 +114,23 @@ class ClockSampler:
 
     def _read(self):
         for line in self.proc.stdout:
-            self.lines.append((time.time(), line.strip()))
+            f = [x.strip() for x in line.strip().split(",")]
+            if len(f) < 10:
+                continue
+            try:
+                self.samples.append((time.time(), float(f[2]), float(f[3]), float(f[4]),
+                                     {n for n, v in zip(self.NAMES, f[6:10]) if v.lower().startswith("active")}))
+            except ValueError:
+                continue
 
     def __exit__(self, *a):
+        self.stop.set()
+        if self.nvml is not None:
+            self.t.join(timeout=1)
+            try:
+                self.nvml.nvmlShutdown()
+            except Exception:
+                pass
         if self.proc:
             time.sleep(0.1)
             self.proc.terminate()
@@ -94,26 +141,19 @@ class ClockSampler:
 
     def summary(self, t0=None, t1=None):
         sm, pw, mx, reasons = [], [], None, set()
-        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
-        for ts, ln in list(self.lines):
-            if t0 is not None and not (t0 - 0.025 <= ts <= (t1 if t1 is not None else ts) + 0.025):
+        for ts, c, m, p, rs in list(self.samples):
+            if t0 is not None and not (t0 - 0.002 <= ts <= (t1 if t1 is not None else ts) + 0.002):
                 continue
-            f = [x.strip() for x in ln.split(",")]
-            if len(f) < 10:
-                continue
-            try:
-                sm.append(float(f[2]))
-                mx = float(f[3])
-                pw.append(float(f[4]))
-            except ValueError:
-                continue
-            for n, v in zip(names, f[6:10]):
-                if v.lower().startswith("active"):
-                    reasons.add(n)
+            sm.append(c)
+            mx = m
+            pw.append(p)
+            reasons |= rs
         if not sm:
-            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["unavailable"], "samples": 0}
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["unavailable"], "samples": 0,
+                    "source": self.source}
         return {"sm_mhz": float(np.median(sm)), "sm_min_mhz": float(min(sm)), "sm_max_mhz": mx,
-                "reasons": sorted(reasons), "samples": len(sm), "power_w_max": max(pw) if pw else None}
+                "reasons": sorted(reasons), "samples": len(sm), "power_w_max": max(pw) if pw else None,
+                "source": self.source}
 
 
 def lscpu_model():
@@ -344,7 +384,10 @@ def main():
     r.render(img, z, t, out=out)  # first call (allocations, lazy init)
     torch.cuda.synchronize()
 
-    with ClockSampler(torch.cuda.current_device()) as clk:
+    props = torch.cuda.get_device_properties(dev)
+    pci = (f"{props.pci_domain_id:08x}:{props.pci_bus_id:02x}:{props.pci_device_id:02x}.0"
+           if hasattr(props, "pci_bus_id") else None)
+    with ClockSampler(torch.cuda.current_device(), pci) as clk:
         t_all0 = time.time()
         # the fused kernel alone (roofline): half of the dedicated loop (after its own pre-warm)
         # before the timed steps, half after them
