@@ -1,1 +1,1 @@
-python bench.py --steps 20 --warmup 3 --no-cpu-baseline --no-extra 2>&1 | tail -1 | python -c "import json,sys; d=json.loads(sys.stdin.read()); print(d['value'], d['ms_per_step'], d['roofline']['frac'], d['roofline']['fused_le_step']); print(d['clocks'])"
+./tools/mlp_umma_probe
