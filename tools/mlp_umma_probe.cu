@@ -14,9 +14,11 @@ using namespace p2s;
 
 #define CK(x) do { cudaError_t e = (x); if (e != cudaSuccess) { printf("CUDA %s @%d: %s\n", #x, __LINE__, cudaGetErrorString(e)); exit(1);} } while (0)
 
-// mode 0: idle; 1: 8 warps tcgen05.ld columns [256, 512); 2: 8 warps st.shared into a scratch area
+// mode 0: idle; 1: 8 warps tcgen05.ld columns [256, 512); 2: 8 warps st.shared into a scratch area;
+// 3/4: warp 1 streams global -> shared bulk copies into a scratch area while the UMMAs run (3: 1.8 KB
+// copies, the fused kernel's per-slab TMA boxes; 4: 19.7 KB copies, one per ring stage)
 __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(288, 1)
-    k_mlp(int N, int n, int mode, unsigned long long* cyc) {
+    k_mlp(int N, int n, int mode, unsigned long long* cyc, const uint8_t* src) {
   extern __shared__ __align__(1024) uint8_t smem[];
   __shared__ uint64_t bar;
   __shared__ uint32_t tslot;
@@ -53,7 +55,27 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(288, 1)
     }
     __syncwarp();
     if (lane_id() == 0) done = 1;
-  } else if (warp >= 1 && mode != 0) {
+  } else if (warp == 1 && mode >= 3) {
+    // bulk copies, up to 3 in flight (a 3-stage ring), into [160 KB, 200 KB)
+    __shared__ uint64_t cb[3];
+    if (lane_id() == 0) {
+      for (int i = 0; i < 3; ++i) mbar_init(&cb[i], 1);
+      fence_mbar_init();
+      const uint32_t bytes = mode == 3 ? 1792u : 19712u;
+      uint32_t ph[3] = {0, 0, 0};
+      int it = 0;
+      while (!done && it < 200000) {
+        const int s = it % 3;
+        if (it >= 3) { mbar_wait(&cb[s], ph[s]); ph[s] ^= 1u; }
+        mbar_arrive_expect_tx(&cb[s], bytes);
+        bulk_g2s(smem + 160 * 1024 + (mode == 3 ? s * 2048 : 0), src + (size_t)(it % 64) * 32768, bytes, &cb[s]);
+        ++it;
+      }
+      for (int s = 0; s < 3 && it >= 3; ++s) { mbar_wait(&cb[(it + s) % 3], ph[(it + s) % 3]); }
+      cyc[1] = it;
+    }
+    __syncwarp();
+  } else if (warp >= 1 && mode != 0 && mode < 3) {
     const uint32_t tq = tmem + ((uint32_t)(32 * (warp & 3)) << 16);
     uint32_t acc = 0;
     int it = 0;
@@ -81,13 +103,16 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(288, 1)
 int main() {
   unsigned long long* d;
   CK(cudaMalloc(&d, 16));
+  uint8_t* src;
+  CK(cudaMalloc(&src, 64 * 32768 + 65536));
+  CK(cudaMemset(src, 0, 64 * 32768 + 65536));
   CK(cudaFuncSetAttribute(k_mlp, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024));
-  const char* names[] = {"idle", "8 warps tcgen05.ld", "8 warps st.shared"};
-  for (int mode = 0; mode < 3; ++mode)
+  const char* names[] = {"idle", "8 warps tcgen05.ld", "8 warps st.shared", "bulk 1.8 KB copies", "bulk 19.7 KB copies"};
+  for (int mode = 0; mode < 5; ++mode)
     for (int N : {48, 80, 112, 128, 208, 256}) {
       unsigned long long c = 0;
       for (int rep = 0; rep < 3; ++rep) {
-        k_mlp<<<2, 288, 200 * 1024>>>(N, 390, mode, d);
+        k_mlp<<<2, 288, 200 * 1024>>>(N, 390, mode, d, src);
         CK(cudaDeviceSynchronize());
       }
       CK(cudaMemcpy(&c, d, 8, cudaMemcpyDeviceToHost));
