@@ -391,7 +391,12 @@ def main():
         t_all0 = time.time()
         # the fused kernel alone (roofline): half of the dedicated loop (after its own pre-warm)
         # before the timed steps, half after them
-        fused_pre_res = tm.fused(r, lambda: r.render(img, z, t, out=out), N_FUSED // 2, defer=True)
+        # the dedicated loop runs the fused kernel alone (p2s_debug_blur: the same launch writing J
+        # to a caller buffer, no warp kernel after it), the library's events right around it
+        Jbuf = torch.empty_like(img)
+        fused_fn = ((lambda: r.render(img, z, t, out=out)) if os.environ.get("P2S_FUSED_LOOP") == "render"
+                    else (lambda: r.debug_blur(img, z, out=Jbuf)))
+        fused_pre_res = tm.fused(r, fused_fn, N_FUSED // 2, defer=True)
         # W untimed warm-up steps, enqueued back to back right behind the fused loop's work
         for _ in range(args.warmup):
             flush.fill_(1.0)
@@ -418,7 +423,7 @@ def main():
         ms_per_step = tot_ms / args.steps
 
         # ---- the fused kernel alone: the second half of the dedicated loop
-        fused_post, evstep_post = tm.fused(r, lambda: r.render(img, z, t, out=out), N_FUSED - N_FUSED // 2)
+        fused_post, evstep_post = tm.fused(r, fused_fn, N_FUSED - N_FUSED // 2)
         fused_ms = np.concatenate([fused_pre, fused_post])
         if os.environ.get("P2S_BENCH_DEBUG"):
             print("fused_pre", np.round(fused_pre * 1e3, 1).tolist(), "\nfused_post", np.round(fused_post * 1e3, 1).tolist(),
@@ -670,10 +675,10 @@ def main():
             ncu = None
     roof = roofline_entry(spec, info, fused_ms, peak, peak_src, traffic=traffic)
     roof["fused_le_step"] = bool(roof["fused_ms_median"] <= ms_per_step)
-    roof["fused_timing"] = (f"dedicated loop of {N_FUSED} renders, half before and half after the timed steps, L2 "
-                            "flushed before each; CUDA events recorded by the library right around the fused "
-                            "launch on its stream (an event between the fused and the warp kernel stops the "
-                            "warp's programmatic launch, so these renders are not timed steps)")
+    roof["fused_timing"] = (f"dedicated loop of {N_FUSED} launches of the fused kernel alone (p2s_debug_blur: the same "
+                            "kernel, J to a caller buffer, no warp kernel after it), half before and half after "
+                            "the timed steps, each behind an L2 flush and a pre-warm; CUDA events recorded by "
+                            "the library right around the launch on its stream")
     roof["evented_render_ms_median"] = float(np.median(evstep_ms))
     roof["fused_share_of_evented_render"] = float(np.median(fused_ms) / np.median(evstep_ms))
     roof["whole_render_frac"] = flops_frame * B / (ms_per_step / 1e3) / 1e12 / peak
