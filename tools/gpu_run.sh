@@ -1,6 +1,2 @@
-for i in 1 2 3; do
-for m in blur render; do
-P2S_FUSED_LOOP=$m python bench.py --no-cpu-baseline 2>&1 | tail -1 | python -c "
-import json,sys; d=json.loads(sys.stdin.read()); r=d['roofline']; print('$m', 'step', round(d['ms_per_step']*1e3,1), 'fused', round(r['fused_ms_median']*1e3,1), 'min', round(r['fused_ms_min']*1e3,1), 'max', round(r['fused_ms_max']*1e3,1), 'evented', round(r['evented_render_ms_median']*1e3,1), d['clocks']['all_legs']['reasons'])"
-done
-done
+timeout 600 python -m pytest tests/test_gpu_parity.py -m gpu -q -p no:cacheprovider -x -k "sampl or dense" 2>&1 | tail -2
+ncu --metrics gpu__time_duration.sum --clock-control none -k regex:"k_draw_y|k_sample_dense" --csv python tools/draw_run.py 2>/dev/null | grep -E "k_draw_y|k_sample_dense" | tail -2 | awk -F'","' '{print $5, $NF}'
