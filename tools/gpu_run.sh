@@ -1,2 +1,4 @@
-timeout 600 python -m pytest tests/test_gpu_parity.py -m gpu -q -p no:cacheprovider -x -k "sampl or dense" 2>&1 | tail -2
-ncu --metrics gpu__time_duration.sum --clock-control none -k regex:"k_draw_y|k_sample_dense" --csv python tools/draw_run.py 2>/dev/null | grep -E "k_draw_y|k_sample_dense" | tail -2 | awk -F'","' '{print $5, $NF}'
+mkdir -p gpurun_out
+timeout 900 compute-sanitizer --tool memcheck --error-exitcode 9 python tools/sanitize_small.py > gpurun_out/san_memcheck.log 2>&1; echo "memcheck rc=$?"; tail -3 gpurun_out/san_memcheck.log
+timeout 900 compute-sanitizer --tool racecheck --error-exitcode 9 python tools/sanitize_small.py > gpurun_out/san_racecheck.log 2>&1; echo "racecheck rc=$?"; tail -3 gpurun_out/san_racecheck.log
+timeout 900 compute-sanitizer --tool synccheck --error-exitcode 9 python tools/sanitize_small.py > gpurun_out/san_synccheck.log 2>&1; echo "synccheck rc=$?"; tail -3 gpurun_out/san_synccheck.log
