@@ -1435,7 +1435,7 @@ p2s_status p2s_render_anchors_host(p2s_handle* h, const float* image_host, int B
 
 p2s_status p2s_debug_profile_buffer(p2s_handle* h, void* device_counters) {
   if (!h) return P2S_ERR_INVALID_ARG;
-#ifdef P2S_PROFILE
+#if defined(P2S_PROFILE) || defined(P2S_STARTUP_PROF)
   h->prof = (unsigned long long*)device_counters;
   return P2S_OK;
 #else

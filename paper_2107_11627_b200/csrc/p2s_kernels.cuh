@@ -161,6 +161,14 @@ struct FusedParams {
 #else
 #define WAIT_PROD(bar, par) mbar_wait(bar, par)
 #endif
+// P2S_STARTUP_PROF builds (tools/startup_trace.py): globaltimer stamps of CTA 0's launch phases
+#ifdef P2S_STARTUP_PROF
+#define STAMP(i) do { if (p.prof && blockIdx.x == 0) p.prof[(i)] = globaltimer_ns(); } while (0)
+#define STAMP_CTA(base) do { if (p.prof) p.prof[(base) + blockIdx.x] = globaltimer_ns(); } while (0)
+#else
+#define STAMP(i) do {} while (0)
+#define STAMP_CTA(base) do {} while (0)
+#endif
 #ifdef P2S_PROFILE
 #define PROF_T0() const long long _pt0 = clock64()
 #define PROF_ADD(slot) prof_acc[slot] += (unsigned long long)(clock64() - _pt0)
@@ -641,6 +649,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads)
   prof_acc[10] = globaltimer_ns();
 #endif
 
+  if (threadIdx.x == 0) { STAMP(0); STAMP_CTA(16); }
   // ---- setup: the item, step and constant tables -> shared memory as 4-byte async copies, all
   // in flight at once (dependent load/store loops cost one global round trip per table)
   {
@@ -663,6 +672,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads)
     for (int i = threadIdx.x; i < n_const; i += kThreads) cp_async4(sConst + i, p.consts + i);
     cp_async_wait_all();
   }
+  if (threadIdx.x == 0) STAMP(1);
   if (threadIdx.x == 0) {
     mbar_init(&bars[BAR_A1_FULL], 2 * kNumBuildWarps);
     mbar_init(&bars[BAR_A1_EMPTY], 1);
@@ -684,6 +694,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads)
   tc_fence_before();
   __syncthreads();
   cluster_sync();  // both CTAs' barriers are initialised before any remote arrive
+  if (threadIdx.x == 0) STAMP(2);
   tc_fence_after();
   const uint32_t tmem = *tmem_slot;
 
@@ -738,6 +749,9 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads)
 #endif
     const int ntl = pr_end - pr_begin;
     const int total = ntl > 0 ? nA + (ntl - 1) * nB + ntl * (nfr - 1) * nS : 0;
+#ifdef P2S_STARTUP_PROF
+    bool stamped_conv = false;
+#endif
     MmaItem cur = sMma[0];
     for (int step = 0, it = 0, fr = 0, g = 0; step < total; ++step) {
       const int n_items = seg_len(it, fr);
@@ -762,6 +776,10 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads)
       { PROF_T0(); mbar_wait(&ring_full[s], ph); PROF_ADD(5); }
 #endif
       tc_fence_after();
+#ifdef P2S_STARTUP_PROF
+      if (lane == 0 && step == 0) STAMP(5);
+      if (lane == 0 && (f & MI_CONV) && !stamped_conv) { STAMP(6); stamped_conv = true; }
+#endif
 #ifdef P2S_PROFILE
       const long long tr_b = clock64();
 #endif
@@ -846,6 +864,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads)
       }
     }
     if (pending >= 0) umma2_commit_elect(&ring_empty[pending]);
+    if (lane == 0) STAMP(10);
   } else if (builder_index(warp) >= 0) {
     // ================= builders: A1 (Zernike tile, fp16) and E views (fp16, centred) =====
     const int tid = builder_index(warp) * 32 + lane;
@@ -884,6 +903,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads)
         fence_proxy_async_smem();
         __syncwarp();
         if (lane == 0) mbar_arrive_remote(&bars[BAR_A1_FULL], 0);
+        if (lane == 0 && builder_index(warp) == 0 && a1_builds == 1) STAMP(3);
       }
       if (pmode == 1 || fr > 0) continue;  // E views: once per tile (every frame shares the image)
       // --- E views of every channel (the CTA's first tile: built by the idle epilogue warps)
@@ -921,6 +941,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads)
       fence_proxy_async_smem();
       named_bar_sync(2, 32 * kNumEpiWarps);
       if (warp - kWarpEpi0 < kNumBuildWarps && lane == 0) mbar_arrive_remote(&bars[BAR_E_FULL0], 0);
+      if (warp == kWarpEpi0 && lane == 0) STAMP(4);
     }
     const int ew = warp - kWarpEpi0;        // 0..7
     const int wg = ew >> 2;                 // warpgroup 0 / 1
@@ -1016,6 +1037,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads)
       }
       { PROF_T0(); WAIT_EPI(&bars[BAR_ACC_FULL], acc_waits & 1); PROF_ADD(15); }
       ++acc_waits;
+      if (acc_waits == 1 && warp == kWarpEpi0 && lane == 0) STAMP(7);
       tc_fence_after();
 #ifdef P2S_PROFILE
       const long long te0 = clock64();
@@ -1098,6 +1120,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads)
         tc_fence_before();
         __syncwarp();
         if (lane == 0) mbar_arrive_remote(&bars[fr == nfr - 1 ? BAR_TMEM_FREE : BAR_SCR_FREE], 0);
+        if (acc_waits == 1 && warp == kWarpEpi0 && lane == 0) STAMP(8);
 #ifdef P2S_PROFILE
         prof_acc[16] += (unsigned long long)(clock64() - te0);
 #endif
@@ -1125,6 +1148,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads)
         if (lane == 0) mbar_arrive_remote(&bars[BAR_TMEM_FREE], 0);
       }
     }
+    if (warp == kWarpEpi0 && lane == 0) STAMP(9);
   }
 #ifdef P2S_PROFILE
   {
@@ -1148,6 +1172,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads)
   __syncthreads();
   cluster_sync();
   tc_fence_after();
+  if (threadIdx.x == 0) STAMP_CTA(16 + 160);
   if (warp == kWarpMma) tmem_dealloc2<kTmemCols>(tmem);
 }
 
