@@ -455,7 +455,11 @@ __device__ __forceinline__ void adj_u_epi(uint32_t tl, int scr_col, int Nk, int 
 #pragma unroll
       for (int c = 0; c < NC; ++c) jc[c] = fmaf(bv[i], av[c][i], jc[c]);
     }
+#ifdef P2S_ABL_NOUSTORE
+    if (st && u && gj[0] == 12345.f) {  // timing-only ablation: no U stores
+#else
     if (st && u) {
+#endif
 #pragma unroll
       for (int i = 0; i < 16; ++i) {
         const int k = gi * 16 + i;
