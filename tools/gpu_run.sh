@@ -1,1 +1,3 @@
-python tools/pdl_probe.py
+mkdir -p gpurun_out
+bash tools/ncu_adjoint_run.sh
+bash tools/ncu_dz_run.sh

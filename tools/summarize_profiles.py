@@ -100,9 +100,9 @@ if os.path.exists(adj_csv) and os.path.exists(adj_rep):
     ki, vi = hdr.index("Kernel Name"), hdr.index("Metric Value")
     seq = [(r[ki].split("(")[0], float(r[vi].replace(",", ""))) for r in rows[start + 1:]]
     # the last p2s_backward call of the run (warm-up calls precede it): its kernels in order
-    roles = ["(dL/dJ scatter)", "(MLP + convolutions -> J, dL/dbeta, U = beta dL/dJ)", "(dL/dt)", "(dL/dI)",
-             "(dL/dz)"]
-    last = seq[-5:]  # dL/dJ scatter, fused pass (J, dL/dbeta, U), dL/dt, k_adjoint_image, k_mlp_backward
+    roles = ["(dL/dJ scatter)", "(max |dL/dJ| per plane: U's fp16 range scale)",
+             "(MLP + convolutions -> J, dL/dbeta, U = beta dL/dJ)", "(dL/dt)", "(dL/dI)", "(dL/dz)"]
+    last = seq[-6:]  # scatter, absmax, fused pass (J, dL/dbeta, U), dL/dt, k_adjoint_image, k_mlp_backward
     raw = subprocess.run(["ncu", "-i", adj_rep, "--page", "raw", "--csv"], capture_output=True, text=True).stdout
     rr = list(csv.reader(raw.splitlines()))
     m = {a: (c, b) for a, b, c in zip(rr[0], rr[1], rr[2])}
@@ -115,10 +115,36 @@ if os.path.exists(adj_csv) and os.path.exists(adj_rep):
                 "gpu__time_duration.sum --clock-control none (cold-cache, serialised); last call's launches "
                 "(tools/adjoint_time.py 1 all4; full list in " + f"{tag}_adjoint_launches.csv):\n")
         for (name, ns), role in zip(last, roles):
-            f.write(f"  {ns / 1e3:9.1f} us  {name.removeprefix('void '):24s} {role}\n")
+            f.write(f"  {ns / 1e3:9.1f} us  {name.removeprefix('void ').split('(')[0].removeprefix('<unnamed>::'):24s} {role}\n")
         f.write("\nncu --set full --clock-control none -k regex:k_adjoint_image -c 1 (dL/dI of one cfg3 frame)\n\n")
         for k in want:
             if k in m:
                 f.write(f"{k:80s} {m[k][0]:>16s} {m[k][1]}\n")
     shutil.copy(adj_csv, os.path.join(PROF, f"{tag}_adjoint_launches.csv"))
     print(open(os.path.join(PROF, f"{tag}_ncu_adjoint.txt")).read())
+
+# ---- dL/dz (tools/ncu_dz_run.sh): the resident and the streamed variant, one --set full capture each
+dz = [(os.path.join(OUT, "prof_dz_res.ncu-rep"), "resident variant k_mlp_backward<1> (the default on cfg1-4 MLPs)"),
+      (os.path.join(OUT, "prof_dz_str.ncu-rep"), "streamed variant k_mlp_backward_s<1> (the default for 33-256-256-100)")]
+if all(os.path.exists(f) for f, _ in dz):
+    want = ["gpu__time_duration.sum", "sm__cycles_elapsed.avg.per_second", "dram__bytes_read.sum",
+            "dram__bytes_write.sum", "sm__pipe_tensor_cycles_active.avg.pct_of_peak_sustained_active",
+            "smsp__issue_active.avg.pct_of_peak_sustained_active", "smsp__inst_executed.sum",
+            "lts__throughput.avg.pct_of_peak_sustained_elapsed", "launch__grid_size", "launch__block_size",
+            "launch__registers_per_thread", "launch__shared_mem_per_block_dynamic"]
+    with open(os.path.join(PROF, f"{tag}_ncu_mlp_backward.txt"), "w") as f:
+        f.write("dL/dz (p2s_mlp_backward): ncu --set full --clock-control none --import-source on, one launch each "
+                "(tools/ncu_dz_run.sh; the first on a cfg3 frame, the second the streamed variant forced on the "
+                "same frame's inputs after P2S_MB_MODE handling in tools/dz_time.py)\n")
+        for rep, title in dz:
+            raw = subprocess.run(["ncu", "-i", rep, "--page", "raw", "--csv"], capture_output=True, text=True).stdout
+            rr = list(csv.reader(raw.splitlines()))
+            m = {a: (c, b) for a, b, c in zip(rr[0], rr[1], rr[2])}
+            f.write(f"\n{title}\n")
+            for k in want:
+                if k in m:
+                    f.write(f"  {k:80s} {m[k][0]:>16s} {m[k][1]}\n")
+        if os.path.exists(os.path.join(OUT, "dz_time.log")):
+            f.write("\nTiming without ncu (tools/dz_time.py, CUDA events, median of 20): " +
+                    open(os.path.join(OUT, "dz_time.log")).read().strip().splitlines()[-1] + "\n")
+    print(open(os.path.join(PROF, f"{tag}_ncu_mlp_backward.txt")).read())
