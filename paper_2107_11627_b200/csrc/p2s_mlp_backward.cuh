@@ -124,16 +124,27 @@ P2S_DEV void publish() {
 // this thread's z values of tile t (chunks 4i + q of 8 channels). Loads clamp the pixel into the
 // frame (a ragged tile's extra rows are never stored) and address channels by 32-bit offsets
 // from the frame base (host: (n_in + 2) HW, K HW < 2^31).
+// 8 channels (nvalid real, the rest 0) of one pixel, `stride` floats apart, by a running pointer
+// (the drains are issue-bound: per-load offset products and bound checks cost ~2 instructions
+// each over the whole tile; full chunks take the unpredicated path)
+P2S_DEV void load8(const float* ptr, size_t stride, int nvalid, float (&v)[8]) {
+  if (nvalid >= 8) {
+#pragma unroll
+    for (int j = 0; j < 8; ++j, ptr += stride) v[j] = __ldcs(ptr);
+  } else {
+#pragma unroll
+    for (int j = 0; j < 8; ++j, ptr += stride) v[j] = j < nvalid ? __ldcs(ptr) : 0.f;
+  }
+}
 P2S_DEV void load_z(const MlpbParams& p, int t, int m, int q, float (&zv)[2][8]) {
   const int b = t / p.tiles_per_frame;
   const int px = min((t - b * p.tiles_per_frame) * 128 + m, p.HW - 1);
-  const float* zb = p.z + (size_t)b * p.n_in * (size_t)p.HW + px;
+  const size_t HW = (size_t)p.HW;
+  const float* zb = p.z + (size_t)b * p.n_in * HW + px;
 #pragma unroll
   for (int i = 0; i < 2; ++i) {
     const int c = 4 * i + q;
-    uint32_t off = (uint32_t)(c * 8) * (uint32_t)p.HW;
-#pragma unroll
-    for (int j = 0; j < 8; ++j, off += (uint32_t)p.HW) zv[i][j] = (c * 8 + j < p.n_in) ? __ldcs(zb + off) : 0.f;
+    load8(zb + (size_t)(c * 8) * HW, HW, p.n_in - c * 8, zv[i]);
   }
 }
 
@@ -233,9 +244,7 @@ __global__ void __launch_bounds__(kMbThreads, 1) k_mlp_backward(const __grid_con
 #pragma unroll
       for (int i = 0; i < 4; ++i) {
         const int c = 4 * i + q;
-        uint32_t off = (uint32_t)(c * 8) * (uint32_t)p.HW;
-#pragma unroll
-        for (int j = 0; j < 8; ++j, off += (uint32_t)p.HW) gv[i][j] = (c * 8 + j < p.K) ? __ldcs(gbb + off) : 0.f;
+        load8(gbb + (size_t)(c * 8) * HW, HW, p.K - c * 8, gv[i]);
       }
     }
     mbar_wait(bar_mma, ph);
@@ -362,10 +371,16 @@ __global__ void __launch_bounds__(kMbThreads, 1) k_mlp_backward(const __grid_con
       tmem_ld16(tq + (uint32_t)(q * 16), v);
       tmem_ld_wait();
       if (valid) {
-        uint32_t off = (uint32_t)(q * 16) * (uint32_t)p.HW;
+        float* ptr = gzb + (size_t)(q * 16) * HW;
+        const int nv = p.n_in - q * 16;
+        if (nv >= 16) {  // (two in-range power-of-two factors, as the scaling)
 #pragma unroll
-        for (int j = 0; j < 16; ++j, off += (uint32_t)p.HW)
-          if (q * 16 + j < p.n_in) __stcs(gzb + off, v[j] * u1 * u2);
+          for (int j = 0; j < 16; ++j, ptr += HW) __stcs(ptr, v[j] * u1 * u2);
+        } else {
+#pragma unroll
+          for (int j = 0; j < 16; ++j, ptr += HW)
+            if (j < nv) __stcs(ptr, v[j] * u1 * u2);
+        }
       }
     }
     tc_fence_before();  // TMEM reads before the next tile's F1 (ordered by its publish())
@@ -479,12 +494,13 @@ __global__ void __launch_bounds__(kMbsThreads, 2) k_mlp_backward_s(const __grid_
           const int c = 2 * i + hh;
           if (c * 8 < p.K1) {
             float v[8];
-            uint32_t off = (uint32_t)(c * 8) * (uint32_t)p.HW;
+            load8(zb + (size_t)(c * 8) * HW, HW, p.n_in - c * 8, v);
+            if (kFold)
 #pragma unroll
-            for (int j = 0; j < 8; ++j, off += (uint32_t)p.HW) {
-              const int ch = c * 8 + j;
-              v[j] = ch < p.n_in ? __ldcs(zb + off) : ((kFold && ch < p.n_in + 2) ? 1.f : 0.f);
-            }
+              for (int j = 0; j < 8; ++j) {
+                const int ch = c * 8 + j;
+                if (ch >= p.n_in && ch < p.n_in + 2) v[j] = 1.f;
+              }
             st8f(row_k1, c, v);
           }
         }
@@ -530,9 +546,7 @@ __global__ void __launch_bounds__(kMbsThreads, 2) k_mlp_backward_s(const __grid_
 #pragma unroll
         for (int i = 0; i < 8; ++i) {
           const int c = 2 * i + hh;
-          uint32_t off = (uint32_t)(c * 8) * (uint32_t)p.HW;
-#pragma unroll
-          for (int j = 0; j < 8; ++j, off += (uint32_t)p.HW) gv[i][j] = (c * 8 + j < p.K) ? __ldcs(gbb + off) : 0.f;
+          load8(gbb + (size_t)(c * 8) * HW, HW, p.K - c * 8, gv[i]);
         }
       }
       float mx = 0.f;
@@ -637,11 +651,16 @@ __global__ void __launch_bounds__(kMbsThreads, 2) k_mlp_backward_s(const __grid_
           tmem_ld_wait();
           if (valid) {
             const float u1 = exp2i(-e1), u2 = exp2i(ex + e1);
-            float* gzb = p.gz + (size_t)b * p.n_in * HW + px;
-            uint32_t off = (uint32_t)(g * 16) * (uint32_t)p.HW;
+            float* ptr = p.gz + (size_t)b * p.n_in * HW + px + (size_t)(g * 16) * HW;
+            const int nv = p.n_in - g * 16;
+            if (nv >= 16) {
 #pragma unroll
-            for (int j = 0; j < 16; ++j, off += (uint32_t)p.HW)
-              if (g * 16 + j < p.n_in) __stcs(gzb + off, v[j] * u1 * u2);
+              for (int j = 0; j < 16; ++j, ptr += HW) __stcs(ptr, v[j] * u1 * u2);
+            } else {
+#pragma unroll
+              for (int j = 0; j < 16; ++j, ptr += HW)
+                if (j < nv) __stcs(ptr, v[j] * u1 * u2);
+            }
           }
         }
       }
