@@ -1,3 +1,6 @@
-timeout 900 python -m pytest tests/test_gpu_parity.py tests/test_gpu_full_frames.py -m gpu -q -p no:cacheprovider -x -k "image or backward or adjoint or color" 2>&1 | tail -3
-for w in image all; do python tools/adjoint_time.py 20 $w 2>&1 | head -1; done
-ncu --metrics gpu__time_duration.sum --clock-control none -k regex:"k_fused|k_adjoint_image" --csv python tools/adjoint_time.py 2 image 2>/dev/null | grep -E "k_fused|k_adjoint" | tail -2 | awk -F'","' '{print $5, $NF}'
+# round-end evidence: full GPU tests, bench (default), reference arm, smoke, launch list, ncu of the fused kernel
+mkdir -p gpurun_out
+timeout 1500 python -m pytest tests -m gpu -q -p no:cacheprovider > gpurun_out/gputest.log 2>&1; tail -2 gpurun_out/gputest.log
+bash tools/evidence_run.sh
+bash tools/ncu_full_run.sh
+python tools/dz_time.py > gpurun_out/dz_time.log 2>&1
