@@ -50,10 +50,16 @@ struct ConvStep { uint32_t off, lbo; Tap tap[16]; };
 struct ConvPlan {
   std::vector<ConvStep> steps;
   std::vector<int> ey_a0, ex_a;
-  int npos_y = 0, npos_x = 0, chan_bytes = 0, rr = 0;
+  int npos_y = 0, npos_x = 0, chan_bytes = 0, rr = 0, chan_bytes1 = 0;
+  // half-E mode (ehalf): the E views split by tap rows into two halves with their own buffers --
+  // half 0 = EY blocks [0, blkA), half 1 = the rest + the EX rows -- so a tile's second half builds
+  // while its first is convolved and the next tile's first half while its second is (double
+  // buffering at half the shared memory). Steps [0, cut) read half 0, [cut, n) half 1; offsets are
+  // relative to their half's buffer and chan_bytes is the larger half's per-channel size.
+  int ehalf = 0, blkA = 0, cut = 0;
 };
 
-ConvPlan plan_conv(int S) {
+ConvPlan plan_conv(int S, bool halves = false) {
   ConvPlan P;
   const int r = (S - 1) / 2, rr = (r + 3) / 4 * 4, sh = rr - r;  // E entry 0 <-> column x0 - rr
   const int nv16 = S / 16, L = S - 16 * nv16;
@@ -102,6 +108,21 @@ ConvPlan plan_conv(int S) {
       P.steps.push_back(st);
     }
   P.rr = rr;
+  P.chan_bytes1 = P.chan_bytes;
+  if (halves && ngroups >= 2) {
+    const int gA = ngroups / 2, blkA = 2 * gA;
+    const uint32_t xbase_b = (uint32_t)(nblk - blkA) * ystride;  // EX rows follow half 1's blocks
+    P.ehalf = 1;
+    P.blkA = blkA;
+    P.cut = gA * S;  // the V16 steps of groups [0, gA)
+    P.chan_bytes = (int)((uint32_t)blkA * ystride);
+    P.chan_bytes1 = (int)(xbase_b + (uint32_t)nex * P.npos_x * 16);
+    for (size_t i = (size_t)P.cut; i < P.steps.size(); ++i) {
+      ConvStep& st = P.steps[i];
+      if (st.off >= xbase) st.off = st.off - xbase + xbase_b;  // H steps (EX rows)
+      else st.off -= (uint32_t)blkA * ystride;                 // V16 / V8 steps of half 1's blocks
+    }
+  }
   return P;
 }
 
@@ -215,6 +236,9 @@ FusedParams make_params(const p2s_handle* h, int B, int C, int H, int W, int mod
   for (int i = 0; i < p.n_ey; ++i) p.ey_a0[i] = h->plan.ey_a0[i];
   for (int i = 0; i < p.n_ex; ++i) p.ex_a[i] = h->plan.ex_a[i];
   p.chan_bytes = h->plan.chan_bytes;
+  p.ehalf = h->plan.ehalf;
+  p.blkA = h->plan.blkA;
+  p.chan_bytes1 = h->plan.chan_bytes1;
   p.n_ebuf = h->n_ebuf;
   p.scr_col = h->scr_col;
   p.stage_bytes = h->stage_bytes; p.nring = h->nring;
@@ -323,6 +347,7 @@ p2s_status p2s_init(const p2s_basis* basis, const p2s_mlp* mlp, p2s_handle** out
   h->n_in = mlp->n_in; h->h1 = mlp->h1; h->h2 = mlp->h2;
   h->Nk = up16(K); h->K1 = up16(mlp->n_in); h->N1 = up16(mlp->h1); h->N2 = up16(mlp->h2);
   h->plan = plan_conv(S);
+  const ConvPlan plan_half = plan_conv(S, true);  // used when full double-buffered E views do not fit
   h->sm_count = prop.multiProcessorCount;
   if (const char* e = std::getenv("P2S_PROGRESSIVE")) h->progressive = std::atoi(e) != 0;
   const ConvPlan& P = h->plan;
@@ -374,7 +399,8 @@ p2s_status p2s_init(const p2s_basis* basis, const p2s_mlp* mlp, p2s_handle** out
   const int kh = std::max(h->N1, h->N2);
   const int a2_bytes = kTileM * kh * 2;
   const int hold_bytes = kTileM * hold_cols * 2;
-  const int e1_bytes = 3 * P.chan_bytes;
+  int e1_bytes = 3 * P.chan_bytes;
+  int conv_cut = 0;  // half-E plans: conv items never straddle step `cut`
   const int const_bytes = (h->bias_folded ? 256 : 256 + 2 * kMaxN) * 4;  // b1, b2 unused when folded
   const int red_bytes = 2 * 128 * 16;
   // anchor-grid mode: y-interpolated anchor rows of one tile [n_in][kAncCols] (kernel falls back to
@@ -405,7 +431,8 @@ p2s_status p2s_init(const p2s_basis* basis, const p2s_mlp* mlp, p2s_handle** out
     int mlp = 0;
     for (int o = 0; o < h->n_ops; ++o)
       mlp += count_stages(sb, h->ops[o].nks, h->ops[o].N, h->ops[o].layer == 2 && h->l3_hold_ks > 0);
-    const int conv = count_stages(sb, nconv, h->Nk, false);
+    const int conv = conv_cut ? count_stages(sb, conv_cut, h->Nk, false) + count_stages(sb, nconv - conv_cut, h->Nk, false)
+                              : count_stages(sb, nconv, h->Nk, false);
     int fst = 0;  // first-tile list: whole-layer L1 / L2 (or the per-tile L1 / L2), L3, conv
     for (int o = 0; o < h->n_ops + h->n_fops; ++o) {
       const bool in_first = h->n_fops > 0 ? (o >= h->n_ops || h->ops[o].layer == 2) : true;
@@ -420,11 +447,26 @@ p2s_status p2s_init(const p2s_basis* basis, const p2s_mlp* mlp, p2s_handle** out
                       (red_in_hold ? 0 : al(red_bytes)) + al(bar_bytes) + al(anc_bytes);
     int ring_avail = 0;
     const int ebuf_max = std::getenv("P2S_NEBUF") ? std::max(1, std::min(2, std::atoi(std::getenv("P2S_NEBUF")))) : 2;
-    for (h->n_ebuf = ebuf_max; h->n_ebuf >= 1; --h->n_ebuf) {
-      ring_avail = kSmemLimit - fixed - al(h->n_ebuf * e1_bytes) - 1024;
-      if (ring_avail >= 3 * 12288) break;
+    // E views: two full buffers if they leave >= 3 ring stages of 12 KB; else two half buffers
+    // (plan_half, tap rows split in two); else one full buffer (P2S_EHALF = 1 / 0 forces / forbids
+    // the half plan where it exists)
+    const char* eh_env = std::getenv("P2S_EHALF");
+    const int eh_pref = eh_env ? std::atoi(eh_env) : -1;
+    const int e1_full = 3 * h->plan.chan_bytes, e2_half = 3 * (plan_half.chan_bytes + plan_half.chan_bytes1);
+    const bool full2_fits = kSmemLimit - fixed - al(2 * e1_full) - 1024 >= 3 * 12288;
+    const bool use_half = plan_half.ehalf && ebuf_max == 2 && (eh_pref == 1 || (eh_pref != 0 && !full2_fits));
+    e1_bytes = use_half ? (e2_half + 1) / 2 : e1_full;  // (n_ebuf * e1_bytes covers both halves)
+    conv_cut = use_half ? plan_half.cut : 0;
+    if (use_half) {
+      h->n_ebuf = 2;
+      e1_bytes = (e2_half + 1) / 2;
+    } else {
+      for (h->n_ebuf = ebuf_max; h->n_ebuf >= 1; --h->n_ebuf) {
+        ring_avail = kSmemLimit - fixed - al(h->n_ebuf * e1_bytes) - 1024;
+        if (ring_avail >= 3 * 12288) break;
+      }
+      if (h->n_ebuf < 1) h->n_ebuf = 1;
     }
-    if (h->n_ebuf < 1) h->n_ebuf = 1;
     ring_avail = kSmemLimit - fixed - al(h->n_ebuf * e1_bytes) - 1024;
     // prefer 3 large stages (fewer ring transitions for the UMMA issuer), else 4, else 2
     // (P2S_NRING overrides the stage count for tuning experiments)
@@ -442,6 +484,7 @@ p2s_status p2s_init(const p2s_basis* basis, const p2s_mlp* mlp, p2s_handle** out
     tab_cap = (need + 7) / 8 * 8;
   }
   if (table_need(sb) > tab_cap) { delete h; return P2S_ERR_UNSUPPORTED; }
+  if (conv_cut) h->plan = plan_half;  // (P refers to h->plan: same taps, half-relative offsets)
   h->tab_cap = tab_cap;
   h->nring = nring;
   h->stage_bytes = sb;
@@ -530,15 +573,18 @@ p2s_status p2s_init(const p2s_basis* basis, const p2s_mlp* mlp, p2s_handle** out
   auto make_items = [&](size_t base, int nks, int N, uint8_t kind, uint8_t op, std::vector<Item>& out) {
     const uint32_t hs = (uint32_t)N * 16, per = std::max<uint32_t>(1, (uint32_t)sb / hs);
     const int mi = map_of(N);
-    // L3 items never straddle the hold-buffer / A2 boundary of their A operand
+    // L3 items never straddle the hold-buffer / A2 boundary of their A operand; conv items of a
+    // half-E plan never straddle its half boundary
     const bool is_l3 = kind == 0 && h->ops[op].layer == 2 && h->l3_hold_ks > 0;
     const int cut0 = h->hold_k0, cut1 = h->hold_k0 + h->l3_hold_ks;
+    const int ecut = kind == 1 ? h->plan.cut : 0;
     for (int s0 = 0; s0 < nks;) {
       int ns = std::min<int>(per, nks - s0);
       if (is_l3) {
         if (s0 < cut0) ns = std::min(ns, cut0 - s0);
         else if (s0 < cut1) ns = std::min(ns, cut1 - s0);
       }
+      if (ecut > 0 && s0 < ecut) ns = std::min(ns, ecut - s0);
       Item it{};
       it.src_off = (uint32_t)(base + (size_t)s0 * hs);
       it.bytes = (uint32_t)ns * hs;
@@ -596,9 +642,14 @@ p2s_status p2s_init(const p2s_basis* basis, const p2s_mlp* mlp, p2s_handle** out
     mi.nslabs = (uint8_t)it.nslabs;
     if (it.kind == 1) {
       mi.n16 = (uint8_t)(h->Nk / 16);
-      // mode 3 = the adjoint's conv-only list: its first stage also waits for the accumulators
-      mi.flags = MI_CONV | ((it.flags & IT_BEGIN) ? (MI_WAIT_E | (mode == 3 ? MI_WAIT_TMEM : 0)) : 0) |
-                 ((it.flags & IT_END) ? MI_COMMIT_ACC : 0);
+      // mode 3 = the adjoint's conv-only list: its first stage also waits for the accumulators.
+      // Half-E plans: each half's first stage waits for its E buffer, its last releases it.
+      const int ecut = h->plan.ehalf ? h->plan.cut : 0, end = it.first + it.nslabs;
+      const bool half1 = ecut > 0 && it.first >= ecut;
+      const bool e_begin = (it.flags & IT_BEGIN) || (ecut > 0 && it.first == ecut);
+      const bool e_end = (it.flags & IT_END) || (ecut > 0 && end == ecut);
+      mi.flags = MI_CONV | (e_begin ? MI_WAIT_E : 0) | (((it.flags & IT_BEGIN) && mode == 3) ? MI_WAIT_TMEM : 0) |
+                 (e_end ? MI_COMMIT_E : 0) | (half1 ? MI_EHALF1 : 0) | ((it.flags & IT_END) ? MI_COMMIT_ACC : 0);
       return mi;
     }
     const MlpOp& op = h->ops[it.op];

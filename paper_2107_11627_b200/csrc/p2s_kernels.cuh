@@ -74,7 +74,9 @@ static_assert(sizeof(Item) == 24, "Item layout");
 // shared-memory base is added on the device), width, dependency waits and commits.
 enum MmaItemFlags : uint16_t {
   MI_CONV = 1, MI_WAIT_A1 = 2, MI_WAIT_SCR = 4, MI_WAIT_E = 8,
-  MI_COMMIT_A1 = 16, MI_COMMIT_MLP = 32, MI_COMMIT_ACC = 64, MI_WAIT_TMEM = 128
+  MI_COMMIT_A1 = 16, MI_COMMIT_MLP = 32, MI_COMMIT_ACC = 64, MI_WAIT_TMEM = 128,
+  MI_COMMIT_E = 256,   // the item is the last reader of its E buffer
+  MI_EHALF1 = 512      // half-E plans: the item reads half 1's buffer (else half 0's)
 };
 struct MmaItem {
   uint32_t a_lo_rel;   // (smem offset >> 4) | (LBO >> 4) << 16, without the smem base
@@ -138,6 +140,10 @@ struct FusedParams {
   int ey_a0[kMaxEy], ex_a[kMaxEx];
   int chan_bytes;             // E region bytes per channel (buffers are sized for C = 3)
   int n_ebuf;                 // 1 or 2 E buffers
+  int ehalf, blkA;            // half-E plan (host plan_conv): buffer h holds tap-row half h of one
+                              // tile (EY blocks [0, blkA) | the rest + EX rows), not a whole tile
+  int chan_bytes1;            // half-E plans: half 1's per-channel bytes (chan_bytes: half 0's);
+                              // buffer 1 starts at 3 chan_bytes (else both are chan_bytes)
   int scr_col;                // TMEM column of the MLP scratch (= 3 * Nk)
   int stage_bytes, nring;
   int off_ring, off_a1, off_a2, off_hold, off_e, off_tab, off_const, off_red, off_bar, smem_bytes;
@@ -291,51 +297,53 @@ __device__ __forceinline__ void load_ex(const FusedParams& p, const float* img, 
     for (int q = 0; q < 12; ++q) v[q] = __ldg(row + clampi(col0 + q, 0, p.W - 1));
   }
 }
+// Blocks [blk0, blk1) and EX rows [ex0, ex1) of every channel into Eb, block blk0 at offset 0 and
+// the EX rows after the blocks (a whole tile: [0, n_ey) / [0, n_ex); a half-E plan: one half).
 template <int NT>
 __device__ __forceinline__ void build_E_all(const FusedParams& p, uint8_t* Eb, const float* img_b, int y, int x0,
-                                            int tid) {
+                                            int tid, int blk0, int blk1, int ex0, int ex1, int cstride) {
   const int cx0 = x0 - p.rr;
   const bool vec = (p.W & 3) == 0;
   const size_t HW = (size_t)p.H * p.W;
-  const int ngy = p.npos_y >> 2, per_c_y = p.n_ey * ngy;
+  const int ngy = p.npos_y >> 2, per_c_y = (blk1 - blk0) * ngy;
   const int tot_y = p.C * per_c_y;
   for (int w = tid; w < tot_y; w += 2 * NT) {
     const int w2 = w + NT;
-    const int c0 = w / per_c_y, r0 = w - c0 * per_c_y, blk0 = r0 / ngy, g0 = r0 - blk0 * ngy;
+    const int c0 = w / per_c_y, r0 = w - c0 * per_c_y, bl0 = r0 / ngy, g0 = r0 - bl0 * ngy;
     float v0[4][8], v1[4][8];
-    load_ey(p, img_b + c0 * HW, y, cx0, blk0, g0, vec, v0);
-    int c1 = 0, blk1 = 0, g1 = 0;
+    load_ey(p, img_b + c0 * HW, y, cx0, blk0 + bl0, g0, vec, v0);
+    int c1 = 0, bl1 = 0, g1 = 0;
     if (w2 < tot_y) {
       c1 = w2 / per_c_y;
       const int r1 = w2 - c1 * per_c_y;
-      blk1 = r1 / ngy;
-      g1 = r1 - blk1 * ngy;
-      load_ey(p, img_b + c1 * HW, y, cx0, blk1, g1, vec, v1);
+      bl1 = r1 / ngy;
+      g1 = r1 - bl1 * ngy;
+      load_ey(p, img_b + c1 * HW, y, cx0, blk0 + bl1, g1, vec, v1);
     }
-    store_ey(p, Eb + (size_t)c0 * p.chan_bytes, blk0, g0, v0);
-    if (w2 < tot_y) store_ey(p, Eb + (size_t)c1 * p.chan_bytes, blk1, g1, v1);
+    store_ey(p, Eb + (size_t)c0 * cstride, bl0, g0, v0);
+    if (w2 < tot_y) store_ey(p, Eb + (size_t)c1 * cstride, bl1, g1, v1);
   }
-  const int ngx = p.npos_x >> 2, per_c_x = p.n_ex * ngx;
+  const int ngx = p.npos_x >> 2, per_c_x = (ex1 - ex0) * ngx;
   const int tot_x = p.C * per_c_x;
-  const size_t xoff = (size_t)p.n_ey * p.npos_y * 16;
+  const size_t xoff = (size_t)(blk1 - blk0) * p.npos_y * 16;
   for (int w = tid; w < tot_x; w += 2 * NT) {
     const int w2 = w + NT;
     const int c0 = w / per_c_x, r0 = w - c0 * per_c_x, e0 = r0 / ngx, g0 = r0 - e0 * ngx;
     float v0[12], v1[12];
-    load_ex(p, img_b + c0 * HW, y, cx0, e0, g0, vec, v0);
+    load_ex(p, img_b + c0 * HW, y, cx0, ex0 + e0, g0, vec, v0);
     int c1 = 0, e1 = 0, g1 = 0;
     if (w2 < tot_x) {
       c1 = w2 / per_c_x;
       const int r1 = w2 - c1 * per_c_x;
       e1 = r1 / ngx;
       g1 = r1 - e1 * ngx;
-      load_ex(p, img_b + c1 * HW, y, cx0, e1, g1, vec, v1);
+      load_ex(p, img_b + c1 * HW, y, cx0, ex0 + e1, g1, vec, v1);
     }
-    uint8_t* d0 = Eb + (size_t)c0 * p.chan_bytes + xoff + (size_t)e0 * p.npos_x * 16 + (size_t)(4 * g0) * 16;
+    uint8_t* d0 = Eb + (size_t)c0 * cstride + xoff + (size_t)e0 * p.npos_x * 16 + (size_t)(4 * g0) * 16;
 #pragma unroll
     for (int q = 0; q < 4; ++q) *reinterpret_cast<uint4*>(d0 + q * 16) = pack8_centred(v0 + q);
     if (w2 < tot_x) {
-      uint8_t* d1 = Eb + (size_t)c1 * p.chan_bytes + xoff + (size_t)e1 * p.npos_x * 16 + (size_t)(4 * g1) * 16;
+      uint8_t* d1 = Eb + (size_t)c1 * cstride + xoff + (size_t)e1 * p.npos_x * 16 + (size_t)(4 * g1) * 16;
 #pragma unroll
       for (int q = 0; q < 4; ++q) *reinterpret_cast<uint4*>(d1 + q * 16) = pack8_centred(v1 + q);
     }
@@ -737,16 +745,16 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads)
     const uint32_t hi_conv = (128u >> 4) | (1u << 14);
     const uint32_t id_conv = idesc_f16(256, p.Nk);
     const uint32_t stage16 = (uint32_t)p.stage_bytes >> 4;
-    const uint32_t ch16 = (uint32_t)p.chan_bytes >> 4;
-    const uint32_t ebuf16 = 3u * ch16;
-    const int C = p.C, nring = p.nring, ebufs = p.n_ebuf, mode = pmode;
+    const uint32_t ch16_0 = (uint32_t)p.chan_bytes >> 4, ch16_1 = (uint32_t)p.chan_bytes1 >> 4;
+    const uint32_t ebuf16 = 3u * ch16_0;  // buffer 1's offset
+    const int C = p.C, nring = p.nring, ebufs = p.n_ebuf, mode = pmode, ehalf = p.ehalf;
     const uint32_t acc1 = tmem + (uint32_t)p.Nk, acc2 = tmem + 2u * (uint32_t)p.Nk;
     const uint32_t smem_lo = smem_u32(smem) >> 4;
     const uint32_t id_base = idesc_f16(256, 0);
     int s = 0;
     uint32_t ph = 0;
     uint32_t scr_waits = 0, a1_waits = 0;
-    uint32_t e_use0 = 0, e_use1 = 0;
+    uint32_t e_par = 0;  // bit b: phase parity of E buffer b's next use (branch-free: keeps the loop uniform)
     int pending = -1;  // ring slot whose release commit is deferred behind the next UMMAs
 #ifdef P2S_PROFILE
     prof_acc[11] = globaltimer_ns();
@@ -761,8 +769,11 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads)
       const int n_items = seg_len(it, fr);
       // prefetch the next item: same segment, else the next frame's (S) or the next tile's (B)
       const MmaItem nxt = sMma[g + 1 < n_items ? seg_base(it, fr) + g + 1 : (fr + 1 < nfr ? nA + nB : nA)];
-      const int eb = ebufs == 2 ? (it & 1) : 0;
       const uint32_t f = cur.flags;
+      // E buffer of this item: half-E plans by the item's half, else by tile parity (broadcast
+      // from lane 0: a value ptxas cannot prove warp-uniform costs the issue loop its uniform
+      // datapath, SASS-checked)
+      const int eb = ehalf ? __shfl_sync(0xffffffffu, (f & MI_EHALF1) ? 1 : 0, 0) : (ebufs == 2 ? (it & 1) : 0);
 #ifdef P2S_PROFILE
       const long long tr_a = clock64();
 #endif
@@ -775,7 +786,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads)
         { PROF_T0(); mbar_wait(&bars[BAR_SCR_FREE], scr_waits & 1); PROF_ADD(2); }
         ++scr_waits;
       }
-      if (f & MI_WAIT_E) { PROF_T0(); mbar_wait(&bars[BAR_E_FULL0 + eb], (eb ? e_use1 : e_use0) & 1); PROF_ADD(3); }
+      if (f & MI_WAIT_E) { PROF_T0(); mbar_wait(&bars[BAR_E_FULL0 + eb], (e_par >> eb) & 1u); PROF_ADD(3); }
 #ifndef P2S_ABL_NOTMA
       { PROF_T0(); mbar_wait(&ring_full[s], ph); PROF_ADD(5); }
 #endif
@@ -798,6 +809,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads)
 #endif
         PROF_T0();
         const uint32_t e0 = e_lo + (uint32_t)eb * ebuf16;
+        const uint32_t ch16 = eb ? ch16_1 : ch16_0;  // channel stride of this buffer
         const uint32_t* steps = sSteps + first;
 #pragma unroll 2
         for (uint32_t j = 0; j < n; ++j) {
@@ -837,17 +849,15 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads)
       if (pending >= 0) { umma2_commit_elect(&ring_empty[pending]); pending = -1; }
 #endif
       // completion signals for the epilogue / builders are not deferred
-      if (f & (MI_COMMIT_A1 | MI_COMMIT_MLP | MI_COMMIT_ACC)) {
+      if (f & (MI_COMMIT_A1 | MI_COMMIT_MLP | MI_COMMIT_ACC | MI_COMMIT_E)) {
         umma2_commit_elect(&ring_empty[s]);  // keep ring releases in order before a hand-off
         if (f & MI_COMMIT_A1) umma2_commit_elect(&bars[BAR_A1_EMPTY]);
         if (f & MI_COMMIT_MLP) umma2_commit_elect(&bars[BAR_MLP_DONE]);
-        if (f & MI_COMMIT_ACC) {
-          if ((f & MI_CONV) && mode != 1) {
-            umma2_commit_elect(&bars[BAR_E_EMPTY0 + eb]);
-            if (eb) ++e_use1; else ++e_use0;
-          }
-          umma2_commit_elect(&bars[BAR_ACC_FULL]);
+        if ((f & MI_COMMIT_E) && mode != 1) {  // the last reader of E buffer eb
+          umma2_commit_elect(&bars[BAR_E_EMPTY0 + eb]);
+          e_par ^= 1u << eb;
         }
+        if (f & MI_COMMIT_ACC) umma2_commit_elect(&bars[BAR_ACC_FULL]);
       } else {
         pending = s;
       }
@@ -910,22 +920,28 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads)
         if (lane == 0 && builder_index(warp) == 0 && a1_builds == 1) STAMP(3);
       }
       if (pmode == 1 || fr > 0) continue;  // E views: once per tile (every frame shares the image)
-      // --- E views of every channel (the CTA's first tile: built by the idle epilogue warps)
-      const int eb = p.n_ebuf == 2 ? (it & 1) : 0;
-      if (it == 0) { ++e_use0; continue; }
-      { PROF_T0(); WAIT_BUILD(&bars[BAR_E_EMPTY0 + eb], ((eb ? e_use1 : e_use0) & 1) ^ 1); PROF_ADD(11); }
-      if (eb) ++e_use1; else ++e_use0;
-      uint8_t* Eb = sE + (size_t)eb * 3 * p.chan_bytes;  // buffers are sized for C = 3
-      {
-        PROF_T0();
+      // --- E views of every channel (the CTA's first tile: built by the idle epilogue warps).
+      // Half-E plans: buffer h <- half h of this tile, one after the other
+      if (it == 0) { ++e_use0; if (p.ehalf) ++e_use1; continue; }
+      for (int hh = 0; hh < 1 + p.ehalf; ++hh) {
+        const int eb = p.ehalf ? hh : (p.n_ebuf == 2 ? (it & 1) : 0);
+        { PROF_T0(); WAIT_BUILD(&bars[BAR_E_EMPTY0 + eb], ((eb ? e_use1 : e_use0) & 1) ^ 1); PROF_ADD(11); }
+        if (eb) ++e_use1; else ++e_use0;
+        uint8_t* Eb = sE + (size_t)eb * 3 * p.chan_bytes;  // buffers are sized for C = 3 (half 0 first)
+        {
+          PROF_T0();
 #ifndef P2S_ABL_NOE
-        build_E_all<kBuildThreads>(p, Eb, p.image + (size_t)b * p.C * HW, y, x0, tid);
+          // (one call site: every inlined copy of the builder costs registers the whole kernel shares)
+          const bool h0 = p.ehalf && hh == 0, h1 = p.ehalf && hh == 1;
+          build_E_all<kBuildThreads>(p, Eb, p.image + (size_t)b * p.C * HW, y, x0, tid, h1 ? p.blkA : 0,
+                                     h0 ? p.blkA : p.n_ey, 0, h0 ? 0 : p.n_ex, h1 ? p.chan_bytes1 : p.chan_bytes);
 #endif
-        PROF_ADD(12);
+          PROF_ADD(12);
+        }
+        fence_proxy_async_smem();
+        __syncwarp();
+        if (lane == 0) mbar_arrive_remote(&bars[BAR_E_FULL0 + eb], 0);
       }
-      fence_proxy_async_smem();
-      __syncwarp();
-      if (lane == 0) mbar_arrive_remote(&bars[BAR_E_FULL0 + eb], 0);
     }
   } else if (warp >= kWarpEpi0) {
     // ================= epilogue: two warpgroups split every TMEM drain by 16-col groups =====
@@ -939,12 +955,20 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads)
       tile_coords(p, min(2 * pr_begin + (int)rank, p.ntiles - 1), b0, y0, xs);
       const size_t HW0 = (size_t)p.H * p.W;
 #ifndef P2S_ABL_NOE
-      build_E_all<32 * kNumEpiWarps>(p, sE, p.image + (size_t)b0 * p.C * HW0, y0, xs,
-                                     (warp - kWarpEpi0) * 32 + lane);
+      const int etid = (warp - kWarpEpi0) * 32 + lane;
+      for (int hh = 0; hh < 1 + p.ehalf; ++hh) {  // half-E plans: both halves, into buffers 0 and 1
+        const bool h0 = p.ehalf && hh == 0, h1 = p.ehalf && hh == 1;
+        build_E_all<32 * kNumEpiWarps>(p, sE + (size_t)hh * 3 * p.chan_bytes, p.image + (size_t)b0 * p.C * HW0, y0,
+                                       xs, etid, h1 ? p.blkA : 0, h0 ? p.blkA : p.n_ey, 0, h0 ? 0 : p.n_ex,
+                                       h1 ? p.chan_bytes1 : p.chan_bytes);
+      }
 #endif
       fence_proxy_async_smem();
       named_bar_sync(2, 32 * kNumEpiWarps);
-      if (warp - kWarpEpi0 < kNumBuildWarps && lane == 0) mbar_arrive_remote(&bars[BAR_E_FULL0], 0);
+      if (warp - kWarpEpi0 < kNumBuildWarps && lane == 0) {
+        mbar_arrive_remote(&bars[BAR_E_FULL0], 0);
+        if (p.ehalf) mbar_arrive_remote(&bars[BAR_E_FULL1], 0);
+      }
       if (warp == kWarpEpi0 && lane == 0) STAMP(4);
     }
     const int ew = warp - kWarpEpi0;        // 0..7
