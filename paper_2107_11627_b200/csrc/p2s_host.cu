@@ -370,7 +370,13 @@ p2s_status p2s_init(const p2s_basis* basis, const p2s_mlp* mlp, p2s_handle** out
     const int N = layer_N[l];
     const int nch = (N + CH - 1) / CH;
     if (nch > 2 || (l == 2 && nch > 1)) { delete h; return P2S_ERR_UNSUPPORTED; }
-    const int w0 = nch == 1 ? N : std::min(CH, 128);  // columns [0, w0) and [w0, N)
+    // columns [0, w0) and [w0, N), w0 = 160 (P2S_MLP_W0 tunes it): the upper chunk is the L2 one
+    // parked in the hold buffer, so a wide lower chunk frees shared memory for the ring -- round 2,
+    // measured against w0 = 128: cfg3 fused 176.5 -> 174.5 us, cfg5 401-415 -> 467-479 frames/s,
+    // cfg2 17.8k -> 18.4k frames/s (176: no better on cfg3, 470 on cfg5)
+    int w0 = nch == 1 ? N : std::max(N - CH, std::min(CH, 160));
+    if (const char* e = std::getenv("P2S_MLP_W0"))
+      if (nch == 2) w0 = std::max(N - CH, std::min(CH, std::atoi(e) / 16 * 16));
     if (nch == 1) {
       h->ops[h->n_ops++] = MlpOp{l, 0, N, layer_K[l] / 16, 1, 1, h->scr_col};
     } else {
