@@ -153,6 +153,7 @@ struct p2s_handle {
   PFN_cuTensorMapEncodeTiled encode = nullptr;
   // dL/dz (k_mlp_backward): resident weight pack and its shared-memory plan (mb_ok = it fits)
   uint8_t* d_mlpb = nullptr;
+  int mb_col_b = 0, mb_col_c = 0;
   int mb_ok = 0, mb_fold = 0, mb_stream = 0, mb_g3 = 1, mb_nring = 0, mb_slot = 0, mb_off_ring = 0, mb_ring_src_off = 0,
       mb_smem = 0, mb_off_w2 = 0, mb_off_w3 = 0, mb_off_bias = 0, mb_wbytes = 0, mb_off_act = 0, mb_off_bar = 0;
   MlpOp ops[kMaxOps];  // [0, n_ops) per-tile ops, then n_fops first-tile whole-layer ops
@@ -830,7 +831,12 @@ p2s_status p2s_init(const p2s_basis* basis, const p2s_mlp* mlp, p2s_handle** out
     const int kact = std::max(std::max(K1, N1), std::max(N2, Nk));
     const int act_bytes = 128 * kact * 2;
     auto al128 = [](int v) { return (v + 127) / 128 * 128; };
-    const int smem_res = al128(w1 + w2 + w3 + bb) + act_bytes + 32 + 4 * 128 * 4;
+    const int smem_res = al128(w1 + w2 + w3 + bb) + act_bytes + 64 + 4 * 128 * 4;
+    // resident variant's TMEM: RA = [0, maxN) (F1, B1), RB = [col_b, +maxN) (F2, B2), RC =
+    // [col_c, +K1) (B3; separate so the next tile's F1 overlaps this tile's dL/dz drain)
+    const int maxN = std::max(N1, N2);
+    const int col_b = maxN + K1 <= 256 ? 256 : maxN, col_c = col_b + maxN;
+    const bool res_fits = smem_res <= kSmemLimit && col_c + K1 <= 512 && Nk <= 128;
     // biases as fp16 hi/lo pairs on constant-1 inputs when each layer input has 2 spare columns
     const bool fold = h->n_in + 2 <= K1 && h->h1 + 2 <= N1;
     if (K1 <= 64) {
@@ -864,7 +870,7 @@ p2s_status p2s_init(const p2s_basis* basis, const p2s_mlp* mlp, p2s_handle** out
       for (int j = 0; j < h->h1; ++j) bias[j] = mlp->b1[j];
       for (int j = 0; j < h->h2; ++j) bias[N1 + j] = mlp->b2[j];
       const char* mode = std::getenv("P2S_MB_MODE");
-      const bool stream = smem_res > kSmemLimit || (mode && std::strcmp(mode, "stream") == 0);
+      const bool stream = !res_fits || (mode && std::strcmp(mode, "stream") == 0);
       if (!stream) {
         // resident pack [W1 | W2 | W3^T | b1 | b2], copied to shared memory offset 0
         std::vector<uint8_t> pk((size_t)w1 + w2 + w3 + bb);
@@ -887,6 +893,8 @@ p2s_status p2s_init(const p2s_basis* basis, const p2s_mlp* mlp, p2s_handle** out
         h->mb_wbytes = (int)pk.size();
         h->mb_off_act = al128((int)pk.size());
         h->mb_off_bar = h->mb_off_act + act_bytes;
+        h->mb_col_b = col_b;
+        h->mb_col_c = col_c;
       } else {
         // slab table, per tile: [F1: W1 K-slabs | F2: W2 K-slabs | B1: W3^T K-slabs | B2: W2 row
         // pairs (W2^T K'-slabs) | B3: W1 row pairs, g3 per slot]; K-slabs re-laid [N][16]
@@ -1195,6 +1203,7 @@ p2s_status p2s_mlp_backward(p2s_handle* h, const float* zernike_field, const flo
   p.ntiles = (int)(tpf * B);
   p.off_w2 = h->mb_off_w2; p.off_w3 = h->mb_off_w3; p.off_bias = h->mb_off_bias; p.wbytes = h->mb_wbytes;
   p.off_act = h->mb_off_act; p.off_bar = h->mb_off_bar;
+  p.col_b = h->mb_col_b; p.col_c = h->mb_col_c;
   cudaStream_t st = (cudaStream_t)stream;
   if (h->mb_stream) {
     p.ring_src = h->d_mlpb + h->mb_ring_src_off;

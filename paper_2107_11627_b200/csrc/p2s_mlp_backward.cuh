@@ -54,13 +54,16 @@ struct MlpbParams {
   int tiles_per_frame, ntiles;
   int off_w2, off_w3, off_bias, wbytes;  // byte offsets in wpack (= in shared memory)
   int off_act, off_bar;
+  int col_b, col_c;     // resident variant: TMEM columns of the RB / RC accumulator regions
   // streamed variant (k_mlp_backward_s): the slab table and the ring (B3's W1^T K'-steps are
   // small, K1 x 32 B: g3 of them share one slot, contiguous in W1's layout)
   const uint8_t* ring_src;
   int off_ring, nring, slab_stride, g3;
 };
 
-constexpr int kMbThreads = 512;
+// resident variant: 16 drain warps (4 per TMEM lane quadrant) + the UMMA issuer (warp 16)
+constexpr int kMbDrainWarps = 16;
+constexpr int kMbThreads = 32 * (kMbDrainWarps + 1);
 
 namespace mlpb {
 
@@ -112,6 +115,9 @@ P2S_DEV void gemm_ring(uint32_t d, uint32_t a_s, int nks, uint32_t ring_s, uint3
   }
 }
 
+// barrier among the 16 drain warps only (the issuer warp never joins it)
+P2S_DEV void named_sync_drains() { asm volatile("bar.sync 1, %0;" ::"n"(32 * kMbDrainWarps) : "memory"); }
+
 // the CTA's generic-proxy writes to ACT / its TMEM reads are ordered before the next UMMA
 P2S_DEV void publish() {
   fence_proxy_async_smem();
@@ -121,9 +127,6 @@ P2S_DEV void publish() {
 
 }  // namespace mlpb
 
-// this thread's z values of tile t (chunks 4i + q of 8 channels). Loads clamp the pixel into the
-// frame (a ragged tile's extra rows are never stored) and address channels by 32-bit offsets
-// from the frame base (host: (n_in + 2) HW, K HW < 2^31).
 // 8 channels (nvalid real, the rest 0) of one pixel, `stride` floats apart, by a running pointer
 // (the drains are issue-bound: per-load offset products and bound checks cost ~2 instructions
 // each over the whole tile; full chunks take the unpredicated path)
@@ -136,18 +139,6 @@ P2S_DEV void load8(const float* ptr, size_t stride, int nvalid, float (&v)[8]) {
     for (int j = 0; j < 8; ++j, ptr += stride) v[j] = j < nvalid ? __ldcs(ptr) : 0.f;
   }
 }
-P2S_DEV void load_z(const MlpbParams& p, int t, int m, int q, float (&zv)[2][8]) {
-  const int b = t / p.tiles_per_frame;
-  const int px = min((t - b * p.tiles_per_frame) * 128 + m, p.HW - 1);
-  const size_t HW = (size_t)p.HW;
-  const float* zb = p.z + (size_t)b * p.n_in * HW + px;
-#pragma unroll
-  for (int i = 0; i < 2; ++i) {
-    const int c = 4 * i + q;
-    load8(zb + (size_t)(c * 8) * HW, HW, p.n_in - c * 8, zv[i]);
-  }
-}
-
 template <bool kFold>
 __global__ void __launch_bounds__(kMbThreads, 1) k_mlp_backward(const __grid_constant__ MlpbParams p) {
   using namespace mlpb;
@@ -156,17 +147,18 @@ __global__ void __launch_bounds__(kMbThreads, 1) k_mlp_backward(const __grid_con
   uint64_t* bar_w = reinterpret_cast<uint64_t*>(smem + p.off_bar);
   uint64_t* bar_mma = bar_w + 1;
   uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bar_mma + 1);
-  float* s_max = reinterpret_cast<float*>(smem + p.off_bar + 32);  // [4][128]
+  uint64_t* bar_rnd = bar_w + 4;                                   // [4] operand-round ring
+  float* s_max = reinterpret_cast<float*>(smem + p.off_bar + 64);  // [4][128]
   const float* s_b1 = reinterpret_cast<const float*>(smem + p.off_bias);
   const float* s_b2 = s_b1 + p.N1;
   uint8_t* act = smem + p.off_act;
   const uint32_t act_s = sbase + (uint32_t)p.off_act;
   const int tid = (int)threadIdx.x, warp = (int)warp_id();
-  const int m = tid & 127, q = tid >> 7;  // pixel row (TMEM lane) and column quarter
 
   if (tid == 0) {
     mbar_init(bar_w, 1);
     mbar_init(bar_mma, 1);
+    for (int i = 0; i < 4; ++i) mbar_init(&bar_rnd[i], kMbDrainWarps);
     fence_mbar_init();
   }
   if (warp == 0) tmem_alloc<512>(tmem_slot);
@@ -176,214 +168,258 @@ __global__ void __launch_bounds__(kMbThreads, 1) k_mlp_backward(const __grid_con
   // broadcast from lane 0 so that ptxas keeps the UMMA operands on the uniform datapath (no
   // per-UMMA elect loops; tests/test_abi_cpu.py checks the SASS)
   const uint32_t tmem = __shfl_sync(0xffffffffu, *tmem_slot, 0);
-  const uint32_t tq = tmem + ((uint32_t)(32 * (warp & 3)) << 16);  // this warp's lane quadrant
-  if (tid == 0 && (int)blockIdx.x < p.ntiles) {
+  if (tid == 0) {
     mbar_arrive_expect_tx(bar_w, (uint32_t)p.wbytes);
     for (int off = 0; off < p.wbytes; off += 32768)
       bulk_g2s(smem + off, p.wpack + off, (uint32_t)min(32768, p.wbytes - off), bar_w);
   }
+  // TMEM: RA = [0, N) F1 / B1, RB = [col_b, +N) F2 / B2, RC = [col_c, +K1) B3 (host-checked)
+  const uint32_t tRA = tmem, tRB = tmem + (uint32_t)p.col_b, tRC = tmem + (uint32_t)p.col_c;
 
-  const uint32_t id_f1 = idesc_f16(128, (uint32_t)p.N1), id_f2 = idesc_f16(128, (uint32_t)p.N2);
-  const uint32_t id_b2 = idesc_f16(128, (uint32_t)p.N1) | (1u << 16);
-  const uint32_t id_b3 = idesc_f16(128, (uint32_t)p.K1) | (1u << 16);
-  const uint32_t w1_s = sbase, w2_s = sbase + (uint32_t)p.off_w2, w3_s = sbase + (uint32_t)p.off_w3;
-  const size_t HW = (size_t)p.HW;
-  uint8_t* const row_k1 = row_of(act, m, p.K1);
-  uint8_t* const row_n1 = row_of(act, m, p.N1);
-  uint8_t* const row_n2 = row_of(act, m, p.N2);
-  uint8_t* const row_nk = row_of(act, m, p.Nk);
-  uint32_t ph = 0;
-  bool first = true;
-  float zv[2][8];
-  if ((int)blockIdx.x < p.ntiles) load_z(p, (int)blockIdx.x, m, q, zv);
-
-  for (int t = (int)blockIdx.x; t < p.ntiles; t += (int)gridDim.x) {
-    const int b = t / p.tiles_per_frame;
-    const int px = (t - b * p.tiles_per_frame) * 128 + m;
-    const bool valid = px < p.HW;
-    {  // L2 prefetch of the next tile's dL/dbeta rows (4 lines of 128 B per channel)
-      const int tn = t + (int)gridDim.x;
-      if (tn < p.ntiles) {
-        const int bn = tn / p.tiles_per_frame, p0 = (tn - bn * p.tiles_per_frame) * 128;
-        for (int r = tid; r < 4 * p.K; r += kMbThreads) {
-          const int qq = p0 + (r & 3) * 32;
-          if (qq < p.HW) prefetch_l2(p.gb + ((size_t)bn * p.K + (r >> 2)) * HW + qq);
-        }
+  if (warp == kMbDrainWarps) {
+    // ================= UMMA issuer: every GEMM streams its K-steps as the drains publish the A
+    // operand's 16-column groups, four per round (bar_rnd[round % 4])
+    const uint32_t id_f1 = idesc_f16(128, (uint32_t)p.N1), id_f2 = idesc_f16(128, (uint32_t)p.N2);
+    const uint32_t id_b2 = idesc_f16(128, (uint32_t)p.N1) | (1u << 16);
+    const uint32_t id_b3 = idesc_f16(128, (uint32_t)p.K1) | (1u << 16);
+    const uint32_t w1_s = sbase, w2_s = sbase + (uint32_t)p.off_w2, w3_s = sbase + (uint32_t)p.off_w3;
+    uint32_t rs = 0;
+    auto gemm_rounds = [&](uint32_t d, int nks, uint32_t b_s, uint32_t b_lbo, uint32_t b_sbo, uint32_t b_kstep,
+                           uint32_t idesc) {
+      const uint32_t a_sbo = (uint32_t)nks * 256u;
+      for (int k0 = 0; k0 < nks; k0 += 4, ++rs) {
+        mbar_wait(&bar_rnd[rs & 3u], (rs >> 2) & 1u);
+        tc_fence_after();
+        const int k1 = min(nks, k0 + 4);
+        for (int ks = k0; ks < k1; ++ks)
+          umma_f16_elect(d, sdesc(act_s + (uint32_t)ks * 256u, 128u, a_sbo),
+                         sdesc(b_s + (uint32_t)ks * b_kstep, b_lbo, b_sbo), idesc, ks > 0 ? 1u : 0u);
       }
-    }
-    const int pxc = valid ? px : p.HW - 1;
-    // ---- z (loaded into zv one tile ahead) -> ACT (fp16, K1 columns; kFold: columns n_in,
-    //      n_in + 1 = 1; other padding zeros)
-#pragma unroll
-    for (int i = 0; i < 2; ++i) {
-      const int c = 4 * i + q;
-      if (c * 8 < p.K1) {
-        float v[8];
-#pragma unroll
-        for (int j = 0; j < 8; ++j) {
-          const int ch = c * 8 + j;
-          v[j] = ch < p.n_in ? zv[i][j] : ((kFold && ch < p.n_in + 2) ? 1.f : 0.f);
-        }
-        st8f(row_k1, c, v);
-      }
-    }
-    publish();
-    if (first) {  // resident weights and biases
-      mbar_wait(bar_w, 0);
-      first = false;
-    }
-    if (warp == 0) {
-      tc_fence_after();
-      gemm(tmem, act_s, p.K1 / 16, w1_s, 128u, (uint32_t)p.K1 * 16u, 256u, id_f1);
       umma_commit_elect(bar_mma);
+    };
+    if ((int)blockIdx.x < p.ntiles) mbar_wait(bar_w, 0);
+    for (int t = (int)blockIdx.x; t < p.ntiles; t += (int)gridDim.x) {
+      gemm_rounds(tRA, p.K1 / 16, w1_s, 128u, (uint32_t)p.K1 * 16u, 256u, id_f1);   // F1 <- z
+      gemm_rounds(tRB, p.N1 / 16, w2_s, 128u, (uint32_t)p.N1 * 16u, 256u, id_f2);   // F2 <- a1
+      gemm_rounds(tRA, p.Nk / 16, w3_s, 128u, (uint32_t)p.Nk * 16u, 256u, id_f2);   // B1 <- g3
+      gemm_rounds(tRB, p.N2 / 16, w2_s, (uint32_t)p.N1 * 16u, 128u, (uint32_t)p.N1 * 32u, id_b2);  // B2 <- g2
+      gemm_rounds(tRC, p.N1 / 16, w1_s, (uint32_t)p.K1 * 16u, 128u, (uint32_t)p.K1 * 32u, id_b3);  // B3 <- g1
     }
-    // ---- dL/dbeta of this tile into registers (in flight during F1 / F2)
-    float gv[4][8];
-    {
-      const float* gbb = p.gb + (size_t)b * p.K * HW + pxc;
+  } else {
+    // ================= drains: 4 threads per pixel row (TMEM lane); thread q of a row owns the
+    // 16-column groups g = 4 r + q (round r)
+    const int m = tid & 127, q = tid >> 7;
+    const uint32_t tq = (uint32_t)(32 * (warp & 3)) << 16;  // this warp's lane quadrant
+    const size_t HW = (size_t)p.HW;
+    uint8_t* const row_k1 = row_of(act, m, p.K1);
+    uint8_t* const row_n1 = row_of(act, m, p.N1);
+    uint8_t* const row_n2 = row_of(act, m, p.N2);
+    uint8_t* const row_nk = row_of(act, m, p.Nk);
+    const int G1 = p.N1 / 16, G2 = p.N2 / 16, Gk = p.Nk / 16, Gz = p.K1 / 16;
+    uint32_t ph = 0, rs = 0;
+    // publish this warp's part of one round: generic-proxy ACT writes and TMEM reads are ordered
+    // before the UMMAs the issuer starts on the round's barrier
+    auto round_done = [&] {
+      fence_proxy_async_smem();
+      tc_fence_before();
+      __syncwarp();
+      if ((tid & 31) == 0) mbar_arrive(&bar_rnd[rs & 3u]);
+      ++rs;
+    };
+    auto wait_mma = [&] {
+      mbar_wait(bar_mma, ph);
+      ph ^= 1;
+      tc_fence_after();
+    };
+    // z of tile t -> ACT (K1 <= 64: one round; kFold: columns n_in, n_in + 1 = 1, padding zeros)
+    float zv[16];
+    auto load_z16 = [&](int t) {
+      const int b = t / p.tiles_per_frame;
+      const int px = min((t - b * p.tiles_per_frame) * 128 + m, p.HW - 1);
+      const float* zb = p.z + (size_t)b * p.n_in * HW + px + (size_t)(q * 16) * HW;
+      load8(zb, HW, p.n_in - q * 16, *reinterpret_cast<float(*)[8]>(zv));
+      load8(zb + 8 * HW, HW, p.n_in - q * 16 - 8, *reinterpret_cast<float(*)[8]>(zv + 8));
+    };
+    auto store_z = [&] {
+      if (q < Gz) {
 #pragma unroll
-      for (int i = 0; i < 4; ++i) {
-        const int c = 4 * i + q;
-        load8(gbb + (size_t)(c * 8) * HW, HW, p.K - c * 8, gv[i]);
+        for (int j = 0; j < 16; ++j) {
+          const int ch = q * 16 + j;
+          if (ch >= p.n_in) zv[j] = (kFold && ch < p.n_in + 2) ? 1.f : 0.f;
+        }
+        st8f(row_k1, 2 * q, zv);
+        st8f(row_k1, 2 * q + 1, zv + 8);
       }
-    }
-    mbar_wait(bar_mma, ph);
-    ph ^= 1;
-    tc_fence_after();
-    // ---- drain D1: a1 = relu(pre1) -> ACT (N1 columns), mask1 = [pre1 > 0] bits
-    uint32_t mask1[2] = {0u, 0u};
+      round_done();
+    };
+    load_z16((int)blockIdx.x);
+    store_z();
+    if (!kFold) mbar_wait(bar_w, 0);  // the fp32 biases the drains add
+    for (int t = (int)blockIdx.x; t < p.ntiles; t += (int)gridDim.x) {
+      const int b = t / p.tiles_per_frame;
+      const int px = (t - b * p.tiles_per_frame) * 128 + m;
+      const bool valid = px < p.HW;
+      const int pxc = valid ? px : p.HW - 1;
+      {  // L2 prefetch of the next tile's dL/dbeta rows (4 lines of 128 B per channel)
+        const int tn = t + (int)gridDim.x;
+        if (tn < p.ntiles) {
+          const int bn = tn / p.tiles_per_frame, p0 = (tn - bn * p.tiles_per_frame) * 128;
+          for (int r = tid; r < 4 * p.K; r += kMbDrainWarps * 32) {
+            const int qq = p0 + (r & 3) * 32;
+            if (qq < p.HW) prefetch_l2(p.gb + ((size_t)bn * p.K + (r >> 2)) * HW + qq);
+          }
+        }
+      }
+      // ---- dL/dbeta of this tile into registers (in flight during F1 / D1 / F2): groups 4 r + q
+      float gv[2][16];
+      {
+        const float* gbb = p.gb + (size_t)b * p.K * HW + pxc;
 #pragma unroll
-    for (int i = 0; i < 4; ++i) {
-      const int g = 4 * i + q;
-      if (g * 16 < p.N1) {
+        for (int r = 0; r < 2; ++r) {
+          const int c = 16 * (4 * r + q);
+          load8(gbb + (size_t)c * HW, HW, p.K - c, *reinterpret_cast<float(*)[8]>(gv[r]));
+          load8(gbb + (size_t)(c + 8) * HW, HW, p.K - c - 8, *reinterpret_cast<float(*)[8]>(gv[r] + 8));
+        }
+      }
+      wait_mma();  // F1
+      // ---- D1 (RA): a1 = relu(pre1) -> ACT (N1 columns), mask1 = [pre1 >= +0] sign bits, per round
+      uint32_t mask1[2] = {0u, 0u};
+#pragma unroll
+      for (int r = 0; r < 4; ++r) {
+        const int g = 4 * r + q;
+        if (4 * r < G1) {
+          if (g < G1) {
+            float v[16];
+            tmem_ld16(tRA + tq + (uint32_t)(g * 16), v);
+            tmem_ld_wait();
+            if (!kFold) {
+#pragma unroll
+              for (int j = 0; j < 16; ++j) v[j] += s_b1[g * 16 + j];
+            }
+            uint32_t neg = 0;
+#pragma unroll
+            for (int j = 15; j >= 0; --j) neg = __funnelshift_l(__float_as_uint(v[j]), neg, 1);
+            mask1[r >> 1] |= (~neg & 0xffffu) << ((r & 1) * 16);
+            st8(row_n1, 2 * g, relu2(v[0], v[1]), relu2(v[2], v[3]), relu2(v[4], v[5]), relu2(v[6], v[7]));
+            st8(row_n1, 2 * g + 1, relu2(v[8], v[9]), relu2(v[10], v[11]), relu2(v[12], v[13]), relu2(v[14], v[15]));
+          }
+          round_done();
+        }
+      }
+      // per-pixel power-of-two scale of dL/dbeta (the four quarters agree through s_max)
+      float mx = 0.f;
+#pragma unroll
+      for (int r = 0; r < 2; ++r)
+#pragma unroll
+        for (int j = 0; j < 16; ++j) mx = fmaxf(mx, fabsf(gv[r][j]));
+      s_max[q * 128 + m] = mx;
+      named_sync_drains();
+      mx = fmaxf(fmaxf(s_max[m], s_max[128 + m]), fmaxf(s_max[256 + m], s_max[384 + m]));
+      // mx = f 2^ex with f in [0.5, 1) (normal mx; 0 and subnormals take ex = -126, inf/NaN 129):
+      // scale by 2^-ex and back by 2^ex, each as two in-range power-of-two factors (exact)
+      const int ex = (int)((__float_as_uint(mx) >> 23) & 0xffu) - 126;
+      const int e1 = (-ex) / 2, e2 = -ex - e1;
+      wait_mma();  // F2: ACT is free, pre2 in RB
+      // ---- scaled dL/dbeta -> ACT (Nk columns), per round: B1 streams on them
+      {
+        const float s1 = exp2i(e1), s2 = exp2i(e2);
+#pragma unroll
+        for (int r = 0; r < 2; ++r) {
+          const int g = 4 * r + q;
+          if (4 * r < Gk) {
+            if (g < Gk) {
+              float v[16];
+#pragma unroll
+              for (int j = 0; j < 16; ++j) v[j] = gv[r][j] * s1 * s2;
+              st8f(row_nk, 2 * g, v);
+              st8f(row_nk, 2 * g + 1, v + 8);
+            }
+            round_done();
+          }
+        }
+      }
+      // ---- RB (pre2) -> mask2 sign bits while B1 runs (RB is free for B2 after this)
+      uint32_t mask2[2] = {0u, 0u};
+#pragma unroll
+      for (int r = 0; r < 4; ++r) {
+        const int g = 4 * r + q;
+        if (g < G2) {
+          float v[16];
+          tmem_ld16(tRB + tq + (uint32_t)(g * 16), v);
+          tmem_ld_wait();
+          if (!kFold) {
+#pragma unroll
+            for (int j = 0; j < 16; ++j) v[j] += s_b2[g * 16 + j];
+          }
+          uint32_t neg = 0;
+#pragma unroll
+          for (int j = 15; j >= 0; --j) neg = __funnelshift_l(__float_as_uint(v[j]), neg, 1);
+          mask2[r >> 1] |= (~neg & 0xffffu) << ((r & 1) * 16);
+        }
+      }
+      wait_mma();  // B1: W3^T g3 in RA
+      // ---- D3 (RA): g2 = mask2 ? D3 : 0 -> ACT (N2 columns), per round: B2 streams on them
+#pragma unroll
+      for (int r = 0; r < 4; ++r) {
+        const int g = 4 * r + q;
+        if (4 * r < G2) {
+          if (g < G2) {
+            float v[16];
+            tmem_ld16(tRA + tq + (uint32_t)(g * 16), v);
+            tmem_ld_wait();
+            const uint32_t bits = mask2[r >> 1] >> ((r & 1) * 16);
+#pragma unroll
+            for (int j = 0; j < 16; ++j) v[j] = ((bits >> j) & 1u) ? v[j] : 0.f;
+            st8f(row_n2, 2 * g, v);
+            st8f(row_n2, 2 * g + 1, v + 8);
+          }
+          round_done();
+        }
+      }
+      const bool more = t + (int)gridDim.x < p.ntiles;
+      if (more) load_z16(t + (int)gridDim.x);  // next tile's z (in flight during B2 / D4 / B3)
+      wait_mma();  // B2: W2^T g2 in RB
+      // ---- D4 (RB): g1 = mask1 ? D4 : 0 -> ACT (N1 columns), per round: B3 streams on them
+#pragma unroll
+      for (int r = 0; r < 4; ++r) {
+        const int g = 4 * r + q;
+        if (4 * r < G1) {
+          if (g < G1) {
+            float v[16];
+            tmem_ld16(tRB + tq + (uint32_t)(g * 16), v);
+            tmem_ld_wait();
+            const uint32_t bits = mask1[r >> 1] >> ((r & 1) * 16);
+#pragma unroll
+            for (int j = 0; j < 16; ++j) v[j] = ((bits >> j) & 1u) ? v[j] : 0.f;
+            st8f(row_n1, 2 * g, v);
+            st8f(row_n1, 2 * g + 1, v + 8);
+          }
+          round_done();
+        }
+      }
+      wait_mma();  // B3: W1^T g1 in RC; ACT is free
+      if (more) store_z();  // the next tile's F1 (RA) overlaps this tile's dL/dz drain (RC)
+      // ---- D5 (RC) -> dL/dz, unscaled (coalesced: lanes are consecutive pixels)
+      if (q < Gz) {
+        const float u1 = exp2i(-e1), u2 = exp2i(-e2);
         float v[16];
-        tmem_ld16(tq + (uint32_t)(g * 16), v);
+        tmem_ld16(tRC + tq + (uint32_t)(q * 16), v);
         tmem_ld_wait();
-        if (!kFold) {
+        if (valid) {
+          float* ptr = p.gz + (size_t)b * p.n_in * HW + px + (size_t)(q * 16) * HW;
+          const int nv = p.n_in - q * 16;
+          if (nv >= 16) {  // (two in-range power-of-two factors, as the scaling)
 #pragma unroll
-          for (int j = 0; j < 16; ++j) v[j] += s_b1[g * 16 + j];
-        }
-        uint32_t bits = 0;
+            for (int j = 0; j < 16; ++j, ptr += HW) __stcs(ptr, v[j] * u1 * u2);
+          } else {
 #pragma unroll
-        for (int j = 0; j < 16; ++j) bits |= (v[j] > 0.f ? 1u : 0u) << j;
-        mask1[i >> 1] |= bits << ((i & 1) * 16);
-        st8(row_n1, 2 * g, relu2(v[0], v[1]), relu2(v[2], v[3]), relu2(v[4], v[5]), relu2(v[6], v[7]));
-        st8(row_n1, 2 * g + 1, relu2(v[8], v[9]), relu2(v[10], v[11]), relu2(v[12], v[13]), relu2(v[14], v[15]));
-      }
-    }
-    publish();
-    if (warp == 0) {
-      tc_fence_after();
-      gemm(tmem + 256u, act_s, p.N1 / 16, w2_s, 128u, (uint32_t)p.N1 * 16u, 256u, id_f2);
-      umma_commit_elect(bar_mma);
-    }
-    // per-pixel power-of-two scale of dL/dbeta (the four quarters agree through s_max)
-    float mx = 0.f;
-#pragma unroll
-    for (int i = 0; i < 4; ++i)
-#pragma unroll
-      for (int j = 0; j < 8; ++j) mx = fmaxf(mx, fabsf(gv[i][j]));
-    s_max[q * 128 + m] = mx;
-    mbar_wait(bar_mma, ph);  // F2 done: ACT is free
-    ph ^= 1;
-    tc_fence_after();
-    __syncthreads();
-    mx = fmaxf(fmaxf(s_max[m], s_max[128 + m]), fmaxf(s_max[256 + m], s_max[384 + m]));
-    // mx = f 2^ex with f in [0.5, 1) (normal mx; 0 and subnormals take ex = -126, inf/NaN 129):
-    // scale by 2^-ex and back by 2^ex, each as two in-range power-of-two factors (exact)
-    const int ex = (int)((__float_as_uint(mx) >> 23) & 0xffu) - 126;
-    const int e1 = (-ex) / 2, e2 = -ex - e1;
-    const float s1 = exp2i(e1), s2 = exp2i(e2);
-    // ---- scaled dL/dbeta -> ACT (Nk columns)
-#pragma unroll
-    for (int i = 0; i < 4; ++i) {
-      const int c = 4 * i + q;
-      if (c * 8 < p.Nk) {
-        float v[8];
-#pragma unroll
-        for (int j = 0; j < 8; ++j) v[j] = gv[i][j] * s1 * s2;
-        st8f(row_nk, c, v);
-      }
-    }
-    publish();
-    if (warp == 0) {
-      tc_fence_after();
-      gemm(tmem, act_s, p.Nk / 16, w3_s, 128u, (uint32_t)p.Nk * 16u, 256u, id_f2);
-      umma_commit_elect(bar_mma);
-    }
-    mbar_wait(bar_mma, ph);
-    ph ^= 1;
-    tc_fence_after();
-    // ---- drain D2 (pre2) and D3 (W3^T g3): g2 = (pre2 > 0) ? D3 : 0 -> ACT (N2 columns)
-#pragma unroll
-    for (int i = 0; i < 4; ++i) {
-      const int g = 4 * i + q;
-      if (g * 16 < p.N2) {
-        float v2[16], v3[16];
-        tmem_ld16(tq + 256u + (uint32_t)(g * 16), v2);
-        tmem_ld16(tq + (uint32_t)(g * 16), v3);
-        tmem_ld_wait();
-#pragma unroll
-        for (int j = 0; j < 16; ++j) v3[j] = (v2[j] + (kFold ? 0.f : s_b2[g * 16 + j]) > 0.f) ? v3[j] : 0.f;
-        st8f(row_n2, 2 * g, v3);
-        st8f(row_n2, 2 * g + 1, v3 + 8);
-      }
-    }
-    publish();
-    if (warp == 0) {
-      tc_fence_after();
-      gemm(tmem + 256u, act_s, p.N2 / 16, w2_s, (uint32_t)p.N1 * 16u, 128u, (uint32_t)p.N1 * 32u, id_b2);
-      umma_commit_elect(bar_mma);
-    }
-    mbar_wait(bar_mma, ph);
-    ph ^= 1;
-    tc_fence_after();
-    // ---- drain D4 (W2^T g2): g1 = mask1 ? D4 : 0 -> ACT (N1 columns)
-#pragma unroll
-    for (int i = 0; i < 4; ++i) {
-      const int g = 4 * i + q;
-      if (g * 16 < p.N1) {
-        float v[16];
-        tmem_ld16(tq + 256u + (uint32_t)(g * 16), v);
-        tmem_ld_wait();
-        const uint32_t bits = mask1[i >> 1] >> ((i & 1) * 16);
-#pragma unroll
-        for (int j = 0; j < 16; ++j) v[j] = ((bits >> j) & 1u) ? v[j] : 0.f;
-        st8f(row_n1, 2 * g, v);
-        st8f(row_n1, 2 * g + 1, v + 8);
-      }
-    }
-    publish();
-    if (warp == 0) {
-      tc_fence_after();
-      gemm(tmem, act_s, p.N1 / 16, w1_s, (uint32_t)p.K1 * 16u, 128u, (uint32_t)p.K1 * 32u, id_b3);
-      umma_commit_elect(bar_mma);
-    }
-    if (t + (int)gridDim.x < p.ntiles) load_z(p, t + (int)gridDim.x, m, q, zv);  // next tile's z
-    mbar_wait(bar_mma, ph);
-    ph ^= 1;
-    tc_fence_after();
-    // ---- drain D5 (W1^T g1) -> dL/dz, unscaled (coalesced: lanes are consecutive pixels)
-    if (q * 16 < p.K1) {
-      const float u1 = exp2i(-e1), u2 = exp2i(-e2);
-      float* gzb = p.gz + (size_t)b * p.n_in * HW + px;
-      float v[16];
-      tmem_ld16(tq + (uint32_t)(q * 16), v);
-      tmem_ld_wait();
-      if (valid) {
-        float* ptr = gzb + (size_t)(q * 16) * HW;
-        const int nv = p.n_in - q * 16;
-        if (nv >= 16) {  // (two in-range power-of-two factors, as the scaling)
-#pragma unroll
-          for (int j = 0; j < 16; ++j, ptr += HW) __stcs(ptr, v[j] * u1 * u2);
-        } else {
-#pragma unroll
-          for (int j = 0; j < 16; ++j, ptr += HW)
-            if (j < nv) __stcs(ptr, v[j] * u1 * u2);
+            for (int j = 0; j < 16; ++j, ptr += HW)
+              if (j < nv) __stcs(ptr, v[j] * u1 * u2);
+          }
         }
       }
+      tc_fence_before();  // RC reads before the next tile's B3 (ordered by its D4 rounds)
     }
-    tc_fence_before();  // TMEM reads before the next tile's F1 (ordered by its publish())
   }
   tc_fence_before();
   __syncthreads();

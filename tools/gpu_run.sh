@@ -1,5 +1,6 @@
-for lib in paper_2107_11627_b200/libp2s.so paper_2107_11627_b200/abl_seq.so; do
-P2S_LIB=$lib python bench.py --steps 20 --warmup 3 --no-cpu-baseline --no-e2e --no-configs --no-anchor-mode --no-batch-mode --no-adjoint-mode 2>&1 | tail -1 | python -c "
-import json,sys; d=json.loads(sys.stdin.read())
-print('$lib', 'render', round(d['value']), 'seq', round(d['sequence_mode']['value']), 'color', round(d['color_mode']['value']))" || true
-done
+# scratch driver of one gpurun call
+cd $GRAFT_REPO_ROOT
+timeout 600 python -m pytest tests -m gpu -x -q -k "mlp_backward or backward_anchors or adjoint_chain or envelope or color" > gpurun_out/dz_tests.log 2>&1; echo "pytest rc=$?"
+tail -3 gpurun_out/dz_tests.log
+timeout 300 python tools/dz_time.py > gpurun_out/dz_time.log 2>&1; echo "dz rc=$?"
+tail -2 gpurun_out/dz_time.log
