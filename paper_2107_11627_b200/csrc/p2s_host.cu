@@ -153,7 +153,7 @@ struct p2s_handle {
   PFN_cuTensorMapEncodeTiled encode = nullptr;
   // dL/dz (k_mlp_backward): resident weight pack and its shared-memory plan (mb_ok = it fits)
   uint8_t* d_mlpb = nullptr;
-  int mb_col_b = 0, mb_col_c = 0;
+  int mb_col_b = 0, mb_col_c = 0, mb_off_z = 0;
   int mb_ok = 0, mb_fold = 0, mb_stream = 0, mb_g3 = 1, mb_nring = 0, mb_slot = 0, mb_off_ring = 0, mb_ring_src_off = 0,
       mb_smem = 0, mb_off_w2 = 0, mb_off_w3 = 0, mb_off_bias = 0, mb_wbytes = 0, mb_off_act = 0, mb_off_bar = 0;
   MlpOp ops[kMaxOps];  // [0, n_ops) per-tile ops, then n_fops first-tile whole-layer ops
@@ -895,6 +895,12 @@ p2s_status p2s_init(const p2s_basis* basis, const p2s_mlp* mlp, p2s_handle** out
         h->mb_off_bar = h->mb_off_act + act_bytes;
         h->mb_col_b = col_b;
         h->mb_col_c = col_c;
+        // the z tile's own buffer after s_max, where it fits
+        const int off_z = al128(h->mb_off_bar + 64 + 4 * 128 * 4);
+        if (std::getenv("P2S_MB_NOZSEP") == nullptr && off_z + 128 * K1 * 2 <= kSmemLimit) {
+          h->mb_off_z = off_z;
+          h->mb_smem = off_z + 128 * K1 * 2;
+        }
       } else {
         // slab table, per tile: [F1: W1 K-slabs | F2: W2 K-slabs | B1: W3^T K-slabs | B2: W2 row
         // pairs (W2^T K'-slabs) | B3: W1 row pairs, g3 per slot]; K-slabs re-laid [N][16]
@@ -1203,7 +1209,7 @@ p2s_status p2s_mlp_backward(p2s_handle* h, const float* zernike_field, const flo
   p.ntiles = (int)(tpf * B);
   p.off_w2 = h->mb_off_w2; p.off_w3 = h->mb_off_w3; p.off_bias = h->mb_off_bias; p.wbytes = h->mb_wbytes;
   p.off_act = h->mb_off_act; p.off_bar = h->mb_off_bar;
-  p.col_b = h->mb_col_b; p.col_c = h->mb_col_c;
+  p.col_b = h->mb_col_b; p.col_c = h->mb_col_c; p.off_z = h->mb_off_z;
   cudaStream_t st = (cudaStream_t)stream;
   if (h->mb_stream) {
     p.ring_src = h->d_mlpb + h->mb_ring_src_off;

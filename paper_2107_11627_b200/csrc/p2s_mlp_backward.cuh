@@ -55,6 +55,7 @@ struct MlpbParams {
   int off_w2, off_w3, off_bias, wbytes;  // byte offsets in wpack (= in shared memory)
   int off_act, off_bar;
   int col_b, col_c;     // resident variant: TMEM columns of the RB / RC accumulator regions
+  int off_z;            // resident variant: the z tile's own buffer (0: z goes into ACT)
   // streamed variant (k_mlp_backward_s): the slab table and the ring (B3's W1^T K'-steps are
   // small, K1 x 32 B: g3 of them share one slot, contiguous in W1's layout)
   const uint8_t* ring_src;
@@ -139,25 +140,59 @@ P2S_DEV void load8(const float* ptr, size_t stride, int nvalid, float (&v)[8]) {
     for (int j = 0; j < 8; ++j, ptr += stride) v[j] = j < nvalid ? __ldcs(ptr) : 0.f;
   }
 }
+// 16 channels (nvalid real, the rest 0) of one pixel, strideB bytes apart (a warp-uniform 64-bit
+// increment per load: two integer instructions instead of an index product and a shift)
+P2S_DEV void load16b(const float* ptr, size_t strideB, int nvalid, float* v) {
+  const char* c = reinterpret_cast<const char*>(ptr);
+  if (nvalid >= 16) {
+#pragma unroll
+    for (int j = 0; j < 16; ++j) {
+      v[j] = __ldcs(reinterpret_cast<const float*>(c));
+      asm volatile("" : "+l"(c));  // one running pointer (no precomputed address per load)
+      c += strideB;
+    }
+  } else {
+#pragma unroll
+    for (int j = 0; j < 16; ++j, c += strideB) v[j] = j < nvalid ? __ldcs(reinterpret_cast<const float*>(c)) : 0.f;
+  }
+}
+// 16 fp32 values -> bits j = [v_j >= +0] (sign bits by two 8-deep funnel-shift chains)
+P2S_DEV uint32_t nonneg_bits16(const float (&v)[16]) {
+  uint32_t lo = 0, hi = 0;
+#pragma unroll
+  for (int j = 7; j >= 0; --j) {
+    lo = __funnelshift_l(__float_as_uint(v[j]), lo, 1);
+    hi = __funnelshift_l(__float_as_uint(v[j + 8]), hi, 1);
+  }
+  return ~(lo | (hi << 8)) & 0xffffu;
+}
+
 template <bool kFold>
 __global__ void __launch_bounds__(kMbThreads, 1) k_mlp_backward(const __grid_constant__ MlpbParams p) {
   using namespace mlpb;
   extern __shared__ __align__(1024) uint8_t smem[];
   const uint32_t sbase = smem_u32(smem);
   uint64_t* bar_w = reinterpret_cast<uint64_t*>(smem + p.off_bar);
-  uint64_t* bar_mma = bar_w + 1;
-  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bar_mma + 1);
+  uint64_t* bar_mma = bar_w + 1;                                   // F2, B1, B2, B3 done
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bar_w + 2);
+  uint64_t* bar_f1 = bar_w + 3;                                    // F1 done
   uint64_t* bar_rnd = bar_w + 4;                                   // [4] operand-round ring
   float* s_max = reinterpret_cast<float*>(smem + p.off_bar + 64);  // [4][128]
   const float* s_b1 = reinterpret_cast<const float*>(smem + p.off_bias);
   const float* s_b2 = s_b1 + p.N1;
   uint8_t* act = smem + p.off_act;
   const uint32_t act_s = sbase + (uint32_t)p.off_act;
+  // z tile: its own buffer when it fits (the next tile's F1 then runs right behind this tile's
+  // B3), else the first K1 columns of ACT
+  const bool zsep = p.off_z > 0;
+  uint8_t* zbuf = zsep ? smem + p.off_z : act;
+  const uint32_t z_s = sbase + (uint32_t)(zsep ? p.off_z : p.off_act);
   const int tid = (int)threadIdx.x, warp = (int)warp_id();
 
   if (tid == 0) {
     mbar_init(bar_w, 1);
     mbar_init(bar_mma, 1);
+    mbar_init(bar_f1, 1);
     for (int i = 0; i < 4; ++i) mbar_init(&bar_rnd[i], kMbDrainWarps);
     fence_mbar_init();
   }
@@ -184,40 +219,42 @@ __global__ void __launch_bounds__(kMbThreads, 1) k_mlp_backward(const __grid_con
     const uint32_t id_b3 = idesc_f16(128, (uint32_t)p.K1) | (1u << 16);
     const uint32_t w1_s = sbase, w2_s = sbase + (uint32_t)p.off_w2, w3_s = sbase + (uint32_t)p.off_w3;
     uint32_t rs = 0;
-    auto gemm_rounds = [&](uint32_t d, int nks, uint32_t b_s, uint32_t b_lbo, uint32_t b_sbo, uint32_t b_kstep,
-                           uint32_t idesc) {
+    auto gemm_rounds = [&](uint32_t d, uint32_t a_s, int nks, uint32_t b_s, uint32_t b_lbo, uint32_t b_sbo,
+                           uint32_t b_kstep, uint32_t idesc, uint64_t* done) {
       const uint32_t a_sbo = (uint32_t)nks * 256u;
       for (int k0 = 0; k0 < nks; k0 += 4, ++rs) {
         mbar_wait(&bar_rnd[rs & 3u], (rs >> 2) & 1u);
         tc_fence_after();
         const int k1 = min(nks, k0 + 4);
         for (int ks = k0; ks < k1; ++ks)
-          umma_f16_elect(d, sdesc(act_s + (uint32_t)ks * 256u, 128u, a_sbo),
+          umma_f16_elect(d, sdesc(a_s + (uint32_t)ks * 256u, 128u, a_sbo),
                          sdesc(b_s + (uint32_t)ks * b_kstep, b_lbo, b_sbo), idesc, ks > 0 ? 1u : 0u);
       }
-      umma_commit_elect(bar_mma);
+      umma_commit_elect(done);
     };
     if ((int)blockIdx.x < p.ntiles) mbar_wait(bar_w, 0);
     for (int t = (int)blockIdx.x; t < p.ntiles; t += (int)gridDim.x) {
-      gemm_rounds(tRA, p.K1 / 16, w1_s, 128u, (uint32_t)p.K1 * 16u, 256u, id_f1);   // F1 <- z
-      gemm_rounds(tRB, p.N1 / 16, w2_s, 128u, (uint32_t)p.N1 * 16u, 256u, id_f2);   // F2 <- a1
-      gemm_rounds(tRA, p.Nk / 16, w3_s, 128u, (uint32_t)p.Nk * 16u, 256u, id_f2);   // B1 <- g3
-      gemm_rounds(tRB, p.N2 / 16, w2_s, (uint32_t)p.N1 * 16u, 128u, (uint32_t)p.N1 * 32u, id_b2);  // B2 <- g2
-      gemm_rounds(tRC, p.N1 / 16, w1_s, (uint32_t)p.K1 * 16u, 128u, (uint32_t)p.K1 * 32u, id_b3);  // B3 <- g1
+      gemm_rounds(tRA, z_s, p.K1 / 16, w1_s, 128u, (uint32_t)p.K1 * 16u, 256u, id_f1, bar_f1);       // F1 <- z
+      gemm_rounds(tRB, act_s, p.N1 / 16, w2_s, 128u, (uint32_t)p.N1 * 16u, 256u, id_f2, bar_mma);    // F2 <- a1
+      gemm_rounds(tRA, act_s, p.Nk / 16, w3_s, 128u, (uint32_t)p.Nk * 16u, 256u, id_f2, bar_mma);    // B1 <- g3
+      gemm_rounds(tRB, act_s, p.N2 / 16, w2_s, (uint32_t)p.N1 * 16u, 128u, (uint32_t)p.N1 * 32u, id_b2,
+                  bar_mma);  // B2 <- g2 (W2 transposed)
+      gemm_rounds(tRC, act_s, p.N1 / 16, w1_s, (uint32_t)p.K1 * 16u, 128u, (uint32_t)p.K1 * 32u, id_b3,
+                  bar_mma);  // B3 <- g1 (W1 transposed)
     }
   } else {
     // ================= drains: 4 threads per pixel row (TMEM lane); thread q of a row owns the
     // 16-column groups g = 4 r + q (round r)
     const int m = tid & 127, q = tid >> 7;
     const uint32_t tq = (uint32_t)(32 * (warp & 3)) << 16;  // this warp's lane quadrant
-    const size_t HW = (size_t)p.HW;
-    uint8_t* const row_k1 = row_of(act, m, p.K1);
+    const size_t HW = (size_t)p.HW, HWB = HW * 4;
+    uint8_t* const row_k1 = row_of(zbuf, m, p.K1);
     uint8_t* const row_n1 = row_of(act, m, p.N1);
     uint8_t* const row_n2 = row_of(act, m, p.N2);
     uint8_t* const row_nk = row_of(act, m, p.Nk);
     const int G1 = p.N1 / 16, G2 = p.N2 / 16, Gk = p.Nk / 16, Gz = p.K1 / 16;
-    uint32_t ph = 0, rs = 0;
-    // publish this warp's part of one round: generic-proxy ACT writes and TMEM reads are ordered
+    uint32_t ph = 0, ph1 = 0, rs = 0;
+    // publish this warp's part of one round: generic-proxy writes and TMEM reads are ordered
     // before the UMMAs the issuer starts on the round's barrier
     auto round_done = [&] {
       fence_proxy_async_smem();
@@ -231,14 +268,17 @@ __global__ void __launch_bounds__(kMbThreads, 1) k_mlp_backward(const __grid_con
       ph ^= 1;
       tc_fence_after();
     };
-    // z of tile t -> ACT (K1 <= 64: one round; kFold: columns n_in, n_in + 1 = 1, padding zeros)
+    // tile t = (frame b, tile lt of the frame), advanced by the grid stride without divisions
+    int b = (int)blockIdx.x / p.tiles_per_frame, lt = (int)blockIdx.x - b * p.tiles_per_frame;
+    auto advance = [&](int& bb, int& ll) {
+      ll += (int)gridDim.x;
+      while (ll >= p.tiles_per_frame) { ll -= p.tiles_per_frame; ++bb; }
+    };
+    // z of a tile -> the z buffer (K1 <= 64: one round; kFold: columns n_in, n_in + 1 = 1)
     float zv[16];
-    auto load_z16 = [&](int t) {
-      const int b = t / p.tiles_per_frame;
-      const int px = min((t - b * p.tiles_per_frame) * 128 + m, p.HW - 1);
-      const float* zb = p.z + (size_t)b * p.n_in * HW + px + (size_t)(q * 16) * HW;
-      load8(zb, HW, p.n_in - q * 16, *reinterpret_cast<float(*)[8]>(zv));
-      load8(zb + 8 * HW, HW, p.n_in - q * 16 - 8, *reinterpret_cast<float(*)[8]>(zv + 8));
+    auto load_z16 = [&](int bb, int ll) {
+      const int px = min(ll * 128 + m, p.HW - 1);
+      load16b(p.z + (size_t)bb * p.n_in * HW + px + (size_t)(q * 16) * HW, HWB, p.n_in - q * 16, zv);
     };
     auto store_z = [&] {
       if (q < Gz) {
@@ -252,22 +292,22 @@ __global__ void __launch_bounds__(kMbThreads, 1) k_mlp_backward(const __grid_con
       }
       round_done();
     };
-    load_z16((int)blockIdx.x);
+    load_z16(b, lt);
     store_z();
     if (!kFold) mbar_wait(bar_w, 0);  // the fp32 biases the drains add
     for (int t = (int)blockIdx.x; t < p.ntiles; t += (int)gridDim.x) {
-      const int b = t / p.tiles_per_frame;
-      const int px = (t - b * p.tiles_per_frame) * 128 + m;
+      const int px = lt * 128 + m;
       const bool valid = px < p.HW;
       const int pxc = valid ? px : p.HW - 1;
-      {  // L2 prefetch of the next tile's dL/dbeta rows (4 lines of 128 B per channel)
-        const int tn = t + (int)gridDim.x;
-        if (tn < p.ntiles) {
-          const int bn = tn / p.tiles_per_frame, p0 = (tn - bn * p.tiles_per_frame) * 128;
-          for (int r = tid; r < 4 * p.K; r += kMbDrainWarps * 32) {
-            const int qq = p0 + (r & 3) * 32;
-            if (qq < p.HW) prefetch_l2(p.gb + ((size_t)bn * p.K + (r >> 2)) * HW + qq);
-          }
+      int bn = b, ltn = lt;
+      advance(bn, ltn);
+      const bool more = t + (int)gridDim.x < p.ntiles;
+      if (more) {  // L2 prefetch of the next tile's dL/dbeta rows (4 lines of 128 B per channel)
+        const int p0 = ltn * 128;
+        const float* gn = p.gb + (size_t)bn * p.K * HW + p0;
+        for (int r = tid; r < 4 * p.K; r += kMbDrainWarps * 32) {
+          const int qq = p0 + (r & 3) * 32;
+          if (qq < p.HW) prefetch_l2(gn + (size_t)(r >> 2) * HW + (r & 3) * 32);
         }
       }
       // ---- dL/dbeta of this tile into registers (in flight during F1 / D1 / F2): groups 4 r + q
@@ -277,11 +317,12 @@ __global__ void __launch_bounds__(kMbThreads, 1) k_mlp_backward(const __grid_con
 #pragma unroll
         for (int r = 0; r < 2; ++r) {
           const int c = 16 * (4 * r + q);
-          load8(gbb + (size_t)c * HW, HW, p.K - c, *reinterpret_cast<float(*)[8]>(gv[r]));
-          load8(gbb + (size_t)(c + 8) * HW, HW, p.K - c - 8, *reinterpret_cast<float(*)[8]>(gv[r] + 8));
+          load16b(gbb + (size_t)c * HW, HWB, p.K - c, gv[r]);
         }
       }
-      wait_mma();  // F1
+      mbar_wait(bar_f1, ph1);  // F1
+      ph1 ^= 1;
+      tc_fence_after();
       // ---- D1 (RA): a1 = relu(pre1) -> ACT (N1 columns), mask1 = [pre1 >= +0] sign bits, per round
       uint32_t mask1[2] = {0u, 0u};
 #pragma unroll
@@ -296,10 +337,7 @@ __global__ void __launch_bounds__(kMbThreads, 1) k_mlp_backward(const __grid_con
 #pragma unroll
               for (int j = 0; j < 16; ++j) v[j] += s_b1[g * 16 + j];
             }
-            uint32_t neg = 0;
-#pragma unroll
-            for (int j = 15; j >= 0; --j) neg = __funnelshift_l(__float_as_uint(v[j]), neg, 1);
-            mask1[r >> 1] |= (~neg & 0xffffu) << ((r & 1) * 16);
+            mask1[r >> 1] |= nonneg_bits16(v) << ((r & 1) * 16);
             st8(row_n1, 2 * g, relu2(v[0], v[1]), relu2(v[2], v[3]), relu2(v[4], v[5]), relu2(v[6], v[7]));
             st8(row_n1, 2 * g + 1, relu2(v[8], v[9]), relu2(v[10], v[11]), relu2(v[12], v[13]), relu2(v[14], v[15]));
           }
@@ -351,10 +389,7 @@ __global__ void __launch_bounds__(kMbThreads, 1) k_mlp_backward(const __grid_con
 #pragma unroll
             for (int j = 0; j < 16; ++j) v[j] += s_b2[g * 16 + j];
           }
-          uint32_t neg = 0;
-#pragma unroll
-          for (int j = 15; j >= 0; --j) neg = __funnelshift_l(__float_as_uint(v[j]), neg, 1);
-          mask2[r >> 1] |= (~neg & 0xffffu) << ((r & 1) * 16);
+          mask2[r >> 1] |= nonneg_bits16(v) << ((r & 1) * 16);
         }
       }
       wait_mma();  // B1: W3^T g3 in RA
@@ -376,8 +411,7 @@ __global__ void __launch_bounds__(kMbThreads, 1) k_mlp_backward(const __grid_con
           round_done();
         }
       }
-      const bool more = t + (int)gridDim.x < p.ntiles;
-      if (more) load_z16(t + (int)gridDim.x);  // next tile's z (in flight during B2 / D4 / B3)
+      if (more) load_z16(bn, ltn);  // next tile's z (in flight during B2 / D4)
       wait_mma();  // B2: W2^T g2 in RB
       // ---- D4 (RB): g1 = mask1 ? D4 : 0 -> ACT (N1 columns), per round: B3 streams on them
 #pragma unroll
@@ -397,8 +431,11 @@ __global__ void __launch_bounds__(kMbThreads, 1) k_mlp_backward(const __grid_con
           round_done();
         }
       }
+      // the next tile's z: with its own buffer now (F1 follows B3 on the tensor core; RA's last
+      // reader, D3, is done), else once B3 has read g1 out of ACT
+      if (more && zsep) store_z();
       wait_mma();  // B3: W1^T g1 in RC; ACT is free
-      if (more) store_z();  // the next tile's F1 (RA) overlaps this tile's dL/dz drain (RC)
+      if (more && !zsep) store_z();
       // ---- D5 (RC) -> dL/dz, unscaled (coalesced: lanes are consecutive pixels)
       if (q < Gz) {
         const float u1 = exp2i(-e1), u2 = exp2i(-e2);
@@ -406,19 +443,21 @@ __global__ void __launch_bounds__(kMbThreads, 1) k_mlp_backward(const __grid_con
         tmem_ld16(tRC + tq + (uint32_t)(q * 16), v);
         tmem_ld_wait();
         if (valid) {
-          float* ptr = p.gz + (size_t)b * p.n_in * HW + px + (size_t)(q * 16) * HW;
+          char* ptr = reinterpret_cast<char*>(p.gz + (size_t)b * p.n_in * HW + px + (size_t)(q * 16) * HW);
           const int nv = p.n_in - q * 16;
           if (nv >= 16) {  // (two in-range power-of-two factors, as the scaling)
 #pragma unroll
-            for (int j = 0; j < 16; ++j, ptr += HW) __stcs(ptr, v[j] * u1 * u2);
+            for (int j = 0; j < 16; ++j, ptr += HWB) __stcs(reinterpret_cast<float*>(ptr), v[j] * u1 * u2);
           } else {
 #pragma unroll
-            for (int j = 0; j < 16; ++j, ptr += HW)
-              if (j < nv) __stcs(ptr, v[j] * u1 * u2);
+            for (int j = 0; j < 16; ++j, ptr += HWB)
+              if (j < nv) __stcs(reinterpret_cast<float*>(ptr), v[j] * u1 * u2);
           }
         }
       }
       tc_fence_before();  // RC reads before the next tile's B3 (ordered by its D4 rounds)
+      b = bn;
+      lt = ltn;
     }
   }
   tc_fence_before();
