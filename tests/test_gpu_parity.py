@@ -72,6 +72,10 @@ SMALL = {
                                   t_std=1.2),
     "many_tiles_C1_S9": synth.custom("mt1", 212, B=3, C=1, H=200, W=257, K=24, S=9, h1=40, h2=40,
                                      t_std=2.2),
+    # a wide first hidden layer with n_in = 40: the resident dL/dz kernel's RB region starts at
+    # column max(N1, N2) instead of 256 (max(N1, N2) + K1 > 256), unfolded biases
+    "h224_n40": synth.custom("h224", 216, B=1, C=1, H=20, W=300, K=16, S=5, n_in=40, h1=224, h2=32,
+                             t_std=1.0),
 }
 # Degenerate 1x1 frames: every tap reads the same pixel, so J = I * sum_k beta_k s_k is tiny
 # (rms 0.04) and its relative L2 error is the fp16 rounding of (I - 0.5) divided by I --
@@ -877,7 +881,7 @@ def test_large_ragged_frame_sampled(p2s):
 #      oracle.adjoint.mlp_backward with the masks decided in the GPU's fp16 precision (reading N5)
 
 DZ_CASES = ["cfg1", "ragged_rgb_S7", "narrow_S15_K16", "S33_K100_C2", "S1_K1", "S17_K128_n64", "S25", "W1_H1",
-            "many_tiles_C1_S9", "tiny_widths"]
+            "many_tiles_C1_S9", "tiny_widths", "h224_n40"]
 
 
 def _dz_ref(inp, gbeta, amb_rel=(2e-5, 2e-4)):
