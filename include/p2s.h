@@ -148,13 +148,15 @@ P2S_API p2s_status p2s_render_color(p2s_handle* h, p2s_image image, const float*
  *   grad_image (DEVICE [B][C][H][W] or NULL) = dL/dI_c(q) = sum over the taps that read q (after
  *     the replicate clamp) of phi_k[i][j] beta_k(p) dL/dJ_c(p): the transpose of Eq. 5's
  *     beta-weighted convolution ("scatter order"), on the tensor cores with U = beta dL/dJ
- *     rounded to fp16 (|beta dL/dJ| must stay below 65504)
+ *     rounded to fp16 after scaling each (frame, channel) plane by a power of two (any finite
+ *     grad_out range; the sums are scaled back)
  * where dL/dJ scatters grad_out through the warp's bilinear weights (float atomics: the
  * summation order, hence the last bits, vary run to run; grad_image's border pixels likewise).
  * grad_beta recomputes the K convolutions on the tensor cores; grad_tilt also recomputes J (one
- * forward); grad_image recomputes beta (one MLP pass) and needs workspace for beta [B][K][H][W]
- * fp32 and U [B][C][K][W][ceil8(H)] fp16 (grown on first use: synchronising, like p2s_render's).
- * Errors as p2s_render; all three outputs NULL -> P2S_ERR_INVALID_ARG. */
+ * forward); grad_image recomputes beta (one MLP pass, in the forward's fused kernel) and needs
+ * workspace for dL/dJ [B][C][H][W] fp32 and U [B][C][K][H][ceil8(W)] fp16 (grown on first use:
+ * synchronising, like p2s_render's; p2s_reserve_ex pre-sizes them). Errors as p2s_render; all
+ * three outputs NULL, or an output overlapping an input or another output -> P2S_ERR_INVALID_ARG. */
 P2S_API p2s_status p2s_backward(p2s_handle* h, p2s_image image, const float* zernike_field,
                                 const float* tilt_field, const float* grad_out, float* grad_beta,
                                 float* grad_tilt, float* grad_image, p2s_stream_t stream);
@@ -246,8 +248,24 @@ P2S_API p2s_status p2s_sample_anchors(p2s_sampler* s, unsigned long long seed, i
                                       float* anchors, p2s_stream_t stream);
 P2S_API void p2s_sampler_destroy(p2s_sampler* s);
 
-/* Pre-sizes the workspace (and host-path staging) for frames up to B x C x H x W. */
+/* Pre-sizes the render workspace (J, B*C*H*W fp32) for frames up to B x C x H x W, so that later
+ * p2s_render / p2s_render_sequence / p2s_render_color calls of that size neither allocate nor
+ * synchronise (and can be captured in a CUDA graph). Synchronises the device when it grows the
+ * workspace. Errors: NULL handle or a size < 1 -> P2S_ERR_INVALID_ARG; P2S_ERR_CUDA / OOM. */
 P2S_API p2s_status p2s_reserve(p2s_handle* h, int B, int C, int H, int W);
+
+/* p2s_reserve with a choice of workspaces (bitwise OR of P2S_RESERVE_*), for frames up to
+ * B x C x H x W: RENDER = the render workspace (as p2s_reserve); HOST = also the device staging
+ * of p2s_render_host / p2s_render_anchors_host (image, out, Zernike field, tilt) and its input
+ * stream; ADJOINT = also p2s_backward's dL/dJ buffer (enough for grad_beta / grad_tilt);
+ * ADJOINT_IMAGE = also its grad_image workspaces (U = beta dL/dJ, fp16 [B][C][K][H][ceil8(W)],
+ * and the per-(frame, channel) range exponents). After it, calls of at most that size allocate
+ * nothing and do not synchronise. Errors: as p2s_reserve; unknown bits -> P2S_ERR_INVALID_ARG. */
+#define P2S_RESERVE_RENDER 1u
+#define P2S_RESERVE_HOST 2u
+#define P2S_RESERVE_ADJOINT 4u
+#define P2S_RESERVE_ADJOINT_IMAGE 8u
+P2S_API p2s_status p2s_reserve_ex(p2s_handle* h, int B, int C, int H, int W, unsigned what);
 
 /* When both events are non-NULL, every later p2s_render records ev_begin right before the
  * fused MLP+convolution kernel and ev_end right after it on the render stream (so its

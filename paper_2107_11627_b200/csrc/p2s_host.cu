@@ -199,6 +199,63 @@ p2s_status ensure_J(p2s_handle* h, size_t n) {
   return P2S_OK;
 }
 
+// Device staging of the host path (p2s_render_host): image, out [chw], Zernike [px n_in], tilt
+// [2 px], plus its input stream and events. Growing synchronises the device.
+p2s_status ensure_stage(p2s_handle* h, size_t px, size_t chw) {
+  if (px > h->stage_px_cap || chw > h->stage_chw_cap) {
+    P2S_CUDA(cudaDeviceSynchronize());
+    cudaFree(h->h_img); cudaFree(h->h_z); cudaFree(h->h_t); cudaFree(h->h_out);
+    h->h_img = h->h_z = h->h_t = h->h_out = nullptr;
+    h->stage_px_cap = h->stage_chw_cap = 0;
+    P2S_CUDA(cudaMalloc(&h->h_img, chw * 4));
+    P2S_CUDA(cudaMalloc(&h->h_out, chw * 4));
+    P2S_CUDA(cudaMalloc(&h->h_z, px * h->n_in * 4));
+    P2S_CUDA(cudaMalloc(&h->h_t, px * 2 * 4));
+    h->stage_px_cap = px;
+    h->stage_chw_cap = chw;
+  }
+  if (!h->s_in) {
+    P2S_CUDA(cudaStreamCreateWithFlags(&h->s_in, cudaStreamNonBlocking));
+    P2S_CUDA(cudaEventCreateWithFlags(&h->ev_entry, cudaEventDisableTiming));
+    P2S_CUDA(cudaEventCreateWithFlags(&h->ev_band, cudaEventDisableTiming));
+  }
+  return P2S_OK;
+}
+
+// Adjoint workspaces (p2s_backward): dL/dJ [chw] fp32; with dL/dI also U = beta dL/dJ fp16
+// [B C K H Ws] and the per-(frame, channel) range exponents. Growing synchronises the device.
+p2s_status ensure_adjoint(p2s_handle* h, int B, int C, int H, int W, bool image) {
+  const size_t chw = (size_t)B * C * H * W;
+  if (chw > h->gJ_cap) {
+    P2S_CUDA(cudaDeviceSynchronize());
+    cudaFree(h->d_gJ);
+    h->d_gJ = nullptr;
+    h->gJ_cap = 0;
+    P2S_CUDA(cudaMalloc(&h->d_gJ, chw * sizeof(float)));
+    h->gJ_cap = chw;
+  }
+  if (!image) return P2S_OK;
+  const size_t nu = (size_t)B * C * h->K * H * (size_t)((W + 7) / 8 * 8);
+  if (nu > h->ut_cap) {
+    P2S_CUDA(cudaDeviceSynchronize());
+    cudaFree(h->d_ut);
+    h->d_ut = nullptr;
+    h->ut_cap = 0;
+    P2S_CUDA(cudaMalloc(&h->d_ut, nu * sizeof(__half)));
+    h->ut_cap = nu;
+  }
+  const size_t nbc = (size_t)B * C;
+  if (nbc > h->umax_cap) {
+    P2S_CUDA(cudaDeviceSynchronize());
+    cudaFree(h->d_umax);
+    h->d_umax = nullptr;
+    h->umax_cap = 0;
+    P2S_CUDA(cudaMalloc(&h->d_umax, nbc * sizeof(uint32_t)));
+    h->umax_cap = nbc;
+  }
+  return P2S_OK;
+}
+
 bool overlaps(const void* a, size_t na, const void* b, size_t nb) {
   if (!a || !b) return false;
   const char *pa = (const char*)a, *pb = (const char*)b;
@@ -968,6 +1025,20 @@ p2s_status p2s_reserve(p2s_handle* h, int B, int C, int H, int W) {
   return ensure_J(h, (size_t)B * C * H * W);
 }
 
+p2s_status p2s_reserve_ex(p2s_handle* h, int B, int C, int H, int W, unsigned what) {
+  if (!h || B < 1 || C < 1 || H < 1 || W < 1 ||
+      (what & ~(unsigned)(P2S_RESERVE_RENDER | P2S_RESERVE_HOST | P2S_RESERVE_ADJOINT | P2S_RESERVE_ADJOINT_IMAGE)))
+    return P2S_ERR_INVALID_ARG;
+  const size_t px = (size_t)B * H * W, chw = px * C;
+  p2s_status s = P2S_OK;
+  if (what & (P2S_RESERVE_RENDER | P2S_RESERVE_HOST | P2S_RESERVE_ADJOINT | P2S_RESERVE_ADJOINT_IMAGE))
+    s = ensure_J(h, chw);
+  if (s == P2S_OK && (what & P2S_RESERVE_HOST)) s = ensure_stage(h, px, chw);
+  if (s == P2S_OK && (what & (P2S_RESERVE_ADJOINT | P2S_RESERVE_ADJOINT_IMAGE)))
+    s = ensure_adjoint(h, B, C, H, W, (what & P2S_RESERVE_ADJOINT_IMAGE) != 0);
+  return s;
+}
+
 p2s_status p2s_set_profile_events(p2s_handle* h, p2s_event_t ev_begin, p2s_event_t ev_end) {
   if (!h || ((ev_begin == nullptr) != (ev_end == nullptr))) return P2S_ERR_INVALID_ARG;
   h->ev_begin = (cudaEvent_t)ev_begin;
@@ -1075,16 +1146,24 @@ p2s_status p2s_backward(p2s_handle* h, p2s_image im, const float* zernike_field,
   if (!zernike_field || !grad_out || (!grad_beta && !grad_tilt && !grad_image)) return P2S_ERR_INVALID_ARG;
   cudaStream_t st = (cudaStream_t)stream;
   const size_t HW = (size_t)im.H * im.W, chw = (size_t)im.B * im.C * HW;
+  {  // outputs must not overlap the inputs (or each other)
+    const size_t nz = (size_t)im.B * h->n_in * HW * 4, nb = (size_t)im.B * h->K * HW * 4, nt = (size_t)im.B * 2 * HW * 4,
+                 ni = chw * 4;
+    const void* in[4] = {im.data, zernike_field, tilt_field, grad_out};
+    const size_t in_n[4] = {ni, nz, nt, ni};
+    const void* outs[3] = {grad_beta, grad_tilt, grad_image};
+    const size_t out_n[3] = {nb, nt, ni};
+    for (int o = 0; o < 3; ++o) {
+      for (int i = 0; i < 4; ++i)
+        if (overlaps(outs[o], out_n[o], in[i], in_n[i])) return P2S_ERR_INVALID_ARG;
+      for (int o2 = o + 1; o2 < 3; ++o2)
+        if (overlaps(outs[o], out_n[o], outs[o2], out_n[o2])) return P2S_ERR_INVALID_ARG;
+    }
+  }
   s = ensure_J(h, chw);
   if (s != P2S_OK) return s;
-  if (chw > h->gJ_cap) {
-    P2S_CUDA(cudaDeviceSynchronize());
-    cudaFree(h->d_gJ);
-    h->d_gJ = nullptr;
-    h->gJ_cap = 0;
-    P2S_CUDA(cudaMalloc(&h->d_gJ, chw * sizeof(float)));
-    h->gJ_cap = chw;
-  }
+  s = ensure_adjoint(h, im.B, im.C, im.H, im.W, grad_image != nullptr);
+  if (s != P2S_OK) return s;
   // dL/dJ: dL/dout scattered through the warp's bilinear weights (needs no J)
   P2S_CUDA(cudaMemsetAsync(h->d_gJ, 0, chw * sizeof(float), st));
   const size_t npx = (size_t)im.B * HW;
@@ -1093,24 +1172,7 @@ p2s_status p2s_backward(p2s_handle* h, p2s_image im, const float* zernike_field,
   P2S_CUDA(cudaPeekAtLastError());
   const int Ws = (im.W + 7) / 8 * 8;
   if (grad_image) {
-    const size_t nu = (size_t)im.B * im.C * h->K * im.H * Ws;
-    if (nu > h->ut_cap) {
-      P2S_CUDA(cudaDeviceSynchronize());
-      cudaFree(h->d_ut);
-      h->d_ut = nullptr;
-      h->ut_cap = 0;
-      P2S_CUDA(cudaMalloc(&h->d_ut, nu * sizeof(__half)));
-      h->ut_cap = nu;
-    }
     const size_t nbc = (size_t)im.B * im.C;
-    if (nbc > h->umax_cap) {
-      P2S_CUDA(cudaDeviceSynchronize());
-      cudaFree(h->d_umax);
-      h->d_umax = nullptr;
-      h->umax_cap = 0;
-      P2S_CUDA(cudaMalloc(&h->d_umax, nbc * sizeof(uint32_t)));
-      h->umax_cap = nbc;
-    }
     // per-(frame, channel) max |dL/dJ|: U = beta dL/dJ is stored in fp16 scaled by a power of two
     // chosen from it, and k_adjoint_image scales its sums back (any finite dL/dout range)
     P2S_CUDA(cudaMemsetAsync(h->d_umax, 0, nbc * sizeof(uint32_t), st));
@@ -1341,23 +1403,8 @@ p2s_status p2s_render_host(p2s_handle* h, const float* image_host, int B, int C,
   if (s != P2S_OK) return s;
   cudaStream_t st = (cudaStream_t)stream;
   const size_t HW = (size_t)H * W, px = (size_t)B * HW, chw = px * C;
-  if (px > h->stage_px_cap || chw > h->stage_chw_cap) {
-    P2S_CUDA(cudaDeviceSynchronize());
-    cudaFree(h->h_img); cudaFree(h->h_z); cudaFree(h->h_t); cudaFree(h->h_out);
-    h->h_img = h->h_z = h->h_t = h->h_out = nullptr;
-    h->stage_px_cap = h->stage_chw_cap = 0;
-    P2S_CUDA(cudaMalloc(&h->h_img, chw * 4));
-    P2S_CUDA(cudaMalloc(&h->h_out, chw * 4));
-    P2S_CUDA(cudaMalloc(&h->h_z, px * h->n_in * 4));
-    P2S_CUDA(cudaMalloc(&h->h_t, px * 2 * 4));
-    h->stage_px_cap = px;
-    h->stage_chw_cap = chw;
-  }
-  if (!h->s_in) {
-    P2S_CUDA(cudaStreamCreateWithFlags(&h->s_in, cudaStreamNonBlocking));
-    P2S_CUDA(cudaEventCreateWithFlags(&h->ev_entry, cudaEventDisableTiming));
-    P2S_CUDA(cudaEventCreateWithFlags(&h->ev_band, cudaEventDisableTiming));
-  }
+  s = ensure_stage(h, px, chw);
+  if (s != P2S_OK) return s;
   s = ensure_J(h, chw);
   if (s != P2S_OK) return s;
   // Pipelined over row bands (inputs are PCIe-bound): the input stream copies
@@ -1446,18 +1493,8 @@ p2s_status p2s_render_anchors_host(p2s_handle* h, const float* image_host, int B
   if (s != P2S_OK) return s;
   cudaStream_t st = (cudaStream_t)stream;
   const size_t HW = (size_t)H * W, px = (size_t)B * HW, chw = px * C, nanc = (size_t)h->n_in * G * G;
-  if (px > h->stage_px_cap || chw > h->stage_chw_cap) {
-    P2S_CUDA(cudaDeviceSynchronize());
-    cudaFree(h->h_img); cudaFree(h->h_z); cudaFree(h->h_t); cudaFree(h->h_out);
-    h->h_img = h->h_z = h->h_t = h->h_out = nullptr;
-    h->stage_px_cap = h->stage_chw_cap = 0;
-    P2S_CUDA(cudaMalloc(&h->h_img, chw * 4));
-    P2S_CUDA(cudaMalloc(&h->h_out, chw * 4));
-    P2S_CUDA(cudaMalloc(&h->h_z, px * h->n_in * 4));
-    P2S_CUDA(cudaMalloc(&h->h_t, px * 2 * 4));
-    h->stage_px_cap = px;
-    h->stage_chw_cap = chw;
-  }
+  s = ensure_stage(h, px, chw);
+  if (s != P2S_OK) return s;
   if ((size_t)B * nanc > h->anc_cap) {
     P2S_CUDA(cudaDeviceSynchronize());
     cudaFree(h->h_anc);
@@ -1465,11 +1502,6 @@ p2s_status p2s_render_anchors_host(p2s_handle* h, const float* image_host, int B
     h->anc_cap = 0;
     P2S_CUDA(cudaMalloc(&h->h_anc, (size_t)B * nanc * 4));
     h->anc_cap = (size_t)B * nanc;
-  }
-  if (!h->s_in) {
-    P2S_CUDA(cudaStreamCreateWithFlags(&h->s_in, cudaStreamNonBlocking));
-    P2S_CUDA(cudaEventCreateWithFlags(&h->ev_entry, cudaEventDisableTiming));
-    P2S_CUDA(cudaEventCreateWithFlags(&h->ev_band, cudaEventDisableTiming));
   }
   s = ensure_J(h, chw);
   if (s != P2S_OK) return s;

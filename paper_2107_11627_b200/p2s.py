@@ -28,7 +28,9 @@ EXPORTED = ("p2s_init", "p2s_render", "p2s_render_host", "p2s_reserve", "p2s_set
             "p2s_render_anchors", "p2s_render_anchors_host", "p2s_debug_blur_anchors",
             "p2s_render_sequence", "p2s_sampler_init", "p2s_sample_anchors", "p2s_sampler_destroy",
             "p2s_backward", "p2s_render_color", "p2s_mlp_backward", "p2s_interp_anchors",
-            "p2s_anchors_backward", "p2s_backward_color", "p2s_sampler_init_dense")
+            "p2s_anchors_backward", "p2s_backward_color", "p2s_sampler_init_dense", "p2s_reserve_ex")
+# p2s_reserve_ex workspace bits (include/p2s.h)
+RESERVE_RENDER, RESERVE_HOST, RESERVE_ADJOINT, RESERVE_ADJOINT_IMAGE = 1, 2, 4, 8
 
 
 class P2SError(RuntimeError):
@@ -81,6 +83,7 @@ def load_library(path: str = LIB_PATH) -> ctypes.CDLL:
     lib.p2s_render.argtypes = [v, _Image, v, v, v, v]
     lib.p2s_render_host.argtypes = [v, v, i, i, i, i, v, v, v, v]
     lib.p2s_reserve.argtypes = [v, i, i, i, i]
+    lib.p2s_reserve_ex.argtypes = [v, i, i, i, i, ctypes.c_uint]
     lib.p2s_set_profile_events.argtypes = [v, v, v]
     lib.p2s_get_info.argtypes = [v, ctypes.POINTER(Info)]
     lib.p2s_destroy.argtypes = [v]
@@ -112,7 +115,7 @@ def load_library(path: str = LIB_PATH) -> ctypes.CDLL:
                  "p2s_render_anchors", "p2s_render_anchors_host", "p2s_debug_blur_anchors",
                  "p2s_render_sequence", "p2s_sampler_init", "p2s_sample_anchors", "p2s_backward",
                  "p2s_render_color", "p2s_mlp_backward", "p2s_interp_anchors", "p2s_anchors_backward",
-                 "p2s_backward_color", "p2s_sampler_init_dense"):
+                 "p2s_backward_color", "p2s_sampler_init_dense", "p2s_reserve_ex"):
         getattr(lib, name).restype = st
     _lib = lib
     return lib
@@ -397,8 +400,15 @@ class Renderer:
                "p2s_render_host")
         return out
 
-    def reserve(self, B, C, H, W):
-        _check(self._lib.p2s_reserve(self._h, B, C, H, W), "p2s_reserve")
+    def reserve(self, B, C, H, W, host=False, adjoint=False, adjoint_image=False):
+        """p2s_reserve (render workspace), or p2s_reserve_ex when the host-path staging or the
+        adjoint workspaces are asked for too."""
+        what = RESERVE_RENDER | (RESERVE_HOST if host else 0) | (RESERVE_ADJOINT if adjoint else 0) | \
+            (RESERVE_ADJOINT_IMAGE if adjoint_image else 0)
+        if what == RESERVE_RENDER:
+            _check(self._lib.p2s_reserve(self._h, B, C, H, W), "p2s_reserve")
+        else:
+            _check(self._lib.p2s_reserve_ex(self._h, B, C, H, W, what), "p2s_reserve_ex")
 
     def set_profile_events(self, ev_begin=None, ev_end=None):
         """p2s_set_profile_events with torch.cuda.Event objects (created on first use)."""

@@ -1341,6 +1341,46 @@ def test_adjoint_chain_is_cuda_graph_capturable(p2s):
     r.close()
 
 
+def test_reserve_ex_makes_backward_capturable_without_warmup(p2s):
+    """p2s_reserve_ex pre-sizes the adjoint workspaces (dL/dJ, U and its range exponents): a
+    p2s_backward with every output is then captured in a CUDA graph with no eager call before it,
+    and its replay matches an eager call (the adjoint workspaces could not be reserved)."""
+    import torch
+    spec = SMALL["ragged_rgb_S7"]
+    inp = synth.make_inputs(spec)
+    r = p2s.Renderer(inp.basis, inp.mlp)
+    B, C, H, W = inp.image.shape
+    r.reserve(B, C, H, W, host=True, adjoint=True, adjoint_image=True)
+    img, z, t, g = _dev(inp.image), _dev(inp.zernike), _dev(inp.tilt), _dev(synth.make_upstream_grad(spec))
+    s = torch.cuda.Stream()
+    torch.cuda.synchronize()
+    graph = torch.cuda.CUDAGraph()
+    with torch.cuda.graph(graph, stream=s):
+        outs = r.backward(img, z, t, g, want_beta=True, want_tilt=True, want_image=True, stream=s)
+    graph.replay()
+    torch.cuda.synchronize()
+    eager = r.backward(img, z, t, g, want_beta=True, want_tilt=True, want_image=True)
+    torch.cuda.synchronize()
+    for what, a, b in zip(("dL/dbeta", "dL/dt", "dL/dI"), outs, eager):
+        a, b = a.cpu().numpy(), b.cpu().numpy()
+        np.testing.assert_allclose(a, b, rtol=1e-4, atol=1e-4 * np.abs(b).max(), err_msg=what)
+    # the host path's staging is reserved too (same result as the device path)
+    out_h = np.empty_like(inp.image)
+    r.render_host(inp.image, inp.zernike, inp.tilt, out_h)
+    np.testing.assert_array_equal(out_h, r.render(img, z, t).cpu().numpy())
+    # outputs overlapping an input or each other are argument errors (checked before any launch)
+    im = p2s._Image(img.data_ptr(), B, C, H, W)
+    gi, gt = torch.empty_like(img), torch.empty_like(t)
+    vp = lambda x: ctypes.c_void_p(x.data_ptr() if x is not None else None)  # noqa: E731
+    for gbeta, gtilt, gimg in ((None, None, img), (None, t, None), (g, None, None), (None, gt, gt[:, :1]),
+                               (None, None, g)):
+        st = r._lib.p2s_backward(r._h, im, vp(z), vp(t), vp(g), vp(gbeta), vp(gtilt), vp(gimg), None)
+        assert st == p2s.P2S_ERR_INVALID_ARG
+    assert r._lib.p2s_backward(r._h, im, vp(z), vp(t), vp(g), None, vp(gt), vp(gi), None) == p2s.P2S_OK
+    torch.cuda.synchronize()
+    r.close()
+
+
 # ---- adjoint of the wavelength-dependent colour render (p2s_backward_color)
 
 @pytest.mark.parametrize("name", ["ragged_rgb_S7", "S33_K100_C2", "tiny_widths", "W1_H1"])
