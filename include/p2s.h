@@ -281,6 +281,9 @@ typedef struct {
   int kernels_per_render;            /* launches queued by one p2s_render */
   int stage_bytes, nring;            /* B-operand ring: bytes per stage, stages */
   int mlp_backward;                  /* 1: p2s_mlp_backward supports this MLP (all p2s_init accepts) */
+  int c1_plan;                       /* 1: one-channel calls run on a one-channel plan (E buffers and
+                                        TMEM for C = 1; one op per MLP layer) */
+  int c1_smem_bytes, c1_nring, c1_stage_bytes; /* that plan's shared memory and ring (0 if none) */
 } p2s_info;
 P2S_API p2s_status p2s_get_info(const p2s_handle* h, p2s_info* info);
 

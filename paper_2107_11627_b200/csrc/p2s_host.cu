@@ -184,6 +184,8 @@ struct p2s_handle {
   CUtensorMap maps[kMaxMaps];
   int n_maps = 0;
   int progressive = 1;
+  int cmax = 3;                 // channels the E buffers and the TMEM layout are planned for
+  p2s_handle* c1 = nullptr;     // a one-channel plan of the same model (C = 1 calls use it)
 };
 
 namespace {
@@ -313,6 +315,7 @@ FusedParams make_params(const p2s_handle* h, int B, int C, int H, int W, int mod
   p.prof = h->prof;
   for (int i = 0; i < kMaxMaps; ++i) p.maps[i] = h->maps[i];
   p.progressive = h->progressive;
+  p.ecmax = h->cmax;
   return p;
 }
 
@@ -380,7 +383,14 @@ const char* p2s_status_string(p2s_status s) {
 
 const char* p2s_last_cuda_error(void) { return g_last_cuda_error.c_str(); }
 
-p2s_status p2s_init(const p2s_basis* basis, const p2s_mlp* mlp, p2s_handle** out_handle) {
+}  // extern "C"
+
+namespace {
+// The handle for frames of up to `cmax` channels: E buffers for cmax channels, the MLP scratch
+// after cmax conv accumulators. cmax = 1 leaves 400 TMEM columns for the MLP, so
+// each layer is one op (three MLP round trips per tile instead of five) and the E buffers take a
+// third of the shared memory.
+p2s_status init_impl(const p2s_basis* basis, const p2s_mlp* mlp, int cmax, p2s_handle** out_handle) {
   if (!basis || !mlp || !out_handle || !basis->taps || !mlp->W1 || !mlp->b1 || !mlp->W2 ||
       !mlp->b2 || !mlp->W3 || !mlp->b3)
     return P2S_ERR_INVALID_ARG;
@@ -401,6 +411,7 @@ p2s_status p2s_init(const p2s_basis* basis, const p2s_mlp* mlp, p2s_handle** out
 
   p2s_handle* h = new (std::nothrow) p2s_handle();
   if (!h) return P2S_ERR_OOM;
+  h->cmax = cmax;
   h->K = K; h->S = S; h->r = (S - 1) / 2;
   h->n_in = mlp->n_in; h->h1 = mlp->h1; h->h2 = mlp->h2;
   h->Nk = up16(K); h->K1 = up16(mlp->n_in); h->N1 = up16(mlp->h1); h->N2 = up16(mlp->h2);
@@ -418,7 +429,7 @@ p2s_status p2s_init(const p2s_basis* basis, const p2s_mlp* mlp, p2s_handle** out
   if (const char* e = std::getenv("P2S_NO_BIAS_FOLD")) h->bias_folded = std::atoi(e) == 0 && h->bias_folded;
 
   // ---- TMEM: conv accumulators [0, 3*Nk), MLP scratch / beta [3*Nk, 3*Nk + CH)
-  h->scr_col = 3 * h->Nk;
+  h->scr_col = cmax * h->Nk;
   const int CH = std::min(256, (512 - h->scr_col) / 16 * 16);  // widest MLP chunk
   // ---- MLP ops: each layer split into <= 2 column chunks of <= CH (L3 = one chunk = beta)
   const int layer_N[3] = {h->N1, h->N2, h->Nk};
@@ -463,7 +474,7 @@ p2s_status p2s_init(const p2s_basis* basis, const p2s_mlp* mlp, p2s_handle** out
   const int kh = std::max(h->N1, h->N2);
   const int a2_bytes = kTileM * kh * 2;
   const int hold_bytes = kTileM * hold_cols * 2;
-  int e1_bytes = 3 * P.chan_bytes;
+  int e1_bytes = cmax * P.chan_bytes;
   int conv_cut = 0;  // half-E plans: conv items never straddle step `cut`
   const int const_bytes = (h->bias_folded ? 256 : 256 + 2 * kMaxN) * 4;  // b1, b2 unused when folded
   const int red_bytes = 2 * 128 * 16;
@@ -516,7 +527,7 @@ p2s_status p2s_init(const p2s_basis* basis, const p2s_mlp* mlp, p2s_handle** out
     // the half plan where it exists)
     const char* eh_env = std::getenv("P2S_EHALF");
     const int eh_pref = eh_env ? std::atoi(eh_env) : -1;
-    const int e1_full = 3 * h->plan.chan_bytes, e2_half = 3 * (plan_half.chan_bytes + plan_half.chan_bytes1);
+    const int e1_full = cmax * h->plan.chan_bytes, e2_half = cmax * (plan_half.chan_bytes + plan_half.chan_bytes1);
     const bool full2_fits = kSmemLimit - fixed - al(2 * e1_full) - 1024 >= 3 * 12288;
     const bool use_half = plan_half.ehalf && ebuf_max == 2 && (eh_pref == 1 || (eh_pref != 0 && !full2_fits));
     e1_bytes = use_half ? (e2_half + 1) / 2 : e1_full;  // (n_ebuf * e1_bytes covers both halves)
@@ -1020,8 +1031,25 @@ p2s_status p2s_init(const p2s_basis* basis, const p2s_mlp* mlp, p2s_handle** out
   return P2S_OK;
 }
 
+// C = 1 calls run on the one-channel plan when the handle has one
+inline p2s_handle* for_c(p2s_handle* h, int C) { return (h && C == 1 && h->c1) ? h->c1 : h; }
+}  // namespace
+
+extern "C" {
+
+p2s_status p2s_init(const p2s_basis* basis, const p2s_mlp* mlp, p2s_handle** out_handle) {
+  p2s_status s = init_impl(basis, mlp, 3, out_handle);
+  if (s != P2S_OK || std::getenv("P2S_NO_C1")) return s;
+  p2s_handle* c1 = nullptr;
+  const p2s_status s1 = init_impl(basis, mlp, 1, &c1);
+  if (s1 == P2S_OK) (*out_handle)->c1 = c1;  // (optional: C = 1 calls fall back to the main plan)
+  if (std::getenv("P2S_DEBUG_C1")) std::fprintf(stderr, "p2s: one-channel plan %s\n", p2s_status_string(s1));
+  return P2S_OK;
+}
+
 p2s_status p2s_reserve(p2s_handle* h, int B, int C, int H, int W) {
   if (!h || B < 1 || C < 1 || H < 1 || W < 1) return P2S_ERR_INVALID_ARG;
+  h = for_c(h, C);
   return ensure_J(h, (size_t)B * C * H * W);
 }
 
@@ -1029,6 +1057,7 @@ p2s_status p2s_reserve_ex(p2s_handle* h, int B, int C, int H, int W, unsigned wh
   if (!h || B < 1 || C < 1 || H < 1 || W < 1 ||
       (what & ~(unsigned)(P2S_RESERVE_RENDER | P2S_RESERVE_HOST | P2S_RESERVE_ADJOINT | P2S_RESERVE_ADJOINT_IMAGE)))
     return P2S_ERR_INVALID_ARG;
+  h = for_c(h, C);
   const size_t px = (size_t)B * H * W, chw = px * C;
   p2s_status s = P2S_OK;
   if (what & (P2S_RESERVE_RENDER | P2S_RESERVE_HOST | P2S_RESERVE_ADJOINT | P2S_RESERVE_ADJOINT_IMAGE))
@@ -1043,6 +1072,7 @@ p2s_status p2s_set_profile_events(p2s_handle* h, p2s_event_t ev_begin, p2s_event
   if (!h || ((ev_begin == nullptr) != (ev_end == nullptr))) return P2S_ERR_INVALID_ARG;
   h->ev_begin = (cudaEvent_t)ev_begin;
   h->ev_end = (cudaEvent_t)ev_end;
+  if (h->c1) p2s_set_profile_events(h->c1, ev_begin, ev_end);
   return P2S_OK;
 }
 
@@ -1081,6 +1111,7 @@ static p2s_status render_impl(p2s_handle* h, p2s_image im, const float* z, const
 
 p2s_status p2s_render(p2s_handle* h, p2s_image im, const float* zernike_field, const float* tilt_field,
                       float* out, p2s_stream_t stream) {
+  h = for_c(h, im.C);
   p2s_status s = check_image(h, im);
   if (s != P2S_OK) return s;
   if (!zernike_field || !out) return P2S_ERR_INVALID_ARG;
@@ -1089,6 +1120,7 @@ p2s_status p2s_render(p2s_handle* h, p2s_image im, const float* zernike_field, c
 
 p2s_status p2s_render_sequence(p2s_handle* h, p2s_image im, const float* zernike_field, const float* tilt_field,
                                int F, float* out, p2s_stream_t stream) {
+  h = for_c(h, im.C);
   p2s_status s = check_image(h, im);
   if (s != P2S_OK) return s;
   if (!zernike_field || !out || im.B != 1 || F < 1 || F > 65535) return P2S_ERR_INVALID_ARG;
@@ -1114,6 +1146,7 @@ p2s_status p2s_render_sequence(p2s_handle* h, p2s_image im, const float* zernike
 
 p2s_status p2s_render_color(p2s_handle* h, p2s_image im, const float* zernike_field, const float* tilt_field,
                             float* out, p2s_stream_t stream) {
+  h = for_c(h, im.C);
   p2s_status s = check_image(h, im);
   if (s != P2S_OK) return s;
   if (!zernike_field || !out) return P2S_ERR_INVALID_ARG;
@@ -1141,6 +1174,7 @@ p2s_status p2s_render_color(p2s_handle* h, p2s_image im, const float* zernike_fi
 p2s_status p2s_backward(p2s_handle* h, p2s_image im, const float* zernike_field, const float* tilt_field,
                         const float* grad_out, float* grad_beta, float* grad_tilt, float* grad_image,
                         p2s_stream_t stream) {
+  h = for_c(h, im.C);
   p2s_status s = check_image(h, im);
   if (s != P2S_OK) return s;
   if (!zernike_field || !grad_out || (!grad_beta && !grad_tilt && !grad_image)) return P2S_ERR_INVALID_ARG;
@@ -1360,6 +1394,7 @@ p2s_status p2s_backward_color(p2s_handle* h, p2s_image im, const float* zernike_
 
 p2s_status p2s_render_anchors(p2s_handle* h, p2s_image im, const float* anchors, int G,
                               const float* tilt_field, float* out, p2s_stream_t stream) {
+  h = for_c(h, im.C);
   p2s_status s = check_image(h, im);
   if (s != P2S_OK) return s;
   if (!anchors || !out || G < 1 || G > 4096) return P2S_ERR_INVALID_ARG;
@@ -1368,6 +1403,7 @@ p2s_status p2s_render_anchors(p2s_handle* h, p2s_image im, const float* anchors,
 
 p2s_status p2s_debug_blur_anchors(p2s_handle* h, p2s_image im, const float* anchors, int G, float* J_out,
                                   p2s_stream_t stream) {
+  h = for_c(h, im.C);
   p2s_status s = check_image(h, im);
   if (s != P2S_OK) return s;
   if (!anchors || !J_out || G < 1 || G > 4096) return P2S_ERR_INVALID_ARG;
@@ -1376,6 +1412,7 @@ p2s_status p2s_debug_blur_anchors(p2s_handle* h, p2s_image im, const float* anch
 
 p2s_status p2s_debug_blur(p2s_handle* h, p2s_image im, const float* zernike_field, float* J_out,
                           p2s_stream_t stream) {
+  h = for_c(h, im.C);
   p2s_status s = check_image(h, im);
   if (s != P2S_OK) return s;
   if (!zernike_field || !J_out) return P2S_ERR_INVALID_ARG;
@@ -1396,6 +1433,7 @@ p2s_status p2s_debug_beta(p2s_handle* h, const float* zernike_field, int B, int 
 p2s_status p2s_render_host(p2s_handle* h, const float* image_host, int B, int C, int H, int W,
                            const float* zernike_host, const float* tilt_host, float* out_host,
                            p2s_stream_t stream) {
+  h = for_c(h, C);
   if (!h || !image_host || !zernike_host || !out_host) return P2S_ERR_INVALID_ARG;
   p2s_image im{nullptr, B, C, H, W};
   im.data = image_host;  // validated below against the device copy
@@ -1487,6 +1525,7 @@ p2s_status p2s_render_host(p2s_handle* h, const float* image_host, int B, int C,
 p2s_status p2s_render_anchors_host(p2s_handle* h, const float* image_host, int B, int C, int H, int W,
                                    const float* anchors_host, int G, const float* tilt_host, float* out_host,
                                    p2s_stream_t stream) {
+  h = for_c(h, C);
   if (!h || !image_host || !anchors_host || !out_host || G < 1 || G > 4096) return P2S_ERR_INVALID_ARG;
   p2s_image im{image_host, B, C, H, W};
   p2s_status s = check_image(h, im);
@@ -1541,6 +1580,7 @@ p2s_status p2s_debug_profile_buffer(p2s_handle* h, void* device_counters) {
   if (!h) return P2S_ERR_INVALID_ARG;
 #if defined(P2S_PROFILE) || defined(P2S_STARTUP_PROF)
   h->prof = (unsigned long long*)device_counters;
+  if (h->c1) h->c1->prof = h->prof;
   return P2S_OK;
 #else
   (void)device_counters;
@@ -1558,11 +1598,16 @@ p2s_status p2s_get_info(const p2s_handle* h, p2s_info* info) {
   info->stage_bytes = h->stage_bytes;
   info->nring = h->nring;
   info->mlp_backward = h->mb_ok;
+  info->c1_plan = h->c1 ? 1 : 0;
+  info->c1_smem_bytes = h->c1 ? h->c1->smem_bytes : 0;
+  info->c1_nring = h->c1 ? h->c1->nring : 0;
+  info->c1_stage_bytes = h->c1 ? h->c1->stage_bytes : 0;
   return P2S_OK;
 }
 
 void p2s_destroy(p2s_handle* h) {
   if (!h) return;
+  if (h->c1) p2s_destroy(h->c1);
   cudaDeviceSynchronize();
   cudaFree(h->d_stream); cudaFree(h->d_items); cudaFree(h->d_mma); cudaFree(h->d_steps); cudaFree(h->d_consts);
   cudaFree(h->d_J);

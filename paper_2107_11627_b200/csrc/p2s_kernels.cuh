@@ -150,6 +150,7 @@ struct FusedParams {
   int a1_sbo, a2_sbo, hold_sbo;
   unsigned long long* prof;   // P2S_PROFILE builds only: [grid][4][20] cycle counters
   int progressive;            // 1: release beta / each conv accumulator as soon as it is read
+  int ecmax;                  // channels the E buffers are sized for (buffer 1 at ecmax chan_bytes)
 };
 
 #ifdef P2S_SLEEP_BUILD
@@ -746,7 +747,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads)
     const uint32_t id_conv = idesc_f16(256, p.Nk);
     const uint32_t stage16 = (uint32_t)p.stage_bytes >> 4;
     const uint32_t ch16_0 = (uint32_t)p.chan_bytes >> 4, ch16_1 = (uint32_t)p.chan_bytes1 >> 4;
-    const uint32_t ebuf16 = 3u * ch16_0;  // buffer 1's offset
+    const uint32_t ebuf16 = (uint32_t)p.ecmax * ch16_0;  // buffer 1's offset
     const int C = p.C, nring = p.nring, ebufs = p.n_ebuf, mode = pmode, ehalf = p.ehalf;
     const uint32_t acc1 = tmem + (uint32_t)p.Nk, acc2 = tmem + 2u * (uint32_t)p.Nk;
     const uint32_t smem_lo = smem_u32(smem) >> 4;
@@ -927,7 +928,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads)
         const int eb = p.ehalf ? hh : (p.n_ebuf == 2 ? (it & 1) : 0);
         { PROF_T0(); WAIT_BUILD(&bars[BAR_E_EMPTY0 + eb], ((eb ? e_use1 : e_use0) & 1) ^ 1); PROF_ADD(11); }
         if (eb) ++e_use1; else ++e_use0;
-        uint8_t* Eb = sE + (size_t)eb * 3 * p.chan_bytes;  // buffers are sized for C = 3 (half 0 first)
+        uint8_t* Eb = sE + (size_t)eb * p.ecmax * p.chan_bytes;  // buffers are sized for ecmax channels (half 0 first)
         {
           PROF_T0();
 #ifndef P2S_ABL_NOE
@@ -958,7 +959,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads)
       const int etid = (warp - kWarpEpi0) * 32 + lane;
       for (int hh = 0; hh < 1 + p.ehalf; ++hh) {  // half-E plans: both halves, into buffers 0 and 1
         const bool h0 = p.ehalf && hh == 0, h1 = p.ehalf && hh == 1;
-        build_E_all<32 * kNumEpiWarps>(p, sE + (size_t)hh * 3 * p.chan_bytes, p.image + (size_t)b0 * p.C * HW0, y0,
+        build_E_all<32 * kNumEpiWarps>(p, sE + (size_t)hh * p.ecmax * p.chan_bytes, p.image + (size_t)b0 * p.C * HW0, y0,
                                        xs, etid, h1 ? p.blkA : 0, h0 ? p.blkA : p.n_ey, 0, h0 ? 0 : p.n_ex,
                                        h1 ? p.chan_bytes1 : p.chan_bytes);
       }
