@@ -185,6 +185,8 @@ struct p2s_handle {
   int n_maps = 0;
   int progressive = 1;
   int cmax = 3;                 // channels the E buffers and the TMEM layout are planned for
+  int beta_col = 0;             // TMEM column of beta (L3's output): scr_col, or its own region
+  int mlp_ahead = 0;            // 1: a tile's L1 / L2 run ahead of the previous tile's conv epilogue
   p2s_handle* c1 = nullptr;     // a one-channel plan of the same model (C = 1 calls use it)
 };
 
@@ -300,7 +302,8 @@ FusedParams make_params(const p2s_handle* h, int B, int C, int H, int W, int mod
   p.blkA = h->plan.blkA;
   p.chan_bytes1 = h->plan.chan_bytes1;
   p.n_ebuf = h->n_ebuf;
-  p.scr_col = h->scr_col;
+  p.scr_col = h->beta_col;  // (the kernel reads beta there; MLP ops carry their own columns)
+  p.mlp_ahead = h->mlp_ahead;
   p.stage_bytes = h->stage_bytes; p.nring = h->nring;
   p.off_ring = h->off_ring; p.off_a1 = h->off_a1; p.off_a2 = h->off_a2; p.off_e = h->off_e;
   p.off_tab = h->off_tab; p.off_const = h->off_const; p.off_red = h->off_red; p.off_bar = h->off_bar;
@@ -453,6 +456,18 @@ p2s_status init_impl(const p2s_basis* basis, const p2s_mlp* mlp, int cmax, p2s_h
       // while the lower chunk still reads A2, so the hold buffer is as small as possible
       h->ops[h->n_ops++] = MlpOp{l, w0, N - w0, layer_K[l] / 16, 1, 0, h->scr_col};
       h->ops[h->n_ops++] = MlpOp{l, 0, w0, layer_K[l] / 16, 0, 1, h->scr_col};
+    }
+  }
+  // One-channel plan with every layer a single op: beta gets its own TMEM region after the L1/L2
+  // scratch, so the next tile's L1 and L2 (which only need that scratch and A1) can run while this
+  // tile's conv epilogue still reads beta and the accumulator ("MLP ahead"; P2S_NO_AHEAD=1 off)
+  h->beta_col = h->scr_col;
+  {
+    const int maxN = std::max(h->N1, h->N2);
+    if (cmax == 1 && h->n_ops == 3 && h->scr_col + maxN + h->Nk <= 512 && !std::getenv("P2S_NO_AHEAD")) {
+      h->beta_col = h->scr_col + maxN;
+      h->ops[2].d_col = h->beta_col;
+      h->mlp_ahead = 1;
     }
   }
   // (Whole-layer L1/L2 ops for a CTA's first tile, in its still idle accumulator columns, were
@@ -685,11 +700,20 @@ p2s_status init_impl(const p2s_basis* basis, const p2s_mlp* mlp, int cmax, p2s_h
   const int gaps = std::max(1, h->n_ops - 1);
   const int per_gap = std::max(1, (ncs - 1) / gaps);
   size_t ci = 0;
-  for (int o = 0; o < h->n_ops; ++o) {
-    make_items(op_off[o], h->ops[o].nks, h->ops[o].N, 0, (uint8_t)o, full);
-    make_items(op_off[o], h->ops[o].nks, h->ops[o].N, 0, (uint8_t)o, beta);
-    if (o + 1 < h->n_ops)
-      for (int k = 0; k < per_gap && ci + 1 < conv_items.size(); ++k) full.push_back(conv_items[ci++]);
+  if (h->mlp_ahead) {
+    // MLP ahead: L1, L2 back to back (they do not wait for the accumulators), the conv stages (the
+    // first waits for the previous tile's epilogue), L3 after a third of them
+    for (int o = 0; o < h->n_ops; ++o) make_items(op_off[o], h->ops[o].nks, h->ops[o].N, 0, (uint8_t)o, beta);
+    for (int o = 0; o < 2; ++o) make_items(op_off[o], h->ops[o].nks, h->ops[o].N, 0, (uint8_t)o, full);
+    for (int k = 0; k < std::max(1, ncs / 3) && ci + 1 < conv_items.size(); ++k) full.push_back(conv_items[ci++]);
+    make_items(op_off[2], h->ops[2].nks, h->ops[2].N, 0, (uint8_t)2, full);
+  } else {
+    for (int o = 0; o < h->n_ops; ++o) {
+      make_items(op_off[o], h->ops[o].nks, h->ops[o].N, 0, (uint8_t)o, full);
+      make_items(op_off[o], h->ops[o].nks, h->ops[o].N, 0, (uint8_t)o, beta);
+      if (o + 1 < h->n_ops)
+        for (int k = 0; k < per_gap && ci + 1 < conv_items.size(); ++k) full.push_back(conv_items[ci++]);
+    }
   }
   while (ci < conv_items.size()) full.push_back(conv_items[ci++]);
   // First tile of every CTA: the epilogue warps build its E views up front (they are idle until
@@ -723,7 +747,8 @@ p2s_status init_impl(const p2s_basis* basis, const p2s_mlp* mlp, int cmax, p2s_h
       const bool half1 = ecut > 0 && it.first >= ecut;
       const bool e_begin = (it.flags & IT_BEGIN) || (ecut > 0 && it.first == ecut);
       const bool e_end = (it.flags & IT_END) || (ecut > 0 && end == ecut);
-      mi.flags = MI_CONV | (e_begin ? MI_WAIT_E : 0) | (((it.flags & IT_BEGIN) && mode == 3) ? MI_WAIT_TMEM : 0) |
+      const bool wait_acc = (it.flags & IT_BEGIN) && (mode == 3 || (mode == 0 && h->mlp_ahead));
+      mi.flags = MI_CONV | (e_begin ? MI_WAIT_E : 0) | (wait_acc ? MI_WAIT_TMEM : 0) |
                  (e_end ? MI_COMMIT_E : 0) | (half1 ? MI_EHALF1 : 0) | ((it.flags & IT_END) ? MI_COMMIT_ACC : 0);
       return mi;
     }
@@ -742,7 +767,8 @@ p2s_status init_impl(const p2s_basis* basis, const p2s_mlp* mlp, int cmax, p2s_h
     // mode 2 = a sequence frame after the tile's first: its L1 waits for the previous frame's
     // beta to leave the scratch (SCR_FREE), not for the conv accumulators (they stay)
     if (it.flags & IT_BEGIN) {
-      if (op.layer == 0 && op.first_of_layer) f |= MI_WAIT_A1 | (mode == 2 ? MI_WAIT_SCR : MI_WAIT_TMEM);
+      if (op.layer == 0 && op.first_of_layer)
+        f |= MI_WAIT_A1 | (mode == 2 ? MI_WAIT_SCR : ((mode == 0 && h->mlp_ahead) ? 0 : MI_WAIT_TMEM));
       else f |= MI_WAIT_SCR;
     }
     if (it.flags & IT_END) {

@@ -144,13 +144,15 @@ struct FusedParams {
                               // tile (EY blocks [0, blkA) | the rest + EX rows), not a whole tile
   int chan_bytes1;            // half-E plans: half 1's per-channel bytes (chan_bytes: half 0's);
                               // buffer 1 starts at 3 chan_bytes (else both are chan_bytes)
-  int scr_col;                // TMEM column of the MLP scratch (= 3 * Nk)
+  int scr_col;                // TMEM column of beta (L3's output; the MLP scratch start unless mlp_ahead)
   int stage_bytes, nring;
   int off_ring, off_a1, off_a2, off_hold, off_e, off_tab, off_const, off_red, off_bar, smem_bytes;
   int a1_sbo, a2_sbo, hold_sbo;
   unsigned long long* prof;   // P2S_PROFILE builds only: [grid][4][20] cycle counters
   int progressive;            // 1: release beta / each conv accumulator as soon as it is read
   int ecmax;                  // channels the E buffers are sized for (buffer 1 at ecmax chan_bytes)
+  int mlp_ahead;              // 1 (one-channel plan): the epilogue drains the next tile's L1 before this
+                              // tile's conv epilogue (its L1 / L2 run ahead, beta has its own columns)
 };
 
 #ifdef P2S_SLEEP_BUILD
@@ -993,9 +995,16 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads)
       // a CTA's first tile (mode 0) runs L1 and L2 as whole-layer ops (p.ops[n_ops, +n_fops))
       const bool fops = pmode == 0 && it == 0 && fr == 0 && p.n_fops > 0;
       const int o_begin = fops ? p.n_ops : 0, o_end = pmode == 2 ? 0 : (fops ? p.n_ops + p.n_fops : p.n_ops);
-      for (int o = o_begin; o < o_end; ++o) {
+      // MLP ahead (one-channel plan, one frame per tile): this tile's L1 was drained in the previous
+      // iteration and the next tile's L1 is drained (after this tile's L2) before this tile's conv
+      // epilogue, so the tensor core runs the next L2 while the epilogue reads beta and the
+      // accumulator. One loop body for every drain (a second inlined copy costs registers).
+      const bool ahead = pmode == 0 && nfr == 1 && p.mlp_ahead != 0;
+      const int o_stop = o_end + ((ahead && pr + 1 < pr_end) ? 1 : 0);
+      for (int k = o_begin; k < o_stop; ++k) {
+        const int o = k < o_end ? k : 0;
+        if (k < o_end && (p.ops[o].layer == 2 || (ahead && o == 0 && it > 0))) continue;  // (beta stays)
         const MlpOp op = p.ops[o];
-        if (op.layer == 2) continue;        // beta stays in TMEM for the conv epilogue
         { PROF_T0(); WAIT_EPI(&bars[BAR_MLP_DONE], mlp_waits & 1); PROF_ADD(13); }
         ++mlp_waits;
         tc_fence_after();

@@ -1,2 +1,4 @@
 cd $GRAFT_REPO_ROOT
-python tools/c1_time.py; P2S_NO_C1=1 python tools/c1_time.py; python tools/c1_time.py
+L=paper_2107_11627_b200/libp2s_prof.so
+P2S_LIB=$L timeout 120 python tools/mma_trace.py 2 0 60 > gpurun_out/trace_c1.txt 2>&1
+P2S_LIB=$L timeout 120 python tools/role_profile.py 2 > gpurun_out/roles_c1.txt 2>&1
