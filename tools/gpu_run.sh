@@ -1,4 +1,8 @@
 cd $GRAFT_REPO_ROOT
-L=paper_2107_11627_b200/libp2s_prof.so
-P2S_LIB=$L timeout 120 python tools/mma_trace.py 2 0 60 > gpurun_out/trace_c1.txt 2>&1
-P2S_LIB=$L timeout 120 python tools/role_profile.py 2 > gpurun_out/roles_c1.txt 2>&1
+timeout 600 python bench.py > gpurun_out/bench_full.log 2>&1; echo "bench rc=$?"
+python -c "
+import json; d=json.loads(open('gpurun_out/bench_full.log').read().strip().splitlines()[-1])
+print(d['value'], d['roofline']['frac'], d['roofline']['fused_ms_median'], d['e2e']['value'])
+for k,v in d['configs'].items(): print(k, v['value'], v['roofline']['frac'], {kk: vv for kk, vv in v.items() if kk in ('batched',)})
+for k in ('sequence_mode','color_mode','batch_mode','anchor_mode','adjoint_mode'): print(k, d[k]['value'])
+"
