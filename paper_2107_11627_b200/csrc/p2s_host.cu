@@ -1184,6 +1184,17 @@ p2s_status p2s_render_color(p2s_handle* h, p2s_image im, const float* zernike_fi
   cudaStream_t st = (cudaStream_t)stream;
   s = ensure_J(h, n_out);
   if (s != P2S_OK) return s;
+  if (h->c1 && im.C > 1 && !std::getenv("P2S_COLOR_FUSED")) {
+    // channel c of frame b is a one-channel frame with its own field: one launch of the
+    // one-channel plan over the B*C frames (image [B*C][1][H][W], fields [B*C][n_in][H][W], J in
+    // [B][C][H][W] order), then the warp of the B frames with their shared tilt
+    const p2s_image im1{im.data, im.B * im.C, 1, im.H, im.W};
+    s = check_image(h->c1, im1);
+    if (s != P2S_OK) return s;
+    s = render_impl(h->c1, im1, zernike_field, nullptr, nullptr, h->d_J, st);
+    if (s != P2S_OK) return s;
+    return launch_warp(h, h->d_J, tilt_field, out, im.B, im.C, im.H, im.W, st);
+  }
   FusedParams p = make_params(h, im.B, im.C, im.H, im.W, 0);
   p.nfr = im.C;  // per tile: the C channels' convolutions once, then one MLP + J pass per channel
   p.color = 1;
