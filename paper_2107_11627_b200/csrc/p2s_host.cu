@@ -187,6 +187,7 @@ struct p2s_handle {
   int cmax = 3;                 // channels the E buffers and the TMEM layout are planned for
   int beta_col = 0;             // TMEM column of beta (L3's output): scr_col, or its own region
   int mlp_ahead = 0;            // 1: a tile's L1 / L2 run ahead of the previous tile's conv epilogue
+  int l1_early = 0;             // 1: the first L1 chunk lies past beta and issues before the accumulators free
   p2s_handle* c1 = nullptr;     // a one-channel plan of the same model (C = 1 calls use it)
 };
 
@@ -462,6 +463,16 @@ p2s_status init_impl(const p2s_basis* basis, const p2s_mlp* mlp, int cmax, p2s_h
   // scratch, so the next tile's L1 and L2 (which only need that scratch and A1) can run while this
   // tile's conv epilogue still reads beta and the accumulator ("MLP ahead"; P2S_NO_AHEAD=1 off)
   h->beta_col = h->scr_col;
+  // Early L1 (multi-channel plan): the first L1 chunk goes to the columns after beta's, free while
+  // the previous tile's epilogue still reads beta and the accumulators, so it issues without
+  // waiting for them (the tile's first conv stage waits instead): the tensor core works in the
+  // tile-boundary bubble (P2S_NO_L1EARLY=1 off)
+  h->l1_early = 0;
+  if (h->n_ops >= 2 && h->ops[0].layer == 0 && !h->ops[0].last_of_layer &&
+      h->scr_col + h->Nk + h->ops[0].N <= 512 && !std::getenv("P2S_NO_L1EARLY")) {
+    h->ops[0].d_col = h->scr_col + h->Nk;
+    h->l1_early = 1;
+  }
   {
     const int maxN = std::max(h->N1, h->N2);
     if (cmax == 1 && h->n_ops == 3 && h->scr_col + maxN + h->Nk <= 512 && !std::getenv("P2S_NO_AHEAD")) {
@@ -747,7 +758,7 @@ p2s_status init_impl(const p2s_basis* basis, const p2s_mlp* mlp, int cmax, p2s_h
       const bool half1 = ecut > 0 && it.first >= ecut;
       const bool e_begin = (it.flags & IT_BEGIN) || (ecut > 0 && it.first == ecut);
       const bool e_end = (it.flags & IT_END) || (ecut > 0 && end == ecut);
-      const bool wait_acc = (it.flags & IT_BEGIN) && (mode == 3 || (mode == 0 && h->mlp_ahead));
+      const bool wait_acc = (it.flags & IT_BEGIN) && (mode == 3 || (mode == 0 && (h->mlp_ahead || h->l1_early)));
       mi.flags = MI_CONV | (e_begin ? MI_WAIT_E : 0) | (wait_acc ? MI_WAIT_TMEM : 0) |
                  (e_end ? MI_COMMIT_E : 0) | (half1 ? MI_EHALF1 : 0) | ((it.flags & IT_END) ? MI_COMMIT_ACC : 0);
       return mi;
@@ -768,7 +779,7 @@ p2s_status init_impl(const p2s_basis* basis, const p2s_mlp* mlp, int cmax, p2s_h
     // beta to leave the scratch (SCR_FREE), not for the conv accumulators (they stay)
     if (it.flags & IT_BEGIN) {
       if (op.layer == 0 && op.first_of_layer)
-        f |= MI_WAIT_A1 | (mode == 2 ? MI_WAIT_SCR : ((mode == 0 && h->mlp_ahead) ? 0 : MI_WAIT_TMEM));
+        f |= MI_WAIT_A1 | (mode == 2 ? MI_WAIT_SCR : ((mode == 0 && (h->mlp_ahead || h->l1_early)) ? 0 : MI_WAIT_TMEM));
       else f |= MI_WAIT_SCR;
     }
     if (it.flags & IT_END) {
