@@ -779,7 +779,10 @@ p2s_status init_impl(const p2s_basis* basis, const p2s_mlp* mlp, int cmax, p2s_h
     // beta to leave the scratch (SCR_FREE), not for the conv accumulators (they stay)
     if (it.flags & IT_BEGIN) {
       if (op.layer == 0 && op.first_of_layer)
-        f |= MI_WAIT_A1 | (mode == 2 ? MI_WAIT_SCR : ((mode == 0 && (h->mlp_ahead || h->l1_early)) ? 0 : MI_WAIT_TMEM));
+        f |= MI_WAIT_A1 | (mode == 2 ? (h->l1_early ? 0 : MI_WAIT_SCR)
+                                     : ((mode == 0 && (h->mlp_ahead || h->l1_early)) ? 0 : MI_WAIT_TMEM));
+      else if (mode == 2 && h->l1_early && op.layer == 0 && it.op == 1)
+        f |= MI_WAIT_SCR | MI_WAIT_SCR2;  // a sequence frame's L1c1: the previous reduction + L1c0's drain
       else f |= MI_WAIT_SCR;
     }
     if (it.flags & IT_END) {

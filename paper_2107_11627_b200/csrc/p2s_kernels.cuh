@@ -76,7 +76,9 @@ enum MmaItemFlags : uint16_t {
   MI_CONV = 1, MI_WAIT_A1 = 2, MI_WAIT_SCR = 4, MI_WAIT_E = 8,
   MI_COMMIT_A1 = 16, MI_COMMIT_MLP = 32, MI_COMMIT_ACC = 64, MI_WAIT_TMEM = 128,
   MI_COMMIT_E = 256,   // the item is the last reader of its E buffer
-  MI_EHALF1 = 512      // half-E plans: the item reads half 1's buffer (else half 0's)
+  MI_EHALF1 = 512,     // half-E plans: the item reads half 1's buffer (else half 0's)
+  MI_WAIT_SCR2 = 1024  // a second SCR_FREE phase (a sequence frame's L1c1: the previous frame's
+                       // reduction and this frame's early L1c0 drain)
 };
 struct MmaItem {
   uint32_t a_lo_rel;   // (smem offset >> 4) | (LBO >> 4) << 16, without the smem base
@@ -789,6 +791,10 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads)
         { PROF_T0(); mbar_wait(&bars[BAR_SCR_FREE], scr_waits & 1); PROF_ADD(2); }
         ++scr_waits;
       }
+      if (kAdj != 1 && (f & MI_WAIT_SCR2)) {
+        mbar_wait(&bars[BAR_SCR_FREE], scr_waits & 1);
+        ++scr_waits;
+      }
       if (f & MI_WAIT_E) { PROF_T0(); mbar_wait(&bars[BAR_E_FULL0 + eb], (e_par >> eb) & 1u); PROF_ADD(3); }
 #ifndef P2S_ABL_NOTMA
       { PROF_T0(); mbar_wait(&ring_full[s], ph); PROF_ADD(5); }
@@ -999,6 +1005,9 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads)
       // iteration and the next tile's L1 is drained (after this tile's L2) before this tile's conv
       // epilogue, so the tensor core runs the next L2 while the epilogue reads beta and the
       // accumulator. One loop body for every drain (a second inlined copy costs registers).
+      // (Sequence frames of an early-L1 plan keep this order: their L1c0 runs during the previous
+      // frame's reduction but is drained after it -- draining it first put the A1 build on the
+      // epilogue's path, measured slower.)
       const bool ahead = pmode == 0 && nfr == 1 && p.mlp_ahead != 0;
       const int o_stop = o_end + ((ahead && pr + 1 < pr_end) ? 1 : 0);
       for (int k = o_begin; k < o_stop; ++k) {
