@@ -785,7 +785,8 @@ def _margins_ok(buf, pad):
     return bool(np.all(b[:pad] == 12345.0) and np.all(b[-pad:] == 12345.0))
 
 
-@pytest.mark.parametrize("name", ["ragged_rgb_S7", "S33_K100_C2", "W1_H1", "S65_K100_h256"])
+@pytest.mark.parametrize("name", ["ragged_rgb_S7", "S33_K100_C2", "W1_H1", "S65_K100_h256", "many_tiles_C1_S9",
+                                  "h224_n40"])
 def test_outputs_stay_in_bounds(p2s, name):
     spec = SMALL[name]
     inp = synth.make_inputs(spec)
@@ -812,6 +813,11 @@ def test_outputs_stay_in_bounds(p2s, name):
     bb, beta, pbb = _guarded((B, spec.K, H, W))
     r.debug_beta(z, out=beta)
     checks.append(("debug_beta", bb, pbb))
+    F = 3  # a sequence of F frames of the first image (one-channel / early-L1 plans included)
+    sinp = synth.make_inputs(spec, frames=range(F))
+    sb, sout, ps = _guarded((F, C, H, W))
+    r.render_sequence(_dev(sinp.image[:1]), _dev(sinp.zernike), _dev(sinp.tilt), out=sout)
+    checks.append(("render_sequence", sb, ps))
     if r.info()["mlp_backward"]:
         gz_buf, gz, pz = _guarded((B, spec.n_in, H, W))
         r.mlp_backward(z, gb, out=gz)
