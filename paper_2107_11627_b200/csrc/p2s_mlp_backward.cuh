@@ -311,15 +311,11 @@ __global__ void __launch_bounds__(kMbThreads, 1) k_mlp_backward(const __grid_con
         }
       }
       // ---- dL/dbeta of this tile into registers (in flight during F1 / D1 / F2): groups 4 r + q
+      // (the two groups' loads in two batches, the second during D1: 32 loads per thread at once
+      // back up the load/store queue)
       float gv[2][16];
-      {
-        const float* gbb = p.gb + (size_t)b * p.K * HW + pxc;
-#pragma unroll
-        for (int r = 0; r < 2; ++r) {
-          const int c = 16 * (4 * r + q);
-          load16b(gbb + (size_t)c * HW, HWB, p.K - c, gv[r]);
-        }
-      }
+      const float* gbb = p.gb + (size_t)b * p.K * HW + pxc;
+      load16b(gbb + (size_t)(16 * q) * HW, HWB, p.K - 16 * q, gv[0]);
       mbar_wait(bar_f1, ph1);  // F1
       ph1 ^= 1;
       tc_fence_after();
@@ -343,6 +339,7 @@ __global__ void __launch_bounds__(kMbThreads, 1) k_mlp_backward(const __grid_con
           }
           round_done();
         }
+        if (r == 0) load16b(gbb + (size_t)(16 * (4 + q)) * HW, HWB, p.K - 16 * (4 + q), gv[1]);
       }
       // per-pixel power-of-two scale of dL/dbeta (the four quarters agree through s_max)
       float mx = 0.f;
