@@ -180,6 +180,11 @@ struct p2s_handle {
   // host path (p2s_render_host): input-copy stream and its events
   cudaStream_t s_in = nullptr;
   cudaEvent_t ev_entry = nullptr, ev_band = nullptr;
+  // host path, output side: row bands are warped and copied back on s_out as soon as the J rows
+  // they read are rendered (one event per rendered band, one per warped frame)
+  cudaStream_t s_out = nullptr;
+  std::vector<cudaEvent_t> ev_rend;
+  cudaEvent_t ev_warped = nullptr;
   unsigned long long* prof = nullptr;
   CUtensorMap maps[kMaxMaps];
   int n_maps = 0;
@@ -223,6 +228,10 @@ p2s_status ensure_stage(p2s_handle* h, size_t px, size_t chw) {
     P2S_CUDA(cudaStreamCreateWithFlags(&h->s_in, cudaStreamNonBlocking));
     P2S_CUDA(cudaEventCreateWithFlags(&h->ev_entry, cudaEventDisableTiming));
     P2S_CUDA(cudaEventCreateWithFlags(&h->ev_band, cudaEventDisableTiming));
+  }
+  if (!h->s_out) {
+    P2S_CUDA(cudaStreamCreateWithFlags(&h->s_out, cudaStreamNonBlocking));
+    P2S_CUDA(cudaEventCreateWithFlags(&h->ev_warped, cudaEventDisableTiming));
   }
   return P2S_OK;
 }
@@ -339,8 +348,9 @@ p2s_status launch_fused(p2s_handle* h, const FusedParams& p, cudaStream_t st) {
 // Tilt warp (step a3), launched as a programmatic dependent of the fused kernel on `st`
 // (its launch and tilt loads overlap the fused kernel's tail; it waits for J on the device).
 p2s_status launch_warp(const p2s_handle* h, const float* J, const float* tilt, float* out, int B, int C,
-                       int H, int W, cudaStream_t st) {
-  const size_t npx = (size_t)B * H * W;
+                       int H, int W, cudaStream_t st, int wy0 = 0, int wny = -1, bool pdl = true) {
+  if (wny < 0) wny = H;
+  const size_t npx = (size_t)B * wny * W;
   const bool vec = (W % 4) == 0 && ((uintptr_t)J % 16) == 0 && ((uintptr_t)out % 16) == 0 &&
                    ((uintptr_t)tilt % 16) == 0;
   cudaLaunchConfig_t cfg{};
@@ -348,16 +358,16 @@ p2s_status launch_warp(const p2s_handle* h, const float* J, const float* tilt, f
   attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
   attr[0].val.programmaticStreamSerializationAllowed = 1;
   cfg.attrs = attr;
-  cfg.numAttrs = 1;
+  cfg.numAttrs = pdl ? 1 : 0;
   cfg.blockDim = dim3(256);
   cfg.dynamicSmemBytes = 0;
   cfg.stream = st;
   if (vec) {
     cfg.gridDim = dim3((unsigned)((npx / 4 + 255) / 256));
-    P2S_CUDA(cudaLaunchKernelEx(&cfg, k_tilt_warp4, J, tilt, out, B, C, H, W));
+    P2S_CUDA(cudaLaunchKernelEx(&cfg, k_tilt_warp4, J, tilt, out, B, C, H, W, wy0, wny));
   } else {
     cfg.gridDim = dim3((unsigned)std::min<size_t>((npx + 255) / 256, (size_t)h->sm_count * 16));
-    P2S_CUDA(cudaLaunchKernelEx(&cfg, k_tilt_warp, J, tilt, out, B, C, H, W));
+    P2S_CUDA(cudaLaunchKernelEx(&cfg, k_tilt_warp, J, tilt, out, B, C, H, W, wy0, wny));
   }
   return P2S_OK;
 }
@@ -1527,12 +1537,21 @@ p2s_status p2s_render_host(p2s_handle* h, const float* image_host, int B, int C,
     for (int k = 0; k < nhead; ++k) bands.push_back(left * (k + 1) / nhead - left * k / nhead);
     bands.insert(bands.end(), tailb.rbegin(), tailb.rend());
   }
+  while (h->ev_rend.size() < bands.size()) {
+    cudaEvent_t e;
+    P2S_CUDA(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
+    h->ev_rend.push_back(e);
+  }
+  std::vector<int> band_y0(bands.size() + 1, 0);
+  for (size_t k = 0; k < bands.size(); ++k) band_y0[k + 1] = band_y0[k] + bands[k];
   for (int f = 0; f < B; ++f) {
     const size_t fo_img = (size_t)f * C * HW, fo_z = (size_t)f * h->n_in * HW, fo_t = (size_t)f * 2 * HW;
     P2S_CUDA(cudaMemcpyAsync(h->h_img + fo_img, image_host + fo_img, (size_t)C * HW * 4, cudaMemcpyHostToDevice, h->s_in));
     if (tilt_host)
       P2S_CUDA(cudaMemcpyAsync(h->h_t + fo_t, tilt_host + fo_t, 2 * HW * 4, cudaMemcpyHostToDevice, h->s_in));
     mark("image+tilt in", h->s_in);
+    // J is one buffer: the previous frame's warps must have read it before this frame renders
+    if (f > 0) P2S_CUDA(cudaStreamWaitEvent(st, h->ev_warped, 0));
     for (size_t k = 0, y0 = 0; k < bands.size(); ++k) {
       const int ny = bands[k];
       if (ny == 0) continue;
@@ -1551,14 +1570,49 @@ p2s_status p2s_render_host(p2s_handle* h, const float* image_host, int B, int C,
       s = launch_fused(h, p, st);
       if (s != P2S_OK) return s;
       mark("band rendered", st);
+      P2S_CUDA(cudaEventRecord(h->ev_rend[k], st));
       y0 += ny;
     }
-    s = launch_warp(h, h->d_J, tilt_host ? h->h_t + fo_t : nullptr, h->h_out + fo_img, 1, C, H, W, st);
-    if (s != P2S_OK) return s;
-    mark("warped", st);
-    P2S_CUDA(cudaMemcpyAsync(out_host + fo_img, h->h_out + fo_img, (size_t)C * HW * 4, cudaMemcpyDeviceToHost, st));
-    mark("out copied", st);
+    // Output side, band by band on s_out: the warp of rows [a, b) reads J rows within the frame's
+    // largest |y tilt| (+2 for the bilinear cell and the clamp) of them, so it waits for the band
+    // holding row b - 1 + reach; then those rows go back to the host. Only the last bands' warps
+    // and copies are left once the last input band has rendered.
+    static const bool one_warp = std::getenv("P2S_HOST_ONEWARP") != nullptr;  // (A/B: the old tail)
+    if (one_warp) {
+      s = launch_warp(h, h->d_J, tilt_host ? h->h_t + fo_t : nullptr, h->h_out + fo_img, 1, C, H, W, st);
+      if (s != P2S_OK) return s;
+      P2S_CUDA(cudaMemcpyAsync(out_host + fo_img, h->h_out + fo_img, (size_t)C * HW * 4, cudaMemcpyDeviceToHost, st));
+      P2S_CUDA(cudaEventRecord(h->ev_warped, st));
+      continue;
+    }
+    int reach = 2;
+    if (tilt_host) {
+      const float* ty = tilt_host + fo_t + HW;
+      float m = 0.f;
+      for (size_t i = 0; i < HW; ++i) m = std::max(m, std::fabs(ty[i]));
+      reach = (std::isfinite(m) && m < (float)H) ? (int)std::ceil(m) + 2 : H;
+    }
+    int waited = -1;
+    for (size_t k = 0; k < bands.size(); ++k) {
+      const int a = band_y0[k], ny = bands[k];
+      if (ny == 0) continue;
+      const int need = std::min(H - 1, a + ny - 1 + reach);
+      int j = (int)k;
+      while (band_y0[j + 1] <= need) ++j;  // the band holding row `need`
+      if (j > waited) {
+        P2S_CUDA(cudaStreamWaitEvent(h->s_out, h->ev_rend[j], 0));
+        waited = j;
+      }
+      s = launch_warp(h, h->d_J, tilt_host ? h->h_t + fo_t : nullptr, h->h_out + fo_img, 1, C, H, W, h->s_out, a,
+                      ny, false);
+      if (s != P2S_OK) return s;
+      P2S_CUDA(cudaMemcpy2DAsync(out_host + fo_img + (size_t)a * W, HW * 4, h->h_out + fo_img + (size_t)a * W, HW * 4,
+                                 (size_t)ny * W * 4, C, cudaMemcpyDeviceToHost, h->s_out));
+    }
+    mark("out copied", h->s_out);
+    P2S_CUDA(cudaEventRecord(h->ev_warped, h->s_out));
   }
+  P2S_CUDA(cudaStreamSynchronize(h->s_out));
   P2S_CUDA(cudaStreamSynchronize(st));
   if (trace) {
     cudaDeviceSynchronize();
@@ -1670,6 +1724,9 @@ void p2s_destroy(p2s_handle* h) {
   if (h->s_in) cudaStreamDestroy(h->s_in);
   if (h->ev_entry) cudaEventDestroy(h->ev_entry);
   if (h->ev_band) cudaEventDestroy(h->ev_band);
+  if (h->s_out) cudaStreamDestroy(h->s_out);
+  if (h->ev_warped) cudaEventDestroy(h->ev_warped);
+  for (cudaEvent_t e : h->ev_rend) cudaEventDestroy(e);
   delete h;
 }
 

@@ -1228,16 +1228,18 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads)
 // loads and output stores; the 4 x C gathers per pixel stay scalar). Launched as a programmatic
 // dependent of k_fused_p2s: the tilt (independent of J) is loaded before griddepcontrol.wait,
 // so its HBM latency and the launch overlap the fused kernel's tail.
+// Rows [wy0, wy0 + wny) of every frame (the host path warps row bands as they complete).
 __global__ void __launch_bounds__(256) k_tilt_warp4(const float* __restrict__ J, const float* __restrict__ tilt,
-                                                    float* __restrict__ out, int B, int C, int H, int W) {
-  const size_t HW = (size_t)H * W;
-  const size_t nq = (size_t)B * HW / 4;
+                                                    float* __restrict__ out, int B, int C, int H, int W, int wy0,
+                                                    int wny) {
+  const size_t HW = (size_t)H * W, BW = (size_t)wny * W;
+  const size_t nq = (size_t)B * BW / 4;
   const size_t q = blockIdx.x * (size_t)blockDim.x + threadIdx.x;
   float4 tx = make_float4(0.f, 0.f, 0.f, 0.f), ty = tx;
   size_t b = 0, pix = 0;
   if (q < nq) {
-    b = (q * 4) / HW;
-    pix = q * 4 - b * HW;
+    b = (q * 4) / BW;
+    pix = (size_t)wy0 * W + (q * 4 - b * BW);
     if (tilt) {
       tx = __ldg(reinterpret_cast<const float4*>(tilt + (b * 2 + 0) * HW + pix));
       ty = __ldg(reinterpret_cast<const float4*>(tilt + (b * 2 + 1) * HW + pix));
@@ -1273,12 +1275,13 @@ __global__ void __launch_bounds__(256) k_tilt_warp4(const float* __restrict__ J,
 }
 
 __global__ void __launch_bounds__(256) k_tilt_warp(const float* __restrict__ J, const float* __restrict__ tilt,
-                                                   float* __restrict__ out, int B, int C, int H, int W) {
+                                                   float* __restrict__ out, int B, int C, int H, int W, int wy0,
+                                                   int wny) {
   asm volatile("griddepcontrol.wait;" ::: "memory");
-  const size_t HW = (size_t)H * W;
-  const size_t n = (size_t)B * HW;
+  const size_t HW = (size_t)H * W, BW = (size_t)wny * W;
+  const size_t n = (size_t)B * BW;
   for (size_t i = blockIdx.x * (size_t)blockDim.x + threadIdx.x; i < n; i += (size_t)gridDim.x * blockDim.x) {
-    const size_t b = i / HW, pix = i - b * HW;
+    const size_t b = i / BW, pix = (size_t)wy0 * W + (i - b * BW);
     const int y = (int)(pix / W), x = (int)(pix - (size_t)y * W);
     float tx = 0.f, ty = 0.f;
     if (tilt) {

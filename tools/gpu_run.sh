@@ -1,8 +1,17 @@
 cd $GRAFT_REPO_ROOT
-P2S_LIB=paper_2107_11627_b200/abl_dzv2.so timeout 600 python -m pytest tests -m gpu -x -q -k "mlp_backward or anchors_chain or adjoint_chain" > gpurun_out/t.log 2>&1; echo "pytest rc=$?"; tail -1 gpurun_out/t.log
-for L in abl_dzv abl_dzv2 abl_dzv abl_dzv2; do
-P2S_LIB=paper_2107_11627_b200/$L.so timeout 300 python tools/dz_time.py > gpurun_out/dz_$L.log 2>&1
+timeout 900 python -m pytest tests -m gpu -x -q -k "host or reserve" > gpurun_out/t.log 2>&1; echo "pytest rc=$?"; tail -1 gpurun_out/t.log
+for v in 0 1 0 1; do
+if [ $v = 1 ]; then export P2S_HOST_ONEWARP=1; else unset P2S_HOST_ONEWARP; fi
+timeout 300 python bench.py --steps 20 --warmup 3 --no-cpu-baseline --no-anchor-mode --no-adjoint-mode --no-configs --no-batch-mode --no-sequence-mode --no-color-mode --e2e-steps 60 > gpurun_out/e2e_$v.log 2>&1
 python -c "
-import json; d=json.loads(open('gpurun_out/dz_$L.log').read().strip().splitlines()[-1])
-print('$L', {k: round(v['us_per_frame'],1) for k,v in d.items() if 'stream' not in k and 'cfg5' not in k})"
+import json; d=json.loads(open('gpurun_out/e2e_$v.log').read().strip().splitlines()[-1])
+print('ONEWARP=$v', round(d['value']), 'e2e', round(d['e2e']['value'],1))"
 done
+P2S_HOST_TRACE=1 python -c "
+import numpy as np, torch
+from paper_2107_11627_b200 import p2s, synth
+spec=synth.CONFIGS[3]; inp=synth.make_inputs(spec, frames=[0]); r=p2s.Renderer(inp.basis, inp.mlp)
+pin=lambda a: torch.from_numpy(np.ascontiguousarray(a)).pin_memory().numpy()
+i,z,t=pin(inp.image),pin(inp.zernike),pin(inp.tilt); o=pin(np.zeros_like(inp.image))
+for _ in range(4): r.render_host(i,z,t,o)
+" 2>&1 | tail -24
