@@ -1,17 +1,11 @@
 cd $GRAFT_REPO_ROOT
-timeout 900 python -m pytest tests -m gpu -x -q -k "host or reserve" > gpurun_out/t.log 2>&1; echo "pytest rc=$?"; tail -1 gpurun_out/t.log
-for v in 0 1 0 1; do
-if [ $v = 1 ]; then export P2S_HOST_ONEWARP=1; else unset P2S_HOST_ONEWARP; fi
-timeout 300 python bench.py --steps 20 --warmup 3 --no-cpu-baseline --no-anchor-mode --no-adjoint-mode --no-configs --no-batch-mode --no-sequence-mode --no-color-mode --e2e-steps 60 > gpurun_out/e2e_$v.log 2>&1
-python -c "
-import json; d=json.loads(open('gpurun_out/e2e_$v.log').read().strip().splitlines()[-1])
-print('ONEWARP=$v', round(d['value']), 'e2e', round(d['e2e']['value'],1))"
-done
-P2S_HOST_TRACE=1 python -c "
-import numpy as np, torch
-from paper_2107_11627_b200 import p2s, synth
-spec=synth.CONFIGS[3]; inp=synth.make_inputs(spec, frames=[0]); r=p2s.Renderer(inp.basis, inp.mlp)
-pin=lambda a: torch.from_numpy(np.ascontiguousarray(a)).pin_memory().numpy()
-i,z,t=pin(inp.image),pin(inp.zernike),pin(inp.tilt); o=pin(np.zeros_like(inp.image))
-for _ in range(4): r.render_host(i,z,t,o)
-" 2>&1 | tail -24
+timeout 120 python -c "import __graft_entry__ as g; g.smoke()" > gpurun_out/smoke.log 2>&1; echo "smoke rc=$?"; tail -1 gpurun_out/smoke.log
+timeout 300 python bench.py --steps 5 --warmup 3 --no-cpu-baseline --no-e2e --no-anchor-mode --no-batch-mode --no-sequence-mode --no-adjoint-mode --no-color-mode --no-configs > gpurun_out/plain_bench.log 2>&1; echo "plain rc=$?"
+timeout 600 ncu --metrics gpu__time_duration.sum --clock-control none --csv --log-file gpurun_out/launches.csv \
+    python bench.py --steps 5 --warmup 3 --no-cpu-baseline --no-e2e --no-anchor-mode --no-batch-mode --no-sequence-mode --no-adjoint-mode --no-color-mode --no-configs > gpurun_out/ncu_launch.log 2>&1; echo "ncu launch rc=$?"
+timeout 120 python tools/profile_run.py 3 3 > gpurun_out/prof_plain.log 2>&1
+timeout 600 ncu --set full --clock-control none --import-source on -k regex:k_fused -s 1 -c 1 \
+    -o gpurun_out/prof_fused -f python tools/profile_run.py 3 3 > gpurun_out/ncu_full.log 2>&1; echo "ncu full rc=$?"
+timeout 300 python tools/dz_time.py > gpurun_out/dz_time.log 2>&1
+timeout 300 ncu --set full --clock-control none --import-source on -k regex:k_mlp_backward -s 3 -c 1 \
+    -o gpurun_out/prof_dz_res -f python tools/dz_time.py > gpurun_out/ncu_dz_res.log 2>&1; echo "ncu dz rc=$?"

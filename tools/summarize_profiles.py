@@ -31,7 +31,9 @@ for r in rows[start + 1:]:
     cnt[name] += 1
 shutil.copy(os.path.join(OUT, "launches.csv"), os.path.join(PROF, f"{tag}_launches.csv"))
 ours = {k: v for k, v in tot.items() if k.startswith("p2s::")}
-step_ns = sum(ours.values()) / max(cnt.get("p2s::k_fused_p2s", 1), 1)
+# one render = one launch of each of our kernels (the bench's dedicated fused-kernel loop adds
+# fused launches without a warp, so shares use per-launch averages)
+step_ns = sum(v / cnt[k] for k, v in ours.items())
 with open(os.path.join(PROF, f"{tag}_launch_shares.txt"), "w") as f:
     f.write("ncu --metrics gpu__time_duration.sum --clock-control none (cold-cache, serialised launches)\n")
     f.write("of: python bench.py --steps 5 --warmup 3 --no-cpu-baseline --no-e2e\n\n")
@@ -39,7 +41,7 @@ with open(os.path.join(PROF, f"{tag}_launch_shares.txt"), "w") as f:
         f.write(f"{tot[k] / cnt[k] / 1e3:10.1f} us/launch x{cnt[k]:3d}  {k}\n")
     f.write("\nshare of one p2s_render (our kernels only):\n")
     for k, v in ours.items():
-        f.write(f"  {k:28s} {v / cnt[k] / step_ns * 100:5.1f} %\n")
+        f.write(f"  {k:28s} {v / cnt[k] / step_ns * 100:5.1f} %  (per-launch average / sum of averages)\n")
 
 # ---- full capture of the fused kernel
 rep = os.path.join(OUT, "prof_fused.ncu-rep")
