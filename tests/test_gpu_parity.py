@@ -166,6 +166,9 @@ HOST_CASES = {
     "one_band": SMALL["ragged_rgb_S7"],
     # H = 300: two 118-row bands + a 64-row last band, two frames, ragged W
     "bands_B2": synth.custom("bands", 211, B=2, C=3, H=300, W=130, K=20, S=9, h1=32, h2=32, t_std=2.0),
+    # large tilt (std 25 px): a band's warp reads rows several bands below it (banded output waits
+    # for them); one channel (the one-channel plan); W % 4 != 0 (the scalar warp kernel)
+    "big_tilt_C1": synth.custom("bigtilt", 217, B=2, C=1, H=300, W=130, K=16, S=9, h1=32, h2=32, t_std=25.0),
 }
 
 
