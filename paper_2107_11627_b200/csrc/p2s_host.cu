@@ -154,6 +154,7 @@ struct p2s_handle {
   // dL/dz (k_mlp_backward): resident weight pack and its shared-memory plan (mb_ok = it fits)
   uint8_t* d_mlpb = nullptr;
   int mb_col_b = 0, mb_col_c = 0, mb_off_z = 0;
+  bool mf_ok = false;  // k_mlp_forward usable (resident plan, TMEM regions fit)
   int mb_ok = 0, mb_fold = 0, mb_stream = 0, mb_g3 = 1, mb_nring = 0, mb_slot = 0, mb_off_ring = 0, mb_ring_src_off = 0,
       mb_smem = 0, mb_off_w2 = 0, mb_off_w3 = 0, mb_off_bias = 0, mb_wbytes = 0, mb_off_act = 0, mb_off_bar = 0;
   MlpOp ops[kMaxOps];  // [0, n_ops) per-tile ops, then n_fops first-tile whole-layer ops
@@ -369,6 +370,29 @@ p2s_status launch_warp(const p2s_handle* h, const float* J, const float* tilt, f
     cfg.gridDim = dim3((unsigned)std::min<size_t>((npx + 255) / 256, (size_t)h->sm_count * 16));
     P2S_CUDA(cudaLaunchKernelEx(&cfg, k_tilt_warp, J, tilt, out, B, C, H, W, wy0, wny));
   }
+  return P2S_OK;
+}
+
+// Step a1 for B frames by k_mlp_forward (the resident dL/dz plan's weights, offsets and threads)
+p2s_status launch_mlp_forward(const p2s_handle* h, const float* z, int B, int H, int W, float* beta,
+                              cudaStream_t st) {
+  const size_t HW = (size_t)H * W;
+  const long long tpf = ((long long)HW + 127) / 128;
+  if (tpf * B > 0x7fffffffLL || (unsigned long long)std::max(h->K, h->n_in + 2) * HW > 0x7fffffffULL)
+    return P2S_ERR_UNSUPPORTED;
+  MlpbParams p{};
+  p.z = z; p.wpack = h->d_mlpb; p.b3 = h->d_consts; p.beta = beta;
+  p.B = B; p.HW = (int)HW; p.n_in = h->n_in; p.K = h->K;
+  p.K1 = h->K1; p.N1 = h->N1; p.N2 = h->N2; p.Nk = h->Nk;
+  p.tiles_per_frame = (int)tpf;
+  p.ntiles = (int)(tpf * B);
+  p.off_w2 = h->mb_off_w2; p.off_w3 = h->mb_off_w3; p.off_bias = h->mb_off_bias; p.wbytes = h->mb_wbytes;
+  p.off_act = h->mb_off_act; p.off_bar = h->mb_off_bar;
+  p.col_b = h->mb_col_b; p.col_c = h->mb_col_c; p.off_z = h->mb_off_z;
+  const int grid = std::min(p.ntiles, h->sm_count);
+  if (h->mb_fold) k_mlp_forward<true><<<grid, kMbThreads, h->mb_smem, st>>>(p);
+  else k_mlp_forward<false><<<grid, kMbThreads, h->mb_smem, st>>>(p);
+  P2S_CUDA(cudaPeekAtLastError());
   return P2S_OK;
 }
 
@@ -1002,6 +1026,10 @@ p2s_status init_impl(const p2s_basis* basis, const p2s_mlp* mlp, int cmax, p2s_h
         if ((e = cudaFuncSetAttribute(k_mlp_backward<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, kSmemLimit)) !=
                 cudaSuccess ||
             (e = cudaFuncSetAttribute(k_mlp_backward<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, kSmemLimit)) !=
+                cudaSuccess ||
+            (e = cudaFuncSetAttribute(k_mlp_forward<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, kSmemLimit)) !=
+                cudaSuccess ||
+            (e = cudaFuncSetAttribute(k_mlp_forward<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, kSmemLimit)) !=
                 cudaSuccess)
           return fail(cuda_fail(e, "cudaFuncSetAttribute(k_mlp_backward)"));
         h->mb_smem = smem_res;
@@ -1013,6 +1041,9 @@ p2s_status init_impl(const p2s_basis* basis, const p2s_mlp* mlp, int cmax, p2s_h
         h->mb_off_bar = h->mb_off_act + act_bytes;
         h->mb_col_b = col_b;
         h->mb_col_c = col_c;
+        // the forward MLP kernel (k_mlp_forward) alternates two regions of max(N1, N2, Nk) columns
+        const int wf = std::max(maxN, Nk);
+        h->mf_ok = wf <= col_b && col_b + wf <= 512 && !std::getenv("P2S_BETA_FUSED");
         // the z tile's own buffer after s_max, where it fits
         const int off_z = al128(h->mb_off_bar + 64 + 4 * 128 * 4);
         if (std::getenv("P2S_MB_NOZSEP") == nullptr && off_z + 128 * K1 * 2 <= kSmemLimit) {
@@ -1485,6 +1516,7 @@ p2s_status p2s_debug_beta(p2s_handle* h, const float* zernike_field, int B, int 
   if (!h || !zernike_field || !beta_out || B < 1 || H < 1 || W < 1) return P2S_ERR_INVALID_ARG;
   const size_t n_b = (size_t)B * h->K * H * W, n_z = (size_t)B * h->n_in * H * W;
   if (overlaps(beta_out, n_b * 4, zernike_field, n_z * 4)) return P2S_ERR_INVALID_ARG;
+  if (h->mf_ok) return launch_mlp_forward(h, zernike_field, B, H, W, beta_out, (cudaStream_t)stream);
   FusedParams p = make_params(h, B, 1, H, W, 1);
   p.zernike = zernike_field;
   p.beta_out = beta_out;

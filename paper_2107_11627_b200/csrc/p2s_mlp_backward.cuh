@@ -56,6 +56,8 @@ struct MlpbParams {
   int off_act, off_bar;
   int col_b, col_c;     // resident variant: TMEM columns of the RB / RC accumulator regions
   int off_z;            // resident variant: the z tile's own buffer (0: z goes into ACT)
+  const float* b3;      // k_mlp_forward: fp32 b3 [K] (read through L1)
+  float* beta;          // k_mlp_forward: [B][K][HW] fp32 beta (output)
   // streamed variant (k_mlp_backward_s): the slab table and the ring (B3's W1^T K'-steps are
   // small, K1 x 32 B: g3 of them share one slot, contiguous in W1's layout)
   const uint8_t* ring_src;
@@ -453,6 +455,193 @@ __global__ void __launch_bounds__(kMbThreads, 1) k_mlp_backward(const __grid_con
         }
       }
       tc_fence_before();  // RC reads before the next tile's B3 (ordered by its D4 rounds)
+      b = bn;
+      lt = ltn;
+    }
+  }
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
+  if (warp == 0) tmem_dealloc<512>(tmem);
+}
+
+// ================================================================================================
+// k_mlp_forward: step a1 alone -- beta = W3 relu(W2 relu(W1 z + b1) + b2) + b3 per pixel -- with
+// the resident variant's weight pack, threads and round streaming (used by p2s_debug_beta and by
+// the sequence mode's beta pass): F1 Z W1^T, F2 A1 W2^T, F3 A2 W3^T (W3^T read
+// transposed out of the pack's W3^T tile, like B2 reads W2). TMEM regions X / Y alternate per
+// tile (F1 -> X, F2 -> Y, F3 -> X), so the next tile's F1 (into this tile's Y) runs while this
+// tile's beta drain reads X. b3 is added in fp32 by the beta drain.
+template <bool kFold>
+__global__ void __launch_bounds__(kMbThreads, 1) k_mlp_forward(const __grid_constant__ MlpbParams p) {
+  using namespace mlpb;
+  extern __shared__ __align__(1024) uint8_t smem[];
+  const uint32_t sbase = smem_u32(smem);
+  uint64_t* bar_w = reinterpret_cast<uint64_t*>(smem + p.off_bar);
+  uint64_t* bar_mma = bar_w + 1;  // F2, F3 done
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bar_w + 2);
+  uint64_t* bar_f1 = bar_w + 3;   // F1 done
+  uint64_t* bar_rnd = bar_w + 4;  // [4] operand-round ring
+  const float* s_b1 = reinterpret_cast<const float*>(smem + p.off_bias);
+  const float* s_b2 = s_b1 + p.N1;
+  uint8_t* act = smem + p.off_act;
+  const uint32_t act_s = sbase + (uint32_t)p.off_act;
+  const bool zsep = p.off_z > 0;
+  uint8_t* zbuf = zsep ? smem + p.off_z : act;
+  const uint32_t z_s = sbase + (uint32_t)(zsep ? p.off_z : p.off_act);
+  const int tid = (int)threadIdx.x, warp = (int)warp_id();
+
+  if (tid == 0) {
+    mbar_init(bar_w, 1);
+    mbar_init(bar_mma, 1);
+    mbar_init(bar_f1, 1);
+    for (int i = 0; i < 4; ++i) mbar_init(&bar_rnd[i], kMbDrainWarps);
+    fence_mbar_init();
+  }
+  if (warp == 0) tmem_alloc<512>(tmem_slot);
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
+  const uint32_t tmem = __shfl_sync(0xffffffffu, *tmem_slot, 0);
+  if (tid == 0) {
+    mbar_arrive_expect_tx(bar_w, (uint32_t)p.wbytes);
+    for (int off = 0; off < p.wbytes; off += 32768)
+      bulk_g2s(smem + off, p.wpack + off, (uint32_t)min(32768, p.wbytes - off), bar_w);
+  }
+  const uint32_t tR0 = tmem, tR1 = tmem + (uint32_t)p.col_b;  // X = tR0 on even tiles of the CTA
+
+  if (warp == kMbDrainWarps) {
+    // ================= UMMA issuer
+    const uint32_t id_f1 = idesc_f16(128, (uint32_t)p.N1), id_f2 = idesc_f16(128, (uint32_t)p.N2);
+    const uint32_t id_f3 = idesc_f16(128, (uint32_t)p.Nk) | (1u << 16);
+    const uint32_t w1_s = sbase, w2_s = sbase + (uint32_t)p.off_w2, w3_s = sbase + (uint32_t)p.off_w3;
+    uint32_t rs = 0;
+    auto gemm_rounds = [&](uint32_t d, uint32_t a_s, int nks, uint32_t b_s, uint32_t b_lbo, uint32_t b_sbo,
+                           uint32_t b_kstep, uint32_t idesc, uint64_t* done) {
+      const uint32_t a_sbo = (uint32_t)nks * 256u;
+      for (int k0 = 0; k0 < nks; k0 += 4, ++rs) {
+        mbar_wait(&bar_rnd[rs & 3u], (rs >> 2) & 1u);
+        tc_fence_after();
+        const int k1 = min(nks, k0 + 4);
+        for (int ks = k0; ks < k1; ++ks)
+          umma_f16_elect(d, sdesc(a_s + (uint32_t)ks * 256u, 128u, a_sbo),
+                         sdesc(b_s + (uint32_t)ks * b_kstep, b_lbo, b_sbo), idesc, ks > 0 ? 1u : 0u);
+      }
+      umma_commit_elect(done);
+    };
+    if ((int)blockIdx.x < p.ntiles) mbar_wait(bar_w, 0);
+    uint32_t par = 0;
+    for (int t = (int)blockIdx.x; t < p.ntiles; t += (int)gridDim.x, par ^= 1u) {
+      const uint32_t tX = par ? tR1 : tR0, tY = par ? tR0 : tR1;
+      gemm_rounds(tX, z_s, p.K1 / 16, w1_s, 128u, (uint32_t)p.K1 * 16u, 256u, id_f1, bar_f1);     // F1 <- z
+      gemm_rounds(tY, act_s, p.N1 / 16, w2_s, 128u, (uint32_t)p.N1 * 16u, 256u, id_f2, bar_mma);  // F2 <- a1
+      gemm_rounds(tX, act_s, p.N2 / 16, w3_s, (uint32_t)p.Nk * 16u, 128u, (uint32_t)p.Nk * 32u, id_f3,
+                  bar_mma);  // F3 <- a2 (W3^T tile read transposed)
+    }
+  } else {
+    // ================= drains (4 threads per pixel row, groups 4 r + q)
+    const int m = tid & 127, q = tid >> 7;
+    const uint32_t tq = (uint32_t)(32 * (warp & 3)) << 16;
+    const size_t HW = (size_t)p.HW, HWB = HW * 4;
+    uint8_t* const row_k1 = row_of(zbuf, m, p.K1);
+    uint8_t* const row_n1 = row_of(act, m, p.N1);
+    uint8_t* const row_n2 = row_of(act, m, p.N2);
+    const int G1 = p.N1 / 16, G2 = p.N2 / 16, Gk = p.Nk / 16, Gz = p.K1 / 16;
+    uint32_t ph = 0, ph1 = 0, rs = 0, par = 0;
+    auto round_done = [&] {
+      fence_proxy_async_smem();
+      tc_fence_before();
+      __syncwarp();
+      if ((tid & 31) == 0) mbar_arrive(&bar_rnd[rs & 3u]);
+      ++rs;
+    };
+    auto wait_mma = [&] {
+      mbar_wait(bar_mma, ph);
+      ph ^= 1;
+      tc_fence_after();
+    };
+    int b = (int)blockIdx.x / p.tiles_per_frame, lt = (int)blockIdx.x - b * p.tiles_per_frame;
+    auto advance = [&](int& bb, int& ll) {
+      ll += (int)gridDim.x;
+      while (ll >= p.tiles_per_frame) { ll -= p.tiles_per_frame; ++bb; }
+    };
+    float zv[16];
+    auto load_z16 = [&](int bb, int ll) {
+      const int px = min(ll * 128 + m, p.HW - 1);
+      load16b(p.z + (size_t)bb * p.n_in * HW + px + (size_t)(q * 16) * HW, HWB, p.n_in - q * 16, zv);
+    };
+    auto store_z = [&] {
+      if (q < Gz) {
+#pragma unroll
+        for (int j = 0; j < 16; ++j) {
+          const int ch = q * 16 + j;
+          if (ch >= p.n_in) zv[j] = (kFold && ch < p.n_in + 2) ? 1.f : 0.f;
+        }
+        st8f(row_k1, 2 * q, zv);
+        st8f(row_k1, 2 * q + 1, zv + 8);
+      }
+      round_done();
+    };
+    // one relu drain of a TMEM region into the ACT columns of the next GEMM, per round
+    auto relu_drain = [&](uint32_t tr, int G, uint8_t* row, const float* bias) {
+#pragma unroll
+      for (int r = 0; r < 4; ++r) {
+        const int g = 4 * r + q;
+        if (4 * r < G) {
+          if (g < G) {
+            float v[16];
+            tmem_ld16(tr + tq + (uint32_t)(g * 16), v);
+            tmem_ld_wait();
+            if (!kFold) {
+#pragma unroll
+              for (int j = 0; j < 16; ++j) v[j] += bias[g * 16 + j];
+            }
+            st8(row, 2 * g, relu2(v[0], v[1]), relu2(v[2], v[3]), relu2(v[4], v[5]), relu2(v[6], v[7]));
+            st8(row, 2 * g + 1, relu2(v[8], v[9]), relu2(v[10], v[11]), relu2(v[12], v[13]), relu2(v[14], v[15]));
+          }
+          round_done();
+        }
+      }
+    };
+    load_z16(b, lt);
+    store_z();
+    if (!kFold) mbar_wait(bar_w, 0);  // the fp32 biases the drains add
+    for (int t = (int)blockIdx.x; t < p.ntiles; t += (int)gridDim.x, par ^= 1u) {
+      const uint32_t tX = par ? tR1 : tR0, tY = par ? tR0 : tR1;
+      const int px = lt * 128 + m;
+      const bool valid = px < p.HW;
+      int bn = b, ltn = lt;
+      advance(bn, ltn);
+      const bool more = t + (int)gridDim.x < p.ntiles;
+      mbar_wait(bar_f1, ph1);  // F1
+      ph1 ^= 1;
+      tc_fence_after();
+      relu_drain(tX, G1, row_n1, s_b1);  // a1 -> ACT (F2 streams on it)
+      if (more) load_z16(bn, ltn);        // next tile's z (in flight during F2 / D2)
+      wait_mma();                         // F2: ACT is free
+      relu_drain(tY, G2, row_n2, s_b2);  // a2 -> ACT (F3 streams on it)
+      if (more && zsep) store_z();        // the next tile's F1 (into Y) runs behind F3
+      wait_mma();                         // F3: beta in X; ACT is free
+      if (more && !zsep) store_z();
+      // ---- beta = D3 + b3 -> global [b][k][px] (K real columns; coalesced: lanes are pixels)
+      float* ob = p.beta + (size_t)b * p.K * HW + px;
+#pragma unroll
+      for (int r = 0; r < 2; ++r) {
+        const int g = 4 * r + q;
+        if (g < Gk) {
+          float v[16];
+          tmem_ld16(tX + tq + (uint32_t)(g * 16), v);
+          tmem_ld_wait();
+          if (valid) {
+            char* ptr = reinterpret_cast<char*>(ob + (size_t)(g * 16) * HW);
+            const int nv = p.K - g * 16;
+#pragma unroll
+            for (int j = 0; j < 16; ++j, ptr += HWB)
+              if (j < nv) __stcs(reinterpret_cast<float*>(ptr), v[j] + __ldg(p.b3 + g * 16 + j));
+          }
+        }
+      }
+      tc_fence_before();  // X reads before the next tile's F2 (ordered by its D1 rounds)
       b = bn;
       lt = ltn;
     }

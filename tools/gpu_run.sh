@@ -1,2 +1,4 @@
 cd $GRAFT_REPO_ROOT
-timeout 600 python -m pytest tests -m gpu -q -k "host" > gpurun_out/t.log 2>&1; echo "pytest rc=$?"; tail -2 gpurun_out/t.log
+timeout 900 python -m pytest tests -m gpu -q > gpurun_out/gputest.log 2>&1; echo "pytest rc=$?"
+tail -2 gpurun_out/gputest.log
+python tools/beta_time.py
