@@ -257,6 +257,8 @@ ANCHOR_CASES = {
     "rgb_S7_G1": (SMALL["ragged_rgb_S7"], 1),
     "S33_K100_G16": (SMALL["S33_K100_C2"], 16),
     "S33_K100_G2": (SMALL["S33_K100_C2"], 2),
+    # one channel: the one-channel plan (MLP ahead) with anchor-grid A1 builds, several tiles per CTA
+    "C1_S9_G7": (SMALL["many_tiles_C1_S9"], 7),
 }
 
 
@@ -295,8 +297,9 @@ def test_anchor_grid_cfg3_sampled(p2s, G):
     _cmp(out[bxy[:, 0], :, bxy[:, 1], bxy[:, 2]], oref, f"render_anchors[cfg3 G={G} sampled]")
 
 
-def test_anchor_grid_host_matches_device(p2s):
-    spec, G = ANCHOR_CASES["rgb_S7_G5"]
+@pytest.mark.parametrize("name", ["rgb_S7_G5", "C1_S9_G7"])
+def test_anchor_grid_host_matches_device(p2s, name):
+    spec, G = ANCHOR_CASES[name]
     inp = synth.make_inputs(spec)
     anc = _anchors(spec, G, 11)
     r = p2s.Renderer(inp.basis, inp.mlp)
