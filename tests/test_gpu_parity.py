@@ -835,6 +835,22 @@ def test_outputs_stay_in_bounds(p2s, name):
         assert np.all(np.isfinite(inner)), f"{what}: non-finite values"
 
 
+@pytest.mark.parametrize("cfg", [1, 2, 3, 5])
+def test_info_reports_the_plans(p2s, cfg):
+    """p2s_get_info: the BASELINE configs' handles carry a one-channel plan (used by every C = 1
+    call) next to the multi-channel one, each within the 227 KB shared-memory limit."""
+    spec = synth.CONFIGS[cfg]
+    inp = synth.make_inputs(spec, frames=[0])
+    r = p2s.Renderer(inp.basis, inp.mlp)
+    info = r.info()
+    assert info["c1_plan"] == 1 and info["mlp_backward"] == 1
+    for k in ("smem_bytes", "c1_smem_bytes"):
+        assert 0 < info[k] <= 232448, (k, info[k])
+    assert info["nring"] >= 2 and info["c1_nring"] >= 2
+    assert info["n_pad"] % 16 == 0 and info["n_pad"] >= spec.K
+    r.close()
+
+
 def test_empty_and_out_of_envelope_dims(p2s):
     """Zero-sized frames are argument errors, C > 3 is outside the envelope (include/p2s.h)."""
     inp = synth.make_inputs(SMALL["ragged_rgb_S7"])
