@@ -284,6 +284,9 @@ typedef struct {
   int c1_plan;                       /* 1: one-channel calls run on a one-channel plan (E buffers and
                                         TMEM for C = 1; one op per MLP layer) */
   int c1_smem_bytes, c1_nring, c1_stage_bytes; /* that plan's shared memory and ring (0 if none) */
+  int seq_plan;                      /* 1: p2s_render_sequence (C > 1) runs on a half-E plan of its own
+                                        (two half-size E buffers, a larger operand ring) */
+  int seq_nring, seq_stage_bytes;    /* that plan's ring (0 if none) */
 } p2s_info;
 P2S_API p2s_status p2s_get_info(const p2s_handle* h, p2s_info* info);
 

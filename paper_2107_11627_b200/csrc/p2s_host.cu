@@ -195,6 +195,7 @@ struct p2s_handle {
   int mlp_ahead = 0;            // 1: a tile's L1 / L2 run ahead of the previous tile's conv epilogue
   int l1_early = 0;             // 1: the first L1 chunk lies past beta and issues before the accumulators free
   p2s_handle* c1 = nullptr;     // a one-channel plan of the same model (C = 1 calls use it)
+  p2s_handle* seq = nullptr;    // a half-E plan of the same model (p2s_render_sequence, C > 1, uses it)
 };
 
 namespace {
@@ -428,7 +429,11 @@ namespace {
 // after cmax conv accumulators. cmax = 1 leaves 400 TMEM columns for the MLP, so
 // each layer is one op (three MLP round trips per tile instead of five) and the E buffers take a
 // third of the shared memory.
-p2s_status init_impl(const p2s_basis* basis, const p2s_mlp* mlp, int cmax, p2s_handle** out_handle) {
+// force_half: take the half-E plan (two half buffers, a larger ring) where it exists even if two full
+// E buffers fit -- the plan of the sequence sub-handle; *out_handle is then null
+// (P2S_OK) when that plan does not exist or the default plan is a half-E plan already.
+p2s_status init_impl(const p2s_basis* basis, const p2s_mlp* mlp, int cmax, p2s_handle** out_handle,
+                     bool force_half = false) {
   if (!basis || !mlp || !out_handle || !basis->taps || !mlp->W1 || !mlp->b1 || !mlp->W2 ||
       !mlp->b2 || !mlp->W3 || !mlp->b3)
     return P2S_ERR_INVALID_ARG;
@@ -589,7 +594,12 @@ p2s_status init_impl(const p2s_basis* basis, const p2s_mlp* mlp, int cmax, p2s_h
     const int eh_pref = eh_env ? std::atoi(eh_env) : -1;
     const int e1_full = cmax * h->plan.chan_bytes, e2_half = cmax * (plan_half.chan_bytes + plan_half.chan_bytes1);
     const bool full2_fits = kSmemLimit - fixed - al(2 * e1_full) - 1024 >= 3 * 12288;
-    const bool use_half = plan_half.ehalf && ebuf_max == 2 && (eh_pref == 1 || (eh_pref != 0 && !full2_fits));
+    const bool use_half = plan_half.ehalf && ebuf_max == 2 &&
+                          (force_half || eh_pref == 1 || (eh_pref != 0 && !full2_fits));
+    if (force_half && (!plan_half.ehalf || ebuf_max != 2 || !full2_fits || eh_pref >= 0)) {
+      delete h;  // no separate half-E plan to make
+      return P2S_OK;
+    }
     e1_bytes = use_half ? (e2_half + 1) / 2 : e1_full;  // (n_ebuf * e1_bytes covers both halves)
     conv_cut = use_half ? plan_half.cut : 0;
     if (use_half) {
@@ -1125,6 +1135,12 @@ p2s_status p2s_init(const p2s_basis* basis, const p2s_mlp* mlp, p2s_handle** out
   const p2s_status s1 = init_impl(basis, mlp, 1, &c1);
   if (s1 == P2S_OK) (*out_handle)->c1 = c1;  // (optional: C = 1 calls fall back to the main plan)
   if (std::getenv("P2S_DEBUG_C1")) std::fprintf(stderr, "p2s: one-channel plan %s\n", p2s_status_string(s1));
+  // sequences of multi-channel frames are MLP passes over resident accumulators: the half-E plan's
+  // larger ring serves them better; optional, like the one-channel plan
+  if (!std::getenv("P2S_NO_SEQPLAN")) {
+    p2s_handle* sq = nullptr;
+    if (init_impl(basis, mlp, 3, &sq, true) == P2S_OK && sq) (*out_handle)->seq = sq;
+  }
   return P2S_OK;
 }
 
@@ -1154,6 +1170,7 @@ p2s_status p2s_set_profile_events(p2s_handle* h, p2s_event_t ev_begin, p2s_event
   h->ev_begin = (cudaEvent_t)ev_begin;
   h->ev_end = (cudaEvent_t)ev_end;
   if (h->c1) p2s_set_profile_events(h->c1, ev_begin, ev_end);
+  if (h->seq) p2s_set_profile_events(h->seq, ev_begin, ev_end);
   return P2S_OK;
 }
 
@@ -1213,13 +1230,16 @@ p2s_status p2s_render_sequence(p2s_handle* h, p2s_image im, const float* zernike
   cudaStream_t st = (cudaStream_t)stream;
   s = ensure_J(h, n_out);
   if (s != P2S_OK) return s;
-  FusedParams p = make_params(h, 1, im.C, im.H, im.W, 0);
+  // the fused pass runs on the sequence sub-plan where there is one (J stays this handle's workspace,
+  // so p2s_reserve covers sequences as before)
+  p2s_handle* hf = (h->seq && im.C > 1) ? h->seq : h;
+  FusedParams p = make_params(hf, 1, im.C, im.H, im.W, 0);
   p.nfr = F;  // tiles of the one image; every tile serves all F frames (J / Zernike frame = fr)
   p.image = im.data;
   p.zernike = zernike_field;
   p.J = h->d_J;
   if (h->ev_begin) P2S_CUDA(cudaEventRecord(h->ev_begin, st));
-  s = launch_fused(h, p, st);
+  s = launch_fused(hf, p, st);
   if (s != P2S_OK) return s;
   if (h->ev_end) P2S_CUDA(cudaEventRecord(h->ev_end, st));
   return launch_warp(h, h->d_J, tilt_field, out, F, im.C, im.H, im.W, st);
@@ -1718,6 +1738,7 @@ p2s_status p2s_debug_profile_buffer(p2s_handle* h, void* device_counters) {
 #if defined(P2S_PROFILE) || defined(P2S_STARTUP_PROF)
   h->prof = (unsigned long long*)device_counters;
   if (h->c1) h->c1->prof = h->prof;
+  if (h->seq) h->seq->prof = h->prof;
   return P2S_OK;
 #else
   (void)device_counters;
@@ -1739,12 +1760,16 @@ p2s_status p2s_get_info(const p2s_handle* h, p2s_info* info) {
   info->c1_smem_bytes = h->c1 ? h->c1->smem_bytes : 0;
   info->c1_nring = h->c1 ? h->c1->nring : 0;
   info->c1_stage_bytes = h->c1 ? h->c1->stage_bytes : 0;
+  info->seq_plan = h->seq ? 1 : 0;
+  info->seq_nring = h->seq ? h->seq->nring : 0;
+  info->seq_stage_bytes = h->seq ? h->seq->stage_bytes : 0;
   return P2S_OK;
 }
 
 void p2s_destroy(p2s_handle* h) {
   if (!h) return;
   if (h->c1) p2s_destroy(h->c1);
+  if (h->seq) p2s_destroy(h->seq);
   cudaDeviceSynchronize();
   cudaFree(h->d_stream); cudaFree(h->d_items); cudaFree(h->d_mma); cudaFree(h->d_steps); cudaFree(h->d_consts);
   cudaFree(h->d_J);

@@ -61,7 +61,8 @@ class Info(ctypes.Structure):
     _fields_ = [(n, ctypes.c_int) for n in ("K", "S", "n_in", "h1", "h2", "n_pad", "h1_pad", "h2_pad",
                                             "in_pad", "conv_steps", "smem_bytes", "kernels_per_render",
                                             "stage_bytes", "nring", "mlp_backward", "c1_plan", "c1_smem_bytes",
-                                            "c1_nring", "c1_stage_bytes")]
+                                            "c1_nring", "c1_stage_bytes", "seq_plan", "seq_nring",
+                                            "seq_stage_bytes")]
 
     def as_dict(self):
         return {n: getattr(self, n) for n, _ in self._fields_}
