@@ -309,6 +309,29 @@ def test_anchor_grid_host_matches_device(p2s, name):
     np.testing.assert_array_equal(host, dev)
 
 
+@pytest.mark.parametrize("case", ["rgb_tilt", "rgb_big_tilt", "rgb_no_tilt", "gray_tilt"])
+def test_anchor_grid_host_tall_frames_match_device(p2s, case):
+    """p2s_render_anchors_host on taller frames (264 rows, two frames per call; written for a
+    row-banded variant of the path that measured slower and was not kept):
+    bit-identical to the device path with a small tilt, a tilt reaching ~100 rows, and no tilt,
+    on both channel plans, also on warm staging buffers."""
+    C = 1 if case == "gray_tilt" else 3
+    t_std = {"rgb_tilt": 1.5, "rgb_big_tilt": 30.0, "rgb_no_tilt": 0.0, "gray_tilt": 2.0}[case]
+    spec = synth.custom(f"anc_host_{case}", 1200 + len(case), B=2, C=C, H=264, W=130, K=20, S=9, h1=48, h2=40,
+                        t_std=max(t_std, 0.1))
+    inp = synth.make_inputs(spec)
+    anc = synth.make_anchors(spec, 6)
+    tilt = None if case == "rgb_no_tilt" else inp.tilt
+    r = p2s.Renderer(inp.basis, inp.mlp)
+    dev = r.render_anchors(_dev(inp.image), _dev(anc), _dev(tilt) if tilt is not None else None).cpu().numpy()
+    host = np.full_like(inp.image, np.nan)
+    r.render_anchors_host(inp.image, anc, tilt, host)
+    np.testing.assert_array_equal(host, dev)
+    host2 = np.full_like(inp.image, np.nan)  # a second call on warm staging buffers
+    r.render_anchors_host(inp.image, anc, tilt, host2)
+    np.testing.assert_array_equal(host2, dev)
+
+
 def test_anchor_grid_invalid_args(p2s):
     spec, G = ANCHOR_CASES["rgb_S7_G5"]
     inp = synth.make_inputs(spec)
