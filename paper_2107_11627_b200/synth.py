@@ -29,7 +29,8 @@ from typing import Optional
 
 import numpy as np
 
-STREAM_IMAGE, STREAM_ZERNIKE, STREAM_TILT, STREAM_BASIS, STREAM_MLP, STREAM_RECT, STREAM_ANCHORS, STREAM_GRAD = range(8)
+STREAM_IMAGE, STREAM_ZERNIKE, STREAM_TILT, STREAM_BASIS, STREAM_MLP, STREAM_RECT, STREAM_ANCHORS, STREAM_GRAD, \
+    STREAM_TILE = range(9)
 
 
 @dataclass(frozen=True)
@@ -238,3 +239,21 @@ def make_inputs(spec: Spec, frames: Optional[range] = None) -> Inputs:
     z = np.stack([make_zernike(spec, f) for f in frames])
     t = np.stack([make_tilt(spec, f) for f in frames])
     return Inputs(replace(spec, B=len(frames)), img, z, t, make_basis(spec), make_mlp(spec))
+
+
+# ---- huge frames (maximum-size tests): a base block tiled ry x rx times, every replica scaled by its
+# own seeded factors so that no two tiles hold the same values. The full arrays (several GB) are
+# only ever built on the device, by indexing alone (the test's `repeat` + two multiplies in this
+# order); the host takes crops of the same definition: big[..., y, x] =
+# (base[..., y % bh, x % bw] * sy[y // bh]) * sx[x // bw], all in fp32.
+def tile_scales(spec: Spec, n: int, axis: int) -> np.ndarray:
+    """n per-tile scale factors U[0.75, 1.25) (fp32) for tile rows (axis 0) or columns (axis 1)."""
+    return _rng(spec.cfg_id, axis, STREAM_TILE).uniform(0.75, 1.25, n).astype(np.float32)
+
+
+def tiled_crop(base: np.ndarray, sy: np.ndarray, sx: np.ndarray, y0: int, y1: int, x0: int, x1: int) -> np.ndarray:
+    """Rows [y0, y1) x columns [x0, x1) of the tiled array of `base` [..., bh, bw] (fp32)."""
+    bh, bw = base.shape[-2:]
+    ys, xs = np.arange(y0, y1), np.arange(x0, x1)
+    blk = np.asarray(base, np.float32)[..., (ys % bh)[:, None], (xs % bw)[None, :]]
+    return (blk * sy[ys // bh][:, None]) * sx[xs // bw][None, :]

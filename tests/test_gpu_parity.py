@@ -297,6 +297,64 @@ def test_anchor_grid_cfg3_sampled(p2s, G):
     _cmp(out[bxy[:, 0], :, bxy[:, 1], bxy[:, 2]], oref, f"render_anchors[cfg3 G={G} sampled]")
 
 
+@pytest.mark.parametrize("C", [1, 3])
+def test_huge_frame_offsets_beyond_2_31_elements(p2s, C):
+    """Maximum sizes: one 6144 x 6144 frame with n_in = 64 -- the Zernike field has 2.4e9 elements
+    (9.7 GB), so every element index and byte offset in the path must be 64-bit. The frame is a
+    256 x 256 base block tiled 24 x 24 times with per-tile scale factors (built on the device by
+    indexing; synth.tiled_crop gives the host the same values); the oracle renders 64 x 64 windows
+    (corners, centre, tile seams, the last rows) and every pixel whose dependencies (r rows / columns
+    of taps + the tilt) lie inside its window -- or that sits at a true frame edge -- is compared."""
+    import torch
+    free, _ = torch.cuda.mem_get_info()
+    if free < 16 << 30:
+        pytest.skip("needs 16 GB of free device memory")
+    bh = bw = 256
+    ry = rx = 24
+    H, W = bh * ry, bw * rx
+    spec = synth.custom(f"huge_C{C}", 1300 + C, B=1, C=C, H=bh, W=bw, K=8, S=7, n_in=64, h1=32, h2=32, t_std=1.5)
+    assert spec.n_in * H * W > 2 ** 31
+    inp = synth.make_inputs(spec)
+    sy, sx = synth.tile_scales(spec, ry, 0), synth.tile_scales(spec, rx, 1)
+    sy_d = _dev(sy).repeat_interleave(bh)[:, None]
+    sx_d = _dev(sx).repeat_interleave(bw)[None, :]
+
+    def big(base):  # [1, n, bh, bw] -> [1, n, H, W] on the device: (base * sy) * sx
+        t = _dev(base).repeat(1, 1, ry, rx)
+        t *= sy_d
+        t *= sx_d
+        return t
+
+    # the image stays in [0, 1.25^2); the tilt is scaled too (max |t| below is taken per window)
+    img_d, z_d, t_d = big(inp.image), big(inp.zernike), big(inp.tilt)
+    r = p2s.Renderer(inp.basis, inp.mlp)
+    out_d = r.render(img_d, z_d, t_d)
+    torch.cuda.synchronize()
+    rad = (spec.S - 1) // 2
+    Wn = 64
+    wins = [(0, 0), (H - Wn, W - Wn), (H - Wn, 0), (0, W - Wn), (H // 2 - 17, W // 2 + 5),
+            (bh * 11 - 30, bw * 7 - 34), (bh * 23 - 32, bw * 23 - 32), (H - Wn, bw * 12 - 20)]
+    worst = 0.0
+    for (y0, x0) in wins:
+        y1, x1 = y0 + Wn, x0 + Wn
+        ci = synth.tiled_crop(inp.image, sy, sx, y0, y1, x0, x1)
+        cz = synth.tiled_crop(inp.zernike, sy, sx, y0, y1, x0, x1)
+        ct = synth.tiled_crop(inp.tilt, sy, sx, y0, y1, x0, x1)
+        np.testing.assert_array_equal(cz, z_d[..., y0:y1, x0:x1].cpu().numpy())  # same inputs on both sides
+        ref, _ = oracle.render(ci, cz, ct, inp.basis, inp.mlp)
+        m = rad + int(np.ceil(np.abs(ct).max())) + 2
+        assert 2 * m < Wn - 8, m
+        ya, yb = (0 if y0 == 0 else m), (Wn if y1 == H else Wn - m)
+        xa, xb = (0 if x0 == 0 else m), (Wn if x1 == W else Wn - m)
+        got = out_d[..., y0:y1, x0:x1].cpu().numpy()
+        mx, _ = _cmp(got[..., ya:yb, xa:xb], ref[..., ya:yb, xa:xb], f"huge[C={C} window ({y0},{x0})]")
+        worst = max(worst, mx)
+    print(f"huge[C={C}]: worst window max_abs {worst:.3e}")
+    r.close()
+    del img_d, z_d, t_d, out_d
+    torch.cuda.empty_cache()
+
+
 @pytest.mark.parametrize("name", ["rgb_S7_G5", "C1_S9_G7"])
 def test_anchor_grid_host_matches_device(p2s, name):
     spec, G = ANCHOR_CASES[name]

@@ -45,6 +45,9 @@ with open(os.path.join(PROF, f"{tag}_launch_shares.txt"), "w") as f:
 
 # ---- full capture of the fused kernel
 rep = os.path.join(OUT, "prof_fused.ncu-rep")
+if not os.path.exists(rep):  # a launch-list-only evidence run (tools/evidence_run.sh): keep the last capture
+    print(open(os.path.join(PROF, f"{tag}_launch_shares.txt")).read())
+    sys.exit(0)
 raw = subprocess.run(["ncu", "-i", rep, "--page", "raw", "--csv"], capture_output=True, text=True).stdout
 rr = list(csv.reader(raw.splitlines()))
 h, u, v = rr[0], rr[1], rr[2]
