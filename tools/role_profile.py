@@ -1,7 +1,8 @@
 """Per-role cycle breakdown of k_fused_p2s (needs libp2s_prof.so, built with -DP2S_PROFILE).
 
 Usage: P2S_LIB=paper_2107_11627_b200/libp2s_prof.so python tools/role_profile.py [cfg]
-       (ADJ=image: the adjoint's fused pass instead of the render; ANCHOR_G=G: anchor mode)
+       (ADJ=image: the adjoint's fused pass instead of the render; ANCHOR_G=G: anchor mode;
+        TRACE_B=n: n frames per call)
 Counters (clock64 cycles, averaged over CTAs), per role:
   MMA issuer : 0 wait A1_FULL, 1 wait BETA_FREE, 2 wait SCR_FREE, 3 wait E_FULL,
                4 wait ring (MLP), 5 wait ring (conv), 6 wait ACC_FREE (first conv stage), 19 total
@@ -22,7 +23,8 @@ cfg = int(sys.argv[1]) if len(sys.argv) > 1 else 3
 spec = synth.CONFIGS[cfg]
 if os.environ.get("TRACE_H"):
     spec = synth.custom("h", cfg, B=1, C=spec.C, H=int(os.environ["TRACE_H"]), W=spec.W, K=spec.K, S=spec.S, h1=spec.h1, h2=spec.h2)
-inp = synth.make_inputs(spec, frames=range(1))
+NB = int(os.environ.get("TRACE_B", "1"))  # frames per call
+inp = synth.make_inputs(spec, frames=range(NB))
 r = p2s.Renderer(inp.basis, inp.mlp)
 img, z, t = (torch.from_numpy(a).cuda() for a in (inp.image, inp.zernike, inp.tilt))
 out = torch.empty_like(img)
@@ -50,7 +52,7 @@ names = {0: {0: "wait A1_FULL", 1: "wait TMEM_FREE", 2: "wait SCR_FREE", 3: "wai
          2: {9: "wait A1_EMPTY", 11: "wait E_EMPTY", 12: "build E", 19: "total"},
          3: {13: "wait MLP_DONE", 15: "wait ACC_FULL", 16: "conv epi to release", 17: "MLP drain work", 18: "drain fence+arrive", 19: "total"}}
 roles = ["MMA", "producer", "builder", "epilogue"]
-ntiles = spec.H * ((spec.W + 127) // 128)
+ntiles = NB * spec.H * ((spec.W + 127) // 128)
 print(f"cfg{cfg}: {ntiles} tiles over 148 CTAs (~{ntiles / 148:.1f} tiles/CTA); cycles per CTA (mean / max)")
 for ri, role in enumerate(roles):
     for k, n in names[ri].items():
