@@ -9,7 +9,8 @@ if [ "$1" = build ]; then
     n=${v%%:*}; f=${v#*:}; f=${f//_-D/ -D}
     /usr/local/cuda/bin/nvcc -gencode arch=compute_100a,code=sm_100a -O3 -std=c++17 -shared -Xcompiler -fPIC \
       -Xcompiler -fvisibility=hidden -maxrregcount=144 -Iinclude -Ipaper_2107_11627_b200/csrc $f \
-      paper_2107_11627_b200/csrc/p2s_host.cu -o paper_2107_11627_b200/abl_$n.so &
+      paper_2107_11627_b200/csrc/p2s_host.cu paper_2107_11627_b200/csrc/p2s_sampler.cu paper_2107_11627_b200/csrc/p2s_anchor.cu \
+      -o paper_2107_11627_b200/abl_$n.so &
   done
   wait
 else
