@@ -6,6 +6,7 @@ configs on sampled pixels the oracle computes one by one (oracle.pixels), at exa
 launch configuration bench.py times.
 """
 import ctypes
+import os
 
 import numpy as np
 import pytest
@@ -116,6 +117,29 @@ def test_render_parity(p2s, name):
     ref, _ = oracle.render(inp.image, inp.zernike, inp.tilt, inp.basis, inp.mlp)
     _cmp(out, ref, f"render[{name}]", norm_ref=inp.image if name in REL_TO_INPUT else None)
     r.close()
+
+
+def test_golden_hand_worked_3x3_frame(p2s):
+    """The CUDA path against tests/golden/worked_3x3.json directly (values worked by hand from
+    PAPER.md:224-235, :280-283, :172 — not the oracle's): beta, J and the warped frame."""
+    import json
+    g = json.load(open(os.path.join(os.path.dirname(__file__), "golden", "worked_3x3.json")))
+    img = np.array(g["image"], np.float32)[None, None]
+    z = np.array(g["zernike"], np.float32)[None, None]
+    t = np.zeros((1, 2, 3, 3), np.float32)
+    t[:, 0], t[:, 1] = g["tilt_x"], g["tilt_y"]
+    phi = np.array(g["phi"], np.float32)
+    mlp = {k: np.array(v, np.float32) for k, v in g["mlp"].items()}
+    r = p2s.Renderer(phi, mlp)
+    b = r.debug_beta(_dev(z)).cpu().numpy()
+    J = r.debug_blur(_dev(img), _dev(z)).cpu().numpy()
+    out = r.render(_dev(img), _dev(z), _dev(t)).cpu().numpy()
+    r.close()
+    assert np.abs(b[0, :, 0, 0] - np.array(g["beta_at_0_0"])).max() <= 2e-3
+    assert np.abs(b[0, :, 1, 1] - np.array(g["beta_at_1_1"])).max() <= 2e-3
+    eJ, eo = np.abs(J[0, 0] - np.array(g["J"])).max(), np.abs(out[0, 0] - np.array(g["out"])).max()
+    print(f"golden 3x3: max|J - hand| = {eJ:.2e}, max|out - hand| = {eo:.2e}")
+    assert eJ <= 2e-3 and eo <= 2e-3
 
 
 def test_cfg2_full_frame(p2s):

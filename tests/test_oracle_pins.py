@@ -741,3 +741,36 @@ def test_backward_color_reduces_to_shared_and_matches_finite_differences():
         e[c % 2, y, x] = 1e-3
         fd = (loss(img, zc, t + e) - loss(img, zc, t - e)) / 2e-3
         assert abs(fd - gt[c % 2, y, x]) < 1e-3 * (1 + abs(gt[c % 2, y, x])), ("t", fd, gt[c % 2, y, x])
+
+
+# ---------------------------------------------------------------- hand-worked fixture
+def _golden_3x3():
+    import json
+    import os
+    g = json.load(open(os.path.join(os.path.dirname(__file__), "golden", "worked_3x3.json")))
+    img = np.array(g["image"], np.float32)[None, None]
+    z = np.array(g["zernike"], np.float32)[None, None]
+    t = np.zeros((1, 2, 3, 3), np.float32)
+    t[:, 0], t[:, 1] = g["tilt_x"], g["tilt_y"]
+    phi = np.array(g["phi"], np.float32)
+    mlp = {k: np.array(v, np.float32) for k, v in g["mlp"].items()}
+    return g, img, z, t, phi, mlp
+
+
+def test_golden_hand_worked_3x3_frame():
+    """tests/golden/worked_3x3.json — a whole frame (MLP with a ReLU that switches at one pixel,
+    two delta basis functions, half-pixel tilt) worked by hand from PAPER.md:224-235 (Eq. 4-5),
+    :280-283 and :172; the file carries the derivation. The paper prints no numeric example
+    (SURVEY.md:218), so the expected numbers are the hand's, not the oracle's: a correlation
+    instead of a convolution, beta taken at the source pixel, a forward warp, swapped tilt planes
+    or a wrong clamp each change them."""
+    g, img, z, t, phi, mlp = _golden_3x3()
+    out, J = oracle.render(img, z, t, phi, mlp, want_blur=True)
+    b = oracle.beta(img, z, phi, mlp)
+    np.testing.assert_allclose(b[0, :, 0, 0], g["beta_at_0_0"], rtol=0, atol=1e-12)
+    np.testing.assert_allclose(b[0, :, 1, 1], g["beta_at_1_1"], rtol=0, atol=1e-12)
+    np.testing.assert_allclose(J[0, 0], np.array(g["J"]), rtol=0, atol=1e-6)      # inputs are fp32
+    np.testing.assert_allclose(out[0, 0], np.array(g["out"]), rtol=0, atol=1e-6)
+    # swapping the tilt planes (a vertical half-pixel shift) must NOT give the same frame
+    out_sw, _ = oracle.render(img, z, t[:, ::-1].copy(), phi, mlp, want_blur=True)
+    assert np.abs(out_sw[0, 0] - np.array(g["out"])).max() > 0.05
